@@ -1,0 +1,252 @@
+"""CPU oracle (TEST INFRASTRUCTURE ONLY) — ctypes wrapper around oracle/bt_oracle.c.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+may import this package.  The product path (paper_2108_00516_b200) never does; it fails
+loudly when its CUDA library is missing.
+
+Everything here is marshalling: the arithmetic lives in bt_oracle.c (plain C, double),
+written from PAPER.md (arXiv 2108.00516) §IV-B and §IV-D Eq. (2)/(3).
+Functions with no independent pin: none (see tests/test_oracle_*.py and DESIGN.md §4).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "bt_oracle.c")
+_HDR = os.path.join(_HERE, "bt_oracle.h")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+STATUS_OK, STATUS_FEW_MATCHES, STATUS_FEW_INLIERS, STATUS_REFIT_DEGENERATE = 0, 1, 2, 3
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc, -O2, no fast-math)."""
+    stale = not os.path.exists(_LIB) or any(
+        os.path.getmtime(p) > os.path.getmtime(_LIB) for p in (_SRC, _HDR))
+    if force or stale:
+        subprocess.check_call(["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        _setup(_lib)
+    return _lib
+
+
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_vp = C.c_void_p
+
+
+class PairResult(C.Structure):
+    _fields_ = [("status", C.c_int32), ("n_matches", C.c_int32), ("best_hyp", C.c_int32),
+                ("best_count", C.c_int32), ("T_best", C.c_double * 12),
+                ("T_refit", C.c_double * 12), ("refit_sig_ratio", C.c_double)]
+
+
+def _setup(L):
+    L.bto_philox4x32_10.argtypes = [_u32p, _u32p, _u32p]
+    L.bto_triple.argtypes = [_u32p, C.c_int32, _i32p]
+    L.bto_match.restype = C.c_int32
+    L.bto_match.argtypes = [_f32p, C.c_int32, _f32p, C.c_int32, C.c_int32, C.c_double,
+                            _i32p, _i32p, _i32p, _u8p, _u8p, _vp]
+    L.bto_arun.argtypes = [_f64p, _f64p, C.c_int32, _f64p, _f64p, C.POINTER(C.c_double)]
+    L.bto_svd3.argtypes = [_f64p, _f64p, _f64p, _f64p]
+    L.bto_ransac_counts.argtypes = [_f32p, _f32p, _f32p, _f32p, C.c_int32, C.c_int32, C.c_uint32,
+                                    C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                    _i32p, _i32p, _i32p, _vp, _vp]
+    L.bto_inliers.restype = C.c_int32
+    L.bto_inliers.argtypes = [_f64p, _f32p, _f32p, _f32p, _f32p, C.c_int32, C.c_double, C.c_double,
+                              _vp, _vp]
+    L.bto_ransac_finish.argtypes = [_f32p, _f32p, _f32p, _f32p, C.c_int32, C.c_int32, _i32p, _f64p,
+                                    C.c_double, C.c_double, C.c_double, C.c_int32,
+                                    C.POINTER(PairResult), _vp]
+    L.bto_huber.argtypes = [C.c_double, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.bto_feature_edge.argtypes = [_f32p, _f32p, _u32p, C.c_int32, _f32p, _f32p, C.c_double, _f64p]
+    L.bto_dense_edge.argtypes = [_f32p, _f32p, _u8p, _f32p, _f32p, _u8p, C.c_int32, C.c_int32,
+                                 C.c_double, C.c_double, C.c_double, C.c_double, _f32p, _f32p,
+                                 C.c_double, C.c_double, C.c_double, C.c_int32, _f64p, _vp, _vp]
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ------------------------------------------------------------------------------ sampler
+def philox(ctr, key) -> np.ndarray:
+    out = np.zeros(4, np.uint32)
+    lib().bto_philox4x32_10(_c(ctr, np.uint32), _c(key, np.uint32), out)
+    return out
+
+
+def triple(r, M: int) -> np.ndarray:
+    out = np.zeros(3, np.int32)
+    lib().bto_triple(_c(r, np.uint32), int(M), out)
+    return out
+
+
+# ----------------------------------------------------------------------------- matching
+def match(A, B, ratio: float = 1.0):
+    """Mutual NN of descriptor sets A [na][dim], B [nb][dim] (float32)."""
+    A = _c(A, np.float32)
+    B = _c(B, np.float32)
+    na, nb = len(A), len(B)
+    dim = A.shape[1] if A.ndim == 2 and na else (B.shape[1] if B.ndim == 2 and nb else 128)
+    pairs = np.zeros((max(min(na, nb), 1), 2), np.int32)
+    nn_ab = np.zeros(max(na, 1), np.int32)
+    nn_ba = np.zeros(max(nb, 1), np.int32)
+    rb = np.zeros(max(na, 1), np.uint8)
+    cb = np.zeros(max(nb, 1), np.uint8)
+    dbest = np.zeros(max(na, 1), np.float64)
+    M = lib().bto_match(A.reshape(-1) if na else np.zeros(1, np.float32), na,
+                        B.reshape(-1) if nb else np.zeros(1, np.float32), nb, dim, float(ratio),
+                        pairs, nn_ab, nn_ba, rb, cb, _ptr(dbest))
+    return dict(pairs=pairs[:M].copy(), nn_ab=nn_ab[:na], nn_ba=nn_ba[:nb],
+                row_border=rb[:na].astype(bool), col_border=cb[:nb].astype(bool), d_best=dbest[:na])
+
+
+# ------------------------------------------------------------------------- least squares
+def svd3(A):
+    U = np.zeros(9)
+    s = np.zeros(3)
+    V = np.zeros(9)
+    lib().bto_svd3(_c(np.asarray(A).reshape(9), np.float64), U, s, V)
+    return U.reshape(3, 3), s, V.reshape(3, 3)
+
+
+def arun(pa, pb):
+    pa = _c(pa, np.float64).reshape(-1, 3)
+    pb = _c(pb, np.float64).reshape(-1, 3)
+    R = np.zeros(9)
+    t = np.zeros(3)
+    sig = C.c_double()
+    lib().bto_arun(pa.reshape(-1), pb.reshape(-1), len(pa), R, t, C.byref(sig))
+    return R.reshape(3, 3), t, sig.value
+
+
+# ---------------------------------------------------------------------------------- RANSAC
+def ransac_counts(pa, na, pb, nb, n_hyp: int, pair_uid: int, seed: int, delta=0.005,
+                  cos_alpha=float(np.cos(np.deg2rad(45.0))), tau=1e-3):
+    pa, na, pb, nb = (_c(x, np.float32).reshape(-1) for x in (pa, na, pb, nb))
+    M = len(pa) // 3
+    cnt = np.zeros(n_hyp, np.int32)
+    lo = np.zeros(n_hyp, np.int32)
+    hi = np.zeros(n_hyp, np.int32)
+    hyp = np.zeros((n_hyp, 12), np.float64)
+    tri = np.zeros((n_hyp, 3), np.int32)
+    z = np.zeros(3, np.float32)
+    lib().bto_ransac_counts(pa if M else z, na if M else z, pb if M else z, nb if M else z, M, n_hyp,
+                            int(pair_uid) & 0xffffffff, int(seed) & 0xffffffffffffffff,
+                            float(delta), float(cos_alpha), float(tau), cnt, lo, hi, _ptr(hyp), _ptr(tri))
+    return dict(cnt=cnt, lo=lo, hi=hi, hyp=hyp, tri=tri)
+
+
+def inliers(T12, pa, na, pb, nb, delta=0.005, cos_alpha=float(np.cos(np.deg2rad(45.0)))):
+    pa, na, pb, nb = (_c(x, np.float32).reshape(-1) for x in (pa, na, pb, nb))
+    M = len(pa) // 3
+    mask = np.zeros(max((M + 31) // 32, 1), np.uint32)
+    border = np.zeros(max(M, 1), np.uint8)
+    z = np.zeros(3, np.float32)
+    n = lib().bto_inliers(_c(T12, np.float64), pa if M else z, na if M else z, pb if M else z,
+                          nb if M else z, M, float(delta), float(cos_alpha), _ptr(mask), _ptr(border))
+    return n, mask, border[:M].astype(bool)
+
+
+def ransac_finish(pa, na, pb, nb, counts, delta=0.005, cos_alpha=float(np.cos(np.deg2rad(45.0))),
+                  tau=1e-3, min_inliers=3):
+    pa, na, pb, nb = (_c(x, np.float32).reshape(-1) for x in (pa, na, pb, nb))
+    M = len(pa) // 3
+    res = PairResult()
+    mask = np.zeros(max((M + 31) // 32, 1), np.uint32)
+    z = np.zeros(3, np.float32)
+    H = len(counts["cnt"])
+    lib().bto_ransac_finish(pa if M else z, na if M else z, pb if M else z, nb if M else z, M, H,
+                            _c(counts["cnt"], np.int32), _c(counts["hyp"], np.float64).reshape(-1),
+                            float(delta), float(cos_alpha), float(tau), int(min_inliers),
+                            C.byref(res), _ptr(mask))
+    return dict(status=res.status, n_matches=res.n_matches, best_hyp=res.best_hyp,
+                best_count=res.best_count, T_best=np.array(res.T_best[:]),
+                T_refit=np.array(res.T_refit[:]), refit_sig_ratio=res.refit_sig_ratio, mask=mask)
+
+
+def huber(r: float, delta: float):
+    rho = C.c_double()
+    w = C.c_double()
+    lib().bto_huber(float(r), float(delta), C.byref(rho), C.byref(w))
+    return rho.value, w.value
+
+
+# ------------------------------------------------------------------------------- edges
+def feature_edge(pa, pb, mask, Ti, Tj, huber_delta=0.005) -> np.ndarray:
+    pa = _c(pa, np.float32).reshape(-1)
+    pb = _c(pb, np.float32).reshape(-1)
+    M = len(pa) // 3
+    out = np.zeros(96)
+    mk = _c(mask, np.uint32) if M else np.zeros(1, np.uint32)
+    z = np.zeros(3, np.float32)
+    lib().bto_feature_edge(pa if M else z, pb if M else z, mk, M, _c(Ti, np.float32),
+                           _c(Tj, np.float32), float(huber_delta), out)
+    return out
+
+
+def dense_edge(depth_i, normal_i, mask_i, depth_j, normal_j, mask_j, K, Ti, Tj, dist_gate=0.02,
+               cos_gate=float(np.cos(np.deg2rad(45.0))), huber_delta=0.005, stride=1,
+               want_pixels=False):
+    H, W = np.asarray(depth_i).shape
+    out = np.zeros(32)
+    pix = np.zeros(H * W, np.int32) if want_pixels else None
+    pbd = np.zeros(H * W, np.uint8) if want_pixels else None
+    lib().bto_dense_edge(_c(depth_i, np.float32).reshape(-1), _c(normal_i, np.float32).reshape(-1),
+                         _c(mask_i, np.uint8).reshape(-1), _c(depth_j, np.float32).reshape(-1),
+                         _c(normal_j, np.float32).reshape(-1), _c(mask_j, np.uint8).reshape(-1),
+                         W, H, float(K.fx), float(K.fy), float(K.cx), float(K.cy),
+                         _c(Ti, np.float32), _c(Tj, np.float32), float(dist_gate), float(cos_gate),
+                         float(huber_delta), int(stride), out, _ptr(pix), _ptr(pbd))
+    if want_pixels:
+        return out, pix.reshape(H, W), pbd.reshape(H, W).astype(bool)
+    return out
+
+
+# --------------------------------------------------------------- whole pair registration
+def register_pair(scene, a: int, b: int, uid: int, n_hyp: int, seed: int, node_poses=None,
+                  delta=0.005, cos_alpha=float(np.cos(np.deg2rad(45.0))), tau=1e-3, min_inliers=3,
+                  ratio=1.0, huber_delta=0.005, dense=None, counts_out=False):
+    """The whole hot path for one frame pair (a, b), step by step in the paper's order:
+    match -> RANSAC counts -> best + refit -> Eq. (2) blocks -> Eq. (3)
+    blocks of both directed edges.  `dense` = dict(dist_gate, cos_gate, huber_delta,
+    stride) or None to skip the dense edges."""
+    na_, nb_ = int(scene.n_kp[a]), int(scene.n_kp[b])
+    mt = match(scene.desc[a, :na_], scene.desc[b, :nb_], ratio)
+    P = mt["pairs"]
+    ia, ib = P[:, 0], P[:, 1]
+    pa, pb = scene.pts[a][ia], scene.pts[b][ib]
+    nra, nrb = scene.nrm[a][ia], scene.nrm[b][ib]
+    cnt = ransac_counts(pa, nra, pb, nrb, n_hyp, uid, seed, delta, cos_alpha, tau)
+    fin = ransac_finish(pa, nra, pb, nrb, cnt, delta, cos_alpha, tau, min_inliers)
+    rec = dict(match=mt, counts=cnt if counts_out else None, **fin)
+    if node_poses is not None:
+        rec["feat"] = feature_edge(pa, pb, fin["mask"], node_poses[a], node_poses[b], huber_delta)
+        if dense is not None:
+            rec["dense_ij"] = dense_edge(scene.depth[a], scene.normal[a], scene.mask[a], scene.depth[b],
+                                         scene.normal[b], scene.mask[b], scene.K, node_poses[a],
+                                         node_poses[b], **dense)
+            rec["dense_ji"] = dense_edge(scene.depth[b], scene.normal[b], scene.mask[b], scene.depth[a],
+                                         scene.normal[a], scene.mask[a], scene.K, node_poses[b],
+                                         node_poses[a], **dense)
+    return rec

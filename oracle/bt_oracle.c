@@ -1,0 +1,558 @@
+/* bt_oracle.c — TEST INFRASTRUCTURE ONLY (see bt_oracle.h).
+ *
+ * Plain, slow, double-precision CPU oracle of BundleTrack's pairwise registration hot
+ * path, written from the paper (arXiv 2108.00516, /root/reference/PAPER.md, "P:n" = line n).
+ * It follows the paper's steps in the paper's order; where the paper is silent the reading
+ * adopted is the one listed in DESIGN.md §2 ("R1".."R22").  No blocking, fusion or
+ * reordering: every loop is the definition written out.  Shares no code with the CUDA path.
+ *
+ * Parity pins (tests/test_oracle_*.py): Random123 KATs, triple-mapping enumeration,
+ * exact SE(3) recovery, brute-force SO(3) search, exhaustive triple enumeration, finite
+ * differences of the residuals, analytic plane / identity closed forms.
+ */
+#include "bt_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+static double band(double th) { return BTO_BAND_REL * (fabs(th) > 1.0 ? fabs(th) : 1.0); }
+
+/* ---------------------------------------------------------------------------------------
+ * Counter-based sampler.  P:25 only says "RANSAC"; the north star fixes a counter-based
+ * Philox sampler shared by both sides (reading R6).  Philox4x32-10 as published by
+ * Salmon et al. (SC'11): 10 rounds of
+ *   (hi0,lo0) = M0 * c0, (hi1,lo1) = M1 * c2,  c = (hi1^c1^k0, lo1, hi0^c3^k1, lo0),
+ * with the key bumped by the Weyl constants between rounds.
+ * ------------------------------------------------------------------------------------- */
+void bto_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int round = 0; round < 10; ++round) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* "Each registration sample consists of 3 pairs of keypoints": a uniformly random
+ * ordered triple of DISTINCT match indices in [0, M), reading R6:
+ *   i0 = floor(r0*M / 2^32); i1 = floor(r1*(M-1)/2^32), skip i0; i2 = floor(r2*(M-2)/2^32),
+ *   skip min(i0,i1) then max(i0,i1). */
+void bto_triple(const uint32_t r[4], int32_t M, int32_t out[3]) {
+  uint32_t i0 = (uint32_t)(((uint64_t)r[0] * (uint64_t)M) >> 32);
+  uint32_t i1 = (uint32_t)(((uint64_t)r[1] * (uint64_t)(M - 1)) >> 32);
+  if (i1 >= i0) i1 += 1;
+  uint32_t i2 = (uint32_t)(((uint64_t)r[2] * (uint64_t)(M - 2)) >> 32);
+  uint32_t lo = i0 < i1 ? i0 : i1, hi = i0 < i1 ? i1 : i0;
+  if (i2 >= lo) i2 += 1;
+  if (i2 >= hi) i2 += 1;
+  out[0] = (int32_t)i0; out[1] = (int32_t)i1; out[2] = (int32_t)i2;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Feature matching, "feature matching and outlier pruning" (P:4).  Readings R1-R4:
+ * squared Euclidean distance d(i,j) = sum_k (a_ik - b_jk)^2 (k ascending, double);
+ * NN ties -> lowest index; mutual NN; optional Lowe ratio on squared distances;
+ * output ascending in i.
+ * ------------------------------------------------------------------------------------- */
+int32_t bto_match(const float *A, int32_t na, const float *B, int32_t nb, int32_t dim, double ratio,
+                  int32_t *pairs, int32_t *nn_ab, int32_t *nn_ba, uint8_t *row_border,
+                  uint8_t *col_border, double *d_ab_best) {
+  double *D = (double *)malloc(sizeof(double) * (size_t)(na > 0 ? na : 1) * (size_t)(nb > 0 ? nb : 1));
+  uint8_t *row_ratio_ok = (uint8_t *)malloc((size_t)(na > 0 ? na : 1));
+  for (int32_t i = 0; i < na; ++i)
+    for (int32_t j = 0; j < nb; ++j) {
+      double s = 0.0;
+      for (int32_t k = 0; k < dim; ++k) {
+        double d = (double)A[(size_t)i * dim + k] - (double)B[(size_t)j * dim + k];
+        s += d * d;
+      }
+      D[(size_t)i * nb + j] = s;
+    }
+  double r2 = ratio * ratio;
+  for (int32_t i = 0; i < na; ++i) {
+    double b1 = INFINITY, b2 = INFINITY;
+    int32_t j1 = -1;
+    for (int32_t j = 0; j < nb; ++j) {
+      double d = D[(size_t)i * nb + j];
+      if (d < b1) { b2 = b1; b1 = d; j1 = j; }
+      else if (d < b2) { b2 = d; }
+    }
+    nn_ab[i] = j1;
+    if (d_ab_best) d_ab_best[i] = b1;
+    uint8_t bd = (nb >= 2) && (b2 - b1 <= band(b1));
+    row_ratio_ok[i] = 1;
+    if (ratio < 1.0 && nb >= 2) {
+      row_ratio_ok[i] = b1 < r2 * b2;
+      if (fabs(b1 - r2 * b2) <= band(r2 * b2)) bd = 1;
+    }
+    row_border[i] = bd;
+  }
+  for (int32_t j = 0; j < nb; ++j) {
+    double b1 = INFINITY, b2 = INFINITY;
+    int32_t i1 = -1;
+    for (int32_t i = 0; i < na; ++i) {
+      double d = D[(size_t)i * nb + j];
+      if (d < b1) { b2 = b1; b1 = d; i1 = i; }
+      else if (d < b2) { b2 = d; }
+    }
+    nn_ba[j] = i1;
+    col_border[j] = (na >= 2) && (b2 - b1 <= band(b1));
+  }
+  int32_t M = 0;
+  for (int32_t i = 0; i < na; ++i) {
+    int32_t j = nn_ab[i];
+    if (j >= 0 && nn_ba[j] == i && row_ratio_ok[i]) {
+      pairs[2 * M] = i;
+      pairs[2 * M + 1] = j;
+      ++M;
+    }
+  }
+  free(row_ratio_ok);
+  free(D);
+  return M;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Least squares rigid pose, "generated from a sample via least squares \cite{arun1987least}"
+ * (P:25).  Arun, Huang & Blostein 1987, with the det(VU^T) correction (reading R7).
+ * ------------------------------------------------------------------------------------- */
+void bto_svd3(const double A[9], double U[9], double s[3], double V[9]) {
+  double a[9], v[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  memcpy(a, A, sizeof a);
+  /* one-sided (Hestenes) Jacobi: rotate column pairs of a (and v) until orthogonal */
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    int rotated = 0;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        double alpha = 0, beta = 0, gamma = 0;
+        for (int r = 0; r < 3; ++r) {
+          alpha += a[r * 3 + p] * a[r * 3 + p];
+          beta += a[r * 3 + q] * a[r * 3 + q];
+          gamma += a[r * 3 + p] * a[r * 3 + q];
+        }
+        if (gamma == 0.0 || fabs(gamma) <= DBL_EPSILON * sqrt(alpha * beta)) continue;
+        rotated = 1;
+        double zeta = (beta - alpha) / (2.0 * gamma);
+        double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+        for (int r = 0; r < 3; ++r) {
+          double ap = a[r * 3 + p], aq = a[r * 3 + q];
+          a[r * 3 + p] = c * ap - sn * aq;
+          a[r * 3 + q] = sn * ap + c * aq;
+          double vp = v[r * 3 + p], vq = v[r * 3 + q];
+          v[r * 3 + p] = c * vp - sn * vq;
+          v[r * 3 + q] = sn * vp + c * vq;
+        }
+      }
+    if (!rotated) break;
+  }
+  double sv[3];
+  for (int k = 0; k < 3; ++k)
+    sv[k] = sqrt(a[0 * 3 + k] * a[0 * 3 + k] + a[1 * 3 + k] * a[1 * 3 + k] + a[2 * 3 + k] * a[2 * 3 + k]);
+  int ord[3] = {0, 1, 2};
+  for (int i = 0; i < 3; ++i)          /* sort descending by singular value */
+    for (int j = i + 1; j < 3; ++j)
+      if (sv[ord[j]] > sv[ord[i]]) { int tmp = ord[i]; ord[i] = ord[j]; ord[j] = tmp; }
+  for (int k = 0; k < 3; ++k) {
+    s[k] = sv[ord[k]];
+    for (int r = 0; r < 3; ++r) V[r * 3 + k] = v[r * 3 + ord[k]];
+  }
+  /* U columns: a_k / s_k; completed by orthogonality where s_k vanishes */
+  double tiny = 1e-300 + s[0] * 1e-15;
+  for (int k = 0; k < 3; ++k) {
+    if (s[k] > tiny) {
+      for (int r = 0; r < 3; ++r) U[r * 3 + k] = a[r * 3 + ord[k]] / s[k];
+    } else if (k == 2) {
+      U[0 * 3 + 2] = U[1 * 3 + 0] * U[2 * 3 + 1] - U[2 * 3 + 0] * U[1 * 3 + 1];
+      U[1 * 3 + 2] = U[2 * 3 + 0] * U[0 * 3 + 1] - U[0 * 3 + 0] * U[2 * 3 + 1];
+      U[2 * 3 + 2] = U[0 * 3 + 0] * U[1 * 3 + 1] - U[1 * 3 + 0] * U[0 * 3 + 1];
+    } else {
+      /* s1 (and s2) vanish: any unit vector orthogonal to the earlier columns */
+      double e[3] = {0, 0, 0};
+      int axis = 0;
+      double best = 2.0;
+      for (int r = 0; r < 3; ++r) {
+        double c = fabs(k > 0 ? U[r * 3 + 0] : 0.0);
+        if (c < best) { best = c; axis = r; }
+      }
+      e[axis] = 1.0;
+      for (int j = 0; j < k; ++j) {
+        double d = e[0] * U[0 * 3 + j] + e[1] * U[1 * 3 + j] + e[2] * U[2 * 3 + j];
+        for (int r = 0; r < 3; ++r) e[r] -= d * U[r * 3 + j];
+      }
+      double nrm = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+      for (int r = 0; r < 3; ++r) U[r * 3 + k] = e[r] / nrm;
+    }
+  }
+}
+
+static double det3(const double M[9]) {
+  return M[0] * (M[4] * M[8] - M[5] * M[7]) - M[1] * (M[3] * M[8] - M[5] * M[6]) +
+         M[2] * (M[3] * M[7] - M[4] * M[6]);
+}
+
+void bto_arun(const double *pa, const double *pb, int32_t n, double R[9], double t[3],
+              double *sig_ratio) {
+  double abar[3] = {0, 0, 0}, bbar[3] = {0, 0, 0};
+  for (int32_t k = 0; k < n; ++k)
+    for (int r = 0; r < 3; ++r) { abar[r] += pa[3 * k + r]; bbar[r] += pb[3 * k + r]; }
+  for (int r = 0; r < 3; ++r) { abar[r] /= n; bbar[r] /= n; }
+  double Hm[9] = {0};
+  for (int32_t k = 0; k < n; ++k)
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c)
+        Hm[r * 3 + c] += (pa[3 * k + r] - abar[r]) * (pb[3 * k + c] - bbar[c]);
+  double U[9], s[3], V[9];
+  bto_svd3(Hm, U, s, V);
+  *sig_ratio = s[0] > 0 ? s[1] / s[0] : 0.0;
+  double d = det3(V) * det3(U);          /* = det(V U^T) = +-1 */
+  double D[3] = {1.0, 1.0, d > 0 ? 1.0 : -1.0};
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      double acc = 0.0;
+      for (int k = 0; k < 3; ++k) acc += V[r * 3 + k] * D[k] * U[c * 3 + k];
+      R[r * 3 + c] = acc;
+    }
+  for (int r = 0; r < 3; ++r)
+    t[r] = bbar[r] - (R[r * 3 + 0] * abar[0] + R[r * 3 + 1] * abar[1] + R[r * 3 + 2] * abar[2]);
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Hypothesis evaluation: "inlier correspondences have a distance between
+ * transformed point pairs below a threshold delta and an angle formed by the normals
+ * within a threshold alpha" — strict gates (R9), unsigned angle without abs (R10).
+ * ------------------------------------------------------------------------------------- */
+/* returns 1 inlier / 0 outlier; *border = 1 when the decision is within the band */
+static int inlier_test(const double R[9], const double t[3], const float *pa, const float *na,
+                       const float *pb, const float *nb, double delta, double cos_alpha,
+                       int *border) {
+  double e[3], rn[3];
+  for (int r = 0; r < 3; ++r) {
+    e[r] = R[r * 3 + 0] * (double)pa[0] + R[r * 3 + 1] * (double)pa[1] + R[r * 3 + 2] * (double)pa[2] +
+           t[r] - (double)pb[r];
+    rn[r] = R[r * 3 + 0] * (double)na[0] + R[r * 3 + 1] * (double)na[1] + R[r * 3 + 2] * (double)na[2];
+  }
+  double dist = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+  double c = rn[0] * (double)nb[0] + rn[1] * (double)nb[1] + rn[2] * (double)nb[2];
+  double bd = band(delta), bc = band(cos_alpha);
+  int certain_out = (dist > delta + bd) || (c < cos_alpha - bc);
+  int certain_in = (dist < delta - bd) && (c > cos_alpha + bc);
+  *border = !certain_out && !certain_in;
+  return (dist < delta) && (c > cos_alpha);
+}
+
+int32_t bto_inliers(const double T[12], const float *pa, const float *na, const float *pb,
+                    const float *nb, int32_t M, double delta, double cos_alpha, uint32_t *mask,
+                    uint8_t *border) {
+  int32_t cnt = 0;
+  if (mask) memset(mask, 0, sizeof(uint32_t) * (size_t)((M + 31) / 32));
+  for (int32_t m = 0; m < M; ++m) {
+    int bd;
+    int in = inlier_test(T, T + 9, pa + 3 * m, na + 3 * m, pb + 3 * m, nb + 3 * m, delta, cos_alpha, &bd);
+    if (border) border[m] = (uint8_t)bd;
+    if (in) {
+      ++cnt;
+      if (mask) mask[m / 32] |= 1u << (m % 32);
+    }
+  }
+  return cnt;
+}
+
+void bto_ransac_counts(const float *pa, const float *na, const float *pb, const float *nb, int32_t M,
+                       int32_t n_hyp, uint32_t pair_uid, uint64_t seed, double delta,
+                       double cos_alpha, double tau_deg, int32_t *cnt, int32_t *lo, int32_t *hi,
+                       double *hyp, int32_t *tri) {
+  const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+  for (int32_t h = 0; h < n_hyp; ++h) {
+    if (M < 3) {                     /* no sample can be drawn (status FEW_MATCHES) */
+      cnt[h] = lo[h] = hi[h] = -1;
+      if (tri) tri[3 * h] = tri[3 * h + 1] = tri[3 * h + 2] = -1;
+      if (hyp) memset(hyp + 12 * h, 0, 12 * sizeof(double));
+      continue;
+    }
+    const uint32_t ctr[4] = {(uint32_t)h, pair_uid, 0u, 0u};
+    uint32_t r[4];
+    int32_t s3[3];
+    bto_philox4x32_10(ctr, key, r);
+    bto_triple(r, M, s3);
+    double A[9], B[9];
+    for (int k = 0; k < 3; ++k)
+      for (int c = 0; c < 3; ++c) {
+        A[3 * k + c] = (double)pa[3 * s3[k] + c];
+        B[3 * k + c] = (double)pb[3 * s3[k] + c];
+      }
+    double T[12], sig;
+    bto_arun(A, B, 3, T, T + 9, &sig);
+    if (tri) { tri[3 * h] = s3[0]; tri[3 * h + 1] = s3[1]; tri[3 * h + 2] = s3[2]; }
+    if (hyp) memcpy(hyp + 12 * h, T, sizeof T);
+    int deg = sig < tau_deg;                                /* reading R8 */
+    int deg_border = fabs(sig - tau_deg) <= band(tau_deg);
+    if (deg && !deg_border) { cnt[h] = lo[h] = hi[h] = -1; continue; }
+    int32_t n_in = 0, n_cin = 0, n_bd = 0;
+    for (int32_t m = 0; m < M; ++m) {
+      int bd;
+      int in = inlier_test(T, T + 9, pa + 3 * m, na + 3 * m, pb + 3 * m, nb + 3 * m, delta, cos_alpha, &bd);
+      n_in += in;
+      n_bd += bd;
+      n_cin += in && !bd;
+    }
+    cnt[h] = deg ? -1 : n_in;
+    lo[h] = deg_border ? -1 : n_cin;
+    hi[h] = n_cin + n_bd;
+  }
+}
+
+static void identity12(double T[12]) {
+  memset(T, 0, 12 * sizeof(double));
+  T[0] = T[4] = T[8] = 1.0;
+}
+
+void bto_ransac_finish(const float *pa, const float *na, const float *pb, const float *nb, int32_t M,
+                       int32_t n_hyp, const int32_t *cnt, const double *hyp, double delta,
+                       double cos_alpha, double tau_deg, int32_t min_inliers, bto_pair_result *res,
+                       uint32_t *mask) {
+  memset(res, 0, sizeof *res);
+  res->n_matches = M;
+  res->best_hyp = -1;
+  identity12(res->T_best);
+  identity12(res->T_refit);
+  int32_t words = (M + 31) / 32;
+  if (mask && words > 0) memset(mask, 0, sizeof(uint32_t) * (size_t)words);
+  if (M < 3) { res->status = 1; return; }                /* FEW_MATCHES */
+  /* "T_t^{t-1} is the best sampled correspondence hypothesis": max count, ties ->
+     lowest h (reading R11) */
+  int32_t best = 0;
+  for (int32_t h = 1; h < n_hyp; ++h)
+    if (cnt[h] > cnt[best]) best = h;
+  if (n_hyp <= 0 || cnt[best] < 0) { res->status = 2; return; }   /* all degenerate */
+  res->best_hyp = best;
+  memcpy(res->T_best, hyp + 12 * best, 12 * sizeof(double));
+  memcpy(res->T_refit, hyp + 12 * best, 12 * sizeof(double));
+  uint32_t *mk = (uint32_t *)calloc((size_t)(words > 0 ? words : 1), sizeof(uint32_t));
+  res->best_count = bto_inliers(res->T_best, pa, na, pb, nb, M, delta, cos_alpha, mk, NULL);
+  if (mask) memcpy(mask, mk, sizeof(uint32_t) * (size_t)words);
+  if (res->best_count < min_inliers) { res->status = 2; free(mk); return; }  /* FEW_INLIERS */
+  /* refit on all inliers of h* (north star; reading R12) */
+  double *A = (double *)malloc(sizeof(double) * 3 * (size_t)res->best_count);
+  double *B = (double *)malloc(sizeof(double) * 3 * (size_t)res->best_count);
+  int32_t k = 0;
+  for (int32_t m = 0; m < M; ++m)
+    if (mk[m / 32] >> (m % 32) & 1u) {
+      for (int c = 0; c < 3; ++c) { A[3 * k + c] = pa[3 * m + c]; B[3 * k + c] = pb[3 * m + c]; }
+      ++k;
+    }
+  double T[12], sig;
+  bto_arun(A, B, k, T, T + 9, &sig);
+  res->refit_sig_ratio = sig;
+  if (sig < tau_deg) res->status = 3;                   /* REFIT_DEGENERATE: keep T_best */
+  else memcpy(res->T_refit, T, sizeof T);
+  free(A); free(B); free(mk);
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Huber M-estimator, "rho is the M-estimator, where Huber loss is used"; IRLS
+ * weight "W ... computed by the M-estimator rho and residual".
+ * ------------------------------------------------------------------------------------- */
+void bto_huber(double r, double delta, double *rho, double *w) {
+  double a = fabs(r);
+  if (a <= delta) { *rho = 0.5 * a * a; *w = 1.0; }
+  else { *rho = delta * (a - 0.5 * delta); *w = delta / a; }
+}
+
+/* pose helpers (double) */
+static void pose_of(const float T[12], double R[9], double t[3]) {
+  for (int k = 0; k < 9; ++k) R[k] = T[k];
+  for (int k = 0; k < 3; ++k) t[k] = T[9 + k];
+}
+/* x_obj = R^T (x_cam - t) */
+static void inv_apply(const double R[9], const double t[3], const double x[3], double y[3]) {
+  for (int r = 0; r < 3; ++r)
+    y[r] = R[0 * 3 + r] * (x[0] - t[0]) + R[1 * 3 + r] * (x[1] - t[1]) + R[2 * 3 + r] * (x[2] - t[2]);
+}
+static void skew(const double p[3], double S[9]) {
+  S[0] = 0;     S[1] = -p[2]; S[2] = p[1];
+  S[3] = p[2];  S[4] = 0;     S[5] = -p[0];
+  S[6] = -p[1]; S[7] = p[0];  S[8] = 0;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Eq. (2): E_f(i,j) = sum_{(m,n) in C_ij} rho(|| T_i^-1 p_m - T_j^-1 p_n ||).
+ * Gauss-Newton blocks ((J^T W J) dxi = J^T W E): J = [J_i | J_j] (3 x 12) of the
+ * residual e with respect to the left perturbations T <- exp(d) T, d = (v, w) (R18):
+ *   J_i = -R_i^T [ I | -[p_m]x ],   J_j = R_j^T [ I | -[p_n]x ].
+ * ------------------------------------------------------------------------------------- */
+void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, int32_t M,
+                      const float Ti[12], const float Tj[12], double huber_delta, double out[96]) {
+  double Ri[9], ti[3], Rj[9], tj[3];
+  pose_of(Ti, Ri, ti);
+  pose_of(Tj, Rj, tj);
+  double Hf[12][12], g[12], E = 0.0;
+  memset(Hf, 0, sizeof Hf);
+  memset(g, 0, sizeof g);
+  int32_t count = 0;
+  for (int32_t m = 0; m < M; ++m) {
+    if (!(mask[m / 32] >> (m % 32) & 1u)) continue;
+    double p[3] = {pa[3 * m], pa[3 * m + 1], pa[3 * m + 2]};
+    double q[3] = {pb[3 * m], pb[3 * m + 1], pb[3 * m + 2]};
+    double xi[3], xj[3], e[3];
+    inv_apply(Ri, ti, p, xi);
+    inv_apply(Rj, tj, q, xj);
+    for (int r = 0; r < 3; ++r) e[r] = xi[r] - xj[r];
+    double nrm = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+    double rho, w;
+    bto_huber(nrm, huber_delta, &rho, &w);
+    double J[3][12], Sp[9], Sq[9];
+    skew(p, Sp);
+    skew(q, Sq);
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        double RiT = Ri[c * 3 + r], RjT = Rj[c * 3 + r];   /* (R^T)[r][c] */
+        J[r][c] = -RiT;
+        J[r][6 + c] = RjT;
+        double a = 0.0, b = 0.0;                          /* (R^T [p]x)[r][c] */
+        for (int k = 0; k < 3; ++k) { a += Ri[k * 3 + r] * Sp[k * 3 + c]; b += Rj[k * 3 + r] * Sq[k * 3 + c]; }
+        J[r][3 + c] = a;
+        J[r][9 + c] = -b;
+      }
+    for (int a = 0; a < 12; ++a) {
+      for (int b = 0; b < 12; ++b) {
+        double s = 0.0;
+        for (int r = 0; r < 3; ++r) s += J[r][a] * J[r][b];
+        Hf[a][b] += w * s;
+      }
+      double s = 0.0;
+      for (int r = 0; r < 3; ++r) s += J[r][a] * e[r];
+      g[a] += w * s;
+    }
+    E += rho;
+    ++count;
+  }
+  memset(out, 0, 96 * sizeof(double));
+  int k = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) out[k++] = Hf[a][b];               /* H_ii upper */
+  for (int a = 0; a < 6; ++a)
+    for (int b = 0; b < 6; ++b) out[k++] = Hf[a][6 + b];           /* H_ij */
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) out[k++] = Hf[6 + a][6 + b];       /* H_jj upper */
+  for (int a = 0; a < 12; ++a) out[k++] = g[a];                    /* g_i, g_j */
+  out[k++] = E;
+  out[k++] = count;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Eq. (3): E_g(i,j) = sum_{p in I_i} rho( n_i(x) . (T_i T_j^-1 pi_D^-1(pi(T_j T_i^-1 p)) - p) ).
+ * "dense pixel-wise correspondences are associated by point re-projection, while outliers
+ * are filtered based on the distance between the point pair and the angle formed by their
+ * normals".  Readings: nearest-pixel rounding (R14), gates (R15), normals compared
+ * in camera i (R16), Huber delta (R17), left-perturbation Jacobian of T_i with the
+ * association held fixed, J = [n_i^T, (q x n_i)^T] (R18), all masked valid pixels (R20).
+ * ------------------------------------------------------------------------------------- */
+void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *mask_i,
+                    const float *depth_j, const float *normal_j, const uint8_t *mask_j,
+                    int32_t W, int32_t H, double fx, double fy, double cx, double cy,
+                    const float Ti[12], const float Tj[12], double dist_gate, double cos_gate,
+                    double huber_delta, int32_t stride, double out[32], int32_t *pix_out,
+                    uint8_t *pix_border) {
+  double Ri[9], ti[3], Rj[9], tj[3];
+  pose_of(Ti, Ri, ti);
+  pose_of(Tj, Rj, tj);
+  /* T_j T_i^-1 : R = R_j R_i^T, t = t_j - R t_i;  T_i T_j^-1 : R = R_i R_j^T, t = t_i - R t_j */
+  double Rji[9], tji[3], Rij[9], tij[3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      double a = 0.0, b = 0.0;
+      for (int k = 0; k < 3; ++k) { a += Rj[r * 3 + k] * Ri[c * 3 + k]; b += Ri[r * 3 + k] * Rj[c * 3 + k]; }
+      Rji[r * 3 + c] = a;
+      Rij[r * 3 + c] = b;
+    }
+  for (int r = 0; r < 3; ++r) {
+    tji[r] = tj[r] - (Rji[r * 3 + 0] * ti[0] + Rji[r * 3 + 1] * ti[1] + Rji[r * 3 + 2] * ti[2]);
+    tij[r] = ti[r] - (Rij[r * 3 + 0] * tj[0] + Rij[r * 3 + 1] * tj[1] + Rij[r * 3 + 2] * tj[2]);
+  }
+  double Hs[6][6], g[6], E = 0.0;
+  memset(Hs, 0, sizeof Hs);
+  memset(g, 0, sizeof g);
+  int32_t count = 0, count_border = 0;
+  if (stride < 1) stride = 1;
+  for (int32_t v = 0; v < H; ++v)
+    for (int32_t u = 0; u < W; ++u) {
+      size_t pix = (size_t)v * W + u;
+      if (pix_out) pix_out[pix] = -1;
+      if (pix_border) pix_border[pix] = 0;
+      if (u % stride || v % stride) continue;
+      double d = depth_i[pix];
+      const float *ni_f = normal_i + 3 * pix;
+      if (!mask_i[pix] || !(d > 0.0) || (ni_f[0] == 0.f && ni_f[1] == 0.f && ni_f[2] == 0.f)) continue;
+      double ni[3] = {ni_f[0], ni_f[1], ni_f[2]};
+      /* p = pi^-1(x, d): unprojection with pixel centres at integer coordinates */
+      double p[3] = {((double)u - cx) * d / fx, ((double)v - cy) * d / fy, d};
+      double y[3];
+      for (int r = 0; r < 3; ++r)
+        y[r] = Rji[r * 3 + 0] * p[0] + Rji[r * 3 + 1] * p[1] + Rji[r * 3 + 2] * p[2] + tji[r];
+      int border = fabs(y[2]) <= band(0.0);
+      if (!(y[2] > 0.0)) { if (border) { ++count_border; if (pix_border) pix_border[pix] = 1; } continue; }
+      /* pi(y) and nearest pixel: x' = floor(u' + 0.5) */
+      double up = fx * y[0] / y[2] + cx, vp = fy * y[1] / y[2] + cy;
+      double fu = up + 0.5 - floor(up + 0.5), fv = vp + 0.5 - floor(vp + 0.5);
+      if (fu <= band(up) || 1.0 - fu <= band(up) || fv <= band(vp) || 1.0 - fv <= band(vp)) border = 1;
+      double xu = floor(up + 0.5), xv = floor(vp + 0.5);
+      if (xu < 0 || xu >= W || xv < 0 || xv >= H) {
+        if (border) { ++count_border; if (pix_border) pix_border[pix] = 1; }
+        continue;
+      }
+      int32_t uj = (int32_t)xu, vj = (int32_t)xv;
+      size_t pj = (size_t)vj * W + uj;
+      double dj = depth_j[pj];
+      const float *nj_f = normal_j + 3 * pj;
+      if (!mask_j[pj] || !(dj > 0.0) || (nj_f[0] == 0.f && nj_f[1] == 0.f && nj_f[2] == 0.f)) {
+        if (border) { ++count_border; if (pix_border) pix_border[pix] = 1; }
+        continue;
+      }
+      /* s = pi_D^-1(x'), q = T_i T_j^-1 s */
+      double s[3] = {((double)uj - cx) * dj / fx, ((double)vj - cy) * dj / fy, dj};
+      double q[3], nj[3];
+      for (int r = 0; r < 3; ++r) {
+        q[r] = Rij[r * 3 + 0] * s[0] + Rij[r * 3 + 1] * s[1] + Rij[r * 3 + 2] * s[2] + tij[r];
+        nj[r] = Rij[r * 3 + 0] * nj_f[0] + Rij[r * 3 + 1] * nj_f[1] + Rij[r * 3 + 2] * nj_f[2];
+      }
+      double dq[3] = {q[0] - p[0], q[1] - p[1], q[2] - p[2]};
+      double dist = sqrt(dq[0] * dq[0] + dq[1] * dq[1] + dq[2] * dq[2]);
+      double c = ni[0] * nj[0] + ni[1] * nj[1] + ni[2] * nj[2];
+      int pass = (dist < dist_gate) && (c > cos_gate);
+      int certain_out = (dist > dist_gate + band(dist_gate)) || (c < cos_gate - band(cos_gate));
+      int certain_in = (dist < dist_gate - band(dist_gate)) && (c > cos_gate + band(cos_gate));
+      if (!certain_out && !certain_in) border = 1;
+      if (border) { ++count_border; if (pix_border) pix_border[pix] = 1; }
+      if (!pass) continue;
+      double r = ni[0] * dq[0] + ni[1] * dq[1] + ni[2] * dq[2];
+      double rho, w;
+      bto_huber(r, huber_delta, &rho, &w);
+      double J[6] = {ni[0], ni[1], ni[2],
+                     q[1] * ni[2] - q[2] * ni[1], q[2] * ni[0] - q[0] * ni[2], q[0] * ni[1] - q[1] * ni[0]};
+      for (int a = 0; a < 6; ++a) {
+        for (int b = 0; b < 6; ++b) Hs[a][b] += w * J[a] * J[b];
+        g[a] += w * J[a] * r;
+      }
+      E += rho;
+      ++count;
+      if (pix_out) pix_out[pix] = (int32_t)pj;
+    }
+  memset(out, 0, 32 * sizeof(double));
+  int k = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) out[k++] = Hs[a][b];
+  for (int a = 0; a < 6; ++a) out[k++] = g[a];
+  out[k++] = E;
+  out[k++] = count;
+  out[k++] = count_border;
+}

@@ -1,0 +1,113 @@
+/* bt_oracle.h — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, double-precision CPU oracle of BundleTrack's pairwise registration hot
+ * path (arXiv 2108.00516, §IV-B P:25 and §IV-D Eq. (2)/(3) P:54-72).  Only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may load it.  It shares
+ * no code, header, table or constant generator with the CUDA library
+ * (paper_2108_00516_b200/csrc, include/bt.h); neither side includes the other.
+ *
+ * Inputs are the same float32 arrays the CUDA path receives; every value is converted
+ * exactly to double before any arithmetic.  Layout conventions (identical by contract,
+ * not by shared code): poses are 12 floats, R row-major then t, object->camera
+ * (x_cam = R x_obj + t); points / normals are [n][3]; descriptors [n][dim].
+ */
+#ifndef BT_ORACLE_H
+#define BT_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* band rule (north star "excluding points within 1e-6 of a threshold"):
+   a decision on the double value x against threshold th is borderline iff
+   |x - th| <= 1e-6 * max(1, |th|). */
+#define BTO_BAND_REL 1e-6
+
+/* Philox4x32-10 (Salmon et al., SC'11 "Parallel random numbers: as easy as 1, 2, 3"). */
+void bto_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+/* Distinct ordered triple in [0, M) from three 32-bit words (reading R6). */
+void bto_triple(const uint32_t r[4], int32_t M, int32_t out[3]);
+
+/* Brute-force mutual nearest neighbours (readings R1-R4).
+   Returns the number of matches M; pairs[M][2] = (i, j) ascending in i.
+   nn_ab[na], nn_ba[nb]: nearest neighbour indices (-1 if the other set is empty).
+   row_border[na] / col_border[nb]: 1 iff best and second-best squared distances are
+   within the band (ambiguous nearest neighbour), or the ratio test is borderline.
+   d_ab_best[na] (may be NULL): the best squared distance per row. */
+int32_t bto_match(const float *A, int32_t na, const float *B, int32_t nb, int32_t dim, double ratio,
+                  int32_t *pairs, int32_t *nn_ab, int32_t *nn_ba, uint8_t *row_border,
+                  uint8_t *col_border, double *d_ab_best);
+
+/* Arun et al. 1987 least squares: R, t minimising sum ||R a_k + t - b_k||^2 over SO(3)
+   via the SVD of H = sum (a_k - abar)(b_k - bbar)^T = U S V^T, R = V diag(1,1,det(VU^T)) U^T,
+   t = bbar - R abar.  sig_ratio = s2/s1 (0 when s1 = 0).  pa, pb: [n][3] double. */
+void bto_arun(const double *pa, const double *pb, int32_t n, double R[9], double t[3],
+              double *sig_ratio);
+
+/* One-sided Jacobi SVD of a 3x3 matrix (exposed for tests): A = U diag(s) V^T, s descending. */
+void bto_svd3(const double A[9], double U[9], double s[3], double V[9]);
+
+/* RANSAC over 3-correspondence samples.  pa/na/pb/nb: [M][3] float (the matched
+   keypoint points and normals of frames a and b, in match order).  For every hypothesis h:
+     cnt[h]  = the oracle's own count (double decisions), -1 if degenerate;
+     lo[h], hi[h] = the interval any correct fp implementation's count must lie in
+                    (borderline tests / degeneracy excluded per the band rule);
+     hyp[h][12] (may be NULL) = the hypothesis pose (R row-major, t);
+     tri[h][3]  (may be NULL) = the sampled triple. */
+void bto_ransac_counts(const float *pa, const float *na, const float *pb, const float *nb, int32_t M,
+                       int32_t n_hyp, uint32_t pair_uid, uint64_t seed, double delta,
+                       double cos_alpha, double tau_deg, int32_t *cnt, int32_t *lo, int32_t *hi,
+                       double *hyp, int32_t *tri);
+
+/* Inlier test of one pose on all M correspondences (P:25 gates), double decisions.
+   mask: ceil(M/32) words, bit m of word m/32.  border (may be NULL): per-m 1 iff the
+   decision is borderline.  Returns the count. */
+int32_t bto_inliers(const double T[12], const float *pa, const float *na, const float *pb,
+                    const float *nb, int32_t M, double delta, double cos_alpha, uint32_t *mask,
+                    uint8_t *border);
+
+/* Per-pair record, oracle side (double). */
+typedef struct {
+  int32_t status;      /* 0 OK, 1 FEW_MATCHES, 2 FEW_INLIERS, 3 REFIT_DEGENERATE */
+  int32_t n_matches;
+  int32_t best_hyp;    /* -1 if none */
+  int32_t best_count;
+  double T_best[12];
+  double T_refit[12];
+  double refit_sig_ratio;
+} bto_pair_result;
+
+/* Select h* (max count, ties -> lowest h), build C_ij = inliers(h*), refit (Arun on
+   C_ij, north star), status.  cnt from bto_ransac_counts.  mask: ceil(M/32) words out. */
+void bto_ransac_finish(const float *pa, const float *na, const float *pb, const float *nb, int32_t M,
+                       int32_t n_hyp, const int32_t *cnt, const double *hyp, double delta,
+                       double cos_alpha, double tau_deg, int32_t min_inliers, bto_pair_result *res,
+                       uint32_t *mask);
+
+/* Huber M-estimator: value and IRLS weight of a residual magnitude r >= 0. */
+void bto_huber(double r, double delta, double *rho, double *w);
+
+/* Eq. (2) feature-edge linearization at node poses Ti, Tj (12 floats each):
+   e = Ti^-1 p_m - Tj^-1 p_n over the masked correspondences; left perturbation
+   T <- exp(d) T, twist order (v, w).  out[96]: H_ii(21, upper row-major) H_ij(36 row-major)
+   H_jj(21) g_i(6) g_j(6) E(1) count(1) pad(4).  H = sum w J^T J, g = sum w J^T e,
+   E = sum rho(||e||). */
+void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, int32_t M,
+                      const float Ti[12], const float Tj[12], double huber_delta, double out[96]);
+
+/* Eq. (3) dense point-to-plane edge i -> j.  Maps: depth [H][W], normal [H][W][3],
+   mask [H][W].  out[32]: H(21 upper) g(6) E count count_border pad(2).
+   pix_out (may be NULL): [H][W] int32 per source pixel: -1 skipped, else the associated
+   target pixel index y'*W+x'.  pix_border (may be NULL): [H][W] u8, 1 iff borderline. */
+void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *mask_i,
+                    const float *depth_j, const float *normal_j, const uint8_t *mask_j,
+                    int32_t W, int32_t H, double fx, double fy, double cx, double cy,
+                    const float Ti[12], const float Tj[12], double dist_gate, double cos_gate,
+                    double huber_delta, int32_t stride, double out[32], int32_t *pix_out,
+                    uint8_t *pix_border);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

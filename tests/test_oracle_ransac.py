@@ -1,0 +1,168 @@
+"""Pins of the oracle's RANSAC (3-pair samples, Arun hypotheses, delta = 5 mm and
+alpha = 45 deg gates, best sampled hypothesis; refit per the north star)."""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+COS45 = float(np.cos(np.deg2rad(45.0)))
+SEED = synth.PHILOX_SEED
+
+
+def _T12(R, t):
+    return np.concatenate([np.asarray(R).reshape(9), np.asarray(t)])
+
+
+def test_gate_special_cases():
+    """Distances just inside / outside delta, normal angles inside / outside alpha, and a
+    flipped normal (unsigned angle, no abs: reading R10) under T = identity."""
+    I = _T12(np.eye(3), np.zeros(3))
+    pa = np.zeros((6, 3), np.float32) + np.float32([0, 0, 0.6])
+    na = np.tile(np.float32([0, 0, -1]), (6, 1))
+    pb = pa.copy()
+    nb = na.copy()
+    pb[0, 0] += 0.0049                 # in
+    pb[1, 0] += 0.0051                 # out (distance)
+    a44, a46 = np.deg2rad(44.0), np.deg2rad(46.0)
+    nb[2] = [np.sin(a44), 0, -np.cos(a44)]     # in
+    nb[3] = [np.sin(a46), 0, -np.cos(a46)]     # out (angle)
+    nb[4] = [0, 0, 1]                          # flipped normal: out
+    n, mask, border = oracle.inliers(I, pa, na, pb, nb)
+    assert n == 3 and mask[0] == 0b100101 and not border.any()
+
+
+def test_borderline_flagged():
+    I = _T12(np.eye(3), np.zeros(3))
+    pa = np.float32([[0, 0, 0.6]])
+    na = np.float32([[0, 0, -1]])
+    pb = pa + np.float32([[0.005, 0, 0]])          # dist = 5 mm (as float32) ~ delta
+    n, _, border = oracle.inliers(I, pa, na, pb, na)
+    assert border[0]
+
+
+def test_exhaustive_enumeration_small_M():
+    """M <= 8: every sampled hypothesis's count equals the count of its (unordered) triple
+    in an exhaustive enumeration of all C(M,3) triples; the best sampled count never
+    exceeds the exhaustive maximum and reaches it once every triple has been sampled."""
+    rng = np.random.default_rng(0)
+    for M in (3, 4, 6, 8):
+        pa, na, pb, nb, R, t, inl = synth.make_correspondences(rng, M, 0.6, noise=0.002)
+        table = {}
+        for tri in itertools.combinations(range(M), 3):
+            Rh, th, sig = oracle.arun(pa[list(tri)], pb[list(tri)])
+            c = oracle.inliers(_T12(Rh, th), pa, na, pb, nb)[0] if sig >= 1e-3 else -1
+            table[tri] = c
+        H = 400
+        res = oracle.ransac_counts(pa, na, pb, nb, H, 11, SEED)
+        seen = set()
+        for h in range(H):
+            key = tuple(sorted(res["tri"][h].tolist()))
+            seen.add(key)
+            assert res["cnt"][h] == table[key]
+            assert res["lo"][h] <= res["cnt"][h] <= res["hi"][h]
+        assert seen == set(table)                     # all triples covered by h < 400
+        assert res["cnt"].max() == max(table.values())
+
+
+def test_c1_zero_noise_best_is_first_all_inlier_sample():
+    """C1 with zero noise: all-inlier samples recover T_true, count* = #GT inliers (350);
+    outlier partners are >= 10 delta away, so h* is the first h whose Philox triple lies
+    inside the GT inlier set (computable from generator labels + Philox alone)."""
+    sc, Rt, tt, inl_b = synth.make_pair_c1()
+    m = oracle.match(sc.desc[0, :500], sc.desc[1, :500])
+    P = m["pairs"]
+    assert len(P) == 500
+    gt_inlier = inl_b[P[:, 1]]
+    assert gt_inlier.sum() == 350
+    ia, ib = P[:, 0], P[:, 1]
+    pa, pb = sc.pts[0][ia], sc.pts[1][ib]
+    na, nb = sc.nrm[0][ia], sc.nrm[1][ib]
+    H = 1024
+    res = oracle.ransac_counts(pa, na, pb, nb, H, 0, SEED)
+    key = [SEED & 0xffffffff, SEED >> 32]
+    first = None
+    for h in range(H):
+        tri = oracle.triple(oracle.philox([h, 0, 0, 0], key), 500)
+        if gt_inlier[tri].all():
+            first = h
+            break
+    assert first is not None
+    fin = oracle.ransac_finish(pa, na, pb, nb, res)
+    assert fin["best_hyp"] == first
+    assert fin["best_count"] == 350
+    assert fin["status"] == 0
+    Tr = fin["T_refit"]
+    assert np.abs(Tr[:9].reshape(3, 3) - Rt).max() < 1e-6 and np.abs(Tr[9:] - tt).max() < 1e-6
+    mask_bits = np.array([(fin["mask"][i // 32] >> (i % 32)) & 1 for i in range(500)], bool)
+    assert np.array_equal(mask_bits, gt_inlier)
+
+
+def test_every_reported_inlier_rechecks_both_gates():
+    rng = np.random.default_rng(1)
+    pa, na, pb, nb, R, t, inl = synth.make_correspondences(rng, 300, 0.5, noise=0.001)
+    res = oracle.ransac_counts(pa, na, pb, nb, 256, 3, SEED)
+    fin = oracle.ransac_finish(pa, na, pb, nb, res)
+    T = fin["T_best"]
+    Rb, tb = T[:9].reshape(3, 3), T[9:]
+    for mi in range(300):
+        if (fin["mask"][mi // 32] >> (mi % 32)) & 1:
+            e = Rb @ pa[mi].astype(float) + tb - pb[mi]
+            assert np.linalg.norm(e) < 0.005
+            assert (Rb @ na[mi].astype(float)) @ nb[mi] > COS45
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_spec_statistical_recovery(seed):
+    """500 matches, 60 % outliers, 1 mm noise -> rotation < 1 deg and translation
+    < 3 mm (SPEC asks >= 19/20 seeds; with 1024 hypotheses every seed passes here)."""
+    pa, na, pb, nb, R, t, inl = synth.make_correspondences(1000 + seed, 500, 0.4, noise=0.001)
+    res = oracle.ransac_counts(pa, na, pb, nb, 1024, seed, SEED)
+    fin = oracle.ransac_finish(pa, na, pb, nb, res)
+    assert fin["status"] == 0
+    Rr, tr = fin["T_refit"][:9].reshape(3, 3), fin["T_refit"][9:]
+    ang = np.degrees(synth.geodesic(Rr, R))
+    assert ang < 1.0 and np.linalg.norm(tr - t) < 0.003
+
+
+def test_status_signals():
+    pa, na, pb, nb, *_ = synth.make_correspondences(2, 2, 1.0)
+    res = oracle.ransac_counts(pa, na, pb, nb, 16, 0, SEED)
+    assert (res["cnt"] == -1).all()
+    assert oracle.ransac_finish(pa, na, pb, nb, res)["status"] == oracle.STATUS_FEW_MATCHES
+    # all outliers: no consistent triple -> registration failure signal
+    pa, na, pb, nb, *_ = synth.make_correspondences(3, 200, 0.0)
+    res = oracle.ransac_counts(pa, na, pb, nb, 512, 0, SEED)
+    fin = oracle.ransac_finish(pa, na, pb, nb, res)
+    assert fin["status"] == oracle.STATUS_FEW_INLIERS
+
+
+def test_degenerate_samples_are_never_selected():
+    # every point on one line except two: most triples are collinear -> count -1
+    M = 12
+    pa = np.zeros((M, 3), np.float32)
+    pa[:, 0] = np.arange(M) * 0.01
+    pa[:, 2] = 0.6
+    pa[10] = [0.03, 0.05, 0.6]
+    pa[11] = [0.07, -0.04, 0.62]
+    na = np.tile(np.float32([0, 0, -1]), (M, 1))
+    res = oracle.ransac_counts(pa, na, pa, na, 300, 0, SEED)
+    for h in range(300):
+        tri = set(res["tri"][h].tolist())
+        if not (tri & {10, 11}):
+            assert res["cnt"][h] == -1
+        else:
+            assert res["cnt"][h] == M
+    fin = oracle.ransac_finish(pa, na, pa, na, res)
+    assert fin["best_count"] == M and res["cnt"][fin["best_hyp"]] == M
+
+
+def test_determinism_and_uid_keying():
+    pa, na, pb, nb, *_ = synth.make_correspondences(4, 100, 0.5, noise=0.001)
+    a = oracle.ransac_counts(pa, na, pb, nb, 64, 5, SEED)
+    b = oracle.ransac_counts(pa, na, pb, nb, 64, 5, SEED)
+    c = oracle.ransac_counts(pa, na, pb, nb, 64, 6, SEED)
+    assert np.array_equal(a["cnt"], b["cnt"]) and np.array_equal(a["tri"], b["tri"])
+    assert not np.array_equal(a["tri"], c["tri"])
