@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the BundleTrack pairwise-registration hot path on B200.
+
+One STEP = one bt_register_pairs call over the BundleTrack per-frame workload of
+BASELINE.json configs[1] ("C2"): the current frame against K = 15 keyframes -> the 16-node
+pose graph's 120 frame pairs, n = 500 keypoints (128-d), 640x480 depth / normal / mask maps,
+4096 RANSAC hypotheses per pair: mutual-NN matching -> RANSAC -> refit -> Eq. (2) feature
+blocks -> both directed Eq. (3) dense edges (240).  Under torchrun each rank runs its own
+track (weak scaling) and the per-pair records are all-gathered over NCCL (the exchange the
+pose-graph solve needs).
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (oracle/, plain C,
+fp64) on a bounded sample of the same workload instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "frame-pairs registered/sec + RANSAC hypotheses/sec at 1/2/4/8 B200 vs roofline"
+UNIT = "pairs/s"
+N_FRAMES, N_KP, N_MAX, N_HYP, W, H = 16, 500, 512, 4096, 640, 480
+FLOPS_PER_TEST = 43          # 9 FMA + 3 FMA(t) ... per (hypothesis, correspondence)
+SM_COUNT, FP32_LANES = 148, 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def workload(rank: int):
+    """Rank r's track: the C2 scene with seed DATA_SEED + r, node poses perturbed by <= 5 deg /
+    2 cm (the state a pose-graph iteration linearizes at), global pair uids r*120 + k."""
+    sc = synth.make_scene(N_FRAMES, n=N_KP, n_max=N_MAX, width=W, height=H, seed=synth.DATA_SEED + rank)
+    pairs = synth.all_pairs(N_FRAMES)
+    uids = (rank * len(pairs) + np.arange(len(pairs))).astype(np.uint32)
+    poses = sc.perturbed_poses(seed=1000 + rank)
+    return sc, pairs, uids, poses
+
+
+def dense_params():
+    return dict(dist_gate=0.02, cos_gate=float(np.cos(np.deg2rad(45.0))), huber_delta=0.005, stride=1)
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampler of SM clock and clock-event reasons during the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = get_r(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------- the oracle arm
+def oracle_pairs_per_s(sc, pairs, uids, poses, sample_pairs):
+    """The CPU oracle as it stands (single thread) on `sample_pairs` of the workload."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    for p in sample_pairs:
+        a, b = pairs[p]
+        oracle.register_pair(sc, int(a), int(b), int(uids[p]), N_HYP, synth.PHILOX_SEED, node_poses=poses,
+                             dense=dense_params())
+    dt = time.perf_counter() - t0
+    return len(sample_pairs) / dt, dt
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sc, pairs, uids, poses = workload(0)
+    # each step: one frame pair of the C2 workload (round robin), full per-pair work
+    for s in range(args.warmup):
+        oracle_pairs_per_s(sc, pairs, uids, poses, [s % len(pairs)])
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        oracle_pairs_per_s(sc, pairs, uids, poses, [(args.warmup + s) % len(pairs)])
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    sample = (f"1 of the 120 C2 frame pairs per step (round robin): matching + {N_HYP}-hypothesis RANSAC + "
+              f"refit + Eq.(2) blocks + both dense edges at {W}x{H}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block():
+    return {"workload": "C2: BundleTrack per-frame step, current frame vs K=15 keyframes (120 pairs, 240 "
+                        "directed dense edges), n=500 keypoints, 128-d descriptors, 640x480 maps, 4096 "
+                        "hypotheses/pair",
+            "pairs_per_step": 120, "n": N_KP, "n_max": N_MAX, "hypotheses_per_pair": N_HYP, "frames": N_FRAMES,
+            "height": H, "width": W, "l2": "flushed between timed steps (512 MiB memset, outside the events)"}
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2108_00516_b200 as bt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    sc, pairs, uids, poses = workload(rank)
+    P = len(pairs)
+    fb = bt.FrameBatch.from_scene(sc, dev)
+    t_pairs = torch.from_numpy(pairs).to(dev)
+    t_uid = torch.from_numpy(uids.view(np.int32)).to(dev)
+    t_pose = torch.from_numpy(poses).to(dev)
+    rw = bt.record_words(N_MAX)
+    rec = torch.zeros((P, rw), dtype=torch.int32, device=dev)
+    all_rec = torch.zeros((world * P, rw), dtype=torch.int32, device=dev) if world > 1 else None
+    ctx = bt.Context(local)
+    ctx.reserve(P, N_MAX, N_HYP, N_FRAMES, W, H)
+    rprm = bt.ransac_params(N_HYP, synth.PHILOX_SEED)
+    eprm = bt.edge_params()
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        ctx.register_pairs(fb, sc.K, t_pose, t_pairs, t_uid, rprm, eprm, rec, stream=stream)
+        if world > 1:
+            dist.all_gather_into_tensor(all_rec, rec)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = ctx.last_launches
+    dec = bt.decode_records(rec, N_MAX)
+    M = dec["n_matches"].astype(np.int64)
+    tests = int(M.sum()) * N_HYP
+    n_assoc = float(dec["dense_ij"][:, 28].sum() + dec["dense_ji"][:, 28].sum())
+
+    ctx.profile(True)
+    ctx.profile_read()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()                                # evict L2 (outside the events)
+            starts[k].record(stream)
+            step()
+            stops[k].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = float(sum(a.elapsed_time(b) for a, b in zip(starts, stops)))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    sec = ms_max / 1e3
+    value = world * P * args.steps / sec
+    hyp_per_s = world * P * N_HYP * args.steps / sec
+
+    # ---- per-kernel roofline (algorithmic work / measured launch duration) ----------
+    mhz_max = 1965.0
+    fp32_peak_tflops = SM_COUNT * FP32_LANES * 2 * mhz_max * 1e6 / 1e12
+    import json as _j
+    peaks = _j.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    npx = W * H
+    n_valid = float(sum(int(sc.mask[f].sum()) for f in range(N_FRAMES)))
+    kern = {}
+
+    def add(name, bound, work, unit, peak):
+        tot, n = prof.get(name, (0.0, 0))
+        if n == 0:
+            return
+        avg_ms = tot / n
+        per_launch = work / (n / args.steps) if n else work
+        ach = per_launch / (avg_ms / 1e3) / (1e12 if unit == "TFLOP/s" else 1e9)
+        kern[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                      "avg_launch_ms": avg_ms, "launches_per_step": n / args.steps,
+                      "share_of_step": tot / ms if ms else None}
+    pair_sizes = float(sum(int(sc.n_kp[a]) * int(sc.n_kp[b]) for a, b in pairs))
+    add("k_nearest", "alu", 2 * pair_sizes * 128 * 3, "TFLOP/s", fp32_peak_tflops)
+    add("k_ransac_score", "alu", tests * FLOPS_PER_TEST, "TFLOP/s", fp32_peak_tflops)
+    # dense: bytes that must be read: source mask of every pixel, depth+normal of valid source
+    # pixels (edges of one source share nothing in this kernel), target gathers of associated px
+    dense_bytes = 2 * P * npx * 1 + 2 * P * (n_valid / N_FRAMES) * 16 + n_assoc * 17
+    add("k_dense", "hbm", dense_bytes, "GB/s", hbm_peak)
+    dom = max(kern, key=lambda k: kern[k]["share_of_step"] or 0) if kern else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if dom and os.path.exists(tf):
+        traffic = _j.load(open(tf)).get(dom)
+    roof = dict(kern[dom]) if dom else None
+    if roof:
+        roof["kernel"] = dom
+        roof["traffic"] = traffic
+        roof["peak_note"] = ("FP32 FMA pipe: 148 SMs x 128 lanes x 2 flop x 1965 MHz (derived, B200_PROFILING "
+                             "unit counts)" if roof["bound"] == "alu" else "MEASURED_PEAKS.json hbm_gbs")
+
+    # ---- end to end through the C ABI with pinned HOST buffers -------------------------
+    e2e = None
+    if not args.no_e2e:
+        hb = bt.FrameBatch.from_scene(sc, device="cpu", pin=True)
+        h_pairs = torch.from_numpy(pairs).pin_memory()
+        h_uid = torch.from_numpy(uids.view(np.int32)).pin_memory()
+        h_pose = torch.from_numpy(poses).pin_memory()
+        h_rec = torch.zeros((P, rw), dtype=torch.int32).pin_memory()
+        h2d = sum(x.numel() * x.element_size() for x in (hb.n_kp, hb.desc, hb.pts, hb.nrm, hb.depth, hb.normal,
+                                                         hb.mask, h_pairs, h_uid, h_pose))
+        d2h = h_rec.numel() * 4
+        for _ in range(2):
+            ctx.register_pairs(hb, sc.K, h_pose, h_pairs, h_uid, rprm, eprm, h_rec, stream=stream, host=True)
+        e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.e2e_steps)]
+        e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.e2e_steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.e2e_steps):
+            e_s[k].record(stream)
+            ctx.register_pairs(hb, sc.K, h_pose, h_pairs, h_uid, rprm, eprm, h_rec, stream=stream, host=True)
+            if world > 1:
+                dist.all_gather_into_tensor(all_rec, rec)
+            e_e[k].record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(e_s, e_e))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * P * args.e2e_steps / (float(e_ms.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "api": "bt_register_pairs_host (pinned host buffers, copies + sync inside the call)"}
+        assert np.array_equal(h_rec.numpy(), rec.cpu().numpy()), "host-buffer path disagrees with device path"
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = list(range(0, P, 1))
+        v, dt = oracle_pairs_per_s(sc, pairs, uids, poses, sample)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu": cpu_model(),
+               "sample": f"the full C2 step ({len(sample)} pairs: matching, {N_HYP}-hypothesis RANSAC, refit, "
+                         f"Eq.(2) blocks, 240 dense edges), single-threaded C fp64, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded analytic ellipsoid scene, synth/)", "config": config_block(),
+                "hypotheses_per_s": hyp_per_s, "tests_per_s": world * tests * args.steps / sec,
+                "parallelism": f"dp{world} (one track per rank, records all-gathered over NCCL)" if world > 1
+                else "single GPU",
+                "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
+                "roofline": roof, "kernels": kern, "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,191 @@
+/* bt.h — C ABI of the B200-native BundleTrack pairwise-registration hot path.
+ *
+ * BundleTrack (Wen & Bekris, arXiv 2108.00516; PAPER.md = /root/reference/PAPER.md, "P:n" =
+ * line n).  For every frame pair of the pose graph the library computes, on one sm_100a GPU:
+ *   bt_match       feature matching (P:4 "feature matching and outlier pruning"):
+ *                  mutual nearest neighbours of 128-d descriptors (D_i in R^128);
+ *   bt_ransac      RANSAC over 3-pair samples ("Each registration sample consists of 3
+ *                  pairs of keypoints"), Arun least-squares hypotheses ("generated from a
+ *                  sample via least squares"), inlier gates delta = 5 mm / alpha = 45 deg,
+ *                  best sampled hypothesis (T_t^{t-1}), refit on its inliers, C_ij;
+ *   bt_dense_corr  dense reprojection association + point-to-plane residuals of Eq. (3)
+ *                  (P:64-72), reduced to one 6x6 J^T W J block per directed edge;
+ *   bt_register_pairs  all of the above for P pairs (matching, RANSAC, refit, Eq. (2)
+ *                  feature-edge blocks at the node poses, both directed dense edges).
+ * Readings of what the paper leaves open are listed in DESIGN.md §2 (R1..R22).
+ *
+ * Conventions
+ *  - Every buffer pointer is a CUDA DEVICE pointer owned by the caller (except in
+ *    bt_register_pairs_host), 16-byte aligned.  Inputs are read-only.  The library owns only
+ *    the scratch reserved by bt_reserve; calls never allocate, never synchronise the host and
+ *    only enqueue work on `stream` (a cudaStream_t passed as void*, NULL = legacy default
+ *    stream), so they can be captured in a CUDA graph.  Outputs are valid once the stream
+ *    reaches them.
+ *  - Poses are object->camera, x_cam = R x_obj + t ("object pose in the camera's
+ *    frame"), R row-major.  Points / normals are camera-frame metres / unit vectors.
+ *  - Pixel centres sit at integer (u, v); pi(x) = (fx x/z + cx, fy y/z + cy); depth 0 =
+ *    invalid; normal (0,0,0) = invalid; mask nonzero = object.
+ *  - Twists are (v, w): translation first; Jacobians are w.r.t. the LEFT
+ *    perturbation T <- exp(d) T (reading R18).
+ *  - Errors: a call returns a bt_status; on failure nothing is enqueued and
+ *    bt_last_error(ctx) describes why.  A CUDA launch error makes the context sticky-failed
+ *    (every later call returns BT_ECUDA).  Per-pair outcomes are NOT errors: they are the
+ *    status word of each output record ("registration-failure signal").
+ *  - One context per host thread; a context is bound to the device given to bt_create.
+ */
+#ifndef BT_H
+#define BT_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bt_ctx bt_ctx;
+
+typedef enum {
+  BT_OK = 0,
+  BT_EINVAL = 1,        /* bad argument: NULL / misaligned pointer, n_kp > n_max, ...      */
+  BT_ENOMEM = 2,        /* bt_reserve could not allocate its scratch                          */
+  BT_ECUDA = 3,         /* a CUDA call failed (sticky)                                        */
+  BT_EUNSUPPORTED = 4,  /* device is not sm_100 (CC 10.0) or dim != 128                        */
+  BT_ECAPACITY = 5      /* P, E, n_max, n_hyp, frames or map size beyond what bt_reserve got   */
+} bt_status;
+
+typedef enum {
+  BT_PAIR_OK = 0,
+  BT_PAIR_FEW_MATCHES = 1,       /* M < 3: no sample can be drawn                              */
+  BT_PAIR_FEW_INLIERS = 2,       /* best count < min_inliers, or every hypothesis degenerate   */
+  BT_PAIR_REFIT_DEGENERATE = 3   /* inliers of h* are degenerate: T_refit = T_best              */
+} bt_pair_status;
+
+typedef struct { float fx, fy, cx, cy; int32_t width, height; } bt_intrinsics;
+typedef struct { float R[9]; float t[3]; } bt_pose;
+
+/* keypoints of F frames, each padded to n_max entries */
+typedef struct {
+  int32_t n_frames, n_max, dim;  /* dim must be 128                                    */
+  const int32_t *n_kp;           /* [F]              valid keypoints per frame, <= n_max       */
+  const float *desc;             /* [F][n_max][128]  descriptors                               */
+  const float *pts;              /* [F][n_max][3]    camera-frame points (metres)              */
+  const float *nrm;              /* [F][n_max][3]    unit camera-frame normals                 */
+} bt_keypoints;
+
+/* dense depth / normal / mask maps of F frames */
+typedef struct {
+  int32_t n_frames, width, height;
+  const float *depth;            /* [F][H][W]     metres, 0 = invalid                           */
+  const float *normal;           /* [F][H][W][3]  unit, camera frame, (0,0,0) = invalid         */
+  const uint8_t *mask;           /* [F][H][W]     nonzero = object                              */
+} bt_maps;
+
+typedef struct {
+  float ratio;                   /* Lowe ratio on distances; >= 1 disables it (default 1: R2)   */
+} bt_match_params;
+
+typedef struct {
+  float delta_m;                 /* inlier distance gate, 0.005                          */
+  float cos_alpha;               /* cos of the normal-angle gate, cos 45 deg             */
+  int32_t n_hyp;                 /* hypotheses per pair (1024 / 4096 / 16384), <= reserved      */
+  uint32_t pad_;
+  uint64_t seed;                 /* Philox key (lo, hi words)                                   */
+  float min_sigma_ratio;         /* degeneracy: sigma2/sigma1 of the cross-covariance, 1e-3 (R8) */
+  int32_t min_inliers;           /* FEW_INLIERS below this count, 3                     */
+} bt_ransac_params;
+
+typedef struct {
+  float dist_gate_m;             /* dense association distance gate, 0.02 (R15)                 */
+  float cos_gate;                /* dense normal-angle gate (cos), cos 45 deg (R15)             */
+  float huber_m;                 /* Huber delta for E_g and E_f, 0.005 (R17)                    */
+  int32_t stride;                /* use pixels with u % stride == 0 && v % stride == 0 (R20)    */
+} bt_edge_params;
+
+/* Context.  bt_create fails with BT_EUNSUPPORTED unless the device is compute capability 10.0. */
+bt_status bt_create(bt_ctx **ctx, int cuda_device);
+void bt_destroy(bt_ctx *ctx);
+const char *bt_last_error(const bt_ctx *ctx);
+const char *bt_status_string(bt_status s);
+
+/* Reserve device scratch for calls up to these sizes (may be called again to grow).
+   max_frames / width / height size the staging of bt_register_pairs_host. */
+bt_status bt_reserve(bt_ctx *ctx, int32_t max_pairs, int32_t n_max, int32_t max_hyp,
+                     int32_t max_frames, int32_t width, int32_t height);
+
+/* Per-pair output record, a fixed stride of bt_record_words(n_max) 4-byte words:
+     [0] status  [1] n_matches M  [2] best_hyp h* (-1 none)  [3] best_count
+     [4..15]  T_best  (f32: R row-major, t)   — the best SAMPLED hypothesis, a -> b
+     [16..27] T_refit (f32)                   — Arun on the inliers of h* (north star)
+     [28 .. 28+W)  inlier mask C_ij, W = ceil(n_max/32); bit m of word m/32 = match m
+     then (bt_register_pairs only):
+     dense_ij[32], dense_ji[32]  (f32, layout of bt_dense_corr's out rows)
+     feat[96] (f32): H_ii(21, upper row-major) H_ij(36 row-major) H_jj(21) g_i(6) g_j(6)
+                     E(1) count(1) pad(4)  — Eq. (2) at the node poses, i = pair.a, j = pair.b
+   T maps frame-a points to frame-b points: p_b ~ R p_a + t. */
+size_t bt_record_words(int32_t n_max);
+
+/* Mutual nearest-neighbour matching of P frame pairs.
+   pairs [P][2] (a, b) frame ids.  Out: matches [P][n_max][2] (i in a, j in b) ascending in
+   i, n_matches [P].  Squared Euclidean distance; ties -> lowest index (R1-R4). */
+bt_status bt_match(bt_ctx *ctx, const bt_keypoints *kp, const int32_t *pairs, int32_t P,
+                   const bt_match_params *prm, int32_t *matches, int32_t *n_matches, void *stream);
+
+/* RANSAC + refit of P pairs given their matches (as produced by bt_match).
+   pair_uid [P]: the Philox counter word of each pair (a GLOBAL id: results do not depend on
+   how pairs are batched or sharded).  Hypothesis h of pair p draws Philox4x32-10 with
+   counter (h, uid, 0, 0), key (seed lo, seed hi) -> distinct triple (R6).
+   Out: records [P][bt_record_words] words 0 .. 28+W; hyp_counts [P][n_hyp] (may be NULL):
+   inlier count of each hypothesis, -1 if degenerate. */
+bt_status bt_ransac(bt_ctx *ctx, const bt_keypoints *kp, const int32_t *pairs,
+                    const uint32_t *pair_uid, int32_t P, const int32_t *matches,
+                    const int32_t *n_matches, const bt_ransac_params *prm, uint32_t *records,
+                    int32_t *hyp_counts, void *stream);
+
+/* Eq. (3) dense edges.  edges [E][2] directed (i -> j) frame ids; node_pose [F] (device).
+   Out: out [E][32] f32: H (21, upper row-major of sum w J^T J) g (6, sum w J^T r)
+   E (sum rho(r)) count (associated pixels) pad(3); J = [n_i^T, (q x n_i)^T] w.r.t. the
+   left perturbation of T_i (the caller expands the T_j blocks with Adj(T_i T_j^-1)). */
+bt_status bt_dense_corr(bt_ctx *ctx, const bt_maps *maps, const bt_intrinsics *K,
+                        const bt_pose *node_pose, const int32_t *edges, int32_t E,
+                        const bt_edge_params *prm, float *out, void *stream);
+
+/* The whole per-pair hot path for P pairs: bt_match -> bt_ransac -> Eq. (2) blocks at the
+   node poses -> both directed Eq. (3) edges.  eprm may be NULL: dense + feature words are
+   then left untouched (the first stage of a frame step). */
+bt_status bt_register_pairs(bt_ctx *ctx, const bt_keypoints *kp, const bt_maps *maps,
+                            const bt_intrinsics *K, const bt_pose *node_pose, const int32_t *pairs,
+                            const uint32_t *pair_uid, int32_t P, const bt_match_params *mprm,
+                            const bt_ransac_params *rprm, const bt_edge_params *eprm,
+                            uint32_t *records, void *stream);
+
+/* Same as bt_register_pairs but every pointer (including those inside kp and maps) is a
+   HOST pointer (pinned memory gives full PCIe/C2C speed).  Copies the inputs into the
+   context's staging, runs the path, copies the records back and synchronises `stream`
+   before returning.  Needs bt_reserve(max_frames, width, height). */
+bt_status bt_register_pairs_host(bt_ctx *ctx, const bt_keypoints *kp, const bt_maps *maps,
+                                 const bt_intrinsics *K, const bt_pose *node_pose,
+                                 const int32_t *pairs, const uint32_t *pair_uid, int32_t P,
+                                 const bt_match_params *mprm, const bt_ransac_params *rprm,
+                                 const bt_edge_params *eprm, uint32_t *records, void *stream);
+
+/* out[n] = a[n] * b[n] (device bt_pose arrays): the coarse pose T~_t = T_rel T_{t-1} of
+   P:25 under object->camera poses (reading R13), without a host round trip. */
+bt_status bt_compose_poses(bt_ctx *ctx, const bt_pose *a, const bt_pose *b, bt_pose *out,
+                           int32_t n, void *stream);
+
+/* number of kernels the last bt_* call enqueued (for the bench's gpu_launches claim) */
+int32_t bt_last_launch_count(const bt_ctx *ctx);
+
+/* Per-kernel timing for roofline accounting.  When enabled, every kernel launch is bracketed
+   by a pair of CUDA events recorded on the launching stream.  bt_profile_read waits for the
+   recorded events, and returns (and resets) the accumulated time in ms and the launch count
+   of kernel `kernel_id` (0 .. bt_profile_kernels()-1) since the previous read. */
+bt_status bt_profile_enable(bt_ctx *ctx, int32_t on);
+int32_t bt_profile_kernels(void);
+const char *bt_profile_name(int32_t kernel_id);
+bt_status bt_profile_read(bt_ctx *ctx, int32_t kernel_id, double *total_ms, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BT_H */

@@ -197,7 +197,7 @@ def feature_edge(pa, pb, mask, Ti, Tj, huber_delta=0.005) -> np.ndarray:
     pa = _c(pa, np.float32).reshape(-1)
     pb = _c(pb, np.float32).reshape(-1)
     M = len(pa) // 3
-    out = np.zeros(96)
+    out = np.zeros(108)
     mk = _c(mask, np.uint32) if M else np.zeros(1, np.uint32)
     z = np.zeros(3, np.float32)
     lib().bto_feature_edge(pa if M else z, pb if M else z, mk, M, _c(Ti, np.float32),
@@ -209,7 +209,7 @@ def dense_edge(depth_i, normal_i, mask_i, depth_j, normal_j, mask_j, K, Ti, Tj, 
                cos_gate=float(np.cos(np.deg2rad(45.0))), huber_delta=0.005, stride=1,
                want_pixels=False):
     H, W = np.asarray(depth_i).shape
-    out = np.zeros(32)
+    out = np.zeros(48)
     pix = np.zeros(H * W, np.int32) if want_pixels else None
     pbd = np.zeros(H * W, np.uint8) if want_pixels else None
     lib().bto_dense_edge(_c(depth_i, np.float32).reshape(-1), _c(normal_i, np.float32).reshape(-1),

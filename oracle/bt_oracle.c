@@ -391,13 +391,14 @@ static void skew(const double p[3], double S[9]) {
  *   J_i = -R_i^T [ I | -[p_m]x ],   J_j = R_j^T [ I | -[p_n]x ].
  * ------------------------------------------------------------------------------------- */
 void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, int32_t M,
-                      const float Ti[12], const float Tj[12], double huber_delta, double out[96]) {
+                      const float Ti[12], const float Tj[12], double huber_delta, double out[108]) {
   double Ri[9], ti[3], Rj[9], tj[3];
   pose_of(Ti, Ri, ti);
   pose_of(Tj, Rj, tj);
-  double Hf[12][12], g[12], E = 0.0;
+  double Hf[12][12], g[12], gs[12], E = 0.0;
   memset(Hf, 0, sizeof Hf);
   memset(g, 0, sizeof g);
+  memset(gs, 0, sizeof gs);
   int32_t count = 0;
   for (int32_t m = 0; m < M; ++m) {
     if (!(mask[m / 32] >> (m % 32) & 1u)) continue;
@@ -429,14 +430,15 @@ void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, in
         for (int r = 0; r < 3; ++r) s += J[r][a] * J[r][b];
         Hf[a][b] += w * s;
       }
-      double s = 0.0;
-      for (int r = 0; r < 3; ++r) s += J[r][a] * e[r];
+      double s = 0.0, sa = 0.0;
+      for (int r = 0; r < 3; ++r) { s += J[r][a] * e[r]; sa += fabs(J[r][a] * e[r]); }
       g[a] += w * s;
+      gs[a] += w * sa;
     }
     E += rho;
     ++count;
   }
-  memset(out, 0, 96 * sizeof(double));
+  memset(out, 0, 108 * sizeof(double));
   int k = 0;
   for (int a = 0; a < 6; ++a)
     for (int b = a; b < 6; ++b) out[k++] = Hf[a][b];               /* H_ii upper */
@@ -447,6 +449,7 @@ void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, in
   for (int a = 0; a < 12; ++a) out[k++] = g[a];                    /* g_i, g_j */
   out[k++] = E;
   out[k++] = count;
+  for (int a = 0; a < 12; ++a) out[96 + a] = gs[a];             /* tolerance scale of g */
 }
 
 /* ---------------------------------------------------------------------------------------
@@ -457,11 +460,39 @@ void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, in
  * in camera i (R16), Huber delta (R17), left-perturbation Jacobian of T_i with the
  * association held fixed, J = [n_i^T, (q x n_i)^T] (R18), all masked valid pixels (R20).
  * ------------------------------------------------------------------------------------- */
+/* Contribution of source point p (normal ni) associated with target pixel (uj, vj) of frame j,
+   ignoring the gates: J = [n_i, q x n_i], r = n_i . (q - p), Huber weight.  Returns 0 when the
+   target pixel is out of bounds or invalid.  Used only for the borderline allowance. */
+static int dense_contrib(const float *depth_j, const float *normal_j, const uint8_t *mask_j, int32_t W,
+                         int32_t H, double fx, double fy, double cx, double cy, const double Rij[9],
+                         const double tij[3], const double p[3], const double ni[3], double huber_delta,
+                         int32_t uj, int32_t vj, double *Hfro, double gabs[6], double *rho_out) {
+  if (uj < 0 || uj >= W || vj < 0 || vj >= H) return 0;
+  size_t pj = (size_t)vj * W + uj;
+  double dj = depth_j[pj];
+  const float *nj_f = normal_j + 3 * pj;
+  if (!mask_j[pj] || !(dj > 0.0) || (nj_f[0] == 0.f && nj_f[1] == 0.f && nj_f[2] == 0.f)) return 0;
+  double s[3] = {((double)uj - cx) * dj / fx, ((double)vj - cy) * dj / fy, dj};
+  double q[3];
+  for (int r = 0; r < 3; ++r)
+    q[r] = Rij[r * 3 + 0] * s[0] + Rij[r * 3 + 1] * s[1] + Rij[r * 3 + 2] * s[2] + tij[r];
+  double r = ni[0] * (q[0] - p[0]) + ni[1] * (q[1] - p[1]) + ni[2] * (q[2] - p[2]);
+  double rho, w;
+  bto_huber(r, huber_delta, &rho, &w);
+  double J[6] = {ni[0], ni[1], ni[2],
+                 q[1] * ni[2] - q[2] * ni[1], q[2] * ni[0] - q[0] * ni[2], q[0] * ni[1] - q[1] * ni[0]};
+  double jj = 0.0;
+  for (int a = 0; a < 6; ++a) { jj += J[a] * J[a]; gabs[a] = w * fabs(J[a] * r); }
+  *Hfro = w * jj;                         /* |w J^T J|_F = w |J|^2 */
+  *rho_out = rho;
+  return 1;
+}
+
 void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *mask_i,
                     const float *depth_j, const float *normal_j, const uint8_t *mask_j,
                     int32_t W, int32_t H, double fx, double fy, double cx, double cy,
                     const float Ti[12], const float Tj[12], double dist_gate, double cos_gate,
-                    double huber_delta, int32_t stride, double out[32], int32_t *pix_out,
+                    double huber_delta, int32_t stride, double out[48], int32_t *pix_out,
                     uint8_t *pix_border) {
   double Ri[9], ti[3], Rj[9], tj[3];
   pose_of(Ti, Ri, ti);
@@ -479,9 +510,11 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
     tji[r] = tj[r] - (Rji[r * 3 + 0] * ti[0] + Rji[r * 3 + 1] * ti[1] + Rji[r * 3 + 2] * ti[2]);
     tij[r] = ti[r] - (Rij[r * 3 + 0] * tj[0] + Rij[r * 3 + 1] * tj[1] + Rij[r * 3 + 2] * tj[2]);
   }
-  double Hs[6][6], g[6], E = 0.0;
+  double Hs[6][6], g[6], gs[6], E = 0.0;
+  double al_g[6] = {0, 0, 0, 0, 0, 0}, al_E = 0.0, al_H = 0.0;   /* borderline allowance */
   memset(Hs, 0, sizeof Hs);
   memset(g, 0, sizeof g);
+  memset(gs, 0, sizeof gs);
   int32_t count = 0, count_border = 0;
   if (stride < 1) stride = 1;
   for (int32_t v = 0; v < H; ++v)
@@ -499,40 +532,67 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
       double y[3];
       for (int r = 0; r < 3; ++r)
         y[r] = Rji[r * 3 + 0] * p[0] + Rji[r * 3 + 1] * p[1] + Rji[r * 3 + 2] * p[2] + tji[r];
-      int border = fabs(y[2]) <= band(0.0);
-      if (!(y[2] > 0.0)) { if (border) { ++count_border; if (pix_border) pix_border[pix] = 1; } continue; }
+      if (fabs(y[2]) <= band(0.0)) {      /* never in practice: counted, no allowance bound */
+        ++count_border;
+        if (pix_border) pix_border[pix] = 1;
+        continue;
+      }
+      if (!(y[2] > 0.0)) continue;
       /* pi(y) and nearest pixel: x' = floor(u' + 0.5) */
       double up = fx * y[0] / y[2] + cx, vp = fy * y[1] / y[2] + cy;
       double fu = up + 0.5 - floor(up + 0.5), fv = vp + 0.5 - floor(vp + 0.5);
-      if (fu <= band(up) || 1.0 - fu <= band(up) || fv <= band(vp) || 1.0 - fv <= band(vp)) border = 1;
       double xu = floor(up + 0.5), xv = floor(vp + 0.5);
-      if (xu < 0 || xu >= W || xv < 0 || xv >= H) {
-        if (border) { ++count_border; if (pix_border) pix_border[pix] = 1; }
-        continue;
-      }
+      /* targets a correct fp implementation may round to (band rule on the pixel coordinate) */
+      int32_t cu[2] = {(int32_t)xu, (int32_t)xu}, cv[2] = {(int32_t)xv, (int32_t)xv};
+      int nu = 1, nv = 1;
+      if (fu <= band(up)) cu[nu++] = (int32_t)xu - 1;
+      else if (1.0 - fu <= band(up)) cu[nu++] = (int32_t)xu + 1;
+      if (fv <= band(vp)) cv[nv++] = (int32_t)xv - 1;
+      else if (1.0 - fv <= band(vp)) cv[nv++] = (int32_t)xv + 1;
+      int border = nu > 1 || nv > 1;
+      int pass = 0;
       int32_t uj = (int32_t)xu, vj = (int32_t)xv;
       size_t pj = (size_t)vj * W + uj;
-      double dj = depth_j[pj];
-      const float *nj_f = normal_j + 3 * pj;
-      if (!mask_j[pj] || !(dj > 0.0) || (nj_f[0] == 0.f && nj_f[1] == 0.f && nj_f[2] == 0.f)) {
-        if (border) { ++count_border; if (pix_border) pix_border[pix] = 1; }
-        continue;
+      double q[3], dq[3];
+      if (xu >= 0 && xu < W && xv >= 0 && xv < H) {
+        double dj = depth_j[pj];
+        const float *nj_f = normal_j + 3 * pj;
+        if (mask_j[pj] && dj > 0.0 && !(nj_f[0] == 0.f && nj_f[1] == 0.f && nj_f[2] == 0.f)) {
+          /* s = pi_D^-1(x'), q = T_i T_j^-1 s */
+          double s[3] = {((double)uj - cx) * dj / fx, ((double)vj - cy) * dj / fy, dj};
+          double nj[3];
+          for (int r = 0; r < 3; ++r) {
+            q[r] = Rij[r * 3 + 0] * s[0] + Rij[r * 3 + 1] * s[1] + Rij[r * 3 + 2] * s[2] + tij[r];
+            nj[r] = Rij[r * 3 + 0] * nj_f[0] + Rij[r * 3 + 1] * nj_f[1] + Rij[r * 3 + 2] * nj_f[2];
+            dq[r] = q[r] - p[r];
+          }
+          double dist = sqrt(dq[0] * dq[0] + dq[1] * dq[1] + dq[2] * dq[2]);
+          double c = ni[0] * nj[0] + ni[1] * nj[1] + ni[2] * nj[2];
+          pass = (dist < dist_gate) && (c > cos_gate);
+          int certain_out = (dist > dist_gate + band(dist_gate)) || (c < cos_gate - band(cos_gate));
+          int certain_in = (dist < dist_gate - band(dist_gate)) && (c > cos_gate + band(cos_gate));
+          if (!certain_out && !certain_in) border = 1;
+        }
       }
-      /* s = pi_D^-1(x'), q = T_i T_j^-1 s */
-      double s[3] = {((double)uj - cx) * dj / fx, ((double)vj - cy) * dj / fy, dj};
-      double q[3], nj[3];
-      for (int r = 0; r < 3; ++r) {
-        q[r] = Rij[r * 3 + 0] * s[0] + Rij[r * 3 + 1] * s[1] + Rij[r * 3 + 2] * s[2] + tij[r];
-        nj[r] = Rij[r * 3 + 0] * nj_f[0] + Rij[r * 3 + 1] * nj_f[1] + Rij[r * 3 + 2] * nj_f[2];
+      if (border) {
+        /* allowance: the largest contribution over every target this pixel may round to */
+        ++count_border;
+        if (pix_border) pix_border[pix] = 1;
+        double mh = 0.0, me = 0.0, mg[6] = {0, 0, 0, 0, 0, 0};
+        for (int a = 0; a < nu; ++a)
+          for (int b = 0; b < nv; ++b) {
+            double hf, ga[6], rh;
+            if (!dense_contrib(depth_j, normal_j, mask_j, W, H, fx, fy, cx, cy, Rij, tij, p, ni, huber_delta,
+                               cu[a], cv[b], &hf, ga, &rh))
+              continue;
+            if (hf > mh) mh = hf;
+            if (rh > me) me = rh;
+            for (int k = 0; k < 6; ++k) if (ga[k] > mg[k]) mg[k] = ga[k];
+          }
+        al_H += mh;
+        al_E += me;
+        for (int k = 0; k < 6; ++k) al_g[k] += mg[k];
       }
-      double dq[3] = {q[0] - p[0], q[1] - p[1], q[2] - p[2]};
-      double dist = sqrt(dq[0] * dq[0] + dq[1] * dq[1] + dq[2] * dq[2]);
-      double c = ni[0] * nj[0] + ni[1] * nj[1] + ni[2] * nj[2];
-      int pass = (dist < dist_gate) && (c > cos_gate);
-      int certain_out = (dist > dist_gate + band(dist_gate)) || (c < cos_gate - band(cos_gate));
-      int certain_in = (dist < dist_gate - band(dist_gate)) && (c > cos_gate + band(cos_gate));
-      if (!certain_out && !certain_in) border = 1;
-      if (border) { ++count_border; if (pix_border) pix_border[pix] = 1; }
       if (!pass) continue;
       double r = ni[0] * dq[0] + ni[1] * dq[1] + ni[2] * dq[2];
       double rho, w;
@@ -542,12 +602,13 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
       for (int a = 0; a < 6; ++a) {
         for (int b = 0; b < 6; ++b) Hs[a][b] += w * J[a] * J[b];
         g[a] += w * J[a] * r;
+        gs[a] += w * fabs(J[a] * r);
       }
       E += rho;
       ++count;
       if (pix_out) pix_out[pix] = (int32_t)pj;
     }
-  memset(out, 0, 32 * sizeof(double));
+  memset(out, 0, 48 * sizeof(double));
   int k = 0;
   for (int a = 0; a < 6; ++a)
     for (int b = a; b < 6; ++b) out[k++] = Hs[a][b];
@@ -555,4 +616,8 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
   out[k++] = E;
   out[k++] = count;
   out[k++] = count_border;
+  for (int a = 0; a < 6; ++a) out[32 + a] = gs[a];              /* tolerance scale of g */
+  for (int a = 0; a < 6; ++a) out[38 + a] = al_g[a];            /* borderline allowances */
+  out[44] = al_E;
+  out[45] = al_H;
 }

@@ -1,0 +1,419 @@
+// bt_api.cu — the C ABI of include/bt.h: context, scratch reservation, argument validation and
+// stream-ordered orchestration of the kernels in bt_match.cu / bt_ransac.cu / bt_dense.cu.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "bt_internal.cuh"
+
+struct bt_ctx {
+  int device = 0;
+  bool sticky = false;
+  char err[512] = {0};
+  bt::Launch launch;                          // kernels enqueued by the current / last call
+  // per-kernel event timing (bt_profile_*)
+  struct Pending { int kid; cudaEvent_t start, stop; };
+  bool prof_on = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<Pending> pending;
+  double prof_ms[bt::K_COUNT] = {0};
+  int64_t prof_n[bt::K_COUNT] = {0};
+  // capacity
+  int cap_pairs = 0, cap_nmax = 0, cap_hyp = 0, cap_frames = 0, cap_w = 0, cap_h = 0;
+  int cap_partials = 0;                       // dense partials per edge
+  // scratch
+  int32_t *nn_ab = nullptr, *nn_ba = nullptr, *matches = nullptr, *n_matches = nullptr;
+  uint8_t *ratio_ok = nullptr;
+  unsigned long long *best_key = nullptr;
+  float *partials = nullptr;
+  // staging for bt_register_pairs_host
+  int32_t *st_nkp = nullptr, *st_pairs = nullptr;
+  uint32_t *st_uid = nullptr, *st_records = nullptr;
+  float *st_desc = nullptr, *st_pts = nullptr, *st_nrm = nullptr, *st_depth = nullptr, *st_normal = nullptr;
+  uint8_t *st_mask = nullptr;
+  bt_pose *st_pose = nullptr;
+};
+
+namespace {
+
+bt_status fail(bt_ctx *c, bt_status s, const char *fmt, ...) {
+  if (c) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->err, sizeof c->err, fmt, ap);
+    va_end(ap);
+    if (s == BT_ECUDA) c->sticky = true;
+  }
+  return s;
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+template <class T>
+void free_dev(T *&p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+void free_scratch(bt_ctx *c) {
+  free_dev(c->nn_ab); free_dev(c->nn_ba); free_dev(c->matches); free_dev(c->n_matches);
+  free_dev(c->ratio_ok); free_dev(c->best_key); free_dev(c->partials);
+  free_dev(c->st_nkp); free_dev(c->st_pairs); free_dev(c->st_uid); free_dev(c->st_records);
+  free_dev(c->st_desc); free_dev(c->st_pts); free_dev(c->st_nrm); free_dev(c->st_depth);
+  free_dev(c->st_normal); free_dev(c->st_mask); free_dev(c->st_pose);
+}
+
+#define BT_CHECK_CTX(c)                                                                  \
+  do {                                                                                   \
+    if (!(c)) return BT_EINVAL;                                                          \
+    if ((c)->sticky) return BT_ECUDA;                                                    \
+    if (cudaSetDevice((c)->device) != cudaSuccess)                                       \
+      return fail((c), BT_ECUDA, "cudaSetDevice(%d) failed", (c)->device);               \
+    (c)->launch.count = 0;                                                               \
+  } while (0)
+
+bt_status after_launch(bt_ctx *c, const char *what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, BT_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return BT_OK;
+}
+
+bt_status check_kp(bt_ctx *c, const bt_keypoints *kp) {
+  if (!kp) return fail(c, BT_EINVAL, "keypoints: NULL");
+  if (kp->dim != bt::kDim) return fail(c, BT_EUNSUPPORTED, "descriptor dim %d != 128", kp->dim);
+  if (kp->n_frames < 1 || kp->n_max < 1) return fail(c, BT_EINVAL, "keypoints: n_frames/n_max < 1");
+  if (kp->n_max > c->cap_nmax)
+    return fail(c, BT_ECAPACITY, "n_max %d > reserved %d", kp->n_max, c->cap_nmax);
+  if (!kp->n_kp || !kp->desc || !kp->pts || !kp->nrm) return fail(c, BT_EINVAL, "keypoints: NULL buffer");
+  if (!aligned16(kp->desc) || !aligned16(kp->pts) || !aligned16(kp->nrm) || !aligned16(kp->n_kp))
+    return fail(c, BT_EINVAL, "keypoints: buffers must be 16-byte aligned");
+  return BT_OK;
+}
+
+bt_status check_maps(bt_ctx *c, const bt_maps *mp, const bt_intrinsics *K) {
+  if (!mp || !K) return fail(c, BT_EINVAL, "maps / intrinsics: NULL");
+  if (mp->width != K->width || mp->height != K->height)
+    return fail(c, BT_EINVAL, "maps %dx%d != intrinsics %dx%d", mp->width, mp->height, K->width, K->height);
+  if (mp->width < 1 || mp->height < 1 || mp->n_frames < 1) return fail(c, BT_EINVAL, "maps: empty");
+  if (bt::dense_partials_per_edge(mp->width, mp->height) > c->cap_partials)
+    return fail(c, BT_ECAPACITY, "maps %dx%d larger than reserved %dx%d", mp->width, mp->height, c->cap_w, c->cap_h);
+  if (!mp->depth || !mp->normal || !mp->mask) return fail(c, BT_EINVAL, "maps: NULL buffer");
+  if (!aligned16(mp->depth) || !aligned16(mp->normal) || !aligned16(mp->mask))
+    return fail(c, BT_EINVAL, "maps: buffers must be 16-byte aligned");
+  if (!(K->fx > 0.f) || !(K->fy > 0.f)) return fail(c, BT_EINVAL, "intrinsics: fx, fy must be > 0");
+  return BT_OK;
+}
+
+bt_status check_ransac(bt_ctx *c, const bt_ransac_params *r) {
+  if (!r) return fail(c, BT_EINVAL, "ransac params: NULL");
+  if (r->n_hyp < 1) return fail(c, BT_EINVAL, "n_hyp < 1");
+  if (r->n_hyp > c->cap_hyp) return fail(c, BT_ECAPACITY, "n_hyp %d > reserved %d", r->n_hyp, c->cap_hyp);
+  if (!(r->delta_m > 0.f)) return fail(c, BT_EINVAL, "delta_m must be > 0");
+  return BT_OK;
+}
+
+bt_status check_edge(bt_ctx *c, const bt_edge_params *e) {
+  if (!e) return fail(c, BT_EINVAL, "edge params: NULL");
+  if (!(e->dist_gate_m > 0.f) || !(e->huber_m > 0.f)) return fail(c, BT_EINVAL, "edge gates must be > 0");
+  return BT_OK;
+}
+
+bt::KpView kview(const bt_keypoints *kp) {
+  return bt::KpView{kp->n_frames, kp->n_max, kp->n_kp, kp->desc, kp->pts, kp->nrm};
+}
+bt::MapView mview(const bt_maps *m) {
+  return bt::MapView{m->n_frames, m->width, m->height, m->depth, m->normal, m->mask};
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *bt_status_string(bt_status s) {
+  switch (s) {
+    case BT_OK: return "BT_OK";
+    case BT_EINVAL: return "BT_EINVAL";
+    case BT_ENOMEM: return "BT_ENOMEM";
+    case BT_ECUDA: return "BT_ECUDA";
+    case BT_EUNSUPPORTED: return "BT_EUNSUPPORTED";
+    case BT_ECAPACITY: return "BT_ECAPACITY";
+  }
+  return "BT_?";
+}
+
+bt_status bt_create(bt_ctx **out, int cuda_device) {
+  if (!out) return BT_EINVAL;
+  *out = nullptr;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) return BT_ECUDA;
+  if (prop.major != 10 || prop.minor != 0) return BT_EUNSUPPORTED;   // built for sm_100a only
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return BT_ECUDA;
+  bt_ctx *c = new (std::nothrow) bt_ctx;
+  if (!c) return BT_ENOMEM;
+  c->device = cuda_device;
+  *out = c;
+  return BT_OK;
+}
+
+void bt_destroy(bt_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto &p : c->pending) { cudaEventDestroy(p.start); if (p.stop) cudaEventDestroy(p.stop); }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  free_scratch(c);
+  delete c;
+}
+
+const char *bt_last_error(const bt_ctx *c) { return c ? c->err : "no context"; }
+
+int32_t bt_last_launch_count(const bt_ctx *c) { return c ? c->launch.count : 0; }
+
+size_t bt_record_words(int32_t n_max) { return n_max < 1 ? 0 : (size_t)bt::rec_words(n_max); }
+
+bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hyp, int32_t max_frames,
+                     int32_t width, int32_t height) {
+  BT_CHECK_CTX(c);
+  if (max_pairs < 1 || n_max < 1 || max_hyp < 1 || max_frames < 0 || width < 0 || height < 0)
+    return fail(c, BT_EINVAL, "bt_reserve: bad sizes");
+  cudaDeviceSynchronize();
+  free_scratch(c);
+  c->cap_pairs = c->cap_nmax = c->cap_hyp = c->cap_frames = c->cap_w = c->cap_h = c->cap_partials = 0;
+  const size_t PN = (size_t)max_pairs * n_max;
+  const int nparts = (width > 0 && height > 0) ? bt::dense_partials_per_edge(width, height) : 0;
+  bool ok = cudaMalloc(&c->nn_ab, PN * 4) == cudaSuccess && cudaMalloc(&c->nn_ba, PN * 4) == cudaSuccess &&
+            cudaMalloc(&c->matches, PN * 8) == cudaSuccess && cudaMalloc(&c->n_matches, (size_t)max_pairs * 4) == cudaSuccess &&
+            cudaMalloc(&c->ratio_ok, PN) == cudaSuccess &&
+            cudaMalloc(&c->best_key, (size_t)max_pairs * 8) == cudaSuccess;
+  if (ok && nparts > 0)
+    ok = cudaMalloc(&c->partials, (size_t)2 * max_pairs * nparts * 32 * sizeof(float)) == cudaSuccess;
+  if (ok && max_frames > 0) {
+    const size_t FN = (size_t)max_frames * n_max, FP = (size_t)max_frames * width * height;
+    ok = cudaMalloc(&c->st_nkp, (size_t)max_frames * 4) == cudaSuccess &&
+         cudaMalloc(&c->st_desc, FN * 128 * 4) == cudaSuccess && cudaMalloc(&c->st_pts, FN * 12) == cudaSuccess &&
+         cudaMalloc(&c->st_nrm, FN * 12) == cudaSuccess && cudaMalloc(&c->st_pose, (size_t)max_frames * sizeof(bt_pose)) == cudaSuccess &&
+         cudaMalloc(&c->st_pairs, (size_t)max_pairs * 8) == cudaSuccess && cudaMalloc(&c->st_uid, (size_t)max_pairs * 4) == cudaSuccess &&
+         cudaMalloc(&c->st_records, (size_t)max_pairs * bt::rec_words(n_max) * 4) == cudaSuccess;
+    if (ok && FP > 0)
+      ok = cudaMalloc(&c->st_depth, FP * 4) == cudaSuccess && cudaMalloc(&c->st_normal, FP * 12) == cudaSuccess &&
+           cudaMalloc(&c->st_mask, FP) == cudaSuccess;
+  }
+  if (!ok) {
+    cudaGetLastError();
+    free_scratch(c);
+    return fail(c, BT_ENOMEM, "bt_reserve: cudaMalloc failed");
+  }
+  c->cap_pairs = max_pairs; c->cap_nmax = n_max; c->cap_hyp = max_hyp; c->cap_frames = max_frames;
+  c->cap_w = width; c->cap_h = height; c->cap_partials = nparts;
+  return BT_OK;
+}
+
+bt_status bt_match(bt_ctx *c, const bt_keypoints *kp, const int32_t *pairs, int32_t P,
+                   const bt_match_params *prm, int32_t *matches, int32_t *n_matches, void *stream) {
+  BT_CHECK_CTX(c);
+  bt_status s;
+  if ((s = check_kp(c, kp)) != BT_OK) return s;
+  if (P < 0) return fail(c, BT_EINVAL, "P < 0");
+  if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
+  if (P == 0) return BT_OK;
+  if (!pairs || !matches || !n_matches) return fail(c, BT_EINVAL, "bt_match: NULL buffer");
+  const float ratio = prm ? prm->ratio : 1.f;
+  bt::launch_match(kview(kp), pairs, P, ratio, c->nn_ab, c->nn_ba, c->ratio_ok, matches, n_matches,
+                   (cudaStream_t)stream, c->launch);
+  return after_launch(c, "bt_match");
+}
+
+bt_status bt_ransac(bt_ctx *c, const bt_keypoints *kp, const int32_t *pairs, const uint32_t *pair_uid,
+                    int32_t P, const int32_t *matches, const int32_t *n_matches, const bt_ransac_params *prm,
+                    uint32_t *records, int32_t *hyp_counts, void *stream) {
+  BT_CHECK_CTX(c);
+  bt_status s;
+  if ((s = check_kp(c, kp)) != BT_OK) return s;
+  if ((s = check_ransac(c, prm)) != BT_OK) return s;
+  if (P < 0) return fail(c, BT_EINVAL, "P < 0");
+  if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
+  if (P == 0) return BT_OK;
+  if (!pairs || !pair_uid || !matches || !n_matches || !records) return fail(c, BT_EINVAL, "bt_ransac: NULL buffer");
+  bt::launch_ransac(kview(kp), pairs, pair_uid, P, matches, n_matches, *prm, c->best_key, records,
+                    bt::rec_words(kp->n_max), hyp_counts, nullptr, 0.f, (cudaStream_t)stream, c->launch);
+  return after_launch(c, "bt_ransac");
+}
+
+bt_status bt_dense_corr(bt_ctx *c, const bt_maps *maps, const bt_intrinsics *K, const bt_pose *node_pose,
+                        const int32_t *edges, int32_t E, const bt_edge_params *prm, float *out, void *stream) {
+  BT_CHECK_CTX(c);
+  bt_status s;
+  if ((s = check_maps(c, maps, K)) != BT_OK) return s;
+  if ((s = check_edge(c, prm)) != BT_OK) return s;
+  if (E < 0) return fail(c, BT_EINVAL, "E < 0");
+  if (E > 2 * c->cap_pairs) return fail(c, BT_ECAPACITY, "E %d > 2 * reserved pairs %d", E, c->cap_pairs);
+  if (E == 0) return BT_OK;
+  if (!node_pose || !edges || !out) return fail(c, BT_EINVAL, "bt_dense_corr: NULL buffer");
+  bt::launch_dense(mview(maps), *K, node_pose, edges, nullptr, E, *prm, c->partials, c->cap_partials, out, 32,
+                   nullptr, 0, 0, 0, (cudaStream_t)stream, c->launch);
+  return after_launch(c, "bt_dense_corr");
+}
+
+static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_maps *maps,
+                                    const bt_intrinsics *K, const bt_pose *node_pose, const int32_t *pairs,
+                                    const uint32_t *uid, int32_t P, const bt_match_params *mprm,
+                                    const bt_ransac_params *rprm, const bt_edge_params *eprm,
+                                    uint32_t *records, cudaStream_t st) {
+  const int rw = bt::rec_words(kp->n_max);
+  const float ratio = mprm ? mprm->ratio : 1.f;
+  bt::launch_match(kview(kp), pairs, P, ratio, c->nn_ab, c->nn_ba, c->ratio_ok, c->matches, c->n_matches, st,
+                   c->launch);
+  bt::launch_ransac(kview(kp), pairs, uid, P, c->matches, c->n_matches, *rprm, c->best_key, records, rw, nullptr,
+                    eprm ? node_pose : nullptr, eprm ? eprm->huber_m : 0.f, st, c->launch);
+  if (eprm)
+    bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->partials, c->cap_partials,
+                     nullptr, 0, records, rw, bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), st,
+                     c->launch);
+  return after_launch(c, "bt_register_pairs");
+}
+
+bt_status bt_register_pairs(bt_ctx *c, const bt_keypoints *kp, const bt_maps *maps, const bt_intrinsics *K,
+                            const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid, int32_t P,
+                            const bt_match_params *mprm, const bt_ransac_params *rprm, const bt_edge_params *eprm,
+                            uint32_t *records, void *stream) {
+  BT_CHECK_CTX(c);
+  bt_status s;
+  if ((s = check_kp(c, kp)) != BT_OK) return s;
+  if ((s = check_ransac(c, rprm)) != BT_OK) return s;
+  if (eprm) {
+    if ((s = check_edge(c, eprm)) != BT_OK) return s;
+    if ((s = check_maps(c, maps, K)) != BT_OK) return s;
+    if (!node_pose) return fail(c, BT_EINVAL, "bt_register_pairs: node_pose NULL");
+    if (maps->n_frames < kp->n_frames) return fail(c, BT_EINVAL, "maps cover fewer frames than keypoints");
+  }
+  if (P < 0) return fail(c, BT_EINVAL, "P < 0");
+  if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
+  if (P == 0) return BT_OK;
+  if (!pairs || !pair_uid || !records) return fail(c, BT_EINVAL, "bt_register_pairs: NULL buffer");
+  return register_pairs_dev(c, kp, maps, K, node_pose, pairs, pair_uid, P, mprm, rprm, eprm, records,
+                            (cudaStream_t)stream);
+}
+
+bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_maps *maps, const bt_intrinsics *K,
+                                 const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid,
+                                 int32_t P, const bt_match_params *mprm, const bt_ransac_params *rprm,
+                                 const bt_edge_params *eprm, uint32_t *records, void *stream) {
+  BT_CHECK_CTX(c);
+  bt_status s;
+  if (!kp) return fail(c, BT_EINVAL, "keypoints: NULL");
+  if (kp->n_frames > c->cap_frames) return fail(c, BT_ECAPACITY, "frames %d > reserved %d", kp->n_frames, c->cap_frames);
+  if ((s = check_ransac(c, rprm)) != BT_OK) return s;
+  if (P < 0) return fail(c, BT_EINVAL, "P < 0");
+  if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
+  if (kp->n_max > c->cap_nmax) return fail(c, BT_ECAPACITY, "n_max %d > reserved %d", kp->n_max, c->cap_nmax);
+  if (P == 0) return BT_OK;
+  if (!pairs || !pair_uid || !records || !kp->n_kp || !kp->desc || !kp->pts || !kp->nrm)
+    return fail(c, BT_EINVAL, "bt_register_pairs_host: NULL buffer");
+  if (eprm) {
+    if (!maps || !K || !node_pose) return fail(c, BT_EINVAL, "bt_register_pairs_host: NULL maps/K/poses");
+    if (maps->n_frames > c->cap_frames || maps->width * maps->height > c->cap_w * c->cap_h)
+      return fail(c, BT_ECAPACITY, "maps beyond reserved staging");
+  }
+  const cudaStream_t st = (cudaStream_t)stream;
+  const int F = kp->n_frames;
+  const size_t FN = (size_t)F * kp->n_max;
+  cudaMemcpyAsync(c->st_nkp, kp->n_kp, (size_t)F * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_desc, kp->desc, FN * 128 * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_pts, kp->pts, FN * 12, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_nrm, kp->nrm, FN * 12, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_pairs, pairs, (size_t)P * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_uid, pair_uid, (size_t)P * 4, cudaMemcpyHostToDevice, st);
+  bt_keypoints dk = *kp;
+  dk.n_kp = c->st_nkp; dk.desc = c->st_desc; dk.pts = c->st_pts; dk.nrm = c->st_nrm;
+  bt_maps dm{};
+  if (eprm) {
+    const size_t FP = (size_t)maps->n_frames * maps->width * maps->height;
+    cudaMemcpyAsync(c->st_depth, maps->depth, FP * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(c->st_normal, maps->normal, FP * 12, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(c->st_mask, maps->mask, FP, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(c->st_pose, node_pose, (size_t)maps->n_frames * sizeof(bt_pose), cudaMemcpyHostToDevice, st);
+    dm = *maps;
+    dm.depth = c->st_depth; dm.normal = c->st_normal; dm.mask = c->st_mask;
+  }
+  if ((s = after_launch(c, "bt_register_pairs_host: H2D")) != BT_OK) return s;
+  s = bt_register_pairs(c, &dk, eprm ? &dm : nullptr, K, eprm ? c->st_pose : nullptr, c->st_pairs, c->st_uid, P,
+                        mprm, rprm, eprm, c->st_records, stream);
+  if (s != BT_OK) return s;
+  const int launches = c->launch.count;
+  cudaMemcpyAsync(records, c->st_records, (size_t)P * bt::rec_words(kp->n_max) * 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return fail(c, BT_ECUDA, "bt_register_pairs_host: sync failed");
+  c->launch.count = launches;
+  return after_launch(c, "bt_register_pairs_host");
+}
+
+bt_status bt_compose_poses(bt_ctx *c, const bt_pose *a, const bt_pose *b, bt_pose *out, int32_t n, void *stream) {
+  BT_CHECK_CTX(c);
+  if (n < 0) return fail(c, BT_EINVAL, "n < 0");
+  if (n == 0) return BT_OK;
+  if (!a || !b || !out) return fail(c, BT_EINVAL, "bt_compose_poses: NULL buffer");
+  bt::launch_compose(a, b, out, n, (cudaStream_t)stream, c->launch);
+  return after_launch(c, "bt_compose_poses");
+}
+
+static const char *kKernelNames[bt::K_COUNT] = {"k_nearest", "k_mutual", "k_ransac_score",
+                                                 "k_ransac_finish", "k_dense", "k_dense_reduce",
+                                                 "k_compose"};
+
+static cudaEvent_t take_event(bt_ctx *c) {
+  if (c->ev_pool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = c->ev_pool.back();
+  c->ev_pool.pop_back();
+  return e;
+}
+
+static void prof_hook(void *user, int kid, int phase, cudaStream_t s) {
+  bt_ctx *c = (bt_ctx *)user;
+  cudaEvent_t e = take_event(c);
+  cudaEventRecord(e, s);
+  if (phase == 0) c->pending.push_back({kid, e, nullptr});
+  else c->pending.back().stop = e;
+}
+
+bt_status bt_profile_enable(bt_ctx *c, int32_t on) {
+  BT_CHECK_CTX(c);
+  c->prof_on = on != 0;
+  c->launch.hook = c->prof_on ? prof_hook : nullptr;
+  c->launch.user = c;
+  return BT_OK;
+}
+
+int32_t bt_profile_kernels(void) { return bt::K_COUNT; }
+
+const char *bt_profile_name(int32_t k) { return (k >= 0 && k < bt::K_COUNT) ? kKernelNames[k] : "?"; }
+
+bt_status bt_profile_read(bt_ctx *c, int32_t kid, double *total_ms, int64_t *launches) {
+  if (!c) return BT_EINVAL;
+  if (kid < 0 || kid >= bt::K_COUNT || !total_ms || !launches) return fail(c, BT_EINVAL, "bt_profile_read: bad args");
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, BT_ECUDA, "cudaSetDevice failed");
+  for (auto &p : c->pending) {                 // fold every completed bracket into the totals
+    if (!p.stop) continue;
+    if (cudaEventSynchronize(p.stop) != cudaSuccess) return fail(c, BT_ECUDA, "bt_profile_read: event sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.start, p.stop);
+    c->prof_ms[p.kid] += ms;
+    c->prof_n[p.kid] += 1;
+    c->ev_pool.push_back(p.start);
+    c->ev_pool.push_back(p.stop);
+  }
+  c->pending.clear();
+  *total_ms = c->prof_ms[kid];
+  *launches = c->prof_n[kid];
+  c->prof_ms[kid] = 0.0;
+  c->prof_n[kid] = 0;
+  return BT_OK;
+}
+
+}  // extern "C"

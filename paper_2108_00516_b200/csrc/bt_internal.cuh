@@ -1,0 +1,68 @@
+// bt_internal.cuh — internal launch interfaces and device helpers of libbt (sm_100a).
+// Not part of the ABI (include/bt.h is).  Nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bt.h"
+
+namespace bt {
+
+constexpr int kDim = 128;               // descriptor length, D_i in R^128
+
+// ---- record layout (see bt.h) -------------------------------------------------------
+constexpr int kRecStatus = 0, kRecNMatch = 1, kRecBestHyp = 2, kRecBestCount = 3;
+constexpr int kRecTBest = 4, kRecTRefit = 16, kRecMask = 28;
+__host__ __device__ inline int mask_words(int n_max) { return (n_max + 31) / 32; }
+__host__ __device__ inline int rec_dense_ij(int n_max) { return kRecMask + mask_words(n_max); }
+__host__ __device__ inline int rec_dense_ji(int n_max) { return rec_dense_ij(n_max) + 32; }
+__host__ __device__ inline int rec_feat(int n_max) { return rec_dense_ij(n_max) + 64; }
+__host__ __device__ inline int rec_words(int n_max) { return rec_dense_ij(n_max) + 64 + 96; }
+
+// ---- device views of the ABI structs ---------------------------------------------------
+struct KpView {
+  int n_frames, n_max;
+  const int32_t *n_kp;
+  const float *desc, *pts, *nrm;
+};
+struct MapView {
+  int n_frames, W, H;
+  const float *depth, *normal;
+  const uint8_t *mask;
+};
+
+// ---- launch bookkeeping: counts kernels and (optionally) brackets each with events ----
+enum KernelId {
+  K_NEAREST = 0, K_MUTUAL, K_RANSAC_SCORE, K_RANSAC_FINISH, K_DENSE, K_DENSE_REDUCE, K_COMPOSE,
+  K_COUNT
+};
+struct Launch {
+  int count = 0;
+  void (*hook)(void *user, int kernel_id, int phase, cudaStream_t s) = nullptr;
+  void *user = nullptr;
+  void begin(int k, cudaStream_t s) { if (hook) hook(user, k, 0, s); }
+  void end(int k, cudaStream_t s) { ++count; if (hook) hook(user, k, 1, s); }
+};
+
+// ---- launchers (stream-ordered, no sync) -------------------------------------------
+// matching
+void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, int32_t *nn_ab,
+                  int32_t *nn_ba, uint8_t *ratio_ok, int32_t *matches, int32_t *n_matches,
+                  cudaStream_t s, Launch &L);
+// RANSAC scoring + finish (+ optional Eq. (2) blocks at node poses)
+void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, int P,
+                   const int32_t *matches, const int32_t *n_matches, const bt_ransac_params &prm,
+                   unsigned long long *best_key, uint32_t *records, int rec_stride,
+                   int32_t *hyp_counts, const bt_pose *node_pose, float huber, cudaStream_t s,
+                   Launch &L);
+// dense Eq. (3): edges either explicit (edges != null) or derived from pairs (2 per pair)
+void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose,
+                  const int32_t *edges, const int32_t *pairs, int E, const bt_edge_params &prm,
+                  float *partials, int max_partials_per_edge, float *out, int out_stride,
+                  uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
+                  cudaStream_t s, Launch &L);
+int dense_partials_per_edge(int W, int H);
+void launch_compose(const bt_pose *a, const bt_pose *b, bt_pose *out, int n, cudaStream_t s,
+                    Launch &L);
+
+}  // namespace bt

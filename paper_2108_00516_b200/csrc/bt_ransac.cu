@@ -1,0 +1,642 @@
+// bt_ransac.cu — RANSAC over 3-pair samples, best-hypothesis refit and the Eq. (2)
+// feature-edge blocks.
+//
+//  k_ransac_score   one lane per hypothesis: Philox4x32-10 (counter (h, uid, 0, 0), key =
+//                   seed) -> distinct triple (reading R6) -> closed-form 3-point Arun in
+//                   fp64 (triangle frames + 2x2 Procrustes, reading R7) -> R, t in fp32.
+//                   Then each warp scores its 32 hypotheses, 4 at a time held in registers,
+//                   against the pair's correspondences staged in shared memory as four
+//                   float4 streams (p_a, p_b, O = n_b n_a^T): 24 FMA-pipe instructions per
+//                   (hypothesis, correspondence) test.  Per-lane integer counts are combined
+//                   by a 31-shuffle transpose reduction; the per-pair best is an atomicMax
+//                   on the key ((count+1) << 32 | ~h): max count, ties -> lowest h (R11).
+//  k_ransac_finish  one CTA per pair: re-derives h* (same noinline solver => same bits),
+//                   inlier mask by ballot, refit by fp64 cross-covariance + Jacobi SVD with
+//                   the det fix (north star, R12), status, and — when node poses are given —
+//                   the Eq. (2) J^T W J blocks at those poses in fp64, reduced in a fixed order.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "bt_internal.cuh"
+
+namespace bt {
+namespace {
+
+constexpr int kScoreThreads = 256;
+constexpr int kHypPerThread = 1;
+constexpr int kHypPerBlock = kScoreThreads * kHypPerThread;
+constexpr int kMaxChunk = 1024;           // correspondences staged per smem pass
+
+// ---------------------------------------------------------------- Philox4x32-10
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// distinct ordered triple in [0, M): floor(r * n / 2^32) with skips (R6)
+__device__ __forceinline__ void sample_triple(uint4 r, int M, int &i0, int &i1, int &i2) {
+  const uint32_t a = __umulhi(r.x, (uint32_t)M);
+  uint32_t b = __umulhi(r.y, (uint32_t)(M - 1));
+  if (b >= a) ++b;
+  uint32_t c = __umulhi(r.z, (uint32_t)(M - 2));
+  const uint32_t lo = min(a, b), hi = max(a, b);
+  if (c >= lo) ++c;
+  if (c >= hi) ++c;
+  i0 = (int)a; i1 = (int)b; i2 = (int)c;
+}
+
+// ---------------------------------------------------------------- fp64 3-point Arun
+struct d3 { double x, y, z; };
+__device__ __forceinline__ d3 mk(double x, double y, double z) { return {x, y, z}; }
+__device__ __forceinline__ d3 sub(d3 a, d3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ d3 cross(d3 a, d3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ d3 scale(d3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+
+// R, t minimising sum_k |R a_k + t - b_k|^2 for three correspondences.  Centred points of a
+// triangle lie in its plane: in orthonormal in-plane frames (e1, e2) / (f1, f2) the
+// cross-covariance is E_a M E_b^T with the 2x2 M = sum alpha_k beta_k^T, so its singular
+// values are those of M: s1,2 = (p +- q)/2 with p = |(m00+m11, m01-m10)|,
+// q = |(m00-m11, m01+m10)|.  The optimal proper rotation maps n_a -> +n_b with an in-plane
+// rotation (value p) or n_a -> -n_b with an in-plane reflection (value q); the larger wins.
+// Returns false when degenerate: s2/s1 < tau (R8) or a collinear / coincident triangle.
+// __noinline__: scoring and finish kernels execute the very same instructions.
+__device__ __noinline__ bool solve3(const float *A, const float *B, double tau, float *out) {
+  const d3 a0 = mk(A[0], A[1], A[2]), a1 = mk(A[3], A[4], A[5]), a2 = mk(A[6], A[7], A[8]);
+  const d3 b0 = mk(B[0], B[1], B[2]), b1 = mk(B[3], B[4], B[5]), b2 = mk(B[6], B[7], B[8]);
+  const double third = 1.0 / 3.0;
+  const d3 ac = scale(mk(a0.x + a1.x + a2.x, a0.y + a1.y + a2.y, a0.z + a1.z + a2.z), third);
+  const d3 bc = scale(mk(b0.x + b1.x + b2.x, b0.y + b1.y + b2.y, b0.z + b1.z + b2.z), third);
+  const d3 ua = sub(a1, a0), ub = sub(b1, b0);
+  const d3 na = cross(ua, sub(a2, a0)), nb = cross(ub, sub(b2, b0));
+  const double lua = sqrt(dot(ua, ua)), lub = sqrt(dot(ub, ub));
+  const double lna = sqrt(dot(na, na)), lnb = sqrt(dot(nb, nb));
+  if (!(lua > 0.0) || !(lub > 0.0) || !(lna > 0.0) || !(lnb > 0.0)) return false;
+  const d3 e1 = scale(ua, 1.0 / lua), n = scale(na, 1.0 / lna), e2 = cross(n, e1);
+  const d3 f1 = scale(ub, 1.0 / lub), m = scale(nb, 1.0 / lnb), f2 = cross(m, f1);
+  double m00 = 0, m01 = 0, m10 = 0, m11 = 0;
+  const d3 as[3] = {sub(a0, ac), sub(a1, ac), sub(a2, ac)};
+  const d3 bs[3] = {sub(b0, bc), sub(b1, bc), sub(b2, bc)};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double x0 = dot(e1, as[k]), x1 = dot(e2, as[k]);
+    const double y0 = dot(f1, bs[k]), y1 = dot(f2, bs[k]);
+    m00 += x0 * y0; m01 += x0 * y1; m10 += x1 * y0; m11 += x1 * y1;
+  }
+  const double p = hypot(m00 + m11, m01 - m10), q = hypot(m00 - m11, m01 + m10);
+  const double s1 = 0.5 * (p + q), s2 = 0.5 * fabs(p - q);
+  if (!(s1 > 0.0) || s2 / s1 < tau) return false;
+  double q00, q01, q10, q11, sg;
+  if (p >= q) {                                  // rotation branch, R n_a = n_b
+    const double c = (m00 + m11) / p, s = (m01 - m10) / p;
+    q00 = c; q01 = -s; q10 = s; q11 = c; sg = 1.0;
+  } else {                                       // reflection branch, R n_a = -n_b
+    const double c = (m00 - m11) / q, s = (m01 + m10) / q;
+    q00 = c; q01 = s; q10 = s; q11 = -c; sg = -1.0;
+  }
+  // R = [f1 f2 m] diag(Q, sg) [e1 e2 n]^T
+  const d3 c0 = mk(q00 * f1.x + q10 * f2.x, q00 * f1.y + q10 * f2.y, q00 * f1.z + q10 * f2.z);
+  const d3 c1 = mk(q01 * f1.x + q11 * f2.x, q01 * f1.y + q11 * f2.y, q01 * f1.z + q11 * f2.z);
+  const d3 c2 = scale(m, sg);
+  double R[9];
+  R[0] = c0.x * e1.x + c1.x * e2.x + c2.x * n.x;
+  R[1] = c0.x * e1.y + c1.x * e2.y + c2.x * n.y;
+  R[2] = c0.x * e1.z + c1.x * e2.z + c2.x * n.z;
+  R[3] = c0.y * e1.x + c1.y * e2.x + c2.y * n.x;
+  R[4] = c0.y * e1.y + c1.y * e2.y + c2.y * n.y;
+  R[5] = c0.y * e1.z + c1.y * e2.z + c2.y * n.z;
+  R[6] = c0.z * e1.x + c1.z * e2.x + c2.z * n.x;
+  R[7] = c0.z * e1.y + c1.z * e2.y + c2.z * n.y;
+  R[8] = c0.z * e1.z + c1.z * e2.z + c2.z * n.z;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) out[k] = (float)R[k];
+  out[9] = (float)(bc.x - (R[0] * ac.x + R[1] * ac.y + R[2] * ac.z));
+  out[10] = (float)(bc.y - (R[3] * ac.x + R[4] * ac.y + R[5] * ac.z));
+  out[11] = (float)(bc.z - (R[6] * ac.x + R[7] * ac.y + R[8] * ac.z));
+  return true;
+}
+
+// gather the sample's points and solve hypothesis h of a pair
+__device__ __forceinline__ bool make_hypothesis(int h, uint32_t uid, uint32_t k0, uint32_t k1, int M,
+                                                const int32_t *mt, const float *pa_f, const float *pb_f,
+                                                double tau, float *out) {
+  const uint4 r = philox4x32_10(make_uint4((uint32_t)h, uid, 0u, 0u), k0, k1);
+  int s[3];
+  sample_triple(r, M, s[0], s[1], s[2]);
+  float A[9], B[9];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int i = mt[2 * s[k]], j = mt[2 * s[k] + 1];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      A[3 * k + c] = pa_f[3 * i + c];
+      B[3 * k + c] = pb_f[3 * j + c];
+    }
+  }
+  return solve3(A, B, tau, out);
+}
+
+// ---------------------------------------------------------------- the inlier test
+// Correspondence m as four float4: q0 = (ax, ay, az, bx), q1 = (by, bz, O00, O01),
+// q2 = (O02, O10, O11, O12), q3 = (O20, O21, O22, 0) with O = n_b n_a^T, so that
+// (R n_a) . n_b = <R, O>_F.  Explicit _rn intrinsics: identical bits in every kernel.
+__device__ __forceinline__ bool inlier(const float *T, const float4 q0, const float4 q1,
+                                       const float4 q2, const float4 q3, float delta2, float cosa) {
+  const float ex = __fsub_rn(__fmaf_rn(T[0], q0.x, __fmaf_rn(T[1], q0.y, __fmaf_rn(T[2], q0.z, T[9]))), q0.w);
+  const float ey = __fsub_rn(__fmaf_rn(T[3], q0.x, __fmaf_rn(T[4], q0.y, __fmaf_rn(T[5], q0.z, T[10]))), q1.x);
+  const float ez = __fsub_rn(__fmaf_rn(T[6], q0.x, __fmaf_rn(T[7], q0.y, __fmaf_rn(T[8], q0.z, T[11]))), q1.y);
+  const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+  float c = __fmul_rn(T[0], q1.z);
+  c = __fmaf_rn(T[1], q1.w, c);
+  c = __fmaf_rn(T[2], q2.x, c);
+  c = __fmaf_rn(T[3], q2.y, c);
+  c = __fmaf_rn(T[4], q2.z, c);
+  c = __fmaf_rn(T[5], q2.w, c);
+  c = __fmaf_rn(T[6], q3.x, c);
+  c = __fmaf_rn(T[7], q3.y, c);
+  c = __fmaf_rn(T[8], q3.z, c);
+  return (d2 < delta2) & (c > cosa);
+}
+
+__device__ __forceinline__ void pack_corr(const float *pa, const float *na, const float *pb,
+                                          const float *nb, float4 &q0, float4 &q1, float4 &q2,
+                                          float4 &q3) {
+  q0 = make_float4(pa[0], pa[1], pa[2], pb[0]);
+  q1 = make_float4(pb[1], pb[2], __fmul_rn(nb[0], na[0]), __fmul_rn(nb[0], na[1]));
+  q2 = make_float4(__fmul_rn(nb[0], na[2]), __fmul_rn(nb[1], na[0]), __fmul_rn(nb[1], na[1]),
+                   __fmul_rn(nb[1], na[2]));
+  q3 = make_float4(__fmul_rn(nb[2], na[0]), __fmul_rn(nb[2], na[1]), __fmul_rn(nb[2], na[2]), 0.f);
+}
+
+struct ScoreArgs {
+  KpView kp;
+  const int32_t *pairs;
+  const uint32_t *uid;
+  const int32_t *matches;
+  const int32_t *n_matches;
+  int n_hyp, chunk;
+  uint32_t k0, k1;
+  float delta2, cosa;
+  double tau;
+  unsigned long long *best_key;
+  int32_t *hyp_counts;
+};
+
+__global__ void __launch_bounds__(kScoreThreads, 2) k_ransac_score(ScoreArgs A) {
+  extern __shared__ float4 sm4[];
+  const int chunk = A.chunk;
+  float4 *s0 = sm4, *s1 = sm4 + chunk, *s2 = sm4 + 2 * chunk, *s3 = sm4 + 3 * chunk;
+  float *hs = reinterpret_cast<float *>(sm4 + 4 * chunk);         // [256][12] hypotheses
+  const int p = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int M = A.n_matches[p];
+  const int H = A.n_hyp;
+  const int h = blockIdx.x * kHypPerBlock + threadIdx.x;
+  const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+  const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
+  const float *pa_f = A.kp.pts + (size_t)fa * A.kp.n_max * 3, *pb_f = A.kp.pts + (size_t)fb * A.kp.n_max * 3;
+  const float *na_f = A.kp.nrm + (size_t)fa * A.kp.n_max * 3, *nb_f = A.kp.nrm + (size_t)fb * A.kp.n_max * 3;
+
+  if (M < 3) {                                                   // FEW_MATCHES: no samples
+    if (A.hyp_counts && h < H) A.hyp_counts[(size_t)p * H + h] = -1;
+    return;
+  }
+  float T[12];
+  bool valid = false;
+  if (h < H) valid = make_hypothesis(h, A.uid[p], A.k0, A.k1, M, mt, pa_f, pb_f, A.tau, T);
+  if (!valid) {
+#pragma unroll
+    for (int k = 0; k < 12; ++k) T[k] = 0.f;
+  }
+  float4 *hs4 = reinterpret_cast<float4 *>(hs + 12 * threadIdx.x);
+  hs4[0] = make_float4(T[0], T[1], T[2], T[3]);
+  hs4[1] = make_float4(T[4], T[5], T[6], T[7]);
+  hs4[2] = make_float4(T[8], T[9], T[10], T[11]);
+
+  int acc[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) acc[c] = 0;
+  for (int c0 = 0; c0 < M; c0 += chunk) {
+    const int len = min(chunk, M - c0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < len; k += kScoreThreads) {
+      const int i = mt[2 * (c0 + k)], j = mt[2 * (c0 + k) + 1];
+      float4 q0, q1, q2, q3;
+      pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
+      s0[k] = q0; s1[k] = q1; s2[k] = q2; s3[k] = q3;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      float Th[4][12];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float4 *src = reinterpret_cast<const float4 *>(hs + 12 * (warp * 32 + 4 * g + k));
+        const float4 x = src[0], y = src[1], z = src[2];
+        Th[k][0] = x.x; Th[k][1] = x.y; Th[k][2] = x.z; Th[k][3] = x.w;
+        Th[k][4] = y.x; Th[k][5] = y.y; Th[k][6] = y.z; Th[k][7] = y.w;
+        Th[k][8] = z.x; Th[k][9] = z.y; Th[k][10] = z.z; Th[k][11] = z.w;
+      }
+      for (int m = lane; m < len; m += 32) {
+        const float4 q0 = s0[m], q1 = s1[m], q2 = s2[m], q3 = s3[m];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[4 * g + k] += inlier(Th[k], q0, q1, q2, q3, A.delta2, A.cosa);
+      }
+    }
+  }
+  // transpose reduction: lane l ends with the total of acc[l] (= hypothesis warp*32 + l)
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int c = 0; c < o; ++c) {
+      const int send = upper ? acc[c] : acc[c + o];
+      const int keep = upper ? acc[c + o] : acc[c];
+      acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  const int count = valid ? acc[0] : -1;
+  unsigned long long key = 0ull;
+  if (h < H) {
+    if (A.hyp_counts) A.hyp_counts[(size_t)p * H + h] = count;
+    key = ((unsigned long long)(uint32_t)(count + 1) << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)h);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+    key = other > key ? other : key;
+  }
+  if (lane == 0 && key) atomicMax(A.best_key + p, key);
+}
+
+// ---------------------------------------------------------------- finish: refit + Eq. (2)
+// one-sided Jacobi SVD of a 3x3 (fp64): A = U diag(s) V^T, s descending
+__device__ void svd3_jacobi(const double *Ain, double *U, double *s, double *V) {
+  double a[9], v[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  for (int k = 0; k < 9; ++k) a[k] = Ain[k];
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rot = false;
+    for (int pq = 0; pq < 3; ++pq) {
+      const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2;
+      double al = 0, be = 0, ga = 0;
+      for (int r = 0; r < 3; ++r) {
+        al += a[3 * r + p] * a[3 * r + p];
+        be += a[3 * r + q] * a[3 * r + q];
+        ga += a[3 * r + p] * a[3 * r + q];
+      }
+      if (ga == 0.0 || fabs(ga) <= 2.220446049250313e-16 * sqrt(al * be)) continue;
+      rot = true;
+      const double z = (be - al) / (2.0 * ga);
+      const double t = (z >= 0 ? 1.0 : -1.0) / (fabs(z) + sqrt(1.0 + z * z));
+      const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+      for (int r = 0; r < 3; ++r) {
+        const double x = a[3 * r + p], y = a[3 * r + q];
+        a[3 * r + p] = c * x - sn * y;
+        a[3 * r + q] = sn * x + c * y;
+        const double vx = v[3 * r + p], vy = v[3 * r + q];
+        v[3 * r + p] = c * vx - sn * vy;
+        v[3 * r + q] = sn * vx + c * vy;
+      }
+    }
+    if (!rot) break;
+  }
+  double sv[3];
+  int o[3] = {0, 1, 2};
+  for (int k = 0; k < 3; ++k) sv[k] = sqrt(a[k] * a[k] + a[3 + k] * a[3 + k] + a[6 + k] * a[6 + k]);
+  for (int i = 0; i < 3; ++i)
+    for (int j = i + 1; j < 3; ++j)
+      if (sv[o[j]] > sv[o[i]]) { const int t = o[i]; o[i] = o[j]; o[j] = t; }
+  for (int k = 0; k < 3; ++k) {
+    s[k] = sv[o[k]];
+    for (int r = 0; r < 3; ++r) V[3 * r + k] = v[3 * r + o[k]];
+  }
+  const double tiny = 1e-300 + s[0] * 1e-15;
+  for (int k = 0; k < 2; ++k) {
+    if (s[k] > tiny) {
+      for (int r = 0; r < 3; ++r) U[3 * r + k] = a[3 * r + o[k]] / s[k];
+    } else {                                  // rank <= k: any orthonormal completion
+      double e[3] = {0, 0, 0};
+      int ax = 0;
+      double best = 2.0;
+      for (int r = 0; r < 3; ++r) {
+        const double c = k > 0 ? fabs(U[3 * r]) : 0.0;
+        if (c < best) { best = c; ax = r; }
+      }
+      e[ax] = 1.0;
+      for (int j = 0; j < k; ++j) {
+        const double d = e[0] * U[j] + e[1] * U[3 + j] + e[2] * U[6 + j];
+        for (int r = 0; r < 3; ++r) e[r] -= d * U[3 * r + j];
+      }
+      const double nr = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+      for (int r = 0; r < 3; ++r) U[3 * r + k] = e[r] / nr;
+    }
+  }
+  U[2] = U[3] * U[7] - U[6] * U[4];           // u3 = u1 x u2 (sign is fixed by the det fix)
+  U[5] = U[6] * U[1] - U[0] * U[7];
+  U[8] = U[0] * U[4] - U[3] * U[1];
+}
+
+__device__ __forceinline__ double det3(const double *M) {
+  return M[0] * (M[4] * M[8] - M[5] * M[7]) - M[1] * (M[3] * M[8] - M[5] * M[6]) +
+         M[2] * (M[3] * M[7] - M[4] * M[6]);
+}
+
+// fixed-order block sum of one double (256 threads, result valid in every thread)
+template <int NT>
+__device__ double block_sum(double v, double *red) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < NT / 32; ++w) t += red[w];
+  return t;
+}
+
+struct FinishArgs {
+  KpView kp;
+  const int32_t *pairs;
+  const uint32_t *uid;
+  const int32_t *matches;
+  const int32_t *n_matches;
+  int n_hyp, min_inliers;
+  uint32_t k0, k1;
+  float delta2, cosa;
+  double tau;
+  const unsigned long long *best_key;
+  uint32_t *records;
+  int rec_stride;
+  const bt_pose *node_pose;      // null: no feature blocks
+  double huber;
+};
+
+constexpr int kFinThreads = 256;
+constexpr int kFeatChunk = 64;
+// per-inlier feature data staged in smem: e(3) J(3x12) w rho
+constexpr int kFeatRow = 3 + 36 + 2;
+
+__global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
+  __shared__ float Tb[12];
+  __shared__ double red[kFinThreads / 32];
+  __shared__ double fstage[kFeatChunk * kFeatRow];
+  __shared__ int sh_idx[kFeatChunk];
+  __shared__ double shT[12];
+  __shared__ int sh_status;
+  const int p = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_max = A.kp.n_max, W = mask_words(n_max);
+  const int M = A.n_matches[p];
+  uint32_t *rec = A.records + (size_t)p * A.rec_stride;
+  const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+  const int32_t *mt = A.matches + (size_t)p * n_max * 2;
+  const float *pa_f = A.kp.pts + (size_t)fa * n_max * 3, *pb_f = A.kp.pts + (size_t)fb * n_max * 3;
+  const float *na_f = A.kp.nrm + (size_t)fa * n_max * 3, *nb_f = A.kp.nrm + (size_t)fb * n_max * 3;
+
+  int status = BT_PAIR_OK, best_h = -1;
+  const unsigned long long key = A.best_key[p];
+  const uint32_t c1 = (uint32_t)(key >> 32);
+  if (M < 3) status = BT_PAIR_FEW_MATCHES;
+  else if (c1 == 0u) status = BT_PAIR_FEW_INLIERS;                 // every hypothesis degenerate
+  else best_h = (int)(0xFFFFFFFFu - (uint32_t)key);
+
+  if (tid == 0) {
+    bool ok = false;
+    if (best_h >= 0) {
+      float T[12];
+      ok = make_hypothesis(best_h, A.uid[p], A.k0, A.k1, M, mt, pa_f, pb_f, A.tau, T);
+      for (int k = 0; k < 12; ++k) Tb[k] = T[k];
+    }
+    if (!ok) {
+      for (int k = 0; k < 12; ++k) Tb[k] = (k == 0 || k == 4 || k == 8) ? 1.f : 0.f;
+    }
+  }
+  __syncthreads();
+  // inlier mask C_ij of h* (all words up to n_max written; bit m = match m)
+  float T[12];
+  for (int k = 0; k < 12; ++k) T[k] = Tb[k];
+  int cnt = 0;
+  for (int m0 = 0; m0 < W * 32; m0 += kFinThreads) {
+    const int m = m0 + tid;
+    bool in = false;
+    if (best_h >= 0 && m < M) {
+      const int i = mt[2 * m], j = mt[2 * m + 1];
+      float4 q0, q1, q2, q3;
+      pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
+      in = inlier(T, q0, q1, q2, q3, A.delta2, A.cosa);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if (lane == 0 && (m0 >> 5) + warp < W) rec[kRecMask + (m0 >> 5) + warp] = bal;
+    cnt += lane == 0 ? __popc(bal) : 0;
+  }
+  const int best_count = (int)block_sum<kFinThreads>((double)cnt, red);
+  if (best_h >= 0 && best_count < A.min_inliers) status = BT_PAIR_FEW_INLIERS;
+
+  // refit: Arun on all inliers (fp64), two-pass centroid / cross-covariance
+  double Rr[9], tr[3];
+  bool refit_ok = false;
+  if (status == BT_PAIR_OK) {
+    double sa[3] = {0, 0, 0}, sb[3] = {0, 0, 0};
+    for (int m = tid; m < M; m += kFinThreads) {
+      if (!((rec[kRecMask + (m >> 5)] >> (m & 31)) & 1u)) continue;
+      const int i = mt[2 * m], j = mt[2 * m + 1];
+      for (int c = 0; c < 3; ++c) { sa[c] += pa_f[3 * i + c]; sb[c] += pb_f[3 * j + c]; }
+    }
+    double ca[3], cb[3];
+    for (int c = 0; c < 3; ++c) {
+      ca[c] = block_sum<kFinThreads>(sa[c], red) / best_count;
+      cb[c] = block_sum<kFinThreads>(sb[c], red) / best_count;
+    }
+    double Hl[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int m = tid; m < M; m += kFinThreads) {
+      if (!((rec[kRecMask + (m >> 5)] >> (m & 31)) & 1u)) continue;
+      const int i = mt[2 * m], j = mt[2 * m + 1];
+      double da[3], db[3];
+      for (int c = 0; c < 3; ++c) { da[c] = pa_f[3 * i + c] - ca[c]; db[c] = pb_f[3 * j + c] - cb[c]; }
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) Hl[3 * r + c] += da[r] * db[c];
+    }
+    double Hm[9];
+    for (int k = 0; k < 9; ++k) Hm[k] = block_sum<kFinThreads>(Hl[k], red);
+    if (tid == 0) {
+      double U[9], s[3], V[9];
+      svd3_jacobi(Hm, U, s, V);
+      const double ratio = s[0] > 0 ? s[1] / s[0] : 0.0;
+      if (ratio < A.tau) {
+        sh_status = BT_PAIR_REFIT_DEGENERATE;
+      } else {
+        sh_status = BT_PAIR_OK;
+        const double d = det3(V) * det3(U) > 0 ? 1.0 : -1.0;
+        for (int r = 0; r < 3; ++r)
+          for (int c = 0; c < 3; ++c)
+            shT[3 * r + c] = V[3 * r] * U[3 * c] + V[3 * r + 1] * U[3 * c + 1] + d * V[3 * r + 2] * U[3 * c + 2];
+        for (int r = 0; r < 3; ++r)
+          shT[9 + r] = cb[r] - (shT[3 * r] * ca[0] + shT[3 * r + 1] * ca[1] + shT[3 * r + 2] * ca[2]);
+      }
+    }
+    __syncthreads();
+    status = sh_status;
+    refit_ok = status == BT_PAIR_OK;
+    for (int k = 0; k < 9; ++k) Rr[k] = shT[k];
+    for (int k = 0; k < 3; ++k) tr[k] = shT[9 + k];
+  }
+  if (tid == 0) {
+    rec[kRecStatus] = (uint32_t)status;
+    rec[kRecNMatch] = (uint32_t)M;
+    rec[kRecBestHyp] = (uint32_t)best_h;
+    rec[kRecBestCount] = (uint32_t)(best_h >= 0 ? best_count : 0);
+    for (int k = 0; k < 12; ++k) rec[kRecTBest + k] = __float_as_uint(Tb[k]);
+    for (int k = 0; k < 12; ++k)
+      rec[kRecTRefit + k] = __float_as_uint(refit_ok ? (float)(k < 9 ? Rr[k] : tr[k - 9]) : Tb[k]);
+  }
+  if (A.node_pose == nullptr) return;
+
+  // ---- Eq. (2) feature edge at the node poses, fp64, fixed-order reduction ----------
+  // e = R_i^T (p_m - t_i) - R_j^T (p_n - t_j);  J_i = -R_i^T [I | -[p_m]x],
+  // J_j = R_j^T [I | -[p_n]x];  H += w J^T J, g += w J^T e, E += rho(|e|).
+  double Ri[9], ti[3], Rj[9], tj[3];
+  {
+    const bt_pose Pi = A.node_pose[fa], Pj = A.node_pose[fb];
+    for (int k = 0; k < 9; ++k) { Ri[k] = Pi.R[k]; Rj[k] = Pj.R[k]; }
+    for (int k = 0; k < 3; ++k) { ti[k] = Pi.t[k]; tj[k] = Pj.t[k]; }
+  }
+  // output entry owned by this thread (tid < 92): (a, b) of the 12x12 H, or g / E / count
+  int oa = -1, ob = -1, kind = -1;   // kind 0: H(a,b)  1: g(a)  2: E  3: count
+  {
+    int k = tid;
+    if (k < 21) {                      // H_ii upper
+      int a = 0;
+      while (k >= 6 - a) { k -= 6 - a; ++a; }
+      oa = a; ob = a + k; kind = 0;
+    } else if (k < 57) {               // H_ij
+      k -= 21; oa = k / 6; ob = 6 + k % 6; kind = 0;
+    } else if (k < 78) {               // H_jj upper
+      k -= 57;
+      int a = 0;
+      while (k >= 6 - a) { k -= 6 - a; ++a; }
+      oa = 6 + a; ob = 6 + a + k; kind = 0;
+    } else if (k < 90) { oa = k - 78; kind = 1; }
+    else if (k == 90) kind = 2;
+    else if (k == 91) kind = 3;
+  }
+  double acc = 0.0;
+  const int n_in = best_h >= 0 ? best_count : 0;        // C_ij = inliers of h*, whatever the status
+  // walk the inliers in match order, kFeatChunk at a time
+  int m_next = 0;
+  for (int done = 0; done < n_in; done += kFeatChunk) {
+    __syncthreads();
+    if (tid == 0) {                    // collect the next chunk of inlier indices (in order)
+      int c = 0;
+      while (c < kFeatChunk && m_next < M) {
+        if ((rec[kRecMask + (m_next >> 5)] >> (m_next & 31)) & 1u) sh_idx[c++] = m_next;
+        ++m_next;
+      }
+      for (; c < kFeatChunk; ++c) sh_idx[c] = -1;
+    }
+    __syncthreads();
+    if (tid < kFeatChunk && sh_idx[tid] >= 0) {
+      const int m = sh_idx[tid];
+      const int i = mt[2 * m], j = mt[2 * m + 1];
+      const double pm[3] = {pa_f[3 * i], pa_f[3 * i + 1], pa_f[3 * i + 2]};
+      const double pn[3] = {pb_f[3 * j], pb_f[3 * j + 1], pb_f[3 * j + 2]};
+      double *row = fstage + tid * kFeatRow;
+      double e[3];
+      for (int r = 0; r < 3; ++r) {
+        e[r] = Ri[r] * (pm[0] - ti[0]) + Ri[3 + r] * (pm[1] - ti[1]) + Ri[6 + r] * (pm[2] - ti[2]) -
+               (Rj[r] * (pn[0] - tj[0]) + Rj[3 + r] * (pn[1] - tj[1]) + Rj[6 + r] * (pn[2] - tj[2]));
+        row[r] = e[r];
+      }
+      // J rows: r = 0..2, cols 0..11
+      for (int r = 0; r < 3; ++r) {
+        // (R^T)[r][c] = R[c][r]
+        for (int c = 0; c < 3; ++c) {
+          row[3 + 12 * r + c] = -Ri[3 * c + r];
+          row[3 + 12 * r + 6 + c] = Rj[3 * c + r];
+        }
+        // (R^T [p]x)[r][c] = sum_k R[k][r] S[k][c], S = [p]x
+        const double Sp[9] = {0, -pm[2], pm[1], pm[2], 0, -pm[0], -pm[1], pm[0], 0};
+        const double Sq[9] = {0, -pn[2], pn[1], pn[2], 0, -pn[0], -pn[1], pn[0], 0};
+        for (int c = 0; c < 3; ++c) {
+          double x = 0, y = 0;
+          for (int k = 0; k < 3; ++k) { x += Ri[3 * k + r] * Sp[3 * k + c]; y += Rj[3 * k + r] * Sq[3 * k + c]; }
+          row[3 + 12 * r + 3 + c] = x;
+          row[3 + 12 * r + 9 + c] = -y;
+        }
+      }
+      const double nrm = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+      double w, rho;
+      if (nrm <= A.huber) { w = 1.0; rho = 0.5 * nrm * nrm; }
+      else { w = A.huber / nrm; rho = A.huber * (nrm - 0.5 * A.huber); }
+      row[39] = w;
+      row[40] = rho;
+    }
+    __syncthreads();
+    if (kind >= 0) {
+      const int nc = min(kFeatChunk, n_in - done);
+      for (int c = 0; c < nc; ++c) {
+        const double *row = fstage + c * kFeatRow;
+        const double *J = row + 3;
+        if (kind == 0) acc += row[39] * (J[oa] * J[ob] + J[12 + oa] * J[12 + ob] + J[24 + oa] * J[24 + ob]);
+        else if (kind == 1) acc += row[39] * (J[oa] * row[0] + J[12 + oa] * row[1] + J[24 + oa] * row[2]);
+        else if (kind == 2) acc += row[40];
+        else acc += 1.0;
+      }
+    }
+  }
+  const int fo = rec_feat(n_max);
+  if (tid < 96) rec[fo + tid] = __float_as_uint(kind >= 0 ? (float)acc : 0.f);
+  (void)warp;
+}
+
+}  // namespace
+
+void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, int P,
+                   const int32_t *matches, const int32_t *n_matches, const bt_ransac_params &prm,
+                   unsigned long long *best_key, uint32_t *records, int rec_stride,
+                   int32_t *hyp_counts, const bt_pose *node_pose, float huber, cudaStream_t s,
+                   Launch &L) {
+  if (P <= 0) return;
+  const int chunk = kp.n_max < kMaxChunk ? ((kp.n_max + 31) / 32) * 32 : kMaxChunk;
+  const size_t smem = (size_t)4 * chunk * sizeof(float4) + (size_t)kScoreThreads * 12 * sizeof(float);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_ransac_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         4 * kMaxChunk * (int)sizeof(float4) + kScoreThreads * 12 * (int)sizeof(float));
+    attr_done = true;
+  }
+  cudaMemsetAsync(best_key, 0, sizeof(unsigned long long) * P, s);
+  ScoreArgs a;
+  a.kp = kp; a.pairs = pairs; a.uid = uid; a.matches = matches; a.n_matches = n_matches;
+  a.n_hyp = prm.n_hyp; a.chunk = chunk;
+  a.k0 = (uint32_t)(prm.seed & 0xffffffffull); a.k1 = (uint32_t)(prm.seed >> 32);
+  a.delta2 = (float)((double)prm.delta_m * (double)prm.delta_m);
+  a.cosa = prm.cos_alpha;
+  a.tau = prm.min_sigma_ratio;
+  a.best_key = best_key;
+  a.hyp_counts = hyp_counts;
+  dim3 grid((prm.n_hyp + kHypPerBlock - 1) / kHypPerBlock, P);
+  L.begin(K_RANSAC_SCORE, s);
+  k_ransac_score<<<grid, kScoreThreads, smem, s>>>(a);
+  L.end(K_RANSAC_SCORE, s);
+  FinishArgs f;
+  f.kp = kp; f.pairs = pairs; f.uid = uid; f.matches = matches; f.n_matches = n_matches;
+  f.n_hyp = prm.n_hyp; f.min_inliers = prm.min_inliers;
+  f.k0 = a.k0; f.k1 = a.k1; f.delta2 = a.delta2; f.cosa = a.cosa; f.tau = a.tau;
+  f.best_key = best_key; f.records = records; f.rec_stride = rec_stride;
+  f.node_pose = node_pose; f.huber = huber;
+  L.begin(K_RANSAC_FINISH, s);
+  k_ransac_finish<<<P, kFinThreads, 0, s>>>(f);
+  L.end(K_RANSAC_FINISH, s);
+}
+
+}  // namespace bt

@@ -1,0 +1,352 @@
+"""GPU parity: the CUDA path through the C ABI (libbt.so via the ctypes binding) against the
+CPU oracle on the same seeded inputs.  Integer outputs bit-exact outside the band rule;
+poses within 1e-4 rad / 1e-5 m; J^T J within 1e-4 relative (north star)."""
+import numpy as np
+import pytest
+
+import oracle
+import parity
+import synth
+
+pytestmark = pytest.mark.gpu
+
+COS45 = float(np.cos(np.deg2rad(45.0)))
+SEED = synth.PHILOX_SEED
+DENSE = dict(dist_gate=0.02, cos_gate=COS45, huber_delta=0.005, stride=1)
+
+
+@pytest.fixture(scope="module")
+def bt():
+    import paper_2108_00516_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    return t
+
+
+@pytest.fixture(scope="module")
+def ctx(bt):
+    c = bt.Context(0)
+    c.reserve(256, 4096, 16384, 16, 640, 480)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def c2(bt):
+    sc = synth.make_scene(16)
+    return sc
+
+
+def _dev(torch, a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def gpu_match(bt, torch, ctx, scene, pairs, ratio=1.0):
+    fb = bt.FrameBatch.from_scene(scene)
+    P = len(pairs)
+    pr = _dev(torch, np.asarray(pairs, np.int32))
+    n_max = scene.desc.shape[1]
+    mt = torch.full((P, n_max, 2), -7, dtype=torch.int32, device="cuda")
+    nm = torch.zeros(P, dtype=torch.int32, device="cuda")
+    ctx.match(fb, pr, mt, nm, ratio)
+    torch.cuda.synchronize()
+    nm = nm.cpu().numpy()
+    mt = mt.cpu().numpy()
+    return [mt[p, :nm[p]] for p in range(P)], fb, pr
+
+
+# ------------------------------------------------------------------------------ smoke
+def test_smoke():
+    import __graft_entry__ as g
+    g.smoke()
+
+
+# ----------------------------------------------------------------------------- matching
+def test_match_parity_c2_all_pairs(bt, torch, ctx, c2):
+    pairs = synth.all_pairs(16)
+    got, _, _ = gpu_match(bt, torch, ctx, c2, pairs)
+    excluded = 0
+    for p, (a, b) in enumerate(pairs):
+        o = oracle.match(c2.desc[a, :c2.n_kp[a]], c2.desc[b, :c2.n_kp[b]])
+        excluded += parity.compare_matches(got[p], o)
+    assert excluded <= 2
+
+
+def test_match_ratio_test(bt, torch, ctx, c2):
+    pairs = synth.all_pairs(16)[:20]
+    got, _, _ = gpu_match(bt, torch, ctx, c2, pairs, ratio=0.8)
+    for p, (a, b) in enumerate(pairs):
+        o = oracle.match(c2.desc[a, :c2.n_kp[a]], c2.desc[b, :c2.n_kp[b]], ratio=0.8)
+        parity.compare_matches(got[p], o)
+
+
+def _custom_scene(n_kps, n_max=512, seed=0, dup=False):
+    rng = np.random.default_rng(seed)
+    F = len(n_kps)
+    sc = synth.make_scene(2, render_maps=False, seed=seed)
+    desc = np.zeros((F, n_max, 128), np.float32)
+    pts = np.zeros((F, n_max, 3), np.float32)
+    nrm = np.zeros((F, n_max, 3), np.float32)
+    base = rng.normal(size=(n_max, 128))
+    for f, n in enumerate(n_kps):
+        x = base[rng.permutation(n_max)[:n]] + 0.05 * rng.normal(size=(n, 128))
+        desc[f, :n] = x / np.linalg.norm(x, axis=1, keepdims=True)
+        pts[f, :n] = rng.normal(scale=0.05, size=(n, 3)) + [0, 0, 0.6]
+        v = rng.normal(size=(n, 3))
+        nrm[f, :n] = v / np.linalg.norm(v, axis=1, keepdims=True)
+    if dup and n_kps[0] > 3:
+        desc[0, 1] = desc[0, 2]                      # exact duplicate descriptors -> ties
+    sc.n_kp = np.asarray(n_kps, np.int32)
+    sc.desc, sc.pts, sc.nrm = desc, pts, nrm
+    sc.depth = sc.normal = sc.mask = None
+    return sc
+
+
+def test_match_edge_cases(bt, torch, ctx):
+    sc = _custom_scene([0, 1, 2, 37, 512, 300, 511], dup=True)
+    sc.desc[6, :300] = sc.desc[5, :300]              # identical sets -> identity
+    pairs = [(0, 4), (4, 0), (1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (6, 5), (0, 0), (4, 4), (3, 3)]
+    got, _, _ = gpu_match(bt, torch, ctx, sc, pairs)
+    for p, (a, b) in enumerate(pairs):
+        o = oracle.match(sc.desc[a, :sc.n_kp[a]], sc.desc[b, :sc.n_kp[b]])
+        parity.compare_matches(got[p], o)
+    assert len(got[0]) == 0 and len(got[8]) == 0
+    assert got[9].tolist() == [[i, i] for i in range(512)]
+
+
+# -------------------------------------------------------------------------------- RANSAC
+def gpu_ransac(bt, torch, ctx, scene, pairs, match_lists, n_hyp, uids=None, seed=SEED):
+    fb = bt.FrameBatch.from_scene(scene)
+    P = len(pairs)
+    n_max = scene.desc.shape[1]
+    mt = np.zeros((P, n_max, 2), np.int32)
+    nm = np.zeros(P, np.int32)
+    for p, m in enumerate(match_lists):
+        mt[p, :len(m)] = m
+        nm[p] = len(m)
+    uid = np.arange(P, dtype=np.uint32) if uids is None else np.asarray(uids, np.uint32)
+    rw = bt.record_words(n_max)
+    rec = torch.zeros((P, rw), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((P, n_hyp), dtype=torch.int32, device="cuda")
+    ctx.ransac(fb, _dev(torch, np.asarray(pairs, np.int32)), _dev(torch, uid.view(np.int32)), _dev(torch, mt),
+               _dev(torch, nm), bt.ransac_params(n_hyp, seed), rec, cnt)
+    torch.cuda.synchronize()
+    return bt.decode_records(rec, n_max), cnt.cpu().numpy()
+
+
+def _pair_arrays(scene, a, b, m):
+    ia, ib = m[:, 0], m[:, 1]
+    return scene.pts[a][ia], scene.nrm[a][ia], scene.pts[b][ib], scene.nrm[b][ib]
+
+
+def _check_ransac(bt, torch, ctx, scene, pairs, n_hyp, uids=None):
+    mls = [oracle.match(scene.desc[a, :scene.n_kp[a]], scene.desc[b, :scene.n_kp[b]])["pairs"] for a, b in pairs]
+    rec, cnt = gpu_ransac(bt, torch, ctx, scene, pairs, mls, n_hyp, uids)
+    uids = np.arange(len(pairs)) if uids is None else uids
+    n_ambiguous = 0
+    for p, (a, b) in enumerate(pairs):
+        pa, na, pb, nb = _pair_arrays(scene, a, b, mls[p])
+        oc = oracle.ransac_counts(pa, na, pb, nb, n_hyp, int(uids[p]), SEED)
+        r = {k: v[p] for k, v in rec.items()}
+        fin = parity.compare_ransac(cnt[p], r, oc, pa, na, pb, nb, what=f"pair {p} ({a},{b})")
+        n_ambiguous += fin is None
+    return rec, cnt, n_ambiguous
+
+
+def test_ransac_parity_c1(bt, torch, ctx):
+    sc, Rt, tt, _ = synth.make_pair_c1()
+    rec, cnt, amb = _check_ransac(bt, torch, ctx, sc, [(0, 1)], 1024)
+    assert amb == 0 and rec["best_count"][0] == 350 and rec["status"][0] == 0
+
+
+def test_ransac_parity_c1_noisy_nonmultiple_hyp(bt, torch, ctx):
+    sc, *_ = synth.make_pair_c1(seed=7, point_noise=0.001)
+    _check_ransac(bt, torch, ctx, sc, [(0, 1), (1, 0)], 1000, uids=[3, 11])
+
+
+def test_ransac_parity_c2_pairs(bt, torch, ctx, c2):
+    pairs = [tuple(x) for x in synth.all_pairs(16)[::7]]
+    _, _, amb = _check_ransac(bt, torch, ctx, c2, pairs, 4096, uids=np.arange(len(pairs)) * 7)
+    assert amb <= 2
+
+
+def test_ransac_edge_cases(bt, torch, ctx):
+    sc = _custom_scene([0, 1, 2, 3, 4, 64, 200], seed=3)
+    # collinear frame: all points on a line -> every hypothesis degenerate
+    sc.pts[5, :64] = np.outer(np.arange(64) * 0.003, [1, 0.5, 0.2]) + [0, 0, 0.6]
+    ms = [np.stack([np.arange(n), np.arange(n)], 1).astype(np.int32) for n in (0, 1, 2, 3, 4, 64, 200)]
+    pairs = [(0, 0), (1, 1), (2, 2), (3, 3), (4, 4), (5, 5), (6, 6)]
+    rec, cnt = gpu_ransac(bt, torch, ctx, sc, pairs, ms, 300)
+    for p, (a, b) in enumerate(pairs):
+        pa, na, pb, nb = _pair_arrays(sc, a, b, ms[p])
+        oc = oracle.ransac_counts(pa, na, pb, nb, 300, p, SEED)
+        r = {k: v[p] for k, v in rec.items()}
+        parity.compare_ransac(cnt[p], r, oc, pa, na, pb, nb, what=f"edge {p}")
+    assert list(rec["status"][:3]) == [1, 1, 1]
+    assert rec["status"][5] == 2 and (cnt[5] == -1).all()
+    assert rec["best_count"][6] == 200                  # identical frames: everything inlier
+
+
+def test_ransac_chunked_large_M(bt, torch, ctx):
+    """n_max = 4096 (C5 size): M > 1024 correspondences stream through shared memory."""
+    rng = np.random.default_rng(5)
+    M = 3000
+    pa, na, pb, nb, R, t, inl = synth.make_correspondences(rng, M, 0.45, noise=0.0005)
+    sc = _custom_scene([M, M], n_max=4096, seed=5)
+    sc.pts[0, :M], sc.nrm[0, :M], sc.pts[1, :M], sc.nrm[1, :M] = pa, na, pb, nb
+    m = np.stack([np.arange(M), np.arange(M)], 1).astype(np.int32)
+    rec, cnt = gpu_ransac(bt, torch, ctx, sc, [(0, 1)], [m], 2048)
+    oc = oracle.ransac_counts(pa, na, pb, nb, 2048, 0, SEED)
+    r = {k: v[0] for k, v in rec.items()}
+    parity.compare_ransac(cnt[0], r, oc, pa, na, pb, nb, what="M=3000")
+
+
+# --------------------------------------------------------------------------------- dense
+def gpu_dense(bt, torch, ctx, scene, poses, edges, stride=1, gate=0.02):
+    fb = bt.FrameBatch.from_scene(scene)
+    E = len(edges)
+    out = torch.zeros((E, 32), dtype=torch.float32, device="cuda")
+    ctx.dense_corr(fb, scene.K, _dev(torch, poses), _dev(torch, np.asarray(edges, np.int32)),
+                   bt.edge_params(dist_gate_m=gate, stride=stride), out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("variant", ["gt", "perturbed", "stride2", "gate5mm"])
+def test_dense_parity_c2(bt, torch, ctx, c2, variant):
+    poses = c2.node_poses() if variant in ("gt", "stride2") else c2.perturbed_poses(3)
+    stride = 2 if variant == "stride2" else 1
+    gate = 0.005 if variant == "gate5mm" else 0.02
+    edges = [(0, 1), (1, 0), (0, 7), (5, 2), (15, 3), (9, 9), (4, 12), (12, 4)]
+    got = gpu_dense(bt, torch, ctx, c2, poses, edges, stride, gate)
+    for e, (i, j) in enumerate(edges):
+        o = oracle.dense_edge(c2.depth[i], c2.normal[i], c2.mask[i], c2.depth[j], c2.normal[j], c2.mask[j],
+                              c2.K, poses[i], poses[j], dist_gate=gate, stride=stride)
+        parity.assert_dense_close(got[e], o, f"edge {i}->{j}")
+        assert o[28] > 1000
+
+
+def test_dense_parity_c1_crop(bt, torch, ctx):
+    sc, *_ = synth.make_pair_c1()
+    poses = sc.node_poses()
+    got = gpu_dense(bt, torch, ctx, sc, poses, [(0, 1), (1, 0)])
+    for e, (i, j) in enumerate([(0, 1), (1, 0)]):
+        o = oracle.dense_edge(sc.depth[i], sc.normal[i], sc.mask[i], sc.depth[j], sc.normal[j], sc.mask[j],
+                              sc.K, poses[i], poses[j])
+        parity.assert_dense_close(got[e], o, f"c1 {i}->{j}")
+
+
+# ------------------------------------------------------------------- whole path (C2 size)
+def gpu_register(bt, torch, ctx, scene, pairs, uids, poses, n_hyp, host=False, dense=True):
+    n_max = scene.desc.shape[1]
+    rw = bt.record_words(n_max)
+    P = len(pairs)
+    if host:
+        fb = bt.FrameBatch.from_scene(scene, device="cpu", pin=True)
+        rec = torch.zeros((P, rw), dtype=torch.int32).pin_memory()
+        pr = torch.from_numpy(np.asarray(pairs, np.int32)).pin_memory()
+        ud = torch.from_numpy(np.asarray(uids, np.uint32).view(np.int32)).pin_memory()
+        ps = torch.from_numpy(poses).pin_memory()
+    else:
+        fb = bt.FrameBatch.from_scene(scene)
+        rec = torch.zeros((P, rw), dtype=torch.int32, device="cuda")
+        pr = _dev(torch, np.asarray(pairs, np.int32))
+        ud = _dev(torch, np.asarray(uids, np.uint32).view(np.int32))
+        ps = _dev(torch, poses)
+    ctx.register_pairs(fb, scene.K, ps, pr, ud, bt.ransac_params(n_hyp, SEED),
+                       bt.edge_params() if dense else None, rec, host=host)
+    torch.cuda.synchronize()
+    return rec.cpu().numpy()
+
+
+def test_register_pairs_c2_full_size_sampled(bt, torch, ctx, c2):
+    """BASELINE configs[1] at full size in the bench's launch configuration (120 pairs, 4096
+    hypotheses, 640x480, K = 15); records of sampled pairs checked against the oracle."""
+    pairs = synth.all_pairs(16)
+    uids = np.arange(len(pairs), dtype=np.uint32)
+    poses = c2.perturbed_poses(11)
+    raw = gpu_register(bt, torch, ctx, c2, pairs, uids, poses, 4096)
+    rec = bt.decode_records(raw, c2.desc.shape[1])
+    assert (rec["status"] == 0).all()
+    for p in (0, 17, 64, 119):
+        a, b = pairs[p]
+        o = oracle.register_pair(c2, a, b, int(uids[p]), 4096, SEED, node_poses=poses, dense=DENSE,
+                                 counts_out=True)
+        assert rec["n_matches"][p] == o["n_matches"]
+        parity.compare_matches(o["match"]["pairs"], o["match"])
+        r = {k: v[p] for k, v in rec.items()}
+        P_ = o["match"]["pairs"]
+        pa, na, pb, nb = _pair_arrays(c2, a, b, P_)
+        fin = parity.compare_ransac(None, r, o["counts"], pa, na, pb, nb, what=f"pair {p}")
+        if fin is not None and np.array_equal(parity.mask_bits(r["mask"], len(P_)),
+                                              parity.mask_bits(o["mask"], len(P_))):
+            parity.assert_feat_close(r["feat"], o["feat"], f"pair {p} feat")
+        parity.assert_dense_close(r["dense_ij"], o["dense_ij"], f"pair {p} ij")
+        parity.assert_dense_close(r["dense_ji"], o["dense_ji"], f"pair {p} ji")
+    # determinism: bitwise identical on a second run and under a different batching
+    raw2 = gpu_register(bt, torch, ctx, c2, pairs, uids, poses, 4096)
+    assert np.array_equal(raw, raw2)
+    half = gpu_register(bt, torch, ctx, c2, pairs[60:], uids[60:], poses, 4096)
+    assert np.array_equal(raw[60:], half)
+
+
+def test_register_pairs_host_buffers_equal_device(bt, torch, ctx):
+    sc = synth.make_scene(5, seed=99)
+    pairs = synth.all_pairs(5)
+    uids = np.arange(100, 100 + len(pairs), dtype=np.uint32)
+    poses = sc.node_poses()
+    d = gpu_register(bt, torch, ctx, sc, pairs, uids, poses, 1024)
+    h = gpu_register(bt, torch, ctx, sc, pairs, uids, poses, 1024, host=True)
+    assert np.array_equal(d, h)
+
+
+def test_register_pairs_without_dense_leaves_dense_words(bt, torch, ctx):
+    sc = synth.make_scene(3, seed=5)
+    pairs = synth.all_pairs(3)
+    raw = gpu_register(bt, torch, ctx, sc, pairs, np.arange(3), sc.node_poses(), 512, dense=False)
+    rec = bt.decode_records(raw, 512)
+    assert (rec["dense_ij"] == 0).all() and (rec["feat"] == 0).all()
+
+
+def test_compose_poses(bt, torch, ctx):
+    rng = np.random.default_rng(0)
+    A = np.stack([synth.pose12(synth.random_rotation(rng, 3.0), rng.normal(size=3)) for _ in range(50)])
+    B = np.stack([synth.pose12(synth.random_rotation(rng, 3.0), rng.normal(size=3)) for _ in range(50)])
+    out = torch.zeros((50, 12), dtype=torch.float32, device="cuda")
+    ctx.compose_poses(_dev(torch, A), _dev(torch, B), out)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    for k in range(50):
+        Ra, ta = A[k, :9].reshape(3, 3).astype(float), A[k, 9:].astype(float)
+        Rb, tb = B[k, :9].reshape(3, 3).astype(float), B[k, 9:].astype(float)
+        assert np.allclose(o[k, :9].reshape(3, 3), Ra @ Rb, atol=1e-6)
+        assert np.allclose(o[k, 9:], Ra @ tb + ta, atol=1e-6)
+
+
+def test_error_statuses(bt, torch):
+    c = bt.Context(0)
+    c.reserve(2, 512, 256)
+    sc = _custom_scene([10, 10])
+    fb = bt.FrameBatch.from_scene(sc)
+    pr = _dev(torch, np.zeros((3, 2), np.int32))
+    mt = torch.zeros((3, 512, 2), dtype=torch.int32, device="cuda")
+    nm = torch.zeros(3, dtype=torch.int32, device="cuda")
+    with pytest.raises(bt.BtError) as e:
+        c.match(fb, pr, mt, nm)                          # P = 3 > reserved 2
+    assert e.value.status == bt.BT_ECAPACITY
+    rec = torch.zeros((2, bt.record_words(512)), dtype=torch.int32, device="cuda")
+    with pytest.raises(bt.BtError) as e:
+        c.ransac(fb, pr[:2], nm[:2], mt[:2], nm[:2], bt.ransac_params(1024, 1), rec)   # n_hyp > 256
+    assert e.value.status == bt.BT_ECAPACITY
+    fb.desc = fb.desc[:, :, :64].contiguous()
+    with pytest.raises(bt.BtError) as e:
+        c.match(fb, pr[:2], mt[:2], nm[:2])
+    assert e.value.status == bt.BT_EUNSUPPORTED
+    c.close()
