@@ -258,26 +258,29 @@ def main():
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     npx = W * H
-    n_valid = float(sum(int(sc.mask[f].sum()) for f in range(N_FRAMES)))
     kern = {}
 
-    def add(name, bound, work, unit, peak):
+    def add(name, bound, work_per_step, unit, peak, note):
         tot, n = prof.get(name, (0.0, 0))
         if n == 0:
             return
-        avg_ms = tot / n
-        per_launch = work / (n / args.steps) if n else work
-        ach = per_launch / (avg_ms / 1e3) / (1e12 if unit == "TFLOP/s" else 1e9)
+        step_ms = tot / args.steps                      # this kernel's device time per step
+        ach = work_per_step / (step_ms / 1e3) / (1e12 if unit == "TFLOP/s" else 1e9)
         kern[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                      "avg_launch_ms": avg_ms, "launches_per_step": n / args.steps,
-                      "share_of_step": tot / ms if ms else None}
+                      "avg_launch_ms": tot / n, "launches_per_step": n / args.steps,
+                      "share_of_step": tot / ms if ms else None, "work": note}
     pair_sizes = float(sum(int(sc.n_kp[a]) * int(sc.n_kp[b]) for a, b in pairs))
-    add("k_nearest", "alu", 2 * pair_sizes * 128 * 3, "TFLOP/s", fp32_peak_tflops)
-    add("k_ransac_score", "alu", tests * FLOPS_PER_TEST, "TFLOP/s", fp32_peak_tflops)
-    # dense: bytes that must be read: source mask of every pixel, depth+normal of valid source
-    # pixels (edges of one source share nothing in this kernel), target gathers of associated px
-    dense_bytes = 2 * P * npx * 1 + 2 * P * (n_valid / N_FRAMES) * 16 + n_assoc * 17
-    add("k_dense", "hbm", dense_bytes, "GB/s", hbm_peak)
+    add("k_nearest", "alu", 2 * pair_sizes * 128 * 3, "TFLOP/s", fp32_peak_tflops,
+        "3 flop per (i, j, k) per direction, both directions")
+    add("k_ransac_score", "alu", tests * FLOPS_PER_TEST, "TFLOP/s", fp32_peak_tflops,
+        f"{FLOPS_PER_TEST} flop per (hypothesis, correspondence) test")
+    valid_per_frame = np.array([float(((sc.mask[f] > 0) & (sc.depth[f] > 0)).sum()) for f in range(N_FRAMES)])
+    src_px_edges = float(sum(valid_per_frame[a] + valid_per_frame[b] for a, b in pairs))
+    add("k_dense", "alu", 30 * src_px_edges + 160 * n_assoc, "TFLOP/s", fp32_peak_tflops,
+        "30 flop per (valid source pixel, edge) + 160 flop per associated (pixel, edge)")
+    # prep: must-read bytes = every mask byte + depth & normal of valid pixels; writes 32 B per entry
+    add("k_dense_prep", "hbm", N_FRAMES * npx * 1 + valid_per_frame.sum() * (16 + 32), "GB/s", hbm_peak,
+        "mask of every pixel + depth/normal of valid pixels + 32-B entry per valid pixel")
     dom = max(kern, key=lambda k: kern[k]["share_of_step"] or 0) if kern else None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")

@@ -24,12 +24,12 @@ struct bt_ctx {
   int64_t prof_n[bt::K_COUNT] = {0};
   // capacity
   int cap_pairs = 0, cap_nmax = 0, cap_hyp = 0, cap_frames = 0, cap_w = 0, cap_h = 0;
-  int cap_partials = 0;                       // dense partials per edge
+  size_t cap_dense = 0;                       // bytes of dense scratch
   // scratch
   int32_t *nn_ab = nullptr, *nn_ba = nullptr, *matches = nullptr, *n_matches = nullptr;
   uint8_t *ratio_ok = nullptr;
   unsigned long long *best_key = nullptr;
-  float *partials = nullptr;
+  void *dense = nullptr;
   // staging for bt_register_pairs_host
   int32_t *st_nkp = nullptr, *st_pairs = nullptr;
   uint32_t *st_uid = nullptr, *st_records = nullptr;
@@ -61,7 +61,7 @@ void free_dev(T *&p) {
 
 void free_scratch(bt_ctx *c) {
   free_dev(c->nn_ab); free_dev(c->nn_ba); free_dev(c->matches); free_dev(c->n_matches);
-  free_dev(c->ratio_ok); free_dev(c->best_key); free_dev(c->partials);
+  free_dev(c->ratio_ok); free_dev(c->best_key); free_dev(c->dense);
   free_dev(c->st_nkp); free_dev(c->st_pairs); free_dev(c->st_uid); free_dev(c->st_records);
   free_dev(c->st_desc); free_dev(c->st_pts); free_dev(c->st_nrm); free_dev(c->st_depth);
   free_dev(c->st_normal); free_dev(c->st_mask); free_dev(c->st_pose);
@@ -99,8 +99,9 @@ bt_status check_maps(bt_ctx *c, const bt_maps *mp, const bt_intrinsics *K) {
   if (mp->width != K->width || mp->height != K->height)
     return fail(c, BT_EINVAL, "maps %dx%d != intrinsics %dx%d", mp->width, mp->height, K->width, K->height);
   if (mp->width < 1 || mp->height < 1 || mp->n_frames < 1) return fail(c, BT_EINVAL, "maps: empty");
-  if (bt::dense_partials_per_edge(mp->width, mp->height) > c->cap_partials)
-    return fail(c, BT_ECAPACITY, "maps %dx%d larger than reserved %dx%d", mp->width, mp->height, c->cap_w, c->cap_h);
+  if (mp->n_frames > c->cap_frames || (size_t)mp->width * mp->height > (size_t)c->cap_w * c->cap_h || !c->dense)
+    return fail(c, BT_ECAPACITY, "maps %d x %dx%d beyond reserved %d x %dx%d", mp->n_frames, mp->width, mp->height,
+                c->cap_frames, c->cap_w, c->cap_h);
   if (!mp->depth || !mp->normal || !mp->mask) return fail(c, BT_EINVAL, "maps: NULL buffer");
   if (!aligned16(mp->depth) || !aligned16(mp->normal) || !aligned16(mp->mask))
     return fail(c, BT_EINVAL, "maps: buffers must be 16-byte aligned");
@@ -182,15 +183,16 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
     return fail(c, BT_EINVAL, "bt_reserve: bad sizes");
   cudaDeviceSynchronize();
   free_scratch(c);
-  c->cap_pairs = c->cap_nmax = c->cap_hyp = c->cap_frames = c->cap_w = c->cap_h = c->cap_partials = 0;
+  c->cap_pairs = c->cap_nmax = c->cap_hyp = c->cap_frames = c->cap_w = c->cap_h = 0;
+  c->cap_dense = 0;
   const size_t PN = (size_t)max_pairs * n_max;
-  const int nparts = (width > 0 && height > 0) ? bt::dense_partials_per_edge(width, height) : 0;
+  const size_t dense_bytes = (width > 0 && height > 0 && max_frames > 0)
+                                 ? bt::dense_scratch_bytes(max_frames, 2 * max_pairs, width, height) : 0;
   bool ok = cudaMalloc(&c->nn_ab, PN * 4) == cudaSuccess && cudaMalloc(&c->nn_ba, PN * 4) == cudaSuccess &&
             cudaMalloc(&c->matches, PN * 8) == cudaSuccess && cudaMalloc(&c->n_matches, (size_t)max_pairs * 4) == cudaSuccess &&
             cudaMalloc(&c->ratio_ok, PN) == cudaSuccess &&
             cudaMalloc(&c->best_key, (size_t)max_pairs * 8) == cudaSuccess;
-  if (ok && nparts > 0)
-    ok = cudaMalloc(&c->partials, (size_t)2 * max_pairs * nparts * 32 * sizeof(float)) == cudaSuccess;
+  if (ok && dense_bytes > 0) ok = cudaMalloc(&c->dense, dense_bytes) == cudaSuccess;
   if (ok && max_frames > 0) {
     const size_t FN = (size_t)max_frames * n_max, FP = (size_t)max_frames * width * height;
     ok = cudaMalloc(&c->st_nkp, (size_t)max_frames * 4) == cudaSuccess &&
@@ -208,7 +210,7 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
     return fail(c, BT_ENOMEM, "bt_reserve: cudaMalloc failed");
   }
   c->cap_pairs = max_pairs; c->cap_nmax = n_max; c->cap_hyp = max_hyp; c->cap_frames = max_frames;
-  c->cap_w = width; c->cap_h = height; c->cap_partials = nparts;
+  c->cap_w = width; c->cap_h = height; c->cap_dense = dense_bytes;
   return BT_OK;
 }
 
@@ -253,8 +255,8 @@ bt_status bt_dense_corr(bt_ctx *c, const bt_maps *maps, const bt_intrinsics *K, 
   if (E > 2 * c->cap_pairs) return fail(c, BT_ECAPACITY, "E %d > 2 * reserved pairs %d", E, c->cap_pairs);
   if (E == 0) return BT_OK;
   if (!node_pose || !edges || !out) return fail(c, BT_EINVAL, "bt_dense_corr: NULL buffer");
-  bt::launch_dense(mview(maps), *K, node_pose, edges, nullptr, E, *prm, c->partials, c->cap_partials, out, 32,
-                   nullptr, 0, 0, 0, (cudaStream_t)stream, c->launch);
+  bt::launch_dense(mview(maps), *K, node_pose, edges, nullptr, E, *prm, c->dense, out, 32, nullptr, 0, 0, 0,
+                   (cudaStream_t)stream, c->launch);
   return after_launch(c, "bt_dense_corr");
 }
 
@@ -270,9 +272,8 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
   bt::launch_ransac(kview(kp), pairs, uid, P, c->matches, c->n_matches, *rprm, c->best_key, records, rw, nullptr,
                     eprm ? node_pose : nullptr, eprm ? eprm->huber_m : 0.f, st, c->launch);
   if (eprm)
-    bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->partials, c->cap_partials,
-                     nullptr, 0, records, rw, bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), st,
-                     c->launch);
+    bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, nullptr, 0, records, rw,
+                     bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), st, c->launch);
   return after_launch(c, "bt_register_pairs");
 }
 
@@ -360,8 +361,8 @@ bt_status bt_compose_poses(bt_ctx *c, const bt_pose *a, const bt_pose *b, bt_pos
 }
 
 static const char *kKernelNames[bt::K_COUNT] = {"k_nearest", "k_mutual", "k_ransac_score",
-                                                 "k_ransac_finish", "k_dense", "k_dense_reduce",
-                                                 "k_compose"};
+                                                 "k_ransac_finish", "k_dense_prep", "k_dense",
+                                                 "k_dense_reduce", "k_compose"};
 
 static cudaEvent_t take_event(bt_ctx *c) {
   if (c->ev_pool.empty()) {

@@ -5,11 +5,28 @@
 // normals".  Readings: nearest pixel (R14), gates (R15), normals compared in camera i (R16),
 // Huber (R17), J = [n_i^T, (q x n_i)^T] for the left perturbation of T_i (R18).
 //
-// k_dense: one CTA per (edge, span of 256 x kPix pixels): coalesced reads of the source
-// mask / depth / normal rows, the gathered target pixel, and 29 running fp32 sums per
-// thread (H 21, g 6, E, count) reduced by warp shuffles + shared memory into one partial
-// per CTA.  k_dense_reduce: fixed-order fp64 sum of the partials of an edge (bitwise
-// deterministic, no float atomics).
+// Factored formulation (the oracle's algebra, regrouped — no use of R^-1 = R^T, which does
+// not hold exactly for float32-rounded rotations):
+//   q - p = R_i R_j^T (s - t_j) + t_i - p = R_i x_s - (p - t_i),  x_s = R_j^T (s - t_j),
+//   r = n_i . (q - p),  |q - p|,  n_i . (R_i R_j^T n_j) = (R_i^T n_i) . (R_j^T n_j).
+// The residual cancels two ~0.5 m positions down to ~1e-5 m near the optimum, so x_s and
+// p - t_i are fp64 and x_s is computed ONCE per target pixel per call (not per edge); R_i is
+// a per-CTA constant.
+//
+//  k_edge_prep    one thread per edge: T_j T_i^-1 (fp32, for the projection); one CTA per
+//                 source frame builds that frame's ordered list of outgoing edges.
+//  k_dense_prep   one CTA per (frame, 32x32 tile): coalesced vector reads (uchar4 mask,
+//                 float4 depth, 3 x float4 normals) of 4 pixels per thread; per valid pixel the
+//                 fp64 object-frame point and fp32 object-frame normal go to a per-frame map
+//                 (gathered as a TARGET), a validity byte is written for every pixel, and a
+//                 block scan compacts the tile's valid source pixels (pixel order, stride
+//                 applied) into 32-byte entries.
+//  k_dense        one CTA per (frame, tile): entries + their fp64 points staged in shared
+//                 memory once and reused for every edge leaving the frame (source reuse).
+//                 Per (entry, edge): fp32 projection, gather of the target validity + map entry
+//                 (all of a thread's gathers issued together), fp64 gates / residual, Huber,
+//                 29 running sums; per edge a 31-shuffle warp transpose reduction + smem.
+//  k_dense_reduce fixed-order fp64 sum of the per-tile partials of an edge (deterministic).
 #include <cuda_runtime.h>
 
 #include "bt_internal.cuh"
@@ -17,10 +34,17 @@
 namespace bt {
 namespace {
 
+constexpr int kTS = 32;                       // tile side (pixels)
+constexpr int kTile = kTS * kTS;
 constexpr int kDenseThreads = 256;
-constexpr int kPix = 8;                       // pixels per thread
+constexpr int kPer = kTile / kDenseThreads;   // 4 pixels / entries per thread
 constexpr int kAcc = 29;                      // H 21, g 6, E, count
 constexpr int kPartStride = 32;
+
+struct MapEntry {                             // 48 bytes, per valid pixel of every frame
+  double x, y, z;                             // x = R^T (p - t), fp64
+  float nx, ny, nz, pad[3];                   // object-frame normal
+};
 
 struct DenseArgs {
   MapView mp;
@@ -29,167 +53,336 @@ struct DenseArgs {
   const bt_pose *node_pose;
   const int32_t *edges;       // [E][2] or null (then derived from pairs)
   const int32_t *pairs;
-  int E, stride;
-  float gate2, cos_gate, huber;
-  float *partials;            // [E][nblk][32]
-  int nblk;
+  int E, stride, tx, ty, tiles;
+  double gate2;
+  float cos_gate, huber;
+  float *tji;                 // [E][12] T_j T_i^-1
+  int32_t *elist;             // [F][E] outgoing edges per source frame, ascending
+  int32_t *ecount;            // [F]
+  float4 *entries;            // [F][tiles][kTile][2]
+  int32_t *counts;            // [F][tiles]
+  MapEntry *pmap;             // [F][H*W]
+  uint8_t *vmap;              // [F][H*W]
+  float *partials;            // [E][tiles][32]
 };
 
-__device__ __forceinline__ void edge_frames(const DenseArgs &A, int e, int &fi, int &fj) {
-  if (A.edges) { fi = A.edges[2 * e]; fj = A.edges[2 * e + 1]; }
+__device__ __forceinline__ void edge_frames(const int32_t *edges, const int32_t *pairs, int e, int &fi, int &fj) {
+  if (edges) { fi = edges[2 * e]; fj = edges[2 * e + 1]; }
   else {
     const int p = e >> 1;
-    fi = A.pairs[2 * p + (e & 1)];
-    fj = A.pairs[2 * p + 1 - (e & 1)];
+    fi = pairs[2 * p + (e & 1)];
+    fj = pairs[2 * p + 1 - (e & 1)];
   }
 }
 
-__global__ void __launch_bounds__(kDenseThreads) k_dense(DenseArgs A) {
-  __shared__ float C[24];                     // Rji(9) tji(3) Rij(9) tij(3)
-  __shared__ double Cd[12];                   // Rij(9) tij(3) in fp64 for the residual
-  __shared__ float red[kDenseThreads / 32][kAcc];
-  const int e = blockIdx.y;
+__global__ void k_edge_consts(DenseArgs A) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= A.E) return;
   int fi, fj;
-  edge_frames(A, e, fi, fj);
-  if (threadIdx.x == 0) {
-    // T_j T_i^-1: R = R_j R_i^T, t = t_j - R t_i ;  T_i T_j^-1: R = R_i R_j^T, t = t_i - R t_j
-    const bt_pose Pi = A.node_pose[fi], Pj = A.node_pose[fj];
-    double Rji[9], Rij[9];
-    for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) {
-        double x = 0, y = 0;
-        for (int k = 0; k < 3; ++k) {
-          x += (double)Pj.R[3 * r + k] * Pi.R[3 * c + k];
-          y += (double)Pi.R[3 * r + k] * Pj.R[3 * c + k];
-        }
-        Rji[3 * r + c] = x;
-        Rij[3 * r + c] = y;
-      }
-    for (int k = 0; k < 9; ++k) { C[k] = (float)Rji[k]; C[12 + k] = (float)Rij[k]; Cd[k] = Rij[k]; }
-    for (int r = 0; r < 3; ++r) {
-      C[9 + r] = (float)(Pj.t[r] - (Rji[3 * r] * Pi.t[0] + Rji[3 * r + 1] * Pi.t[1] + Rji[3 * r + 2] * Pi.t[2]));
-      Cd[9 + r] = Pi.t[r] - (Rij[3 * r] * Pj.t[0] + Rij[3 * r + 1] * Pj.t[1] + Rij[3 * r + 2] * Pj.t[2]);
-      C[21 + r] = (float)Cd[9 + r];
+  edge_frames(A.edges, A.pairs, e, fi, fj);
+  // T_j T_i^-1: R = R_j R_i^T, t = t_j - R t_i
+  const bt_pose Pi = A.node_pose[fi], Pj = A.node_pose[fj];
+  double R[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      double x = 0;
+      for (int k = 0; k < 3; ++k) x += (double)Pj.R[3 * r + k] * Pi.R[3 * c + k];
+      R[3 * r + c] = x;
     }
-  }
-  __syncthreads();
-  float Rji[9], tji[3], Rij[9], tij[3];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) { Rji[k] = C[k]; Rij[k] = C[12 + k]; }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) { tji[k] = C[9 + k]; tij[k] = C[21 + k]; }
+  float *o = A.tji + 12 * e;
+  for (int k = 0; k < 9; ++k) o[k] = (float)R[k];
+  for (int r = 0; r < 3; ++r)
+    o[9 + r] = (float)(Pj.t[r] - (R[3 * r] * Pi.t[0] + R[3 * r + 1] * Pi.t[1] + R[3 * r + 2] * Pi.t[2]));
+}
 
-  const int W = A.mp.W, H = A.mp.H, npx = W * H;
-  const size_t off_i = (size_t)fi * npx, off_j = (size_t)fj * npx;
-  const float *dep_i = A.mp.depth + off_i, *dep_j = A.mp.depth + off_j;
-  const float *nor_i = A.mp.normal + 3 * off_i, *nor_j = A.mp.normal + 3 * off_j;
-  const uint8_t *msk_i = A.mp.mask + off_i, *msk_j = A.mp.mask + off_j;
-
-  float acc[kAcc];
-#pragma unroll
-  for (int k = 0; k < kAcc; ++k) acc[k] = 0.f;
-  const int base = blockIdx.x * kDenseThreads * kPix;
-#pragma unroll 1
-  for (int it = 0; it < kPix; ++it) {
-    const int pix = base + it * kDenseThreads + threadIdx.x;
-    if (pix >= npx) break;
-    const int v = pix / W, u = pix - v * W;
-    if (A.stride > 1 && (u % A.stride || v % A.stride)) continue;
-    if (!msk_i[pix]) continue;
-    const float d = dep_i[pix];
-    const float n0 = nor_i[3 * pix], n1 = nor_i[3 * pix + 1], n2 = nor_i[3 * pix + 2];
-    if (!(d > 0.f) || (n0 == 0.f && n1 == 0.f && n2 == 0.f)) continue;
-    // p = pi^-1(x, d)
-    const float px = ((float)u - A.cx) * d * A.ifx, py = ((float)v - A.cy) * d * A.ify, pz = d;
-    // y = T_j T_i^-1 p
-    const float yx = fmaf(Rji[0], px, fmaf(Rji[1], py, fmaf(Rji[2], pz, tji[0])));
-    const float yy = fmaf(Rji[3], px, fmaf(Rji[4], py, fmaf(Rji[5], pz, tji[1])));
-    const float yz = fmaf(Rji[6], px, fmaf(Rji[7], py, fmaf(Rji[8], pz, tji[2])));
-    if (!(yz > 0.f)) continue;
-    const float iz = 1.0f / yz;
-    const float up = fmaf(A.fx * yx, iz, A.cx), vp = fmaf(A.fy * yy, iz, A.cy);
-    const float xu = floorf(up + 0.5f), xv = floorf(vp + 0.5f);
-    if (!(xu >= 0.f && xu < (float)W && xv >= 0.f && xv < (float)H)) continue;
-    const int uj = (int)xu, vj = (int)xv, pj = vj * W + uj;
-    if (!msk_j[pj]) continue;
-    const float dj = dep_j[pj];
-    const float m0 = nor_j[3 * pj], m1 = nor_j[3 * pj + 1], m2 = nor_j[3 * pj + 2];
-    if (!(dj > 0.f) || (m0 == 0.f && m1 == 0.f && m2 == 0.f)) continue;
-    // s = pi_D^-1(x'), q = T_i T_j^-1 s, n_j in camera i
-    const float sx = ((float)uj - A.cx) * dj * A.ifx, sy = ((float)vj - A.cy) * dj * A.ify, sz = dj;
-    const float qx = fmaf(Rij[0], sx, fmaf(Rij[1], sy, fmaf(Rij[2], sz, tij[0])));
-    const float qy = fmaf(Rij[3], sx, fmaf(Rij[4], sy, fmaf(Rij[5], sz, tij[1])));
-    const float qz = fmaf(Rij[6], sx, fmaf(Rij[7], sy, fmaf(Rij[8], sz, tij[2])));
-    const float k0 = fmaf(Rij[0], m0, fmaf(Rij[1], m1, Rij[2] * m2));
-    const float k1 = fmaf(Rij[3], m0, fmaf(Rij[4], m1, Rij[5] * m2));
-    const float k2 = fmaf(Rij[6], m0, fmaf(Rij[7], m1, Rij[8] * m2));
-    const float dx = qx - px, dy = qy - py, dz = qz - pz;
-    const float dist2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    const float c = fmaf(n0, k0, fmaf(n1, k1, n2 * k2));
-    if (!(dist2 < A.gate2 && c > A.cos_gate)) continue;
-    // the point-to-plane residual cancels two ~0.5 m positions down to ~1e-5 m near the
-    // optimum: evaluate it in fp64 (B200 FP64 runs at half the FP32 rate)
-    double r_d;
-    {
-      const double pxd = ((double)u - A.cxd) * (double)d * A.ifxd, pyd = ((double)v - A.cyd) * (double)d * A.ifyd;
-      const double sxd = ((double)uj - A.cxd) * (double)dj * A.ifxd, syd = ((double)vj - A.cyd) * (double)dj * A.ifyd;
-      const double szd = dj;
-      const double qxd = fma(Cd[0], sxd, fma(Cd[1], syd, fma(Cd[2], szd, Cd[9])));
-      const double qyd = fma(Cd[3], sxd, fma(Cd[4], syd, fma(Cd[5], szd, Cd[10])));
-      const double qzd = fma(Cd[6], sxd, fma(Cd[7], syd, fma(Cd[8], szd, Cd[11])));
-      r_d = fma((double)n0, qxd - pxd, fma((double)n1, qyd - pyd, (double)n2 * (qzd - (double)d)));
-    }
-    const float r = (float)r_d;
-    const float ar = fabsf(r);
-    const float w = ar <= A.huber ? 1.f : A.huber / ar;
-    const float rho = ar <= A.huber ? 0.5f * r * r : A.huber * (ar - 0.5f * A.huber);
-    const float J[6] = {n0, n1, n2, qy * n2 - qz * n1, qz * n0 - qx * n2, qx * n1 - qy * n0};
-    int k = 0;
-#pragma unroll
-    for (int a = 0; a < 6; ++a) {
-      const float wa = w * J[a];
-#pragma unroll
-      for (int b = a; b < 6; ++b) { acc[k] = fmaf(wa, J[b], acc[k]); ++k; }
-    }
-#pragma unroll
-    for (int a = 0; a < 6; ++a) acc[21 + a] = fmaf(w * J[a], r, acc[21 + a]);
-    acc[27] += rho;
-    acc[28] += 1.f;
-  }
-  // block reduction (fixed order)
+// per source frame: the ascending list of edges leaving it (deterministic ballot compaction)
+__global__ void k_edge_lists(DenseArgs A) {
+  __shared__ int wsum[8];
+  const int f = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int base = 0;
+  for (int e0 = 0; e0 < A.E; e0 += 256) {
+    const int e = e0 + threadIdx.x;
+    bool mine = false;
+    if (e < A.E) {
+      int fi, fj;
+      edge_frames(A.edges, A.pairs, e, fi, fj);
+      mine = fi == f;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, mine);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < 8; ++w) { off += w < warp ? wsum[w] : 0; tot += wsum[w]; }
+    if (mine) A.elist[(size_t)f * A.E + base + off + __popc(bal & ((1u << lane) - 1u))] = e;
+    base += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) A.ecount[f] = base;
+}
+
+__global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
+  __shared__ int wsum[kDenseThreads / 32];
+  const int f = blockIdx.y, t = blockIdx.x;
+  const int W = A.mp.W, H = A.mp.H, npx = W * H;
+  const int ty = t / A.tx, tx = t - ty * A.tx;
+  const int row = threadIdx.x >> 3, col0 = (threadIdx.x & 7) * 4;
+  const int v = ty * kTS + row, u0 = tx * kTS + col0;
+  const size_t off = (size_t)f * npx;
+  const int pix0 = v * W + u0;
+  bool in[kPer];
+  float dep[kPer], nr[kPer * 3];
 #pragma unroll
-  for (int k = 0; k < kAcc; ++k) {
-    float x = acc[k];
+  for (int k = 0; k < kPer; ++k) { in[k] = false; dep[k] = 0.f; nr[3 * k] = nr[3 * k + 1] = nr[3 * k + 2] = 0.f; }
+  if (v < H) {
+    if ((W & 3) == 0 && u0 + kPer <= W) {
+      const uchar4 m4 = *reinterpret_cast<const uchar4 *>(A.mp.mask + off + pix0);
+      if (m4.x | m4.y | m4.z | m4.w) {
+        const float4 d4 = *reinterpret_cast<const float4 *>(A.mp.depth + off + pix0);
+        const float4 *n4 = reinterpret_cast<const float4 *>(A.mp.normal + 3 * (off + pix0));
+        const float4 a = n4[0], b = n4[1], c = n4[2];
+        dep[0] = d4.x; dep[1] = d4.y; dep[2] = d4.z; dep[3] = d4.w;
+        nr[0] = a.x; nr[1] = a.y; nr[2] = a.z; nr[3] = a.w; nr[4] = b.x; nr[5] = b.y;
+        nr[6] = b.z; nr[7] = b.w; nr[8] = c.x; nr[9] = c.y; nr[10] = c.z; nr[11] = c.w;
+        in[0] = m4.x != 0; in[1] = m4.y != 0; in[2] = m4.z != 0; in[3] = m4.w != 0;
+      }
+    } else {
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) red[warp][k] = x;
+      for (int k = 0; k < kPer; ++k) {
+        const int u = u0 + k;
+        if (u < W && A.mp.mask[off + pix0 + k]) {
+          in[k] = true;
+          dep[k] = A.mp.depth[off + pix0 + k];
+          for (int c = 0; c < 3; ++c) nr[3 * k + c] = A.mp.normal[3 * (off + pix0 + k) + c];
+        }
+      }
+    }
+  }
+  const bt_pose P = A.node_pose[f];
+  bool src[kPer];
+  int n_mine = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int u = u0 + k;
+    const bool valid = in[k] && dep[k] > 0.f && !(nr[3 * k] == 0.f && nr[3 * k + 1] == 0.f && nr[3 * k + 2] == 0.f);
+    if (v < H && u < W) A.vmap[off + pix0 + k] = valid ? 1 : 0;
+    if (valid) {
+      // x = R^T (p - t) in fp64 from the exact inputs; n_o = R^T n
+      const double d = dep[k];
+      const double p0 = ((double)u - A.cxd) * d * A.ifxd - P.t[0];
+      const double p1 = ((double)v - A.cyd) * d * A.ifyd - P.t[1];
+      const double p2 = d - P.t[2];
+      MapEntry me;
+      me.x = P.R[0] * p0 + P.R[3] * p1 + P.R[6] * p2;
+      me.y = P.R[1] * p0 + P.R[4] * p1 + P.R[7] * p2;
+      me.z = P.R[2] * p0 + P.R[5] * p1 + P.R[8] * p2;
+      const double m0 = nr[3 * k], m1 = nr[3 * k + 1], m2 = nr[3 * k + 2];
+      me.nx = (float)(P.R[0] * m0 + P.R[3] * m1 + P.R[6] * m2);
+      me.ny = (float)(P.R[1] * m0 + P.R[4] * m1 + P.R[7] * m2);
+      me.nz = (float)(P.R[2] * m0 + P.R[5] * m1 + P.R[8] * m2);
+      me.pad[0] = me.pad[1] = me.pad[2] = 0.f;
+      A.pmap[off + pix0 + k] = me;
+    }
+    src[k] = valid && (A.stride <= 1 || (u % A.stride == 0 && v % A.stride == 0));
+    n_mine += src[k];
+  }
+  // block exclusive scan of n_mine (thread order = row-major pixel order within the tile)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = n_mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int woff = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kDenseThreads / 32; ++w) {
+    woff += w < warp ? wsum[w] : 0;
+    total += wsum[w];
+  }
+  int pos = woff + incl - n_mine;
+  float4 *out = A.entries + ((size_t)f * A.tiles + t) * kTile * 2;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    if (!src[k]) continue;
+    const int u = u0 + k;
+    const float d = dep[k];
+    out[2 * pos] = make_float4(((float)u - A.cx) * d * A.ifx, ((float)v - A.cy) * d * A.ify, d,
+                               __int_as_float(u | (v << 16)));
+    out[2 * pos + 1] = make_float4(nr[3 * k], nr[3 * k + 1], nr[3 * k + 2], 0.f);
+    ++pos;
+  }
+  if (threadIdx.x == 0) A.counts[(size_t)f * A.tiles + t] = total;
+}
+
+constexpr size_t kDenseSmem = kTile * (16 + 16 + 8 + 24) + (kDenseThreads / 32) * 32 * 4;
+
+__global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float4 *sP = reinterpret_cast<float4 *>(dsm);                    // p (camera, fp32), (u | v << 16)
+  float4 *sN = sP + kTile;                                         // n_i (camera), n_o,i.x
+  float2 *sNo = reinterpret_cast<float2 *>(sN + kTile);            // n_o,i.y, n_o,i.z
+  double *sX = reinterpret_cast<double *>(sNo + kTile);            // p - t_i (fp64)
+  float (*red)[32] = reinterpret_cast<float (*)[32]>(sX + 3 * kTile);
+  const int f = blockIdx.y, t = blockIdx.x;
+  const int n = A.counts[(size_t)f * A.tiles + t];
+  const int ne = A.ecount[f];
+  if (n == 0 || ne == 0) return;
+  const int W = A.mp.W, H = A.mp.H, npx = W * H;
+  double Rd[9];                                                    // R_i (fp64)
+  {
+    const bt_pose P = A.node_pose[f];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Rd[k] = P.R[k];
+    const double t0 = P.t[0], t1 = P.t[1], t2 = P.t[2];
+    const float4 *src = A.entries + ((size_t)f * A.tiles + t) * kTile * 2;
+    for (int k = threadIdx.x; k < n; k += kDenseThreads) {
+      const float4 a = src[2 * k], b = src[2 * k + 1];
+      const int uv = __float_as_int(a.w), u = uv & 0xffff, v = uv >> 16;
+      const double d = a.z;                                        // p.z = depth exactly
+      sX[3 * k] = ((double)u - A.cxd) * d * A.ifxd - t0;
+      sX[3 * k + 1] = ((double)v - A.cyd) * d * A.ifyd - t1;
+      sX[3 * k + 2] = d - t2;
+      const double m0 = b.x, m1 = b.y, m2 = b.z;                   // n_o,i = R_i^T n_i
+      const float o0 = (float)(Rd[0] * m0 + Rd[3] * m1 + Rd[6] * m2);
+      const float o1 = (float)(Rd[1] * m0 + Rd[4] * m1 + Rd[7] * m2);
+      const float o2 = (float)(Rd[2] * m0 + Rd[5] * m1 + Rd[8] * m2);
+      sP[k] = a;
+      sN[k] = make_float4(b.x, b.y, b.z, o0);
+      sNo[k] = make_float2(o1, o2);
+    }
   }
   __syncthreads();
-  if (threadIdx.x < kAcc) {
-    float t = 0.f;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (int ie = 0; ie < ne; ++ie) {
+    const int e = A.elist[(size_t)f * A.E + ie];
+    int fi, fj;
+    edge_frames(A.edges, A.pairs, e, fi, fj);
+    float T[12];
 #pragma unroll
-    for (int w = 0; w < kDenseThreads / 32; ++w) t += red[w][threadIdx.x];
-    A.partials[((size_t)e * A.nblk + blockIdx.x) * kPartStride + threadIdx.x] = t;
+    for (int k = 0; k < 12; ++k) T[k] = __ldg(A.tji + 12 * e + k);
+    const size_t off_j = (size_t)fj * npx;
+    const uint8_t *vm = A.vmap + off_j;
+    const float4 *pm = reinterpret_cast<const float4 *>(A.pmap + off_j);
+    float acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc[k] = 0.f;
+#pragma unroll
+    for (int half = 0; half < kPer; half += 2) {
+      // phase 1: project two entries; phase 2: issue their gathers together; phase 3: compute
+      int tj[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int k = threadIdx.x + (half + s) * kDenseThreads;
+        tj[s] = -1;
+        if (k < n) {
+          const float4 a = sP[k];
+          const float yx = fmaf(T[0], a.x, fmaf(T[1], a.y, fmaf(T[2], a.z, T[9])));
+          const float yy = fmaf(T[3], a.x, fmaf(T[4], a.y, fmaf(T[5], a.z, T[10])));
+          const float yz = fmaf(T[6], a.x, fmaf(T[7], a.y, fmaf(T[8], a.z, T[11])));
+          if (yz > 0.f) {
+            const float iz = __fdividef(1.0f, yz);
+            const float up = fmaf(A.fx * yx, iz, A.cx), vp = fmaf(A.fy * yy, iz, A.cy);
+            const float xu = floorf(up + 0.5f), xv = floorf(vp + 0.5f);
+            if (xu >= 0.f && xu < (float)W && xv >= 0.f && xv < (float)H) tj[s] = (int)xv * W + (int)xu;
+          }
+        }
+      }
+      bool gv[2];
+      float4 g0[2], g1[2], g2[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        gv[s] = tj[s] >= 0 && __ldg(vm + tj[s]) != 0;
+        if (gv[s]) {
+          const float4 *q4 = pm + 3 * (size_t)tj[s];
+          g0[s] = __ldg(q4);
+          g1[s] = __ldg(q4 + 1);
+          g2[s] = __ldg(q4 + 2);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (!gv[s]) continue;
+        const int k = threadIdx.x + (half + s) * kDenseThreads;
+        // target map entry: x_s = R_j^T (s - t_j) (fp64), n_o,j (fp32)
+        const double xs0 = __hiloint2double(__float_as_int(g0[s].y), __float_as_int(g0[s].x));
+        const double xs1 = __hiloint2double(__float_as_int(g0[s].w), __float_as_int(g0[s].z));
+        const double xs2 = __hiloint2double(__float_as_int(g1[s].y), __float_as_int(g1[s].x));
+        const float mj0 = g1[s].z, mj1 = g1[s].w, mj2 = g2[s].x;
+        // q - p = R_i x_s - (p - t_i)
+        const double dq0 = fma(Rd[0], xs0, fma(Rd[1], xs1, Rd[2] * xs2)) - sX[3 * k];
+        const double dq1 = fma(Rd[3], xs0, fma(Rd[4], xs1, Rd[5] * xs2)) - sX[3 * k + 1];
+        const double dq2 = fma(Rd[6], xs0, fma(Rd[7], xs1, Rd[8] * xs2)) - sX[3 * k + 2];
+        const double dist2 = fma(dq0, dq0, fma(dq1, dq1, dq2 * dq2));
+        const float4 nc = sN[k];
+        const float2 no = sNo[k];
+        const float c = fmaf(nc.w, mj0, fmaf(no.x, mj1, no.y * mj2));
+        if (!(dist2 < A.gate2 && c > A.cos_gate)) continue;
+        const float n0 = nc.x, n1 = nc.y, n2 = nc.z;
+        const float r = (float)fma((double)n0, dq0, fma((double)n1, dq1, (double)n2 * dq2));
+        const float4 a = sP[k];
+        const float qx = a.x + (float)dq0, qy = a.y + (float)dq1, qz = a.z + (float)dq2;
+        const float ar = fabsf(r);
+        const float w = ar <= A.huber ? 1.f : __fdividef(A.huber, ar);
+        const float rho = ar <= A.huber ? 0.5f * r * r : A.huber * (ar - 0.5f * A.huber);
+        const float J[6] = {n0, n1, n2, qy * n2 - qz * n1, qz * n0 - qx * n2, qx * n1 - qy * n0};
+        int q = 0;
+#pragma unroll
+        for (int aa = 0; aa < 6; ++aa) {
+          const float wa = w * J[aa];
+#pragma unroll
+          for (int b = aa; b < 6; ++b) { acc[q] = fmaf(wa, J[b], acc[q]); ++q; }
+        }
+#pragma unroll
+        for (int aa = 0; aa < 6; ++aa) acc[21 + aa] = fmaf(w * J[aa], r, acc[21 + aa]);
+        acc[27] += rho;
+        acc[28] += 1.f;
+      }
+    }
+    // warp transpose reduction: lane l ends with the warp total of acc[l]
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const bool upper = (lane & o) != 0;
+#pragma unroll
+      for (int c = 0; c < o; ++c) {
+        const float send = upper ? acc[c] : acc[c + o];
+        const float keep = upper ? acc[c + o] : acc[c];
+        acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    red[warp][lane] = acc[0];
+    __syncthreads();
+    if (warp == 0) {
+      float s = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < kDenseThreads / 32; ++w2) s += red[w2][lane];
+      A.partials[((size_t)e * A.tiles + t) * kPartStride + lane] = s;
+    }
+    __syncthreads();
   }
 }
 
-__global__ void k_dense_reduce(const float *__restrict__ partials, int nblk, int E, const int32_t *edges,
-                               float *out, int out_stride, uint32_t *records, int rec_stride,
-                               int off_ij, int off_ji) {
+__global__ void k_dense_reduce(const float *__restrict__ partials, const int32_t *__restrict__ counts, int tiles,
+                               const int32_t *edges, const int32_t *pairs, float *out, int out_stride,
+                               uint32_t *records, int rec_stride, int off_ij, int off_ji) {
   const int e = blockIdx.x;
   const int k = threadIdx.x;                  // 32 threads
-  double t = 0.0;
+  int fi, fj;
+  edge_frames(edges, pairs, e, fi, fj);
+  double s = 0.0;
   if (k < kAcc)
-    for (int b = 0; b < nblk; ++b) t += (double)partials[((size_t)e * nblk + b) * kPartStride + k];
-  const float v = k < kAcc ? (float)t : 0.f;
+    for (int t = 0; t < tiles; ++t)
+      if (counts[(size_t)fi * tiles + t] > 0) s += (double)partials[((size_t)e * tiles + t) * kPartStride + k];
+  const float v = k < kAcc ? (float)s : 0.f;
   if (records) {
     const int p = e >> 1;
     records[(size_t)p * rec_stride + ((e & 1) ? off_ji : off_ij) + k] = __float_as_uint(v);
   } else {
     out[(size_t)e * out_stride + k] = v;
   }
-  (void)E; (void)edges;
 }
 
 __global__ void k_compose(const bt_pose *a, const bt_pose *b, bt_pose *out, int n) {
@@ -209,16 +402,22 @@ __global__ void k_compose(const bt_pose *a, const bt_pose *b, bt_pose *out, int 
   out[i] = O;
 }
 
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
 }  // namespace
 
-int dense_partials_per_edge(int W, int H) {
-  return (W * H + kDenseThreads * kPix - 1) / (kDenseThreads * kPix);
+int dense_tiles(int W, int H) { return ((W + kTS - 1) / kTS) * ((H + kTS - 1) / kTS); }
+
+size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H) {
+  const size_t tiles = dense_tiles(W, H), F = max_frames, npx = (size_t)W * H;
+  return align256(F * tiles * kTile * 32) + align256(F * tiles * 4) + align256((size_t)max_edges * tiles * kPartStride * 4) +
+         align256((size_t)max_edges * 48) + align256(F * max_edges * 4) + align256(F * 4) +
+         align256(F * npx * sizeof(MapEntry)) + align256(F * npx);
 }
 
-void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose,
-                  const int32_t *edges, const int32_t *pairs, int E, const bt_edge_params &prm,
-                  float *partials, int max_partials_per_edge, float *out, int out_stride,
-                  uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
+void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
+                  const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, float *out,
+                  int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
                   cudaStream_t s, Launch &L) {
   if (E <= 0) return;
   DenseArgs a;
@@ -226,26 +425,50 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   a.fx = K.fx; a.fy = K.fy; a.cx = K.cx; a.cy = K.cy;
   a.ifx = 1.0f / K.fx; a.ify = 1.0f / K.fy;
   a.cxd = K.cx; a.cyd = K.cy; a.ifxd = 1.0 / (double)K.fx; a.ifyd = 1.0 / (double)K.fy;
-  a.node_pose = node_pose; a.edges = edges; a.pairs = pairs; a.E = E;
+  a.node_pose = node_pose;
+  a.edges = edges; a.pairs = pairs; a.E = E;
   a.stride = prm.stride < 1 ? 1 : prm.stride;
-  a.gate2 = (float)((double)prm.dist_gate_m * (double)prm.dist_gate_m);
+  a.tx = (mp.W + kTS - 1) / kTS;
+  a.ty = (mp.H + kTS - 1) / kTS;
+  a.tiles = a.tx * a.ty;
+  a.gate2 = (double)prm.dist_gate_m * (double)prm.dist_gate_m;
   a.cos_gate = prm.cos_gate;
   a.huber = prm.huber_m;
-  a.partials = partials;
-  a.nblk = dense_partials_per_edge(mp.W, mp.H);
-  (void)max_partials_per_edge;
-  dim3 grid(a.nblk, E);
+  // carve the scratch
+  char *p = (char *)scratch;
+  const size_t tiles = a.tiles, F = mp.n_frames, npx = (size_t)mp.W * mp.H;
+  a.entries = (float4 *)p;   p += align256(F * tiles * kTile * 32);
+  a.counts = (int32_t *)p;   p += align256(F * tiles * 4);
+  a.partials = (float *)p;   p += align256((size_t)E * tiles * kPartStride * 4);
+  a.tji = (float *)p;        p += align256((size_t)E * 48);
+  a.elist = (int32_t *)p;    p += align256(F * E * 4);
+  a.ecount = (int32_t *)p;   p += align256(F * 4);
+  a.pmap = (MapEntry *)p;    p += align256(F * npx * sizeof(MapEntry));
+  a.vmap = (uint8_t *)p;
+  L.begin(K_DENSE_PREP, s);
+  k_edge_consts<<<(E + 127) / 128, 128, 0, s>>>(a);
+  L.end(K_DENSE_PREP, s);
+  L.begin(K_DENSE_PREP, s);
+  k_edge_lists<<<mp.n_frames, 256, 0, s>>>(a);
+  L.end(K_DENSE_PREP, s);
+  L.begin(K_DENSE_PREP, s);
+  k_dense_prep<<<dim3(a.tiles, mp.n_frames), kDenseThreads, 0, s>>>(a);
+  L.end(K_DENSE_PREP, s);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDenseSmem);
+    attr = true;
+  }
   L.begin(K_DENSE, s);
-  k_dense<<<grid, kDenseThreads, 0, s>>>(a);
+  k_dense<<<dim3(a.tiles, mp.n_frames), kDenseThreads, kDenseSmem, s>>>(a);
   L.end(K_DENSE, s);
   L.begin(K_DENSE_REDUCE, s);
-  k_dense_reduce<<<E, 32, 0, s>>>(partials, a.nblk, E, edges, out, out_stride, records, rec_stride,
-                                  rec_off_ij, rec_off_ji);
+  k_dense_reduce<<<E, 32, 0, s>>>(a.partials, a.counts, a.tiles, edges, pairs, out, out_stride, records,
+                                  rec_stride, rec_off_ij, rec_off_ji);
   L.end(K_DENSE_REDUCE, s);
 }
 
-void launch_compose(const bt_pose *a, const bt_pose *b, bt_pose *out, int n, cudaStream_t s,
-                    Launch &L) {
+void launch_compose(const bt_pose *a, const bt_pose *b, bt_pose *out, int n, cudaStream_t s, Launch &L) {
   if (n <= 0) return;
   L.begin(K_COMPOSE, s);
   k_compose<<<(n + 127) / 128, 128, 0, s>>>(a, b, out, n);

@@ -33,7 +33,8 @@ struct MapView {
 
 // ---- launch bookkeeping: counts kernels and (optionally) brackets each with events ----
 enum KernelId {
-  K_NEAREST = 0, K_MUTUAL, K_RANSAC_SCORE, K_RANSAC_FINISH, K_DENSE, K_DENSE_REDUCE, K_COMPOSE,
+  K_NEAREST = 0, K_MUTUAL, K_RANSAC_SCORE, K_RANSAC_FINISH, K_DENSE_PREP, K_DENSE, K_DENSE_REDUCE,
+  K_COMPOSE,
   K_COUNT
 };
 struct Launch {
@@ -56,12 +57,12 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
                    int32_t *hyp_counts, const bt_pose *node_pose, float huber, cudaStream_t s,
                    Launch &L);
 // dense Eq. (3): edges either explicit (edges != null) or derived from pairs (2 per pair)
-void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose,
-                  const int32_t *edges, const int32_t *pairs, int E, const bt_edge_params &prm,
-                  float *partials, int max_partials_per_edge, float *out, int out_stride,
-                  uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
+void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
+                  const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, float *out,
+                  int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
                   cudaStream_t s, Launch &L);
-int dense_partials_per_edge(int W, int H);
+int dense_tiles(int W, int H);
+size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H);
 void launch_compose(const bt_pose *a, const bt_pose *b, bt_pose *out, int n, cudaStream_t s,
                     Launch &L);
 

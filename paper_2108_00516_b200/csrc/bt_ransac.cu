@@ -350,18 +350,25 @@ __device__ __forceinline__ double det3(const double *M) {
          M[2] * (M[3] * M[7] - M[4] * M[6]);
 }
 
-// fixed-order block sum of one double (256 threads, result valid in every thread)
-template <int NT>
-__device__ double block_sum(double v, double *red) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+// fixed-order block sums of N doubles (256 threads; results valid in every thread)
+template <int N>
+__device__ void block_sum_n(double (&v)[N], double *red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
   __syncthreads();
-  if (lane == 0) red[warp] = v;
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) red[warp * N + k] = v[k];
   __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < NT / 32; ++w) t += red[w];
-  return t;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w * N + k];
+    v[k] = t;
+  }
 }
 
 struct FinishArgs {
@@ -387,10 +394,11 @@ constexpr int kFeatChunk = 64;
 constexpr int kFeatRow = 3 + 36 + 2;
 
 __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
+  extern __shared__ int inl[];                     // [n_max] inlier match indices, in order
   __shared__ float Tb[12];
-  __shared__ double red[kFinThreads / 32];
+  __shared__ double red[(kFinThreads / 32) * 9];
   __shared__ double fstage[kFeatChunk * kFeatRow];
-  __shared__ int sh_idx[kFeatChunk];
+  __shared__ int wcnt[kFinThreads / 32];
   __shared__ double shT[12];
   __shared__ int sh_status;
   const int p = blockIdx.x;
@@ -422,10 +430,12 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     }
   }
   __syncthreads();
-  // inlier mask C_ij of h* (all words up to n_max written; bit m = match m)
+  // inlier mask C_ij of h* (all words up to n_max written; bit m = match m) and the
+  // ordered inlier list, by ballots + a block prefix over warps
   float T[12];
+#pragma unroll
   for (int k = 0; k < 12; ++k) T[k] = Tb[k];
-  int cnt = 0;
+  int n_in = 0;
   for (int m0 = 0; m0 < W * 32; m0 += kFinThreads) {
     const int m = m0 + tid;
     bool in = false;
@@ -436,41 +446,54 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
       in = inlier(T, q0, q1, q2, q3, A.delta2, A.cosa);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, in);
-    if (lane == 0 && (m0 >> 5) + warp < W) rec[kRecMask + (m0 >> 5) + warp] = bal;
-    cnt += lane == 0 ? __popc(bal) : 0;
+    if (lane == 0) {
+      if ((m0 >> 5) + warp < W) rec[kRecMask + (m0 >> 5) + warp] = bal;
+      wcnt[warp] = __popc(bal);
+    }
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < kFinThreads / 32; ++w) {
+      off += w < warp ? wcnt[w] : 0;
+      tot += wcnt[w];
+    }
+    if (in) inl[n_in + off + __popc(bal & ((1u << lane) - 1u))] = m;
+    n_in += tot;
+    __syncthreads();
   }
-  const int best_count = (int)block_sum<kFinThreads>((double)cnt, red);
+  const int best_count = n_in;
   if (best_h >= 0 && best_count < A.min_inliers) status = BT_PAIR_FEW_INLIERS;
 
   // refit: Arun on all inliers (fp64), two-pass centroid / cross-covariance
   double Rr[9], tr[3];
   bool refit_ok = false;
   if (status == BT_PAIR_OK) {
-    double sa[3] = {0, 0, 0}, sb[3] = {0, 0, 0};
-    for (int m = tid; m < M; m += kFinThreads) {
-      if (!((rec[kRecMask + (m >> 5)] >> (m & 31)) & 1u)) continue;
+    double s6[6] = {0, 0, 0, 0, 0, 0};
+    for (int k = tid; k < best_count; k += kFinThreads) {
+      const int m = inl[k];
       const int i = mt[2 * m], j = mt[2 * m + 1];
-      for (int c = 0; c < 3; ++c) { sa[c] += pa_f[3 * i + c]; sb[c] += pb_f[3 * j + c]; }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { s6[c] += pa_f[3 * i + c]; s6[3 + c] += pb_f[3 * j + c]; }
     }
+    block_sum_n<6>(s6, red);
     double ca[3], cb[3];
-    for (int c = 0; c < 3; ++c) {
-      ca[c] = block_sum<kFinThreads>(sa[c], red) / best_count;
-      cb[c] = block_sum<kFinThreads>(sb[c], red) / best_count;
-    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { ca[c] = s6[c] / best_count; cb[c] = s6[3 + c] / best_count; }
     double Hl[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int m = tid; m < M; m += kFinThreads) {
-      if (!((rec[kRecMask + (m >> 5)] >> (m & 31)) & 1u)) continue;
+    for (int k = tid; k < best_count; k += kFinThreads) {
+      const int m = inl[k];
       const int i = mt[2 * m], j = mt[2 * m + 1];
       double da[3], db[3];
+#pragma unroll
       for (int c = 0; c < 3; ++c) { da[c] = pa_f[3 * i + c] - ca[c]; db[c] = pb_f[3 * j + c] - cb[c]; }
+#pragma unroll
       for (int r = 0; r < 3; ++r)
+#pragma unroll
         for (int c = 0; c < 3; ++c) Hl[3 * r + c] += da[r] * db[c];
     }
-    double Hm[9];
-    for (int k = 0; k < 9; ++k) Hm[k] = block_sum<kFinThreads>(Hl[k], red);
+    block_sum_n<9>(Hl, red);
     if (tid == 0) {
       double U[9], s[3], V[9];
-      svd3_jacobi(Hm, U, s, V);
+      svd3_jacobi(Hl, U, s, V);
       const double ratio = s[0] > 0 ? s[1] / s[0] : 0.0;
       if (ratio < A.tau) {
         sh_status = BT_PAIR_REFIT_DEGENERATE;
@@ -487,7 +510,9 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     __syncthreads();
     status = sh_status;
     refit_ok = status == BT_PAIR_OK;
+#pragma unroll
     for (int k = 0; k < 9; ++k) Rr[k] = shT[k];
+#pragma unroll
     for (int k = 0; k < 3; ++k) tr[k] = shT[9 + k];
   }
   if (tid == 0) {
@@ -530,22 +555,11 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     else if (k == 91) kind = 3;
   }
   double acc = 0.0;
-  const int n_in = best_h >= 0 ? best_count : 0;        // C_ij = inliers of h*, whatever the status
-  // walk the inliers in match order, kFeatChunk at a time
-  int m_next = 0;
-  for (int done = 0; done < n_in; done += kFeatChunk) {
+  const int n_feat = best_h >= 0 ? best_count : 0;     // C_ij = inliers of h*, whatever the status
+  for (int done = 0; done < n_feat; done += kFeatChunk) {
     __syncthreads();
-    if (tid == 0) {                    // collect the next chunk of inlier indices (in order)
-      int c = 0;
-      while (c < kFeatChunk && m_next < M) {
-        if ((rec[kRecMask + (m_next >> 5)] >> (m_next & 31)) & 1u) sh_idx[c++] = m_next;
-        ++m_next;
-      }
-      for (; c < kFeatChunk; ++c) sh_idx[c] = -1;
-    }
-    __syncthreads();
-    if (tid < kFeatChunk && sh_idx[tid] >= 0) {
-      const int m = sh_idx[tid];
+    if (tid < kFeatChunk && done + tid < n_feat) {
+      const int m = inl[done + tid];
       const int i = mt[2 * m], j = mt[2 * m + 1];
       const double pm[3] = {pa_f[3 * i], pa_f[3 * i + 1], pa_f[3 * i + 2]};
       const double pn[3] = {pb_f[3 * j], pb_f[3 * j + 1], pb_f[3 * j + 2]};
@@ -556,17 +570,13 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
                (Rj[r] * (pn[0] - tj[0]) + Rj[3 + r] * (pn[1] - tj[1]) + Rj[6 + r] * (pn[2] - tj[2]));
         row[r] = e[r];
       }
-      // J rows: r = 0..2, cols 0..11
+      const double Sp[9] = {0, -pm[2], pm[1], pm[2], 0, -pm[0], -pm[1], pm[0], 0};
+      const double Sq[9] = {0, -pn[2], pn[1], pn[2], 0, -pn[0], -pn[1], pn[0], 0};
       for (int r = 0; r < 3; ++r) {
-        // (R^T)[r][c] = R[c][r]
+        // (R^T)[r][c] = R[c][r];  (R^T [p]x)[r][c] = sum_k R[k][r] S[k][c]
         for (int c = 0; c < 3; ++c) {
           row[3 + 12 * r + c] = -Ri[3 * c + r];
           row[3 + 12 * r + 6 + c] = Rj[3 * c + r];
-        }
-        // (R^T [p]x)[r][c] = sum_k R[k][r] S[k][c], S = [p]x
-        const double Sp[9] = {0, -pm[2], pm[1], pm[2], 0, -pm[0], -pm[1], pm[0], 0};
-        const double Sq[9] = {0, -pn[2], pn[1], pn[2], 0, -pn[0], -pn[1], pn[0], 0};
-        for (int c = 0; c < 3; ++c) {
           double x = 0, y = 0;
           for (int k = 0; k < 3; ++k) { x += Ri[3 * k + r] * Sp[3 * k + c]; y += Rj[3 * k + r] * Sq[3 * k + c]; }
           row[3 + 12 * r + 3 + c] = x;
@@ -582,7 +592,7 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     }
     __syncthreads();
     if (kind >= 0) {
-      const int nc = min(kFeatChunk, n_in - done);
+      const int nc = min(kFeatChunk, n_feat - done);
       for (int c = 0; c < nc; ++c) {
         const double *row = fstage + c * kFeatRow;
         const double *J = row + 3;
@@ -595,7 +605,6 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   }
   const int fo = rec_feat(n_max);
   if (tid < 96) rec[fo + tid] = __float_as_uint(kind >= 0 ? (float)acc : 0.f);
-  (void)warp;
 }
 
 }  // namespace
@@ -635,7 +644,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   f.best_key = best_key; f.records = records; f.rec_stride = rec_stride;
   f.node_pose = node_pose; f.huber = huber;
   L.begin(K_RANSAC_FINISH, s);
-  k_ransac_finish<<<P, kFinThreads, 0, s>>>(f);
+  k_ransac_finish<<<P, kFinThreads, (size_t)mask_words(kp.n_max) * 32 * sizeof(int), s>>>(f);
   L.end(K_RANSAC_FINISH, s);
 }
 
