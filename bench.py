@@ -270,8 +270,9 @@ def main():
                       "avg_launch_ms": tot / n, "launches_per_step": n / args.steps,
                       "share_of_step": tot / ms if ms else None, "work": note}
     pair_sizes = float(sum(int(sc.n_kp[a]) * int(sc.n_kp[b]) for a, b in pairs))
-    add("k_nearest", "alu", 2 * pair_sizes * 128 * 3, "TFLOP/s", fp32_peak_tflops,
-        "3 flop per (i, j, k) per direction, both directions")
+    tc_peak = float(peaks.get("bf16_tflops", 1614.4))     # fp16 kind::f16 = bf16 rate (guide ratio 1:1)
+    add("k_match_tc", "tensor", 2 * pair_sizes * 128, "TFLOP/s", tc_peak,
+        "2 n_a n_b 128 flop per pair (the Gram contraction, counted once)")
     add("k_ransac_score", "alu", tests * FLOPS_PER_TEST, "TFLOP/s", fp32_peak_tflops,
         f"{FLOPS_PER_TEST} flop per (hypothesis, correspondence) test")
     valid_per_frame = np.array([float(((sc.mask[f] > 0) & (sc.depth[f] > 0)).sum()) for f in range(N_FRAMES)])
@@ -282,6 +283,7 @@ def main():
     add("k_dense_prep", "hbm", N_FRAMES * npx * 1 + valid_per_frame.sum() * (16 + 32), "GB/s", hbm_peak,
         "mask of every pixel + depth/normal of valid pixels + 32-B entry per valid pixel")
     dom = max(kern, key=lambda k: kern[k]["share_of_step"] or 0) if kern else None
+    step_ms_by_kernel = {k: v[0] / args.steps for k, v in prof.items() if v[1]}
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if dom and os.path.exists(tf):
@@ -343,7 +345,8 @@ def main():
                 "parallelism": f"dp{world} (one track per rank, records all-gathered over NCCL)" if world > 1
                 else "single GPU",
                 "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
-                "roofline": roof, "kernels": kern, "e2e": e2e, "cpu_baseline": cpu}
+                "roofline": roof, "kernels": kern, "kernel_ms_per_step": step_ms_by_kernel,
+                "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -2,7 +2,10 @@
 // stream-ordered orchestration of the kernels in bt_match.cu / bt_ransac.cu / bt_dense.cu.
 #include <cuda_runtime.h>
 
+#include <cudaTypedefs.h>
+
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -23,11 +26,14 @@ struct bt_ctx {
   double prof_ms[bt::K_COUNT] = {0};
   int64_t prof_n[bt::K_COUNT] = {0};
   // capacity
-  int cap_pairs = 0, cap_nmax = 0, cap_hyp = 0, cap_frames = 0, cap_w = 0, cap_h = 0;
+  int cap_pairs = 0, cap_nmax = 0, cap_hyp = 0, cap_frames = 0, cap_w = 0, cap_h = 0, cap_stage = 0;
   size_t cap_dense = 0;                       // bytes of dense scratch
   // scratch
-  int32_t *nn_ab = nullptr, *nn_ba = nullptr, *matches = nullptr, *n_matches = nullptr;
-  uint8_t *ratio_ok = nullptr;
+  void *match = nullptr;                      // matching scratch (bt::MatchScratch)
+  bt::MatchScratch ms{};
+  CUtensorMap tmap_desc;                      // TMA view of ms.desc16: [frames * n_pad][128] fp16
+  int force_fallback = 0;                     // BT_FORCE_FALLBACK: exact rescoring of every row
+  int32_t *matches = nullptr, *n_matches = nullptr;
   unsigned long long *best_key = nullptr;
   void *dense = nullptr;
   // staging for bt_register_pairs_host
@@ -60,8 +66,8 @@ void free_dev(T *&p) {
 }
 
 void free_scratch(bt_ctx *c) {
-  free_dev(c->nn_ab); free_dev(c->nn_ba); free_dev(c->matches); free_dev(c->n_matches);
-  free_dev(c->ratio_ok); free_dev(c->best_key); free_dev(c->dense);
+  free_dev(c->match); free_dev(c->matches); free_dev(c->n_matches);
+  free_dev(c->best_key); free_dev(c->dense);
   free_dev(c->st_nkp); free_dev(c->st_pairs); free_dev(c->st_uid); free_dev(c->st_records);
   free_dev(c->st_desc); free_dev(c->st_pts); free_dev(c->st_nrm); free_dev(c->st_depth);
   free_dev(c->st_normal); free_dev(c->st_mask); free_dev(c->st_pose);
@@ -88,6 +94,8 @@ bt_status check_kp(bt_ctx *c, const bt_keypoints *kp) {
   if (kp->n_frames < 1 || kp->n_max < 1) return fail(c, BT_EINVAL, "keypoints: n_frames/n_max < 1");
   if (kp->n_max > c->cap_nmax)
     return fail(c, BT_ECAPACITY, "n_max %d > reserved %d", kp->n_max, c->cap_nmax);
+  if (kp->n_frames > c->cap_frames)
+    return fail(c, BT_ECAPACITY, "keypoint frames %d > reserved %d", kp->n_frames, c->cap_frames);
   if (!kp->n_kp || !kp->desc || !kp->pts || !kp->nrm) return fail(c, BT_EINVAL, "keypoints: NULL buffer");
   if (!aligned16(kp->desc) || !aligned16(kp->pts) || !aligned16(kp->nrm) || !aligned16(kp->n_kp))
     return fail(c, BT_EINVAL, "keypoints: buffers must be 16-byte aligned");
@@ -156,6 +164,8 @@ bt_status bt_create(bt_ctx **out, int cuda_device) {
   bt_ctx *c = new (std::nothrow) bt_ctx;
   if (!c) return BT_ENOMEM;
   c->device = cuda_device;
+  const char *ff = getenv("BT_FORCE_FALLBACK");
+  c->force_fallback = ff && ff[0] && ff[0] != '0';
   *out = c;
   return BT_OK;
 }
@@ -188,10 +198,29 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
   const size_t PN = (size_t)max_pairs * n_max;
   const size_t dense_bytes = (width > 0 && height > 0 && max_frames > 0)
                                  ? bt::dense_scratch_bytes(max_frames, 2 * max_pairs, width, height) : 0;
-  bool ok = cudaMalloc(&c->nn_ab, PN * 4) == cudaSuccess && cudaMalloc(&c->nn_ba, PN * 4) == cudaSuccess &&
+  const int mframes = max_frames > 0 ? max_frames : 1;
+  bool ok = cudaMalloc(&c->match, bt::match_scratch_bytes(mframes, max_pairs, n_max)) == cudaSuccess &&
             cudaMalloc(&c->matches, PN * 8) == cudaSuccess && cudaMalloc(&c->n_matches, (size_t)max_pairs * 4) == cudaSuccess &&
-            cudaMalloc(&c->ratio_ok, PN) == cudaSuccess &&
             cudaMalloc(&c->best_key, (size_t)max_pairs * 8) == cudaSuccess;
+  if (ok) {
+    c->ms = bt::carve_match_scratch(c->match, mframes, max_pairs, n_max);
+    // TMA tensor map over the fp16 unit descriptors: 2-D [rows][128], 64 x 128 boxes, 128B swizzle
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        encode = nullptr;
+    }
+    const cuuint64_t rows = (cuuint64_t)mframes * bt::match_n_pad(n_max);
+    cuuint64_t dims[2] = {(cuuint64_t)bt::kDim, rows};
+    cuuint64_t strides[1] = {(cuuint64_t)bt::kDim * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    ok = encode && encode(&c->tmap_desc, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, c->ms.desc16, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   if (ok && dense_bytes > 0) ok = cudaMalloc(&c->dense, dense_bytes) == cudaSuccess;
   if (ok && max_frames > 0) {
     const size_t FN = (size_t)max_frames * n_max, FP = (size_t)max_frames * width * height;
@@ -209,8 +238,8 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
     free_scratch(c);
     return fail(c, BT_ENOMEM, "bt_reserve: cudaMalloc failed");
   }
-  c->cap_pairs = max_pairs; c->cap_nmax = n_max; c->cap_hyp = max_hyp; c->cap_frames = max_frames;
-  c->cap_w = width; c->cap_h = height; c->cap_dense = dense_bytes;
+  c->cap_pairs = max_pairs; c->cap_nmax = n_max; c->cap_hyp = max_hyp; c->cap_frames = mframes;
+  c->cap_w = width; c->cap_h = height; c->cap_dense = dense_bytes; c->cap_stage = max_frames;
   return BT_OK;
 }
 
@@ -224,7 +253,7 @@ bt_status bt_match(bt_ctx *c, const bt_keypoints *kp, const int32_t *pairs, int3
   if (P == 0) return BT_OK;
   if (!pairs || !matches || !n_matches) return fail(c, BT_EINVAL, "bt_match: NULL buffer");
   const float ratio = prm ? prm->ratio : 1.f;
-  bt::launch_match(kview(kp), pairs, P, ratio, c->nn_ab, c->nn_ba, c->ratio_ok, matches, n_matches,
+  bt::launch_match(kview(kp), pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, matches, n_matches,
                    (cudaStream_t)stream, c->launch);
   return after_launch(c, "bt_match");
 }
@@ -267,8 +296,8 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
                                     uint32_t *records, cudaStream_t st) {
   const int rw = bt::rec_words(kp->n_max);
   const float ratio = mprm ? mprm->ratio : 1.f;
-  bt::launch_match(kview(kp), pairs, P, ratio, c->nn_ab, c->nn_ba, c->ratio_ok, c->matches, c->n_matches, st,
-                   c->launch);
+  bt::launch_match(kview(kp), pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches, c->n_matches,
+                   st, c->launch);
   bt::launch_ransac(kview(kp), pairs, uid, P, c->matches, c->n_matches, *rprm, c->best_key, records, rw, nullptr,
                     eprm ? node_pose : nullptr, eprm ? eprm->huber_m : 0.f, st, c->launch);
   if (eprm)
@@ -306,7 +335,7 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
   BT_CHECK_CTX(c);
   bt_status s;
   if (!kp) return fail(c, BT_EINVAL, "keypoints: NULL");
-  if (kp->n_frames > c->cap_frames) return fail(c, BT_ECAPACITY, "frames %d > reserved %d", kp->n_frames, c->cap_frames);
+  if (kp->n_frames > c->cap_stage) return fail(c, BT_ECAPACITY, "frames %d > reserved staging %d", kp->n_frames, c->cap_stage);
   if ((s = check_ransac(c, rprm)) != BT_OK) return s;
   if (P < 0) return fail(c, BT_EINVAL, "P < 0");
   if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
@@ -316,7 +345,7 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
     return fail(c, BT_EINVAL, "bt_register_pairs_host: NULL buffer");
   if (eprm) {
     if (!maps || !K || !node_pose) return fail(c, BT_EINVAL, "bt_register_pairs_host: NULL maps/K/poses");
-    if (maps->n_frames > c->cap_frames || maps->width * maps->height > c->cap_w * c->cap_h)
+    if (maps->n_frames > c->cap_stage || maps->width * maps->height > c->cap_w * c->cap_h)
       return fail(c, BT_ECAPACITY, "maps beyond reserved staging");
   }
   const cudaStream_t st = (cudaStream_t)stream;
@@ -360,9 +389,9 @@ bt_status bt_compose_poses(bt_ctx *c, const bt_pose *a, const bt_pose *b, bt_pos
   return after_launch(c, "bt_compose_poses");
 }
 
-static const char *kKernelNames[bt::K_COUNT] = {"k_nearest", "k_mutual", "k_ransac_score",
-                                                 "k_ransac_finish", "k_dense_prep", "k_dense",
-                                                 "k_dense_reduce", "k_compose"};
+static const char *kKernelNames[bt::K_COUNT] = {"k_desc_prep", "k_match_tc", "k_resolve", "k_mutual",
+                                                 "k_ransac_score", "k_ransac_finish", "k_dense_prep",
+                                                 "k_dense", "k_dense_reduce", "k_compose"};
 
 static cudaEvent_t take_event(bt_ctx *c) {
   if (c->ev_pool.empty()) {

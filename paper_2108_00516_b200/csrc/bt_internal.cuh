@@ -1,6 +1,8 @@
 // bt_internal.cuh — internal launch interfaces and device helpers of libbt (sm_100a).
 // Not part of the ABI (include/bt.h is).  Nothing here is shared with oracle/.
 #pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -33,9 +35,20 @@ struct MapView {
 
 // ---- launch bookkeeping: counts kernels and (optionally) brackets each with events ----
 enum KernelId {
-  K_NEAREST = 0, K_MUTUAL, K_RANSAC_SCORE, K_RANSAC_FINISH, K_DENSE_PREP, K_DENSE, K_DENSE_REDUCE,
-  K_COMPOSE,
+  K_DESC_PREP = 0, K_MATCH_TC, K_RESOLVE, K_MUTUAL, K_RANSAC_SCORE, K_RANSAC_FINISH, K_DENSE_PREP,
+  K_DENSE, K_DENSE_REDUCE, K_COMPOSE,
   K_COUNT
+};
+
+// matching scratch (carved from one allocation; see match_scratch_bytes)
+struct MatchScratch {
+  __half *desc16;          // [F][n_pad][128] unit descriptors (TMA source)
+  float *norm;             // [F][n_pad]
+  unsigned *maxnorm;       // [F] float bits of max |a|
+  uint2 *rowcand;          // [P][n_pad]           top-2 keys per row
+  uint2 *colcand;          // [P][n_pad/128][n_pad] top-2 keys per column per row tile
+  int32_t *nn_ab, *nn_ba;  // [P][n_max]
+  uint8_t *ratio_ok;       // [P][n_max]
 };
 struct Launch {
   int count = 0;
@@ -47,8 +60,11 @@ struct Launch {
 
 // ---- launchers (stream-ordered, no sync) -------------------------------------------
 // matching
-void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, int32_t *nn_ab,
-                  int32_t *nn_ba, uint8_t *ratio_ok, int32_t *matches, int32_t *n_matches,
+int match_n_pad(int n_max);
+size_t match_scratch_bytes(int max_frames, int max_pairs, int n_max);
+MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_max);
+void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, const MatchScratch &S,
+                  const CUtensorMap *tmap, int force_fallback, int32_t *matches, int32_t *n_matches,
                   cudaStream_t s, Launch &L);
 // RANSAC scoring + finish (+ optional Eq. (2) blocks at node poses)
 void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, int P,

@@ -1,14 +1,31 @@
 // bt_match.cu — mutual nearest-neighbour descriptor matching (P:4 "feature matching",
 // P:25 "n keypoints ... feature descriptor D_i in R^128"), readings R1-R4 of DESIGN.md:
 // squared Euclidean distance, ties -> lowest index, mutual NN, optional Lowe ratio,
-// output ascending in i.
+// output ascending in i.  The result is the EXACT brute-force one; the tensor cores only
+// prune candidates under a proven error bound.
 //
-// Exact fp32 distances on the FP32 pipe, one warp per query descriptor:
-//   lane l owns descriptor words [4l, 4l+4) (one LDG.128 per reference descriptor, a warp
-//   reads 512 contiguous bytes); 32 reference descriptors are processed per step and their
-//   32 lane-partials are combined by a 5-level "transpose reduction" (31 shuffles for 32
-//   sums) after which lane l holds the distance to reference j0 + l.  The summation order
-//   (4 sequential terms per lane, then a fixed binary tree) is the same for every (i, j).
+//  k_desc_prep   per frame and keypoint: |a| (fp32) and the unit descriptor a/|a| in fp16
+//                ([F][n_pad][128], zero padded), plus the frame's max |a| (certificate).
+//  k_match_tc    one CTA per (pair, 128-row tile of frame a).  TMA (128B-swizzled boxes of
+//                64 x 128 fp16) stages the A tile once and B in 256-column chunks; one thread
+//                issues tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = 256, K = 8 x 16) into
+//                a 256-column fp32 TMEM accumulator, S = A_hat . B_hat^T; four epilogue warps
+//                read TMEM with tcgen05.ld (row = TMEM lane = thread), form
+//                d_hat = |a|^2 + |b|^2 - 2 |a||b| S and keep, as packed (sortable value | index)
+//                keys, the two smallest per row (thread-local min/max) and per column (two
+//                redux.sync.min per column per warp, merged across warps in smem).
+//  k_resolve     one warp per row (and per column): the nearest neighbour is certified when
+//                the runner-up's d_hat exceeds the best's by more than twice the bound
+//                eps = 2.2e-3 |a||b|max + 1e-6 (|a|^2 + |b|max^2) (+ key truncation):
+//                fp16 unit vectors have relative error 2^-11 per element, so
+//                |S_hat - S| <= 2^-10 + 128 * 2^-23 (fp32 accumulation, any rounding mode)
+//                ~ 1.0e-3, hence |d_hat - d| <= 2.0e-3 |a||b| + fp32 evaluation error.
+//                Certified rows take the best candidate; every other row (ties, ratio test,
+//                BT_FORCE_FALLBACK) is rescored exactly over all references in fp32 (lane l
+//                owns words [4l, 4l+4), 32 references per step, transpose reduction).
+//  k_mutual      keep (i, NN_ab(i)) iff NN_ba(NN_ab(i)) == i (+ ratio flag), compact ascending.
+#include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -18,27 +35,256 @@ namespace bt {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
+constexpr int kTcThreads = 128;               // 4 epilogue warps = the 128 TMEM lanes
+constexpr int kChunk = 256;                   // B columns per MMA chunk (N)
+constexpr unsigned kNone = 0xFFFFFFFFu;
 
-__device__ __forceinline__ void top2_update(float d, int j, float &b1, int &j1, float &b2) {
-  if (d < b1) { b2 = b1; b1 = d; j1 = j; }
-  else if (d < b2) { b2 = d; }
+// ---------------------------------------------------------------- small PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  uint32_t ok = 0;
+  for (uint32_t spin = 0; !ok; ++spin) {
+    if (spin == (1u << 26)) __trap();                             // never hang the device
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart
+__device__ __forceinline__ uint64_t umma_desc_sw128(const void *p) {
+  const uint64_t addr = smem_u32(p);
+  return ((addr & 0x3FFFFull) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+#define BT_TMEM_LD32(taddr, v)                                                                              \
+  asm volatile(                                                                                             \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"  \
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),      \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),            \
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),          \
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),          \
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                               \
+      : "r"(taddr))
+
+__device__ __forceinline__ unsigned sortable(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unsortable(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
 }
 
-// nn[p][q] = argmin_r d(query q, reference r) for queries of frame pairs[p][dir] against
-// references of frame pairs[p][1-dir]; for dir == 0 also the ratio-test flag.
+// ---------------------------------------------------------------- descriptor prep
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_nearest(KpView kp, const int32_t *__restrict__ pairs, int dir, float ratio2,
-          int32_t *__restrict__ nn, uint8_t *__restrict__ ratio_ok) {
-  const int p = blockIdx.y;
+k_desc_prep(KpView kp, MatchScratch S, int n_pad) {
+  const int f = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int fq = pairs[2 * p + dir], fr = pairs[2 * p + 1 - dir];
-  const int nq = min(kp.n_kp[fq], kp.n_max), nr = min(kp.n_kp[fr], kp.n_max);
-  const int q = blockIdx.x * kWarpsPerBlock + warp;
-  if (q >= nq) return;                                           // warp-uniform
-  const float4 a = reinterpret_cast<const float4 *>(kp.desc + ((size_t)fq * kp.n_max + q) * kDim)[lane];
-  const float4 *R = reinterpret_cast<const float4 *>(kp.desc + (size_t)fr * kp.n_max * kDim);
-  float b1 = CUDART_INF_F, b2 = CUDART_INF_F;
-  int j1 = -1;
+  const int i = blockIdx.x * kWarpsPerBlock + warp;
+  if (i >= n_pad) return;
+  const int n = min(kp.n_kp[f], kp.n_max);
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < n) a = reinterpret_cast<const float4 *>(kp.desc + ((size_t)f * kp.n_max + i) * kDim)[lane];
+  float s = __fmul_rn(a.x, a.x);
+  s = __fmaf_rn(a.y, a.y, s);
+  s = __fmaf_rn(a.z, a.z, s);
+  s = __fmaf_rn(a.w, a.w, s);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float nrm = sqrtf(s);
+  const float inv = nrm > 0.f ? 1.0f / nrm : 0.f;
+  __half2 h01 = __floats2half2_rn(a.x * inv, a.y * inv), h23 = __floats2half2_rn(a.z * inv, a.w * inv);
+  uint2 packed;
+  packed.x = *reinterpret_cast<uint32_t *>(&h01);
+  packed.y = *reinterpret_cast<uint32_t *>(&h23);
+  reinterpret_cast<uint2 *>(S.desc16 + ((size_t)f * n_pad + i) * kDim)[lane] = packed;
+  if (lane == 0) {
+    S.norm[(size_t)f * n_pad + i] = nrm;
+    if (i < n) atomicMax(S.maxnorm + f, __float_as_uint(nrm));       // nrm >= 0: bits are monotone
+  }
+}
+
+// ---------------------------------------------------------------- tcgen05 candidate search
+struct TcArgs {
+  KpView kp;
+  const int32_t *pairs;
+  MatchScratch S;
+  int n_pad, rt_count, ibits;
+};
+
+constexpr size_t kTcSmem = 1024 /*align*/ + 32768 /*A*/ + 65536 /*B*/ + 4 * kChunk * 8 /*colbuf*/ + kChunk * 8 /*nbv*/;
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_match_tc(const __grid_constant__ CUtensorMap tmap, TcArgs A) {
+  extern __shared__ uint8_t tc_smem_raw[];
+  __shared__ __align__(8) uint64_t bar_load, bar_mma;
+  __shared__ uint32_t tmem_base_sh;
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = base;                        // [2 K-atoms][128 rows][128 B]
+  uint8_t *sB = base + 32768;                // [2 K-atoms][256 rows][128 B]
+  uint2 *colbuf = reinterpret_cast<uint2 *>(base + 98304);         // [4 warps][256]
+  float2 *nbv = reinterpret_cast<float2 *>(colbuf + 4 * kChunk);   // [256]
+
+  const int p = blockIdx.y, rt = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+  const int na = min(A.kp.n_kp[fa], A.kp.n_max), nb = min(A.kp.n_kp[fb], A.kp.n_max);
+  if (rt * 128 >= na || nb == 0) return;                          // block-uniform
+  const int n_pad = A.n_pad;
+  const unsigned imask = (1u << A.ibits) - 1u;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(kChunk)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(&bar_load, 1);
+    mbar_init(&bar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  const int i = rt * 128 + tid;                                   // this thread's row (= TMEM lane)
+  const bool row_valid = i < na;
+  const float na_n = A.S.norm[(size_t)fa * n_pad + i];
+  const float na2 = na_n * na_n, m2na = -2.f * na_n;
+  unsigned r1 = kNone, r2 = kNone;
+  // instruction descriptor: D f32, A/B f16, K-major both, N = 256, M = 128
+  const uint32_t idesc = (1u << 4) | ((uint32_t)(kChunk >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const int nchunks = (nb + kChunk - 1) / kChunk;
+  uint32_t ph_load = 0, ph_mma = 0;
+
+  for (int c = 0; c < nchunks; ++c) {
+    for (int jj = tid; jj < kChunk; jj += kTcThreads) {
+      const int j = c * kChunk + jj;
+      const float v = j < nb ? A.S.norm[(size_t)fb * n_pad + j] : 0.f;
+      nbv[jj] = make_float2(v, v * v);
+    }
+    if (tid == 0) {
+      mbar_expect_tx(&bar_load, (c == 0 ? 32768u : 0u) + 65536u);
+      if (c == 0) {
+        tma_load_2d(sA, &tmap, 0, fa * n_pad + rt * 128, &bar_load);
+        tma_load_2d(sA + 16384, &tmap, 64, fa * n_pad + rt * 128, &bar_load);
+      }
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          tma_load_2d(sB + kb * 32768 + h * 16384, &tmap, kb * 64, fb * n_pad + c * kChunk + h * 128, &bar_load);
+    }
+    mbar_wait(&bar_load, ph_load);
+    ph_load ^= 1;
+    __syncthreads();                                              // nbv visible
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {                               // K = 128 = 8 x 16
+        const int kb = k >> 2, ks = k & 3;
+        umma_f16(tmem, umma_desc_sw128(sA + kb * 16384 + ks * 32), umma_desc_sw128(sB + kb * 32768 + ks * 32),
+                 idesc, k > 0 ? 1u : 0u);
+      }
+      umma_commit(&bar_mma);
+    }
+    mbar_wait(&bar_mma, ph_mma);
+    ph_mma ^= 1;
+    tc_fence_after();
+    // ---- epilogue: TMEM lane (32 warp + lane) = row i; 32 columns per tcgen05.ld
+#pragma unroll 1
+    for (int cc = 0; cc < kChunk / 32; ++cc) {
+      const int j0 = c * kChunk + cc * 32;
+      if (j0 >= nb) {                                             // uniform: past the last column
+        colbuf[warp * kChunk + cc * 32 + lane] = make_uint2(kNone, kNone);
+        continue;
+      }
+      uint32_t v[32];
+      BT_TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cc * 32), v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      unsigned cm1 = kNone, cm2 = kNone;
+#pragma unroll
+      for (int col = 0; col < 32; ++col) {
+        const int j = j0 + col;
+        if (j >= nb) break;                                       // uniform
+        const float2 bn = nbv[cc * 32 + col];
+        const float d = __fmaf_rn(m2na * bn.x, __uint_as_float(v[col]), na2 + bn.y);
+        const unsigned key = sortable(d) & ~imask;
+        const unsigned rk = row_valid ? (key | (unsigned)j) : kNone;
+        r2 = min(r2, max(r1, rk));
+        r1 = min(r1, rk);
+        const unsigned ck = row_valid ? (key | (unsigned)i) : kNone;
+        const unsigned m1 = __reduce_min_sync(0xffffffffu, ck);
+        const unsigned m2 = __reduce_min_sync(0xffffffffu, ck == m1 ? kNone : ck);
+        if (lane == col) { cm1 = m1; cm2 = m2; }
+      }
+      colbuf[warp * kChunk + cc * 32 + lane] = make_uint2(cm1, cm2);
+    }
+    tc_fence_before();
+    __syncthreads();
+    // merge the 4 warps' per-column top-2 (keys are unique: the row index is packed in)
+    for (int jj = tid; jj < kChunk; jj += kTcThreads) {
+      const int j = c * kChunk + jj;
+      if (j >= nb) continue;
+      unsigned a1 = kNone, a2 = kNone;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint2 x = colbuf[w * kChunk + jj];
+        if (x.x < a1) { a2 = min(a1, x.y); a1 = x.x; }
+        else a2 = min(a2, x.x);
+      }
+      A.S.colcand[((size_t)p * A.rt_count + rt) * n_pad + j] = make_uint2(a1, a2);
+    }
+    __syncthreads();
+  }
+  if (row_valid) A.S.rowcand[(size_t)p * n_pad + i] = make_uint2(r1, r2);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kChunk) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- exact fp32 rescoring
+// warp-cooperative brute force over all nr references: best, index (ties lowest), second
+__device__ void exact_scan(const float4 a, const float4 *R, int nr, int lane, float &b1, int &j1, float &b2) {
+  b1 = CUDART_INF_F; b2 = CUDART_INF_F; j1 = -1;
   for (int j0 = 0; j0 < nr; j0 += 32) {
     float v[32];
 #pragma unroll
@@ -56,8 +302,7 @@ k_nearest(KpView kp, const int32_t *__restrict__ pairs, int dir, float ratio2,
       }
       v[c] = s;
     }
-    // transpose reduction: after the step with offset o, lane keeps the half of its
-    // columns selected by (lane & o) and adds the partner's copy of that half.
+    // transpose reduction: lane l ends with the distance to reference j0 + l
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
       const bool upper = (lane & o) != 0;
@@ -65,26 +310,86 @@ k_nearest(KpView kp, const int32_t *__restrict__ pairs, int dir, float ratio2,
       for (int c = 0; c < o; ++c) {
         const float send = upper ? v[c] : v[c + o];
         const float keep = upper ? v[c + o] : v[c];
-        const float recv = __shfl_xor_sync(0xffffffffu, send, o);
-        v[c] = __fadd_rn(keep, recv);
+        v[c] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
       }
     }
-    const int j = j0 + lane;                                      // column owned by this lane
-    if (j < nr) top2_update(v[0], j, b1, j1, b2);
+    const int j = j0 + lane;
+    if (j < nr) {
+      if (v[0] < b1) { b2 = b1; b1 = v[0]; j1 = j; }
+      else if (v[0] < b2) b2 = v[0];
+    }
   }
-  // warp merge of (best, index, second) with ties -> lowest index
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
     const float ob1 = __shfl_xor_sync(0xffffffffu, b1, o);
     const int oj1 = __shfl_xor_sync(0xffffffffu, j1, o);
     const float ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
     const bool mine = (b1 < ob1) || (b1 == ob1 && (unsigned)j1 < (unsigned)oj1);
-    if (mine) { b2 = fminf(b2, ob1); }
+    if (mine) b2 = fminf(b2, ob1);
     else { b2 = fminf(ob2, b1); b1 = ob1; j1 = oj1; }
   }
+}
+
+struct ResolveArgs {
+  KpView kp;
+  const int32_t *pairs;
+  MatchScratch S;
+  int n_pad, rt_count, ibits, force_fallback;
+  float ratio2;
+};
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_resolve(ResolveArgs A) {
+  const int dir = blockIdx.z, p = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fq = A.pairs[2 * p + dir], fr = A.pairs[2 * p + 1 - dir];
+  const int nq = min(A.kp.n_kp[fq], A.kp.n_max), nr = min(A.kp.n_kp[fr], A.kp.n_max);
+  const int q = blockIdx.x * kWarpsPerBlock + warp;
+  if (q >= nq) return;                                            // warp-uniform
+  int32_t *nn = dir == 0 ? A.S.nn_ab : A.S.nn_ba;
+  const size_t o = (size_t)p * A.kp.n_max + q;
+  if (nr == 0) {
+    if (lane == 0) { nn[o] = -1; if (dir == 0) A.S.ratio_ok[o] = 1; }
+    return;
+  }
+  const unsigned imask = (1u << A.ibits) - 1u;
+  unsigned k1 = kNone, k2 = kNone;
+  if (dir == 0) {
+    const uint2 c = A.S.rowcand[(size_t)p * A.n_pad + q];
+    k1 = c.x; k2 = c.y;
+  } else {
+    const int rts = (nr + 127) / 128;                              // row tiles of frame a
+    for (int rt = 0; rt < rts; ++rt) {
+      const uint2 x = A.S.colcand[((size_t)p * A.rt_count + rt) * A.n_pad + q];
+      if (x.x < k1) { k2 = min(k1, x.y); k1 = x.x; }
+      else k2 = min(k2, x.x);
+    }
+  }
+  bool certified = false;
+  if (!A.force_fallback && A.ratio2 >= 1.f && k1 != kNone) {
+    if (k2 == kNone) certified = true;                             // a single reference
+    else {
+      const float v1 = unsortable(k1 & ~imask), v2 = unsortable(k2 & ~imask);
+      const float nq_n = A.S.norm[(size_t)fq * A.n_pad + q];
+      const float mr = __uint_as_float(A.S.maxnorm[fr]);
+      const float eps = 2.2e-3f * nq_n * mr + 1e-6f * (nq_n * nq_n + mr * mr);
+      const float trunc = ldexpf(fabsf(v1) + fabsf(v2), A.ibits - 22) + 1e-30f;   // cleared key bits
+      certified = (v2 - v1) > 2.f * eps + trunc;
+    }
+  }
+  int j_best;
+  bool ratio_ok = true;
+  if (certified) {
+    j_best = (int)(k1 & imask);
+  } else {
+    const float4 a = reinterpret_cast<const float4 *>(A.kp.desc + ((size_t)fq * A.kp.n_max + q) * kDim)[lane];
+    const float4 *R = reinterpret_cast<const float4 *>(A.kp.desc + (size_t)fr * A.kp.n_max * kDim);
+    float b1, b2;
+    exact_scan(a, R, nr, lane, b1, j_best, b2);
+    ratio_ok = (A.ratio2 >= 1.f) || (nr < 2) || (b1 < A.ratio2 * b2);
+  }
   if (lane == 0) {
-    nn[(size_t)p * kp.n_max + q] = j1;
-    if (dir == 0) ratio_ok[(size_t)p * kp.n_max + q] = (ratio2 >= 1.f) || (nr < 2) || (b1 < ratio2 * b2);
+    nn[o] = j_best;
+    if (dir == 0) A.S.ratio_ok[o] = ratio_ok;
   }
 }
 
@@ -128,22 +433,66 @@ k_mutual(KpView kp, const int32_t *__restrict__ pairs, const int32_t *__restrict
   if (threadIdx.x == 0) n_matches[p] = base;
 }
 
+int ceil_log2(int x) {
+  int b = 0;
+  while ((1 << b) < x) ++b;
+  return b;
+}
+
 }  // namespace
 
-void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, int32_t *nn_ab,
-                  int32_t *nn_ba, uint8_t *ratio_ok, int32_t *matches, int32_t *n_matches,
+int match_n_pad(int n_max) { return (n_max + 127) / 128 * 128; }
+
+size_t match_scratch_bytes(int max_frames, int max_pairs, int n_max) {
+  const size_t np = match_n_pad(n_max), F = max_frames, P = max_pairs, rt = np / 128;
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  return al(F * np * kDim * 2) + al(F * np * 4) + al(F * 4) + al(P * np * 8) + al(P * rt * np * 8) +
+         al(P * n_max * 4) * 2 + al(P * n_max);
+}
+
+MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_max) {
+  const size_t np = match_n_pad(n_max), F = max_frames, P = max_pairs, rt = np / 128;
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  char *c = (char *)p;
+  MatchScratch S;
+  S.desc16 = (__half *)c;        c += al(F * np * kDim * 2);
+  S.norm = (float *)c;           c += al(F * np * 4);
+  S.maxnorm = (unsigned *)c;     c += al(F * 4);
+  S.rowcand = (uint2 *)c;        c += al(P * np * 8);
+  S.colcand = (uint2 *)c;        c += al(P * rt * np * 8);
+  S.nn_ab = (int32_t *)c;        c += al(P * n_max * 4);
+  S.nn_ba = (int32_t *)c;        c += al(P * n_max * 4);
+  S.ratio_ok = (uint8_t *)c;
+  return S;
+}
+
+void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, const MatchScratch &S,
+                  const CUtensorMap *tmap, int force_fallback, int32_t *matches, int32_t *n_matches,
                   cudaStream_t s, Launch &L) {
   if (P <= 0) return;
-  const float ratio2 = ratio >= 1.f ? 1.f : ratio * ratio;
-  dim3 grid((kp.n_max + kWarpsPerBlock - 1) / kWarpsPerBlock, P);
-  L.begin(K_NEAREST, s);
-  k_nearest<<<grid, kWarpsPerBlock * 32, 0, s>>>(kp, pairs, 0, ratio2, nn_ab, ratio_ok);
-  L.end(K_NEAREST, s);
-  L.begin(K_NEAREST, s);
-  k_nearest<<<grid, kWarpsPerBlock * 32, 0, s>>>(kp, pairs, 1, ratio2, nn_ba, nullptr);
-  L.end(K_NEAREST, s);
+  const int n_pad = match_n_pad(kp.n_max);
+  const int rt_count = n_pad / 128;
+  const int ibits = ceil_log2(n_pad);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_match_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+    attr = true;
+  }
+  cudaMemsetAsync(S.maxnorm, 0, sizeof(unsigned) * kp.n_frames, s);
+  L.begin(K_DESC_PREP, s);
+  k_desc_prep<<<dim3((n_pad + kWarpsPerBlock - 1) / kWarpsPerBlock, kp.n_frames), kWarpsPerBlock * 32, 0, s>>>(
+      kp, S, n_pad);
+  L.end(K_DESC_PREP, s);
+  TcArgs ta{kp, pairs, S, n_pad, rt_count, ibits};
+  L.begin(K_MATCH_TC, s);
+  k_match_tc<<<dim3(rt_count, P), kTcThreads, kTcSmem, s>>>(*tmap, ta);
+  L.end(K_MATCH_TC, s);
+  ResolveArgs ra{kp, pairs, S, n_pad, rt_count, ibits, force_fallback, ratio >= 1.f ? 1.f : ratio * ratio};
+  L.begin(K_RESOLVE, s);
+  k_resolve<<<dim3((kp.n_max + kWarpsPerBlock - 1) / kWarpsPerBlock, P, 2), kWarpsPerBlock * 32, 0, s>>>(ra);
+  L.end(K_RESOLVE, s);
   L.begin(K_MUTUAL, s);
-  k_mutual<<<P, 512, 0, s>>>(kp, pairs, nn_ab, nn_ba, ratio_ok, matches, n_matches);
+  k_mutual<<<P, 512, 0, s>>>(kp, pairs, S.nn_ab, S.nn_ba, S.ratio_ok, matches, n_matches);
   L.end(K_MUTUAL, s);
 }
 

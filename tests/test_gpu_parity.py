@@ -350,3 +350,34 @@ def test_error_statuses(bt, torch):
         c.match(fb, pr[:2], mt[:2], nm[:2])
     assert e.value.status == bt.BT_EUNSUPPORTED
     c.close()
+
+
+def test_match_tensor_core_path_equals_exact_fallback(bt, torch, c2):
+    """The tcgen05 candidate + certificate path and the forced exact path
+    (BT_FORCE_FALLBACK=1: every row/column rescored over all references) give identical
+    nearest neighbours and match lists."""
+    import os
+    pairs = synth.all_pairs(16)
+    outs = []
+    for force in ("0", "1"):
+        os.environ["BT_FORCE_FALLBACK"] = force
+        c = bt.Context(0)
+        c.reserve(len(pairs), 512, 256, 16, 640, 480)
+        got, _, _ = gpu_match(bt, torch, c, c2, pairs)
+        outs.append(got)
+        c.close()
+    os.environ.pop("BT_FORCE_FALLBACK", None)
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_match_large_n_multi_chunk(bt, torch, ctx):
+    """n_max = 4096 (C5 size): several row tiles and 256-column chunks per pair."""
+    sc = _custom_scene([4000, 3900, 4096], n_max=4096, seed=11)
+    sc.desc[1, :3900] = sc.desc[0, 100:4000]                   # a shifted copy: known matches
+    pairs = [(0, 1), (1, 2), (2, 0)]
+    got, _, _ = gpu_match(bt, torch, ctx, sc, pairs)
+    for p, (a, b) in enumerate(pairs):
+        o = oracle.match(sc.desc[a, :sc.n_kp[a]], sc.desc[b, :sc.n_kp[b]])
+        parity.compare_matches(got[p], o)
+    assert len(got[0]) >= 3900
