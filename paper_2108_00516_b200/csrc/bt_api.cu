@@ -389,7 +389,7 @@ bt_status bt_compose_poses(bt_ctx *c, const bt_pose *a, const bt_pose *b, bt_pos
   return after_launch(c, "bt_compose_poses");
 }
 
-static const char *kKernelNames[bt::K_COUNT] = {"k_desc_prep", "k_match_tc", "k_resolve", "k_mutual",
+static const char *kKernelNames[bt::K_COUNT] = {"k_desc_prep", "k_match_tc", "k_rescore", "k_mutual",
                                                  "k_ransac_score", "k_ransac_finish", "k_dense_prep",
                                                  "k_dense", "k_dense_reduce", "k_compose"};
 

@@ -45,8 +45,10 @@ struct MatchScratch {
   __half *desc16;          // [F][n_pad][128] unit descriptors (TMA source)
   float *norm;             // [F][n_pad]
   unsigned *maxnorm;       // [F] float bits of max |a|
-  uint2 *rowcand;          // [P][n_pad]           top-2 keys per row
-  uint2 *colcand;          // [P][n_pad/128][n_pad] top-2 keys per column per row tile
+  uint4 *work;             // [2 queues][work_cap] undecided rows: (dir | i << 1, p, k1, k2);
+                           // queue 0: top-2 rescoring, queue 1: full exact scan
+  size_t work_cap;
+  unsigned *work_count;    // [2]
   int32_t *nn_ab, *nn_ba;  // [P][n_max]
   uint8_t *ratio_ok;       // [P][n_max]
 };

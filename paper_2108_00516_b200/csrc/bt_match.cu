@@ -6,23 +6,28 @@
 //
 //  k_desc_prep   per frame and keypoint: |a| (fp32) and the unit descriptor a/|a| in fp16
 //                ([F][n_pad][128], zero padded), plus the frame's max |a| (certificate).
-//  k_match_tc    one CTA per (pair, 128-row tile of frame a).  TMA (128B-swizzled boxes of
-//                64 x 128 fp16) stages the A tile once and B in 256-column chunks; one thread
-//                issues tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = 256, K = 8 x 16) into
-//                a 256-column fp32 TMEM accumulator, S = A_hat . B_hat^T; four epilogue warps
-//                read TMEM with tcgen05.ld (row = TMEM lane = thread), form
-//                d_hat = |a|^2 + |b|^2 - 2 |a||b| S and keep, as packed (sortable value | index)
-//                keys, the two smallest per row (thread-local min/max) and per column (two
-//                redux.sync.min per column per warp, merged across warps in smem).
-//  k_resolve     one warp per row (and per column): the nearest neighbour is certified when
-//                the runner-up's d_hat exceeds the best's by more than twice the bound
-//                eps = 2.2e-3 |a||b|max + 1e-6 (|a|^2 + |b|max^2) (+ key truncation):
-//                fp16 unit vectors have relative error 2^-11 per element, so
-//                |S_hat - S| <= 2^-10 + 128 * 2^-23 (fp32 accumulation, any rounding mode)
-//                ~ 1.0e-3, hence |d_hat - d| <= 2.0e-3 |a||b| + fp32 evaluation error.
-//                Certified rows take the best candidate; every other row (ties, ratio test,
-//                BT_FORCE_FALLBACK) is rescored exactly over all references in fp32 (lane l
-//                owns words [4l, 4l+4), 32 references per step, transpose reduction).
+//  k_match_tc    one CTA per (128-row tile, pair, direction a->b / b->a).  TMA (128B-swizzled
+//                boxes of 64 x 128 fp16) stages the A tile once and B in 128-column chunks,
+//                double buffered (the next chunk's TMA overlaps this chunk's epilogue); one
+//                thread issues tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = 128, K = 8 x 16)
+//                into one of two 128-column fp32 TMEM accumulators, S = A_hat . B_hat^T; two
+//                warpgroups read TMEM with tcgen05.ld (row = TMEM lane, each warpgroup half the
+//                columns), rank d' = |b|^2 - 2 |a||b| S (= d_hat - |a|^2) and keep the three
+//                smallest as packed (order-preserving value | index) keys with a branch-free
+//                min/max network.  Both directions recompute the tile on the tensor cores
+//                rather than reducing columns across lanes.  The epilogue certifies each row
+//                (below) and decides it, or queues it for k_rescore.
+//  certificate   With the bound
+//                eps = 2.2e-3 |a||b|max + 1e-6 (|a|^2 + |b|max^2) (+ key truncation) — fp16 unit
+//                vectors have relative error 2^-11 per element, so |S_hat - S| <= 2^-10 +
+//                128 * 2^-23 (fp32 accumulation, any rounding mode) ~ 1.0e-3 and
+//                |d_hat - d| <= 2.0e-3 |a||b| + fp32 evaluation error — a reference ranked at
+//                position >= L cannot be the nearest neighbour when d'_(L) - d'_(1) > 2 eps:
+//                L = 2 certifies the best candidate; L = 3 leaves the top two, rescored exactly
+//                in fp32; otherwise (ties, ratio test, BT_FORCE_FALLBACK) the row is rescanned
+//                exactly over all references (lane l owns words [4l, 4l+4), 32 references per
+//                step, transpose reduction — the same summation tree as the top-2 rescoring).
+//  k_rescore     persistent warps over the queue of undecided rows (warp per row).
 //  k_mutual      keep (i, NN_ab(i)) iff NN_ba(NN_ab(i)) == i (+ ratio flag), compact ascending.
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -35,8 +40,6 @@ namespace bt {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
-constexpr int kTcThreads = 128;               // 4 epilogue warps = the 128 TMEM lanes
-constexpr int kChunk = 256;                   // B columns per MMA chunk (N)
 constexpr unsigned kNone = 0xFFFFFFFFu;
 
 // ---------------------------------------------------------------- small PTX wrappers
@@ -100,13 +103,7 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
         "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                               \
       : "r"(taddr))
 
-__device__ __forceinline__ unsigned sortable(float f) {
-  const unsigned u = __float_as_uint(f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float unsortable(unsigned k) {
-  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
-}
+__device__ __forceinline__ float key_value(unsigned k) { return __uint_as_float(k); }
 
 // ---------------------------------------------------------------- descriptor prep
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
@@ -142,142 +139,204 @@ struct TcArgs {
   KpView kp;
   const int32_t *pairs;
   MatchScratch S;
-  int n_pad, rt_count, ibits;
+  int n_pad, ibits, P, force_fallback;
+  float ratio2;
 };
 
-constexpr size_t kTcSmem = 1024 /*align*/ + 32768 /*A*/ + 65536 /*B*/ + 4 * kChunk * 8 /*colbuf*/ + kChunk * 8 /*nbv*/;
+constexpr int kTcWarps = 8;                   // 2 warpgroups: each reads all 128 TMEM lanes, half the columns
+constexpr int kN = 128;                       // B columns per MMA chunk (N); B and TMEM double-buffered
+constexpr size_t kTcSmem = 1024 /*align*/ + 32768 /*A*/ + 2 * 32768 /*B x2*/;
 
-__global__ void __launch_bounds__(kTcThreads, 1) k_match_tc(const __grid_constant__ CUtensorMap tmap, TcArgs A) {
+// certificate of a row's packed top-3 keys: 1 = the best is the nearest neighbour, 2 = it is
+// one of the top two, 0 = undecided.  A reference ranked >= L cannot be the nearest
+// neighbour when d'_(L) - d'_(1) > 2 eps + (truncated key bits).
+__device__ __forceinline__ int certify(unsigned k1, unsigned k2, unsigned k3, float qn, float mr, int ibits) {
+  const unsigned imask = (1u << ibits) - 1u;
+  if (k1 == kNone) return 0;
+  if (k2 == kNone) return 1;
+  const float eps2 = 2.f * (2.2e-3f * qn * mr + 1e-6f * (qn * qn + mr * mr));
+  const float v1 = key_value(k1 & ~imask);
+  const float v2 = key_value(k2 & ~imask);
+  // truncated key bits + the rounding of the offset sum: a few ulps of the values compared
+  if ((v2 - v1) > eps2 + ldexpf(fabsf(v1) + fabsf(v2), ibits - 21) + 1e-30f) return 1;
+  if (k3 == kNone) return 2;
+  const float v3 = key_value(k3 & ~imask);
+  if ((v3 - v1) > eps2 + ldexpf(fabsf(v1) + fabsf(v3), ibits - 21) + 1e-30f) return 2;
+  return 0;
+}
+
+// One CTA per (128-row tile, pair, direction).  Direction 0 ranks frame b for each row of
+// frame a, direction 1 frame a for each row of frame b (the Gram tile is recomputed on the
+// tensor cores instead of reducing columns across lanes).  Thread 0 drives TMA and MMA; the
+// other threads wait at CTA barriers, not on the mbarriers.
+__global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_constant__ CUtensorMap tmap, TcArgs A) {
   extern __shared__ uint8_t tc_smem_raw[];
-  __shared__ __align__(8) uint64_t bar_load, bar_mma;
+  __shared__ __align__(8) uint64_t bar_load[2], bar_mma[2];
   __shared__ uint32_t tmem_base_sh;
+  __shared__ __align__(16) float2 cconst[2 * kN];                  // [2][128] (-2|b_j|, |b_j|^2)
+  __shared__ __align__(16) uint4 rmerge[128];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = base;                        // [2 K-atoms][128 rows][128 B]
-  uint8_t *sB = base + 32768;                // [2 K-atoms][256 rows][128 B]
-  uint2 *colbuf = reinterpret_cast<uint2 *>(base + 98304);         // [4 warps][256]
-  float2 *nbv = reinterpret_cast<float2 *>(colbuf + 4 * kChunk);   // [256]
+  uint8_t *sB = base + 32768;                // [2 buffers][2 K-atoms][128 rows][128 B]
 
-  const int p = blockIdx.y, rt = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+  const int dir = blockIdx.z, p = blockIdx.y, rt = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wg = warp >> 2;
+  const int fa = A.pairs[2 * p + dir], fb = A.pairs[2 * p + 1 - dir];
   const int na = min(A.kp.n_kp[fa], A.kp.n_max), nb = min(A.kp.n_kp[fb], A.kp.n_max);
   if (rt * 128 >= na || nb == 0) return;                          // block-uniform
   const int n_pad = A.n_pad;
   const unsigned imask = (1u << A.ibits) - 1u;
+  const int nchunks = (nb + kN - 1) / kN;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(kChunk)
+                 "r"(2 * kN)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  // column constants of chunk c into buffer c & 1
+  auto stage_consts = [&](int c) {
+    for (int jj = tid; jj < kN; jj += kTcWarps * 32) {
+      const int j = c * kN + jj;
+      const float v = j < nb ? A.S.norm[(size_t)fb * n_pad + j] : 0.f;
+      cconst[(c & 1) * kN + jj] = make_float2(-2.f * v, v * v);
+    }
+  };
+  auto load_b = [&](int c) {                                      // thread 0 only
+    mbar_expect_tx(&bar_load[c & 1], (c == 0 ? 32768u : 0u) + 32768u);
+    if (c == 0) {
+      tma_load_2d(sA, &tmap, 0, fa * n_pad + rt * 128, &bar_load[0]);
+      tma_load_2d(sA + 16384, &tmap, 64, fa * n_pad + rt * 128, &bar_load[0]);
+    }
+    uint8_t *dst = sB + (c & 1) * 32768;
+    tma_load_2d(dst, &tmap, 0, fb * n_pad + c * kN, &bar_load[c & 1]);
+    tma_load_2d(dst + 16384, &tmap, 64, fb * n_pad + c * kN, &bar_load[c & 1]);
+  };
   if (tid == 0) {
-    mbar_init(&bar_load, 1);
-    mbar_init(&bar_mma, 1);
+    mbar_init(&bar_load[0], 1); mbar_init(&bar_load[1], 1);
+    mbar_init(&bar_mma[0], 1); mbar_init(&bar_mma[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    load_b(0);
+    if (nchunks > 1) load_b(1);
   }
+  stage_consts(0);
+  if (nchunks > 1) stage_consts(1);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
-  const int i = rt * 128 + tid;                                   // this thread's row (= TMEM lane)
-  const bool row_valid = i < na;
+  const int lrow = (warp & 3) * 32 + lane;                         // TMEM lane = tile row
+  const int i = rt * 128 + lrow;
   const float na_n = A.S.norm[(size_t)fa * n_pad + i];
-  const float na2 = na_n * na_n, m2na = -2.f * na_n;
-  unsigned r1 = kNone, r2 = kNone;
-  // instruction descriptor: D f32, A/B f16, K-major both, N = 256, M = 128
-  const uint32_t idesc = (1u << 4) | ((uint32_t)(kChunk >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  const int nchunks = (nb + kChunk - 1) / kChunk;
-  uint32_t ph_load = 0, ph_mma = 0;
+  // |S_hat| <= 1 + 1e-3, so d' >= -2.002 |a| max|b|: the offset keeps every ranked value >= 0
+  const float c_row = 2.01f * na_n * __uint_as_float(A.S.maxnorm[fb]) + 1e-30f;
+  // rank by d' = d_hat - |a|^2 = |b|^2 - 2 |a||b| S (the row constant does not change the order);
+  // two independent top-3 sets (even / odd columns) halve the min/max dependency chain
+  unsigned r1 = kNone, r2 = kNone, r3 = kNone, s1 = kNone, s2 = kNone, s3 = kNone;
+  // instruction descriptor: D f32, A/B f16, K-major both, N = 128, M = 128
+  const uint32_t idesc = (1u << 4) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 
-  for (int c = 0; c < nchunks; ++c) {
-    for (int jj = tid; jj < kChunk; jj += kTcThreads) {
-      const int j = c * kChunk + jj;
-      const float v = j < nb ? A.S.norm[(size_t)fb * n_pad + j] : 0.f;
-      nbv[jj] = make_float2(v, v * v);
-    }
-    if (tid == 0) {
-      mbar_expect_tx(&bar_load, (c == 0 ? 32768u : 0u) + 65536u);
-      if (c == 0) {
-        tma_load_2d(sA, &tmap, 0, fa * n_pad + rt * 128, &bar_load);
-        tma_load_2d(sA + 16384, &tmap, 64, fa * n_pad + rt * 128, &bar_load);
-      }
-#pragma unroll
-      for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          tma_load_2d(sB + kb * 32768 + h * 16384, &tmap, kb * 64, fb * n_pad + c * kChunk + h * 128, &bar_load);
-    }
-    mbar_wait(&bar_load, ph_load);
-    ph_load ^= 1;
-    __syncthreads();                                              // nbv visible
-    if (tid == 0) {
-      tc_fence_after();
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {                               // K = 128 = 8 x 16
-        const int kb = k >> 2, ks = k & 3;
-        umma_f16(tmem, umma_desc_sw128(sA + kb * 16384 + ks * 32), umma_desc_sw128(sB + kb * 32768 + ks * 32),
-                 idesc, k > 0 ? 1u : 0u);
-      }
-      umma_commit(&bar_mma);
-    }
-    mbar_wait(&bar_mma, ph_mma);
-    ph_mma ^= 1;
+  // software pipeline: MMA(c + 1) is issued before the epilogue of chunk c (two TMEM
+  // accumulators), TMA(c + 2) as soon as MMA(c) has consumed its B buffer
+  auto issue_mma = [&](int c) {                                   // thread 0 only
+    const int b = c & 1;
+    mbar_wait(&bar_load[b], (c >> 1) & 1);
     tc_fence_after();
-    // ---- epilogue: TMEM lane (32 warp + lane) = row i; 32 columns per tcgen05.ld
-#pragma unroll 1
-    for (int cc = 0; cc < kChunk / 32; ++cc) {
-      const int j0 = c * kChunk + cc * 32;
-      if (j0 >= nb) {                                             // uniform: past the last column
-        colbuf[warp * kChunk + cc * 32 + lane] = make_uint2(kNone, kNone);
-        continue;
-      }
-      uint32_t v[32];
-      BT_TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cc * 32), v);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      unsigned cm1 = kNone, cm2 = kNone;
 #pragma unroll
-      for (int col = 0; col < 32; ++col) {
-        const int j = j0 + col;
-        if (j >= nb) break;                                       // uniform
-        const float2 bn = nbv[cc * 32 + col];
-        const float d = __fmaf_rn(m2na * bn.x, __uint_as_float(v[col]), na2 + bn.y);
-        const unsigned key = sortable(d) & ~imask;
-        const unsigned rk = row_valid ? (key | (unsigned)j) : kNone;
-        r2 = min(r2, max(r1, rk));
-        r1 = min(r1, rk);
-        const unsigned ck = row_valid ? (key | (unsigned)i) : kNone;
-        const unsigned m1 = __reduce_min_sync(0xffffffffu, ck);
-        const unsigned m2 = __reduce_min_sync(0xffffffffu, ck == m1 ? kNone : ck);
-        if (lane == col) { cm1 = m1; cm2 = m2; }
+    for (int k = 0; k < 8; ++k) {                                 // K = 128 = 8 x 16
+      const int kb = k >> 2, ks = k & 3;
+      umma_f16(tmem + b * kN, umma_desc_sw128(sA + kb * 16384 + ks * 32),
+               umma_desc_sw128(sB + b * 32768 + kb * 16384 + ks * 32), idesc, k > 0 ? 1u : 0u);
+    }
+    umma_commit(&bar_mma[b]);
+  };
+  if (tid == 0) issue_mma(0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    if (tid == 0) {
+      if (c + 1 < nchunks) issue_mma(c + 1);                      // TMEM buffer (c+1)&1 was drained last round
+      mbar_wait(&bar_mma[buf], (c >> 1) & 1);                     // chunk c accumulated, its B buffer consumed
+      if (c + 2 < nchunks) load_b(c + 2);                         // prefetch into the freed buffer
+      tc_fence_before();
+    }
+    __syncthreads();
+    tc_fence_after();
+    // ---- epilogue: warpgroup wg reads columns [wg*64, wg*64+64) of the chunk
+#pragma unroll 1
+    for (int cc = wg * 2; cc < wg * 2 + 2; ++cc) {
+      const int j0 = c * kN + cc * 32;
+      if (j0 >= nb) break;                                        // warpgroup-uniform
+      uint32_t v[32];
+      BT_TMEM_LD32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(buf * kN + cc * 32), v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const float4 *cb4 = reinterpret_cast<const float4 *>(cconst + buf * kN + cc * 32);
+      const int ncol = nb - j0;                                   // >= 1; < 32 only in the last block
+      const unsigned jbase = (unsigned)j0;
+#pragma unroll
+      for (int col = 0; col < 32; col += 2) {
+        const float4 cb = cb4[col >> 1];                          // columns col, col + 1
+        // d'' = d' + c_row >= 0, so the float bits order like the values
+        const float d0 = __fadd_rn(__fmaf_rn(na_n * cb.x, __uint_as_float(v[col]), cb.y), c_row);
+        const float d1 = __fadd_rn(__fmaf_rn(na_n * cb.z, __uint_as_float(v[col + 1]), cb.w), c_row);
+        unsigned k0 = (__float_as_uint(d0) & ~imask) | (jbase + col);
+        unsigned k1 = (__float_as_uint(d1) & ~imask) | (jbase + col + 1);
+        if (ncol < 32) {                                          // uniform; only the final block
+          if (col >= ncol) k0 = kNone;
+          if (col + 1 >= ncol) k1 = kNone;
+        }
+        const unsigned a3 = min(r3, max(r2, k0)), a2 = min(r2, max(r1, k0));
+        r1 = min(r1, k0); r2 = a2; r3 = a3;
+        const unsigned b3 = min(s3, max(s2, k1)), b2 = min(s2, max(s1, k1));
+        s1 = min(s1, k1); s2 = b2; s3 = b3;
       }
-      colbuf[warp * kChunk + cc * 32 + lane] = make_uint2(cm1, cm2);
     }
     tc_fence_before();
-    __syncthreads();
-    // merge the 4 warps' per-column top-2 (keys are unique: the row index is packed in)
-    for (int jj = tid; jj < kChunk; jj += kTcThreads) {
-      const int j = c * kChunk + jj;
-      if (j >= nb) continue;
-      unsigned a1 = kNone, a2 = kNone;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const uint2 x = colbuf[w * kChunk + jj];
-        if (x.x < a1) { a2 = min(a1, x.y); a1 = x.x; }
-        else a2 = min(a2, x.x);
-      }
-      A.S.colcand[((size_t)p * A.rt_count + rt) * n_pad + j] = make_uint2(a1, a2);
-    }
-    __syncthreads();
+    __syncthreads();                                              // TMEM buffer free for chunk c + 2
+    if (c + 2 < nchunks) stage_consts(c + 2);                     // this buffer's constants are spent
   }
-  if (row_valid) A.S.rowcand[(size_t)p * n_pad + i] = make_uint2(r1, r2);
+  // merge the even/odd sets, then the two warpgroups' top-3; certify; decide the row or queue it
+  {
+    const unsigned ks[3] = {s1, s2, s3};
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const unsigned k = ks[t];
+      const unsigned n3 = min(r3, max(r2, k)), n2 = min(r2, max(r1, k));
+      r1 = min(r1, k); r2 = n2; r3 = n3;
+    }
+  }
+  if (wg == 1) rmerge[lrow] = make_uint4(r1, r2, r3, 0u);
+  __syncthreads();
+  if (wg == 0 && i < na) {
+    const uint4 o = rmerge[lrow];
+    const unsigned ks[3] = {o.x, o.y, o.z};
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const unsigned k = ks[t];
+      const unsigned n3 = min(r3, max(r2, k)), n2 = min(r2, max(r1, k));
+      r1 = min(r1, k);
+      r2 = n2;
+      r3 = n3;
+    }
+    int level = 0;
+    if (!A.force_fallback && A.ratio2 >= 1.f)
+      level = certify(r1, r2, r3, na_n, __uint_as_float(A.S.maxnorm[fb]), A.ibits);
+    const size_t o_nn = (size_t)p * A.kp.n_max + i;
+    if (level == 1) {
+      (dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o_nn] = (int32_t)(r1 & imask);
+      if (dir == 0) A.S.ratio_ok[o_nn] = 1;
+    } else {                                                      // queue: [0] top-2 rescoring, [1] full scan
+      const int qi = level == 2 ? 0 : 1;
+      const unsigned slot = atomicAdd(A.S.work_count + qi, 1u);
+      A.S.work[(size_t)qi * A.S.work_cap + slot] = make_uint4((unsigned)dir | ((unsigned)i << 1), (unsigned)p, r1, r2);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kChunk) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kN) : "memory");
   }
 }
 
@@ -330,66 +389,84 @@ __device__ void exact_scan(const float4 a, const float4 *R, int nr, int lane, fl
   }
 }
 
-struct ResolveArgs {
+// fp32 distance of one reference, summed in exact_scan's order (4 sequential terms per lane,
+// then the lane tree bit 4, 3, 2, 1, 0 — a butterfly builds the same tree)
+__device__ __forceinline__ float exact_one(const float4 a, const float4 *R, int j, int lane) {
+  const float4 b = __ldg(R + (size_t)j * 32 + lane);
+  const float dx = __fsub_rn(a.x, b.x), dy = __fsub_rn(a.y, b.y);
+  const float dz = __fsub_rn(a.z, b.z), dw = __fsub_rn(a.w, b.w);
+  float s = __fmul_rn(dx, dx);
+  s = __fmaf_rn(dy, dy, s);
+  s = __fmaf_rn(dz, dz, s);
+  s = __fmaf_rn(dw, dw, s);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  return s;
+}
+
+struct RescoreArgs {
   KpView kp;
   const int32_t *pairs;
   MatchScratch S;
-  int n_pad, rt_count, ibits, force_fallback;
+  int ibits;
   float ratio2;
 };
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_resolve(ResolveArgs A) {
-  const int dir = blockIdx.z, p = blockIdx.y;
+// blockIdx.y == 0: warps over the top-2 queue (two exact distances per row);
+// blockIdx.y == 1: CTAs over the full-scan queue, the references split across the 8 warps
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_rescore(RescoreArgs A) {
+  __shared__ float sb1[kWarpsPerBlock], sb2[kWarpsPerBlock];
+  __shared__ int sj1[kWarpsPerBlock];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int fq = A.pairs[2 * p + dir], fr = A.pairs[2 * p + 1 - dir];
-  const int nq = min(A.kp.n_kp[fq], A.kp.n_max), nr = min(A.kp.n_kp[fr], A.kp.n_max);
-  const int q = blockIdx.x * kWarpsPerBlock + warp;
-  if (q >= nq) return;                                            // warp-uniform
-  int32_t *nn = dir == 0 ? A.S.nn_ab : A.S.nn_ba;
-  const size_t o = (size_t)p * A.kp.n_max + q;
-  if (nr == 0) {
-    if (lane == 0) { nn[o] = -1; if (dir == 0) A.S.ratio_ok[o] = 1; }
+  const unsigned imask = (1u << A.ibits) - 1u;
+  if (blockIdx.y == 0) {
+    const unsigned n_work = A.S.work_count[0];
+    const int gw = blockIdx.x * kWarpsPerBlock + warp, nw = gridDim.x * kWarpsPerBlock;
+    for (unsigned w = gw; w < n_work; w += nw) {
+      const uint4 it = A.S.work[w];
+      const int dir = it.x & 1, q = (int)(it.x >> 1), p = (int)it.y;
+      const int fq = A.pairs[2 * p + dir], fr = A.pairs[2 * p + 1 - dir];
+      const float4 a = reinterpret_cast<const float4 *>(A.kp.desc + ((size_t)fq * A.kp.n_max + q) * kDim)[lane];
+      const float4 *R = reinterpret_cast<const float4 *>(A.kp.desc + (size_t)fr * A.kp.n_max * kDim);
+      const int ja = (int)(it.z & imask), jb = (int)(it.w & imask);
+      const float da = exact_one(a, R, ja, lane), db = exact_one(a, R, jb, lane);
+      if (lane == 0) {
+        const size_t o = (size_t)p * A.kp.n_max + q;
+        (dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o] = (db < da || (db == da && jb < ja)) ? jb : ja;
+        if (dir == 0) A.S.ratio_ok[o] = 1;
+      }
+    }
     return;
   }
-  const unsigned imask = (1u << A.ibits) - 1u;
-  unsigned k1 = kNone, k2 = kNone;
-  if (dir == 0) {
-    const uint2 c = A.S.rowcand[(size_t)p * A.n_pad + q];
-    k1 = c.x; k2 = c.y;
-  } else {
-    const int rts = (nr + 127) / 128;                              // row tiles of frame a
-    for (int rt = 0; rt < rts; ++rt) {
-      const uint2 x = A.S.colcand[((size_t)p * A.rt_count + rt) * A.n_pad + q];
-      if (x.x < k1) { k2 = min(k1, x.y); k1 = x.x; }
-      else k2 = min(k2, x.x);
-    }
-  }
-  bool certified = false;
-  if (!A.force_fallback && A.ratio2 >= 1.f && k1 != kNone) {
-    if (k2 == kNone) certified = true;                             // a single reference
-    else {
-      const float v1 = unsortable(k1 & ~imask), v2 = unsortable(k2 & ~imask);
-      const float nq_n = A.S.norm[(size_t)fq * A.n_pad + q];
-      const float mr = __uint_as_float(A.S.maxnorm[fr]);
-      const float eps = 2.2e-3f * nq_n * mr + 1e-6f * (nq_n * nq_n + mr * mr);
-      const float trunc = ldexpf(fabsf(v1) + fabsf(v2), A.ibits - 22) + 1e-30f;   // cleared key bits
-      certified = (v2 - v1) > 2.f * eps + trunc;
-    }
-  }
-  int j_best;
-  bool ratio_ok = true;
-  if (certified) {
-    j_best = (int)(k1 & imask);
-  } else {
+  const unsigned n_work = A.S.work_count[1];
+  for (unsigned w = blockIdx.x; w < n_work; w += gridDim.x) {
+    const uint4 it = A.S.work[(size_t)A.S.work_cap + w];
+    const int dir = it.x & 1, q = (int)(it.x >> 1), p = (int)it.y;
+    const int fq = A.pairs[2 * p + dir], fr = A.pairs[2 * p + 1 - dir];
+    const int nr = min(A.kp.n_kp[fr], A.kp.n_max);
     const float4 a = reinterpret_cast<const float4 *>(A.kp.desc + ((size_t)fq * A.kp.n_max + q) * kDim)[lane];
     const float4 *R = reinterpret_cast<const float4 *>(A.kp.desc + (size_t)fr * A.kp.n_max * kDim);
+    // warp w scans references [w*span, (w+1)*span) (span a multiple of 32: same per-column tree)
+    const int span = ((nr + kWarpsPerBlock * 32 - 1) / (kWarpsPerBlock * 32)) * 32;
+    const int j0 = min(nr, warp * span), j1e = min(nr, j0 + span);
     float b1, b2;
-    exact_scan(a, R, nr, lane, b1, j_best, b2);
-    ratio_ok = (A.ratio2 >= 1.f) || (nr < 2) || (b1 < A.ratio2 * b2);
-  }
-  if (lane == 0) {
-    nn[o] = j_best;
-    if (dir == 0) A.S.ratio_ok[o] = ratio_ok;
+    int jb;
+    exact_scan(a, R + (size_t)j0 * 32, j1e - j0, lane, b1, jb, b2);
+    if (lane == 0) { sb1[warp] = b1; sb2[warp] = b2; sj1[warp] = jb < 0 ? -1 : jb + j0; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float B1 = CUDART_INF_F, B2 = CUDART_INF_F;
+      int J1 = -1;
+      for (int w2 = 0; w2 < kWarpsPerBlock; ++w2) {                // ascending index order: ties -> lowest
+        if (sj1[w2] < 0) continue;
+        if (sb1[w2] < B1) { B2 = fminf(B1, sb2[w2]); B1 = sb1[w2]; J1 = sj1[w2]; }
+        else B2 = fminf(B2, sb1[w2]);
+      }
+      const size_t o = (size_t)p * A.kp.n_max + q;
+      (dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o] = J1;
+      if (dir == 0) A.S.ratio_ok[o] = (A.ratio2 >= 1.f) || (nr < 2) || (B1 < A.ratio2 * B2);
+    }
+    __syncthreads();
   }
 }
 
@@ -446,7 +523,8 @@ int match_n_pad(int n_max) { return (n_max + 127) / 128 * 128; }
 size_t match_scratch_bytes(int max_frames, int max_pairs, int n_max) {
   const size_t np = match_n_pad(n_max), F = max_frames, P = max_pairs, rt = np / 128;
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-  return al(F * np * kDim * 2) + al(F * np * 4) + al(F * 4) + al(P * np * 8) + al(P * rt * np * 8) +
+  (void)rt;
+  return al(F * np * kDim * 2) + al(F * np * 4) + al(F * 4) + al(2 * 2 * P * n_max * 16) + al(16) +
          al(P * n_max * 4) * 2 + al(P * n_max);
 }
 
@@ -458,8 +536,10 @@ MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_m
   S.desc16 = (__half *)c;        c += al(F * np * kDim * 2);
   S.norm = (float *)c;           c += al(F * np * 4);
   S.maxnorm = (unsigned *)c;     c += al(F * 4);
-  S.rowcand = (uint2 *)c;        c += al(P * np * 8);
-  S.colcand = (uint2 *)c;        c += al(P * rt * np * 8);
+  S.work = (uint4 *)c;           c += al(2 * 2 * P * n_max * 16);
+  S.work_cap = 2 * P * n_max;
+  S.work_count = (unsigned *)c;  c += al(16);
+  (void)rt;
   S.nn_ab = (int32_t *)c;        c += al(P * n_max * 4);
   S.nn_ba = (int32_t *)c;        c += al(P * n_max * 4);
   S.ratio_ok = (uint8_t *)c;
@@ -483,13 +563,15 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   k_desc_prep<<<dim3((n_pad + kWarpsPerBlock - 1) / kWarpsPerBlock, kp.n_frames), kWarpsPerBlock * 32, 0, s>>>(
       kp, S, n_pad);
   L.end(K_DESC_PREP, s);
-  TcArgs ta{kp, pairs, S, n_pad, rt_count, ibits};
+  const float ratio2 = ratio >= 1.f ? 1.f : ratio * ratio;
+  cudaMemsetAsync(S.work_count, 0, 2 * sizeof(unsigned), s);
+  TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2};
   L.begin(K_MATCH_TC, s);
-  k_match_tc<<<dim3(rt_count, P), kTcThreads, kTcSmem, s>>>(*tmap, ta);
+  k_match_tc<<<dim3(rt_count, P, 2), kTcWarps * 32, kTcSmem, s>>>(*tmap, ta);
   L.end(K_MATCH_TC, s);
-  ResolveArgs ra{kp, pairs, S, n_pad, rt_count, ibits, force_fallback, ratio >= 1.f ? 1.f : ratio * ratio};
+  RescoreArgs ra{kp, pairs, S, ibits, ratio2};
   L.begin(K_RESOLVE, s);
-  k_resolve<<<dim3((kp.n_max + kWarpsPerBlock - 1) / kWarpsPerBlock, P, 2), kWarpsPerBlock * 32, 0, s>>>(ra);
+  k_rescore<<<dim3(2 * 148, 2), kWarpsPerBlock * 32, 0, s>>>(ra);
   L.end(K_RESOLVE, s);
   L.begin(K_MUTUAL, s);
   k_mutual<<<P, 512, 0, s>>>(kp, pairs, S.nn_ab, S.nn_ba, S.ratio_ok, matches, n_matches);
