@@ -148,14 +148,19 @@ __device__ __forceinline__ bool make_hypothesis(int h, uint32_t uid, uint32_t k0
 // ---------------------------------------------------------------- the inlier test
 // Correspondence m as four float4: q0 = (ax, ay, az, bx), q1 = (by, bz, O00, O01),
 // q2 = (O02, O10, O11, O12), q3 = (O20, O21, O22, 0) with O = n_b n_a^T, so that
-// (R n_a) . n_b = <R, O>_F.  Explicit _rn intrinsics: identical bits in every kernel.
-__device__ __forceinline__ bool inlier(const float *T, const float4 q0, const float4 q1,
-                                       const float4 q2, const float4 q3, float delta2, float cosa) {
+// (R n_a) . n_b = <R, O>_F.  The gates are folded into the FMA chains:
+//   d' = |R a + t - b|^2 - delta^2  (< 0: distance gate, 15 FMA-pipe ops),
+//   c' = <R, O> - cos(alpha)        (> 0: normal gate, 9 FFMA).
+// Explicit _rn intrinsics: the scoring and finish kernels compute identical bits.
+__device__ __forceinline__ float dist_term(const float *T, const float4 q0, const float4 q1, float ndelta2) {
   const float ex = __fsub_rn(__fmaf_rn(T[0], q0.x, __fmaf_rn(T[1], q0.y, __fmaf_rn(T[2], q0.z, T[9]))), q0.w);
   const float ey = __fsub_rn(__fmaf_rn(T[3], q0.x, __fmaf_rn(T[4], q0.y, __fmaf_rn(T[5], q0.z, T[10]))), q1.x);
   const float ez = __fsub_rn(__fmaf_rn(T[6], q0.x, __fmaf_rn(T[7], q0.y, __fmaf_rn(T[8], q0.z, T[11]))), q1.y);
-  const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
-  float c = __fmul_rn(T[0], q1.z);
+  return __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmaf_rn(ez, ez, ndelta2)));
+}
+__device__ __forceinline__ float normal_term(const float *T, const float4 q1, const float4 q2, const float4 q3,
+                                             float ncosa) {
+  float c = __fmaf_rn(T[0], q1.z, ncosa);
   c = __fmaf_rn(T[1], q1.w, c);
   c = __fmaf_rn(T[2], q2.x, c);
   c = __fmaf_rn(T[3], q2.y, c);
@@ -164,7 +169,11 @@ __device__ __forceinline__ bool inlier(const float *T, const float4 q0, const fl
   c = __fmaf_rn(T[6], q3.x, c);
   c = __fmaf_rn(T[7], q3.y, c);
   c = __fmaf_rn(T[8], q3.z, c);
-  return (d2 < delta2) & (c > cosa);
+  return c;
+}
+__device__ __forceinline__ bool inlier(const float *T, const float4 q0, const float4 q1, const float4 q2,
+                                       const float4 q3, float ndelta2, float ncosa) {
+  return (dist_term(T, q0, q1, ndelta2) < 0.f) & (normal_term(T, q1, q2, q3, ncosa) > 0.f);
 }
 
 __device__ __forceinline__ void pack_corr(const float *pa, const float *na, const float *pb,
@@ -185,15 +194,20 @@ struct ScoreArgs {
   const int32_t *n_matches;
   int n_hyp, chunk;
   uint32_t k0, k1;
-  float delta2, cosa;
+  float ndelta2, ncosa;
   double tau;
   unsigned long long *best_key;
   int32_t *hyp_counts;
 };
 
-__global__ void __launch_bounds__(kScoreThreads, 2) k_ransac_score(ScoreArgs A) {
+// One CTA = 256 hypotheses of one pair (one per thread: Philox + fp64 solve).  Each warp then
+// scores its 32 hypotheses, 4 at a time in registers, against all correspondences (lane =
+// correspondence, staged in smem, padded to a multiple of 32 with never-inlier sentinels).
+// Per (hypothesis, 32 correspondences) a warp vote skips the normal gate when no lane passes
+// the distance gate — the common case for samples that contain an outlier.
+__global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) {
   extern __shared__ float4 sm4[];
-  const int chunk = A.chunk;
+  const int chunk = A.chunk;                                      // multiple of 32
   float4 *s0 = sm4, *s1 = sm4 + chunk, *s2 = sm4 + 2 * chunk, *s3 = sm4 + 3 * chunk;
   float *hs = reinterpret_cast<float *>(sm4 + 4 * chunk);         // [256][12] hypotheses
   const int p = blockIdx.y;
@@ -210,61 +224,81 @@ __global__ void __launch_bounds__(kScoreThreads, 2) k_ransac_score(ScoreArgs A) 
     if (A.hyp_counts && h < H) A.hyp_counts[(size_t)p * H + h] = -1;
     return;
   }
+  const int nchunks = (M + chunk - 1) / chunk;
+  auto stage = [&](int c0) {
+    const int len = min(chunk, M - c0), len32 = (len + 31) & ~31;
+    for (int k = threadIdx.x; k < len32; k += kScoreThreads) {
+      float4 q0, q1, q2, q3;
+      if (k < len) {
+        const int i = mt[2 * (c0 + k)], j = mt[2 * (c0 + k) + 1];
+        pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
+      } else {                                                    // sentinel: |e|^2 = inf, c' < 0
+        q0 = make_float4(0.f, 0.f, 0.f, 3.0e38f);
+        q1 = q2 = q3 = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      s0[k] = q0; s1[k] = q1; s2[k] = q2; s3[k] = q3;
+    }
+  };
+  if (nchunks == 1) stage(0);                                     // staged once, read by every group
+
   float T[12];
   bool valid = false;
   if (h < H) valid = make_hypothesis(h, A.uid[p], A.k0, A.k1, M, mt, pa_f, pb_f, A.tau, T);
-  if (!valid) {
+  if (!valid) {                                                  // never passes the distance gate
 #pragma unroll
     for (int k = 0; k < 12; ++k) T[k] = 0.f;
+    T[11] = 3.0e38f;
   }
   float4 *hs4 = reinterpret_cast<float4 *>(hs + 12 * threadIdx.x);
   hs4[0] = make_float4(T[0], T[1], T[2], T[3]);
   hs4[1] = make_float4(T[4], T[5], T[6], T[7]);
   hs4[2] = make_float4(T[8], T[9], T[10], T[11]);
+  __syncthreads();
 
-  int acc[32];
+  int mine = 0;                                                   // count of hypothesis warp*32 + lane
+#pragma unroll 1
+  for (int g = 0; g < 8; ++g) {
+    float Th[4][12];
 #pragma unroll
-  for (int c = 0; c < 32; ++c) acc[c] = 0;
-  for (int c0 = 0; c0 < M; c0 += chunk) {
-    const int len = min(chunk, M - c0);
-    __syncthreads();
-    for (int k = threadIdx.x; k < len; k += kScoreThreads) {
-      const int i = mt[2 * (c0 + k)], j = mt[2 * (c0 + k) + 1];
-      float4 q0, q1, q2, q3;
-      pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
-      s0[k] = q0; s1[k] = q1; s2[k] = q2; s3[k] = q3;
+    for (int k = 0; k < 4; ++k) {
+      const float4 *src = reinterpret_cast<const float4 *>(hs + 12 * (warp * 32 + 4 * g + k));
+      const float4 x = src[0], y = src[1], z = src[2];
+      Th[k][0] = x.x; Th[k][1] = x.y; Th[k][2] = x.z; Th[k][3] = x.w;
+      Th[k][4] = y.x; Th[k][5] = y.y; Th[k][6] = y.z; Th[k][7] = y.w;
+      Th[k][8] = z.x; Th[k][9] = z.y; Th[k][10] = z.z; Th[k][11] = z.w;
     }
-    __syncthreads();
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      float Th[4][12];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float4 *src = reinterpret_cast<const float4 *>(hs + 12 * (warp * 32 + 4 * g + k));
-        const float4 x = src[0], y = src[1], z = src[2];
-        Th[k][0] = x.x; Th[k][1] = x.y; Th[k][2] = x.z; Th[k][3] = x.w;
-        Th[k][4] = y.x; Th[k][5] = y.y; Th[k][6] = y.z; Th[k][7] = y.w;
-        Th[k][8] = z.x; Th[k][9] = z.y; Th[k][10] = z.z; Th[k][11] = z.w;
+    int acc[4] = {0, 0, 0, 0};
+    for (int c0 = 0; c0 < M; c0 += chunk) {
+      if (nchunks > 1) {
+        __syncthreads();
+        stage(c0);
+        __syncthreads();
       }
-      for (int m = lane; m < len; m += 32) {
-        const float4 q0 = s0[m], q1 = s1[m], q2 = s2[m], q3 = s3[m];
+      const int len32 = (min(chunk, M - c0) + 31) & ~31;
+#pragma unroll 2
+      for (int m0 = 0; m0 < len32; m0 += 32) {
+        const int m = m0 + lane;
+        const float4 q0 = s0[m], q1 = s1[m];
+        bool pd[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[4 * g + k] += inlier(Th[k], q0, q1, q2, q3, A.delta2, A.cosa);
+        for (int k = 0; k < 4; ++k) pd[k] = dist_term(Th[k], q0, q1, A.ndelta2) < 0.f;
+        if (__any_sync(0xffffffffu, pd[0] | pd[1] | pd[2] | pd[3])) {
+          const float4 q2 = s2[m], q3 = s3[m];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (__any_sync(0xffffffffu, pd[k])) acc[k] += pd[k] & (normal_term(Th[k], q1, q2, q3, A.ncosa) > 0.f);
+        }
       }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int t = acc[k];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 4 * g + k) mine = t;
     }
   }
-  // transpose reduction: lane l ends with the total of acc[l] (= hypothesis warp*32 + l)
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool upper = (lane & o) != 0;
-#pragma unroll
-    for (int c = 0; c < o; ++c) {
-      const int send = upper ? acc[c] : acc[c + o];
-      const int keep = upper ? acc[c + o] : acc[c];
-      acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-  const int count = valid ? acc[0] : -1;
+  const int count = valid ? mine : -1;
   unsigned long long key = 0ull;
   if (h < H) {
     if (A.hyp_counts) A.hyp_counts[(size_t)p * H + h] = count;
@@ -379,7 +413,7 @@ struct FinishArgs {
   const int32_t *n_matches;
   int n_hyp, min_inliers;
   uint32_t k0, k1;
-  float delta2, cosa;
+  float ndelta2, ncosa;
   double tau;
   const unsigned long long *best_key;
   uint32_t *records;
@@ -443,7 +477,7 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
       const int i = mt[2 * m], j = mt[2 * m + 1];
       float4 q0, q1, q2, q3;
       pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
-      in = inlier(T, q0, q1, q2, q3, A.delta2, A.cosa);
+      in = inlier(T, q0, q1, q2, q3, A.ndelta2, A.ncosa);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, in);
     if (lane == 0) {
@@ -615,7 +649,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
                    int32_t *hyp_counts, const bt_pose *node_pose, float huber, cudaStream_t s,
                    Launch &L) {
   if (P <= 0) return;
-  const int chunk = kp.n_max < kMaxChunk ? ((kp.n_max + 31) / 32) * 32 : kMaxChunk;
+  const int chunk = kp.n_max < kMaxChunk ? ((kp.n_max + 31) / 32) * 32 : kMaxChunk;   // multiple of 32
   const size_t smem = (size_t)4 * chunk * sizeof(float4) + (size_t)kScoreThreads * 12 * sizeof(float);
   static bool attr_done = false;
   if (!attr_done) {
@@ -628,8 +662,8 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   a.kp = kp; a.pairs = pairs; a.uid = uid; a.matches = matches; a.n_matches = n_matches;
   a.n_hyp = prm.n_hyp; a.chunk = chunk;
   a.k0 = (uint32_t)(prm.seed & 0xffffffffull); a.k1 = (uint32_t)(prm.seed >> 32);
-  a.delta2 = (float)((double)prm.delta_m * (double)prm.delta_m);
-  a.cosa = prm.cos_alpha;
+  a.ndelta2 = (float)(-(double)prm.delta_m * (double)prm.delta_m);
+  a.ncosa = -prm.cos_alpha;
   a.tau = prm.min_sigma_ratio;
   a.best_key = best_key;
   a.hyp_counts = hyp_counts;
@@ -640,7 +674,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   FinishArgs f;
   f.kp = kp; f.pairs = pairs; f.uid = uid; f.matches = matches; f.n_matches = n_matches;
   f.n_hyp = prm.n_hyp; f.min_inliers = prm.min_inliers;
-  f.k0 = a.k0; f.k1 = a.k1; f.delta2 = a.delta2; f.cosa = a.cosa; f.tau = a.tau;
+  f.k0 = a.k0; f.k1 = a.k1; f.ndelta2 = a.ndelta2; f.ncosa = a.ncosa; f.tau = a.tau;
   f.best_key = best_key; f.records = records; f.rec_stride = rec_stride;
   f.node_pose = node_pose; f.huber = huber;
   L.begin(K_RANSAC_FINISH, s);
