@@ -423,7 +423,7 @@ struct FinishArgs {
 };
 
 constexpr int kFinThreads = 256;
-constexpr int kFeatChunk = 64;
+constexpr int kFeatChunk = 512;                  // feature rows staged per pass (smem)
 // per-inlier feature data staged in smem: e(3) J(3x12) w rho
 constexpr int kFeatRow = 3 + 36 + 2;
 
@@ -431,7 +431,6 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   extern __shared__ int inl[];                     // [n_max] inlier match indices, in order
   __shared__ float Tb[12];
   __shared__ double red[(kFinThreads / 32) * 9];
-  __shared__ double fstage[kFeatChunk * kFeatRow];
   __shared__ int wcnt[kFinThreads / 32];
   __shared__ double shT[12];
   __shared__ int sh_status;
@@ -560,85 +559,105 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   }
   if (A.node_pose == nullptr) return;
 
-  // ---- Eq. (2) feature edge at the node poses, fp64, fixed-order reduction ----------
-  // e = R_i^T (p_m - t_i) - R_j^T (p_n - t_j);  J_i = -R_i^T [I | -[p_m]x],
-  // J_j = R_j^T [I | -[p_n]x];  H += w J^T J, g += w J^T e, E += rho(|e|).
+  // ---- Eq. (2) feature edge at the node poses ------------------------------------
+  // e = R_i^T (p_m - t_i) - R_j^T (p_n - t_j) (fp64: it cancels ~0.5 m coordinates);
+  // J_i = -R_i^T [I | -[p_m]x], J_j = R_j^T [I | -[p_n]x];  H += w J^T J, g += w J^T e,
+  // E += rho(|e|).  Every thread builds rows (fp32 after the fp64 residual) into smem; warp w
+  // accumulates rows w, w + 8, ... for outputs lane, lane + 32, lane + 64; a fixed-order
+  // combine over the 8 warps keeps the result bitwise deterministic.
+  float *frow = reinterpret_cast<float *>(inl + ((n_max + 3) & ~3));   // [kFeatChunk][kFeatRow]
+  __shared__ float fpart[kFinThreads / 32][96];
   double Ri[9], ti[3], Rj[9], tj[3];
   {
     const bt_pose Pi = A.node_pose[fa], Pj = A.node_pose[fb];
     for (int k = 0; k < 9; ++k) { Ri[k] = Pi.R[k]; Rj[k] = Pj.R[k]; }
     for (int k = 0; k < 3; ++k) { ti[k] = Pi.t[k]; tj[k] = Pj.t[k]; }
   }
-  // output entry owned by this thread (tid < 92): (a, b) of the 12x12 H, or g / E / count
-  int oa = -1, ob = -1, kind = -1;   // kind 0: H(a,b)  1: g(a)  2: E  3: count
-  {
-    int k = tid;
+  // the three outputs of this lane: kind 0 H(a,b), 1 g(a), 2 E, 3 count, -1 none
+  int okind[3], oa[3], ob[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    int k = lane + 32 * s;
+    okind[s] = -1; oa[s] = ob[s] = 0;
     if (k < 21) {                      // H_ii upper
       int a = 0;
       while (k >= 6 - a) { k -= 6 - a; ++a; }
-      oa = a; ob = a + k; kind = 0;
+      oa[s] = a; ob[s] = a + k; okind[s] = 0;
     } else if (k < 57) {               // H_ij
-      k -= 21; oa = k / 6; ob = 6 + k % 6; kind = 0;
+      k -= 21; oa[s] = k / 6; ob[s] = 6 + k % 6; okind[s] = 0;
     } else if (k < 78) {               // H_jj upper
       k -= 57;
       int a = 0;
       while (k >= 6 - a) { k -= 6 - a; ++a; }
-      oa = 6 + a; ob = 6 + a + k; kind = 0;
-    } else if (k < 90) { oa = k - 78; kind = 1; }
-    else if (k == 90) kind = 2;
-    else if (k == 91) kind = 3;
+      oa[s] = 6 + a; ob[s] = 6 + a + k; okind[s] = 0;
+    } else if (k < 90) { oa[s] = k - 78; okind[s] = 1; }
+    else if (k == 90) okind[s] = 2;
+    else if (k == 91) okind[s] = 3;
   }
-  double acc = 0.0;
+  float acc[3] = {0.f, 0.f, 0.f};
   const int n_feat = best_h >= 0 ? best_count : 0;     // C_ij = inliers of h*, whatever the status
   for (int done = 0; done < n_feat; done += kFeatChunk) {
+    const int nc = min(kFeatChunk, n_feat - done);
     __syncthreads();
-    if (tid < kFeatChunk && done + tid < n_feat) {
-      const int m = inl[done + tid];
+    for (int r = tid; r < nc; r += kFinThreads) {
+      const int m = inl[done + r];
       const int i = mt[2 * m], j = mt[2 * m + 1];
       const double pm[3] = {pa_f[3 * i], pa_f[3 * i + 1], pa_f[3 * i + 2]};
       const double pn[3] = {pb_f[3 * j], pb_f[3 * j + 1], pb_f[3 * j + 2]};
-      double *row = fstage + tid * kFeatRow;
+      float *row = frow + r * kFeatRow;
       double e[3];
-      for (int r = 0; r < 3; ++r) {
-        e[r] = Ri[r] * (pm[0] - ti[0]) + Ri[3 + r] * (pm[1] - ti[1]) + Ri[6 + r] * (pm[2] - ti[2]) -
-               (Rj[r] * (pn[0] - tj[0]) + Rj[3 + r] * (pn[1] - tj[1]) + Rj[6 + r] * (pn[2] - tj[2]));
-        row[r] = e[r];
-      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        e[q] = Ri[q] * (pm[0] - ti[0]) + Ri[3 + q] * (pm[1] - ti[1]) + Ri[6 + q] * (pm[2] - ti[2]) -
+               (Rj[q] * (pn[0] - tj[0]) + Rj[3 + q] * (pn[1] - tj[1]) + Rj[6 + q] * (pn[2] - tj[2]));
       const double Sp[9] = {0, -pm[2], pm[1], pm[2], 0, -pm[0], -pm[1], pm[0], 0};
       const double Sq[9] = {0, -pn[2], pn[1], pn[2], 0, -pn[0], -pn[1], pn[0], 0};
-      for (int r = 0; r < 3; ++r) {
-        // (R^T)[r][c] = R[c][r];  (R^T [p]x)[r][c] = sum_k R[k][r] S[k][c]
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        row[q] = (float)e[q];
+        // (R^T)[q][c] = R[c][q];  (R^T [p]x)[q][c] = sum_k R[k][q] S[k][c]
+#pragma unroll
         for (int c = 0; c < 3; ++c) {
-          row[3 + 12 * r + c] = -Ri[3 * c + r];
-          row[3 + 12 * r + 6 + c] = Rj[3 * c + r];
+          row[3 + 12 * q + c] = (float)-Ri[3 * c + q];
+          row[3 + 12 * q + 6 + c] = (float)Rj[3 * c + q];
           double x = 0, y = 0;
-          for (int k = 0; k < 3; ++k) { x += Ri[3 * k + r] * Sp[3 * k + c]; y += Rj[3 * k + r] * Sq[3 * k + c]; }
-          row[3 + 12 * r + 3 + c] = x;
-          row[3 + 12 * r + 9 + c] = -y;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) { x += Ri[3 * k + q] * Sp[3 * k + c]; y += Rj[3 * k + q] * Sq[3 * k + c]; }
+          row[3 + 12 * q + 3 + c] = (float)x;
+          row[3 + 12 * q + 9 + c] = (float)-y;
         }
       }
       const double nrm = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
       double w, rho;
       if (nrm <= A.huber) { w = 1.0; rho = 0.5 * nrm * nrm; }
       else { w = A.huber / nrm; rho = A.huber * (nrm - 0.5 * A.huber); }
-      row[39] = w;
-      row[40] = rho;
+      row[39] = (float)w;
+      row[40] = (float)rho;
     }
     __syncthreads();
-    if (kind >= 0) {
-      const int nc = min(kFeatChunk, n_feat - done);
-      for (int c = 0; c < nc; ++c) {
-        const double *row = fstage + c * kFeatRow;
-        const double *J = row + 3;
-        if (kind == 0) acc += row[39] * (J[oa] * J[ob] + J[12 + oa] * J[12 + ob] + J[24 + oa] * J[24 + ob]);
-        else if (kind == 1) acc += row[39] * (J[oa] * row[0] + J[12 + oa] * row[1] + J[24 + oa] * row[2]);
-        else if (kind == 2) acc += row[40];
-        else acc += 1.0;
+    for (int r = warp; r < nc; r += kFinThreads / 32) {
+      const float *row = frow + r * kFeatRow;
+      const float *J = row + 3;
+      const float w = row[39];
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int a = oa[s], b = ob[s];
+        if (okind[s] == 0) acc[s] = fmaf(w, J[a] * J[b] + J[12 + a] * J[12 + b] + J[24 + a] * J[24 + b], acc[s]);
+        else if (okind[s] == 1) acc[s] = fmaf(w, J[a] * row[0] + J[12 + a] * row[1] + J[24 + a] * row[2], acc[s]);
+        else if (okind[s] == 2) acc[s] += row[40];
+        else if (okind[s] == 3) acc[s] += 1.f;
       }
     }
   }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) fpart[warp][lane + 32 * s] = acc[s];
+  __syncthreads();
   const int fo = rec_feat(n_max);
-  if (tid < 96) rec[fo + tid] = __float_as_uint(kind >= 0 ? (float)acc : 0.f);
+  if (tid < 96) {
+    float t = 0.f;
+    for (int w = 0; w < kFinThreads / 32; ++w) t += fpart[w][tid];
+    rec[fo + tid] = __float_as_uint(tid < 92 ? t : 0.f);
+  }
 }
 
 }  // namespace
@@ -678,7 +697,14 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   f.best_key = best_key; f.records = records; f.rec_stride = rec_stride;
   f.node_pose = node_pose; f.huber = huber;
   L.begin(K_RANSAC_FINISH, s);
-  k_ransac_finish<<<P, kFinThreads, (size_t)mask_words(kp.n_max) * 32 * sizeof(int), s>>>(f);
+  const size_t fin_smem = (size_t)((mask_words(kp.n_max) * 32 + 3) & ~3) * sizeof(int) +
+                          (node_pose ? (size_t)kFeatChunk * kFeatRow * sizeof(float) : 0);
+  static size_t fin_attr = 0;
+  if (fin_smem > fin_attr) {
+    cudaFuncSetAttribute(k_ransac_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fin_smem);
+    fin_attr = fin_smem;
+  }
+  k_ransac_finish<<<P, kFinThreads, fin_smem, s>>>(f);
   L.end(K_RANSAC_FINISH, s);
 }
 
