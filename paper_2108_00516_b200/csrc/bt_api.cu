@@ -18,6 +18,8 @@ struct bt_ctx {
   bool sticky = false;
   char err[512] = {0};
   bt::Launch launch;                          // kernels enqueued by the current / last call
+  cudaStream_t side = nullptr;                // dense Eq.(3) path runs here, overlapping match + RANSAC
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // per-kernel event timing (bt_profile_*)
   struct Pending { int kid; cudaEvent_t start, stop; };
   bool prof_on = false;
@@ -164,6 +166,12 @@ bt_status bt_create(bt_ctx **out, int cuda_device) {
   bt_ctx *c = new (std::nothrow) bt_ctx;
   if (!c) return BT_ENOMEM;
   c->device = cuda_device;
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    return BT_ECUDA;
+  }
   const char *ff = getenv("BT_FORCE_FALLBACK");
   c->force_fallback = ff && ff[0] && ff[0] != '0';
   *out = c;
@@ -176,6 +184,9 @@ void bt_destroy(bt_ctx *c) {
   cudaDeviceSynchronize();
   for (auto &p : c->pending) { cudaEventDestroy(p.start); if (p.stop) cudaEventDestroy(p.stop); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   free_scratch(c);
   delete c;
 }
@@ -296,13 +307,22 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
                                     uint32_t *records, cudaStream_t st) {
   const int rw = bt::rec_words(kp->n_max);
   const float ratio = mprm ? mprm->ratio : 1.f;
+  // fork: the dense edges only need the maps and node poses, so they run on the side stream
+  // while matching and RANSAC run on the caller's stream (event fork / join: capturable)
+  if (eprm) {
+    cudaEventRecord(c->ev_fork, st);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, nullptr, 0, records, rw,
+                     bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch);
+  }
   bt::launch_match(kview(kp), pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches, c->n_matches,
                    st, c->launch);
   bt::launch_ransac(kview(kp), pairs, uid, P, c->matches, c->n_matches, *rprm, c->best_key, records, rw, nullptr,
                     eprm ? node_pose : nullptr, eprm ? eprm->huber_m : 0.f, st, c->launch);
-  if (eprm)
-    bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, nullptr, 0, records, rw,
-                     bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), st, c->launch);
+  if (eprm) {
+    cudaEventRecord(c->ev_join, c->side);
+    cudaStreamWaitEvent(st, c->ev_join, 0);
+  }
   return after_launch(c, "bt_register_pairs");
 }
 

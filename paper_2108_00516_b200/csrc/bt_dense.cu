@@ -136,16 +136,15 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
   for (int k = 0; k < kPer; ++k) { in[k] = false; dep[k] = 0.f; nr[3 * k] = nr[3 * k + 1] = nr[3 * k + 2] = 0.f; }
   if (v < H) {
     if ((W & 3) == 0 && u0 + kPer <= W) {
-      const uchar4 m4 = *reinterpret_cast<const uchar4 *>(A.mp.mask + off + pix0);
-      if (m4.x | m4.y | m4.z | m4.w) {
-        const float4 d4 = *reinterpret_cast<const float4 *>(A.mp.depth + off + pix0);
-        const float4 *n4 = reinterpret_cast<const float4 *>(A.mp.normal + 3 * (off + pix0));
-        const float4 a = n4[0], b = n4[1], c = n4[2];
-        dep[0] = d4.x; dep[1] = d4.y; dep[2] = d4.z; dep[3] = d4.w;
-        nr[0] = a.x; nr[1] = a.y; nr[2] = a.z; nr[3] = a.w; nr[4] = b.x; nr[5] = b.y;
-        nr[6] = b.z; nr[7] = b.w; nr[8] = c.x; nr[9] = c.y; nr[10] = c.z; nr[11] = c.w;
-        in[0] = m4.x != 0; in[1] = m4.y != 0; in[2] = m4.z != 0; in[3] = m4.w != 0;
-      }
+      // mask, depth and normals requested together (one memory round trip, not two)
+      const uchar4 m4 = __ldg(reinterpret_cast<const uchar4 *>(A.mp.mask + off + pix0));
+      const float4 d4 = __ldg(reinterpret_cast<const float4 *>(A.mp.depth + off + pix0));
+      const float4 *n4 = reinterpret_cast<const float4 *>(A.mp.normal + 3 * (off + pix0));
+      const float4 a = __ldg(n4), b = __ldg(n4 + 1), c = __ldg(n4 + 2);
+      dep[0] = d4.x; dep[1] = d4.y; dep[2] = d4.z; dep[3] = d4.w;
+      nr[0] = a.x; nr[1] = a.y; nr[2] = a.z; nr[3] = a.w; nr[4] = b.x; nr[5] = b.y;
+      nr[6] = b.z; nr[7] = b.w; nr[8] = c.x; nr[9] = c.y; nr[10] = c.z; nr[11] = c.w;
+      in[0] = m4.x != 0; in[1] = m4.y != 0; in[2] = m4.z != 0; in[3] = m4.w != 0;
     } else {
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
@@ -217,7 +216,8 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
   if (threadIdx.x == 0) A.counts[(size_t)f * A.tiles + t] = total;
 }
 
-constexpr size_t kDenseSmem = kTile * (16 + 16 + 8 + 24) + (kDenseThreads / 32) * 32 * 4;
+constexpr int kEdgeBatch = 16;                // edges whose per-warp partials are held before one CTA barrier
+constexpr size_t kDenseSmem = kTile * (16 + 16 + 8 + 24) + (kDenseThreads / 32) * kEdgeBatch * 32 * 4;
 
 __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
   float4 *sN = sP + kTile;                                         // n_i (camera), n_o,i.x
   float2 *sNo = reinterpret_cast<float2 *>(sN + kTile);            // n_o,i.y, n_o,i.z
   double *sX = reinterpret_cast<double *>(sNo + kTile);            // p - t_i (fp64)
-  float (*red)[32] = reinterpret_cast<float (*)[32]>(sX + 3 * kTile);
+  float *red = reinterpret_cast<float *>(sX + 3 * kTile);          // [warp][kEdgeBatch][32]
   const int f = blockIdx.y, t = blockIdx.x;
   const int n = A.counts[(size_t)f * A.tiles + t];
   const int ne = A.ecount[f];
@@ -257,32 +257,31 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  for (int ie = 0; ie < ne; ++ie) {
-    const int e = A.elist[(size_t)f * A.E + ie];
-    int fi, fj;
-    edge_frames(A.edges, A.pairs, e, fi, fj);
-    float T[12];
+  for (int ie0 = 0; ie0 < ne; ie0 += kEdgeBatch) {
+    const int nb_e = min(kEdgeBatch, ne - ie0);
+    for (int ib = 0; ib < nb_e; ++ib) {                           // warps run through the batch independently
+      const int e = A.elist[(size_t)f * A.E + ie0 + ib];
+      int fi, fj;
+      edge_frames(A.edges, A.pairs, e, fi, fj);
+      const float *T = A.tji + 12 * e;
+      const size_t off_j = (size_t)fj * npx;
+      const uint8_t *vm = A.vmap + off_j;
+      const float4 *pm = reinterpret_cast<const float4 *>(A.pmap + off_j);
+      float acc[32];
 #pragma unroll
-    for (int k = 0; k < 12; ++k) T[k] = __ldg(A.tji + 12 * e + k);
-    const size_t off_j = (size_t)fj * npx;
-    const uint8_t *vm = A.vmap + off_j;
-    const float4 *pm = reinterpret_cast<const float4 *>(A.pmap + off_j);
-    float acc[32];
+      for (int k = 0; k < 32; ++k) acc[k] = 0.f;
+      // phase 1: project every entry of this thread; phase 2: issue all of its gathers;
+      // phase 3: gates, residual, accumulation
+      int tj[kPer];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) acc[k] = 0.f;
-#pragma unroll
-    for (int half = 0; half < kPer; half += 2) {
-      // phase 1: project two entries; phase 2: issue their gathers together; phase 3: compute
-      int tj[2];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int k = threadIdx.x + (half + s) * kDenseThreads;
+      for (int s = 0; s < kPer; ++s) {
+        const int k = threadIdx.x + s * kDenseThreads;
         tj[s] = -1;
         if (k < n) {
           const float4 a = sP[k];
-          const float yx = fmaf(T[0], a.x, fmaf(T[1], a.y, fmaf(T[2], a.z, T[9])));
-          const float yy = fmaf(T[3], a.x, fmaf(T[4], a.y, fmaf(T[5], a.z, T[10])));
-          const float yz = fmaf(T[6], a.x, fmaf(T[7], a.y, fmaf(T[8], a.z, T[11])));
+          const float yx = fmaf(__ldg(T + 0), a.x, fmaf(__ldg(T + 1), a.y, fmaf(__ldg(T + 2), a.z, __ldg(T + 9))));
+          const float yy = fmaf(__ldg(T + 3), a.x, fmaf(__ldg(T + 4), a.y, fmaf(__ldg(T + 5), a.z, __ldg(T + 10))));
+          const float yz = fmaf(__ldg(T + 6), a.x, fmaf(__ldg(T + 7), a.y, fmaf(__ldg(T + 8), a.z, __ldg(T + 11))));
           if (yz > 0.f) {
             const float iz = __fdividef(1.0f, yz);
             const float up = fmaf(A.fx * yx, iz, A.cx), vp = fmaf(A.fy * yy, iz, A.cy);
@@ -291,22 +290,21 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
           }
         }
       }
-      bool gv[2];
-      float4 g0[2], g1[2], g2[2];
+      bool gv[kPer];
+      float4 g0[kPer], g1[kPer], g2[kPer];
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        gv[s] = tj[s] >= 0 && __ldg(vm + tj[s]) != 0;
-        if (gv[s]) {
-          const float4 *q4 = pm + 3 * (size_t)tj[s];
-          g0[s] = __ldg(q4);
-          g1[s] = __ldg(q4 + 1);
-          g2[s] = __ldg(q4 + 2);
-        }
+      for (int s = 0; s < kPer; ++s) {                             // validity and map entry together
+        const int tt = tj[s] < 0 ? 0 : tj[s];
+        const float4 *q4 = pm + 3 * (size_t)tt;
+        gv[s] = tj[s] >= 0 && __ldg(vm + tt) != 0;
+        g0[s] = __ldg(q4);
+        g1[s] = __ldg(q4 + 1);
+        g2[s] = __ldg(q4 + 2);
       }
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < kPer; ++s) {
         if (!gv[s]) continue;
-        const int k = threadIdx.x + (half + s) * kDenseThreads;
+        const int k = threadIdx.x + s * kDenseThreads;
         // target map entry: x_s = R_j^T (s - t_j) (fp64), n_o,j (fp32)
         const double xs0 = __hiloint2double(__float_as_int(g0[s].y), __float_as_int(g0[s].x));
         const double xs1 = __hiloint2double(__float_as_int(g0[s].w), __float_as_int(g0[s].z));
@@ -341,47 +339,57 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
         acc[27] += rho;
         acc[28] += 1.f;
       }
-    }
-    // warp transpose reduction: lane l ends with the warp total of acc[l]
+      // warp transpose reduction: lane l ends with the warp total of acc[l]
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      const bool upper = (lane & o) != 0;
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool upper = (lane & o) != 0;
 #pragma unroll
-      for (int c = 0; c < o; ++c) {
-        const float send = upper ? acc[c] : acc[c + o];
-        const float keep = upper ? acc[c + o] : acc[c];
-        acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        for (int c = 0; c < o; ++c) {
+          const float send = upper ? acc[c] : acc[c + o];
+          const float keep = upper ? acc[c + o] : acc[c];
+          acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
       }
+      red[(warp * kEdgeBatch + ib) * 32 + lane] = acc[0];
     }
-    red[warp][lane] = acc[0];
     __syncthreads();
-    if (warp == 0) {
+    // CTA partial of each edge of the batch: fixed-order sum over the 8 warps
+    for (int x = threadIdx.x; x < nb_e * 32; x += kDenseThreads) {
+      const int ib = x >> 5, l = x & 31;
       float s = 0.f;
 #pragma unroll
-      for (int w2 = 0; w2 < kDenseThreads / 32; ++w2) s += red[w2][lane];
-      A.partials[((size_t)e * A.tiles + t) * kPartStride + lane] = s;
+      for (int w2 = 0; w2 < kDenseThreads / 32; ++w2) s += red[(w2 * kEdgeBatch + ib) * 32 + l];
+      const int e = A.elist[(size_t)f * A.E + ie0 + ib];
+      A.partials[((size_t)e * A.tiles + t) * kPartStride + l] = s;
     }
     __syncthreads();
   }
 }
 
-__global__ void k_dense_reduce(const float *__restrict__ partials, const int32_t *__restrict__ counts, int tiles,
-                               const int32_t *edges, const int32_t *pairs, float *out, int out_stride,
-                               uint32_t *records, int rec_stride, int off_ij, int off_ji) {
+__global__ void __launch_bounds__(256) k_dense_reduce(const float *__restrict__ partials, const int32_t *__restrict__ counts,
+                                                       int tiles, const int32_t *edges, const int32_t *pairs, float *out,
+                                                       int out_stride, uint32_t *records, int rec_stride, int off_ij,
+                                                       int off_ji) {
+  __shared__ double wsum[8][32];
   const int e = blockIdx.x;
-  const int k = threadIdx.x;                  // 32 threads
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int fi, fj;
   edge_frames(edges, pairs, e, fi, fj);
-  double s = 0.0;
-  if (k < kAcc)
-    for (int t = 0; t < tiles; ++t)
-      if (counts[(size_t)fi * tiles + t] > 0) s += (double)partials[((size_t)e * tiles + t) * kPartStride + k];
-  const float v = k < kAcc ? (float)s : 0.f;
+  double s = 0.0;                                 // warp w: tiles w, w + 8, ... in order; lane = value
+  for (int t = warp; t < tiles; t += 8)
+    if (counts[(size_t)fi * tiles + t] > 0) s += (double)partials[((size_t)e * tiles + t) * kPartStride + lane];
+  wsum[warp][lane] = s;
+  __syncthreads();
+  if (warp != 0) return;
+  double tsum = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tsum += wsum[w][lane];
+  const float v = lane < kAcc ? (float)tsum : 0.f;
   if (records) {
     const int p = e >> 1;
-    records[(size_t)p * rec_stride + ((e & 1) ? off_ji : off_ij) + k] = __float_as_uint(v);
+    records[(size_t)p * rec_stride + ((e & 1) ? off_ji : off_ij) + lane] = __float_as_uint(v);
   } else {
-    out[(size_t)e * out_stride + k] = v;
+    out[(size_t)e * out_stride + lane] = v;
   }
 }
 
@@ -463,7 +471,7 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   k_dense<<<dim3(a.tiles, mp.n_frames), kDenseThreads, kDenseSmem, s>>>(a);
   L.end(K_DENSE, s);
   L.begin(K_DENSE_REDUCE, s);
-  k_dense_reduce<<<E, 32, 0, s>>>(a.partials, a.counts, a.tiles, edges, pairs, out, out_stride, records,
+  k_dense_reduce<<<E, 256, 0, s>>>(a.partials, a.counts, a.tiles, edges, pairs, out, out_stride, records,
                                   rec_stride, rec_off_ij, rec_off_ji);
   L.end(K_DENSE_REDUCE, s);
 }
