@@ -32,7 +32,10 @@ import synth  # noqa: E402
 METRIC = "frame-pairs registered/sec + RANSAC hypotheses/sec at 1/2/4/8 B200 vs roofline"
 UNIT = "pairs/s"
 N_FRAMES, N_KP, N_MAX, N_HYP, W, H = 16, 500, 512, 4096, 640, 480
-FLOPS_PER_TEST = 43          # 9 FMA + 3 FMA(t) ... per (hypothesis, correspondence)
+# per (hypothesis, correspondence) test the distance gate |R a + t - b|^2 < delta^2
+# is 27 flop (9 FMA + 3 sub + 3 FMA); the normal gate <R, n_b n_a^T> > cos(alpha) is 18 flop
+# and is only needed where the distance gate passes (short-circuit AND)
+FLOPS_DIST, FLOPS_NORMAL = 27, 18
 SM_COUNT, FP32_LANES = 148, 128
 
 
@@ -183,6 +186,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2108_00516_b200 as bt
+    from paper_2108_00516_b200 import parallel
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -201,7 +205,6 @@ def main():
     t_pose = torch.from_numpy(poses).to(dev)
     rw = bt.record_words(N_MAX)
     rec = torch.zeros((P, rw), dtype=torch.int32, device=dev)
-    all_rec = torch.zeros((world * P, rw), dtype=torch.int32, device=dev) if world > 1 else None
     ctx = bt.Context(local)
     ctx.reserve(P, N_MAX, N_HYP, N_FRAMES, W, H)
     rprm = bt.ransac_params(N_HYP, synth.PHILOX_SEED)
@@ -211,8 +214,8 @@ def main():
 
     def step():
         ctx.register_pairs(fb, sc.K, t_pose, t_pairs, t_uid, rprm, eprm, rec, stream=stream)
-        if world > 1:
-            dist.all_gather_into_tensor(all_rec, rec)
+        if world > 1:                                    # the pose-graph exchange
+            parallel.all_gather_records(rec, world * P)
 
     for _ in range(args.warmup):
         step()
@@ -221,6 +224,17 @@ def main():
     dec = bt.decode_records(rec, N_MAX)
     M = dec["n_matches"].astype(np.int64)
     tests = int(M.sum()) * N_HYP
+    # sum of per-hypothesis inlier counts (a lower bound on the distance-gate passes), from one
+    # bt_match + bt_ransac call with per-hypothesis counts, outside the timed region
+    mt_ = torch.zeros((P, N_MAX, 2), dtype=torch.int32, device=dev)
+    nm_ = torch.zeros(P, dtype=torch.int32, device=dev)
+    hc_ = torch.zeros((P, N_HYP), dtype=torch.int32, device=dev)
+    rec_ = torch.zeros_like(rec)
+    ctx.match(fb, t_pairs, mt_, nm_, stream=stream)
+    ctx.ransac(fb, t_pairs, t_uid, mt_, nm_, rprm, rec_, hc_, stream=stream)
+    torch.cuda.synchronize()
+    sum_counts = int(hc_.clamp(min=0).sum().item())
+    del mt_, nm_, hc_, rec_
     n_assoc = float(dec["dense_ij"][:, 28].sum() + dec["dense_ji"][:, 28].sum())
 
     ctx.profile(True)
@@ -273,8 +287,9 @@ def main():
     tc_peak = float(peaks.get("bf16_tflops", 1614.4))     # fp16 kind::f16 = bf16 rate (guide ratio 1:1)
     add("k_match_tc", "tensor", 2 * pair_sizes * 128, "TFLOP/s", tc_peak,
         "2 n_a n_b 128 flop per pair (the Gram contraction, counted once)")
-    add("k_ransac_score", "alu", tests * FLOPS_PER_TEST, "TFLOP/s", fp32_peak_tflops,
-        f"{FLOPS_PER_TEST} flop per (hypothesis, correspondence) test")
+    add("k_ransac_score", "alu", tests * FLOPS_DIST + sum_counts * FLOPS_NORMAL, "TFLOP/s", fp32_peak_tflops,
+        f"{FLOPS_DIST} flop per (hypothesis, correspondence) distance gate + {FLOPS_NORMAL} flop per normal gate "
+        f"where the distance passes (lower bound: sum of inlier counts); {tests} tests, {sum_counts} inliers")
     valid_per_frame = np.array([float(((sc.mask[f] > 0) & (sc.depth[f] > 0)).sum()) for f in range(N_FRAMES)])
     src_px_edges = float(sum(valid_per_frame[a] + valid_per_frame[b] for a, b in pairs))
     add("k_dense", "alu", 30 * src_px_edges + 160 * n_assoc, "TFLOP/s", fp32_peak_tflops,
@@ -306,8 +321,16 @@ def main():
         h2d = sum(x.numel() * x.element_size() for x in (hb.n_kp, hb.desc, hb.pts, hb.nrm, hb.depth, hb.normal,
                                                          hb.mask, h_pairs, h_uid, h_pose))
         d2h = h_rec.numel() * 4
-        for _ in range(2):
+        if world > 1:                                    # the exchanged records travel H2D and back
+            h2d += h_rec.numel() * 4
+            d2h += world * h_rec.numel() * 4
+        def e2e_step():
             ctx.register_pairs(hb, sc.K, h_pose, h_pairs, h_uid, rprm, eprm, h_rec, stream=stream, host=True)
+            if world > 1:                                # records back to HBM for the exchange
+                g = parallel.all_gather_records(h_rec.to(dev, non_blocking=True), world * P)
+                g.cpu()
+        for _ in range(2):
+            e2e_step()
         e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.e2e_steps)]
         e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.e2e_steps)]
         if world > 1:
@@ -315,9 +338,7 @@ def main():
         torch.cuda.synchronize()
         for k in range(args.e2e_steps):
             e_s[k].record(stream)
-            ctx.register_pairs(hb, sc.K, h_pose, h_pairs, h_uid, rprm, eprm, h_rec, stream=stream, host=True)
-            if world > 1:
-                dist.all_gather_into_tensor(all_rec, rec)
+            e2e_step()
             e_e[k].record(stream)
         torch.cuda.synchronize()
         e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(e_s, e_e))], dtype=torch.float64, device=dev)

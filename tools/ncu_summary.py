@@ -1,0 +1,92 @@
+"""Summarise ncu evidence for profiles/: per-kernel metrics of a --set full report and the
+share of each kernel in a launch list.  Writes <out>.md and (for the roofline `traffic`
+field of bench.py) profiles/ncu_traffic.json.
+
+usage: python tools/ncu_summary.py <full.ncu-rep> <launches.csv> <out-prefix>"""
+import collections
+import csv
+import json
+import os
+import re
+import subprocess
+import sys
+
+rep, launches, out = sys.argv[1], sys.argv[2], sys.argv[3]
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration (us)", 1e-3),
+    ("dram__bytes_read.sum", "DRAM read (MB)", 1),
+    ("dram__bytes_write.sum", "DRAM write (MB)", 1),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %", 1),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %", 1),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe %", 1),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe %", 1),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %", 1),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 pipe %", 1),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %", 1),
+    ("launch__registers_per_thread", "registers", 1),
+    ("launch__grid_size", "grid", 1),
+    ("smsp__inst_executed.sum", "warp instructions", 1),
+]
+
+
+def short(name):
+    m = re.search(r"::(k_[a-z_0-9]+)", name)
+    return m.group(1) if m else name[:40]
+
+
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(raw.splitlines()))
+hdr, units = rows[0], rows[1]
+per = collections.defaultdict(list)
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    per[short(d.get("Kernel Name", "?"))].append(d)
+
+lines = [f"# ncu --set full summary ({os.path.basename(rep)})", "",
+         "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
+         "(cold cache, serialised, replayed: compare shares, not absolutes).", "",
+         "| kernel | launches | " + " | ".join(m[1] for m in METRICS) + " |",
+         "|---|---|" + "---|" * len(METRICS)]
+traffic = {}
+for k, ds in sorted(per.items()):
+    vals = []
+    for key, _, scale in METRICS:
+        xs = []
+        for d in ds:
+            try:
+                xs.append(float(d.get(key, "nan").replace(",", "")))
+            except ValueError:
+                pass
+        v = sum(xs) / len(xs) if xs else float("nan")
+        if key == "gpu__time_duration.sum":
+            u = units[hdr.index(key)] if key in hdr else "ns"
+            v = v * (1e-3 if u == "ns" else 1.0)
+        vals.append(v)
+    rd = vals[1] * (1e6 if units[hdr.index("dram__bytes_read.sum")].startswith("M") else 1)
+    wr = vals[2] * (1e6 if units[hdr.index("dram__bytes_write.sum")].startswith("M") else 1)
+    traffic[k] = rd + wr
+    lines.append(f"| {k} | {len(ds)} | " + " | ".join(f"{v:.4g}" for v in vals) + " |")
+
+# launch list shares
+lst = list(csv.reader(open(launches).read().splitlines()))
+hi = next(i for i, r in enumerate(lst) if "Kernel Name" in r)
+h = lst[hi]
+ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+tot = collections.Counter()
+cnt = collections.Counter()
+for r in lst[hi + 1:]:
+    if len(r) <= vi:
+        continue
+    v = float(r[vi].replace(",", "")) * (1e-3 if r[ui] == "ns" else 1.0)
+    tot[short(r[ki])] += v
+    cnt[short(r[ki])] += 1
+all_us = sum(tot.values())
+lines += ["", f"## Launch list ({os.path.basename(launches)}): device time per kernel, serialised", "",
+          "| kernel | launches | total us | share |", "|---|---|---|---|"]
+for k, v in tot.most_common():
+    lines.append(f"| {k} | {cnt[k]} | {v:.1f} | {100 * v / all_us:.1f}% |")
+open(out + ".md", "w").write("\n".join(lines) + "\n")
+json.dump({k: v for k, v in traffic.items()}, open(os.path.join(os.path.dirname(out), "ncu_traffic.json"), "w"),
+          indent=1)
+print("\n".join(lines))
