@@ -68,22 +68,45 @@ def ellipsoid_normal(x: np.ndarray, axes=AXES) -> np.ndarray:
     return g / np.linalg.norm(g, axis=-1, keepdims=True)
 
 
-def sample_surface(rng: np.random.Generator, n: int, axes=AXES, min_spacing: float = 0.004) -> np.ndarray:
-    """n points on the ellipsoid, roughly area-uniform, pairwise >= min_spacing apart."""
+def sample_surface(rng: np.random.Generator, n: int, axes=AXES, min_spacing: float | None = None) -> np.ndarray:
+    """n points on the ellipsoid, roughly area-uniform, pairwise >= min_spacing apart (dart
+    throwing with a grid hash).  Default spacing: 0.6 * sqrt(area / n), always satisfiable."""
     a = np.asarray(axes)
-    pts = np.zeros((0, 3))
+    if min_spacing is None:
+        p = 1.6075                                         # Knud Thomsen's surface-area formula
+        area = 4 * np.pi * ((a[0] ** p * a[1] ** p + a[0] ** p * a[2] ** p + a[1] ** p * a[2] ** p) / 3) ** (1 / p)
+        min_spacing = min(0.004, 0.6 * np.sqrt(area / n))
+    cell = min_spacing
+    grid: dict = {}
+    pts = []
+    s2 = min_spacing ** 2
     while len(pts) < n:
         u = rng.normal(size=(4 * n, 3))
         u /= np.linalg.norm(u, axis=1, keepdims=True)
         w = np.linalg.norm(u / a, axis=1)              # area element ~ abc * |u/a|
         keep = rng.uniform(0, w.max(), size=len(w)) < w
-        cand = u[keep] * a
-        for c in cand:
-            if len(pts) == 0 or np.min(np.sum((pts - c) ** 2, axis=1)) >= min_spacing ** 2:
-                pts = np.vstack([pts, c[None]])
+        for c in u[keep] * a:
+            key = tuple(np.floor(c / cell).astype(int))
+            ok = True
+            for dx in (-1, 0, 1):
+                for dy in (-1, 0, 1):
+                    for dz in (-1, 0, 1):
+                        for q in grid.get((key[0] + dx, key[1] + dy, key[2] + dz), ()):
+                            if (q[0] - c[0]) ** 2 + (q[1] - c[1]) ** 2 + (q[2] - c[2]) ** 2 < s2:
+                                ok = False
+                                break
+                        if not ok:
+                            break
+                    if not ok:
+                        break
+                if not ok:
+                    break
+            if ok:
+                grid.setdefault(key, []).append(c)
+                pts.append(c)
                 if len(pts) == n:
                     break
-    return pts
+    return np.array(pts)
 
 
 @dataclasses.dataclass

@@ -381,3 +381,30 @@ def test_match_large_n_multi_chunk(bt, torch, ctx):
         o = oracle.match(sc.desc[a, :sc.n_kp[a]], sc.desc[b, :sc.n_kp[b]])
         parity.compare_matches(got[p], o)
     assert len(got[0]) >= 3900
+
+
+def test_register_pairs_c5_stress_sampled(bt, torch):
+    """BASELINE configs[4] shape on one GPU, reduced in frames: n = 4096 keypoints
+    (n_max 4096), 16384 hypotheses, 6 frames (15 pairs, 30 dense edges at 640x480); two
+    sampled pairs compared end to end with the oracle."""
+    sc = synth.make_scene(6, n=4096, n_max=4096, pool_size=12000, seed=4242, outlier_frac=0.16)
+    pairs = synth.all_pairs(6)
+    uids = np.arange(500, 500 + len(pairs), dtype=np.uint32)
+    poses = sc.perturbed_poses(5)
+    c = bt.Context(0)
+    c.reserve(len(pairs), 4096, 16384, 6, 640, 480)
+    raw = gpu_register(bt, torch, c, sc, pairs, uids, poses, 16384)
+    c.close()
+    rec = bt.decode_records(raw, 4096)
+    assert (rec["status"] == 0).all() and (rec["n_matches"] > 1500).all()
+    for p in (0, 9):
+        a, b = pairs[p]
+        o = oracle.register_pair(sc, a, b, int(uids[p]), 16384, SEED, node_poses=poses, dense=DENSE,
+                                 counts_out=True)
+        assert rec["n_matches"][p] == o["n_matches"]
+        r = {k: v[p] for k, v in rec.items()}
+        P_ = o["match"]["pairs"]
+        pa, na, pb, nb = _pair_arrays(sc, a, b, P_)
+        parity.compare_ransac(None, r, o["counts"], pa, na, pb, nb, what=f"c5 pair {p}")
+        parity.assert_dense_close(r["dense_ij"], o["dense_ij"], f"c5 pair {p} ij")
+        parity.assert_dense_close(r["dense_ji"], o["dense_ji"], f"c5 pair {p} ji")
