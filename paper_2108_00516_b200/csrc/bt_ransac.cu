@@ -1,15 +1,15 @@
 // bt_ransac.cu — RANSAC over 3-pair samples, best-hypothesis refit and the Eq. (2)
 // feature-edge blocks.
 //
-//  k_ransac_score   one lane per hypothesis: Philox4x32-10 (counter (h, uid, 0, 0), key =
+//  k_ransac_score   two hypotheses per lane: Philox4x32-10 (counter (h, uid, 0, 0), key =
 //                   seed) -> distinct triple (reading R6) -> closed-form 3-point Arun in
 //                   fp64 (triangle frames + 2x2 Procrustes, reading R7) -> R, t in fp32.
-//                   Then each warp scores its 32 hypotheses, 4 at a time held in registers,
-//                   against the pair's correspondences staged in shared memory as four
-//                   float4 streams (p_a, p_b, O = n_b n_a^T): 24 FMA-pipe instructions per
-//                   (hypothesis, correspondence) test.  Per-lane integer counts are combined
-//                   by a 31-shuffle transpose reduction; the per-pair best is an atomicMax
-//                   on the key ((count+1) << 32 | ~h): max count, ties -> lowest h (R11).
+//                   The lane then scores its hypotheses against the pair's correspondences
+//                   (staged in shared memory, 64 B each: p_a, p_b, O = n_b n_a^T, read as
+//                   warp broadcasts): 15 FMA-pipe ops for the distance gate, 9 FFMA for the
+//                   normal gate, skipped by a warp vote when no lane's distance gate passes.
+//                   The per-pair best is an atomicMax on the key ((count+1) << 32 | ~h):
+//                   max count, ties -> lowest h (R11).
 //  k_ransac_finish  one CTA per pair: re-derives h* (same noinline solver => same bits),
 //                   inlier mask by ballot, refit by fp64 cross-covariance + Jacobi SVD with
 //                   the det fix (north star, R12), status, and — when node poses are given —
@@ -23,7 +23,7 @@ namespace bt {
 namespace {
 
 constexpr int kScoreThreads = 256;
-constexpr int kHypPerThread = 1;
+constexpr int kHypPerThread = 2;
 constexpr int kHypPerBlock = kScoreThreads * kHypPerThread;
 constexpr int kMaxChunk = 1024;           // correspondences staged per smem pass
 
@@ -53,14 +53,19 @@ __device__ __forceinline__ void sample_triple(uint4 r, int M, int &i0, int &i1, 
 }
 
 // ---------------------------------------------------------------- fp64 3-point Arun
+// Every fp64 operation is an explicit _rn intrinsic, so the (inlined) solver yields the same
+// bits in the scoring and the finish kernel whatever the compiler contracts around it.
 struct d3 { double x, y, z; };
-__device__ __forceinline__ d3 mk(double x, double y, double z) { return {x, y, z}; }
-__device__ __forceinline__ d3 sub(d3 a, d3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
-__device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ d3 cross(d3 a, d3 b) {
-  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ d3 vsub(d3 a, d3 b) { return {dsub(a.x, b.x), dsub(a.y, b.y), dsub(a.z, b.z)}; }
+__device__ __forceinline__ d3 vscale(d3 a, double s) { return {dmul(a.x, s), dmul(a.y, s), dmul(a.z, s)}; }
+__device__ __forceinline__ double vdot(d3 a, d3 b) { return dfma(a.x, b.x, dfma(a.y, b.y, dmul(a.z, b.z))); }
+__device__ __forceinline__ d3 vcross(d3 a, d3 b) {
+  return {dfma(a.y, b.z, -dmul(a.z, b.y)), dfma(a.z, b.x, -dmul(a.x, b.z)), dfma(a.x, b.y, -dmul(a.y, b.x))};
 }
-__device__ __forceinline__ d3 scale(d3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
 
 // R, t minimising sum_k |R a_k + t - b_k|^2 for three correspondences.  Centred points of a
 // triangle lie in its plane: in orthonormal in-plane frames (e1, e2) / (f1, f2) the
@@ -68,60 +73,58 @@ __device__ __forceinline__ d3 scale(d3 a, double s) { return {a.x * s, a.y * s, 
 // values are those of M: s1,2 = (p +- q)/2 with p = |(m00+m11, m01-m10)|,
 // q = |(m00-m11, m01+m10)|.  The optimal proper rotation maps n_a -> +n_b with an in-plane
 // rotation (value p) or n_a -> -n_b with an in-plane reflection (value q); the larger wins.
-// Returns false when degenerate: s2/s1 < tau (R8) or a collinear / coincident triangle.
-// __noinline__: scoring and finish kernels execute the very same instructions.
-__device__ __noinline__ bool solve3(const float *A, const float *B, double tau, float *out) {
-  const d3 a0 = mk(A[0], A[1], A[2]), a1 = mk(A[3], A[4], A[5]), a2 = mk(A[6], A[7], A[8]);
-  const d3 b0 = mk(B[0], B[1], B[2]), b1 = mk(B[3], B[4], B[5]), b2 = mk(B[6], B[7], B[8]);
+// Degenerate (false) when s2/s1 < tau (R8) — tested as (p - q)^2 < tau^2 (p + q)^2 — or for a
+// collinear / coincident triangle.
+__device__ __forceinline__ bool solve3(const float *A, const float *B, double tau, float *out) {
+  const d3 a0 = {A[0], A[1], A[2]}, a1 = {A[3], A[4], A[5]}, a2 = {A[6], A[7], A[8]};
+  const d3 b0 = {B[0], B[1], B[2]}, b1 = {B[3], B[4], B[5]}, b2 = {B[6], B[7], B[8]};
   const double third = 1.0 / 3.0;
-  const d3 ac = scale(mk(a0.x + a1.x + a2.x, a0.y + a1.y + a2.y, a0.z + a1.z + a2.z), third);
-  const d3 bc = scale(mk(b0.x + b1.x + b2.x, b0.y + b1.y + b2.y, b0.z + b1.z + b2.z), third);
-  const d3 ua = sub(a1, a0), ub = sub(b1, b0);
-  const d3 na = cross(ua, sub(a2, a0)), nb = cross(ub, sub(b2, b0));
-  const double lua = sqrt(dot(ua, ua)), lub = sqrt(dot(ub, ub));
-  const double lna = sqrt(dot(na, na)), lnb = sqrt(dot(nb, nb));
+  const d3 ac = vscale({dadd(dadd(a0.x, a1.x), a2.x), dadd(dadd(a0.y, a1.y), a2.y), dadd(dadd(a0.z, a1.z), a2.z)}, third);
+  const d3 bc = vscale({dadd(dadd(b0.x, b1.x), b2.x), dadd(dadd(b0.y, b1.y), b2.y), dadd(dadd(b0.z, b1.z), b2.z)}, third);
+  const d3 ua = vsub(a1, a0), ub = vsub(b1, b0);
+  const d3 na = vcross(ua, vsub(a2, a0)), nb = vcross(ub, vsub(b2, b0));
+  const double lua = vdot(ua, ua), lub = vdot(ub, ub), lna = vdot(na, na), lnb = vdot(nb, nb);
   if (!(lua > 0.0) || !(lub > 0.0) || !(lna > 0.0) || !(lnb > 0.0)) return false;
-  const d3 e1 = scale(ua, 1.0 / lua), n = scale(na, 1.0 / lna), e2 = cross(n, e1);
-  const d3 f1 = scale(ub, 1.0 / lub), m = scale(nb, 1.0 / lnb), f2 = cross(m, f1);
+  const d3 e1 = vscale(ua, rsqrt(lua)), n = vscale(na, rsqrt(lna)), e2 = vcross(n, e1);
+  const d3 f1 = vscale(ub, rsqrt(lub)), m = vscale(nb, rsqrt(lnb)), f2 = vcross(m, f1);
   double m00 = 0, m01 = 0, m10 = 0, m11 = 0;
-  const d3 as[3] = {sub(a0, ac), sub(a1, ac), sub(a2, ac)};
-  const d3 bs[3] = {sub(b0, bc), sub(b1, bc), sub(b2, bc)};
+  const d3 as[3] = {vsub(a0, ac), vsub(a1, ac), vsub(a2, ac)};
+  const d3 bs[3] = {vsub(b0, bc), vsub(b1, bc), vsub(b2, bc)};
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const double x0 = dot(e1, as[k]), x1 = dot(e2, as[k]);
-    const double y0 = dot(f1, bs[k]), y1 = dot(f2, bs[k]);
-    m00 += x0 * y0; m01 += x0 * y1; m10 += x1 * y0; m11 += x1 * y1;
+    const double x0 = vdot(e1, as[k]), x1 = vdot(e2, as[k]);
+    const double y0 = vdot(f1, bs[k]), y1 = vdot(f2, bs[k]);
+    m00 = dfma(x0, y0, m00); m01 = dfma(x0, y1, m01); m10 = dfma(x1, y0, m10); m11 = dfma(x1, y1, m11);
   }
-  const double p = hypot(m00 + m11, m01 - m10), q = hypot(m00 - m11, m01 + m10);
-  const double s1 = 0.5 * (p + q), s2 = 0.5 * fabs(p - q);
-  if (!(s1 > 0.0) || s2 / s1 < tau) return false;
+  const double pr = dadd(m00, m11), pi = dsub(m01, m10), qr = dsub(m00, m11), qi = dadd(m01, m10);
+  const double P2 = dfma(pr, pr, dmul(pi, pi)), Q2 = dfma(qr, qr, dmul(qi, qi));
+  const double PQ = __dsqrt_rn(dmul(P2, Q2));
+  const double sum2 = dadd(P2, Q2);                              // (p +- q)^2 = P2 + Q2 +- 2 PQ
+  if (!(sum2 > 0.0) || dsub(sum2, dmul(2.0, PQ)) < dmul(dmul(tau, tau), dadd(sum2, dmul(2.0, PQ)))) return false;
   double q00, q01, q10, q11, sg;
-  if (p >= q) {                                  // rotation branch, R n_a = n_b
-    const double c = (m00 + m11) / p, s = (m01 - m10) / p;
+  if (P2 >= Q2) {                                                // rotation branch, R n_a = n_b
+    const double ip = rsqrt(P2), c = dmul(pr, ip), s = dmul(pi, ip);
     q00 = c; q01 = -s; q10 = s; q11 = c; sg = 1.0;
-  } else {                                       // reflection branch, R n_a = -n_b
-    const double c = (m00 - m11) / q, s = (m01 + m10) / q;
+  } else {                                                       // reflection branch, R n_a = -n_b
+    const double iq = rsqrt(Q2), c = dmul(qr, iq), s = dmul(qi, iq);
     q00 = c; q01 = s; q10 = s; q11 = -c; sg = -1.0;
   }
   // R = [f1 f2 m] diag(Q, sg) [e1 e2 n]^T
-  const d3 c0 = mk(q00 * f1.x + q10 * f2.x, q00 * f1.y + q10 * f2.y, q00 * f1.z + q10 * f2.z);
-  const d3 c1 = mk(q01 * f1.x + q11 * f2.x, q01 * f1.y + q11 * f2.y, q01 * f1.z + q11 * f2.z);
-  const d3 c2 = scale(m, sg);
+  const d3 c0 = {dfma(q00, f1.x, dmul(q10, f2.x)), dfma(q00, f1.y, dmul(q10, f2.y)), dfma(q00, f1.z, dmul(q10, f2.z))};
+  const d3 c1 = {dfma(q01, f1.x, dmul(q11, f2.x)), dfma(q01, f1.y, dmul(q11, f2.y)), dfma(q01, f1.z, dmul(q11, f2.z))};
+  const d3 c2 = vscale(m, sg);
+  const double cx[3] = {c0.x, c0.y, c0.z}, cy[3] = {c1.x, c1.y, c1.z}, cz[3] = {c2.x, c2.y, c2.z};
+  const double ex[3] = {e1.x, e1.y, e1.z}, ey[3] = {e2.x, e2.y, e2.z}, ez[3] = {n.x, n.y, n.z};
   double R[9];
-  R[0] = c0.x * e1.x + c1.x * e2.x + c2.x * n.x;
-  R[1] = c0.x * e1.y + c1.x * e2.y + c2.x * n.y;
-  R[2] = c0.x * e1.z + c1.x * e2.z + c2.x * n.z;
-  R[3] = c0.y * e1.x + c1.y * e2.x + c2.y * n.x;
-  R[4] = c0.y * e1.y + c1.y * e2.y + c2.y * n.y;
-  R[5] = c0.y * e1.z + c1.y * e2.z + c2.y * n.z;
-  R[6] = c0.z * e1.x + c1.z * e2.x + c2.z * n.x;
-  R[7] = c0.z * e1.y + c1.z * e2.y + c2.z * n.y;
-  R[8] = c0.z * e1.z + c1.z * e2.z + c2.z * n.z;
 #pragma unroll
-  for (int k = 0; k < 9; ++k) out[k] = (float)R[k];
-  out[9] = (float)(bc.x - (R[0] * ac.x + R[1] * ac.y + R[2] * ac.z));
-  out[10] = (float)(bc.y - (R[3] * ac.x + R[4] * ac.y + R[5] * ac.z));
-  out[11] = (float)(bc.z - (R[6] * ac.x + R[7] * ac.y + R[8] * ac.z));
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) R[3 * r + c] = dfma(cx[r], ex[c], dfma(cy[r], ey[c], dmul(cz[r], ez[c])));
+#pragma unroll
+  for (int k = 0; k < 9; ++k) out[k] = __double2float_rn(R[k]);
+  out[9] = __double2float_rn(dsub(bc.x, dfma(R[0], ac.x, dfma(R[1], ac.y, dmul(R[2], ac.z)))));
+  out[10] = __double2float_rn(dsub(bc.y, dfma(R[3], ac.x, dfma(R[4], ac.y, dmul(R[5], ac.z)))));
+  out[11] = __double2float_rn(dsub(bc.z, dfma(R[6], ac.x, dfma(R[7], ac.y, dmul(R[8], ac.z)))));
   return true;
 }
 
@@ -171,9 +174,14 @@ __device__ __forceinline__ float normal_term(const float *T, const float4 q1, co
   c = __fmaf_rn(T[8], q3.z, c);
   return c;
 }
+// inlier <=> sign(d') = 1 and sign(c') = 0 (differs from d' < 0 && c' > 0 only at exact
+// ties d' = -0 / c' = +0, which the band rule leaves undecided); both kernels use it
+__device__ __forceinline__ unsigned pass_bit(float d, float c) {
+  return (__float_as_uint(d) & ~__float_as_uint(c)) >> 31;
+}
 __device__ __forceinline__ bool inlier(const float *T, const float4 q0, const float4 q1, const float4 q2,
                                        const float4 q3, float ndelta2, float ncosa) {
-  return (dist_term(T, q0, q1, ndelta2) < 0.f) & (normal_term(T, q1, q2, q3, ncosa) > 0.f);
+  return pass_bit(dist_term(T, q0, q1, ndelta2), normal_term(T, q1, q2, q3, ncosa)) != 0u;
 }
 
 __device__ __forceinline__ void pack_corr(const float *pa, const float *na, const float *pb,
@@ -200,109 +208,101 @@ struct ScoreArgs {
   int32_t *hyp_counts;
 };
 
-// One CTA = 256 hypotheses of one pair (one per thread: Philox + fp64 solve).  Each warp then
-// scores its 32 hypotheses, 4 at a time in registers, against all correspondences (lane =
-// correspondence, staged in smem, padded to a multiple of 32 with never-inlier sentinels).
-// Per (hypothesis, 32 correspondences) a warp vote skips the normal gate when no lane passes
-// the distance gate — the common case for samples that contain an outlier.
+// One CTA = 512 hypotheses of one pair, two per thread (Philox + fp64 solve by the thread
+// that scores them: lane = hypothesis).  The pair's correspondences are staged in shared
+// memory (AoS, 64 B each) and every warp walks them in the same order, so each q-load is a
+// broadcast.  Per correspondence a warp vote skips the normal gate when no lane's distance
+// gate passes (outlier correspondences), and counts stay in registers: no cross-lane
+// reduction of counts.
 __global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) {
-  extern __shared__ float4 sm4[];
-  const int chunk = A.chunk;                                      // multiple of 32
-  float4 *s0 = sm4, *s1 = sm4 + chunk, *s2 = sm4 + 2 * chunk, *s3 = sm4 + 3 * chunk;
-  float *hs = reinterpret_cast<float *>(sm4 + 4 * chunk);         // [256][12] hypotheses
+  extern __shared__ float4 sq[];                                  // [chunk][4]
+  const int chunk = A.chunk;
   const int p = blockIdx.y;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int M = A.n_matches[p];
   const int H = A.n_hyp;
-  const int h = blockIdx.x * kHypPerBlock + threadIdx.x;
+  const int h_base = blockIdx.x * kHypPerBlock + threadIdx.x;     // hypotheses h_base + k * kScoreThreads
   const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
   const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
   const float *pa_f = A.kp.pts + (size_t)fa * A.kp.n_max * 3, *pb_f = A.kp.pts + (size_t)fb * A.kp.n_max * 3;
   const float *na_f = A.kp.nrm + (size_t)fa * A.kp.n_max * 3, *nb_f = A.kp.nrm + (size_t)fb * A.kp.n_max * 3;
 
   if (M < 3) {                                                   // FEW_MATCHES: no samples
-    if (A.hyp_counts && h < H) A.hyp_counts[(size_t)p * H + h] = -1;
+    if (A.hyp_counts)
+#pragma unroll
+      for (int k = 0; k < kHypPerThread; ++k)
+        if (h_base + k * kScoreThreads < H) A.hyp_counts[(size_t)p * H + h_base + k * kScoreThreads] = -1;
     return;
   }
-  const int nchunks = (M + chunk - 1) / chunk;
-  auto stage = [&](int c0) {
-    const int len = min(chunk, M - c0), len32 = (len + 31) & ~31;
-    for (int k = threadIdx.x; k < len32; k += kScoreThreads) {
-      float4 q0, q1, q2, q3;
-      if (k < len) {
-        const int i = mt[2 * (c0 + k)], j = mt[2 * (c0 + k) + 1];
-        pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
-      } else {                                                    // sentinel: |e|^2 = inf, c' < 0
-        q0 = make_float4(0.f, 0.f, 0.f, 3.0e38f);
-        q1 = q2 = q3 = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      s0[k] = q0; s1[k] = q1; s2[k] = q2; s3[k] = q3;
-    }
-  };
-  if (nchunks == 1) stage(0);                                     // staged once, read by every group
-
-  float T[12];
-  bool valid = false;
-  if (h < H) valid = make_hypothesis(h, A.uid[p], A.k0, A.k1, M, mt, pa_f, pb_f, A.tau, T);
-  if (!valid) {                                                  // never passes the distance gate
-#pragma unroll
-    for (int k = 0; k < 12; ++k) T[k] = 0.f;
-    T[11] = 3.0e38f;
-  }
-  float4 *hs4 = reinterpret_cast<float4 *>(hs + 12 * threadIdx.x);
-  hs4[0] = make_float4(T[0], T[1], T[2], T[3]);
-  hs4[1] = make_float4(T[4], T[5], T[6], T[7]);
-  hs4[2] = make_float4(T[8], T[9], T[10], T[11]);
-  __syncthreads();
-
-  int mine = 0;                                                   // count of hypothesis warp*32 + lane
+  // solve the hypotheses one after the other (no unrolling: one solver's registers live
+  // at a time), park them in shared memory, then hold all four in registers for scoring
+  float *hs = reinterpret_cast<float *>(sq + 4 * chunk);          // [kHypPerThread][kScoreThreads][12]
+  unsigned valid_bits = 0u;
 #pragma unroll 1
-  for (int g = 0; g < 8; ++g) {
-    float Th[4][12];
+  for (int k = 0; k < kHypPerThread; ++k) {
+    const int h = h_base + k * kScoreThreads;
+    float Tk[12];
+    const bool v = h < H && make_hypothesis(h, A.uid[p], A.k0, A.k1, M, mt, pa_f, pb_f, A.tau, Tk);
+    if (!v) {                                                    // never passes the distance gate
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 *src = reinterpret_cast<const float4 *>(hs + 12 * (warp * 32 + 4 * g + k));
-      const float4 x = src[0], y = src[1], z = src[2];
-      Th[k][0] = x.x; Th[k][1] = x.y; Th[k][2] = x.z; Th[k][3] = x.w;
-      Th[k][4] = y.x; Th[k][5] = y.y; Th[k][6] = y.z; Th[k][7] = y.w;
-      Th[k][8] = z.x; Th[k][9] = z.y; Th[k][10] = z.z; Th[k][11] = z.w;
+      for (int q = 0; q < 12; ++q) Tk[q] = 0.f;
+      Tk[11] = 3.0e38f;
     }
-    int acc[4] = {0, 0, 0, 0};
-    for (int c0 = 0; c0 < M; c0 += chunk) {
-      if (nchunks > 1) {
-        __syncthreads();
-        stage(c0);
-        __syncthreads();
-      }
-      const int len32 = (min(chunk, M - c0) + 31) & ~31;
+    valid_bits |= (unsigned)v << k;
+    float4 *dst = reinterpret_cast<float4 *>(hs + 12 * (k * kScoreThreads + threadIdx.x));
+    dst[0] = make_float4(Tk[0], Tk[1], Tk[2], Tk[3]);
+    dst[1] = make_float4(Tk[4], Tk[5], Tk[6], Tk[7]);
+    dst[2] = make_float4(Tk[8], Tk[9], Tk[10], Tk[11]);
+  }
+  float T[kHypPerThread][12];
+#pragma unroll
+  for (int k = 0; k < kHypPerThread; ++k) {
+    const float4 *src = reinterpret_cast<const float4 *>(hs + 12 * (k * kScoreThreads + threadIdx.x));
+    const float4 x = src[0], y = src[1], z = src[2];
+    T[k][0] = x.x; T[k][1] = x.y; T[k][2] = x.z; T[k][3] = x.w;
+    T[k][4] = y.x; T[k][5] = y.y; T[k][6] = y.z; T[k][7] = y.w;
+    T[k][8] = z.x; T[k][9] = z.y; T[k][10] = z.z; T[k][11] = z.w;
+  }
+  unsigned cnt[kHypPerThread];
+#pragma unroll
+  for (int k = 0; k < kHypPerThread; ++k) cnt[k] = 0u;
+  for (int cs = 0; cs < M; cs += chunk) {
+    const int len = min(chunk, M - cs);
+    __syncthreads();
+    for (int k = threadIdx.x; k < len; k += kScoreThreads) {
+      const int i = mt[2 * (cs + k)], j = mt[2 * (cs + k) + 1];
+      float4 q0, q1, q2, q3;
+      pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
+      sq[4 * k] = q0; sq[4 * k + 1] = q1; sq[4 * k + 2] = q2; sq[4 * k + 3] = q3;
+    }
+    __syncthreads();
 #pragma unroll 2
-      for (int m0 = 0; m0 < len32; m0 += 32) {
-        const int m = m0 + lane;
-        const float4 q0 = s0[m], q1 = s1[m];
-        bool pd[4];
+    for (int m = 0; m < len; ++m) {
+      const float4 q0 = sq[4 * m], q1 = sq[4 * m + 1];
+      float d[kHypPerThread];
+      unsigned any_neg = 0u;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) pd[k] = dist_term(Th[k], q0, q1, A.ndelta2) < 0.f;
-        if (__any_sync(0xffffffffu, pd[0] | pd[1] | pd[2] | pd[3])) {
-          const float4 q2 = s2[m], q3 = s3[m];
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (__any_sync(0xffffffffu, pd[k])) acc[k] += pd[k] & (normal_term(Th[k], q1, q2, q3, A.ncosa) > 0.f);
-        }
+      for (int k = 0; k < kHypPerThread; ++k) {
+        d[k] = dist_term(T[k], q0, q1, A.ndelta2);
+        any_neg |= __float_as_uint(d[k]);
       }
-    }
+      if (__any_sync(0xffffffffu, any_neg >> 31)) {
+        const float4 q2 = sq[4 * m + 2], q3 = sq[4 * m + 3];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int t = acc[k];
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 4 * g + k) mine = t;
+        for (int k = 0; k < kHypPerThread; ++k) cnt[k] += pass_bit(d[k], normal_term(T[k], q1, q2, q3, A.ncosa));
+      }
     }
   }
-  const int count = valid ? mine : -1;
   unsigned long long key = 0ull;
-  if (h < H) {
+#pragma unroll
+  for (int k = 0; k < kHypPerThread; ++k) {
+    const int h = h_base + k * kScoreThreads;
+    if (h >= H) continue;
+    const int count = ((valid_bits >> k) & 1u) ? (int)cnt[k] : -1;
     if (A.hyp_counts) A.hyp_counts[(size_t)p * H + h] = count;
-    key = ((unsigned long long)(uint32_t)(count + 1) << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)h);
+    const unsigned long long kk =
+        ((unsigned long long)(uint32_t)(count + 1) << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)h);
+    key = kk > key ? kk : key;
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -669,11 +669,12 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
                    Launch &L) {
   if (P <= 0) return;
   const int chunk = kp.n_max < kMaxChunk ? ((kp.n_max + 31) / 32) * 32 : kMaxChunk;   // multiple of 32
-  const size_t smem = (size_t)4 * chunk * sizeof(float4) + (size_t)kScoreThreads * 12 * sizeof(float);
+  const size_t hyp_smem = (size_t)kHypPerThread * kScoreThreads * 12 * sizeof(float);
+  const size_t smem = (size_t)4 * chunk * sizeof(float4) + hyp_smem;
   static bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(k_ransac_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4 * kMaxChunk * (int)sizeof(float4) + kScoreThreads * 12 * (int)sizeof(float));
+                         (int)(4 * kMaxChunk * sizeof(float4) + hyp_smem));
     attr_done = true;
   }
   cudaMemsetAsync(best_key, 0, sizeof(unsigned long long) * P, s);
