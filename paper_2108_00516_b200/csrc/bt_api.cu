@@ -371,6 +371,12 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
   const cudaStream_t st = (cudaStream_t)stream;
   const int F = kp->n_frames;
   const size_t FN = (size_t)F * kp->n_max;
+  const int rw = bt::rec_words(kp->n_max);
+  c->launch.count = 0;
+  // keypoints first on the caller's stream: matching + RANSAC start as soon as they land,
+  // while the (much larger) maps stream in on the side stream and feed the dense edges there
+  cudaEventRecord(c->ev_fork, st);                               // staging buffers free
+  cudaStreamWaitEvent(c->side, c->ev_fork, 0);
   cudaMemcpyAsync(c->st_nkp, kp->n_kp, (size_t)F * 4, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(c->st_desc, kp->desc, FN * 128 * 4, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(c->st_pts, kp->pts, FN * 12, cudaMemcpyHostToDevice, st);
@@ -379,22 +385,37 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
   cudaMemcpyAsync(c->st_uid, pair_uid, (size_t)P * 4, cudaMemcpyHostToDevice, st);
   bt_keypoints dk = *kp;
   dk.n_kp = c->st_nkp; dk.desc = c->st_desc; dk.pts = c->st_pts; dk.nrm = c->st_nrm;
-  bt_maps dm{};
+  if ((s = check_kp(c, &dk)) != BT_OK) return s;
   if (eprm) {
     const size_t FP = (size_t)maps->n_frames * maps->width * maps->height;
-    cudaMemcpyAsync(c->st_depth, maps->depth, FP * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(c->st_normal, maps->normal, FP * 12, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(c->st_mask, maps->mask, FP, cudaMemcpyHostToDevice, st);
+    // poses on the caller's stream: the finish kernel (Eq. (2) blocks) reads them there
     cudaMemcpyAsync(c->st_pose, node_pose, (size_t)maps->n_frames * sizeof(bt_pose), cudaMemcpyHostToDevice, st);
-    dm = *maps;
+    cudaMemcpyAsync(c->st_mask, maps->mask, FP, cudaMemcpyHostToDevice, c->side);
+    cudaMemcpyAsync(c->st_depth, maps->depth, FP * 4, cudaMemcpyHostToDevice, c->side);
+    cudaMemcpyAsync(c->st_normal, maps->normal, FP * 12, cudaMemcpyHostToDevice, c->side);
+    bt_maps dm = *maps;
     dm.depth = c->st_depth; dm.normal = c->st_normal; dm.mask = c->st_mask;
+    if ((s = check_maps(c, &dm, K)) != BT_OK) return s;
+    if ((s = check_edge(c, eprm)) != BT_OK) return s;
+    // the dense kernels need the pair list and poses too: wait for the caller-stream copies
+    cudaEventRecord(c->ev_join, st);
+    cudaStreamWaitEvent(c->side, c->ev_join, 0);
+    bt::launch_dense(mview(&dm), *K, c->st_pose, nullptr, c->st_pairs, 2 * P, *eprm, c->dense, nullptr, 0,
+                     c->st_records, rw, bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch);
   }
-  if ((s = after_launch(c, "bt_register_pairs_host: H2D")) != BT_OK) return s;
-  s = bt_register_pairs(c, &dk, eprm ? &dm : nullptr, K, eprm ? c->st_pose : nullptr, c->st_pairs, c->st_uid, P,
-                        mprm, rprm, eprm, c->st_records, stream);
-  if (s != BT_OK) return s;
+  const float ratio = mprm ? mprm->ratio : 1.f;
+  bt::launch_match(kview(&dk), c->st_pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches,
+                   c->n_matches, st, c->launch);
+  bt::launch_ransac(kview(&dk), c->st_pairs, c->st_uid, P, c->matches, c->n_matches, *rprm, c->best_key,
+                    c->st_records, rw, nullptr, eprm ? c->st_pose : nullptr, eprm ? eprm->huber_m : 0.f, st,
+                    c->launch);
+  if (eprm) {
+    cudaEventRecord(c->ev_join, c->side);
+    cudaStreamWaitEvent(st, c->ev_join, 0);
+  }
+  if ((s = after_launch(c, "bt_register_pairs_host")) != BT_OK) return s;
   const int launches = c->launch.count;
-  cudaMemcpyAsync(records, c->st_records, (size_t)P * bt::rec_words(kp->n_max) * 4, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(records, c->st_records, (size_t)P * rw * 4, cudaMemcpyDeviceToHost, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return fail(c, BT_ECUDA, "bt_register_pairs_host: sync failed");
   c->launch.count = launches;
   return after_launch(c, "bt_register_pairs_host");
