@@ -408,3 +408,34 @@ def test_register_pairs_c5_stress_sampled(bt, torch):
         parity.compare_ransac(None, r, o["counts"], pa, na, pb, nb, what=f"c5 pair {p}")
         parity.assert_dense_close(r["dense_ij"], o["dense_ij"], f"c5 pair {p} ij")
         parity.assert_dense_close(r["dense_ji"], o["dense_ji"], f"c5 pair {p} ji")
+
+
+def test_cuda_graph_capture_replay(bt, torch):
+    """bt_register_pairs only enqueues stream-ordered work (incl. the side-stream fork/join), so
+    a whole frame step can be captured in a CUDA graph and replayed with identical records."""
+    sc = synth.make_scene(5, seed=77)
+    pairs = synth.all_pairs(5)
+    uids = np.arange(len(pairs), dtype=np.uint32)
+    c = bt.Context(0)
+    c.reserve(len(pairs), 512, 1024, 5, 640, 480)
+    fb = bt.FrameBatch.from_scene(sc)
+    rw = bt.record_words(512)
+    pr = _dev(torch, pairs)
+    ud = _dev(torch, uids.view(np.int32))
+    ps = _dev(torch, sc.perturbed_poses(1))
+    rprm, eprm = bt.ransac_params(1024, SEED), bt.edge_params()
+    eager = torch.zeros((len(pairs), rw), dtype=torch.int32, device="cuda")
+    c.register_pairs(fb, sc.K, ps, pr, ud, rprm, eprm, eager)
+    torch.cuda.synchronize()
+    graphed = torch.zeros_like(eager)
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        c.register_pairs(fb, sc.K, ps, pr, ud, rprm, eprm, graphed, stream=s)
+    for _ in range(3):
+        graphed.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(eager.cpu().numpy(), graphed.cpu().numpy())
+    c.close()
