@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbt.so")
+LIB_PATH = os.environ.get("BT_LIB") or os.path.join(_PKG, "libbt.so")   # BT_LIB: A/B builds (dev tools)
 
 BT_OK, BT_EINVAL, BT_ENOMEM, BT_ECUDA, BT_EUNSUPPORTED, BT_ECAPACITY = range(6)
 PAIR_OK, PAIR_FEW_MATCHES, PAIR_FEW_INLIERS, PAIR_REFIT_DEGENERATE = range(4)

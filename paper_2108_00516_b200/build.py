@@ -29,7 +29,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     stale = not os.path.exists(LIB) or any(os.path.getmtime(p) > os.path.getmtime(LIB) for p in deps())
     if not (force or stale):
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", LIB, *sources()]
+    cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("BT_NVCC_FLAGS", "").split(), "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-o", LIB, *sources()]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

@@ -19,7 +19,8 @@ struct bt_ctx {
   char err[512] = {0};
   bt::Launch launch;                          // kernels enqueued by the current / last call
   cudaStream_t side = nullptr;                // dense Eq.(3) path runs here, overlapping match + RANSAC
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t hi = nullptr;                  // match -> RANSAC chain (the longer one), high priority
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join_hi = nullptr;
   // per-kernel event timing (bt_profile_*)
   struct Pending { int kid; cudaEvent_t start, stop; };
   bool prof_on = false;
@@ -166,7 +167,11 @@ bt_status bt_create(bt_ctx **out, int cuda_device) {
   bt_ctx *c = new (std::nothrow) bt_ctx;
   if (!c) return BT_ENOMEM;
   c->device = cuda_device;
-  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join_hi, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
@@ -185,6 +190,8 @@ void bt_destroy(bt_ctx *c) {
   for (auto &p : c->pending) { cudaEventDestroy(p.start); if (p.stop) cudaEventDestroy(p.stop); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->hi) cudaStreamDestroy(c->hi);
+  if (c->ev_join_hi) cudaEventDestroy(c->ev_join_hi);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   free_scratch(c);
@@ -309,19 +316,27 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
   const float ratio = mprm ? mprm->ratio : 1.f;
   // fork: the dense edges only need the maps and node poses, so they run on the side stream
   // while matching and RANSAC run on the caller's stream (event fork / join: capturable)
+  // with the dense edges forked off, match -> RANSAC (the longer chain) runs on a high-priority
+  // internal stream so the block scheduler dispatches its CTAs ahead of the dense edges'
+  cudaStream_t ms = eprm ? c->hi : st;
   if (eprm) {
     cudaEventRecord(c->ev_fork, st);
     cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    if (ms != st) cudaStreamWaitEvent(ms, c->ev_fork, 0);
     bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, nullptr, 0, records, rw,
                      bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch);
   }
   bt::launch_match(kview(kp), pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches, c->n_matches,
-                   st, c->launch);
+                   ms, c->launch);
   bt::launch_ransac(kview(kp), pairs, uid, P, c->matches, c->n_matches, *rprm, c->best_key, records, rw, nullptr,
-                    eprm ? node_pose : nullptr, eprm ? eprm->huber_m : 0.f, st, c->launch);
+                    eprm ? node_pose : nullptr, eprm ? eprm->huber_m : 0.f, ms, c->launch);
   if (eprm) {
     cudaEventRecord(c->ev_join, c->side);
     cudaStreamWaitEvent(st, c->ev_join, 0);
+    if (ms != st) {
+      cudaEventRecord(c->ev_join_hi, ms);
+      cudaStreamWaitEvent(st, c->ev_join_hi, 0);
+    }
   }
   return after_launch(c, "bt_register_pairs");
 }

@@ -21,13 +21,19 @@
 //                 (gathered as a TARGET), a validity byte is written for every pixel, and a
 //                 block scan compacts the tile's valid source pixels (pixel order, stride
 //                 applied) into 32-byte entries.
-//  k_dense        one CTA per (frame, tile): entries + their fp64 points staged in shared
-//                 memory once and reused for every edge leaving the frame (source reuse).
+//  k_dense_scan   one CTA per frame: exclusive scan of the tile counts, so the frame's valid
+//                 source pixels form one compacted sequence cut into chunks of kTile entries.
+//  k_dense        one CTA per (frame, chunk) work item (grid-stride) — every chunk but a
+//                 frame's last is full, so no CTA reduces a mostly-empty border tile.  A chunk's
+//                 entries (located by binary search in the tile offsets) + their fp64 points are
+//                 staged in shared memory once and reused for every edge leaving the frame.
 //                 Per (entry, edge): fp32 projection, gather of the target validity + map entry
 //                 (all of a thread's gathers issued together), fp64 gates / residual, Huber,
 //                 29 running sums; per edge a 31-shuffle warp transpose reduction + smem.
 //  k_dense_reduce fixed-order fp64 sum of the per-tile partials of an edge (deterministic).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "bt_internal.cuh"
 
@@ -61,9 +67,11 @@ struct DenseArgs {
   int32_t *ecount;            // [F]
   float4 *entries;            // [F][tiles][kTile][2]
   int32_t *counts;            // [F][tiles]
+  int32_t *offs;              // [F][tiles + 1] exclusive scan of counts (entries of frame f before tile t)
+  int32_t *nch;               // [F] chunks of kTile compacted entries (0 if the frame has no outgoing edge)
   MapEntry *pmap;             // [F][H*W]
   uint8_t *vmap;              // [F][H*W]
-  float *partials;            // [E][tiles][32]
+  float *partials;            // [E][tiles][32] (per chunk of the edge's source frame; chunks <= tiles)
 };
 
 __device__ __forceinline__ void edge_frames(const int32_t *edges, const int32_t *pairs, int e, int &fi, int &fj) {
@@ -216,6 +224,38 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
   if (threadIdx.x == 0) A.counts[(size_t)f * A.tiles + t] = total;
 }
 
+// per frame: exclusive scan of the tile counts -> offs, and the number of kTile-entry chunks
+__global__ void __launch_bounds__(kDenseThreads) k_dense_scan(DenseArgs A) {
+  __shared__ int wsum[kDenseThreads / 32];
+  const int f = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t *cnt = A.counts + (size_t)f * A.tiles;
+  int32_t *off = A.offs + (size_t)f * (A.tiles + 1);
+  int carry = 0;
+  for (int t0 = 0; t0 < A.tiles; t0 += kDenseThreads) {
+    const int t = t0 + threadIdx.x;
+    const int c = t < A.tiles ? cnt[t] : 0;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int woff = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kDenseThreads / 32; ++w) { woff += w < warp ? wsum[w] : 0; tot += wsum[w]; }
+    if (t < A.tiles) off[t] = carry + woff + incl - c;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    off[A.tiles] = carry;
+    A.nch[f] = A.ecount[f] > 0 ? (carry + kTile - 1) / kTile : 0;
+  }
+}
+
 constexpr int kEdgeBatch = 16;                // edges whose per-warp partials are held before one CTA barrier
 constexpr size_t kDenseSmem = kTile * (16 + 16 + 8 + 24) + (kDenseThreads / 32) * kEdgeBatch * 32 * 4;
 
@@ -226,20 +266,54 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
   float2 *sNo = reinterpret_cast<float2 *>(sN + kTile);            // n_o,i.y, n_o,i.z
   double *sX = reinterpret_cast<double *>(sNo + kTile);            // p - t_i (fp64)
   float *red = reinterpret_cast<float *>(sX + 3 * kTile);          // [warp][kEdgeBatch][32]
-  const int f = blockIdx.y, t = blockIdx.x;
-  const int n = A.counts[(size_t)f * A.tiles + t];
-  const int ne = A.ecount[f];
-  if (n == 0 || ne == 0) return;
+  int *sCb = reinterpret_cast<int *>(red + (kDenseThreads / 32) * kEdgeBatch * 32);  // [F + 1] chunk base per frame
+  int *sOff = sCb + A.mp.n_frames + 1;                             // [tiles + 1] of the current frame
+  const int F = A.mp.n_frames;
   const int W = A.mp.W, H = A.mp.H, npx = W * H;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {                                                 // chunk bases: prefix over frames
+    int carry = 0;
+    for (int f0 = 0; f0 < F; f0 += 32) {
+      const int c = f0 + lane < F ? A.nch[f0 + lane] : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (f0 + lane < F) sCb[f0 + lane] = carry + incl - c;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) sCb[F] = carry;
+  }
+  __syncthreads();
+  const int total = sCb[F];
+  for (int ch = blockIdx.x; ch < total; ch += gridDim.x) {
+  int f = 0;
+  {
+    int lo = 0, hi = F;                                            // sCb[lo] <= ch < sCb[hi]
+    while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (sCb[mid] <= ch) lo = mid; else hi = mid; }
+    f = lo;
+  }
+  const int cl = ch - sCb[f];                                      // chunk of frame f
+  const int32_t *offg = A.offs + (size_t)f * (A.tiles + 1);
+  for (int k = threadIdx.x; k <= A.tiles; k += kDenseThreads) sOff[k] = offg[k];
+  __syncthreads();
+  const int n = min(kTile, sOff[A.tiles] - cl * kTile);
+  const int ne = A.ecount[f];
   double Rd[9];                                                    // R_i (fp64)
   {
     const bt_pose P = A.node_pose[f];
 #pragma unroll
     for (int k = 0; k < 9; ++k) Rd[k] = P.R[k];
     const double t0 = P.t[0], t1 = P.t[1], t2 = P.t[2];
-    const float4 *src = A.entries + ((size_t)f * A.tiles + t) * kTile * 2;
+    const float4 *src = A.entries + (size_t)f * A.tiles * kTile * 2;
     for (int k = threadIdx.x; k < n; k += kDenseThreads) {
-      const float4 a = src[2 * k], b = src[2 * k + 1];
+      const int gi = cl * kTile + k;                               // compacted entry index within frame f
+      int lo = 0, hi = A.tiles;                                    // sOff[lo] <= gi < sOff[hi]
+      while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (sOff[mid] <= gi) lo = mid; else hi = mid; }
+      const float4 *e2 = src + ((size_t)lo * kTile + (gi - sOff[lo])) * 2;
+      const float4 a = e2[0], b = e2[1];
       const int uv = __float_as_int(a.w), u = uv & 0xffff, v = uv >> 16;
       const double d = a.z;                                        // p.z = depth exactly
       sX[3 * k] = ((double)u - A.cxd) * d * A.ifxd - t0;
@@ -255,8 +329,6 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
     }
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
   for (int ie0 = 0; ie0 < ne; ie0 += kEdgeBatch) {
     const int nb_e = min(kEdgeBatch, ne - ie0);
     for (int ib = 0; ib < nb_e; ++ib) {                           // warps run through the batch independently
@@ -360,13 +432,14 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
 #pragma unroll
       for (int w2 = 0; w2 < kDenseThreads / 32; ++w2) s += red[(w2 * kEdgeBatch + ib) * 32 + l];
       const int e = A.elist[(size_t)f * A.E + ie0 + ib];
-      A.partials[((size_t)e * A.tiles + t) * kPartStride + l] = s;
+      A.partials[((size_t)e * A.tiles + cl) * kPartStride + l] = s;
     }
     __syncthreads();
   }
+  }
 }
 
-__global__ void __launch_bounds__(256) k_dense_reduce(const float *__restrict__ partials, const int32_t *__restrict__ counts,
+__global__ void __launch_bounds__(256) k_dense_reduce(const float *__restrict__ partials, const int32_t *__restrict__ nch,
                                                        int tiles, const int32_t *edges, const int32_t *pairs, float *out,
                                                        int out_stride, uint32_t *records, int rec_stride, int off_ij,
                                                        int off_ji) {
@@ -375,9 +448,9 @@ __global__ void __launch_bounds__(256) k_dense_reduce(const float *__restrict__ 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int fi, fj;
   edge_frames(edges, pairs, e, fi, fj);
-  double s = 0.0;                                 // warp w: tiles w, w + 8, ... in order; lane = value
-  for (int t = warp; t < tiles; t += 8)
-    if (counts[(size_t)fi * tiles + t] > 0) s += (double)partials[((size_t)e * tiles + t) * kPartStride + lane];
+  double s = 0.0;                                 // warp w: chunks w, w + 8, ... in order; lane = value
+  const int nc = nch[fi];
+  for (int t = warp; t < nc; t += 8) s += (double)partials[((size_t)e * tiles + t) * kPartStride + lane];
   wsum[warp][lane] = s;
   __syncthreads();
   if (warp != 0) return;
@@ -418,7 +491,7 @@ int dense_tiles(int W, int H) { return ((W + kTS - 1) / kTS) * ((H + kTS - 1) / 
 
 size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H) {
   const size_t tiles = dense_tiles(W, H), F = max_frames, npx = (size_t)W * H;
-  return align256(F * tiles * kTile * 32) + align256(F * tiles * 4) + align256((size_t)max_edges * tiles * kPartStride * 4) +
+  return align256(F * tiles * kTile * 32) + align256(F * tiles * 4) + align256(F * (tiles + 1) * 4) + align256(F * 4) + align256((size_t)max_edges * tiles * kPartStride * 4) +
          align256((size_t)max_edges * 48) + align256(F * max_edges * 4) + align256(F * 4) +
          align256(F * npx * sizeof(MapEntry)) + align256(F * npx);
 }
@@ -447,6 +520,8 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   const size_t tiles = a.tiles, F = mp.n_frames, npx = (size_t)mp.W * mp.H;
   a.entries = (float4 *)p;   p += align256(F * tiles * kTile * 32);
   a.counts = (int32_t *)p;   p += align256(F * tiles * 4);
+  a.offs = (int32_t *)p;     p += align256(F * (tiles + 1) * 4);
+  a.nch = (int32_t *)p;      p += align256(F * 4);
   a.partials = (float *)p;   p += align256((size_t)E * tiles * kPartStride * 4);
   a.tji = (float *)p;        p += align256((size_t)E * 48);
   a.elist = (int32_t *)p;    p += align256(F * E * 4);
@@ -462,16 +537,23 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   L.begin(K_DENSE_PREP, s);
   k_dense_prep<<<dim3(a.tiles, mp.n_frames), kDenseThreads, 0, s>>>(a);
   L.end(K_DENSE_PREP, s);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDenseSmem);
-    attr = true;
+  L.begin(K_DENSE_PREP, s);
+  k_dense_scan<<<mp.n_frames, kDenseThreads, 0, s>>>(a);
+  L.end(K_DENSE_PREP, s);
+  const size_t smem = kDenseSmem + (size_t)(mp.n_frames + 1 + a.tiles + 1) * 4;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
   }
+  // one CTA per possible chunk (idle ones exit at once), not persistent: CTA boundaries let the
+  // higher-priority match / RANSAC kernels interleave (bt_api.cu register_pairs_dev)
+  const int grid = a.tiles * mp.n_frames;
   L.begin(K_DENSE, s);
-  k_dense<<<dim3(a.tiles, mp.n_frames), kDenseThreads, kDenseSmem, s>>>(a);
+  k_dense<<<grid, kDenseThreads, smem, s>>>(a);
   L.end(K_DENSE, s);
   L.begin(K_DENSE_REDUCE, s);
-  k_dense_reduce<<<E, 256, 0, s>>>(a.partials, a.counts, a.tiles, edges, pairs, out, out_stride, records,
+  k_dense_reduce<<<E, 256, 0, s>>>(a.partials, a.nch, a.tiles, edges, pairs, out, out_stride, records,
                                   rec_stride, rec_off_ij, rec_off_ji);
   L.end(K_DENSE_REDUCE, s);
 }
