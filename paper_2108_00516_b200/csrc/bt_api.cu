@@ -37,7 +37,8 @@ struct bt_ctx {
   CUtensorMap tmap_desc;                      // TMA view of ms.desc16: [frames * n_pad][128] fp16
   int force_fallback = 0;                     // BT_FORCE_FALLBACK: exact rescoring of every row
   int32_t *matches = nullptr, *n_matches = nullptr;
-  unsigned long long *best_key = nullptr;
+  void *rscratch = nullptr;                   // RANSAC hypotheses / counts (bt::RansacScratch)
+  bt::RansacScratch rs{};
   void *dense = nullptr;
   // staging for bt_register_pairs_host
   int32_t *st_nkp = nullptr, *st_pairs = nullptr;
@@ -70,7 +71,7 @@ void free_dev(T *&p) {
 
 void free_scratch(bt_ctx *c) {
   free_dev(c->match); free_dev(c->matches); free_dev(c->n_matches);
-  free_dev(c->best_key); free_dev(c->dense);
+  free_dev(c->rscratch); free_dev(c->dense);
   free_dev(c->st_nkp); free_dev(c->st_pairs); free_dev(c->st_uid); free_dev(c->st_records);
   free_dev(c->st_desc); free_dev(c->st_pts); free_dev(c->st_nrm); free_dev(c->st_depth);
   free_dev(c->st_normal); free_dev(c->st_mask); free_dev(c->st_pose);
@@ -219,9 +220,10 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
   const int mframes = max_frames > 0 ? max_frames : 1;
   bool ok = cudaMalloc(&c->match, bt::match_scratch_bytes(mframes, max_pairs, n_max)) == cudaSuccess &&
             cudaMalloc(&c->matches, PN * 8) == cudaSuccess && cudaMalloc(&c->n_matches, (size_t)max_pairs * 4) == cudaSuccess &&
-            cudaMalloc(&c->best_key, (size_t)max_pairs * 8) == cudaSuccess;
+            cudaMalloc(&c->rscratch, bt::ransac_scratch_bytes(max_pairs, max_hyp)) == cudaSuccess;
   if (ok) {
     c->ms = bt::carve_match_scratch(c->match, mframes, max_pairs, n_max);
+    c->rs = bt::carve_ransac_scratch(c->rscratch, max_pairs, max_hyp);
     // TMA tensor map over the fp16 unit descriptors: 2-D [rows][128], 64 x 128 boxes, 128B swizzle
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
@@ -287,7 +289,7 @@ bt_status bt_ransac(bt_ctx *c, const bt_keypoints *kp, const int32_t *pairs, con
   if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
   if (P == 0) return BT_OK;
   if (!pairs || !pair_uid || !matches || !n_matches || !records) return fail(c, BT_EINVAL, "bt_ransac: NULL buffer");
-  bt::launch_ransac(kview(kp), pairs, pair_uid, P, matches, n_matches, *prm, c->best_key, records,
+  bt::launch_ransac(kview(kp), pairs, pair_uid, P, matches, n_matches, *prm, c->rs, records,
                     bt::rec_words(kp->n_max), hyp_counts, nullptr, 0.f, (cudaStream_t)stream, c->launch);
   return after_launch(c, "bt_ransac");
 }
@@ -328,7 +330,7 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
   }
   bt::launch_match(kview(kp), pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches, c->n_matches,
                    ms, c->launch);
-  bt::launch_ransac(kview(kp), pairs, uid, P, c->matches, c->n_matches, *rprm, c->best_key, records, rw, nullptr,
+  bt::launch_ransac(kview(kp), pairs, uid, P, c->matches, c->n_matches, *rprm, c->rs, records, rw, nullptr,
                     eprm ? node_pose : nullptr, eprm ? eprm->huber_m : 0.f, ms, c->launch);
   if (eprm) {
     cudaEventRecord(c->ev_join, c->side);
@@ -421,7 +423,7 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
   const float ratio = mprm ? mprm->ratio : 1.f;
   bt::launch_match(kview(&dk), c->st_pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches,
                    c->n_matches, st, c->launch);
-  bt::launch_ransac(kview(&dk), c->st_pairs, c->st_uid, P, c->matches, c->n_matches, *rprm, c->best_key,
+  bt::launch_ransac(kview(&dk), c->st_pairs, c->st_uid, P, c->matches, c->n_matches, *rprm, c->rs,
                     c->st_records, rw, nullptr, eprm ? c->st_pose : nullptr, eprm ? eprm->huber_m : 0.f, st,
                     c->launch);
   if (eprm) {
@@ -446,7 +448,7 @@ bt_status bt_compose_poses(bt_ctx *c, const bt_pose *a, const bt_pose *b, bt_pos
 }
 
 static const char *kKernelNames[bt::K_COUNT] = {"k_desc_prep", "k_match_tc", "k_rescore", "k_mutual",
-                                                 "k_ransac_score", "k_ransac_finish", "k_dense_prep",
+                                                 "k_ransac_hyp", "k_ransac_score", "k_ransac_finish", "k_dense_prep",
                                                  "k_dense", "k_dense_reduce", "k_compose"};
 
 static cudaEvent_t take_event(bt_ctx *c) {

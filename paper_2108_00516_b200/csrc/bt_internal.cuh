@@ -35,7 +35,7 @@ struct MapView {
 
 // ---- launch bookkeeping: counts kernels and (optionally) brackets each with events ----
 enum KernelId {
-  K_DESC_PREP = 0, K_MATCH_TC, K_RESOLVE, K_MUTUAL, K_RANSAC_SCORE, K_RANSAC_FINISH, K_DENSE_PREP,
+  K_DESC_PREP = 0, K_MATCH_TC, K_RESOLVE, K_MUTUAL, K_RANSAC_HYP, K_RANSAC_SCORE, K_RANSAC_FINISH, K_DENSE_PREP,
   K_DENSE, K_DENSE_REDUCE, K_COMPOSE,
   K_COUNT
 };
@@ -68,10 +68,17 @@ MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_m
 void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, const MatchScratch &S,
                   const CUtensorMap *tmap, int force_fallback, int32_t *matches, int32_t *n_matches,
                   cudaStream_t s, Launch &L);
-// RANSAC scoring + finish (+ optional Eq. (2) blocks at node poses)
+// RANSAC hypotheses + balanced scoring + finish (+ optional Eq. (2) blocks at node poses).
+// Carved at capacity offsets: hypothesis buffer then per-hypothesis counts.
+struct RansacScratch {
+  void *hyp;
+  int32_t *counts;
+};
+size_t ransac_scratch_bytes(int max_pairs, int max_hyp);
+RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp);
 void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, int P,
                    const int32_t *matches, const int32_t *n_matches, const bt_ransac_params &prm,
-                   unsigned long long *best_key, uint32_t *records, int rec_stride,
+                   const RansacScratch &rs, uint32_t *records, int rec_stride,
                    int32_t *hyp_counts, const bt_pose *node_pose, float huber, cudaStream_t s,
                    Launch &L);
 // dense Eq. (3): edges either explicit (edges != null) or derived from pairs (2 per pair)

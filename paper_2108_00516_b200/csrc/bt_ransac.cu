@@ -1,21 +1,26 @@
 // bt_ransac.cu — RANSAC over 3-pair samples, best-hypothesis refit and the Eq. (2)
 // feature-edge blocks.
 //
-//  k_ransac_score   two hypotheses per lane: Philox4x32-10 (counter (h, uid, 0, 0), key =
-//                   seed) -> distinct triple (reading R6) -> closed-form 3-point Arun in
-//                   fp64 (triangle frames + 2x2 Procrustes, reading R7) -> R, t in fp32.
-//                   The lane then scores its hypotheses against the pair's correspondences
-//                   (staged in shared memory, 64 B each: p_a, p_b, O = n_b n_a^T, read as
-//                   warp broadcasts): 15 FMA-pipe ops for the distance gate, 9 FFMA for the
-//                   normal gate, skipped by a warp vote when no lane's distance gate passes.
-//                   The per-pair best is an atomicMax on the key ((count+1) << 32 | ~h):
-//                   max count, ties -> lowest h (R11).
-//  k_ransac_finish  one CTA per pair: re-derives h* (same noinline solver => same bits),
+//  k_ransac_hyp     per hypothesis: Philox4x32-10 (counter (h, uid, 0, 0), key = seed) ->
+//                   distinct triple (reading R6) -> closed-form 3-point Arun in fp64
+//                   (triangle frames + 2x2 Procrustes, reading R7) -> R, t in fp32, written to
+//                   an L2-resident buffer in the scoring kernel's f32x2 pair layout.
+//  k_ransac_score   balanced: the flat (pair, 512-hypothesis block, correspondence) work range
+//                   is cut into one equal slice per resident CTA slot (no partial last wave).
+//                   Two hypotheses per lane packed in f32x2 registers: every FMA of the
+//                   distance gate (15 FMA-pipe ops) and normal gate (9) is one FFMA2 for both
+//                   (sm_100a), the correspondence (staged in shared memory, 64 B each: p_a,
+//                   -p_b, O = n_b n_a^T) a broadcast operand; the normal gate is skipped by a
+//                   warp vote when no lane's distance gate passes; counts are integer atomics.
+//  k_ransac_finish  one CTA per pair: best key ((count+1) << 32 | ~h) over the counts — max
+//                   count, ties -> lowest h (R11) — re-derives h* (same solver => same bits),
 //                   inlier mask by ballot, refit by fp64 cross-covariance + Jacobi SVD with
 //                   the det fix (north star, R12), status, and — when node poses are given —
 //                   the Eq. (2) J^T W J blocks at those poses in fp64, reduced in a fixed order.
 #include <cuda_runtime.h>
 #include <math_constants.h>
+
+#include <climits>
 
 #include "bt_internal.cuh"
 
@@ -25,7 +30,7 @@ namespace {
 constexpr int kScoreThreads = 256;
 constexpr int kHypPerThread = 2;
 constexpr int kHypPerBlock = kScoreThreads * kHypPerThread;
-constexpr int kMaxChunk = 1024;           // correspondences staged per smem pass
+constexpr int kMaxChunk = 512;            // correspondences staged per smem pass (32 KB)
 
 // ---------------------------------------------------------------- Philox4x32-10
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
@@ -128,6 +133,23 @@ __device__ __forceinline__ bool solve3(const float *A, const float *B, double ta
   return true;
 }
 
+// solve hypothesis h of a pair from its matched points staged as sab[m] = (a_m, b_m)
+__device__ __forceinline__ bool make_hypothesis_staged(int h, uint32_t uid, uint32_t k0, uint32_t k1, int M,
+                                                       const float *sab, double tau, float *out) {
+  const uint4 r = philox4x32_10(make_uint4((uint32_t)h, uid, 0u, 0u), k0, k1);
+  int s[3];
+  sample_triple(r, M, s[0], s[1], s[2]);
+  float A[9], B[9];
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      A[3 * k + c] = sab[6 * s[k] + c];
+      B[3 * k + c] = sab[6 * s[k] + 3 + c];
+    }
+  return solve3(A, B, tau, out);
+}
+
 // gather the sample's points and solve hypothesis h of a pair
 __device__ __forceinline__ bool make_hypothesis(int h, uint32_t uid, uint32_t k0, uint32_t k1, int M,
                                                 const int32_t *mt, const float *pa_f, const float *pb_f,
@@ -149,16 +171,17 @@ __device__ __forceinline__ bool make_hypothesis(int h, uint32_t uid, uint32_t k0
 }
 
 // ---------------------------------------------------------------- the inlier test
-// Correspondence m as four float4: q0 = (ax, ay, az, bx), q1 = (by, bz, O00, O01),
+// Correspondence m as four float4: q0 = (ax, ay, az, -bx), q1 = (-by, -bz, O00, O01),
 // q2 = (O02, O10, O11, O12), q3 = (O20, O21, O22, 0) with O = n_b n_a^T, so that
 // (R n_a) . n_b = <R, O>_F.  The gates are folded into the FMA chains:
 //   d' = |R a + t - b|^2 - delta^2  (< 0: distance gate, 15 FMA-pipe ops),
 //   c' = <R, O> - cos(alpha)        (> 0: normal gate, 9 FFMA).
-// Explicit _rn intrinsics: the scoring and finish kernels compute identical bits.
+// x + (-b) is x - b exactly.  Explicit _rn intrinsics: the scoring kernel (packed f32x2, one
+// IEEE fma.rn per lane) and the finish kernel (scalar) compute identical bits.
 __device__ __forceinline__ float dist_term(const float *T, const float4 q0, const float4 q1, float ndelta2) {
-  const float ex = __fsub_rn(__fmaf_rn(T[0], q0.x, __fmaf_rn(T[1], q0.y, __fmaf_rn(T[2], q0.z, T[9]))), q0.w);
-  const float ey = __fsub_rn(__fmaf_rn(T[3], q0.x, __fmaf_rn(T[4], q0.y, __fmaf_rn(T[5], q0.z, T[10]))), q1.x);
-  const float ez = __fsub_rn(__fmaf_rn(T[6], q0.x, __fmaf_rn(T[7], q0.y, __fmaf_rn(T[8], q0.z, T[11]))), q1.y);
+  const float ex = __fadd_rn(__fmaf_rn(T[0], q0.x, __fmaf_rn(T[1], q0.y, __fmaf_rn(T[2], q0.z, T[9]))), q0.w);
+  const float ey = __fadd_rn(__fmaf_rn(T[3], q0.x, __fmaf_rn(T[4], q0.y, __fmaf_rn(T[5], q0.z, T[10]))), q1.x);
+  const float ez = __fadd_rn(__fmaf_rn(T[6], q0.x, __fmaf_rn(T[7], q0.y, __fmaf_rn(T[8], q0.z, T[11]))), q1.y);
   return __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmaf_rn(ez, ez, ndelta2)));
 }
 __device__ __forceinline__ float normal_term(const float *T, const float4 q1, const float4 q2, const float4 q3,
@@ -184,11 +207,58 @@ __device__ __forceinline__ bool inlier(const float *T, const float4 q0, const fl
   return pass_bit(dist_term(T, q0, q1, ndelta2), normal_term(T, q1, q2, q3, ncosa)) != 0u;
 }
 
+// ---- packed fp32x2 (sm_100a FFMA2 / FADD2): lane .x = hypothesis 0, .y = hypothesis 1 of a
+// thread; a correspondence scalar is a broadcast operand (no extra instruction in SASS)
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk(float lo, float hi) {
+  f32x2 d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, float b, f32x2 c) {      // a * {b, b} + c
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(pk(b, b)), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fma2v(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, float b) {               // a + {b, b}
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(pk(b, b)));
+  return d;
+}
+__device__ __forceinline__ void split(f32x2 x, unsigned &lo, unsigned &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(x));
+}
+// the scalar dist_term / normal_term, op for op, on both hypotheses of a thread
+__device__ __forceinline__ f32x2 dist_term2(const f32x2 *T, const float4 q0, const float4 q1, f32x2 nd2) {
+  const f32x2 ex = add2(fma2(T[0], q0.x, fma2(T[1], q0.y, fma2(T[2], q0.z, T[9]))), q0.w);
+  const f32x2 ey = add2(fma2(T[3], q0.x, fma2(T[4], q0.y, fma2(T[5], q0.z, T[10]))), q1.x);
+  const f32x2 ez = add2(fma2(T[6], q0.x, fma2(T[7], q0.y, fma2(T[8], q0.z, T[11]))), q1.y);
+  return fma2v(ex, ex, fma2v(ey, ey, fma2v(ez, ez, nd2)));
+}
+__device__ __forceinline__ f32x2 normal_term2(const f32x2 *T, const float4 q1, const float4 q2, const float4 q3,
+                                              f32x2 nc2) {
+  f32x2 c = fma2(T[0], q1.z, nc2);
+  c = fma2(T[1], q1.w, c);
+  c = fma2(T[2], q2.x, c);
+  c = fma2(T[3], q2.y, c);
+  c = fma2(T[4], q2.z, c);
+  c = fma2(T[5], q2.w, c);
+  c = fma2(T[6], q3.x, c);
+  c = fma2(T[7], q3.y, c);
+  c = fma2(T[8], q3.z, c);
+  return c;
+}
+
 __device__ __forceinline__ void pack_corr(const float *pa, const float *na, const float *pb,
                                           const float *nb, float4 &q0, float4 &q1, float4 &q2,
                                           float4 &q3) {
-  q0 = make_float4(pa[0], pa[1], pa[2], pb[0]);
-  q1 = make_float4(pb[1], pb[2], __fmul_rn(nb[0], na[0]), __fmul_rn(nb[0], na[1]));
+  q0 = make_float4(pa[0], pa[1], pa[2], -pb[0]);
+  q1 = make_float4(-pb[1], -pb[2], __fmul_rn(nb[0], na[0]), __fmul_rn(nb[0], na[1]));
   q2 = make_float4(__fmul_rn(nb[0], na[2]), __fmul_rn(nb[1], na[0]), __fmul_rn(nb[1], na[1]),
                    __fmul_rn(nb[1], na[2]));
   q3 = make_float4(__fmul_rn(nb[2], na[0]), __fmul_rn(nb[2], na[1]), __fmul_rn(nb[2], na[2]), 0.f);
@@ -200,116 +270,197 @@ struct ScoreArgs {
   const uint32_t *uid;
   const int32_t *matches;
   const int32_t *n_matches;
-  int n_hyp, chunk;
+  int P, n_hyp, nb, chunk;
   uint32_t k0, k1;
   float ndelta2, ncosa;
   double tau;
-  unsigned long long *best_key;
-  int32_t *hyp_counts;
+  f32x2 *hyp;                  // [P][nb][12][kScoreThreads]: T (R row-major, t) of hypotheses
+                               // (b*512 + t, b*512 + 256 + t) packed per thread; never-passing
+                               // sentinel when degenerate or h >= n_hyp
+  int32_t *counts;             // [P][n_hyp] inlier counts (accumulated); < 0 => degenerate
 };
 
-// One CTA = 512 hypotheses of one pair, two per thread (Philox + fp64 solve by the thread
-// that scores them: lane = hypothesis).  The pair's correspondences are staged in shared
-// memory (AoS, 64 B each) and every warp walks them in the same order, so each q-load is a
-// broadcast.  Per correspondence a warp vote skips the normal gate when no lane's distance
-// gate passes (outlier correspondences), and counts stay in registers: no cross-lane
-// reduction of counts.
-__global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) {
-  extern __shared__ float4 sq[];                                  // [chunk][4]
-  const int chunk = A.chunk;
+// One thread per hypothesis: Philox4x32-10 (counter (h, uid, 0, 0), key = seed) -> distinct
+// triple (R6) -> closed-form 3-point Arun in fp64 (R7) -> R, t rounded to fp32, written to the
+// L2-resident hypothesis buffer in the scoring kernel's f32x2 pair layout; the count is
+// initialised to 0, or to a very negative value when degenerate (it stays < 0 whatever the
+// scoring adds — degenerate hypotheses never pass the distance gate anyway).
+constexpr int kHypThreads = 256;
+constexpr int kHypIter = 8;                                       // hypotheses per thread (loop)
+
+// One CTA = kHypThreads x kHypIter hypotheses of one pair.  The pair's matched points are first
+// staged in shared memory (match list, then a_m / b_m), then one thread per hypothesis per
+// iteration: Philox4x32-10 (counter (h, uid, 0, 0), key = seed) -> distinct triple (R6) ->
+// closed-form 3-point Arun in fp64 (R7) -> R, t rounded to fp32, written to the L2-resident
+// hypothesis buffer in the scoring kernel's f32x2 pair layout.  The count is initialised to 0,
+// or to a very negative value when degenerate (it stays < 0 whatever the scoring adds).
+__global__ void __launch_bounds__(kHypThreads) k_ransac_hyp(ScoreArgs A) {
+  extern __shared__ float sab[];                                  // [M][6] = (a_m, b_m)
   const int p = blockIdx.y;
-  const int lane = threadIdx.x & 31;
   const int M = A.n_matches[p];
-  const int H = A.n_hyp;
-  const int h_base = blockIdx.x * kHypPerBlock + threadIdx.x;     // hypotheses h_base + k * kScoreThreads
+  if (M < 3) return;
   const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
   const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
   const float *pa_f = A.kp.pts + (size_t)fa * A.kp.n_max * 3, *pb_f = A.kp.pts + (size_t)fb * A.kp.n_max * 3;
-  const float *na_f = A.kp.nrm + (size_t)fa * A.kp.n_max * 3, *nb_f = A.kp.nrm + (size_t)fb * A.kp.n_max * 3;
-
-  if (M < 3) {                                                   // FEW_MATCHES: no samples
-    if (A.hyp_counts)
-#pragma unroll
-      for (int k = 0; k < kHypPerThread; ++k)
-        if (h_base + k * kScoreThreads < H) A.hyp_counts[(size_t)p * H + h_base + k * kScoreThreads] = -1;
-    return;
+  const uint32_t uid = A.uid[p];
+  for (int x = threadIdx.x; x < 2 * M; x += kHypThreads) {
+    const int m = x >> 1, side = x & 1;
+    const float *src = (side ? pb_f : pa_f) + 3 * mt[x];
+    sab[6 * m + 3 * side] = src[0];
+    sab[6 * m + 3 * side + 1] = src[1];
+    sab[6 * m + 3 * side + 2] = src[2];
   }
-  // solve the hypotheses one after the other (no unrolling: one solver's registers live
-  // at a time), park them in shared memory, then hold all four in registers for scoring
-  float *hs = reinterpret_cast<float *>(sq + 4 * chunk);          // [kHypPerThread][kScoreThreads][12]
-  unsigned valid_bits = 0u;
+  __syncthreads();
 #pragma unroll 1
-  for (int k = 0; k < kHypPerThread; ++k) {
-    const int h = h_base + k * kScoreThreads;
-    float Tk[12];
-    const bool v = h < H && make_hypothesis(h, A.uid[p], A.k0, A.k1, M, mt, pa_f, pb_f, A.tau, Tk);
-    if (!v) {                                                    // never passes the distance gate
-#pragma unroll
-      for (int q = 0; q < 12; ++q) Tk[q] = 0.f;
-      Tk[11] = 3.0e38f;
+  for (int it = 0; it < kHypIter; ++it) {
+    const int h = (blockIdx.x * kHypIter + it) * kHypThreads + threadIdx.x;
+    if (h >= A.nb * kHypPerBlock) break;                           // past the pair's slots
+    float T[12];
+    bool v = false;
+    if (h < A.n_hyp) {
+      v = make_hypothesis_staged(h, uid, A.k0, A.k1, M, sab, A.tau, T);
+      A.counts[(size_t)p * A.n_hyp + h] = v ? 0 : INT_MIN / 2;
     }
-    valid_bits |= (unsigned)v << k;
-    float4 *dst = reinterpret_cast<float4 *>(hs + 12 * (k * kScoreThreads + threadIdx.x));
-    dst[0] = make_float4(Tk[0], Tk[1], Tk[2], Tk[3]);
-    dst[1] = make_float4(Tk[4], Tk[5], Tk[6], Tk[7]);
-    dst[2] = make_float4(Tk[8], Tk[9], Tk[10], Tk[11]);
-  }
-  float T[kHypPerThread][12];
+    if (!v) {                                                      // never passes the distance gate
 #pragma unroll
-  for (int k = 0; k < kHypPerThread; ++k) {
-    const float4 *src = reinterpret_cast<const float4 *>(hs + 12 * (k * kScoreThreads + threadIdx.x));
-    const float4 x = src[0], y = src[1], z = src[2];
-    T[k][0] = x.x; T[k][1] = x.y; T[k][2] = x.z; T[k][3] = x.w;
-    T[k][4] = y.x; T[k][5] = y.y; T[k][6] = y.z; T[k][7] = y.w;
-    T[k][8] = z.x; T[k][9] = z.y; T[k][10] = z.z; T[k][11] = z.w;
-  }
-  unsigned cnt[kHypPerThread];
-#pragma unroll
-  for (int k = 0; k < kHypPerThread; ++k) cnt[k] = 0u;
-  for (int cs = 0; cs < M; cs += chunk) {
-    const int len = min(chunk, M - cs);
-    __syncthreads();
-    for (int k = threadIdx.x; k < len; k += kScoreThreads) {
-      const int i = mt[2 * (cs + k)], j = mt[2 * (cs + k) + 1];
-      float4 q0, q1, q2, q3;
-      pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
-      sq[4 * k] = q0; sq[4 * k + 1] = q1; sq[4 * k + 2] = q2; sq[4 * k + 3] = q3;
+      for (int q = 0; q < 12; ++q) T[q] = 0.f;
+      T[11] = 3.0e38f;
     }
-    __syncthreads();
+    const int b = h / kHypPerBlock, r = h - b * kHypPerBlock;
+    const int t = r % kScoreThreads, k = r / kScoreThreads;
+    float *dst = reinterpret_cast<float *>(A.hyp + ((size_t)p * A.nb + b) * 12 * kScoreThreads + t) + k;
+#pragma unroll
+    for (int q = 0; q < 12; ++q) dst[2 * q * kScoreThreads] = T[q];
+  }
+}
+
+constexpr int kPlanChunk = kScoreThreads;                         // pairs per prefix chunk
+
+// exclusive prefix of the scoring work W_q = nb * M_q (M_q >= 3) over pairs [c0, c0 + 256),
+// offset by carry: cpre[k] for pair c0 + k, cpre[256] = end of the chunk (CTA-uniform call)
+__device__ void plan_chunk(const ScoreArgs &A, int c0, long long carry, long long *cpre, long long *wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = c0 + threadIdx.x;
+  const int Mq = q < A.P ? A.n_matches[q] : 0;
+  const long long w = Mq >= 3 ? (long long)A.nb * Mq : 0;
+  long long incl = w;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();                                                 // previous chunk fully read
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  long long woff = 0, tot = 0;
+#pragma unroll
+  for (int w2 = 0; w2 < kScoreThreads / 32; ++w2) { woff += w2 < warp ? wsum[w2] : 0; tot += wsum[w2]; }
+  cpre[threadIdx.x] = carry + woff + incl - w;
+  if (threadIdx.x == 0) cpre[kPlanChunk] = carry + tot;
+  __syncthreads();
+}
+
+// Balanced scoring.  The work of all pairs — (pair p, block b of kHypPerBlock hypotheses,
+// correspondence m) steps, W_p = nb * M_p — is one flat range cut into gridDim.x equal slices
+// (grid = the resident CTA slots), so every CTA gets the same number of tests whatever the
+// pairs' match counts: no partial last wave.  A slice crosses segment boundaries.  Per segment
+// the CTA loads its 512 hypotheses (two per thread, coalesced 8-B f32x2 loads), stages the
+// segment's correspondences in shared memory (AoS, 64 B each, read as warp broadcasts) and
+// scores with packed f32x2 FMAs (both hypotheses of a thread in one FFMA2; a correspondence
+// scalar is a broadcast operand).  Per correspondence a warp vote skips the normal gate when no
+// lane's distance gate passes.  Counts are added with integer atomics (exact, order-independent).
+__global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) {
+  extern __shared__ float4 sq[];                                  // [chunk][4] correspondences
+  __shared__ long long cpre[kPlanChunk + 1];
+  __shared__ long long wsum[kScoreThreads / 32];
+  const int H = A.n_hyp;
+  // total work: prefix over all pairs, chunk by chunk (one chunk for P <= 256)
+  long long total = 0;
+  int c0 = 0;
+  for (int c = 0; c < A.P; c += kPlanChunk) {
+    plan_chunk(A, c, total, cpre, wsum);
+    total = cpre[kPlanChunk];
+    c0 = c;
+  }
+  const long long lo0 = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
+  if (lo0 >= hi) return;                                           // CTA-uniform
+  if (A.P > kPlanChunk) {                                          // re-plan from the chunk holding lo0
+    long long carry = 0;
+    for (c0 = 0;; c0 += kPlanChunk) {
+      plan_chunk(A, c0, carry, cpre, wsum);
+      if (cpre[kPlanChunk] > lo0 || c0 + kPlanChunk >= A.P) break;
+      carry = cpre[kPlanChunk];
+    }
+  }
+  int p;
+  {
+    int a = 0, b = min(kPlanChunk, A.P - c0);                      // cpre[a] <= lo0 < cpre[b]
+    while (b - a > 1) { const int mid = (a + b) >> 1; if (cpre[mid] <= lo0) a = mid; else b = mid; }
+    p = c0 + a;
+  }
+  long long lo = lo0;
+  while (lo < hi) {
+    for (;;) {                                                     // skip pairs without work
+      if (p - c0 >= kPlanChunk) {
+        const long long carry = cpre[kPlanChunk];
+        c0 += kPlanChunk;
+        plan_chunk(A, c0, carry, cpre, wsum);
+      }
+      const long long end_p = p + 1 - c0 < kPlanChunk ? cpre[p + 1 - c0] : cpre[kPlanChunk];
+      if (end_p > lo) break;
+      ++p;
+    }
+    const int M = A.n_matches[p];
+    const long long rel = lo - cpre[p - c0];
+    const int b = (int)(rel / M), m0 = (int)(rel - (long long)b * M);
+    const int m1 = (int)min((long long)M, m0 + (hi - lo));
+    const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+    const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
+    const float *pa_f = A.kp.pts + (size_t)fa * A.kp.n_max * 3, *pb_f = A.kp.pts + (size_t)fb * A.kp.n_max * 3;
+    const float *na_f = A.kp.nrm + (size_t)fa * A.kp.n_max * 3, *nb_f = A.kp.nrm + (size_t)fb * A.kp.n_max * 3;
+    static_assert(kHypPerThread == 2, "packed f32x2 scoring holds two hypotheses per thread");
+    f32x2 T2[12];                                                  // coalesced 8-B loads, L2-resident
+    {
+      const f32x2 *src = A.hyp + ((size_t)p * A.nb + b) * 12 * kScoreThreads + threadIdx.x;
+#pragma unroll
+      for (int q = 0; q < 12; ++q) T2[q] = __ldcg(src + q * kScoreThreads);
+    }
+    const f32x2 nd2 = pk(A.ndelta2, A.ndelta2), nc2 = pk(A.ncosa, A.ncosa);
+    unsigned cnt[kHypPerThread];
+#pragma unroll
+    for (int k = 0; k < kHypPerThread; ++k) cnt[k] = 0u;
+    for (int cs = m0; cs < m1; cs += A.chunk) {
+      const int len = min(A.chunk, m1 - cs);
+      __syncthreads();
+      for (int k = threadIdx.x; k < len; k += kScoreThreads) {
+        const int i = mt[2 * (cs + k)], j = mt[2 * (cs + k) + 1];
+        float4 q0, q1, q2, q3;
+        pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
+        sq[4 * k] = q0; sq[4 * k + 1] = q1; sq[4 * k + 2] = q2; sq[4 * k + 3] = q3;
+      }
+      __syncthreads();
 #pragma unroll 2
-    for (int m = 0; m < len; ++m) {
-      const float4 q0 = sq[4 * m], q1 = sq[4 * m + 1];
-      float d[kHypPerThread];
-      unsigned any_neg = 0u;
-#pragma unroll
-      for (int k = 0; k < kHypPerThread; ++k) {
-        d[k] = dist_term(T[k], q0, q1, A.ndelta2);
-        any_neg |= __float_as_uint(d[k]);
-      }
-      if (__any_sync(0xffffffffu, any_neg >> 31)) {
-        const float4 q2 = sq[4 * m + 2], q3 = sq[4 * m + 3];
-#pragma unroll
-        for (int k = 0; k < kHypPerThread; ++k) cnt[k] += pass_bit(d[k], normal_term(T[k], q1, q2, q3, A.ncosa));
+      for (int m = 0; m < len; ++m) {
+        const float4 q0 = sq[4 * m], q1 = sq[4 * m + 1];
+        const f32x2 d = dist_term2(T2, q0, q1, nd2);
+        unsigned d0, d1;
+        split(d, d0, d1);
+        if (__any_sync(0xffffffffu, (int)(d0 | d1) < 0)) {
+          const float4 q2 = sq[4 * m + 2], q3 = sq[4 * m + 3];
+          unsigned c0_, c1_;
+          split(normal_term2(T2, q1, q2, q3, nc2), c0_, c1_);
+          cnt[0] += (d0 & ~c0_) >> 31;
+          cnt[1] += (d1 & ~c1_) >> 31;
+        }
       }
     }
-  }
-  unsigned long long key = 0ull;
 #pragma unroll
-  for (int k = 0; k < kHypPerThread; ++k) {
-    const int h = h_base + k * kScoreThreads;
-    if (h >= H) continue;
-    const int count = ((valid_bits >> k) & 1u) ? (int)cnt[k] : -1;
-    if (A.hyp_counts) A.hyp_counts[(size_t)p * H + h] = count;
-    const unsigned long long kk =
-        ((unsigned long long)(uint32_t)(count + 1) << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)h);
-    key = kk > key ? kk : key;
+    for (int k = 0; k < kHypPerThread; ++k) {
+      const int h = b * kHypPerBlock + k * kScoreThreads + threadIdx.x;
+      if (h < H && cnt[k]) atomicAdd(A.counts + (size_t)p * H + h, (int)cnt[k]);
+    }
+    lo += m1 - m0;
   }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-    key = other > key ? other : key;
-  }
-  if (lane == 0 && key) atomicMax(A.best_key + p, key);
 }
 
 // ---------------------------------------------------------------- finish: refit + Eq. (2)
@@ -415,7 +566,8 @@ struct FinishArgs {
   uint32_t k0, k1;
   float ndelta2, ncosa;
   double tau;
-  const unsigned long long *best_key;
+  const int32_t *counts;         // [P][n_hyp] from k_ransac_score (< 0: degenerate)
+  int32_t *hyp_counts;           // optional [P][n_hyp] output (-1: degenerate / no samples)
   uint32_t *records;
   int rec_stride;
   const bt_pose *node_pose;      // null: no feature blocks
@@ -437,6 +589,7 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   const int p = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_max = A.kp.n_max, W = mask_words(n_max);
+  unsigned long long key_all;
   const int M = A.n_matches[p];
   uint32_t *rec = A.records + (size_t)p * A.rec_stride;
   const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
@@ -444,8 +597,31 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   const float *pa_f = A.kp.pts + (size_t)fa * n_max * 3, *pb_f = A.kp.pts + (size_t)fb * n_max * 3;
   const float *na_f = A.kp.nrm + (size_t)fa * n_max * 3, *nb_f = A.kp.nrm + (size_t)fb * n_max * 3;
 
+  // best hypothesis: key ((count + 1) << 32 | ~h) — max count, ties -> lowest h (R11)
+  __shared__ unsigned long long wkey[kFinThreads / 32];
+  {
+    unsigned long long kk = 0ull;
+    const int32_t *cp = A.counts + (size_t)p * A.n_hyp;
+    for (int h = tid; h < A.n_hyp; h += kFinThreads) {
+      const int cnt = M >= 3 ? max(cp[h], -1) : -1;
+      if (A.hyp_counts) A.hyp_counts[(size_t)p * A.n_hyp + h] = cnt;
+      const unsigned long long x = ((unsigned long long)(uint32_t)(cnt + 1) << 32) | (0xFFFFFFFFu - (uint32_t)h);
+      kk = x > kk ? x : kk;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, kk, o);
+      kk = other > kk ? other : kk;
+    }
+    if (lane == 0) wkey[warp] = kk;
+    __syncthreads();
+    kk = 0ull;
+#pragma unroll
+    for (int w = 0; w < kFinThreads / 32; ++w) kk = wkey[w] > kk ? wkey[w] : kk;
+    key_all = kk;
+  }
   int status = BT_PAIR_OK, best_h = -1;
-  const unsigned long long key = A.best_key[p];
+  const unsigned long long key = key_all;
   const uint32_t c1 = (uint32_t)(key >> 32);
   if (M < 3) status = BT_PAIR_FEW_MATCHES;
   else if (c1 == 0u) status = BT_PAIR_FEW_INLIERS;                 // every hypothesis degenerate
@@ -662,40 +838,65 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
 
 }  // namespace
 
+static size_t hyp_slots(int max_pairs, int max_hyp) {
+  return (size_t)max_pairs * ((max_hyp + kHypPerBlock - 1) / kHypPerBlock) * kHypPerBlock;
+}
+
+size_t ransac_scratch_bytes(int max_pairs, int max_hyp) {
+  return (hyp_slots(max_pairs, max_hyp) * 48 + 255) / 256 * 256 + ((size_t)max_pairs * max_hyp * 4 + 255) / 256 * 256;
+}
+
+RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp) {
+  RansacScratch r;
+  r.hyp = scratch;
+  r.counts = (int32_t *)((char *)scratch + (hyp_slots(max_pairs, max_hyp) * 48 + 255) / 256 * 256);
+  return r;
+}
+
 void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, int P,
                    const int32_t *matches, const int32_t *n_matches, const bt_ransac_params &prm,
-                   unsigned long long *best_key, uint32_t *records, int rec_stride,
+                   const RansacScratch &rs, uint32_t *records, int rec_stride,
                    int32_t *hyp_counts, const bt_pose *node_pose, float huber, cudaStream_t s,
                    Launch &L) {
   if (P <= 0) return;
   const int chunk = kp.n_max < kMaxChunk ? ((kp.n_max + 31) / 32) * 32 : kMaxChunk;   // multiple of 32
-  const size_t hyp_smem = (size_t)kHypPerThread * kScoreThreads * 12 * sizeof(float);
-  const size_t smem = (size_t)4 * chunk * sizeof(float4) + hyp_smem;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_ransac_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(4 * kMaxChunk * sizeof(float4) + hyp_smem));
-    attr_done = true;
+  const size_t smem = (size_t)4 * chunk * sizeof(float4);
+  static int score_slots = 0;
+  if (!score_slots) {
+    const int max_smem = (int)(4 * kMaxChunk * sizeof(float4));
+    cudaFuncSetAttribute(k_ransac_score, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    int dev = 0, n_sm = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ransac_score, kScoreThreads, max_smem);
+    score_slots = n_sm * (per_sm > 0 ? per_sm : 1);
   }
-  cudaMemsetAsync(best_key, 0, sizeof(unsigned long long) * P, s);
   ScoreArgs a;
+  a.hyp = (f32x2 *)rs.hyp;
+  a.counts = rs.counts;
   a.kp = kp; a.pairs = pairs; a.uid = uid; a.matches = matches; a.n_matches = n_matches;
-  a.n_hyp = prm.n_hyp; a.chunk = chunk;
+  a.P = P; a.n_hyp = prm.n_hyp; a.nb = (prm.n_hyp + kHypPerBlock - 1) / kHypPerBlock; a.chunk = chunk;
   a.k0 = (uint32_t)(prm.seed & 0xffffffffull); a.k1 = (uint32_t)(prm.seed >> 32);
   a.ndelta2 = (float)(-(double)prm.delta_m * (double)prm.delta_m);
   a.ncosa = -prm.cos_alpha;
   a.tau = prm.min_sigma_ratio;
-  a.best_key = best_key;
-  a.hyp_counts = hyp_counts;
-  dim3 grid((prm.n_hyp + kHypPerBlock - 1) / kHypPerBlock, P);
+  const size_t hyp_smem = (size_t)kp.n_max * 6 * sizeof(float);
+  static size_t hyp_attr = 0;
+  if (hyp_smem > hyp_attr) {
+    cudaFuncSetAttribute(k_ransac_hyp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hyp_smem);
+    hyp_attr = hyp_smem;
+  }
+  L.begin(K_RANSAC_HYP, s);
+  k_ransac_hyp<<<dim3((a.nb * kHypPerBlock / kHypThreads + kHypIter - 1) / kHypIter, P), kHypThreads, hyp_smem, s>>>(a);
+  L.end(K_RANSAC_HYP, s);
   L.begin(K_RANSAC_SCORE, s);
-  k_ransac_score<<<grid, kScoreThreads, smem, s>>>(a);
+  k_ransac_score<<<score_slots, kScoreThreads, smem, s>>>(a);
   L.end(K_RANSAC_SCORE, s);
   FinishArgs f;
   f.kp = kp; f.pairs = pairs; f.uid = uid; f.matches = matches; f.n_matches = n_matches;
   f.n_hyp = prm.n_hyp; f.min_inliers = prm.min_inliers;
   f.k0 = a.k0; f.k1 = a.k1; f.ndelta2 = a.ndelta2; f.ncosa = a.ncosa; f.tau = a.tau;
-  f.best_key = best_key; f.records = records; f.rec_stride = rec_stride;
+  f.counts = a.counts; f.hyp_counts = hyp_counts; f.records = records; f.rec_stride = rec_stride;
   f.node_pose = node_pose; f.huber = huber;
   L.begin(K_RANSAC_FINISH, s);
   const size_t fin_smem = (size_t)((mask_words(kp.n_max) * 32 + 3) & ~3) * sizeof(int) +
