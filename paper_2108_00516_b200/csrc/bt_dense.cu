@@ -24,12 +24,12 @@
 //  k_dense_scan   one CTA per frame: exclusive scan of the tile counts, so the frame's valid
 //                 source pixels form one compacted sequence cut into chunks of kTile entries.
 //  k_dense        one CTA per (frame, chunk) work item (grid-stride) — every chunk but a
-//                 frame's last is full, so no CTA reduces a mostly-empty border tile.  A chunk's
-//                 entries (located by binary search in the tile offsets) + their fp64 points are
-//                 staged in shared memory once and reused for every edge leaving the frame.
-//                 Per (entry, edge): fp32 projection, gather of the target validity + map entry
-//                 (all of a thread's gathers issued together), fp64 gates / residual, Huber,
-//                 29 running sums; per edge a 31-shuffle warp transpose reduction + smem.
+//                 frame's last is full.  A chunk's entries (located by binary search in the tile
+//                 offsets) + their fp64 points are staged in shared memory once and reused for
+//                 every edge leaving the frame; each warp owns whole edges (gathers pipelined
+//                 two entries ahead, one transpose reduction per (warp, edge)).
+//                 Per (entry, edge): fp32 projection, gather of the target validity + map entry,
+//                 fp64 residual difference then fp32 gates / Huber, 29 running sums.
 //  k_dense_reduce fixed-order fp64 sum of the per-tile partials of an edge (deterministic).
 #include <cuda_runtime.h>
 
@@ -61,7 +61,7 @@ struct DenseArgs {
   const int32_t *pairs;
   int E, stride, tx, ty, tiles;
   double gate2;
-  float cos_gate, huber;
+  float gate2f, cos_gate, huber;
   float *tji;                 // [E][12] T_j T_i^-1
   int32_t *elist;             // [F][E] outgoing edges per source frame, ascending
   int32_t *ecount;            // [F]
@@ -256,17 +256,54 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_scan(DenseArgs A) {
   }
 }
 
-constexpr int kEdgeBatch = 16;                // edges whose per-warp partials are held before one CTA barrier
-constexpr size_t kDenseSmem = kTile * (16 + 16 + 8 + 24) + (kDenseThreads / 32) * kEdgeBatch * 32 * 4;
+constexpr size_t kDenseSmem = kTile * (16 + 16 + 8 + 24);
+constexpr int kEdgeThreads = 256;                // k_dense CTA (8 warps, each owning edges)
 
-__global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
+// target-pixel gather of one (entry, edge) item, issued ahead of its use
+struct Gather {
+  float4 g0;                  // x_s.x, x_s.y (fp64 as 2 x 2 words)
+  float4 g1;                  // x_s.z (fp64), n_o,j.x, n_o,j.y
+  float nz;                   // n_o,j.z
+  bool ok;                    // projected into the frame onto a valid pixel
+};
+
+// project entry k of the staged chunk with T = T_j T_i^-1 and issue its target gathers
+__device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, const float (&T)[12], float fx, float fy,
+                                             float cx, float cy, int W, int H, const uint8_t *vm, const float4 *pm,
+                                             Gather &G) {
+  int tj = -1;
+  if (k < n) {
+    const float4 a = sP[k];
+    const float yx = fmaf(T[0], a.x, fmaf(T[1], a.y, fmaf(T[2], a.z, T[9])));
+    const float yy = fmaf(T[3], a.x, fmaf(T[4], a.y, fmaf(T[5], a.z, T[10])));
+    const float yz = fmaf(T[6], a.x, fmaf(T[7], a.y, fmaf(T[8], a.z, T[11])));
+    if (yz > 0.f) {
+      const float iz = __fdividef(1.0f, yz);
+      const float up = fmaf(fx * yx, iz, cx), vp = fmaf(fy * yy, iz, cy);
+      const float xu = floorf(up + 0.5f), xv = floorf(vp + 0.5f);
+      if (xu >= 0.f && xu < (float)W && xv >= 0.f && xv < (float)H) tj = (int)xv * W + (int)xu;
+    }
+  }
+  const int tt = tj < 0 ? 0 : tj;                                  // validity and map entry together
+  const float4 *q4 = pm + 3 * (size_t)tt;
+  G.ok = tj >= 0 && __ldg(vm + tt) != 0;
+  G.g0 = __ldg(q4);
+  G.g1 = __ldg(q4 + 1);
+  G.nz = __ldg(reinterpret_cast<const float *>(q4 + 2));
+}
+
+// Each warp owns whole edges of the chunk: warp w walks edges w, w + 8, ... leaving the frame,
+// and for each one all of the chunk's entries (lane l: entries l, l + 32, ...), with the target
+// gathers software-pipelined two entries ahead so loads stay in flight.  One 31-shuffle
+// transpose reduction per (warp, edge) puts the 29 sums straight into the edge's chunk partial:
+// no shared reduction buffer, no barrier between edges.
+__global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];
   float4 *sP = reinterpret_cast<float4 *>(dsm);                    // p (camera, fp32), (u | v << 16)
   float4 *sN = sP + kTile;                                         // n_i (camera), n_o,i.x
   float2 *sNo = reinterpret_cast<float2 *>(sN + kTile);            // n_o,i.y, n_o,i.z
   double *sX = reinterpret_cast<double *>(sNo + kTile);            // p - t_i (fp64)
-  float *red = reinterpret_cast<float *>(sX + 3 * kTile);          // [warp][kEdgeBatch][32]
-  int *sCb = reinterpret_cast<int *>(red + (kDenseThreads / 32) * kEdgeBatch * 32);  // [F + 1] chunk base per frame
+  int *sCb = reinterpret_cast<int *>(sX + 3 * kTile);              // [F + 1] chunk base per frame
   int *sOff = sCb + A.mp.n_frames + 1;                             // [tiles + 1] of the current frame
   const int F = A.mp.n_frames;
   const int W = A.mp.W, H = A.mp.H, npx = W * H;
@@ -289,112 +326,90 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
   __syncthreads();
   const int total = sCb[F];
   for (int ch = blockIdx.x; ch < total; ch += gridDim.x) {
-  int f = 0;
-  {
-    int lo = 0, hi = F;                                            // sCb[lo] <= ch < sCb[hi]
-    while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (sCb[mid] <= ch) lo = mid; else hi = mid; }
-    f = lo;
-  }
-  const int cl = ch - sCb[f];                                      // chunk of frame f
-  const int32_t *offg = A.offs + (size_t)f * (A.tiles + 1);
-  for (int k = threadIdx.x; k <= A.tiles; k += kDenseThreads) sOff[k] = offg[k];
-  __syncthreads();
-  const int n = min(kTile, sOff[A.tiles] - cl * kTile);
-  const int ne = A.ecount[f];
-  double Rd[9];                                                    // R_i (fp64)
-  {
-    const bt_pose P = A.node_pose[f];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) Rd[k] = P.R[k];
-    const double t0 = P.t[0], t1 = P.t[1], t2 = P.t[2];
-    const float4 *src = A.entries + (size_t)f * A.tiles * kTile * 2;
-    for (int k = threadIdx.x; k < n; k += kDenseThreads) {
-      const int gi = cl * kTile + k;                               // compacted entry index within frame f
-      int lo = 0, hi = A.tiles;                                    // sOff[lo] <= gi < sOff[hi]
-      while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (sOff[mid] <= gi) lo = mid; else hi = mid; }
-      const float4 *e2 = src + ((size_t)lo * kTile + (gi - sOff[lo])) * 2;
-      const float4 a = e2[0], b = e2[1];
-      const int uv = __float_as_int(a.w), u = uv & 0xffff, v = uv >> 16;
-      const double d = a.z;                                        // p.z = depth exactly
-      sX[3 * k] = ((double)u - A.cxd) * d * A.ifxd - t0;
-      sX[3 * k + 1] = ((double)v - A.cyd) * d * A.ifyd - t1;
-      sX[3 * k + 2] = d - t2;
-      const double m0 = b.x, m1 = b.y, m2 = b.z;                   // n_o,i = R_i^T n_i
-      const float o0 = (float)(Rd[0] * m0 + Rd[3] * m1 + Rd[6] * m2);
-      const float o1 = (float)(Rd[1] * m0 + Rd[4] * m1 + Rd[7] * m2);
-      const float o2 = (float)(Rd[2] * m0 + Rd[5] * m1 + Rd[8] * m2);
-      sP[k] = a;
-      sN[k] = make_float4(b.x, b.y, b.z, o0);
-      sNo[k] = make_float2(o1, o2);
+    int f = 0;
+    {
+      int lo = 0, hi = F;                                          // sCb[lo] <= ch < sCb[hi]
+      while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (sCb[mid] <= ch) lo = mid; else hi = mid; }
+      f = lo;
     }
-  }
-  __syncthreads();
-  for (int ie0 = 0; ie0 < ne; ie0 += kEdgeBatch) {
-    const int nb_e = min(kEdgeBatch, ne - ie0);
-    for (int ib = 0; ib < nb_e; ++ib) {                           // warps run through the batch independently
-      const int e = A.elist[(size_t)f * A.E + ie0 + ib];
+    const int cl = ch - sCb[f];                                    // chunk of frame f
+    const int32_t *offg = A.offs + (size_t)f * (A.tiles + 1);
+    __syncthreads();                                               // previous chunk done with smem
+    for (int k = threadIdx.x; k <= A.tiles; k += kEdgeThreads) sOff[k] = offg[k];
+    __syncthreads();
+    const int n = min(kTile, sOff[A.tiles] - cl * kTile);
+    const int ne = A.ecount[f];
+    double Rd[9];                                                  // R_i (fp64)
+    {
+      const bt_pose P = A.node_pose[f];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) Rd[k] = P.R[k];
+
+      const double t0 = P.t[0], t1 = P.t[1], t2 = P.t[2];
+      const float4 *src = A.entries + (size_t)f * A.tiles * kTile * 2;
+      for (int k = threadIdx.x; k < n; k += kEdgeThreads) {
+        const int gi = cl * kTile + k;                             // compacted entry index within frame f
+        int lo = 0, hi = A.tiles;                                  // sOff[lo] <= gi < sOff[hi]
+        while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (sOff[mid] <= gi) lo = mid; else hi = mid; }
+        const float4 *e2 = src + ((size_t)lo * kTile + (gi - sOff[lo])) * 2;
+        const float4 a = e2[0], b = e2[1];
+        const int uv = __float_as_int(a.w), u = uv & 0xffff, v = uv >> 16;
+        const double d = a.z;                                      // p.z = depth exactly
+        sX[3 * k] = ((double)u - A.cxd) * d * A.ifxd - t0;
+        sX[3 * k + 1] = ((double)v - A.cyd) * d * A.ifyd - t1;
+        sX[3 * k + 2] = d - t2;
+        const double m0 = b.x, m1 = b.y, m2 = b.z;                 // n_o,i = R_i^T n_i
+        const float o0 = (float)(Rd[0] * m0 + Rd[3] * m1 + Rd[6] * m2);
+        const float o1 = (float)(Rd[1] * m0 + Rd[4] * m1 + Rd[7] * m2);
+        const float o2 = (float)(Rd[2] * m0 + Rd[5] * m1 + Rd[8] * m2);
+        sP[k] = a;
+        sN[k] = make_float4(b.x, b.y, b.z, o0);
+        sNo[k] = make_float2(o1, o2);
+      }
+    }
+    __syncthreads();
+
+    for (int ie = warp; ie < ne; ie += kEdgeThreads / 32) {
+      const int e = A.elist[(size_t)f * A.E + ie];
       int fi, fj;
       edge_frames(A.edges, A.pairs, e, fi, fj);
-      const float *T = A.tji + 12 * e;
+      float T[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) T[q] = __ldg(A.tji + 12 * e + q);
       const size_t off_j = (size_t)fj * npx;
       const uint8_t *vm = A.vmap + off_j;
       const float4 *pm = reinterpret_cast<const float4 *>(A.pmap + off_j);
       float acc[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) acc[k] = 0.f;
-      // phase 1: project every entry of this thread; phase 2: issue all of its gathers;
-      // phase 3: gates, residual, accumulation
-      int tj[kPer];
-#pragma unroll
-      for (int s = 0; s < kPer; ++s) {
-        const int k = threadIdx.x + s * kDenseThreads;
-        tj[s] = -1;
-        if (k < n) {
-          const float4 a = sP[k];
-          const float yx = fmaf(__ldg(T + 0), a.x, fmaf(__ldg(T + 1), a.y, fmaf(__ldg(T + 2), a.z, __ldg(T + 9))));
-          const float yy = fmaf(__ldg(T + 3), a.x, fmaf(__ldg(T + 4), a.y, fmaf(__ldg(T + 5), a.z, __ldg(T + 10))));
-          const float yz = fmaf(__ldg(T + 6), a.x, fmaf(__ldg(T + 7), a.y, fmaf(__ldg(T + 8), a.z, __ldg(T + 11))));
-          if (yz > 0.f) {
-            const float iz = __fdividef(1.0f, yz);
-            const float up = fmaf(A.fx * yx, iz, A.cx), vp = fmaf(A.fy * yy, iz, A.cy);
-            const float xu = floorf(up + 0.5f), xv = floorf(vp + 0.5f);
-            if (xu >= 0.f && xu < (float)W && xv >= 0.f && xv < (float)H) tj[s] = (int)xv * W + (int)xu;
-          }
-        }
-      }
-      bool gv[kPer];
-      float4 g0[kPer], g1[kPer], g2[kPer];
-#pragma unroll
-      for (int s = 0; s < kPer; ++s) {                             // validity and map entry together
-        const int tt = tj[s] < 0 ? 0 : tj[s];
-        const float4 *q4 = pm + 3 * (size_t)tt;
-        gv[s] = tj[s] >= 0 && __ldg(vm + tt) != 0;
-        g0[s] = __ldg(q4);
-        g1[s] = __ldg(q4 + 1);
-        g2[s] = __ldg(q4 + 2);
-      }
-#pragma unroll
-      for (int s = 0; s < kPer; ++s) {
-        if (!gv[s]) continue;
-        const int k = threadIdx.x + s * kDenseThreads;
+      for (int q = 0; q < 32; ++q) acc[q] = 0.f;
+      Gather G0, G1;
+      issue_gather(sP, lane, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, G0);
+      issue_gather(sP, lane + 32, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, G1);
+      for (int k = lane; k < n; k += 32) {
+        const Gather G = G0;
+        G0 = G1;
+        issue_gather(sP, k + 64, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, G1);
+        if (!G.ok) continue;
         // target map entry: x_s = R_j^T (s - t_j) (fp64), n_o,j (fp32)
-        const double xs0 = __hiloint2double(__float_as_int(g0[s].y), __float_as_int(g0[s].x));
-        const double xs1 = __hiloint2double(__float_as_int(g0[s].w), __float_as_int(g0[s].z));
-        const double xs2 = __hiloint2double(__float_as_int(g1[s].y), __float_as_int(g1[s].x));
-        const float mj0 = g1[s].z, mj1 = g1[s].w, mj2 = g2[s].x;
-        // q - p = R_i x_s - (p - t_i)
-        const double dq0 = fma(Rd[0], xs0, fma(Rd[1], xs1, Rd[2] * xs2)) - sX[3 * k];
-        const double dq1 = fma(Rd[3], xs0, fma(Rd[4], xs1, Rd[5] * xs2)) - sX[3 * k + 1];
-        const double dq2 = fma(Rd[6], xs0, fma(Rd[7], xs1, Rd[8] * xs2)) - sX[3 * k + 2];
-        const double dist2 = fma(dq0, dq0, fma(dq1, dq1, dq2 * dq2));
+        const double xs0 = __hiloint2double(__float_as_int(G.g0.y), __float_as_int(G.g0.x));
+        const double xs1 = __hiloint2double(__float_as_int(G.g0.w), __float_as_int(G.g0.z));
+        const double xs2 = __hiloint2double(__float_as_int(G.g1.y), __float_as_int(G.g1.x));
+        const float mj0 = G.g1.z, mj1 = G.g1.w, mj2 = G.nz;
+        // q - p = R_i x_s - (p - t_i): the cancelling difference in fp64, then fp32 (the
+        // gates and r are ~1e-7 relative from the fp64 values: inside the band rule, R22)
+        const double *Rs = Rd;
+        const float dq0 = (float)(fma(Rs[0], xs0, fma(Rs[1], xs1, Rs[2] * xs2)) - sX[3 * k]);
+        const float dq1 = (float)(fma(Rs[3], xs0, fma(Rs[4], xs1, Rs[5] * xs2)) - sX[3 * k + 1]);
+        const float dq2 = (float)(fma(Rs[6], xs0, fma(Rs[7], xs1, Rs[8] * xs2)) - sX[3 * k + 2]);
+        const float dist2 = fmaf(dq0, dq0, fmaf(dq1, dq1, dq2 * dq2));
         const float4 nc = sN[k];
         const float2 no = sNo[k];
         const float c = fmaf(nc.w, mj0, fmaf(no.x, mj1, no.y * mj2));
-        if (!(dist2 < A.gate2 && c > A.cos_gate)) continue;
+        if (!(dist2 < A.gate2f && c > A.cos_gate)) continue;
         const float n0 = nc.x, n1 = nc.y, n2 = nc.z;
-        const float r = (float)fma((double)n0, dq0, fma((double)n1, dq1, (double)n2 * dq2));
+        const float r = fmaf(n0, dq0, fmaf(n1, dq1, n2 * dq2));
         const float4 a = sP[k];
-        const float qx = a.x + (float)dq0, qy = a.y + (float)dq1, qz = a.z + (float)dq2;
+        const float qx = a.x + dq0, qy = a.y + dq1, qz = a.z + dq2;
         const float ar = fabsf(r);
         const float w = ar <= A.huber ? 1.f : __fdividef(A.huber, ar);
         const float rho = ar <= A.huber ? 0.5f * r * r : A.huber * (ar - 0.5f * A.huber);
@@ -422,20 +437,8 @@ __global__ void __launch_bounds__(kDenseThreads, 2) k_dense(DenseArgs A) {
           acc[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
         }
       }
-      red[(warp * kEdgeBatch + ib) * 32 + lane] = acc[0];
+      A.partials[((size_t)e * A.tiles + cl) * kPartStride + lane] = acc[0];
     }
-    __syncthreads();
-    // CTA partial of each edge of the batch: fixed-order sum over the 8 warps
-    for (int x = threadIdx.x; x < nb_e * 32; x += kDenseThreads) {
-      const int ib = x >> 5, l = x & 31;
-      float s = 0.f;
-#pragma unroll
-      for (int w2 = 0; w2 < kDenseThreads / 32; ++w2) s += red[(w2 * kEdgeBatch + ib) * 32 + l];
-      const int e = A.elist[(size_t)f * A.E + ie0 + ib];
-      A.partials[((size_t)e * A.tiles + cl) * kPartStride + l] = s;
-    }
-    __syncthreads();
-  }
   }
 }
 
@@ -513,6 +516,7 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   a.ty = (mp.H + kTS - 1) / kTS;
   a.tiles = a.tx * a.ty;
   a.gate2 = (double)prm.dist_gate_m * (double)prm.dist_gate_m;
+  a.gate2f = (float)a.gate2;
   a.cos_gate = prm.cos_gate;
   a.huber = prm.huber_m;
   // carve the scratch
@@ -550,7 +554,7 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   // higher-priority match / RANSAC kernels interleave (bt_api.cu register_pairs_dev)
   const int grid = a.tiles * mp.n_frames;
   L.begin(K_DENSE, s);
-  k_dense<<<grid, kDenseThreads, smem, s>>>(a);
+  k_dense<<<grid, kEdgeThreads, smem, s>>>(a);
   L.end(K_DENSE, s);
   L.begin(K_DENSE_REDUCE, s);
   k_dense_reduce<<<E, 256, 0, s>>>(a.partials, a.nch, a.tiles, edges, pairs, out, out_stride, records,
