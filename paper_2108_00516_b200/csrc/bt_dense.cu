@@ -144,15 +144,18 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
   for (int k = 0; k < kPer; ++k) { in[k] = false; dep[k] = 0.f; nr[3 * k] = nr[3 * k + 1] = nr[3 * k + 2] = 0.f; }
   if (v < H) {
     if ((W & 3) == 0 && u0 + kPer <= W) {
-      // mask, depth and normals requested together (one memory round trip, not two)
+      // the mask first; depth and normals only where one of the 4 pixels is in the mask
+      // (~1/8 of the frame): one extra round trip, ~5x fewer bytes
       const uchar4 m4 = __ldg(reinterpret_cast<const uchar4 *>(A.mp.mask + off + pix0));
-      const float4 d4 = __ldg(reinterpret_cast<const float4 *>(A.mp.depth + off + pix0));
-      const float4 *n4 = reinterpret_cast<const float4 *>(A.mp.normal + 3 * (off + pix0));
-      const float4 a = __ldg(n4), b = __ldg(n4 + 1), c = __ldg(n4 + 2);
-      dep[0] = d4.x; dep[1] = d4.y; dep[2] = d4.z; dep[3] = d4.w;
-      nr[0] = a.x; nr[1] = a.y; nr[2] = a.z; nr[3] = a.w; nr[4] = b.x; nr[5] = b.y;
-      nr[6] = b.z; nr[7] = b.w; nr[8] = c.x; nr[9] = c.y; nr[10] = c.z; nr[11] = c.w;
       in[0] = m4.x != 0; in[1] = m4.y != 0; in[2] = m4.z != 0; in[3] = m4.w != 0;
+      if (in[0] | in[1] | in[2] | in[3]) {
+        const float4 d4 = __ldg(reinterpret_cast<const float4 *>(A.mp.depth + off + pix0));
+        const float4 *n4 = reinterpret_cast<const float4 *>(A.mp.normal + 3 * (off + pix0));
+        const float4 a = __ldg(n4), b = __ldg(n4 + 1), c = __ldg(n4 + 2);
+        dep[0] = d4.x; dep[1] = d4.y; dep[2] = d4.z; dep[3] = d4.w;
+        nr[0] = a.x; nr[1] = a.y; nr[2] = a.z; nr[3] = a.w; nr[4] = b.x; nr[5] = b.y;
+        nr[6] = b.z; nr[7] = b.w; nr[8] = c.x; nr[9] = c.y; nr[10] = c.z; nr[11] = c.w;
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
@@ -168,11 +171,22 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
   const bt_pose P = A.node_pose[f];
   bool src[kPer];
   int n_mine = 0;
+  bool vv[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k)
+    vv[k] = in[k] && dep[k] > 0.f && !(nr[3 * k] == 0.f && nr[3 * k + 1] == 0.f && nr[3 * k + 2] == 0.f);
+  if (v < H) {
+    if ((W & 3) == 0 && u0 + kPer <= W)
+      *reinterpret_cast<uchar4 *>(A.vmap + off + pix0) = make_uchar4(vv[0], vv[1], vv[2], vv[3]);
+    else
+#pragma unroll
+      for (int k = 0; k < kPer; ++k)
+        if (u0 + k < W) A.vmap[off + pix0 + k] = vv[k] ? 1 : 0;
+  }
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     const int u = u0 + k;
-    const bool valid = in[k] && dep[k] > 0.f && !(nr[3 * k] == 0.f && nr[3 * k + 1] == 0.f && nr[3 * k + 2] == 0.f);
-    if (v < H && u < W) A.vmap[off + pix0 + k] = valid ? 1 : 0;
+    const bool valid = vv[k];
     if (valid) {
       // x = R^T (p - t) in fp64 from the exact inputs; n_o = R^T n
       const double d = dep[k];
