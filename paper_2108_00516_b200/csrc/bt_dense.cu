@@ -13,7 +13,7 @@
 // p - t_i are fp64 and x_s is computed ONCE per target pixel per call (not per edge); R_i is
 // a per-CTA constant.
 //
-//  k_edge_prep    one thread per edge: T_j T_i^-1 (fp32, for the projection); one CTA per
+//  k_edge_setup   one thread per edge: T_j T_i^-1 (fp32, for the projection); one CTA per
 //                 source frame builds that frame's ordered list of outgoing edges.
 //  k_dense_prep   one CTA per (frame, 32x32 tile): coalesced vector reads (uchar4 mask,
 //                 float4 depth, 3 x float4 normals) of 4 pixels per thread; per valid pixel the
@@ -83,28 +83,29 @@ __device__ __forceinline__ void edge_frames(const int32_t *edges, const int32_t 
   }
 }
 
-__global__ void k_edge_consts(DenseArgs A) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= A.E) return;
-  int fi, fj;
-  edge_frames(A.edges, A.pairs, e, fi, fj);
-  // T_j T_i^-1: R = R_j R_i^T, t = t_j - R t_i
-  const bt_pose Pi = A.node_pose[fi], Pj = A.node_pose[fj];
-  double R[9];
-  for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c) {
-      double x = 0;
-      for (int k = 0; k < 3; ++k) x += (double)Pj.R[3 * r + k] * Pi.R[3 * c + k];
-      R[3 * r + c] = x;
-    }
-  float *o = A.tji + 12 * e;
-  for (int k = 0; k < 9; ++k) o[k] = (float)R[k];
-  for (int r = 0; r < 3; ++r)
-    o[9 + r] = (float)(Pj.t[r] - (R[3 * r] * Pi.t[0] + R[3 * r + 1] * Pi.t[1] + R[3 * r + 2] * Pi.t[2]));
-}
-
-// per source frame: the ascending list of edges leaving it (deterministic ballot compaction)
-__global__ void k_edge_lists(DenseArgs A) {
+// one launch for the per-edge / per-frame setup: blocks [0, F) build frame f's ascending list
+// of outgoing edges (deterministic ballot compaction); blocks F.. compute T_j T_i^-1 per edge
+__global__ void __launch_bounds__(256) k_edge_setup(DenseArgs A) {
+  if ((int)blockIdx.x >= A.mp.n_frames) {
+    const int e = (blockIdx.x - A.mp.n_frames) * blockDim.x + threadIdx.x;
+    if (e >= A.E) return;
+    int fi, fj;
+    edge_frames(A.edges, A.pairs, e, fi, fj);
+    // T_j T_i^-1: R = R_j R_i^T, t = t_j - R t_i
+    const bt_pose Pi = A.node_pose[fi], Pj = A.node_pose[fj];
+    double R[9];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        double x = 0;
+        for (int k = 0; k < 3; ++k) x += (double)Pj.R[3 * r + k] * Pi.R[3 * c + k];
+        R[3 * r + c] = x;
+      }
+    float *o = A.tji + 12 * e;
+    for (int k = 0; k < 9; ++k) o[k] = (float)R[k];
+    for (int r = 0; r < 3; ++r)
+      o[9 + r] = (float)(Pj.t[r] - (R[3 * r] * Pi.t[0] + R[3 * r + 1] * Pi.t[1] + R[3 * r + 2] * Pi.t[2]));
+    return;
+  }
   __shared__ int wsum[8];
   const int f = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -547,10 +548,7 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   a.pmap = (MapEntry *)p;    p += align256(F * npx * sizeof(MapEntry));
   a.vmap = (uint8_t *)p;
   L.begin(K_DENSE_PREP, s);
-  k_edge_consts<<<(E + 127) / 128, 128, 0, s>>>(a);
-  L.end(K_DENSE_PREP, s);
-  L.begin(K_DENSE_PREP, s);
-  k_edge_lists<<<mp.n_frames, 256, 0, s>>>(a);
+  k_edge_setup<<<mp.n_frames + (E + 255) / 256, 256, 0, s>>>(a);
   L.end(K_DENSE_PREP, s);
   L.begin(K_DENSE_PREP, s);
   k_dense_prep<<<dim3(a.tiles, mp.n_frames), kDenseThreads, 0, s>>>(a);

@@ -106,31 +106,51 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ float key_value(unsigned k) { return __uint_as_float(k); }
 
 // ---------------------------------------------------------------- descriptor prep
+constexpr int kPrepPerWarp = 4;                // keypoints per warp (loads issued together)
+
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_desc_prep(KpView kp, MatchScratch S, int n_pad) {
+  __shared__ unsigned wmax[kWarpsPerBlock];
   const int f = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i = blockIdx.x * kWarpsPerBlock + warp;
-  if (i >= n_pad) return;
+  const int i0 = (blockIdx.x * kWarpsPerBlock + warp) * kPrepPerWarp;
   const int n = min(kp.n_kp[f], kp.n_max);
-  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (i < n) a = reinterpret_cast<const float4 *>(kp.desc + ((size_t)f * kp.n_max + i) * kDim)[lane];
-  float s = __fmul_rn(a.x, a.x);
-  s = __fmaf_rn(a.y, a.y, s);
-  s = __fmaf_rn(a.z, a.z, s);
-  s = __fmaf_rn(a.w, a.w, s);
+  float4 a[kPrepPerWarp];
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const float nrm = sqrtf(s);
-  const float inv = nrm > 0.f ? 1.0f / nrm : 0.f;
-  __half2 h01 = __floats2half2_rn(a.x * inv, a.y * inv), h23 = __floats2half2_rn(a.z * inv, a.w * inv);
-  uint2 packed;
-  packed.x = *reinterpret_cast<uint32_t *>(&h01);
-  packed.y = *reinterpret_cast<uint32_t *>(&h23);
-  reinterpret_cast<uint2 *>(S.desc16 + ((size_t)f * n_pad + i) * kDim)[lane] = packed;
-  if (lane == 0) {
-    S.norm[(size_t)f * n_pad + i] = nrm;
-    if (i < n) atomicMax(S.maxnorm + f, __float_as_uint(nrm));       // nrm >= 0: bits are monotone
+  for (int q = 0; q < kPrepPerWarp; ++q) {
+    const int i = i0 + q;
+    a[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < n) a[q] = __ldg(reinterpret_cast<const float4 *>(kp.desc + ((size_t)f * kp.n_max + i) * kDim) + lane);
+  }
+  unsigned mx = 0u;
+#pragma unroll
+  for (int q = 0; q < kPrepPerWarp; ++q) {
+    const int i = i0 + q;
+    float s = __fmul_rn(a[q].x, a[q].x);
+    s = __fmaf_rn(a[q].y, a[q].y, s);
+    s = __fmaf_rn(a[q].z, a[q].z, s);
+    s = __fmaf_rn(a[q].w, a[q].w, s);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float nrm = sqrtf(s);
+    const float inv = nrm > 0.f ? 1.0f / nrm : 0.f;
+    if (i < n_pad) {
+      __half2 h01 = __floats2half2_rn(a[q].x * inv, a[q].y * inv), h23 = __floats2half2_rn(a[q].z * inv, a[q].w * inv);
+      uint2 packed;
+      packed.x = *reinterpret_cast<uint32_t *>(&h01);
+      packed.y = *reinterpret_cast<uint32_t *>(&h23);
+      reinterpret_cast<uint2 *>(S.desc16 + ((size_t)f * n_pad + i) * kDim)[lane] = packed;
+      if (lane == 0) S.norm[(size_t)f * n_pad + i] = nrm;
+    }
+    if (i < n) mx = max(mx, __float_as_uint(nrm));                 // nrm >= 0: bits are monotone
+  }
+  if (lane == 0) wmax[warp] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned m = 0u;
+#pragma unroll
+    for (int w = 0; w < kWarpsPerBlock; ++w) m = max(m, wmax[w]);
+    if (m) atomicMax(S.maxnorm + f, m);
   }
 }
 
@@ -474,9 +494,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_rescore(RescoreArgs A) 
 __global__ void __launch_bounds__(1024)
 k_mutual(KpView kp, const int32_t *__restrict__ pairs, const int32_t *__restrict__ nn_ab,
          const int32_t *__restrict__ nn_ba, const uint8_t *__restrict__ ratio_ok,
-         int32_t *__restrict__ matches, int32_t *__restrict__ n_matches) {
+         int32_t *__restrict__ matches, int32_t *__restrict__ n_matches, MatchScratch S) {
   __shared__ int warp_tot[32];
   const int p = blockIdx.x;
+  if (p == 0) {                            // last reader done: zero for the next call (no memsets)
+    for (int f = threadIdx.x; f < kp.n_frames; f += blockDim.x) S.maxnorm[f] = 0u;
+    if (threadIdx.x < 2) S.work_count[threadIdx.x] = 0u;
+  }
   const int fa = pairs[2 * p], fb = pairs[2 * p + 1];
   const int na = min(kp.n_kp[fa], kp.n_max), nb = min(kp.n_kp[fb], kp.n_max);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -543,6 +567,9 @@ MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_m
   S.nn_ab = (int32_t *)c;        c += al(P * n_max * 4);
   S.nn_ba = (int32_t *)c;        c += al(P * n_max * 4);
   S.ratio_ok = (uint8_t *)c;
+  // maxnorm and the queue counters are zero between calls: zeroed here, re-zeroed by k_mutual
+  cudaMemset(S.maxnorm, 0, F * 4);
+  cudaMemset(S.work_count, 0, 16);
   return S;
 }
 
@@ -558,13 +585,12 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
     cudaFuncSetAttribute(k_match_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
     attr = true;
   }
-  cudaMemsetAsync(S.maxnorm, 0, sizeof(unsigned) * kp.n_frames, s);
   L.begin(K_DESC_PREP, s);
-  k_desc_prep<<<dim3((n_pad + kWarpsPerBlock - 1) / kWarpsPerBlock, kp.n_frames), kWarpsPerBlock * 32, 0, s>>>(
+  constexpr int per_cta = kWarpsPerBlock * kPrepPerWarp;
+  k_desc_prep<<<dim3((n_pad + per_cta - 1) / per_cta, kp.n_frames), kWarpsPerBlock * 32, 0, s>>>(
       kp, S, n_pad);
   L.end(K_DESC_PREP, s);
   const float ratio2 = ratio >= 1.f ? 1.f : ratio * ratio;
-  cudaMemsetAsync(S.work_count, 0, 2 * sizeof(unsigned), s);
   TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2};
   L.begin(K_MATCH_TC, s);
   k_match_tc<<<dim3(rt_count, P, 2), kTcWarps * 32, kTcSmem, s>>>(*tmap, ta);
@@ -574,7 +600,7 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   k_rescore<<<dim3(2 * 148, 2), kWarpsPerBlock * 32, 0, s>>>(ra);
   L.end(K_RESOLVE, s);
   L.begin(K_MUTUAL, s);
-  k_mutual<<<P, 512, 0, s>>>(kp, pairs, S.nn_ab, S.nn_ba, S.ratio_ok, matches, n_matches);
+  k_mutual<<<P, 512, 0, s>>>(kp, pairs, S.nn_ab, S.nn_ba, S.ratio_ok, matches, n_matches, S);
   L.end(K_MUTUAL, s);
 }
 
