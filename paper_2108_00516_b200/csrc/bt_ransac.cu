@@ -13,7 +13,7 @@
 //                   -p_b, O = n_b n_a^T) a broadcast operand; the normal gate is skipped by a
 //                   warp vote when no lane's distance gate passes; counts are integer atomics.
 //  k_ransac_finish  one CTA per pair: best key ((count+1) << 32 | ~h) over the counts — max
-//                   count, ties -> lowest h (R11) — re-derives h* (same solver => same bits),
+//                   count, ties -> lowest h (R11) — reads T of h* from the hypothesis buffer,
 //                   inlier mask by ballot, refit by fp64 cross-covariance + Jacobi SVD with
 //                   the det fix (north star, R12), status, and — when node poses are given —
 //                   the Eq. (2) J^T W J blocks at those poses in fp64, reduced in a fixed order.
@@ -150,25 +150,6 @@ __device__ __forceinline__ bool make_hypothesis_staged(int h, uint32_t uid, uint
   return solve3(A, B, tau, out);
 }
 
-// gather the sample's points and solve hypothesis h of a pair
-__device__ __forceinline__ bool make_hypothesis(int h, uint32_t uid, uint32_t k0, uint32_t k1, int M,
-                                                const int32_t *mt, const float *pa_f, const float *pb_f,
-                                                double tau, float *out) {
-  const uint4 r = philox4x32_10(make_uint4((uint32_t)h, uid, 0u, 0u), k0, k1);
-  int s[3];
-  sample_triple(r, M, s[0], s[1], s[2]);
-  float A[9], B[9];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const int i = mt[2 * s[k]], j = mt[2 * s[k] + 1];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      A[3 * k + c] = pa_f[3 * i + c];
-      B[3 * k + c] = pb_f[3 * j + c];
-    }
-  }
-  return solve3(A, B, tau, out);
-}
 
 // ---------------------------------------------------------------- the inlier test
 // Correspondence m as four float4: q0 = (ax, ay, az, -bx), q1 = (-by, -bz, O00, O01),
@@ -567,6 +548,8 @@ struct FinishArgs {
   float ndelta2, ncosa;
   double tau;
   const int32_t *counts;         // [P][n_hyp] from k_ransac_score (< 0: degenerate)
+  const f32x2 *hyp;              // hypothesis buffer of k_ransac_hyp (same bits as a re-solve)
+  int nb;
   int32_t *hyp_counts;           // optional [P][n_hyp] output (-1: degenerate / no samples)
   uint32_t *records;
   int rec_stride;
@@ -577,7 +560,7 @@ struct FinishArgs {
 constexpr int kFinThreads = 256;
 constexpr int kFeatChunk = 512;                  // feature rows staged per pass (smem)
 // per-inlier feature data staged in smem: e(3) J(3x12) w rho
-constexpr int kFeatRow = 3 + 36 + 2;
+constexpr int kFeatRow = 3 * 13 + 2;             // per residual component q: J_q (12), e_q; w; rho
 
 __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   extern __shared__ int inl[];                     // [n_max] inlier match indices, in order
@@ -602,11 +585,27 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   {
     unsigned long long kk = 0ull;
     const int32_t *cp = A.counts + (size_t)p * A.n_hyp;
-    for (int h = tid; h < A.n_hyp; h += kFinThreads) {
-      const int cnt = M >= 3 ? max(cp[h], -1) : -1;
-      if (A.hyp_counts) A.hyp_counts[(size_t)p * A.n_hyp + h] = cnt;
-      const unsigned long long x = ((unsigned long long)(uint32_t)(cnt + 1) << 32) | (0xFFFFFFFFu - (uint32_t)h);
-      kk = x > kk ? x : kk;
+    if ((A.n_hyp & 3) == 0) {                                      // int4 loads, 4 hypotheses each
+      for (int h4 = tid; h4 < (A.n_hyp >> 2); h4 += kFinThreads) {
+        int4 c4 = make_int4(-1, -1, -1, -1);
+        if (M >= 3) c4 = __ldcg(reinterpret_cast<const int4 *>(cp) + h4);
+        const int cs[4] = {max(c4.x, -1), max(c4.y, -1), max(c4.z, -1), max(c4.w, -1)};
+        if (A.hyp_counts)
+          reinterpret_cast<int4 *>(A.hyp_counts + (size_t)p * A.n_hyp)[h4] = make_int4(cs[0], cs[1], cs[2], cs[3]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t h = 4 * h4 + q;
+          const unsigned long long x = ((unsigned long long)(uint32_t)(cs[q] + 1) << 32) | (0xFFFFFFFFu - h);
+          kk = x > kk ? x : kk;
+        }
+      }
+    } else {
+      for (int h = tid; h < A.n_hyp; h += kFinThreads) {
+        const int cnt = M >= 3 ? max(cp[h], -1) : -1;
+        if (A.hyp_counts) A.hyp_counts[(size_t)p * A.n_hyp + h] = cnt;
+        const unsigned long long x = ((unsigned long long)(uint32_t)(cnt + 1) << 32) | (0xFFFFFFFFu - (uint32_t)h);
+        kk = x > kk ? x : kk;
+      }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -627,15 +626,14 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   else if (c1 == 0u) status = BT_PAIR_FEW_INLIERS;                 // every hypothesis degenerate
   else best_h = (int)(0xFFFFFFFFu - (uint32_t)key);
 
-  if (tid == 0) {
-    bool ok = false;
-    if (best_h >= 0) {
-      float T[12];
-      ok = make_hypothesis(best_h, A.uid[p], A.k0, A.k1, M, mt, pa_f, pb_f, A.tau, T);
-      for (int k = 0; k < 12; ++k) Tb[k] = T[k];
-    }
-    if (!ok) {
-      for (int k = 0; k < 12; ++k) Tb[k] = (k == 0 || k == 4 || k == 8) ? 1.f : 0.f;
+  if (tid < 12) {                                                  // T of h* from the hypothesis buffer
+    if (best_h >= 0) {                                             // (count >= 0: non-degenerate)
+      const int b = best_h / kHypPerBlock, r = best_h - b * kHypPerBlock;
+      const float *src = reinterpret_cast<const float *>(A.hyp + ((size_t)p * A.nb + b) * 12 * kScoreThreads +
+                                                         r % kScoreThreads) + r / kScoreThreads;
+      Tb[tid] = __ldcg(src + 2 * tid * kScoreThreads);
+    } else {
+      Tb[tid] = (tid == 0 || tid == 4 || tid == 8) ? 1.f : 0.f;
     }
   }
   __syncthreads();
@@ -766,7 +764,7 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
       int a = 0;
       while (k >= 6 - a) { k -= 6 - a; ++a; }
       oa[s] = 6 + a; ob[s] = 6 + a + k; okind[s] = 0;
-    } else if (k < 90) { oa[s] = k - 78; okind[s] = 1; }
+    } else if (k < 90) { oa[s] = k - 78; ob[s] = 12; okind[s] = 1; }
     else if (k == 90) okind[s] = 2;
     else if (k == 91) okind[s] = 3;
   }
@@ -790,17 +788,17 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
       const double Sq[9] = {0, -pn[2], pn[1], pn[2], 0, -pn[0], -pn[1], pn[0], 0};
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        row[q] = (float)e[q];
+        row[13 * q + 12] = (float)e[q];
         // (R^T)[q][c] = R[c][q];  (R^T [p]x)[q][c] = sum_k R[k][q] S[k][c]
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          row[3 + 12 * q + c] = (float)-Ri[3 * c + q];
-          row[3 + 12 * q + 6 + c] = (float)Rj[3 * c + q];
+          row[13 * q + c] = (float)-Ri[3 * c + q];
+          row[13 * q + 6 + c] = (float)Rj[3 * c + q];
           double x = 0, y = 0;
 #pragma unroll
           for (int k = 0; k < 3; ++k) { x += Ri[3 * k + q] * Sp[3 * k + c]; y += Rj[3 * k + q] * Sq[3 * k + c]; }
-          row[3 + 12 * q + 3 + c] = (float)x;
-          row[3 + 12 * q + 9 + c] = (float)-y;
+          row[13 * q + 3 + c] = (float)x;
+          row[13 * q + 9 + c] = (float)-y;
         }
       }
       const double nrm = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
@@ -811,17 +809,24 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
       row[40] = (float)rho;
     }
     __syncthreads();
-    for (int r = warp; r < nc; r += kFinThreads / 32) {
-      const float *row = frow + r * kFeatRow;
-      const float *J = row + 3;
-      const float w = row[39];
+    // branch-free: H(a, b) and g(a) = H(a, 12) are the same 3-term dot product of row columns
+    // (g's column 12 is e); E and the count are selects.  Rows r and r + 8 per step (loads of
+    // both in flight), accumulated in the same row order as a one-row loop.
+    auto term = [&](const float *row, int s) {
+      const int a = oa[s], b = ob[s];
+      const float d = fmaf(row[a], row[b], fmaf(row[13 + a], row[13 + b], row[26 + a] * row[26 + b]));
+      return okind[s] <= 1 ? row[39] * d : (okind[s] == 2 ? row[40] : 1.f);
+    };
+    for (int r = warp; r < nc; r += 2 * (kFinThreads / 32)) {
+      const float *r0 = frow + r * kFeatRow;
+      const int r1i = r + kFinThreads / 32;
+      const float *r1 = frow + (r1i < nc ? r1i : r) * kFeatRow;
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
-        const int a = oa[s], b = ob[s];
-        if (okind[s] == 0) acc[s] = fmaf(w, J[a] * J[b] + J[12 + a] * J[12 + b] + J[24 + a] * J[24 + b], acc[s]);
-        else if (okind[s] == 1) acc[s] = fmaf(w, J[a] * row[0] + J[12 + a] * row[1] + J[24 + a] * row[2], acc[s]);
-        else if (okind[s] == 2) acc[s] += row[40];
-        else if (okind[s] == 3) acc[s] += 1.f;
+        if (okind[s] < 0) continue;
+        const float t0 = term(r0, s), t1 = term(r1, s);
+        acc[s] += t0;
+        if (r1i < nc) acc[s] += t1;
       }
     }
   }
@@ -896,7 +901,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   f.kp = kp; f.pairs = pairs; f.uid = uid; f.matches = matches; f.n_matches = n_matches;
   f.n_hyp = prm.n_hyp; f.min_inliers = prm.min_inliers;
   f.k0 = a.k0; f.k1 = a.k1; f.ndelta2 = a.ndelta2; f.ncosa = a.ncosa; f.tau = a.tau;
-  f.counts = a.counts; f.hyp_counts = hyp_counts; f.records = records; f.rec_stride = rec_stride;
+  f.counts = a.counts; f.hyp = a.hyp; f.nb = a.nb; f.hyp_counts = hyp_counts; f.records = records; f.rec_stride = rec_stride;
   f.node_pose = node_pose; f.huber = huber;
   L.begin(K_RANSAC_FINISH, s);
   const size_t fin_smem = (size_t)((mask_words(kp.n_max) * 32 + 3) & ~3) * sizeof(int) +
