@@ -14,7 +14,7 @@
 //                warpgroups read TMEM with tcgen05.ld (row = TMEM lane, each warpgroup half the
 //                columns), rank d' = |b|^2 - 2 |a||b| S (= d_hat - |a|^2) and keep the three
 //                smallest as packed (order-preserving value | index) keys with a branch-free
-//                min/max network.  Both directions recompute the tile on the tensor cores
+//                min/max network (columns past n_b rank at +inf: no per-element bound check).  Both directions recompute the tile on the tensor cores
 //                rather than reducing columns across lanes.  The epilogue certifies each row
 //                (below) and decides it, or queues it for k_rescore.
 //  certificate   With the bound
@@ -218,8 +218,10 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
   auto stage_consts = [&](int c) {
     for (int jj = tid; jj < kN; jj += kTcWarps * 32) {
       const int j = c * kN + jj;
+      // a column past n_b ranks at +inf: it sorts after every real column (certify then sees
+      // v - v1 = inf, as for a missing key), so the loop needs no per-element bound check
       const float v = j < nb ? A.S.norm[(size_t)fb * n_pad + j] : 0.f;
-      cconst[(c & 1) * kN + jj] = make_float2(-2.f * v, v * v);
+      cconst[(c & 1) * kN + jj] = make_float2(-2.f * v, j < nb ? v * v : CUDART_INF_F);
     }
   };
   auto load_b = [&](int c) {                                      // thread 0 only
@@ -292,7 +294,6 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
       BT_TMEM_LD32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(buf * kN + cc * 32), v);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       const float4 *cb4 = reinterpret_cast<const float4 *>(cconst + buf * kN + cc * 32);
-      const int ncol = nb - j0;                                   // >= 1; < 32 only in the last block
       const unsigned jbase = (unsigned)j0;
 #pragma unroll
       for (int col = 0; col < 32; col += 2) {
@@ -300,12 +301,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
         // d'' = d' + c_row >= 0, so the float bits order like the values
         const float d0 = __fadd_rn(__fmaf_rn(na_n * cb.x, __uint_as_float(v[col]), cb.y), c_row);
         const float d1 = __fadd_rn(__fmaf_rn(na_n * cb.z, __uint_as_float(v[col + 1]), cb.w), c_row);
-        unsigned k0 = (__float_as_uint(d0) & ~imask) | (jbase + col);
-        unsigned k1 = (__float_as_uint(d1) & ~imask) | (jbase + col + 1);
-        if (ncol < 32) {                                          // uniform; only the final block
-          if (col >= ncol) k0 = kNone;
-          if (col + 1 >= ncol) k1 = kNone;
-        }
+        const unsigned k0 = (__float_as_uint(d0) & ~imask) | (jbase + col);
+        const unsigned k1 = (__float_as_uint(d1) & ~imask) | (jbase + col + 1);
         const unsigned a3 = min(r3, max(r2, k0)), a2 = min(r2, max(r1, k0));
         r1 = min(r1, k0); r2 = a2; r3 = a3;
         const unsigned b3 = min(s3, max(s2, k1)), b2 = min(s2, max(s1, k1));
