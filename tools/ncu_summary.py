@@ -19,7 +19,9 @@ METRICS = [
     ("dram__bytes_write.sum", "DRAM write (MB)", 1),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %", 1),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %", 1),
-    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe %", 1),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe inst %", 1),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe cycles %", 1),
+    ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", "FMA-heavy cycles % (elapsed)", 1),
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe %", 1),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %", 1),
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 pipe %", 1),
@@ -45,7 +47,9 @@ for r in rows[2:]:
 
 lines = [f"# ncu --set full summary ({os.path.basename(rep)})", "",
          "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
-         "(cold cache, serialised, replayed: compare shares, not absolutes).", "",
+         "(cold cache, serialised, replayed: compare shares, not absolutes).  'FMA pipe inst %' counts an "
+         "FFMA2 (packed fp32x2, k_ransac_score) as one instruction; 'FMA pipe cycles %' / 'FMA-heavy "
+         "cycles %' measure the pipe's occupancy (FFMA2 issues on the FMA-heavy pipe).", "",
          "| kernel | launches | " + " | ".join(m[1] for m in METRICS) + " |",
          "|---|---|" + "---|" * len(METRICS)]
 traffic = {}
