@@ -78,6 +78,14 @@ def _setup(L):
     L.bto_dense_edge.argtypes = [_f32p, _f32p, _u8p, _f32p, _f32p, _u8p, C.c_int32, C.c_int32,
                                  C.c_double, C.c_double, C.c_double, C.c_double, _f32p, _f32p,
                                  C.c_double, C.c_double, C.c_double, C.c_int32, _f64p, _vp, _vp]
+    L.bto_se3_exp.argtypes = [_f64p, _f64p, _f64p]
+    L.bto_se3_adjoint.argtypes = [_f64p, _f64p, _f64p]
+    L.bto_graph_system.restype = C.c_int32
+    L.bto_graph_system.argtypes = [C.c_int32, _f32p, _i32p, C.c_int32, _f64p, _vp, _vp, C.c_double, C.c_double,
+                                   _f64p, _f64p, _f64p]
+    L.bto_graph_step.restype = C.c_int32
+    L.bto_graph_step.argtypes = [C.c_int32, _f32p, _i32p, C.c_int32, _f64p, _vp, _vp, C.c_double, C.c_double,
+                                 C.c_int32, _f64p, _f32p, _f64p]
 
 
 def _c(a, dt):
@@ -250,3 +258,60 @@ def register_pair(scene, a: int, b: int, uid: int, n_hyp: int, seed: int, node_p
                                          scene.normal[a], scene.mask[a], scene.K, node_poses[b],
                                          node_poses[a], **dense)
     return rec
+
+
+# ------------------------------------------------------------ NEXT-1: pose-graph GN step
+def se3_exp(xi):
+    """SE(3) exponential of a (v, w) twist -> (R [3][3], t [3]) (PAPER.md P:83 T = exp(xi))."""
+    R = np.zeros(9)
+    t = np.zeros(3)
+    lib().bto_se3_exp(_c(xi, np.float64), R, t)
+    return R.reshape(3, 3), t
+
+
+def se3_adjoint(R, t):
+    """6x6 adjoint of T = (R, t) on (v, w) twists: exp(Adj d) T = T exp(d)."""
+    A = np.zeros(36)
+    lib().bto_se3_adjoint(_c(R, np.float64).reshape(-1), _c(t, np.float64), A)
+    return A.reshape(6, 6)
+
+
+def _graph_inputs(poses, pairs, feat, dense_ij, dense_ji):
+    poses = _c(poses, np.float32).reshape(-1, 12)
+    pairs = _c(pairs, np.int32).reshape(-1, 2)
+    feat = _c(feat, np.float64).reshape(len(pairs), -1)[:, :96]
+    feat = _c(feat, np.float64)
+    dij = None if dense_ij is None else _c(_c(dense_ij, np.float64).reshape(len(pairs), -1)[:, :32], np.float64)
+    dji = None if dense_ji is None else _c(_c(dense_ji, np.float64).reshape(len(pairs), -1)[:, :32], np.float64)
+    return poses, pairs, feat, dij, dji
+
+
+def graph_system(poses, pairs, feat, dense_ij=None, dense_ji=None, lambda_f=1.0, lambda_g=1.0):
+    """Gauss-Newton system of Eq. (1) from per-pair Eq. (2) blocks feat[P][96] and
+    the Eq. (3) blocks of both directed edges [P][32] at node poses [N][12]: (A, b, (E_f, E_g))."""
+    poses, pairs, feat, dij, dji = _graph_inputs(poses, pairs, feat, dense_ij, dense_ji)
+    n = 6 * len(poses)
+    A = np.zeros(n * n)
+    b = np.zeros(n)
+    e = np.zeros(2)
+    st = lib().bto_graph_system(len(poses), poses, pairs.reshape(-1), len(pairs), feat.reshape(-1), _ptr(dij),
+                                _ptr(dji), float(lambda_f), float(lambda_g), A, b, e)
+    if st != 0:
+        raise ValueError("bad pair list")
+    return A.reshape(n, n), b, tuple(e)
+
+
+def graph_step(poses, pairs, feat, dense_ij=None, dense_ji=None, lambda_f=1.0, lambda_g=1.0, fixed_node=0):
+    """One Gauss-Newton step: solve A d = -b (Cholesky; the fixed node's and
+    unconstrained DOFs pinned), T_i <- exp(d_i) T_i.  Returns (delta [N][6], poses [N][12],
+    (E_f, E_g) at the input poses)."""
+    poses, pairs, feat, dij, dji = _graph_inputs(poses, pairs, feat, dense_ij, dense_ji)
+    N = len(poses)
+    d = np.zeros(6 * N)
+    out = np.zeros(12 * N, np.float32)
+    e = np.zeros(2)
+    st = lib().bto_graph_step(N, poses, pairs.reshape(-1), len(pairs), feat.reshape(-1), _ptr(dij), _ptr(dji),
+                              float(lambda_f), float(lambda_g), int(fixed_node), d, out, e)
+    if st != 0:
+        raise np.linalg.LinAlgError("pose-graph system not positive definite")
+    return d.reshape(N, 6), out.reshape(N, 12), tuple(e)

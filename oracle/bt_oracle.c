@@ -621,3 +621,205 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
   out[44] = al_E;
   out[45] = al_H;
 }
+
+/* ======================================================================= NEXT-1: pose graph
+   PAPER.md §IV-D: Gauss-Newton on Eq. (1) with IRLS weights, the update
+   xi <- xi [+] d accumulated on the left, T_i = exp(xi_i); the initial frame's node fixed. */
+
+void bto_se3_exp(const double xi[6], double R[9], double t[3]) {
+  const double v[3] = {xi[0], xi[1], xi[2]}, w[3] = {xi[3], xi[4], xi[5]};
+  const double th2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2], th = sqrt(th2);
+  double A, B, Cc;                                 /* sin th / th, (1 - cos th)/th^2, (th - sin th)/th^3 */
+  if (th < 1e-6) {
+    A = 1.0 - th2 / 6.0;
+    B = 0.5 - th2 / 24.0;
+    Cc = 1.0 / 6.0 - th2 / 120.0;
+  } else {
+    A = sin(th) / th;
+    B = (1.0 - cos(th)) / th2;
+    Cc = (th - sin(th)) / (th2 * th);
+  }
+  double W[9], W2[9];
+  skew(w, W);
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      double x = 0.0;
+      for (int k = 0; k < 3; ++k) x += W[3 * r + k] * W[3 * k + c];
+      W2[3 * r + c] = x;
+    }
+  for (int k = 0; k < 9; ++k) {
+    const double I = (k % 4 == 0) ? 1.0 : 0.0;
+    R[k] = I + A * W[k] + B * W2[k];
+  }
+  for (int r = 0; r < 3; ++r) {
+    double x = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      const double I = (r == c) ? 1.0 : 0.0;
+      x += (I + B * W[3 * r + c] + Cc * W2[3 * r + c]) * v[c];
+    }
+    t[r] = x;
+  }
+}
+
+void bto_se3_adjoint(const double R[9], const double t[3], double Adj[36]) {
+  double S[9];
+  skew(t, S);
+  for (int k = 0; k < 36; ++k) Adj[k] = 0.0;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      double tr = 0.0;
+      for (int k = 0; k < 3; ++k) tr += S[3 * r + k] * R[3 * k + c];
+      Adj[6 * r + c] = R[3 * r + c];
+      Adj[6 * r + 3 + c] = tr;
+      Adj[6 * (3 + r) + 3 + c] = R[3 * r + c];
+    }
+}
+
+/* unpack a 21-entry upper-triangular row-major 6x6 block */
+static void sym6(const double *u, double H[36]) {
+  int k = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) { H[6 * a + b] = u[k]; H[6 * b + a] = u[k]; ++k; }
+}
+
+static void add_block(double *A, int n, int bi, int bj, const double *M, double s) {
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) A[(size_t)(6 * bi + r) * n + 6 * bj + c] += s * M[6 * r + c];
+}
+
+/* A_ii += H, A_ij += -H Adj, A_ji += -(H Adj)^T, A_jj += Adj^T H Adj, b_i += g, b_j += -Adj^T g */
+static void add_dense(double *A, double *b, int n, int i, int j, const double *blk, const double Ri[9],
+                      const double ti[3], const double Rj[9], const double tj[3], double lam) {
+  double H[36], Adj[36], HA[36], AHA[36], R[9], t[3];
+  sym6(blk, H);
+  /* T_i T_j^-1 = (R_i R_j^T, t_i - R_i R_j^T t_j) */
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      double x = 0.0;
+      for (int k = 0; k < 3; ++k) x += Ri[3 * r + k] * Rj[3 * c + k];
+      R[3 * r + c] = x;
+    }
+  for (int r = 0; r < 3; ++r) t[r] = ti[r] - (R[3 * r] * tj[0] + R[3 * r + 1] * tj[1] + R[3 * r + 2] * tj[2]);
+  bto_se3_adjoint(R, t, Adj);
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) {
+      double x = 0.0;
+      for (int k = 0; k < 6; ++k) x += H[6 * r + k] * Adj[6 * k + c];
+      HA[6 * r + c] = x;
+    }
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) {
+      double x = 0.0;
+      for (int k = 0; k < 6; ++k) x += Adj[6 * k + r] * HA[6 * k + c];
+      AHA[6 * r + c] = x;
+    }
+  double HAt[36];
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) HAt[6 * r + c] = HA[6 * c + r];
+  add_block(A, n, i, i, H, lam);
+  add_block(A, n, i, j, HA, -lam);
+  add_block(A, n, j, i, HAt, -lam);
+  add_block(A, n, j, j, AHA, lam);
+  for (int r = 0; r < 6; ++r) {
+    double x = 0.0;
+    for (int k = 0; k < 6; ++k) x += Adj[6 * k + r] * blk[21 + k];
+    b[6 * i + r] += lam * blk[21 + r];
+    b[6 * j + r] -= lam * x;
+  }
+}
+
+int32_t bto_graph_system(int32_t n_nodes, const float *poses, const int32_t *pairs, int32_t P,
+                         const double *feat, const double *dense_ij, const double *dense_ji,
+                         double lambda_f, double lambda_g, double *A, double *b, double energy[2]) {
+  const int n = 6 * n_nodes;
+  memset(A, 0, sizeof(double) * (size_t)n * n);
+  memset(b, 0, sizeof(double) * (size_t)n);
+  energy[0] = energy[1] = 0.0;
+  for (int p = 0; p < P; ++p) {
+    const int i = pairs[2 * p], j = pairs[2 * p + 1];
+    if (i < 0 || j < 0 || i >= n_nodes || j >= n_nodes || i == j) return -1;
+    /* Eq. (2) blocks, as given (12 x 12 over [i, j]) */
+    const double *f = feat + (size_t)96 * p;
+    double Hii[36], Hjj[36], Hij[36], Hji[36];
+    sym6(f, Hii);
+    sym6(f + 57, Hjj);
+    for (int r = 0; r < 6; ++r)
+      for (int c = 0; c < 6; ++c) { Hij[6 * r + c] = f[21 + 6 * r + c]; Hji[6 * c + r] = f[21 + 6 * r + c]; }
+    add_block(A, n, i, i, Hii, lambda_f);
+    add_block(A, n, i, j, Hij, lambda_f);
+    add_block(A, n, j, i, Hji, lambda_f);
+    add_block(A, n, j, j, Hjj, lambda_f);
+    for (int r = 0; r < 6; ++r) { b[6 * i + r] += lambda_f * f[78 + r]; b[6 * j + r] += lambda_f * f[84 + r]; }
+    energy[0] += lambda_f * f[90];
+    /* Eq. (3) blocks of both directed edges */
+    double Ri[9], ti[3], Rj[9], tj[3];
+    pose_of(poses + 12 * i, Ri, ti);
+    pose_of(poses + 12 * j, Rj, tj);
+    if (dense_ij) {
+      add_dense(A, b, n, i, j, dense_ij + (size_t)32 * p, Ri, ti, Rj, tj, lambda_g);
+      energy[1] += lambda_g * dense_ij[(size_t)32 * p + 27];
+    }
+    if (dense_ji) {
+      add_dense(A, b, n, j, i, dense_ji + (size_t)32 * p, Rj, tj, Ri, ti, lambda_g);
+      energy[1] += lambda_g * dense_ji[(size_t)32 * p + 27];
+    }
+  }
+  return 0;
+}
+
+int32_t bto_graph_step(int32_t n_nodes, const float *poses, const int32_t *pairs, int32_t P,
+                       const double *feat, const double *dense_ij, const double *dense_ji,
+                       double lambda_f, double lambda_g, int32_t fixed_node, double *delta,
+                       float *new_poses, double energy[2]) {
+  const int n = 6 * n_nodes;
+  double *A = (double *)malloc(sizeof(double) * (size_t)n * n);
+  double *b = (double *)malloc(sizeof(double) * (size_t)n);
+  int *free_idx = (int *)malloc(sizeof(int) * (size_t)n);
+  int32_t st = bto_graph_system(n_nodes, poses, pairs, P, feat, dense_ij, dense_ji, lambda_f, lambda_g, A, b, energy);
+  int m = 0;
+  for (int k = 0; k < n; ++k) {
+    delta[k] = 0.0;
+    if (k / 6 != fixed_node && A[(size_t)k * n + k] != 0.0) free_idx[m++] = k;
+  }
+  /* Cholesky of the free block, L L^T = A_ff (lower triangle in place in L) */
+  double *L = (double *)calloc((size_t)m * m + 1, sizeof(double));
+  double *y = (double *)calloc((size_t)m + 1, sizeof(double));
+  for (int r = 0; r < m && st == 0; ++r)
+    for (int c = 0; c <= r; ++c) {
+      double s = A[(size_t)free_idx[r] * n + free_idx[c]];
+      for (int k = 0; k < c; ++k) s -= L[(size_t)r * m + k] * L[(size_t)c * m + k];
+      if (r == c) {
+        if (!(s > 0.0)) { st = -1; break; }
+        L[(size_t)r * m + r] = sqrt(s);
+      } else {
+        L[(size_t)r * m + c] = s / L[(size_t)c * m + c];
+      }
+    }
+  if (st == 0) {
+    for (int r = 0; r < m; ++r) {                  /* L y = -b_f */
+      double s = -b[free_idx[r]];
+      for (int k = 0; k < r; ++k) s -= L[(size_t)r * m + k] * y[k];
+      y[r] = s / L[(size_t)r * m + r];
+    }
+    for (int r = m - 1; r >= 0; --r) {             /* L^T d = y */
+      double s = y[r];
+      for (int k = r + 1; k < m; ++k) s -= L[(size_t)k * m + r] * delta[free_idx[k]];
+      delta[free_idx[r]] = s / L[(size_t)r * m + r];
+    }
+  }
+  for (int i = 0; i < n_nodes; ++i) {              /* T_i <- exp(d_i) T_i */
+    double Rd[9], td[3], R[9], t[3];
+    bto_se3_exp(delta + 6 * i, Rd, td);
+    pose_of(poses + 12 * i, R, t);
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) {
+        double x = 0.0;
+        for (int k = 0; k < 3; ++k) x += Rd[3 * r + k] * R[3 * k + c];
+        new_poses[12 * i + 3 * r + c] = (float)x;
+      }
+      new_poses[12 * i + 9 + r] = (float)(Rd[3 * r] * t[0] + Rd[3 * r + 1] * t[1] + Rd[3 * r + 2] * t[2] + td[r]);
+    }
+  }
+  free(A); free(b); free(free_idx); free(L); free(y);
+  return st;
+}

@@ -110,6 +110,42 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
                     double huber_delta, int32_t stride, double out[48], int32_t *pix_out,
                     uint8_t *pix_border);
 
+/* ---- NEXT-1: pose-graph Gauss-Newton step (§IV-D) -------------------
+   Twists are (v, w) (translation first), perturbations are on the left: T <- exp(d) T
+   (reading R18). */
+
+/* SE(3) exponential: R = exp([w]x) (Rodrigues), t = V v with
+   V = I + (1 - cos th)/th^2 [w]x + (th - sin th)/th^3 [w]x^2 (series below th = 1e-6). */
+void bto_se3_exp(const double xi[6], double R[9], double t[3]);
+
+/* Adjoint of T = (R, t) on (v, w) twists, 6x6 row-major: [[R, [t]x R], [0, R]], so that
+   exp(Adj_T d) T = T exp(d). */
+void bto_se3_adjoint(const double R[9], const double t[3], double Adj[36]);
+
+/* The Gauss-Newton system of Eq. (1) at the node poses: A = sum J^T W J,
+   b = sum J^T W r over
+     * lambda_f x the Eq. (2) block of every pair (feat[96] as in bto_feature_edge, nodes
+       (pairs[2p], pairs[2p+1]) = (i, j)), placed as given;
+     * lambda_g x the Eq. (3) block of both directed edges of every pair (dense[32] as in
+       bto_dense_edge: H, g w.r.t. T_i of edge i -> j), expanded to both nodes with
+       J_j = -J_i Adj(T_i T_j^-1):  A_ii += H, A_ij += -H Adj, A_jj += Adj^T H Adj,
+       b_i += g, b_j += -Adj^T g.
+   poses [N][12]; A [6N][6N] row-major (symmetric), b [6N]; energies out[2] = (sum lambda_f
+   E_f, sum lambda_g E_g).  Nodes outside [0, N) are an error (returns -1). */
+int32_t bto_graph_system(int32_t n_nodes, const float *poses, const int32_t *pairs, int32_t P,
+                         const double *feat, const double *dense_ij, const double *dense_ji,
+                         double lambda_f, double lambda_g, double *A, double *b, double energy[2]);
+
+/* One Gauss-Newton step: solve A d = -b exactly (dense Cholesky, fp64) with the DOFs of
+   fixed_node (I_0, kept constant) and every DOF whose diagonal is 0 (unconstrained)
+   pinned to d = 0, then T_i <- exp(d_i) T_i (rounded to float).  delta [6N], new_poses
+   [N][12] (may alias nothing).  Returns 0, or -1 if the free system is not positive
+   definite. */
+int32_t bto_graph_step(int32_t n_nodes, const float *poses, const int32_t *pairs, int32_t P,
+                       const double *feat, const double *dense_ij, const double *dense_ji,
+                       double lambda_f, double lambda_g, int32_t fixed_node, double *delta,
+                       float *new_poses, double energy[2]);
+
 #ifdef __cplusplus
 }
 #endif
