@@ -330,6 +330,46 @@ def main():
         roof["peak_note"] = ("FP32 FMA pipe: 148 SMs x 128 lanes x 2 flop x 1965 MHz (derived, B200_PROFILING "
                              "unit counts)" if roof["bound"] == "alu" else "MEASURED_PEAKS.json hbm_gbs")
 
+    # ---- NEXT-1: one pose-graph Gauss-Newton step on this step's records -----
+    # assemble (fp64, fixed order) + Jacobi-PCG + exp update, 16 nodes / 120 pairs; CUDA
+    # events on the stream, outside the headline timed region
+    graph = None
+    if world == 1:
+        new_pose = torch.zeros_like(t_pose)
+        gst = torch.zeros(4, dtype=torch.float32, device=dev)
+        for _ in range(3):
+            ctx.pose_graph_step(t_pose, t_pairs, rec, N_MAX, new_pose, stats=gst, stream=stream)
+        torch.cuda.synchronize()
+        ctx.profile(True)
+        ctx.profile_read()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 100
+        g0.record(stream)
+        for _ in range(reps):
+            ctx.pose_graph_step(t_pose, t_pairs, rec, N_MAX, new_pose, stats=gst, stream=stream)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gprof = ctx.profile_read().get("k_graph", (0.0, 0))
+        ctx.profile(False)
+        st = gst.cpu().numpy()
+        jac = torch.zeros(4, dtype=torch.float32, device=dev)   # the diagonal (Jacobi) preconditioner
+        ctx.pose_graph_step(t_pose, t_pairs, rec, N_MAX, new_pose, stats=jac, precond=0, stream=stream)
+        j0, j1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        j0.record(stream)
+        for _ in range(10):
+            ctx.pose_graph_step(t_pose, t_pairs, rec, N_MAX, new_pose, stats=jac, precond=0, stream=stream)
+        j1.record(stream)
+        torch.cuda.synchronize()
+        jac = jac.cpu().numpy()
+        graph = {"api": "bt_pose_graph_step", "precond": "block-Jacobi (6x6 node blocks, reading R23)",
+                 "ms_per_call": g0.elapsed_time(g1) / reps, "nodes": N_FRAMES,
+                 "pairs": P, "unknowns": 6 * N_FRAMES, "launches_per_call": 3,
+                 "kernel_ms_per_call": gprof[0] / max(1, gprof[1]) * 3, "pcg_iterations": float(st[2]),
+                 "pcg_rel_residual": float(st[3]), "energy_feat": float(st[0]), "energy_dense": float(st[1]),
+                 "bound": "latency (96 x 96 fp64 system; single-CTA PCG)",
+                 "jacobi": {"ms_per_call": j0.elapsed_time(j1) / 10, "pcg_iterations": float(jac[2]),
+                            "pcg_rel_residual": float(jac[3])}}
+
     # ---- end to end through the C ABI with pinned HOST buffers -------------------------
     e2e = None
     if not args.no_e2e:
@@ -387,7 +427,7 @@ def main():
                 else "single GPU",
                 "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
                 "roofline": roof, "kernels": kern, "kernel_ms_per_step": step_ms_by_kernel,
-                "e2e": e2e, "cpu_baseline": cpu}
+                "e2e": e2e, "cpu_baseline": cpu, "next_pose_graph": graph}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

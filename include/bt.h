@@ -173,6 +173,39 @@ bt_status bt_register_pairs_host(bt_ctx *ctx, const bt_keypoints *kp, const bt_m
 bt_status bt_compose_poses(bt_ctx *ctx, const bt_pose *a, const bt_pose *b, bt_pose *out,
                            int32_t n, void *stream);
 
+/* ---- NEXT-1: pose-graph Gauss-Newton step (§IV-D) ---------------------
+   Eq. (1): E = sum_{i != j} lambda_1 E_f(i,j) + lambda_2 E_g(i,j).  One Gauss-Newton step
+   (J^T W J) d = -J^T W r (the IRLS weights W already in the blocks), solved with
+   Jacobi-preconditioned CG ("the diagonal matrix J^T W J is used as the preconditioner"),
+   then xi <- xi [+] d as the left update T_i <- exp(d_i) T_i (twists (v, w), reading R18). */
+typedef struct {
+  float lambda_feat;     /* lambda_1 (1) */
+  float lambda_dense;    /* lambda_2 (1) */
+  int32_t fixed_node;    /* node kept constant as the reference (I_0) */
+  int32_t max_iter;      /* PCG iteration cap (>= 1) */
+  float rel_tol;         /* PCG stops when |r| <= rel_tol |b| (e.g. 1e-10) */
+  int32_t precond;       /* 0: the diagonal of J^T W J (Jacobi, P:83 as written);
+                            1: its 6 x 6 node blocks (block-Jacobi, reading R23) */
+} bt_graph_params;
+
+/* One Gauss-Newton step of the pose graph from the blocks bt_register_pairs wrote at the
+   node poses `node_pose` (device [n_nodes]):
+     records  device [P][bt_record_words(n_max)] — per pair (pairs[p] = (i, j)): the Eq. (2)
+              block `feat` over (T_i, T_j) used as given, and the Eq. (3) blocks dense_ij
+              (edge i -> j, w.r.t. T_i) / dense_ji, each expanded to both nodes with
+              J_j = -J_i Adj(T_i T_j^-1) (Adj = [[R, [t]x R], [0, R]]).
+   The system is assembled in fp64 in a fixed order (bitwise reproducible).  DOFs of
+   fixed_node and DOFs whose diagonal is 0 (nodes without edges) are held at d = 0.
+   Outputs (device): new_pose [n_nodes] (may alias node_pose), delta [n_nodes][6] fp64 or
+   NULL, stats [4] f32 or NULL = (lambda_1 sum E_f, lambda_2 sum E_g at the input poses, PCG
+   iterations, final |r| / |b|).  Pair entries with i == j or a node outside [0, n_nodes) are
+   skipped.  Errors: BT_EINVAL (NULL buffers, n_nodes < 1, fixed_node out of range, bad
+   params), BT_ECAPACITY (n_nodes > reserved max_frames, P > reserved max_pairs). */
+bt_status bt_pose_graph_step(bt_ctx *ctx, int32_t n_nodes, const bt_pose *node_pose,
+                             const int32_t *pairs, int32_t P, const uint32_t *records, int32_t n_max,
+                             const bt_graph_params *prm, bt_pose *new_pose, double *delta,
+                             float *stats, void *stream);
+
 /* number of kernels the last bt_* call enqueued (for the bench's gpu_launches claim) */
 int32_t bt_last_launch_count(const bt_ctx *ctx);
 

@@ -25,7 +25,7 @@ PAIR_OK, PAIR_FEW_MATCHES, PAIR_FEW_INLIERS, PAIR_REFIT_DEGENERATE = range(4)
 SYMBOLS = ("bt_create", "bt_destroy", "bt_last_error", "bt_status_string", "bt_reserve",
            "bt_record_words", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
            "bt_register_pairs_host", "bt_compose_poses", "bt_last_launch_count", "bt_profile_enable",
-           "bt_profile_kernels", "bt_profile_name", "bt_profile_read")
+           "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step")
 
 
 class BtError(RuntimeError):
@@ -67,6 +67,11 @@ class EdgeParams(C.Structure):
                 ("stride", C.c_int32)]
 
 
+class GraphParams(C.Structure):
+    _fields_ = [("lambda_feat", C.c_float), ("lambda_dense", C.c_float), ("fixed_node", C.c_int32),
+                ("max_iter", C.c_int32), ("rel_tol", C.c_float), ("precond", C.c_int32)]
+
+
 _lib = None
 
 
@@ -97,6 +102,7 @@ def lib():
         L.bt_register_pairs.argtypes = rp
         L.bt_register_pairs_host.argtypes = rp
         L.bt_compose_poses.argtypes = [vp, vp, vp, vp, i32, vp]
+        L.bt_pose_graph_step.argtypes = [vp, i32, vp, vp, i32, vp, i32, C.POINTER(GraphParams), vp, vp, vp, vp]
         L.bt_last_launch_count.argtypes = [vp]
         L.bt_last_launch_count.restype = i32
         L.bt_profile_enable.argtypes = [vp, i32]
@@ -108,7 +114,7 @@ def lib():
         L.bt_profile_read.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.bt_profile_read.restype = C.c_int
         for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
-                  "bt_register_pairs_host", "bt_compose_poses"):
+                  "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -275,6 +281,18 @@ class Context:
             self._check(L.bt_profile_read(self._h, k, C.byref(ms), C.byref(n)), "bt_profile_read")
             out[L.bt_profile_name(k).decode()] = (ms.value, n.value)
         return out
+
+    def pose_graph_step(self, node_pose, pairs, records, n_max: int, new_pose, lambda_feat: float = 1.0,
+                        lambda_dense: float = 1.0, fixed_node: int = 0, max_iter: int = 200, rel_tol: float = 1e-10,
+                        precond: int = 1, delta=None, stats=None, stream=None):
+        """One Gauss-Newton step of the pose graph from bt_register_pairs records
+        (bt_pose_graph_step).  precond 0 = Jacobi, 1 = block-Jacobi."""
+        prm = GraphParams(float(lambda_feat), float(lambda_dense), int(fixed_node), int(max_iter), float(rel_tol),
+                          int(precond))
+        self._check(lib().bt_pose_graph_step(self._h, int(node_pose.shape[0]), _ptr(node_pose), _ptr(pairs),
+                                             int(pairs.shape[0]), _ptr(records), int(n_max), C.byref(prm),
+                                             _ptr(new_pose), _ptr(delta), _ptr(stats), self._stream(stream)),
+                    "bt_pose_graph_step")
 
     def compose_poses(self, a, b, out, stream=None):
         self._check(lib().bt_compose_poses(self._h, _ptr(a), _ptr(b), _ptr(out), int(a.shape[0]),

@@ -40,6 +40,7 @@ struct bt_ctx {
   void *rscratch = nullptr;                   // RANSAC hypotheses / counts (bt::RansacScratch)
   bt::RansacScratch rs{};
   void *dense = nullptr;
+  void *graph = nullptr;                      // pose-graph step scratch (bt_graph.cu)
   // staging for bt_register_pairs_host
   int32_t *st_nkp = nullptr, *st_pairs = nullptr;
   uint32_t *st_uid = nullptr, *st_records = nullptr;
@@ -71,7 +72,7 @@ void free_dev(T *&p) {
 
 void free_scratch(bt_ctx *c) {
   free_dev(c->match); free_dev(c->matches); free_dev(c->n_matches);
-  free_dev(c->rscratch); free_dev(c->dense);
+  free_dev(c->rscratch); free_dev(c->dense); free_dev(c->graph);
   free_dev(c->st_nkp); free_dev(c->st_pairs); free_dev(c->st_uid); free_dev(c->st_records);
   free_dev(c->st_desc); free_dev(c->st_pts); free_dev(c->st_nrm); free_dev(c->st_depth);
   free_dev(c->st_normal); free_dev(c->st_mask); free_dev(c->st_pose);
@@ -242,6 +243,7 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   if (ok && dense_bytes > 0) ok = cudaMalloc(&c->dense, dense_bytes) == cudaSuccess;
+  if (ok) ok = cudaMalloc(&c->graph, bt::graph_scratch_bytes(mframes, max_pairs)) == cudaSuccess;
   if (ok && max_frames > 0) {
     const size_t FN = (size_t)max_frames * n_max, FP = (size_t)max_frames * width * height;
     ok = cudaMalloc(&c->st_nkp, (size_t)max_frames * 4) == cudaSuccess &&
@@ -447,9 +449,32 @@ bt_status bt_compose_poses(bt_ctx *c, const bt_pose *a, const bt_pose *b, bt_pos
   return after_launch(c, "bt_compose_poses");
 }
 
+bt_status bt_pose_graph_step(bt_ctx *c, int32_t n_nodes, const bt_pose *node_pose, const int32_t *pairs,
+                             int32_t P, const uint32_t *records, int32_t n_max, const bt_graph_params *prm,
+                             bt_pose *new_pose, double *delta, float *stats, void *stream) {
+  BT_CHECK_CTX(c);
+  if (!prm) return fail(c, BT_EINVAL, "bt_pose_graph_step: NULL params");
+  if (n_nodes < 1) return fail(c, BT_EINVAL, "n_nodes %d < 1", n_nodes);
+  if (n_nodes > c->cap_frames) return fail(c, BT_ECAPACITY, "n_nodes %d > reserved max_frames %d", n_nodes, c->cap_frames);
+  if (P < 0) return fail(c, BT_EINVAL, "P < 0");
+  if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
+  if (n_max < 1) return fail(c, BT_EINVAL, "n_max < 1");
+  if (prm->fixed_node < 0 || prm->fixed_node >= n_nodes)
+    return fail(c, BT_EINVAL, "fixed_node %d outside [0, %d)", prm->fixed_node, n_nodes);
+  if (prm->max_iter < 1 || !(prm->rel_tol >= 0.f) || !(prm->lambda_feat >= 0.f) || !(prm->lambda_dense >= 0.f) ||
+      (prm->precond != 0 && prm->precond != 1))
+    return fail(c, BT_EINVAL, "bt_pose_graph_step: bad params");
+  if (!node_pose || !new_pose || (P > 0 && (!pairs || !records)))
+    return fail(c, BT_EINVAL, "bt_pose_graph_step: NULL buffer");
+  c->launch.count = 0;
+  bt::launch_graph(n_nodes, node_pose, pairs, P, records, n_max, *prm, c->graph, new_pose, delta, stats,
+                   (cudaStream_t)stream, c->launch);
+  return after_launch(c, "bt_pose_graph_step");
+}
+
 static const char *kKernelNames[bt::K_COUNT] = {"k_desc_prep", "k_match_tc", "k_rescore", "k_mutual",
                                                  "k_ransac_hyp", "k_ransac_score", "k_ransac_finish", "k_dense_prep",
-                                                 "k_dense", "k_dense_reduce", "k_compose"};
+                                                 "k_dense", "k_dense_reduce", "k_compose", "k_graph"};
 
 static cudaEvent_t take_event(bt_ctx *c) {
   if (c->ev_pool.empty()) {

@@ -59,6 +59,8 @@ int main(void) {
   printf("sizeof.bt_intrinsics %zu\n", sizeof(bt_intrinsics));
   printf("sizeof.bt_edge_params %zu\n", sizeof(bt_edge_params));
   printf("sizeof.bt_pose %zu\n", sizeof(bt_pose));
+  printf("sizeof.bt_graph_params %zu\n", sizeof(bt_graph_params));
+  P(bt_graph_params, fixed_node); P(bt_graph_params, rel_tol); P(bt_graph_params, precond);
   P(bt_ransac_params, seed); P(bt_ransac_params, min_sigma_ratio); P(bt_ransac_params, min_inliers);
   P(bt_keypoints, n_kp); P(bt_keypoints, nrm); P(bt_maps, depth); P(bt_maps, mask);
   return 0;
@@ -87,6 +89,10 @@ def test_ctypes_structs_match_c_layout(bt):
     assert bt.Keypoints.nrm.offset == c["bt_keypoints.nrm"]
     assert bt.Maps.depth.offset == c["bt_maps.depth"]
     assert bt.Maps.mask.offset == c["bt_maps.mask"]
+    assert ctypes.sizeof(bt.GraphParams) == c["sizeof.bt_graph_params"]
+    assert bt.GraphParams.fixed_node.offset == c["bt_graph_params.fixed_node"]
+    assert bt.GraphParams.rel_tol.offset == c["bt_graph_params.rel_tol"]
+    assert bt.GraphParams.precond.offset == c["bt_graph_params.precond"]
 
 
 def test_no_cpu_fallback(bt):
