@@ -78,6 +78,8 @@ def _setup(L):
     L.bto_dense_edge.argtypes = [_f32p, _f32p, _u8p, _f32p, _f32p, _u8p, C.c_int32, C.c_int32,
                                  C.c_double, C.c_double, C.c_double, C.c_double, _f32p, _f32p,
                                  C.c_double, C.c_double, C.c_double, C.c_int32, _f64p, _vp, _vp]
+    L.bto_estimate_normals.argtypes = [_f32p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, C.c_float, _f32p]
     L.bto_se3_exp.argtypes = [_f64p, _f64p, _f64p]
     L.bto_se3_adjoint.argtypes = [_f64p, _f64p, _f64p]
     L.bto_graph_system.restype = C.c_int32
@@ -315,3 +317,18 @@ def graph_step(poses, pairs, feat, dense_ij=None, dense_ji=None, lambda_f=1.0, l
     if st != 0:
         raise np.linalg.LinAlgError("pose-graph system not positive definite")
     return d.reshape(N, 6), out.reshape(N, 12), tuple(e)
+
+
+# ------------------------------------------------------------ NEXT-4: normals from depth
+def estimate_normals(depth, K, jump: float = 0.05) -> np.ndarray:
+    """Normal map [F][H][W][3] from depth [F][H][W] (or [H][W]) by central differences of the
+    unprojected cloud, camera-facing, 5 cm jump test (SPEC estimate_normals S:157-165)."""
+    d = _c(depth, np.float32)
+    squeeze = d.ndim == 2
+    if squeeze:
+        d = d[None]
+    F, H, W = d.shape
+    out = np.zeros((F, H, W, 3), np.float32)
+    lib().bto_estimate_normals(d.reshape(-1), F, W, H, float(K.fx), float(K.fy), float(K.cx), float(K.cy),
+                               float(jump), out.reshape(-1))
+    return out[0] if squeeze else out

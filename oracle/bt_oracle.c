@@ -823,3 +823,37 @@ int32_t bto_graph_step(int32_t n_nodes, const float *poses, const int32_t *pairs
   free(A); free(b); free(free_idx); free(L); free(y);
   return st;
 }
+
+/* ======================================================================= NEXT-4: normals */
+void bto_estimate_normals(const float *depth, int32_t F, int32_t W, int32_t H, double fx, double fy,
+                          double cx, double cy, float jump, float *normal) {
+  for (int f = 0; f < F; ++f)
+    for (int v = 0; v < H; ++v)
+      for (int u = 0; u < W; ++u) {
+        const float *D = depth + (size_t)f * W * H;
+        float *out = normal + 3 * ((size_t)f * W * H + (size_t)v * W + u);
+        out[0] = out[1] = out[2] = 0.0f;
+        const double d = D[v * W + u];
+        if (!(d > 0.0) || u == 0 || v == 0 || u == W - 1 || v == H - 1) continue;
+        const int nu[4] = {u - 1, u + 1, u, u};
+        const int nv[4] = {v, v, v - 1, v + 1};
+        double P[4][3];
+        int ok = 1;
+        for (int k = 0; k < 4; ++k) {
+          const double dk = D[nv[k] * W + nu[k]];
+          if (!(dk > 0.0) || fabs(dk - d) > (double)jump) { ok = 0; break; }
+          P[k][0] = (nu[k] - cx) * dk / fx;
+          P[k][1] = (nv[k] - cy) * dk / fy;
+          P[k][2] = dk;
+        }
+        if (!ok) continue;
+        const double tu[3] = {P[1][0] - P[0][0], P[1][1] - P[0][1], P[1][2] - P[0][2]};
+        const double tv[3] = {P[3][0] - P[2][0], P[3][1] - P[2][1], P[3][2] - P[2][2]};
+        double n[3] = {tu[1] * tv[2] - tu[2] * tv[1], tu[2] * tv[0] - tu[0] * tv[2], tu[0] * tv[1] - tu[1] * tv[0]};
+        const double nn = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        if (!(nn > 0.0)) continue;
+        const double pc[3] = {(u - cx) * d / fx, (v - cy) * d / fy, d};
+        const double s = (n[0] * pc[0] + n[1] * pc[1] + n[2] * pc[2]) > 0.0 ? -1.0 / nn : 1.0 / nn;
+        for (int k = 0; k < 3; ++k) out[k] = (float)(n[k] * s);
+      }
+}

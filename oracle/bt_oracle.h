@@ -146,6 +146,16 @@ int32_t bto_graph_step(int32_t n_nodes, const float *poses, const int32_t *pairs
                        double lambda_f, double lambda_g, int32_t fixed_node, double *delta,
                        float *new_poses, double energy[2]);
 
+/* ---- NEXT-4: input prep — normal map from depth (SPEC estimate_normals; the
+   paper's n_i(x), method unspecified) ------------------------------------------------
+   P(u, v) = ((u - cx) d / fx, (v - cy) d / fy, d) in fp64; n = (P(u+1,v) - P(u-1,v)) x
+   (P(u,v+1) - P(u,v-1)), normalized, flipped to face the camera (n . P(u,v) < 0).  Invalid
+   (0, 0, 0) when d(u,v) <= 0, a 4-neighbour is outside the image or has depth <= 0, a
+   neighbour's |d_n - d(u,v)| > jump (compared in double on the float values), or |n| = 0.
+   depth [F][H][W], normal [F][H][W][3] (float). */
+void bto_estimate_normals(const float *depth, int32_t F, int32_t W, int32_t H, double fx, double fy,
+                          double cx, double cy, float jump, float *normal);
+
 #ifdef __cplusplus
 }
 #endif
