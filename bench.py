@@ -370,6 +370,32 @@ def main():
                  "jacobi": {"ms_per_call": j0.elapsed_time(j1) / 10, "pcg_iterations": float(jac[2]),
                             "pcg_rel_residual": float(jac[3])}}
 
+    # ---- NEXT-4: normal maps from depth for the 16 frames (bt_estimate_normals) ----------
+    # algorithmic bytes 4 (depth read) + 12 (normal written) per pixel; before each call,
+    # outside its events, L2 is flushed AND cleaned (a 256 MiB read after the memset), so the
+    # kernel does not pay for writing back the flush's dirty lines
+    prep = None
+    if world == 1:
+        nrm_out = torch.empty((N_FRAMES, H, W, 3), dtype=torch.float32, device=dev)
+        clean = torch.zeros(64 << 20, dtype=torch.float32, device=dev)
+        for _ in range(3):
+            ctx.estimate_normals(fb.depth, sc.K, nrm_out, stream=stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+        for a_, b_ in ev:
+            flush.zero_()
+            clean.sum()
+            a_.record(stream)
+            ctx.estimate_normals(fb.depth, sc.K, nrm_out, stream=stream)
+            b_.record(stream)
+        torch.cuda.synchronize()
+        t_ms = float(np.median([a_.elapsed_time(b_) for a_, b_ in ev]))
+        nbytes = N_FRAMES * H * W * 16
+        prep = {"api": "bt_estimate_normals", "frames": N_FRAMES, "width": W, "height": H,
+                "ms_per_call": t_ms, "bound": "hbm", "bytes_per_call": nbytes,
+                "achieved_gbs": nbytes / (t_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                "frac": nbytes / (t_ms * 1e-3) / 1e9 / hbm_peak, "l2": "flushed + cleaned before each call"}
+        del clean
+
     # ---- end to end through the C ABI with pinned HOST buffers -------------------------
     e2e = None
     if not args.no_e2e:
@@ -427,7 +453,8 @@ def main():
                 else "single GPU",
                 "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
                 "roofline": roof, "kernels": kern, "kernel_ms_per_step": step_ms_by_kernel,
-                "e2e": e2e, "cpu_baseline": cpu, "next_pose_graph": graph}
+                "e2e": e2e, "cpu_baseline": cpu, "next_pose_graph": graph,
+                "next_input_prep": prep}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

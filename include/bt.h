@@ -206,6 +206,18 @@ bt_status bt_pose_graph_step(bt_ctx *ctx, int32_t n_nodes, const bt_pose *node_p
                              const bt_graph_params *prm, bt_pose *new_pose, double *delta,
                              float *stats, void *stream);
 
+/* ---- NEXT-4: input prep — the normal map n_i(x) of Eq. (3) from depth (SPEC
+   estimate_normals S:157-165) -----------------------------------------------------------
+   depth [F][H][W] f32 device (<= 0: invalid) -> normal [F][H][W][3] f32 device (16-B
+   aligned): central differences of the unprojected cloud P = ((u-cx) d/fx, (v-cy) d/fy, d),
+   n = (P(u+1,v) - P(u-1,v)) x (P(u,v+1) - P(u,v-1)) normalized and facing the camera
+   (n . P < 0); (0, 0, 0) at the image border, where the pixel or a 4-neighbour has depth
+   <= 0, or where a neighbour's depth differs by more than jump_m (SPEC: 0.05).  Only K's
+   fx, fy, cx, cy are used.  Errors: BT_EINVAL (NULL / misaligned buffers, fx or fy <= 0,
+   jump_m < 0, negative sizes). */
+bt_status bt_estimate_normals(bt_ctx *ctx, const float *depth, int32_t n_frames, int32_t width, int32_t height,
+                              const bt_intrinsics *K, float jump_m, float *normal, void *stream);
+
 /* number of kernels the last bt_* call enqueued (for the bench's gpu_launches claim) */
 int32_t bt_last_launch_count(const bt_ctx *ctx);
 

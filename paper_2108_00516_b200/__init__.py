@@ -25,7 +25,8 @@ PAIR_OK, PAIR_FEW_MATCHES, PAIR_FEW_INLIERS, PAIR_REFIT_DEGENERATE = range(4)
 SYMBOLS = ("bt_create", "bt_destroy", "bt_last_error", "bt_status_string", "bt_reserve",
            "bt_record_words", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
            "bt_register_pairs_host", "bt_compose_poses", "bt_last_launch_count", "bt_profile_enable",
-           "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step")
+           "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step",
+           "bt_estimate_normals")
 
 
 class BtError(RuntimeError):
@@ -103,6 +104,7 @@ def lib():
         L.bt_register_pairs_host.argtypes = rp
         L.bt_compose_poses.argtypes = [vp, vp, vp, vp, i32, vp]
         L.bt_pose_graph_step.argtypes = [vp, i32, vp, vp, i32, vp, i32, C.POINTER(GraphParams), vp, vp, vp, vp]
+        L.bt_estimate_normals.argtypes = [vp, vp, i32, i32, i32, C.POINTER(Intrinsics), C.c_float, vp, vp]
         L.bt_last_launch_count.argtypes = [vp]
         L.bt_last_launch_count.restype = i32
         L.bt_profile_enable.argtypes = [vp, i32]
@@ -114,7 +116,7 @@ def lib():
         L.bt_profile_read.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.bt_profile_read.restype = C.c_int
         for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
-                  "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step"):
+                  "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -293,6 +295,13 @@ class Context:
                                              int(pairs.shape[0]), _ptr(records), int(n_max), C.byref(prm),
                                              _ptr(new_pose), _ptr(delta), _ptr(stats), self._stream(stream)),
                     "bt_pose_graph_step")
+
+    def estimate_normals(self, depth, K, normal, jump: float = 0.05, stream=None):
+        """Normal map [F][H][W][3] from depth [F][H][W] (bt_estimate_normals; NEXT-4)."""
+        F, H, W = (1,) + tuple(depth.shape) if depth.dim() == 2 else tuple(depth.shape)
+        Ki = intrinsics(K) if not isinstance(K, Intrinsics) else K
+        self._check(lib().bt_estimate_normals(self._h, _ptr(depth), int(F), int(W), int(H), C.byref(Ki),
+                                              float(jump), _ptr(normal), self._stream(stream)), "bt_estimate_normals")
 
     def compose_poses(self, a, b, out, stream=None):
         self._check(lib().bt_compose_poses(self._h, _ptr(a), _ptr(b), _ptr(out), int(a.shape[0]),

@@ -472,9 +472,23 @@ bt_status bt_pose_graph_step(bt_ctx *c, int32_t n_nodes, const bt_pose *node_pos
   return after_launch(c, "bt_pose_graph_step");
 }
 
+bt_status bt_estimate_normals(bt_ctx *c, const float *depth, int32_t n_frames, int32_t width, int32_t height,
+                              const bt_intrinsics *K, float jump_m, float *normal, void *stream) {
+  BT_CHECK_CTX(c);
+  if (n_frames < 0 || width < 0 || height < 0) return fail(c, BT_EINVAL, "bt_estimate_normals: negative size");
+  if (!K || !(K->fx > 0.f) || !(K->fy > 0.f)) return fail(c, BT_EINVAL, "bt_estimate_normals: bad intrinsics");
+  if (!(jump_m >= 0.f)) return fail(c, BT_EINVAL, "bt_estimate_normals: jump < 0");
+  if ((size_t)n_frames * width * height == 0) return BT_OK;
+  if (!depth || !normal) return fail(c, BT_EINVAL, "bt_estimate_normals: NULL buffer");
+  if (((uintptr_t)normal & 15) != 0) return fail(c, BT_EINVAL, "bt_estimate_normals: normal not 16-B aligned");
+  c->launch.count = 0;
+  bt::launch_normals(depth, n_frames, width, height, *K, jump_m, normal, (cudaStream_t)stream, c->launch);
+  return after_launch(c, "bt_estimate_normals");
+}
+
 static const char *kKernelNames[bt::K_COUNT] = {"k_desc_prep", "k_match_tc", "k_rescore", "k_mutual",
                                                  "k_ransac_hyp", "k_ransac_score", "k_ransac_finish", "k_dense_prep",
-                                                 "k_dense", "k_dense_reduce", "k_compose", "k_graph"};
+                                                 "k_dense", "k_dense_reduce", "k_compose", "k_graph", "k_normals"};
 
 static cudaEvent_t take_event(bt_ctx *c) {
   if (c->ev_pool.empty()) {

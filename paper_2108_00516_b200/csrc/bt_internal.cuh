@@ -36,7 +36,7 @@ struct MapView {
 // ---- launch bookkeeping: counts kernels and (optionally) brackets each with events ----
 enum KernelId {
   K_DESC_PREP = 0, K_MATCH_TC, K_RESOLVE, K_MUTUAL, K_RANSAC_HYP, K_RANSAC_SCORE, K_RANSAC_FINISH, K_DENSE_PREP,
-  K_DENSE, K_DENSE_REDUCE, K_COMPOSE, K_GRAPH,
+  K_DENSE, K_DENSE_REDUCE, K_COMPOSE, K_GRAPH, K_NORMALS,
   K_COUNT
 };
 
@@ -88,6 +88,9 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
                   cudaStream_t s, Launch &L);
 int dense_tiles(int W, int H);
 size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H);
+// NEXT-4 input prep: normal map from depth (bt_prep.cu)
+void launch_normals(const float *depth, int F, int W, int H, const bt_intrinsics &K, float jump, float *normal,
+                    cudaStream_t s, Launch &L);
 // NEXT-1 pose-graph Gauss-Newton step (bt_graph.cu)
 size_t graph_scratch_bytes(int max_nodes, int max_pairs);
 void launch_graph(int N, const bt_pose *pose, const int32_t *pairs, int P, const uint32_t *records, int n_max,
