@@ -206,6 +206,19 @@ bt_status bt_pose_graph_step(bt_ctx *ctx, int32_t n_nodes, const bt_pose *node_p
                              const bt_graph_params *prm, bt_pose *new_pose, double *delta,
                              float *stats, void *stream);
 
+/* Re-linearize the records' Eq. (2) and Eq. (3) blocks at new node poses for the next
+   Gauss-Newton iteration (NEXT-1), reusing each pair's C_ij: "If C_ij has been built during a
+   previous pose graph optimization, it is reused".  Feature blocks are recomputed from
+   the record's inlier mask over the match lists the context kept from the LAST
+   bt_register_pairs (device entry) on this context — the same P pairs and keypoints must be
+   passed; the dense edges are re-associated at the new poses.  Matching, RANSAC and
+   the other record words are untouched; the updated words are bitwise equal to what
+   bt_register_pairs would write at these poses.  Errors: BT_EINVAL (NULL buffers / params, P
+   different from the last bt_register_pairs), else as bt_register_pairs. */
+bt_status bt_relinearize(bt_ctx *ctx, const bt_keypoints *kp, const bt_maps *maps, const bt_intrinsics *K,
+                         const bt_pose *node_pose, const int32_t *pairs, int32_t P, const bt_edge_params *eprm,
+                         uint32_t *records, void *stream);
+
 /* ---- NEXT-4: input prep — the normal map n_i(x) of Eq. (3) from depth (SPEC
    estimate_normals S:157-165) -----------------------------------------------------------
    depth [F][H][W] f32 device (<= 0: invalid) -> normal [F][H][W][3] f32 device (16-B

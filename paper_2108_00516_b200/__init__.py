@@ -26,7 +26,7 @@ SYMBOLS = ("bt_create", "bt_destroy", "bt_last_error", "bt_status_string", "bt_r
            "bt_record_words", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
            "bt_register_pairs_host", "bt_compose_poses", "bt_last_launch_count", "bt_profile_enable",
            "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step",
-           "bt_estimate_normals")
+           "bt_estimate_normals", "bt_relinearize")
 
 
 class BtError(RuntimeError):
@@ -105,6 +105,8 @@ def lib():
         L.bt_compose_poses.argtypes = [vp, vp, vp, vp, i32, vp]
         L.bt_pose_graph_step.argtypes = [vp, i32, vp, vp, i32, vp, i32, C.POINTER(GraphParams), vp, vp, vp, vp]
         L.bt_estimate_normals.argtypes = [vp, vp, i32, i32, i32, C.POINTER(Intrinsics), C.c_float, vp, vp]
+        L.bt_relinearize.argtypes = [vp, C.POINTER(Keypoints), C.POINTER(Maps), C.POINTER(Intrinsics), vp, vp, i32,
+                                     C.POINTER(EdgeParams), vp, vp]
         L.bt_last_launch_count.argtypes = [vp]
         L.bt_last_launch_count.restype = i32
         L.bt_profile_enable.argtypes = [vp, i32]
@@ -116,7 +118,7 @@ def lib():
         L.bt_profile_read.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.bt_profile_read.restype = C.c_int
         for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
-                  "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals"):
+                  "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals", "bt_relinearize"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -295,6 +297,14 @@ class Context:
                                              int(pairs.shape[0]), _ptr(records), int(n_max), C.byref(prm),
                                              _ptr(new_pose), _ptr(delta), _ptr(stats), self._stream(stream)),
                     "bt_pose_graph_step")
+
+    def relinearize(self, fb: FrameBatch, K, node_pose, pairs, eprm: EdgeParams, records, stream=None):
+        """Eq. (2) / Eq. (3) blocks of `records` at new node poses, C_ij reused (bt_relinearize)."""
+        kp, mp = fb.keypoints(), fb.maps()
+        Ki = intrinsics(K) if not isinstance(K, Intrinsics) else K
+        self._check(lib().bt_relinearize(self._h, C.byref(kp), C.byref(mp), C.byref(Ki), _ptr(node_pose), _ptr(pairs),
+                                         int(pairs.shape[0]), C.byref(eprm), _ptr(records), self._stream(stream)),
+                    "bt_relinearize")
 
     def estimate_normals(self, depth, K, normal, jump: float = 0.05, stream=None):
         """Normal map [F][H][W][3] from depth [F][H][W] (bt_estimate_normals; NEXT-4)."""

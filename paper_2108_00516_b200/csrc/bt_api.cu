@@ -41,6 +41,7 @@ struct bt_ctx {
   bt::RansacScratch rs{};
   void *dense = nullptr;
   void *graph = nullptr;                      // pose-graph step scratch (bt_graph.cu)
+  int cached_P = -1;                          // pairs whose match lists c->matches holds (C_ij cache)
   // staging for bt_register_pairs_host
   int32_t *st_nkp = nullptr, *st_pairs = nullptr;
   uint32_t *st_uid = nullptr, *st_records = nullptr;
@@ -342,6 +343,7 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
       cudaStreamWaitEvent(st, c->ev_join_hi, 0);
     }
   }
+  c->cached_P = P;
   return after_launch(c, "bt_register_pairs");
 }
 
@@ -390,6 +392,7 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
   const cudaStream_t st = (cudaStream_t)stream;
   const int F = kp->n_frames;
   const size_t FN = (size_t)F * kp->n_max;
+  c->cached_P = -1;                                              // match lists from staged keypoints
   const int rw = bt::rec_words(kp->n_max);
   c->launch.count = 0;
   // keypoints first on the caller's stream: matching + RANSAC start as soon as they land,
@@ -484,6 +487,35 @@ bt_status bt_estimate_normals(bt_ctx *c, const float *depth, int32_t n_frames, i
   c->launch.count = 0;
   bt::launch_normals(depth, n_frames, width, height, *K, jump_m, normal, (cudaStream_t)stream, c->launch);
   return after_launch(c, "bt_estimate_normals");
+}
+
+bt_status bt_relinearize(bt_ctx *c, const bt_keypoints *kp, const bt_maps *maps, const bt_intrinsics *K,
+                         const bt_pose *node_pose, const int32_t *pairs, int32_t P, const bt_edge_params *eprm,
+                         uint32_t *records, void *stream) {
+  BT_CHECK_CTX(c);
+  bt_status s;
+  if ((s = check_kp(c, kp)) != BT_OK) return s;
+  if ((s = check_maps(c, maps, K)) != BT_OK) return s;
+  if (!eprm) return fail(c, BT_EINVAL, "bt_relinearize: NULL edge params");
+  if ((s = check_edge(c, eprm)) != BT_OK) return s;
+  if (P < 0) return fail(c, BT_EINVAL, "P < 0");
+  if (P == 0) return BT_OK;
+  if (P != c->cached_P)
+    return fail(c, BT_EINVAL, "bt_relinearize: P %d does not match the last bt_register_pairs (%d pairs)", P,
+                c->cached_P);
+  if (!node_pose || !pairs || !records) return fail(c, BT_EINVAL, "bt_relinearize: NULL buffer");
+  const cudaStream_t st = (cudaStream_t)stream;
+  const int rw = bt::rec_words(kp->n_max);
+  c->launch.count = 0;
+  cudaEventRecord(c->ev_fork, st);                                 // dense edges beside the feature blocks
+  cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+  bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, nullptr, 0, records, rw,
+                   bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch);
+  bt::launch_feature_edges(kview(kp), pairs, P, c->matches, c->n_matches, records, rw, node_pose, eprm->huber_m, st,
+                           c->launch);
+  cudaEventRecord(c->ev_join, c->side);
+  cudaStreamWaitEvent(st, c->ev_join, 0);
+  return after_launch(c, "bt_relinearize");
 }
 
 static const char *kKernelNames[bt::K_COUNT] = {"k_desc_prep", "k_match_tc", "k_rescore", "k_mutual",

@@ -88,6 +88,10 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
                   cudaStream_t s, Launch &L);
 int dense_tiles(int W, int H);
 size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H);
+// Eq. (2) blocks re-linearized at new node poses from the records' inlier masks (C_ij reuse)
+void launch_feature_edges(const KpView &kp, const int32_t *pairs, int P, const int32_t *matches,
+                          const int32_t *n_matches, uint32_t *records, int rec_stride, const bt_pose *node_pose,
+                          float huber, cudaStream_t s, Launch &L);
 // NEXT-4 input prep: normal map from depth (bt_prep.cu)
 void launch_normals(const float *depth, int F, int W, int H, const bt_intrinsics &K, float jump, float *normal,
                     cudaStream_t s, Launch &L);

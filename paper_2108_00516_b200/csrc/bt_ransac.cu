@@ -562,6 +562,112 @@ constexpr int kFeatChunk = 512;                  // feature rows staged per pass
 // per-inlier feature data staged in smem: e(3) J(3x12) w rho
 constexpr int kFeatRow = 3 * 13 + 2;             // per residual component q: J_q (12), e_q; w; rho
 
+// Eq. (2) feature-edge blocks of one pair at the node poses, all kFinThreads threads.
+// inl[0 .. n_feat) = the inlier match indices in ascending order (C_ij), frow: smem rows.
+__device__ void feature_blocks(const int *inl, int n_feat, const int32_t *mt, const float *pa_f, const float *pb_f,
+                               const bt_pose &Pi, const bt_pose &Pj, double huber, float *frow,
+                               float (*fpart)[96], uint32_t *feat_out) {
+  // e = R_i^T (p_m - t_i) - R_j^T (p_n - t_j) (fp64: it cancels ~0.5 m coordinates);
+  // J_i = -R_i^T [I | -[p_m]x], J_j = R_j^T [I | -[p_n]x];  H += w J^T J, g += w J^T e,
+  // E += rho(|e|).  Every thread builds rows (fp32 after the fp64 residual) into smem; warp w
+  // accumulates rows w, w + 8, ... for outputs lane, lane + 32, lane + 64; a fixed-order
+  // combine over the 8 warps keeps the result bitwise deterministic.
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double Ri[9], ti[3], Rj[9], tj[3];
+  for (int k = 0; k < 9; ++k) { Ri[k] = Pi.R[k]; Rj[k] = Pj.R[k]; }
+  for (int k = 0; k < 3; ++k) { ti[k] = Pi.t[k]; tj[k] = Pj.t[k]; }
+  // the three outputs of this lane: kind 0 H(a,b), 1 g(a), 2 E, 3 count, -1 none
+  int okind[3], oa[3], ob[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    int k = lane + 32 * s;
+    okind[s] = -1; oa[s] = ob[s] = 0;
+    if (k < 21) {                      // H_ii upper
+      int a = 0;
+      while (k >= 6 - a) { k -= 6 - a; ++a; }
+      oa[s] = a; ob[s] = a + k; okind[s] = 0;
+    } else if (k < 57) {               // H_ij
+      k -= 21; oa[s] = k / 6; ob[s] = 6 + k % 6; okind[s] = 0;
+    } else if (k < 78) {               // H_jj upper
+      k -= 57;
+      int a = 0;
+      while (k >= 6 - a) { k -= 6 - a; ++a; }
+      oa[s] = 6 + a; ob[s] = 6 + a + k; okind[s] = 0;
+    } else if (k < 90) { oa[s] = k - 78; ob[s] = 12; okind[s] = 1; }
+    else if (k == 90) okind[s] = 2;
+    else if (k == 91) okind[s] = 3;
+  }
+  float acc[3] = {0.f, 0.f, 0.f};
+  for (int done = 0; done < n_feat; done += kFeatChunk) {
+    const int nc = min(kFeatChunk, n_feat - done);
+    __syncthreads();
+    for (int r = tid; r < nc; r += kFinThreads) {
+      const int m = inl[done + r];
+      const int i = mt[2 * m], j = mt[2 * m + 1];
+      const double pm[3] = {pa_f[3 * i], pa_f[3 * i + 1], pa_f[3 * i + 2]};
+      const double pn[3] = {pb_f[3 * j], pb_f[3 * j + 1], pb_f[3 * j + 2]};
+      float *row = frow + r * kFeatRow;
+      double e[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        e[q] = Ri[q] * (pm[0] - ti[0]) + Ri[3 + q] * (pm[1] - ti[1]) + Ri[6 + q] * (pm[2] - ti[2]) -
+               (Rj[q] * (pn[0] - tj[0]) + Rj[3 + q] * (pn[1] - tj[1]) + Rj[6 + q] * (pn[2] - tj[2]));
+      const double Sp[9] = {0, -pm[2], pm[1], pm[2], 0, -pm[0], -pm[1], pm[0], 0};
+      const double Sq[9] = {0, -pn[2], pn[1], pn[2], 0, -pn[0], -pn[1], pn[0], 0};
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        row[13 * q + 12] = (float)e[q];
+        // (R^T)[q][c] = R[c][q];  (R^T [p]x)[q][c] = sum_k R[k][q] S[k][c]
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          row[13 * q + c] = (float)-Ri[3 * c + q];
+          row[13 * q + 6 + c] = (float)Rj[3 * c + q];
+          double x = 0, y = 0;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) { x += Ri[3 * k + q] * Sp[3 * k + c]; y += Rj[3 * k + q] * Sq[3 * k + c]; }
+          row[13 * q + 3 + c] = (float)x;
+          row[13 * q + 9 + c] = (float)-y;
+        }
+      }
+      const double nrm = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+      double w, rho;
+      if (nrm <= huber) { w = 1.0; rho = 0.5 * nrm * nrm; }
+      else { w = huber / nrm; rho = huber * (nrm - 0.5 * huber); }
+      row[39] = (float)w;
+      row[40] = (float)rho;
+    }
+    __syncthreads();
+    // branch-free: H(a, b) and g(a) = H(a, 12) are the same 3-term dot product of row columns
+    // (g's column 12 is e); E and the count are selects.  Rows r and r + 8 per step (loads of
+    // both in flight), accumulated in the same row order as a one-row loop.
+    auto term = [&](const float *row, int s) {
+      const int a = oa[s], b = ob[s];
+      const float d = fmaf(row[a], row[b], fmaf(row[13 + a], row[13 + b], row[26 + a] * row[26 + b]));
+      return okind[s] <= 1 ? row[39] * d : (okind[s] == 2 ? row[40] : 1.f);
+    };
+    for (int r = warp; r < nc; r += 2 * (kFinThreads / 32)) {
+      const float *r0 = frow + r * kFeatRow;
+      const int r1i = r + kFinThreads / 32;
+      const float *r1 = frow + (r1i < nc ? r1i : r) * kFeatRow;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        if (okind[s] < 0) continue;
+        const float t0 = term(r0, s), t1 = term(r1, s);
+        acc[s] += t0;
+        if (r1i < nc) acc[s] += t1;
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) fpart[warp][lane + 32 * s] = acc[s];
+  __syncthreads();
+  if (tid < 96) {
+    float t = 0.f;
+    for (int w = 0; w < kFinThreads / 32; ++w) t += fpart[w][tid];
+    feat_out[tid] = __float_as_uint(tid < 92 ? t : 0.f);
+  }
+}
+
 __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   extern __shared__ int inl[];                     // [n_max] inlier match indices, in order
   __shared__ float Tb[12];
@@ -734,111 +840,51 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   if (A.node_pose == nullptr) return;
 
   // ---- Eq. (2) feature edge at the node poses ------------------------------------
-  // e = R_i^T (p_m - t_i) - R_j^T (p_n - t_j) (fp64: it cancels ~0.5 m coordinates);
-  // J_i = -R_i^T [I | -[p_m]x], J_j = R_j^T [I | -[p_n]x];  H += w J^T J, g += w J^T e,
-  // E += rho(|e|).  Every thread builds rows (fp32 after the fp64 residual) into smem; warp w
-  // accumulates rows w, w + 8, ... for outputs lane, lane + 32, lane + 64; a fixed-order
-  // combine over the 8 warps keeps the result bitwise deterministic.
-  float *frow = reinterpret_cast<float *>(inl + ((n_max + 3) & ~3));   // [kFeatChunk][kFeatRow]
   __shared__ float fpart[kFinThreads / 32][96];
-  double Ri[9], ti[3], Rj[9], tj[3];
-  {
-    const bt_pose Pi = A.node_pose[fa], Pj = A.node_pose[fb];
-    for (int k = 0; k < 9; ++k) { Ri[k] = Pi.R[k]; Rj[k] = Pj.R[k]; }
-    for (int k = 0; k < 3; ++k) { ti[k] = Pi.t[k]; tj[k] = Pj.t[k]; }
-  }
-  // the three outputs of this lane: kind 0 H(a,b), 1 g(a), 2 E, 3 count, -1 none
-  int okind[3], oa[3], ob[3];
-#pragma unroll
-  for (int s = 0; s < 3; ++s) {
-    int k = lane + 32 * s;
-    okind[s] = -1; oa[s] = ob[s] = 0;
-    if (k < 21) {                      // H_ii upper
-      int a = 0;
-      while (k >= 6 - a) { k -= 6 - a; ++a; }
-      oa[s] = a; ob[s] = a + k; okind[s] = 0;
-    } else if (k < 57) {               // H_ij
-      k -= 21; oa[s] = k / 6; ob[s] = 6 + k % 6; okind[s] = 0;
-    } else if (k < 78) {               // H_jj upper
-      k -= 57;
-      int a = 0;
-      while (k >= 6 - a) { k -= 6 - a; ++a; }
-      oa[s] = 6 + a; ob[s] = 6 + a + k; okind[s] = 0;
-    } else if (k < 90) { oa[s] = k - 78; ob[s] = 12; okind[s] = 1; }
-    else if (k == 90) okind[s] = 2;
-    else if (k == 91) okind[s] = 3;
-  }
-  float acc[3] = {0.f, 0.f, 0.f};
-  const int n_feat = best_h >= 0 ? best_count : 0;     // C_ij = inliers of h*, whatever the status
-  for (int done = 0; done < n_feat; done += kFeatChunk) {
-    const int nc = min(kFeatChunk, n_feat - done);
+  feature_blocks(inl, best_h >= 0 ? best_count : 0, mt, pa_f, pb_f, A.node_pose[fa], A.node_pose[fb], A.huber,
+                 reinterpret_cast<float *>(inl + ((n_max + 3) & ~3)), fpart, rec + rec_feat(n_max));
+}
+
+
+// Re-linearization of the Eq. (2) blocks at new node poses with C_ij reused: the
+// ascending inlier list is rebuilt from the record's mask, then the same accumulation as the
+// finish kernel (bitwise identical to a registration at these poses).
+struct FeatArgs {
+  KpView kp;
+  const int32_t *pairs;
+  const int32_t *matches;
+  const int32_t *n_matches;
+  uint32_t *records;
+  int rec_stride;
+  const bt_pose *node_pose;
+  double huber;
+};
+
+__global__ void __launch_bounds__(kFinThreads) k_feature_edges(FeatArgs A) {
+  extern __shared__ int inl[];
+  __shared__ int wcnt[kFinThreads / 32];
+  __shared__ float fpart[kFinThreads / 32][96];
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_max = A.kp.n_max, W = mask_words(n_max);
+  const int M = A.n_matches[p];
+  uint32_t *rec = A.records + (size_t)p * A.rec_stride;
+  const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+  int n_in = 0;
+  for (int m0 = 0; m0 < W * 32; m0 += kFinThreads) {
+    const int m = m0 + tid;
+    const bool in = m < M && ((rec[kRecMask + (m >> 5)] >> (m & 31)) & 1u);
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if (lane == 0) wcnt[warp] = __popc(bal);
     __syncthreads();
-    for (int r = tid; r < nc; r += kFinThreads) {
-      const int m = inl[done + r];
-      const int i = mt[2 * m], j = mt[2 * m + 1];
-      const double pm[3] = {pa_f[3 * i], pa_f[3 * i + 1], pa_f[3 * i + 2]};
-      const double pn[3] = {pb_f[3 * j], pb_f[3 * j + 1], pb_f[3 * j + 2]};
-      float *row = frow + r * kFeatRow;
-      double e[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        e[q] = Ri[q] * (pm[0] - ti[0]) + Ri[3 + q] * (pm[1] - ti[1]) + Ri[6 + q] * (pm[2] - ti[2]) -
-               (Rj[q] * (pn[0] - tj[0]) + Rj[3 + q] * (pn[1] - tj[1]) + Rj[6 + q] * (pn[2] - tj[2]));
-      const double Sp[9] = {0, -pm[2], pm[1], pm[2], 0, -pm[0], -pm[1], pm[0], 0};
-      const double Sq[9] = {0, -pn[2], pn[1], pn[2], 0, -pn[0], -pn[1], pn[0], 0};
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        row[13 * q + 12] = (float)e[q];
-        // (R^T)[q][c] = R[c][q];  (R^T [p]x)[q][c] = sum_k R[k][q] S[k][c]
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          row[13 * q + c] = (float)-Ri[3 * c + q];
-          row[13 * q + 6 + c] = (float)Rj[3 * c + q];
-          double x = 0, y = 0;
-#pragma unroll
-          for (int k = 0; k < 3; ++k) { x += Ri[3 * k + q] * Sp[3 * k + c]; y += Rj[3 * k + q] * Sq[3 * k + c]; }
-          row[13 * q + 3 + c] = (float)x;
-          row[13 * q + 9 + c] = (float)-y;
-        }
-      }
-      const double nrm = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
-      double w, rho;
-      if (nrm <= A.huber) { w = 1.0; rho = 0.5 * nrm * nrm; }
-      else { w = A.huber / nrm; rho = A.huber * (nrm - 0.5 * A.huber); }
-      row[39] = (float)w;
-      row[40] = (float)rho;
-    }
+    int off = 0, tot = 0;
+    for (int w = 0; w < kFinThreads / 32; ++w) { off += w < warp ? wcnt[w] : 0; tot += wcnt[w]; }
+    if (in) inl[n_in + off + __popc(bal & ((1u << lane) - 1u))] = m;
+    n_in += tot;
     __syncthreads();
-    // branch-free: H(a, b) and g(a) = H(a, 12) are the same 3-term dot product of row columns
-    // (g's column 12 is e); E and the count are selects.  Rows r and r + 8 per step (loads of
-    // both in flight), accumulated in the same row order as a one-row loop.
-    auto term = [&](const float *row, int s) {
-      const int a = oa[s], b = ob[s];
-      const float d = fmaf(row[a], row[b], fmaf(row[13 + a], row[13 + b], row[26 + a] * row[26 + b]));
-      return okind[s] <= 1 ? row[39] * d : (okind[s] == 2 ? row[40] : 1.f);
-    };
-    for (int r = warp; r < nc; r += 2 * (kFinThreads / 32)) {
-      const float *r0 = frow + r * kFeatRow;
-      const int r1i = r + kFinThreads / 32;
-      const float *r1 = frow + (r1i < nc ? r1i : r) * kFeatRow;
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        if (okind[s] < 0) continue;
-        const float t0 = term(r0, s), t1 = term(r1, s);
-        acc[s] += t0;
-        if (r1i < nc) acc[s] += t1;
-      }
-    }
   }
-#pragma unroll
-  for (int s = 0; s < 3; ++s) fpart[warp][lane + 32 * s] = acc[s];
-  __syncthreads();
-  const int fo = rec_feat(n_max);
-  if (tid < 96) {
-    float t = 0.f;
-    for (int w = 0; w < kFinThreads / 32; ++w) t += fpart[w][tid];
-    rec[fo + tid] = __float_as_uint(tid < 92 ? t : 0.f);
-  }
+  const float *pa_f = A.kp.pts + (size_t)fa * n_max * 3, *pb_f = A.kp.pts + (size_t)fb * n_max * 3;
+  feature_blocks(inl, n_in, A.matches + (size_t)p * n_max * 2, pa_f, pb_f, A.node_pose[fa], A.node_pose[fb],
+                 A.huber, reinterpret_cast<float *>(inl + ((n_max + 3) & ~3)), fpart, rec + rec_feat(n_max));
 }
 
 }  // namespace
@@ -915,4 +961,25 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   L.end(K_RANSAC_FINISH, s);
 }
 
+}  // namespace bt
+
+namespace bt {
+void launch_feature_edges(const KpView &kp, const int32_t *pairs, int P, const int32_t *matches,
+                          const int32_t *n_matches, uint32_t *records, int rec_stride, const bt_pose *node_pose,
+                          float huber, cudaStream_t s, Launch &L) {
+  if (P <= 0) return;
+  FeatArgs f;
+  f.kp = kp; f.pairs = pairs; f.matches = matches; f.n_matches = n_matches; f.records = records;
+  f.rec_stride = rec_stride; f.node_pose = node_pose; f.huber = huber;
+  const size_t smem = (size_t)((mask_words(kp.n_max) * 32 + 3) & ~3) * sizeof(int) +
+                      (size_t)kFeatChunk * kFeatRow * sizeof(float);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(k_feature_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  L.begin(K_RANSAC_FINISH, s);
+  k_feature_edges<<<P, kFinThreads, smem, s>>>(f);
+  L.end(K_RANSAC_FINISH, s);
+}
 }  // namespace bt

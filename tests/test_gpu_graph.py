@@ -171,3 +171,51 @@ def test_graph_step_errors(bt, torch, ctx):
     with pytest.raises(bt.BtError, match="ECAPACITY"):
         big = torch.zeros((17, 12), dtype=torch.float32, device="cuda")
         ctx.pose_graph_step(big, pr, rec, 512, big)
+
+
+def test_relinearize_equals_registration_and_gn_iterations_descend(bt, torch, ctx):
+    """bt_relinearize (C_ij reused) at new poses writes exactly what bt_register_pairs
+    writes there (matching / RANSAC do not depend on the node poses); iterating
+    relinearize + graph step descends Eq. (1)."""
+    sc = synth.make_scene(8, seed=31)
+    pairs = synth.all_pairs(8)
+    uids = np.arange(len(pairs), dtype=np.uint32)
+    fb = bt.FrameBatch.from_scene(sc)
+    rw = bt.record_words(512)
+    pr = torch.from_numpy(pairs).cuda()
+    ud = torch.from_numpy(uids.view(np.int32)).cuda()
+    rprm, eprm = bt.ransac_params(2048, synth.PHILOX_SEED), bt.edge_params()
+
+    def register(P_):
+        rec = torch.zeros((len(pairs), rw), dtype=torch.int32, device="cuda")
+        ctx.register_pairs(fb, sc.K, P_, pr, ud, rprm, eprm, rec)
+        torch.cuda.synchronize()
+        return rec
+
+    def energy(rec):
+        d = bt.decode_records(rec, 512)
+        return float(d["feat"][:, 90].sum() + d["dense_ij"][:, 27].sum() + d["dense_ji"][:, 27].sum())
+
+    P0 = torch.from_numpy(sc.perturbed_poses(12, rot_deg=2.0, trans_m=0.01)).cuda()
+    rec = register(P0)
+    P1 = torch.zeros_like(P0)
+    ctx.pose_graph_step(P0, pr, rec, 512, P1)
+    relin = rec.clone()
+    ctx.relinearize(fb, sc.K, P1, pr, eprm, relin)
+    torch.cuda.synchronize()
+    fresh = register(P1)
+    assert torch.equal(relin, fresh)
+    # Gauss-Newton iterations: relinearize at the current poses, step
+    E = [energy(rec)]
+    P_ = P0.clone()
+    for _ in range(3):
+        ctx.relinearize(fb, sc.K, P_, pr, eprm, rec)
+        Pn = torch.zeros_like(P_)
+        ctx.pose_graph_step(P_, pr, rec, 512, Pn)
+        P_ = Pn
+        ctx.relinearize(fb, sc.K, P_, pr, eprm, rec)
+        torch.cuda.synchronize()
+        E.append(energy(rec))
+    assert E[1] < 0.5 * E[0] and E[3] <= E[1] * 1.001, E
+    with pytest.raises(bt.BtError, match="EINVAL"):
+        ctx.relinearize(fb, sc.K, P_, pr[:5], eprm, rec[:5])
