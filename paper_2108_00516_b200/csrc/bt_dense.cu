@@ -27,7 +27,8 @@
 //                 frame's last is full.  A chunk's entries (located by binary search in the tile
 //                 offsets) + their fp64 points are staged in shared memory once and reused for
 //                 every edge leaving the frame; each warp owns whole edges (gathers pipelined
-//                 two entries ahead, one transpose reduction per (warp, edge)).
+//                 two entries ahead in three fixed slots, one transpose reduction per (warp,
+//                 edge)).
 //                 Per (entry, edge): fp32 projection, gather of the target validity + map entry,
 //                 fp64 residual difference then fp32 gates / Huber, 29 running sums.
 //  k_dense_reduce fixed-order fp64 sum of the per-tile partials of an edge (deterministic).
@@ -279,7 +280,8 @@ struct Gather {
   float4 g0;                  // x_s.x, x_s.y (fp64 as 2 x 2 words)
   float4 g1;                  // x_s.z (fp64), n_o,j.x, n_o,j.y
   float nz;                   // n_o,j.z
-  bool ok;                    // projected into the frame onto a valid pixel
+  unsigned vb;                // target validity byte (tested only when consumed: the load stays in flight)
+  bool in;                    // projected into the frame
 };
 
 // project entry k of the staged chunk with T = T_j T_i^-1 and issue its target gathers
@@ -301,7 +303,8 @@ __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, con
   }
   const int tt = tj < 0 ? 0 : tj;                                  // validity and map entry together
   const float4 *q4 = pm + 3 * (size_t)tt;
-  G.ok = tj >= 0 && __ldg(vm + tt) != 0;
+  G.in = tj >= 0;
+  G.vb = __ldg(vm + tt);
   G.g0 = __ldg(q4);
   G.g1 = __ldg(q4 + 1);
   G.nz = __ldg(reinterpret_cast<const float *>(q4 + 2));
@@ -397,14 +400,10 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
       float acc[32];
 #pragma unroll
       for (int q = 0; q < 32; ++q) acc[q] = 0.f;
-      Gather G0, G1;
-      issue_gather(sP, lane, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, G0);
-      issue_gather(sP, lane + 32, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, G1);
-      for (int k = lane; k < n; k += 32) {
-        const Gather G = G0;
-        G0 = G1;
-        issue_gather(sP, k + 64, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, G1);
-        if (!G.ok) continue;
+      // three prefetch slots in a fixed rotation (unrolled by 3, so no loaded register is moved
+      // and every gather has two entries of work to hide behind)
+      auto consume = [&](const Gather &G, int k) {
+        if (!G.in || G.vb == 0u) return;
         // target map entry: x_s = R_j^T (s - t_j) (fp64), n_o,j (fp32)
         const double xs0 = __hiloint2double(__float_as_int(G.g0.y), __float_as_int(G.g0.x));
         const double xs1 = __hiloint2double(__float_as_int(G.g0.w), __float_as_int(G.g0.z));
@@ -420,7 +419,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         const float4 nc = sN[k];
         const float2 no = sNo[k];
         const float c = fmaf(nc.w, mj0, fmaf(no.x, mj1, no.y * mj2));
-        if (!(dist2 < A.gate2f && c > A.cos_gate)) continue;
+        if (!(dist2 < A.gate2f && c > A.cos_gate)) return;
         const float n0 = nc.x, n1 = nc.y, n2 = nc.z;
         const float r = fmaf(n0, dq0, fmaf(n1, dq1, n2 * dq2));
         const float4 a = sP[k];
@@ -440,6 +439,17 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         for (int aa = 0; aa < 6; ++aa) acc[21 + aa] = fmaf(w * J[aa], r, acc[21 + aa]);
         acc[27] += rho;
         acc[28] += 1.f;
+      };
+      Gather GA, GB, GC;
+      issue_gather(sP, lane, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
+      issue_gather(sP, lane + 32, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GB);
+      for (int k = lane; k < n; k += 96) {
+        issue_gather(sP, k + 64, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GC);
+        consume(GA, k);
+        issue_gather(sP, k + 96, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
+        consume(GB, k + 32);
+        issue_gather(sP, k + 128, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GB);
+        consume(GC, k + 64);
       }
       // warp transpose reduction: lane l ends with the warp total of acc[l]
 #pragma unroll
