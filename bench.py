@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the step's kernels one by one instead of replaying it as a CUDA graph")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="time the step without the per-kernel CUDA-event brackets (overhead check)")
     return ap.parse_args()
@@ -257,6 +259,27 @@ def main():
     ctx.profile(False)
     del mt_, nm_, hc_, rec_, dout_
 
+    graph_exec = None
+    if not args.no_graph:
+        # the step's bt_register_pairs call (fork to the dense stream, match -> RANSAC, join)
+        # captured once as a CUDA graph and replayed every step (the C ABI only enqueues
+        # stream-ordered work; tests/test_gpu_parity.py checks replay == eager bitwise)
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        graph_exec = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_exec, stream=gs):
+            ctx.register_pairs(fb, sc.K, t_pose, t_pairs, t_uid, rprm, eprm, rec, stream=gs)
+        stream.wait_stream(gs)
+        torch.cuda.synchronize()
+
+    def run_step(instrumented):
+        if graph_exec is not None and not instrumented:
+            graph_exec.replay()
+            if world > 1:                                # the pose-graph exchange, after the replay
+                parallel.all_gather_records(rec, world * P)
+        else:
+            step()
+
     def timed_region(instrumented: bool):
         """K steps, L2 flushed before each (outside the events), CUDA events around each step on
         the launching stream, barrier + synchronize on both sides, max over ranks."""
@@ -271,7 +294,7 @@ def main():
             for k in range(args.steps):
                 flush.zero_()                            # evict L2 (outside the events)
                 starts[k].record(stream)
-                step()
+                run_step(instrumented)
                 stops[k].record(stream)
             torch.cuda.synchronize()
         if world > 1:
@@ -490,6 +513,7 @@ def main():
                 "data": "synthetic (seeded analytic ellipsoid scene, synth/)", "config": config_block(),
                 "hypotheses_per_s": hyp_per_s, "tests_per_s": world * tests * args.steps / sec,
                 "ms_per_step_instrumented": ms_i / args.steps,
+                "launch": "CUDA graph replay of bt_register_pairs" if graph_exec is not None else "eager launches",
                 "kernel_timing": "per-kernel CUDA-event brackets on each kernel's stream, over a second timed "
                                  "region of the same K steps (the headline region runs uninstrumented)",
                 "parallelism": f"dp{world} (one track per rank, records all-gathered over NCCL)" if world > 1
