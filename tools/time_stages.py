@@ -47,6 +47,14 @@ for name, fn in stages.items():
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    evu = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evu:                                   # uninstrumented stage time
+        flush.zero_()
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    tu = sorted(a.elapsed_time(b) for a, b in evu)
     ctx.profile(True)
     ctx.profile_read()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
@@ -59,6 +67,6 @@ for name, fn in stages.items():
     prof = ctx.profile_read()
     ctx.profile(False)
     t = sorted(a.elapsed_time(b) for a, b in ev)
-    out[name] = {"median_ms": t[len(t) // 2], "min_ms": t[0],
+    out[name] = {"median_ms": tu[len(tu) // 2], "instrumented_median_ms": t[len(t) // 2], "min_ms": tu[0],
                  "kernels_us": {k: round(1e3 * v[0] / v[1], 2) for k, v in prof.items() if v[1]}}
 print(json.dumps(out, indent=1))
