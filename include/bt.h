@@ -108,7 +108,9 @@ const char *bt_last_error(const bt_ctx *ctx);
 const char *bt_status_string(bt_status s);
 
 /* Reserve device scratch for calls up to these sizes (may be called again to grow).
-   max_frames / width / height size the staging of bt_register_pairs_host. */
+   max_frames / width / height size the dense scratch, the pose-graph system and the staging
+   of bt_register_pairs_host.  n_max <= 8192 (BT_EUNSUPPORTED beyond: a pair's point set is
+   staged in shared memory); BT_EINVAL on non-positive pair / keypoint / hypothesis counts. */
 bt_status bt_reserve(bt_ctx *ctx, int32_t max_pairs, int32_t n_max, int32_t max_hyp,
                      int32_t max_frames, int32_t width, int32_t height);
 

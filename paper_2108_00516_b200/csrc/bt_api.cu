@@ -212,6 +212,8 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
   BT_CHECK_CTX(c);
   if (max_pairs < 1 || n_max < 1 || max_hyp < 1 || max_frames < 0 || width < 0 || height < 0)
     return fail(c, BT_EINVAL, "bt_reserve: bad sizes");
+  if (n_max > 8192)                                              // smem-staged per-pair point sets
+    return fail(c, BT_EUNSUPPORTED, "bt_reserve: n_max %d > 8192", n_max);
   cudaDeviceSynchronize();
   free_scratch(c);
   c->cap_pairs = c->cap_nmax = c->cap_hyp = c->cap_frames = c->cap_w = c->cap_h = 0;

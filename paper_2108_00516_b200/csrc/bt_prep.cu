@@ -24,6 +24,7 @@ struct NormArgs {
   const float *depth;
   float *normal;
   int F, W, H;
+  int vec;                                        // W % 4 == 0 and depth 16-B aligned: float4 rows
   float fx, fy, cx, cy, ifx, ify, jump;
 };
 
@@ -96,14 +97,14 @@ __device__ __forceinline__ void store4(const NormArgs &A, int f, int v, int ub, 
 }
 
 // row r of frame D: 4 depths at ub.. (zero outside) + the 2 side neighbours in c[0], c[5]
-__device__ __forceinline__ void load_row(const float *D, int W, int H, int r, int ub, float *c) {
+__device__ __forceinline__ void load_row(const float *D, int W, int H, int r, int ub, bool vec, float *c) {
   if (r < 0 || r >= H) {
 #pragma unroll
     for (int k = 0; k < 6; ++k) c[k] = 0.f;
     return;
   }
   const float *row = D + (size_t)r * W;
-  if ((W & 3) == 0) {
+  if (vec) {
     const float4 x = ld4(row + ub);
     c[1] = x.x; c[2] = x.y; c[3] = x.z; c[4] = x.w;
   } else {
@@ -126,10 +127,10 @@ __global__ void __launch_bounds__(kNormThreads) k_normals(NormArgs A) {
   const int v = live ? (rem / W4) * 2 : 0, ub = live ? (rem - (rem / W4) * W4) * 4 : 0;
   const float *D = A.depth + (size_t)f * W * H;
   float r0[6], r1[6], r2[6], r3[6], out[12];
-  load_row(D, W, H, v - 1, ub, r0);
-  load_row(D, W, H, v, ub, r1);
-  load_row(D, W, H, v + 1, ub, r2);
-  load_row(D, W, H, v + 2, ub, r3);
+  load_row(D, W, H, v - 1, ub, A.vec, r0);
+  load_row(D, W, H, v, ub, A.vec, r1);
+  load_row(D, W, H, v + 1, ub, A.vec, r2);
+  load_row(D, W, H, v + 2, ub, A.vec, r3);
   float4 *stg = stage[threadIdx.x >> 5];
   normals4(A, v, ub, r1, r0 + 1, r2 + 1, out);
   store4(A, f, v, ub, out, stg, live);
@@ -144,6 +145,7 @@ void launch_normals(const float *depth, int F, int W, int H, const bt_intrinsics
   if (F <= 0 || W <= 0 || H <= 0) return;
   NormArgs a;
   a.depth = depth; a.normal = normal; a.F = F; a.W = W; a.H = H;
+  a.vec = (W % 4 == 0) && ((uintptr_t)depth % 16 == 0);
   a.fx = K.fx; a.fy = K.fy; a.cx = K.cx; a.cy = K.cy;
   a.ifx = 1.0f / K.fx; a.ify = 1.0f / K.fy; a.jump = jump;
   L.begin(K_NORMALS, s);

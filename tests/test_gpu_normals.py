@@ -83,3 +83,24 @@ def test_normals_edge_cases(bt, torch, ctx):
     assert np.array_equal(g[0, 1:-1, 1:-1], np.broadcast_to(np.float32([0, 0, -1]), (118, 158, 3)))
     with pytest.raises(bt.BtError, match="EINVAL"):
         gpu_normals(bt, torch, ctx, d, K, jump=-1.0)
+
+
+def test_normals_unaligned_depth_pointer(bt, torch, ctx):
+    """A depth pointer that is not 16-B aligned takes the scalar path (no misaligned float4)."""
+    K = synth.Intrinsics(600.0, 600.0, 79.5, 59.5, 160, 120)
+    sc = synth.make_scene(1, n=50, width=160, height=120, seed=4, distance=0.35)
+    flat = torch.zeros(1 + 120 * 160, dtype=torch.float32, device="cuda")
+    flat[1:] = torch.from_numpy(sc.depth.reshape(-1)).cuda()
+    d = flat[1:].view(1, 120, 160)                                  # 4-byte offset
+    out = torch.zeros((1, 120, 160, 3), dtype=torch.float32, device="cuda")
+    ctx.estimate_normals(d, K, out)
+    torch.cuda.synchronize()
+    compare(sc.depth, K, out.cpu().numpy(), oracle.estimate_normals(sc.depth, K))
+
+
+def test_reserve_rejects_oversized_keypoint_sets(bt):
+    c = bt.Context(0)
+    with pytest.raises(bt.BtError, match="EUNSUPPORTED"):
+        c.reserve(1, 8193, 16)
+    c.reserve(1, 8192, 16)                                          # the limit itself is fine
+    c.close()
