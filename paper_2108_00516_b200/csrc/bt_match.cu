@@ -13,8 +13,9 @@
 //                into one of two 128-column fp32 TMEM accumulators, S = A_hat . B_hat^T; two
 //                warpgroups read TMEM with tcgen05.ld (row = TMEM lane, each warpgroup half the
 //                columns), rank d' = |b|^2 - 2 |a||b| S (= d_hat - |a|^2) and keep the three
-//                smallest as packed (order-preserving value | index) keys with a branch-free
-//                min/max network (columns past n_b rank at +inf: no per-element bound check).  Both directions recompute the tile on the tensor cores
+//                smallest as packed (order-preserving value | index) keys, merging two keys per
+//                step with 3-input mins (8 ops per 2 keys; columns past n_b rank at +inf: no
+//                per-element bound check; the column index rides with the column constants).  Both directions recompute the tile on the tensor cores
 //                rather than reducing columns across lanes.  The epilogue certifies each row
 //                (below) and decides it, or queues it for k_rescore.
 //  certificate   With the bound
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
   extern __shared__ uint8_t tc_smem_raw[];
   __shared__ __align__(8) uint64_t bar_load[2], bar_mma[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ __align__(16) float2 cconst[2 * kN];                  // [2][128] (-2|b_j|, |b_j|^2)
+  __shared__ __align__(16) float4 cconst[2 * kN];                  // [2][128] (-2|b_j|, |b_j|^2, j bits, 0)
   __shared__ __align__(16) uint4 rmerge[128];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = base;                        // [2 K-atoms][128 rows][128 B]
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
       // a column past n_b ranks at +inf: it sorts after every real column (certify then sees
       // v - v1 = inf, as for a missing key), so the loop needs no per-element bound check
       const float v = j < nb ? A.S.norm[(size_t)fb * n_pad + j] : 0.f;
-      cconst[(c & 1) * kN + jj] = make_float2(-2.f * v, j < nb ? v * v : CUDART_INF_F);
+      cconst[(c & 1) * kN + jj] = make_float4(-2.f * v, j < nb ? v * v : CUDART_INF_F, __uint_as_float((unsigned)j), 0.f);
     }
   };
   auto load_b = [&](int c) {                                      // thread 0 only
@@ -293,20 +294,27 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
       uint32_t v[32];
       BT_TMEM_LD32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(buf * kN + cc * 32), v);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const float4 *cb4 = reinterpret_cast<const float4 *>(cconst + buf * kN + cc * 32);
-      const unsigned jbase = (unsigned)j0;
+      const float4 *cb = cconst + buf * kN + cc * 32;
+      // two keys per step merged into a sorted top-3 with 3-input min (VIMNMX3):
+      //   m = min(x, y), M = max(x, y);  r1' = min(r1, m);  r2' = min(r2, max(r1, m), M);
+      //   r3' = min(r3, max(r2, m), max(r1, M))  — 8 ops per 2 keys; the column index comes with
+      //   the column constants (shared-memory broadcast), so a key is one LOP3
 #pragma unroll
       for (int col = 0; col < 32; col += 2) {
-        const float4 cb = cb4[col >> 1];                          // columns col, col + 1
+        const float4 ca = cb[col], cbb = cb[col + 1];
         // d'' = d' + c_row >= 0, so the float bits order like the values
-        const float d0 = __fadd_rn(__fmaf_rn(na_n * cb.x, __uint_as_float(v[col]), cb.y), c_row);
-        const float d1 = __fadd_rn(__fmaf_rn(na_n * cb.z, __uint_as_float(v[col + 1]), cb.w), c_row);
-        const unsigned k0 = (__float_as_uint(d0) & ~imask) | (jbase + col);
-        const unsigned k1 = (__float_as_uint(d1) & ~imask) | (jbase + col + 1);
-        const unsigned a3 = min(r3, max(r2, k0)), a2 = min(r2, max(r1, k0));
-        r1 = min(r1, k0); r2 = a2; r3 = a3;
-        const unsigned b3 = min(s3, max(s2, k1)), b2 = min(s2, max(s1, k1));
-        s1 = min(s1, k1); s2 = b2; s3 = b3;
+        const float d0 = __fadd_rn(__fmaf_rn(na_n * ca.x, __uint_as_float(v[col]), ca.y), c_row);
+        const float d1 = __fadd_rn(__fmaf_rn(na_n * cbb.x, __uint_as_float(v[col + 1]), cbb.y), c_row);
+        const unsigned k0 = (__float_as_uint(d0) & ~imask) | __float_as_uint(ca.z);
+        const unsigned k1 = (__float_as_uint(d1) & ~imask) | __float_as_uint(cbb.z);
+        const unsigned m = min(k0, k1), M = max(k0, k1);
+        if ((col & 2) == 0) {
+          const unsigned n3 = min(min(r3, max(r2, m)), max(r1, M)), n2 = min(min(r2, max(r1, m)), M);
+          r1 = min(r1, m); r2 = n2; r3 = n3;
+        } else {
+          const unsigned n3 = min(min(s3, max(s2, m)), max(s1, M)), n2 = min(min(s2, max(s1, m)), M);
+          s1 = min(s1, m); s2 = n2; s3 = n3;
+        }
       }
     }
     tc_fence_before();
