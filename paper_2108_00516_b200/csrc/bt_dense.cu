@@ -87,6 +87,7 @@ __device__ __forceinline__ void edge_frames(const int32_t *edges, const int32_t 
 // one launch for the per-edge / per-frame setup: blocks [0, F) build frame f's ascending list
 // of outgoing edges (deterministic ballot compaction); blocks F.. compute T_j T_i^-1 per edge
 __global__ void __launch_bounds__(256) k_edge_setup(DenseArgs A) {
+  pdl_wait();
   if ((int)blockIdx.x >= A.mp.n_frames) {
     const int e = (blockIdx.x - A.mp.n_frames) * blockDim.x + threadIdx.x;
     if (e >= A.E) return;
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(256) k_edge_setup(DenseArgs A) {
 }
 
 __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
+  pdl_wait();
   __shared__ int wsum[kDenseThreads / 32];
   const int f = blockIdx.y, t = blockIdx.x;
   const int W = A.mp.W, H = A.mp.H, npx = W * H;
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
 
 // per frame: exclusive scan of the tile counts -> offs, and the number of kTile-entry chunks
 __global__ void __launch_bounds__(kDenseThreads) k_dense_scan(DenseArgs A) {
+  pdl_wait();
   __shared__ int wsum[kDenseThreads / 32];
   const int f = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -316,6 +319,7 @@ __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, con
 // transpose reduction per (warp, edge) puts the 29 sums straight into the edge's chunk partial:
 // no shared reduction buffer, no barrier between edges.
 __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
   float4 *sP = reinterpret_cast<float4 *>(dsm);                    // p (camera, fp32), (u | v << 16)
   float4 *sN = sP + kTile;                                         // n_i (camera), n_o,i.x
@@ -471,6 +475,7 @@ __global__ void __launch_bounds__(256) k_dense_reduce(const float *__restrict__ 
                                                        int tiles, const int32_t *edges, const int32_t *pairs, float *out,
                                                        int out_stride, uint32_t *records, int rec_stride, int off_ij,
                                                        int off_ji) {
+  pdl_wait();
   __shared__ double wsum[8][32];
   const int e = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -558,13 +563,13 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   a.pmap = (MapEntry *)p;    p += align256(F * npx * sizeof(MapEntry));
   a.vmap = (uint8_t *)p;
   L.begin(K_DENSE_PREP, s);
-  k_edge_setup<<<mp.n_frames + (E + 255) / 256, 256, 0, s>>>(a);
+  launch_pdl(k_edge_setup, mp.n_frames + (E + 255) / 256, 256, 0, s, a);
   L.end(K_DENSE_PREP, s);
   L.begin(K_DENSE_PREP, s);
-  k_dense_prep<<<dim3(a.tiles, mp.n_frames), kDenseThreads, 0, s>>>(a);
+  launch_pdl(k_dense_prep, dim3(a.tiles, mp.n_frames), kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);
   L.begin(K_DENSE_PREP, s);
-  k_dense_scan<<<mp.n_frames, kDenseThreads, 0, s>>>(a);
+  launch_pdl(k_dense_scan, mp.n_frames, kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);
   const size_t smem = kDenseSmem + (size_t)(mp.n_frames + 1 + a.tiles + 1) * 4;
   static size_t attr = 0;
@@ -576,10 +581,10 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   // higher-priority match / RANSAC kernels interleave (bt_api.cu register_pairs_dev)
   const int grid = a.tiles * mp.n_frames;
   L.begin(K_DENSE, s);
-  k_dense<<<grid, kEdgeThreads, smem, s>>>(a);
+  launch_pdl(k_dense, grid, kEdgeThreads, smem, s, a);
   L.end(K_DENSE, s);
   L.begin(K_DENSE_REDUCE, s);
-  k_dense_reduce<<<E, 256, 0, s>>>(a.partials, a.nch, a.tiles, edges, pairs, out, out_stride, records,
+  launch_pdl(k_dense_reduce, E, 256, 0, s, a.partials, a.nch, a.tiles, edges, pairs, out, out_stride, records,
                                   rec_stride, rec_off_ij, rec_off_ji);
   L.end(K_DENSE_REDUCE, s);
 }

@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+
+#include <utility>
 #include <stdint.h>
 
 #include "bt.h"
@@ -59,6 +61,30 @@ struct Launch {
   void begin(int k, cudaStream_t s) { if (hook) hook(user, k, 0, s); }
   void end(int k, cudaStream_t s) { ++count; if (hook) hook(user, k, 1, s); }
 };
+
+// ---- programmatic dependent launch (PDL) -----------------------------------------------
+// Chain kernels are launched with programmatic stream serialization and call pdl_wait() before
+// any memory access (griddepcontrol.wait returns once the predecessor grid has completed and
+// its memory is visible): the dependent's launch overlaps the predecessor's completion
+// (measured 0.385 -> 0.381 ms per step).  No early griddepcontrol.launch_dependents: CTAs
+// launched early park on SM resources the low-priority dense stream needs (measured 0.459 ms).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---- launchers (stream-ordered, no sync) -------------------------------------------
 // matching

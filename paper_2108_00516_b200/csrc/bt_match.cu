@@ -111,6 +111,7 @@ constexpr int kPrepPerWarp = 4;                // keypoints per warp (loads issu
 
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_desc_prep(KpView kp, MatchScratch S, int n_pad) {
+  pdl_wait();
   __shared__ unsigned wmax[kWarpsPerBlock];
   const int f = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -191,6 +192,7 @@ __device__ __forceinline__ int certify(unsigned k1, unsigned k2, unsigned k3, fl
 // tensor cores instead of reducing columns across lanes).  Thread 0 drives TMA and MMA; the
 // other threads wait at CTA barriers, not on the mbarriers.
 __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_constant__ CUtensorMap tmap, TcArgs A) {
+  pdl_wait();
   extern __shared__ uint8_t tc_smem_raw[];
   __shared__ __align__(8) uint64_t bar_load[2], bar_mma[2];
   __shared__ uint32_t tmem_base_sh;
@@ -440,6 +442,7 @@ struct RescoreArgs {
 // blockIdx.y == 0: warps over the top-2 queue (two exact distances per row);
 // blockIdx.y == 1: CTAs over the full-scan queue, the references split across the 8 warps
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_rescore(RescoreArgs A) {
+  pdl_wait();
   __shared__ float sb1[kWarpsPerBlock], sb2[kWarpsPerBlock];
   __shared__ int sj1[kWarpsPerBlock];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -500,6 +503,7 @@ __global__ void __launch_bounds__(1024)
 k_mutual(KpView kp, const int32_t *__restrict__ pairs, const int32_t *__restrict__ nn_ab,
          const int32_t *__restrict__ nn_ba, const uint8_t *__restrict__ ratio_ok,
          int32_t *__restrict__ matches, int32_t *__restrict__ n_matches, MatchScratch S) {
+  pdl_wait();
   __shared__ int warp_tot[32];
   const int p = blockIdx.x;
   if (p == 0) {                            // last reader done: zero for the next call (no memsets)
@@ -592,20 +596,21 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   }
   L.begin(K_DESC_PREP, s);
   constexpr int per_cta = kWarpsPerBlock * kPrepPerWarp;
-  k_desc_prep<<<dim3((n_pad + per_cta - 1) / per_cta, kp.n_frames), kWarpsPerBlock * 32, 0, s>>>(
-      kp, S, n_pad);
+  launch_pdl(k_desc_prep, dim3((n_pad + per_cta - 1) / per_cta, kp.n_frames), kWarpsPerBlock * 32, 0, s, kp, S,
+             n_pad);
   L.end(K_DESC_PREP, s);
   const float ratio2 = ratio >= 1.f ? 1.f : ratio * ratio;
   TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2};
   L.begin(K_MATCH_TC, s);
-  k_match_tc<<<dim3(rt_count, P, 2), kTcWarps * 32, kTcSmem, s>>>(*tmap, ta);
+  launch_pdl(k_match_tc, dim3(rt_count, P, 2), kTcWarps * 32, kTcSmem, s, *tmap, ta);
   L.end(K_MATCH_TC, s);
   RescoreArgs ra{kp, pairs, S, ibits, ratio2};
   L.begin(K_RESOLVE, s);
-  k_rescore<<<dim3(2 * 148, 2), kWarpsPerBlock * 32, 0, s>>>(ra);
+  launch_pdl(k_rescore, dim3(2 * 148, 2), kWarpsPerBlock * 32, 0, s, ra);
   L.end(K_RESOLVE, s);
   L.begin(K_MUTUAL, s);
-  k_mutual<<<P, 512, 0, s>>>(kp, pairs, S.nn_ab, S.nn_ba, S.ratio_ok, matches, n_matches, S);
+  launch_pdl(k_mutual, P, 512, 0, s, kp, pairs, (const int32_t *)S.nn_ab, (const int32_t *)S.nn_ba,
+             (const uint8_t *)S.ratio_ok, matches, n_matches, S);
   L.end(K_MUTUAL, s);
 }
 

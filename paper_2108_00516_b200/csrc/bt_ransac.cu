@@ -276,6 +276,7 @@ constexpr int kHypIter = 8;                                       // hypotheses 
 // hypothesis buffer in the scoring kernel's f32x2 pair layout.  The count is initialised to 0,
 // or to a very negative value when degenerate (it stays < 0 whatever the scoring adds).
 __global__ void __launch_bounds__(kHypThreads) k_ransac_hyp(ScoreArgs A) {
+  pdl_wait();
   extern __shared__ float sab[];                                  // [M][6] = (a_m, b_m)
   const int p = blockIdx.y;
   const int M = A.n_matches[p];
@@ -351,6 +352,7 @@ __device__ void plan_chunk(const ScoreArgs &A, int c0, long long carry, long lon
 // scalar is a broadcast operand).  Per correspondence a warp vote skips the normal gate when no
 // lane's distance gate passes.  Counts are added with integer atomics (exact, order-independent).
 __global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) {
+  pdl_wait();
   extern __shared__ float4 sq[];                                  // [chunk][4] correspondences
   __shared__ long long cpre[kPlanChunk + 1];
   __shared__ long long wsum[kScoreThreads / 32];
@@ -669,6 +671,7 @@ __device__ void feature_blocks(const int *inl, int n_feat, const int32_t *mt, co
 }
 
 __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
+  pdl_wait();
   extern __shared__ int inl[];                     // [n_max] inlier match indices, in order
   __shared__ float Tb[12];
   __shared__ double red[(kFinThreads / 32) * 9];
@@ -938,10 +941,11 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
     hyp_attr = hyp_smem;
   }
   L.begin(K_RANSAC_HYP, s);
-  k_ransac_hyp<<<dim3((a.nb * kHypPerBlock / kHypThreads + kHypIter - 1) / kHypIter, P), kHypThreads, hyp_smem, s>>>(a);
+  launch_pdl(k_ransac_hyp, dim3((a.nb * kHypPerBlock / kHypThreads + kHypIter - 1) / kHypIter, P), kHypThreads,
+             hyp_smem, s, a);
   L.end(K_RANSAC_HYP, s);
   L.begin(K_RANSAC_SCORE, s);
-  k_ransac_score<<<score_slots, kScoreThreads, smem, s>>>(a);
+  launch_pdl(k_ransac_score, score_slots, kScoreThreads, smem, s, a);
   L.end(K_RANSAC_SCORE, s);
   FinishArgs f;
   f.kp = kp; f.pairs = pairs; f.uid = uid; f.matches = matches; f.n_matches = n_matches;
@@ -957,7 +961,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
     cudaFuncSetAttribute(k_ransac_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fin_smem);
     fin_attr = fin_smem;
   }
-  k_ransac_finish<<<P, kFinThreads, fin_smem, s>>>(f);
+  launch_pdl(k_ransac_finish, P, kFinThreads, fin_smem, s, f);
   L.end(K_RANSAC_FINISH, s);
 }
 
