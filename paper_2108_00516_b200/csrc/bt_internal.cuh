@@ -53,6 +53,8 @@ struct MatchScratch {
   unsigned *work_count;    // [2]
   int32_t *nn_ab, *nn_ba;  // [P][n_max]
   uint8_t *ratio_ok;       // [P][n_max]
+  int32_t *fs_rows;        // [2 dirs][P][n_pad / 128 tiles][128] undecided rows for the batched full scan
+  int32_t *fs_count;       // [2][P][tiles]
 };
 struct Launch {
   int count = 0;

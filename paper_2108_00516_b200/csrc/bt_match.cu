@@ -15,9 +15,10 @@
 //                columns), rank d' = |b|^2 - 2 |a||b| S (= d_hat - |a|^2) and keep the three
 //                smallest as packed (order-preserving value | index) keys, merging two keys per
 //                step with 3-input mins (8 ops per 2 keys; columns past n_b rank at +inf: no
-//                per-element bound check; the column index rides with the column constants).  Both directions recompute the tile on the tensor cores
-//                rather than reducing columns across lanes.  The epilogue certifies each row
-//                (below) and decides it, or queues it for k_rescore.
+//                per-element bound check; the column index rides with the column constants).
+//                Both directions recompute the tile on the tensor cores rather than reducing
+//                columns across lanes.  The epilogue certifies each row (below) and decides it,
+//                queues it for top-2 rescoring, or lists it in the tile's full-scan list.
 //  certificate   With the bound
 //                eps = 2.2e-3 |a||b|max + 1e-6 (|a|^2 + |b|max^2) (+ key truncation) — fp16 unit
 //                vectors have relative error 2^-11 per element, so |S_hat - S| <= 2^-10 +
@@ -26,9 +27,15 @@
 //                position >= L cannot be the nearest neighbour when d'_(L) - d'_(1) > 2 eps:
 //                L = 2 certifies the best candidate; L = 3 leaves the top two, rescored exactly
 //                in fp32; otherwise (ties, ratio test, BT_FORCE_FALLBACK) the row is rescanned
-//                exactly over all references (lane l owns words [4l, 4l+4), 32 references per
-//                step, transpose reduction — the same summation tree as the top-2 rescoring).
-//  k_rescore     persistent warps over the queue of undecided rows (warp per row).
+//                exactly over all references, batched per row tile by k_fullscan (the same
+//                summation tree as the top-2 rescoring, bit for bit).
+//  k_rescore     blockIdx.y 0: warps over the top-2 queue (two exact distances per row);
+//                1: CTAs over the full-scan queue (one row per CTA, references split over 8
+//                warps) — used when n_max < 1024.
+//  k_fullscan    n_max >= 1024: per (pair, direction) its undecided rows, compacted per row
+//                tile by k_match_tc, in groups of 32 against all references (chunks of 64)
+//                staged in shared memory, 8 exact distances per thread (a reference is read
+//                once per 32 rows instead of once per row); few rows: one row per CTA.
 //  k_mutual      keep (i, NN_ab(i)) iff NN_ba(NN_ab(i)) == i (+ ratio flag), compact ascending.
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -163,6 +170,7 @@ struct TcArgs {
   MatchScratch S;
   int n_pad, ibits, P, force_fallback;
   float ratio2;
+  int fs_batched;                              // undecided rows -> per-tile lists (k_fullscan), else queue 1
 };
 
 constexpr int kTcWarps = 8;                   // 2 warpgroups: each reads all 128 TMEM lanes, half the columns
@@ -198,6 +206,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
   __shared__ uint32_t tmem_base_sh;
   __shared__ __align__(16) float4 cconst[2 * kN];                  // [2][128] (-2|b_j|, |b_j|^2, j bits, 0)
   __shared__ __align__(16) uint4 rmerge[128];
+  __shared__ int fs_warp[4];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = base;                        // [2 K-atoms][128 rows][128 B]
   uint8_t *sB = base + 32768;                // [2 buffers][2 K-atoms][128 rows][128 B]
@@ -206,7 +215,11 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wg = warp >> 2;
   const int fa = A.pairs[2 * p + dir], fb = A.pairs[2 * p + 1 - dir];
   const int na = min(A.kp.n_kp[fa], A.kp.n_max), nb = min(A.kp.n_kp[fb], A.kp.n_max);
-  if (rt * 128 >= na || nb == 0) return;                          // block-uniform
+  const int fs_tile = (dir * A.P + p) * gridDim.x + rt;           // this tile's full-scan list
+  if (rt * 128 >= na || nb == 0) {                                 // block-uniform
+    if (A.fs_batched && threadIdx.x == 0) A.S.fs_count[fs_tile] = 0;
+    return;
+  }
   const int n_pad = A.n_pad;
   const unsigned imask = (1u << A.ibits) - 1u;
   const int nchunks = (nb + kN - 1) / kN;
@@ -335,6 +348,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
   }
   if (wg == 1) rmerge[lrow] = make_uint4(r1, r2, r3, 0u);
   __syncthreads();
+  int level = 1;
   if (wg == 0 && i < na) {
     const uint4 o = rmerge[lrow];
     const unsigned ks[3] = {o.x, o.y, o.z};
@@ -346,18 +360,30 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
       r2 = n2;
       r3 = n3;
     }
-    int level = 0;
+    level = 0;
     if (!A.force_fallback && A.ratio2 >= 1.f)
       level = certify(r1, r2, r3, na_n, __uint_as_float(A.S.maxnorm[fb]), A.ibits);
     const size_t o_nn = (size_t)p * A.kp.n_max + i;
     if (level == 1) {
       (dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o_nn] = (int32_t)(r1 & imask);
       if (dir == 0) A.S.ratio_ok[o_nn] = 1;
-    } else {                                                      // queue: [0] top-2 rescoring, [1] full scan
+    } else if (level == 2 || !A.fs_batched) {                     // queue: [0] top-2 rescoring, [1] full scan
       const int qi = level == 2 ? 0 : 1;
       const unsigned slot = atomicAdd(A.S.work_count + qi, 1u);
       A.S.work[(size_t)qi * A.S.work_cap + slot] = make_uint4((unsigned)dir | ((unsigned)i << 1), (unsigned)p, r1, r2);
     }
+  }
+  // large reference sets: rows left undecided (level 0) are compacted in row order into this
+  // tile's list for the batched full scan (k_fullscan)
+  if (A.fs_batched && wg == 0) {
+    const bool fs = i < na && level == 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, fs);
+    if (lane == 0) fs_warp[warp] = __popc(bal);
+    asm volatile("bar.sync 1, 128;" ::: "memory");                // warpgroup 0 only
+    int off = 0;
+    for (int w = 0; w < warp; ++w) off += fs_warp[w];
+    if (fs) A.S.fs_rows[(size_t)fs_tile * 128 + off + __popc(bal & ((1u << lane) - 1u))] = i;
+    if (threadIdx.x == 0) A.S.fs_count[fs_tile] = fs_warp[0] + fs_warp[1] + fs_warp[2] + fs_warp[3];
   }
   tc_fence_before();
   __syncthreads();
@@ -368,7 +394,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
 }
 
 // ---------------------------------------------------------------- exact fp32 rescoring
-// warp-cooperative brute force over all nr references: best, index (ties lowest), second
+// warp-cooperative brute force over nr references (lane l owns words 4l..4l+3, 32 references
+// per step, transpose reduction — the butterfly's tree): best, index (ties lowest), second
 __device__ void exact_scan(const float4 a, const float4 *R, int nr, int lane, float &b1, int &j1, float &b2) {
   b1 = CUDART_INF_F; b2 = CUDART_INF_F; j1 = -1;
   for (int j0 = 0; j0 < nr; j0 += 32) {
@@ -416,8 +443,8 @@ __device__ void exact_scan(const float4 a, const float4 *R, int nr, int lane, fl
   }
 }
 
-// fp32 distance of one reference, summed in exact_scan's order (4 sequential terms per lane,
-// then the lane tree bit 4, 3, 2, 1, 0 — a butterfly builds the same tree)
+// fp32 distance of one reference: 4 sequential terms per lane (words 4l..4l+3), then the lane
+// tree bit 4, 3, 2, 1, 0 (a butterfly) — k_fullscan reproduces this tree bit for bit
 __device__ __forceinline__ float exact_one(const float4 a, const float4 *R, int j, int lane) {
   const float4 b = __ldg(R + (size_t)j * 32 + lane);
   const float dx = __fsub_rn(a.x, b.x), dy = __fsub_rn(a.y, b.y);
@@ -430,6 +457,7 @@ __device__ __forceinline__ float exact_one(const float4 a, const float4 *R, int 
   for (int o = 16; o >= 1; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
   return s;
 }
+
 
 struct RescoreArgs {
   KpView kp;
@@ -498,6 +526,181 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_rescore(RescoreArgs A) 
   }
 }
 
+// ---------------------------------------------------------------- exact full scans, batched
+// One CTA per (group of 32, pair, direction): the undecided rows of a (pair, direction) — the
+// row tiles' lists of k_match_tc concatenated in order — in groups of 32 against all
+// references in chunks of 64, both staged in shared memory, so a reference is read once per 32
+// rows instead of once per row; warps without rows skip the arithmetic.  With few rows or few
+// references (C2: n ~ 500) one CTA takes one row and its 8 warps split the references instead.  Warp w owns rows 4w..4w+3 of the
+// group, lane l references 2l, 2l+1 of the chunk: 8 exact fp32 distances per thread.  Each
+// distance is bitwise the value exact_one computes: the 32 "lane" partials (4
+// sequential terms over words 4l..4l+3) combined in the butterfly's tree — leaves visited in
+// bit-reversed order and merged as a binary counter.  Best (ties: lowest index) and second
+// best are combined across lanes order-independently.
+constexpr int kFsRows = 32, kFsRefs = 64, kFsPitch = kFsRefs + 2;   // sB row pitch (8-B aligned pairs)
+constexpr int kFsSmall = 4;                      // (pair, dir)s with at most this many rows: per-row path
+constexpr int kFsBatchRefs = 1024;               // batch only when a row scan reads >= 512 KB
+constexpr size_t kFsSmem = (size_t)(kFsRows * kDim + kDim * kFsPitch) * sizeof(float);
+
+struct FullScanArgs {
+  KpView kp;
+  const int32_t *pairs;
+  MatchScratch S;
+  int P, n_pad, ibits;
+  float ratio2;
+};
+
+__host__ __device__ constexpr int bitrev5(int s) {
+  return ((s & 1) << 4) | ((s & 2) << 2) | (s & 4) | ((s & 8) >> 2) | ((s & 16) >> 4);
+}
+
+__global__ void __launch_bounds__(256) k_fullscan(FullScanArgs A) {
+  pdl_wait();
+  extern __shared__ __align__(16) float fsm[];
+  float *sA = fsm;                                   // [32][128] rows (broadcast reads)
+  float *sB = fsm + kFsRows * kDim;                  // [128][kFsPitch] k-major reference chunk
+  __shared__ int toff[65];                           // prefix of the tiles' list lengths (n_max <= 8192)
+  __shared__ int grow[kFsRows];                      // this group's rows
+  const int g = blockIdx.x, p = blockIdx.y, dir = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n_tiles = A.n_pad / 128;
+  const int tile0 = (dir * A.P + p) * n_tiles;
+  if (threadIdx.x == 0) {                            // the (pair, direction)'s rows, all tiles, in order
+    int acc = 0;
+    for (int t = 0; t < n_tiles; ++t) { toff[t] = acc; acc += A.S.fs_count[tile0 + t]; }
+    toff[n_tiles] = acc;
+  }
+  __syncthreads();
+  const int u = toff[n_tiles];
+  const int fq = A.pairs[2 * p + dir], fr = A.pairs[2 * p + 1 - dir];
+  const int nr = min(A.kp.n_kp[fr], A.kp.n_max);
+  const float *Q = A.kp.desc + (size_t)fq * A.kp.n_max * kDim;
+  const float *R = A.kp.desc + (size_t)fr * A.kp.n_max * kDim;
+  auto row_of = [&](int gi) {                        // gi-th undecided row of (p, dir)
+    int t = 0;
+    while (toff[t + 1] <= gi) ++t;
+    return A.S.fs_rows[(size_t)(tile0 + t) * 128 + (gi - toff[t])];
+  };
+  if (u <= kFsSmall || nr < kFsBatchRefs) {
+    // few rows (or few references in this pair): one row per CTA, the 8 warps split the
+    // references and read them straight from L2 (exact_scan — the same distances, bit for bit)
+    __shared__ float sb1[8], sb2[8];
+    __shared__ int sj1[8];
+    const int span = ((nr + 8 * 32 - 1) / (8 * 32)) * 32;
+    const int j0 = min(nr, warp * span), j1e = min(nr, j0 + span);
+    for (int gi = g; gi < u; gi += gridDim.x) {
+      const int i = row_of(gi);
+      const float4 a = __ldg(reinterpret_cast<const float4 *>(Q + (size_t)i * kDim) + lane);
+      float b1, b2;
+      int jb;
+      exact_scan(a, reinterpret_cast<const float4 *>(R) + (size_t)j0 * 32, j1e - j0, lane, b1, jb, b2);
+      if (lane == 0) { sb1[warp] = b1; sb2[warp] = b2; sj1[warp] = jb < 0 ? -1 : jb + j0; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float B1 = CUDART_INF_F, B2 = CUDART_INF_F;
+        int J1 = -1;
+        for (int w2 = 0; w2 < 8; ++w2) {                            // ascending index order: ties -> lowest
+          if (sj1[w2] < 0) continue;
+          if (sb1[w2] < B1) { B2 = fminf(B1, sb2[w2]); B1 = sb1[w2]; J1 = sj1[w2]; }
+          else B2 = fminf(B2, sb1[w2]);
+        }
+        const size_t o = (size_t)p * A.kp.n_max + i;
+        (dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o] = J1;
+        if (dir == 0) A.S.ratio_ok[o] = (A.ratio2 >= 1.f) || (nr < 2) || (B1 < A.ratio2 * B2);
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const int g0 = g * kFsRows;
+  if (g0 >= u) return;                               // block-uniform
+  const int gn = min(kFsRows, u - g0);
+  if (threadIdx.x < kFsRows) grow[threadIdx.x] = threadIdx.x < gn ? row_of(g0 + threadIdx.x) : -1;
+  __syncthreads();                                   // grow visible to every thread
+  const bool active = 4 * warp < gn;                 // warp-uniform: this warp has rows
+  {
+    __syncthreads();
+    for (int x = threadIdx.x; x < kFsRows * (kDim / 4); x += blockDim.x) {
+      const int r = x / (kDim / 4), c4 = x % (kDim / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < gn) v = __ldg(reinterpret_cast<const float4 *>(Q + (size_t)grow[r] * kDim) + c4);
+      reinterpret_cast<float4 *>(sA)[x] = v;
+    }
+    float b1[4], b2[4];
+    int j1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { b1[q] = CUDART_INF_F; b2[q] = CUDART_INF_F; j1[q] = -1; }
+    for (int jc = 0; jc < nr; jc += kFsRefs) {
+      __syncthreads();                               // previous chunk consumed
+      for (int x = threadIdx.x; x < kFsRefs * (kDim / 4); x += blockDim.x) {
+        const int j = x / (kDim / 4), c4 = x % (kDim / 4);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (jc + j < nr) v = __ldg(reinterpret_cast<const float4 *>(R + (size_t)(jc + j) * kDim) + c4);
+        float *col = sB + (4 * c4) * kFsPitch + j;
+        col[0] = v.x; col[kFsPitch] = v.y; col[2 * kFsPitch] = v.z; col[3 * kFsPitch] = v.w;
+      }
+      __syncthreads();
+      if (!active) continue;                         // still takes part in the staging barriers
+      float lv[4][2][5];                             // binary-counter partial sums per distance
+#pragma unroll
+      for (int s = 0; s < 32; ++s) {
+        const int l = bitrev5(s);
+        float2 bw[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) bw[c] = *reinterpret_cast<const float2 *>(sB + (4 * l + c) * kFsPitch + 2 * lane);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 a = *reinterpret_cast<const float4 *>(sA + (4 * warp + q) * kDim + 4 * l);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float bx = e ? bw[0].y : bw[0].x, by = e ? bw[1].y : bw[1].x;
+            const float bz = e ? bw[2].y : bw[2].x, bv = e ? bw[3].y : bw[3].x;
+            const float dx = __fsub_rn(a.x, bx), dy = __fsub_rn(a.y, by);
+            const float dz = __fsub_rn(a.z, bz), dw = __fsub_rn(a.w, bv);
+            float x = __fmul_rn(dx, dx);
+            x = __fmaf_rn(dy, dy, x);
+            x = __fmaf_rn(dz, dz, x);
+            x = __fmaf_rn(dw, dw, x);
+            // merge leaf s into the pairwise tree (binary counter, resolved at compile time)
+#pragma unroll
+            for (int b = 0; b < 5; ++b) {
+              if (s & (1 << b)) x = __fadd_rn(lv[q][e][b], x);
+              else { lv[q][e][b] = x; break; }
+            }
+            if (s == 31) {                           // x is the full distance
+              const int j = jc + 2 * lane + e;
+              if (j < nr) {
+                if (x < b1[q]) { b2[q] = b1[q]; b1[q] = x; j1[q] = j; }
+                else if (x < b2[q]) b2[q] = x;
+              }
+            }
+          }
+        }
+      }
+    }
+    // combine the lanes' (best, index, second) per row: lowest distance, ties -> lowest index
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const float ob1 = __shfl_xor_sync(0xffffffffu, b1[q], o);
+        const int oj1 = __shfl_xor_sync(0xffffffffu, j1[q], o);
+        const float ob2 = __shfl_xor_sync(0xffffffffu, b2[q], o);
+        const bool mine = (b1[q] < ob1) || (b1[q] == ob1 && (unsigned)j1[q] < (unsigned)oj1);
+        if (mine) b2[q] = fminf(b2[q], ob1);
+        else { b2[q] = fminf(ob2, b1[q]); b1[q] = ob1; j1[q] = oj1; }
+      }
+      const int r = 4 * warp + q;
+      if (lane == 0 && r < gn) {
+        const int i = grow[r];
+        const size_t o = (size_t)p * A.kp.n_max + i;
+        (dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o] = j1[q];
+        if (dir == 0) A.S.ratio_ok[o] = (A.ratio2 >= 1.f) || (nr < 2) || (b1[q] < A.ratio2 * b2[q]);
+      }
+    }
+  }
+}
+
 // keep (i, nn_ab(i)) iff nn_ba(nn_ab(i)) == i (and the ratio flag); compact ascending in i
 __global__ void __launch_bounds__(1024)
 k_mutual(KpView kp, const int32_t *__restrict__ pairs, const int32_t *__restrict__ nn_ab,
@@ -558,7 +761,7 @@ size_t match_scratch_bytes(int max_frames, int max_pairs, int n_max) {
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   (void)rt;
   return al(F * np * kDim * 2) + al(F * np * 4) + al(F * 4) + al(2 * 2 * P * n_max * 16) + al(16) +
-         al(P * n_max * 4) * 2 + al(P * n_max);
+         al(P * n_max * 4) * 2 + al(P * n_max) + al(2 * P * np * 4) + al(2 * P * (np / 128) * 4);
 }
 
 MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_max) {
@@ -575,7 +778,9 @@ MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_m
   (void)rt;
   S.nn_ab = (int32_t *)c;        c += al(P * n_max * 4);
   S.nn_ba = (int32_t *)c;        c += al(P * n_max * 4);
-  S.ratio_ok = (uint8_t *)c;
+  S.ratio_ok = (uint8_t *)c;     c += al(P * n_max);
+  S.fs_rows = (int32_t *)c;      c += al(2 * P * np * 4);
+  S.fs_count = (int32_t *)c;
   // maxnorm and the queue counters are zero between calls: zeroed here, re-zeroed by k_mutual
   cudaMemset(S.maxnorm, 0, F * 4);
   cudaMemset(S.work_count, 0, 16);
@@ -600,12 +805,26 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
              n_pad);
   L.end(K_DESC_PREP, s);
   const float ratio2 = ratio >= 1.f ? 1.f : ratio * ratio;
-  TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2};
+  // batched full scans pay off when a row's scan reads >= 512 KB of references (n >= 1024);
+  // below that the per-row queue (one CTA per row, 8 warps split the references) is faster
+  const int fs_batched = kp.n_max >= kFsBatchRefs ? 1 : 0;
+  TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2, fs_batched};
   L.begin(K_MATCH_TC, s);
   launch_pdl(k_match_tc, dim3(rt_count, P, 2), kTcWarps * 32, kTcSmem, s, *tmap, ta);
   L.end(K_MATCH_TC, s);
-  RescoreArgs ra{kp, pairs, S, ibits, ratio2};
   L.begin(K_RESOLVE, s);
+  RescoreArgs ra{kp, pairs, S, ibits, ratio2};
+  if (fs_batched) {
+    FullScanArgs fa{kp, pairs, S, P, n_pad, ibits, ratio2};
+    static bool fs_attr = false;
+    if (!fs_attr) {
+      cudaFuncSetAttribute(k_fullscan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmem);
+      fs_attr = true;
+    }
+    launch_pdl(k_fullscan, dim3(n_pad / kFsRows, P, 2), 256, kFsSmem, s, fa);
+    L.end(K_RESOLVE, s);
+    L.begin(K_RESOLVE, s);
+  }
   launch_pdl(k_rescore, dim3(2 * 148, 2), kWarpsPerBlock * 32, 0, s, ra);
   L.end(K_RESOLVE, s);
   L.begin(K_MUTUAL, s);

@@ -439,3 +439,28 @@ def test_cuda_graph_capture_replay(bt, torch):
     torch.cuda.synchronize()
     assert np.array_equal(eager.cpu().numpy(), graphed.cpu().numpy())
     c.close()
+
+
+def test_match_batched_full_scan_equals_exact_fallback(bt, torch):
+    """n_max >= 1024 routes undecided rows to the batched full scan (k_fullscan: rows of a
+    (pair, direction) in groups of 32 against shared-memory reference chunks, the butterfly's
+    summation tree reproduced per thread).  Tensor-core path == forced exact path, bit for bit,
+    on a crowded C5-like scene (many rows undecided), and both agree with the oracle."""
+    import os
+    sc = synth.make_scene(4, n=2048, n_max=2048, pool_size=7000, seed=77, outlier_frac=0.16, render_maps=False)
+    pairs = synth.all_pairs(4)
+    outs = []
+    for force in ("0", "1"):
+        os.environ["BT_FORCE_FALLBACK"] = force
+        c = bt.Context(0)
+        c.reserve(len(pairs), 2048, 256, 4)
+        got, _, _ = gpu_match(bt, torch, c, sc, pairs)
+        outs.append(got)
+        c.close()
+    os.environ.pop("BT_FORCE_FALLBACK", None)
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    for p in (0, 5):
+        a, b = pairs[p]
+        o = oracle.match(sc.desc[a, :sc.n_kp[a]], sc.desc[b, :sc.n_kp[b]])
+        parity.compare_matches(outs[0][p], o)
