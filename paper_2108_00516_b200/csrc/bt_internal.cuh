@@ -101,6 +101,7 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
 struct RansacScratch {
   void *hyp;
   int32_t *counts;
+  int32_t *work;               // the scoring kernel's slice counter
 };
 size_t ransac_scratch_bytes(int max_pairs, int max_hyp);
 RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp);

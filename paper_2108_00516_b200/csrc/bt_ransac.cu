@@ -259,6 +259,8 @@ struct ScoreArgs {
                                // (b*512 + t, b*512 + 256 + t) packed per thread; never-passing
                                // sentinel when degenerate or h >= n_hyp
   int32_t *counts;             // [P][n_hyp] inlier counts (accumulated); < 0 => degenerate
+  int32_t *work;               // slice counter of the scoring kernel (zeroed by k_ransac_hyp)
+  int slices;                  // slices the scoring work is cut into (grabbed dynamically)
 };
 
 // One thread per hypothesis: Philox4x32-10 (counter (h, uid, 0, 0), key = seed) -> distinct
@@ -279,6 +281,7 @@ __global__ void __launch_bounds__(kHypThreads) k_ransac_hyp(ScoreArgs A) {
   pdl_wait();
   extern __shared__ float sab[];                                  // [M][6] = (a_m, b_m)
   const int p = blockIdx.y;
+  if ((blockIdx.x | blockIdx.y | threadIdx.x) == 0) *A.work = 0;   // the previous score kernel is done
   const int M = A.n_matches[p];
   if (M < 3) return;
   const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
@@ -316,7 +319,10 @@ __global__ void __launch_bounds__(kHypThreads) k_ransac_hyp(ScoreArgs A) {
   }
 }
 
-constexpr int kPlanChunk = kScoreThreads;                         // pairs per prefix chunk
+constexpr int kPlanChunk = kScoreThreads;
+// slices of the scoring work per resident CTA slot (grabbed dynamically; 2 measured best of
+// 1/2/3/4/8/16 on C2 — tools/sweep history in DESIGN.md)
+constexpr int kScoreSlicesPerSlot = 2;                         // pairs per prefix chunk
 
 // exclusive prefix of the scoring work W_q = nb * M_q (M_q >= 3) over pairs [c0, c0 + 256),
 // offset by carry: cpre[k] for pair c0 + k, cpre[256] = end of the chunk (CTA-uniform call)
@@ -343,19 +349,21 @@ __device__ void plan_chunk(const ScoreArgs &A, int c0, long long carry, long lon
 }
 
 // Balanced scoring.  The work of all pairs — (pair p, block b of kHypPerBlock hypotheses,
-// correspondence m) steps, W_p = nb * M_p — is one flat range cut into gridDim.x equal slices
-// (grid = the resident CTA slots), so every CTA gets the same number of tests whatever the
-// pairs' match counts: no partial last wave.  A slice crosses segment boundaries.  Per segment
-// the CTA loads its 512 hypotheses (two per thread, coalesced 8-B f32x2 loads), stages the
-// segment's correspondences in shared memory (AoS, 64 B each, read as warp broadcasts) and
-// scores with packed f32x2 FMAs (both hypotheses of a thread in one FFMA2; a correspondence
-// scalar is a broadcast operand).  Per correspondence a warp vote skips the normal gate when no
-// lane's distance gate passes.  Counts are added with integer atomics (exact, order-independent).
+// correspondence m) steps, W_p = nb * M_p — is one flat range cut into A.slices equal slices
+// that the CTAs grab from a counter, so the tests spread evenly whatever the pairs' match
+// counts and however many SMs the concurrent dense stream leaves free.  A slice crosses segment
+// boundaries.  Per segment the CTA loads its 512 hypotheses (two per thread, coalesced 8-B f32x2
+// loads), stages the segment's correspondences in shared memory (AoS, 64 B each, read as warp
+// broadcasts) and scores with packed f32x2 FMAs (both hypotheses of a thread in one FFMA2; a
+// correspondence scalar is a broadcast operand).  Per correspondence a warp vote skips the
+// normal gate when no lane's distance gate passes.  Counts are added with integer atomics
+// (exact, order-independent).
 __global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) {
   pdl_wait();
   extern __shared__ float4 sq[];                                  // [chunk][4] correspondences
   __shared__ long long cpre[kPlanChunk + 1];
   __shared__ long long wsum[kScoreThreads / 32];
+  __shared__ int s_slice;
   const int H = A.n_hyp;
   // total work: prefix over all pairs, chunk by chunk (one chunk for P <= 256)
   long long total = 0;
@@ -365,84 +373,99 @@ __global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) 
     total = cpre[kPlanChunk];
     c0 = c;
   }
-  const long long lo0 = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
-  if (lo0 >= hi) return;                                           // CTA-uniform
-  if (A.P > kPlanChunk) {                                          // re-plan from the chunk holding lo0
-    long long carry = 0;
-    for (c0 = 0;; c0 += kPlanChunk) {
-      plan_chunk(A, c0, carry, cpre, wsum);
-      if (cpre[kPlanChunk] > lo0 || c0 + kPlanChunk >= A.P) break;
-      carry = cpre[kPlanChunk];
-    }
-  }
-  int p;
-  {
-    int a = 0, b = min(kPlanChunk, A.P - c0);                      // cpre[a] <= lo0 < cpre[b]
-    while (b - a > 1) { const int mid = (a + b) >> 1; if (cpre[mid] <= lo0) a = mid; else b = mid; }
-    p = c0 + a;
-  }
-  long long lo = lo0;
-  while (lo < hi) {
-    for (;;) {                                                     // skip pairs without work
-      if (p - c0 >= kPlanChunk) {
+  bool fresh = true;                                               // cpre holds the last chunk
+  for (;;) {
+    if (threadIdx.x == 0) s_slice = atomicAdd(A.work, 1);
+    __syncthreads();
+    const int sl = s_slice;
+    __syncthreads();
+    if (sl >= A.slices) break;                                       // CTA-uniform
+    const long long lo0 = total * sl / A.slices, hi = total * (sl + 1) / A.slices;
+    if (lo0 >= hi) continue;
+    if (A.P > kPlanChunk && (fresh || cpre[0] > lo0)) {              // re-plan from the chunk holding lo0
+      long long carry = 0;
+      for (c0 = 0;; c0 += kPlanChunk) {
+        plan_chunk(A, c0, carry, cpre, wsum);
+        if (cpre[kPlanChunk] > lo0 || c0 + kPlanChunk >= A.P) break;
+        carry = cpre[kPlanChunk];
+      }
+    } else if (A.P > kPlanChunk) {                                   // slices ascend: step forward
+      while (cpre[kPlanChunk] <= lo0 && c0 + kPlanChunk < A.P) {
         const long long carry = cpre[kPlanChunk];
         c0 += kPlanChunk;
         plan_chunk(A, c0, carry, cpre, wsum);
       }
-      const long long end_p = p + 1 - c0 < kPlanChunk ? cpre[p + 1 - c0] : cpre[kPlanChunk];
-      if (end_p > lo) break;
-      ++p;
     }
-    const int M = A.n_matches[p];
-    const long long rel = lo - cpre[p - c0];
-    const int b = (int)(rel / M), m0 = (int)(rel - (long long)b * M);
-    const int m1 = (int)min((long long)M, m0 + (hi - lo));
-    const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
-    const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
-    const float *pa_f = A.kp.pts + (size_t)fa * A.kp.n_max * 3, *pb_f = A.kp.pts + (size_t)fb * A.kp.n_max * 3;
-    const float *na_f = A.kp.nrm + (size_t)fa * A.kp.n_max * 3, *nb_f = A.kp.nrm + (size_t)fb * A.kp.n_max * 3;
-    static_assert(kHypPerThread == 2, "packed f32x2 scoring holds two hypotheses per thread");
-    f32x2 T2[12];                                                  // coalesced 8-B loads, L2-resident
+    fresh = false;
+    int p;
     {
-      const f32x2 *src = A.hyp + ((size_t)p * A.nb + b) * 12 * kScoreThreads + threadIdx.x;
-#pragma unroll
-      for (int q = 0; q < 12; ++q) T2[q] = __ldcg(src + q * kScoreThreads);
+      int a = 0, b = min(kPlanChunk, A.P - c0);                      // cpre[a] <= lo0 < cpre[b]
+      while (b - a > 1) { const int mid = (a + b) >> 1; if (cpre[mid] <= lo0) a = mid; else b = mid; }
+      p = c0 + a;
     }
-    const f32x2 nd2 = pk(A.ndelta2, A.ndelta2), nc2 = pk(A.ncosa, A.ncosa);
-    unsigned cnt[kHypPerThread];
-#pragma unroll
-    for (int k = 0; k < kHypPerThread; ++k) cnt[k] = 0u;
-    for (int cs = m0; cs < m1; cs += A.chunk) {
-      const int len = min(A.chunk, m1 - cs);
-      __syncthreads();
-      for (int k = threadIdx.x; k < len; k += kScoreThreads) {
-        const int i = mt[2 * (cs + k)], j = mt[2 * (cs + k) + 1];
-        float4 q0, q1, q2, q3;
-        pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
-        sq[4 * k] = q0; sq[4 * k + 1] = q1; sq[4 * k + 2] = q2; sq[4 * k + 3] = q3;
+    long long lo = lo0;
+    while (lo < hi) {
+      for (;;) {                                                     // skip pairs without work
+        if (p - c0 >= kPlanChunk) {
+          const long long carry = cpre[kPlanChunk];
+          c0 += kPlanChunk;
+          plan_chunk(A, c0, carry, cpre, wsum);
+        }
+        const long long end_p = p + 1 - c0 < kPlanChunk ? cpre[p + 1 - c0] : cpre[kPlanChunk];
+        if (end_p > lo) break;
+        ++p;
       }
-      __syncthreads();
-#pragma unroll 2
-      for (int m = 0; m < len; ++m) {
-        const float4 q0 = sq[4 * m], q1 = sq[4 * m + 1];
-        const f32x2 d = dist_term2(T2, q0, q1, nd2);
-        unsigned d0, d1;
-        split(d, d0, d1);
-        if (__any_sync(0xffffffffu, (int)(d0 | d1) < 0)) {
-          const float4 q2 = sq[4 * m + 2], q3 = sq[4 * m + 3];
-          unsigned c0_, c1_;
-          split(normal_term2(T2, q1, q2, q3, nc2), c0_, c1_);
-          cnt[0] += (d0 & ~c0_) >> 31;
-          cnt[1] += (d1 & ~c1_) >> 31;
+      const int M = A.n_matches[p];
+      const long long rel = lo - cpre[p - c0];
+      const int b = (int)(rel / M), m0 = (int)(rel - (long long)b * M);
+      const int m1 = (int)min((long long)M, m0 + (hi - lo));
+      const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+      const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
+      const float *pa_f = A.kp.pts + (size_t)fa * A.kp.n_max * 3, *pb_f = A.kp.pts + (size_t)fb * A.kp.n_max * 3;
+      const float *na_f = A.kp.nrm + (size_t)fa * A.kp.n_max * 3, *nb_f = A.kp.nrm + (size_t)fb * A.kp.n_max * 3;
+      static_assert(kHypPerThread == 2, "packed f32x2 scoring holds two hypotheses per thread");
+      f32x2 T2[12];                                                  // coalesced 8-B loads, L2-resident
+      {
+        const f32x2 *src = A.hyp + ((size_t)p * A.nb + b) * 12 * kScoreThreads + threadIdx.x;
+  #pragma unroll
+        for (int q = 0; q < 12; ++q) T2[q] = __ldcg(src + q * kScoreThreads);
+      }
+      const f32x2 nd2 = pk(A.ndelta2, A.ndelta2), nc2 = pk(A.ncosa, A.ncosa);
+      unsigned cnt[kHypPerThread];
+  #pragma unroll
+      for (int k = 0; k < kHypPerThread; ++k) cnt[k] = 0u;
+      for (int cs = m0; cs < m1; cs += A.chunk) {
+        const int len = min(A.chunk, m1 - cs);
+        __syncthreads();
+        for (int k = threadIdx.x; k < len; k += kScoreThreads) {
+          const int i = mt[2 * (cs + k)], j = mt[2 * (cs + k) + 1];
+          float4 q0, q1, q2, q3;
+          pack_corr(pa_f + 3 * i, na_f + 3 * i, pb_f + 3 * j, nb_f + 3 * j, q0, q1, q2, q3);
+          sq[4 * k] = q0; sq[4 * k + 1] = q1; sq[4 * k + 2] = q2; sq[4 * k + 3] = q3;
+        }
+        __syncthreads();
+  #pragma unroll 2
+        for (int m = 0; m < len; ++m) {
+          const float4 q0 = sq[4 * m], q1 = sq[4 * m + 1];
+          const f32x2 d = dist_term2(T2, q0, q1, nd2);
+          unsigned d0, d1;
+          split(d, d0, d1);
+          if (__any_sync(0xffffffffu, (int)(d0 | d1) < 0)) {
+            const float4 q2 = sq[4 * m + 2], q3 = sq[4 * m + 3];
+            unsigned c0_, c1_;
+            split(normal_term2(T2, q1, q2, q3, nc2), c0_, c1_);
+            cnt[0] += (d0 & ~c0_) >> 31;
+            cnt[1] += (d1 & ~c1_) >> 31;
+          }
         }
       }
+  #pragma unroll
+      for (int k = 0; k < kHypPerThread; ++k) {
+        const int h = b * kHypPerBlock + k * kScoreThreads + threadIdx.x;
+        if (h < H && cnt[k]) atomicAdd(A.counts + (size_t)p * H + h, (int)cnt[k]);
+      }
+      lo += m1 - m0;
     }
-#pragma unroll
-    for (int k = 0; k < kHypPerThread; ++k) {
-      const int h = b * kHypPerBlock + k * kScoreThreads + threadIdx.x;
-      if (h < H && cnt[k]) atomicAdd(A.counts + (size_t)p * H + h, (int)cnt[k]);
-    }
-    lo += m1 - m0;
   }
 }
 
@@ -678,7 +701,11 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   __shared__ int wcnt[kFinThreads / 32];
   __shared__ double shT[12];
   __shared__ int sh_status;
+  // blockIdx.y == 0: h*, C_ij mask, refit, record words; blockIdx.y == 1 (launched only with
+  // node poses): the same h* and inlier list, then the Eq. (2) blocks — the two latency chains
+  // of a pair run side by side
   const int p = blockIdx.x;
+  const bool feat_cta = blockIdx.y == 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_max = A.kp.n_max, W = mask_words(n_max);
   unsigned long long key_all;
@@ -699,7 +726,7 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
         int4 c4 = make_int4(-1, -1, -1, -1);
         if (M >= 3) c4 = __ldcg(reinterpret_cast<const int4 *>(cp) + h4);
         const int cs[4] = {max(c4.x, -1), max(c4.y, -1), max(c4.z, -1), max(c4.w, -1)};
-        if (A.hyp_counts)
+        if (A.hyp_counts && !feat_cta)
           reinterpret_cast<int4 *>(A.hyp_counts + (size_t)p * A.n_hyp)[h4] = make_int4(cs[0], cs[1], cs[2], cs[3]);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -711,7 +738,7 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     } else {
       for (int h = tid; h < A.n_hyp; h += kFinThreads) {
         const int cnt = M >= 3 ? max(cp[h], -1) : -1;
-        if (A.hyp_counts) A.hyp_counts[(size_t)p * A.n_hyp + h] = cnt;
+        if (A.hyp_counts && !feat_cta) A.hyp_counts[(size_t)p * A.n_hyp + h] = cnt;
         const unsigned long long x = ((unsigned long long)(uint32_t)(cnt + 1) << 32) | (0xFFFFFFFFu - (uint32_t)h);
         kk = x > kk ? x : kk;
       }
@@ -763,7 +790,7 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     }
     const unsigned bal = __ballot_sync(0xffffffffu, in);
     if (lane == 0) {
-      if ((m0 >> 5) + warp < W) rec[kRecMask + (m0 >> 5) + warp] = bal;
+      if (!feat_cta && (m0 >> 5) + warp < W) rec[kRecMask + (m0 >> 5) + warp] = bal;
       wcnt[warp] = __popc(bal);
     }
     __syncthreads();
@@ -777,6 +804,13 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     __syncthreads();
   }
   const int best_count = n_in;
+  __shared__ float fpart[kFinThreads / 32][96];
+  if (feat_cta) {
+    // ---- Eq. (2) feature edge at the node poses ----------------------------------
+    feature_blocks(inl, best_h >= 0 ? best_count : 0, mt, pa_f, pb_f, A.node_pose[fa], A.node_pose[fb], A.huber,
+                   reinterpret_cast<float *>(inl + ((n_max + 3) & ~3)), fpart, rec + rec_feat(n_max));
+    return;
+  }
   if (best_h >= 0 && best_count < A.min_inliers) status = BT_PAIR_FEW_INLIERS;
 
   // refit: Arun on all inliers (fp64), two-pass centroid / cross-covariance
@@ -840,12 +874,6 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     for (int k = 0; k < 12; ++k)
       rec[kRecTRefit + k] = __float_as_uint(refit_ok ? (float)(k < 9 ? Rr[k] : tr[k - 9]) : Tb[k]);
   }
-  if (A.node_pose == nullptr) return;
-
-  // ---- Eq. (2) feature edge at the node poses ------------------------------------
-  __shared__ float fpart[kFinThreads / 32][96];
-  feature_blocks(inl, best_h >= 0 ? best_count : 0, mt, pa_f, pb_f, A.node_pose[fa], A.node_pose[fb], A.huber,
-                 reinterpret_cast<float *>(inl + ((n_max + 3) & ~3)), fpart, rec + rec_feat(n_max));
 }
 
 
@@ -897,13 +925,15 @@ static size_t hyp_slots(int max_pairs, int max_hyp) {
 }
 
 size_t ransac_scratch_bytes(int max_pairs, int max_hyp) {
-  return (hyp_slots(max_pairs, max_hyp) * 48 + 255) / 256 * 256 + ((size_t)max_pairs * max_hyp * 4 + 255) / 256 * 256;
+  return (hyp_slots(max_pairs, max_hyp) * 48 + 255) / 256 * 256 + ((size_t)max_pairs * max_hyp * 4 + 255) / 256 * 256 +
+         256;
 }
 
 RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp) {
   RansacScratch r;
   r.hyp = scratch;
   r.counts = (int32_t *)((char *)scratch + (hyp_slots(max_pairs, max_hyp) * 48 + 255) / 256 * 256);
+  r.work = (int32_t *)((char *)r.counts + ((size_t)max_pairs * max_hyp * 4 + 255) / 256 * 256);
   return r;
 }
 
@@ -928,6 +958,8 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   ScoreArgs a;
   a.hyp = (f32x2 *)rs.hyp;
   a.counts = rs.counts;
+  a.work = rs.work;
+  a.slices = score_slots * kScoreSlicesPerSlot;
   a.kp = kp; a.pairs = pairs; a.uid = uid; a.matches = matches; a.n_matches = n_matches;
   a.P = P; a.n_hyp = prm.n_hyp; a.nb = (prm.n_hyp + kHypPerBlock - 1) / kHypPerBlock; a.chunk = chunk;
   a.k0 = (uint32_t)(prm.seed & 0xffffffffull); a.k1 = (uint32_t)(prm.seed >> 32);
@@ -961,7 +993,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
     cudaFuncSetAttribute(k_ransac_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fin_smem);
     fin_attr = fin_smem;
   }
-  launch_pdl(k_ransac_finish, P, kFinThreads, fin_smem, s, f);
+  launch_pdl(k_ransac_finish, dim3(P, node_pose ? 2 : 1), kFinThreads, fin_smem, s, f);
   L.end(K_RANSAC_FINISH, s);
 }
 

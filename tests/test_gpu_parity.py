@@ -464,3 +464,30 @@ def test_match_batched_full_scan_equals_exact_fallback(bt, torch):
         a, b = pairs[p]
         o = oracle.match(sc.desc[a, :sc.n_kp[a]], sc.desc[b, :sc.n_kp[b]])
         parity.compare_matches(outs[0][p], o)
+
+
+def test_ransac_many_pairs_dynamic_slices(bt, torch):
+    """P = 595 > 2 x 256 pairs: the scoring kernel's work prefix spans three plan chunks and its
+    dynamically grabbed slices cross chunk boundaries.  Counts of pairs around the chunk
+    boundaries equal the oracle's; the whole batch equals the same pairs registered in calls
+    of <= 200 pairs (one plan chunk each) bit for bit."""
+    sc = synth.make_scene(35, n=96, n_max=128, pool_size=400, seed=77, width=160, height=120, distance=0.35)
+    pairs = synth.all_pairs(35)
+    P, H = len(pairs), 256
+    uids = np.arange(1000, 1000 + P, dtype=np.uint32)
+    c = bt.Context(0)
+    c.reserve(P, 128, H, 35, 160, 120)
+    mls = [oracle.match(sc.desc[a, :sc.n_kp[a]], sc.desc[b, :sc.n_kp[b]])["pairs"] for a, b in pairs]
+    rec, cnt = gpu_ransac(bt, torch, c, sc, pairs, mls, H, uids)
+    parts = [gpu_ransac(bt, torch, c, sc, pairs[s:s + 200], mls[s:s + 200], H, uids[s:s + 200])
+             for s in range(0, P, 200)]
+    c.close()
+    assert np.array_equal(cnt, np.concatenate([pc for _, pc in parts]))
+    for k in ("status", "best_hyp", "best_count"):
+        assert np.array_equal(rec[k], np.concatenate([pr[k] for pr, _ in parts]))
+    assert (rec["status"] == 0).sum() > P // 2
+    for p in (0, 255, 256, 257, 511, 512, P - 1):
+        a, b = pairs[p]
+        pa, na, pb, nb = _pair_arrays(sc, a, b, mls[p])
+        oc = oracle.ransac_counts(pa, na, pb, nb, H, int(uids[p]), SEED)
+        parity.compare_ransac(cnt[p], {k: v[p] for k, v in rec.items()}, oc, pa, na, pb, nb, what=f"pair {p}")

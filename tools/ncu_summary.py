@@ -90,6 +90,44 @@ lines += ["", f"## Launch list ({os.path.basename(launches)}): device time per k
           "| kernel | launches | total us | share |", "|---|---|---|---|"]
 for k, v in tot.most_common():
     lines.append(f"| {k} | {cnt[k]} | {v:.1f} | {100 * v / all_us:.1f}% |")
+# the bt_register_pairs step alone (the bench command also runs standalone stage passes and the
+# NEXT-row sections, which reuse the dense kernels): split the list into maximal runs of step
+# kernels (the L2 flush between steps and every other kernel end a run) and keep the runs that
+# hold whole steps (as many k_dense as k_ransac_score launches, at least one)
+STEP = {"k_desc_prep", "k_match_tc", "k_fullscan", "k_rescore", "k_mutual", "k_ransac_hyp", "k_ransac_score",
+        "k_ransac_finish", "k_edge_setup", "k_dense_prep", "k_dense_scan", "k_dense", "k_dense_reduce"}
+stot, scnt, n_steps = collections.Counter(), collections.Counter(), 0
+run_t, run_c = collections.Counter(), collections.Counter()
+
+
+def close_run():
+    global n_steps
+    ns = run_c["k_ransac_score"]
+    if ns and run_c["k_dense"] == ns:
+        stot.update(run_t)
+        scnt.update(run_c)
+        n_steps += ns
+    run_t.clear()
+    run_c.clear()
+
+
+for r in lst[hi + 1:]:
+    if len(r) <= vi:
+        continue
+    k = short(r[ki])
+    if k not in STEP:
+        close_run()
+        continue
+    run_t[k] += float(r[vi].replace(",", "")) * (1e-3 if r[ui] == "ns" else 1.0)
+    run_c[k] += 1
+close_run()
+if n_steps:
+    step_us = sum(stot.values())
+    lines += ["", f"## The registration step only ({n_steps} whole steps in the list; serialised, cold cache)", "",
+              "| kernel | launches / step | us / step | share of the step's kernels |", "|---|---|---|---|"]
+    for k, v in stot.most_common():
+        lines.append(f"| {k} | {scnt[k] / n_steps:g} | {v / n_steps:.1f} | {100 * v / step_us:.1f}% |")
+    lines.append(f"| (sum) | | {step_us / n_steps:.1f} | 100% |")
 open(out + ".md", "w").write("\n".join(lines) + "\n")
 json.dump({k: v for k, v in traffic.items()}, open(os.path.join(os.path.dirname(out), "ncu_traffic.json"), "w"),
           indent=1)
