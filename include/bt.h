@@ -221,6 +221,26 @@ bt_status bt_relinearize(bt_ctx *ctx, const bt_keypoints *kp, const bt_maps *map
                          const bt_pose *node_pose, const int32_t *pairs, int32_t P, const bt_edge_params *eprm,
                          uint32_t *records, void *stream);
 
+/* The C_ij cache across calls ("If C_ij has been built during a previous pose graph
+   optimization, it is reused"): a tracker keeps every pair's match list next to its record so
+   that pairs registered in DIFFERENT bt_register_pairs calls (e.g. each frame's new pairs
+   against the keyframes) can be re-linearized together.
+   bt_copy_matches copies the match lists of the LAST bt_register_pairs (device entry) on this
+   context to caller-owned device buffers: matches [P][n_max][2] i32 (row m of pair p = the
+   m-th mutual match (i, j), ascending i; the record's inlier mask bit m refers to it; rows past
+   n_matches[p] undefined), n_matches [P] i32.  Errors: BT_EINVAL (NULL buffers, P or n_max
+   different from that call's).
+   bt_relinearize_matches is bt_relinearize with the match lists given explicitly (device,
+   layout as above, P pairs, kp->n_max rows each) instead of the context's; the updated words
+   are bitwise equal to what bt_register_pairs writes at these poses.  Errors: BT_EINVAL (NULL
+   buffers / params), BT_ECAPACITY (P > reserved max_pairs), else as bt_register_pairs. */
+bt_status bt_copy_matches(bt_ctx *ctx, int32_t P, int32_t n_max, int32_t *matches, int32_t *n_matches,
+                          void *stream);
+bt_status bt_relinearize_matches(bt_ctx *ctx, const bt_keypoints *kp, const bt_maps *maps,
+                                 const bt_intrinsics *K, const bt_pose *node_pose, const int32_t *pairs,
+                                 int32_t P, const int32_t *matches, const int32_t *n_matches,
+                                 const bt_edge_params *eprm, uint32_t *records, void *stream);
+
 /* ---- NEXT-4: input prep — the normal map n_i(x) of Eq. (3) from depth (SPEC
    estimate_normals S:157-165) -----------------------------------------------------------
    depth [F][H][W] f32 device (<= 0: invalid) -> normal [F][H][W][3] f32 device (16-B

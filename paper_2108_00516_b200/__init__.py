@@ -26,7 +26,7 @@ SYMBOLS = ("bt_create", "bt_destroy", "bt_last_error", "bt_status_string", "bt_r
            "bt_record_words", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
            "bt_register_pairs_host", "bt_compose_poses", "bt_last_launch_count", "bt_profile_enable",
            "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step",
-           "bt_estimate_normals", "bt_relinearize")
+           "bt_estimate_normals", "bt_relinearize", "bt_relinearize_matches", "bt_copy_matches")
 
 
 class BtError(RuntimeError):
@@ -107,6 +107,9 @@ def lib():
         L.bt_estimate_normals.argtypes = [vp, vp, i32, i32, i32, C.POINTER(Intrinsics), C.c_float, vp, vp]
         L.bt_relinearize.argtypes = [vp, C.POINTER(Keypoints), C.POINTER(Maps), C.POINTER(Intrinsics), vp, vp, i32,
                                      C.POINTER(EdgeParams), vp, vp]
+        L.bt_relinearize_matches.argtypes = [vp, C.POINTER(Keypoints), C.POINTER(Maps), C.POINTER(Intrinsics), vp, vp,
+                                             i32, vp, vp, C.POINTER(EdgeParams), vp, vp]
+        L.bt_copy_matches.argtypes = [vp, i32, i32, vp, vp, vp]
         L.bt_last_launch_count.argtypes = [vp]
         L.bt_last_launch_count.restype = i32
         L.bt_profile_enable.argtypes = [vp, i32]
@@ -118,7 +121,8 @@ def lib():
         L.bt_profile_read.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.bt_profile_read.restype = C.c_int
         for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
-                  "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals", "bt_relinearize"):
+                  "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals", "bt_relinearize",
+                  "bt_relinearize_matches", "bt_copy_matches"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -298,13 +302,28 @@ class Context:
                                              _ptr(new_pose), _ptr(delta), _ptr(stats), self._stream(stream)),
                     "bt_pose_graph_step")
 
-    def relinearize(self, fb: FrameBatch, K, node_pose, pairs, eprm: EdgeParams, records, stream=None):
-        """Eq. (2) / Eq. (3) blocks of `records` at new node poses, C_ij reused (bt_relinearize)."""
+    def relinearize(self, fb: FrameBatch, K, node_pose, pairs, eprm: EdgeParams, records, matches=None,
+                    n_matches=None, stream=None):
+        """Eq. (2) / Eq. (3) blocks of `records` at new node poses, C_ij reused: with the match
+        lists of the last register_pairs (bt_relinearize), or with caller-kept lists
+        `matches` [P][n_max][2] / `n_matches` [P] (bt_relinearize_matches)."""
         kp, mp = fb.keypoints(), fb.maps()
         Ki = intrinsics(K) if not isinstance(K, Intrinsics) else K
-        self._check(lib().bt_relinearize(self._h, C.byref(kp), C.byref(mp), C.byref(Ki), _ptr(node_pose), _ptr(pairs),
-                                         int(pairs.shape[0]), C.byref(eprm), _ptr(records), self._stream(stream)),
-                    "bt_relinearize")
+        if matches is None:
+            self._check(lib().bt_relinearize(self._h, C.byref(kp), C.byref(mp), C.byref(Ki), _ptr(node_pose),
+                                             _ptr(pairs), int(pairs.shape[0]), C.byref(eprm), _ptr(records),
+                                             self._stream(stream)), "bt_relinearize")
+        else:
+            self._check(lib().bt_relinearize_matches(self._h, C.byref(kp), C.byref(mp), C.byref(Ki), _ptr(node_pose),
+                                                     _ptr(pairs), int(pairs.shape[0]), _ptr(matches), _ptr(n_matches),
+                                                     C.byref(eprm), _ptr(records), self._stream(stream)),
+                        "bt_relinearize_matches")
+
+    def copy_matches(self, matches, n_matches, stream=None):
+        """The last register_pairs' match lists into caller buffers [P][n_max][2] / [P]
+        (bt_copy_matches) — the C_ij cache a tracker keeps across frames."""
+        self._check(lib().bt_copy_matches(self._h, int(matches.shape[0]), int(matches.shape[1]), _ptr(matches),
+                                          _ptr(n_matches), self._stream(stream)), "bt_copy_matches")
 
     def estimate_normals(self, depth, K, normal, jump: float = 0.05, stream=None):
         """Normal map [F][H][W][3] from depth [F][H][W] (bt_estimate_normals; NEXT-4)."""

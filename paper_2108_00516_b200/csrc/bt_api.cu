@@ -42,6 +42,7 @@ struct bt_ctx {
   void *dense = nullptr;
   void *graph = nullptr;                      // pose-graph step scratch (bt_graph.cu)
   int cached_P = -1;                          // pairs whose match lists c->matches holds (C_ij cache)
+  int cached_nmax = -1;                       // ... and their row stride
   // staging for bt_register_pairs_host
   int32_t *st_nkp = nullptr, *st_pairs = nullptr;
   uint32_t *st_uid = nullptr, *st_records = nullptr;
@@ -346,6 +347,7 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
     }
   }
   c->cached_P = P;
+  c->cached_nmax = kp->n_max;
   return after_launch(c, "bt_register_pairs");
 }
 
@@ -491,21 +493,19 @@ bt_status bt_estimate_normals(bt_ctx *c, const float *depth, int32_t n_frames, i
   return after_launch(c, "bt_estimate_normals");
 }
 
-bt_status bt_relinearize(bt_ctx *c, const bt_keypoints *kp, const bt_maps *maps, const bt_intrinsics *K,
-                         const bt_pose *node_pose, const int32_t *pairs, int32_t P, const bt_edge_params *eprm,
-                         uint32_t *records, void *stream) {
-  BT_CHECK_CTX(c);
+static bt_status relinearize(bt_ctx *c, const char *what, const bt_keypoints *kp, const bt_maps *maps,
+                             const bt_intrinsics *K, const bt_pose *node_pose, const int32_t *pairs, int32_t P,
+                             const int32_t *matches, const int32_t *n_matches, const bt_edge_params *eprm,
+                             uint32_t *records, void *stream) {
   bt_status s;
   if ((s = check_kp(c, kp)) != BT_OK) return s;
   if ((s = check_maps(c, maps, K)) != BT_OK) return s;
-  if (!eprm) return fail(c, BT_EINVAL, "bt_relinearize: NULL edge params");
+  if (!eprm) return fail(c, BT_EINVAL, "%s: NULL edge params", what);
   if ((s = check_edge(c, eprm)) != BT_OK) return s;
   if (P < 0) return fail(c, BT_EINVAL, "P < 0");
   if (P == 0) return BT_OK;
-  if (P != c->cached_P)
-    return fail(c, BT_EINVAL, "bt_relinearize: P %d does not match the last bt_register_pairs (%d pairs)", P,
-                c->cached_P);
-  if (!node_pose || !pairs || !records) return fail(c, BT_EINVAL, "bt_relinearize: NULL buffer");
+  if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "%s: P %d > reserved %d", what, P, c->cap_pairs);
+  if (!node_pose || !pairs || !records || !matches || !n_matches) return fail(c, BT_EINVAL, "%s: NULL buffer", what);
   const cudaStream_t st = (cudaStream_t)stream;
   const int rw = bt::rec_words(kp->n_max);
   c->launch.count = 0;
@@ -513,11 +513,46 @@ bt_status bt_relinearize(bt_ctx *c, const bt_keypoints *kp, const bt_maps *maps,
   cudaStreamWaitEvent(c->side, c->ev_fork, 0);
   bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, nullptr, 0, records, rw,
                    bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch);
-  bt::launch_feature_edges(kview(kp), pairs, P, c->matches, c->n_matches, records, rw, node_pose, eprm->huber_m, st,
+  bt::launch_feature_edges(kview(kp), pairs, P, matches, n_matches, records, rw, node_pose, eprm->huber_m, st,
                            c->launch);
   cudaEventRecord(c->ev_join, c->side);
   cudaStreamWaitEvent(st, c->ev_join, 0);
-  return after_launch(c, "bt_relinearize");
+  return after_launch(c, what);
+}
+
+bt_status bt_relinearize(bt_ctx *c, const bt_keypoints *kp, const bt_maps *maps, const bt_intrinsics *K,
+                         const bt_pose *node_pose, const int32_t *pairs, int32_t P, const bt_edge_params *eprm,
+                         uint32_t *records, void *stream) {
+  BT_CHECK_CTX(c);
+  if (P > 0 && (P != c->cached_P || (kp && kp->n_max != c->cached_nmax)))
+    return fail(c, BT_EINVAL, "bt_relinearize: P %d does not match the last bt_register_pairs (%d pairs)", P,
+                c->cached_P);
+  return relinearize(c, "bt_relinearize", kp, maps, K, node_pose, pairs, P, c->matches, c->n_matches, eprm, records,
+                     stream);
+}
+
+bt_status bt_relinearize_matches(bt_ctx *c, const bt_keypoints *kp, const bt_maps *maps, const bt_intrinsics *K,
+                                 const bt_pose *node_pose, const int32_t *pairs, int32_t P, const int32_t *matches,
+                                 const int32_t *n_matches, const bt_edge_params *eprm, uint32_t *records,
+                                 void *stream) {
+  BT_CHECK_CTX(c);
+  return relinearize(c, "bt_relinearize_matches", kp, maps, K, node_pose, pairs, P, matches, n_matches, eprm, records,
+                     stream);
+}
+
+bt_status bt_copy_matches(bt_ctx *c, int32_t P, int32_t n_max, int32_t *matches, int32_t *n_matches, void *stream) {
+  BT_CHECK_CTX(c);
+  if (!matches || !n_matches) return fail(c, BT_EINVAL, "bt_copy_matches: NULL buffer");
+  if (P != c->cached_P || n_max != c->cached_nmax)
+    return fail(c, BT_EINVAL, "bt_copy_matches: P %d / n_max %d do not match the last bt_register_pairs (%d / %d)", P,
+                n_max, c->cached_P, c->cached_nmax);
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(matches, c->matches, (size_t)P * n_max * 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(n_matches, c->n_matches, (size_t)P * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) !=
+          cudaSuccess)
+    return fail(c, BT_ECUDA, "bt_copy_matches: %s", cudaGetErrorString(cudaGetLastError()));
+  return BT_OK;
 }
 
 static const char *kKernelNames[bt::K_COUNT] = {"k_desc_prep", "k_match_tc", "k_rescore", "k_mutual",

@@ -27,7 +27,7 @@ namespace bt {
 namespace {
 
 constexpr int kContrib = 144 + 12 + 2;          // 12 x 12 over (i, j) row-major, vector, (E_f, E_g)
-constexpr int kPcgThreads = 1024;
+constexpr int kPcgThreads = 256;
 
 struct GraphArgs {
   int N, P, n_max, rec_stride, fixed, max_iter, precond, stage_a;
@@ -154,41 +154,78 @@ __global__ void __launch_bounds__(64) k_graph_contrib(GraphArgs A) {
   }
 }
 
-__global__ void __launch_bounds__(64) k_graph_assemble(GraphArgs A) {
-  const int a = blockIdx.y, bn = blockIdx.x, t = threadIdx.x;
+// one CTA per node block (a, bn): the pairs touching the block are listed in ascending p
+// (ballot compaction over the pair table), then thread (r, c) sums their contributions in that
+// order — the same fixed order as a sequential scan, without a serial walk over all P pairs
+constexpr int kAsmThreads = 64;
+constexpr int kAsmList = 1024;                                     // list capacity per pass
+
+__global__ void __launch_bounds__(kAsmThreads) k_graph_assemble(GraphArgs A) {
+  __shared__ int lst[kAsmList];                                    // p << 2 | role
+  __shared__ int wcnt[kAsmThreads / 32];
+  const int a = blockIdx.y, bn = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int n = 6 * A.N;
-  if (t < 36) {
-    const int r = t / 6, c = t % 6;
-    double s = 0.0;
-    for (int p = 0; p < A.P; ++p) {                                // fixed pair order
-      const int i = A.pairs[2 * p], j = A.pairs[2 * p + 1];
-      if (!pair_ok(i, j, A.N)) continue;
-      const double *C = A.contrib + (size_t)p * kContrib;
-      if (a == i && bn == i) s += C[12 * r + c];
-      else if (a == j && bn == j) s += C[12 * (6 + r) + 6 + c];
-      else if (a == i && bn == j) s += C[12 * r + 6 + c];
-      else if (a == j && bn == i) s += C[12 * (6 + r) + c];
+  const bool diag = a == bn, energy = a == 0 && bn == 0;
+  double s = 0.0;                                                  // t < 36: A block entry; 36..41: b
+  for (int p0 = 0; p0 < A.P; p0 += kAsmList) {
+    const int p1 = min(A.P, p0 + kAsmList);
+    int cnt = 0;
+    for (int q0 = p0; q0 < p1; q0 += kAsmThreads) {               // list the touching pairs in order
+      const int p = q0 + t;
+      int role = -1;
+      if (p < p1) {
+        const int i = A.pairs[2 * p], j = A.pairs[2 * p + 1];
+        if (pair_ok(i, j, A.N)) {
+          if (a == i && bn == i) role = 0;
+          else if (a == j && bn == j) role = 1;
+          else if (a == i && bn == j) role = 2;
+          else if (a == j && bn == i) role = 3;
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, role >= 0);
+      if (lane == 0) wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int off = cnt;
+      for (int w = 0; w < warp; ++w) off += wcnt[w];
+      int tot = 0;
+      for (int w = 0; w < kAsmThreads / 32; ++w) tot += wcnt[w];
+      if (role >= 0) lst[off + __popc(bal & ((1u << lane) - 1u))] = (p << 2) | role;
+      cnt += tot;
+      __syncthreads();
     }
-    A.A[(size_t)(6 * a + r) * n + 6 * bn + c] = s;
-  } else if (a == bn && t < 42) {
-    const int r = t - 36;
-    double s = 0.0;
-    for (int p = 0; p < A.P; ++p) {
-      const int i = A.pairs[2 * p], j = A.pairs[2 * p + 1];
-      if (!pair_ok(i, j, A.N)) continue;
-      const double *C = A.contrib + (size_t)p * kContrib;
-      if (i == a) s += C[144 + r];
-      else if (j == a) s += C[150 + r];
+    if (t < 36) {
+      const int r = t / 6, c = t % 6;
+      const int o[4] = {12 * r + c, 12 * (6 + r) + 6 + c, 12 * r + 6 + c, 12 * (6 + r) + c};
+#pragma unroll 4
+      for (int k = 0; k < cnt; ++k) {
+        const int v = lst[k];
+        s += A.contrib[(size_t)(v >> 2) * kContrib + o[v & 3]];
+      }
+    } else if (diag && t < 42) {
+      const int r = t - 36;
+#pragma unroll 4
+      for (int k = 0; k < cnt; ++k) {
+        const int v = lst[k];
+        s += A.contrib[(size_t)(v >> 2) * kContrib + ((v & 3) == 0 ? 144 : 150) + r];
+      }
     }
-    A.b[6 * a + r] = s;
-  } else if (a == 0 && bn == 0 && t < 44) {
-    const int k = t - 42;
-    double s = 0.0;
-    for (int p = 0; p < A.P; ++p) {
-      const int i = A.pairs[2 * p], j = A.pairs[2 * p + 1];
-      if (pair_ok(i, j, A.N)) s += A.contrib[(size_t)p * kContrib + 156 + k];
+    __syncthreads();                                               // lst reused by the next pass
+  }
+  if (t < 36) A.A[(size_t)(6 * a + t / 6) * n + 6 * bn + t % 6] = s;
+  else if (diag && t < 42) A.b[6 * a + t - 36] = s;
+  if (energy && warp == 1) {                                       // energies: fixed-order warp sums
+    for (int k = 0; k < 2; ++k) {
+      double acc = 0.0;
+      for (int p0 = 0; p0 < A.P; p0 += 32) {
+        const int p = p0 + lane;
+        double v = 0.0;
+        if (p < A.P && pair_ok(A.pairs[2 * p], A.pairs[2 * p + 1], A.N)) v = A.contrib[(size_t)p * kContrib + 156 + k];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        acc += v;
+      }
+      if (lane == 0) A.energy[k] = acc;
     }
-    A.energy[k] = s;
   }
 }
 
@@ -268,17 +305,31 @@ __device__ bool block_inverse(const double *Am, int n, int i, const double *dinv
   return true;
 }
 
-__global__ void __launch_bounds__(kPcgThreads) k_graph_pcg(GraphArgs A) {
+// Graphs of up to 16 nodes (n <= 96 unknowns) keep A in registers: two threads per row, 48
+// columns each (A is symmetric, so row `row` is read as column `row` once from global memory);
+// the mat-vec then reads only p (broadcast).  Larger graphs read A from shared memory (staged,
+// up to kStageLimit) or global memory.
+constexpr int kRegN = 96, kRegHalf = kRegN / 2;
+
+__global__ void __launch_bounds__(kPcgThreads, 1) k_graph_pcg(GraphArgs A) {
   extern __shared__ double gsm[];
   const int n = 6 * A.N;
-  double *x = gsm, *r = x + n, *z = r + n, *p = z + n, *q = p + n, *dinv = q + n;
-  double *Minv = dinv + n;                                         // [N][36] block-Jacobi
+  const bool reg = n <= kRegN;
+  const int nv = reg ? kRegN : n;                                  // vector stride (p padded with 0)
+  double *x = gsm, *r = x + nv, *z = r + nv, *p = z + nv, *q = p + nv, *dinv = q + nv, *r2 = dinv + nv;
+  double *Minv = r2 + nv;                                          // [N][36] block-Jacobi
   double *As = Minv + 36 * A.N;                                    // [n][n] when staged
   const double *Am = A.stage_a ? As : A.A;
   __shared__ double red[64];
+  __shared__ double wred[2][kPcgThreads / 32][2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  if (A.stage_a)
-    for (int k = tid; k < n * n; k += blockDim.x) As[k] = A.A[k];
+  if (A.stage_a) {                                                 // n even: double2, 8 loads in flight
+    const double2 *src = reinterpret_cast<const double2 *>(A.A);
+    double2 *dst = reinterpret_cast<double2 *>(As);
+    const int n2 = n * n / 2;
+#pragma unroll 8
+    for (int k = tid; k < n2; k += kPcgThreads) dst[k] = __ldcg(src + k);
+  }
   for (int k = tid; k < n; k += blockDim.x) {
     const double dg = A.A[(size_t)k * n + k];
     const bool pin = (k / 6 == A.fixed) || dg == 0.0;
@@ -292,6 +343,17 @@ __global__ void __launch_bounds__(kPcgThreads) k_graph_pcg(GraphArgs A) {
   for (int k = tid; k < n; k += blockDim.x) {
     x[k] = 0.0;
     r[k] = dinv[k] != 0.0 ? -A.b[k] : 0.0;
+  }
+  for (int k = n + tid; k < nv; k += blockDim.x) p[k] = 0.0;
+  double areg[kRegHalf];
+  const int rrow = tid >> 1, rh = tid & 1;
+  if (reg) {
+    const bool act = rrow < n && dinv[rrow] != 0.0;
+#pragma unroll
+    for (int j = 0; j < kRegHalf; ++j) {
+      const int c = rh * kRegHalf + j;
+      areg[j] = (act && c < n) ? __ldcg(A.A + (size_t)c * n + rrow) : 0.0;
+    }
   }
   __syncthreads();
   auto apply_m = [&](int k) {                                      // z = M^-1 r
@@ -313,38 +375,91 @@ __global__ void __launch_bounds__(kPcgThreads) k_graph_pcg(GraphArgs A) {
   block_sum2(bb, rz, red);
   double rr = bb;
   const double stop = A.tol * A.tol * bb;
-  int it = 0;
-  for (; it < A.max_iter && rr > stop; ++it) {
-    for (int row = warp; row < n; row += nw) {                     // q = A p, warp per row
-      double s = 0.0;
-      if (dinv[row] != 0.0)
-        for (int c = lane; c < n; c += 32) s += Am[(size_t)row * n + c] * p[c];
+  // Three barriers per iteration: (1) q = A p with the p.q partials, (2) the residual update
+  // (double-buffered r, so a node's z = M^-1 r_new is formed from r_old and q without waiting)
+  // with the r.r / r.z partials, (3) p = z + beta p.  Warp partials go to alternating halves of
+  // `wred`, so a reduction needs one barrier.  A is symmetric: row `row` is read as column
+  // `row` (consecutive rows -> consecutive addresses); S threads share a row when 2n <= T.
+  const int T = blockDim.x, S = 2 * n <= T ? 2 : 1, h = tid % S;
+  double *rn = r2;
+  int par = 0, it = 0;
+  auto wsum = [&](double &u, double &v) {
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) q[row] = s;
+    for (int o = 16; o >= 1; o >>= 1) {
+      u += __shfl_xor_sync(0xffffffffu, u, o);
+      v += __shfl_xor_sync(0xffffffffu, v, o);
     }
+    if (lane == 0) { wred[par][warp][0] = u; wred[par][warp][1] = v; }
     __syncthreads();
+    double su = 0.0, sv = 0.0;
+    for (int w = 0; w < nw; ++w) { su += wred[par][w][0]; sv += wred[par][w][1]; }
+    u = su;
+    v = sv;
+    par ^= 1;
+  };
+  for (; it < A.max_iter && rr > stop; ++it) {
     double pq = 0.0, dummy = 0.0;
-    for (int k = tid; k < n; k += blockDim.x) pq += p[k] * q[k];
-    block_sum2(pq, dummy, red);
+    if (reg) {                                                     // (1) q = A p, A in registers
+      double s0 = 0.0, s1 = 0.0;
+      const double2 *p2 = reinterpret_cast<const double2 *>(p + rh * kRegHalf);
+#pragma unroll
+      for (int j = 0; j < kRegHalf / 2; ++j) {
+        const double2 pv = p2[j];
+        s0 = fma(areg[2 * j], pv.x, s0);
+        s1 = fma(areg[2 * j + 1], pv.y, s1);
+      }
+      double sr = s0 + s1;
+      sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+      if (rrow < n && rh == 0) {
+        q[rrow] = sr;
+        pq = p[rrow] * sr;
+      }
+    } else
+    for (int base = 0; base < n; base += T / S) {                  // (1) q = A p
+      const int row = base + tid / S;
+      double s0 = 0.0, s1 = 0.0;
+      if (row < n && dinv[row] != 0.0) {
+        const int c0 = h * (n / S), c1 = c0 + n / S;
+        int c = c0;
+        for (; c + 1 < c1; c += 2) {
+          s0 = fma(Am[(size_t)c * n + row], p[c], s0);
+          s1 = fma(Am[(size_t)(c + 1) * n + row], p[c + 1], s1);
+        }
+        if (c < c1) s0 = fma(Am[(size_t)c * n + row], p[c], s0);
+      }
+      double sr = s0 + s1;
+      if (S == 2) sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+      if (row < n && h == 0) {
+        q[row] = sr;
+        pq = fma(p[row], sr, pq);
+      }
+    }
+    wsum(pq, dummy);
     if (!(pq > 0.0)) break;
     const double alpha = rz / pq;
-    for (int k = tid; k < n; k += blockDim.x) {
-      x[k] += alpha * p[k];
-      r[k] -= alpha * q[k];
-    }
-    __syncthreads();
     double rr_l = 0.0, rzn = 0.0;
-    for (int k = tid; k < n; k += blockDim.x) {
-      z[k] = apply_m(k);
-      rr_l += r[k] * r[k];
-      rzn += r[k] * z[k];
+    for (int k = tid; k < n; k += T) {                             // (2) x, r, z
+      x[k] = fma(alpha, p[k], x[k]);
+      const double rk = fma(-alpha, q[k], r[k]);
+      double zk;
+      if (A.precond == 1) {
+        const int i = k / 6, a0 = k % 6;
+        zk = 0.0;
+        for (int c = 0; c < 6; ++c) zk = fma(Minv[36 * i + 6 * a0 + c], fma(-alpha, q[6 * i + c], r[6 * i + c]), zk);
+      } else {
+        zk = dinv[k] * rk;
+      }
+      rn[k] = rk;
+      z[k] = zk;
+      rr_l = fma(rk, rk, rr_l);
+      rzn = fma(rk, zk, rzn);
     }
-    block_sum2(rr_l, rzn, red);
+    wsum(rr_l, rzn);
     rr = rr_l;
     const double beta = rzn / rz;
     rz = rzn;
-    for (int k = tid; k < n; k += blockDim.x) p[k] = z[k] + beta * p[k];
+    for (int k = tid; k < n; k += T) p[k] = fma(beta, p[k], z[k]);  // (3)
+    double *t_ = r; r = rn; rn = t_;
     __syncthreads();
   }
   __syncthreads();
@@ -381,11 +496,13 @@ size_t graph_scratch_bytes(int max_nodes, int max_pairs) {
 
 constexpr size_t kStageLimit = 160 * 1024;     // A staged in shared memory up to this size
 
-bool graph_stage_a(int n_nodes) { return (size_t)36 * n_nodes * n_nodes * 8 <= kStageLimit; }
+bool graph_stage_a(int n_nodes) {
+  return 6 * n_nodes > kRegN && (size_t)36 * n_nodes * n_nodes * 8 <= kStageLimit;
+}
 
 size_t graph_pcg_smem(int n_nodes) {
-  const size_t n = 6 * (size_t)n_nodes;
-  return (6 * n + 36 * (size_t)n_nodes + (graph_stage_a(n_nodes) ? n * n : 0)) * sizeof(double);
+  const size_t n = 6 * (size_t)n_nodes, nv = n < (size_t)kRegN ? (size_t)kRegN : n;
+  return (7 * nv + 36 * (size_t)n_nodes + (graph_stage_a(n_nodes) ? n * n : 0)) * sizeof(double);
 }
 
 void launch_graph(int N, const bt_pose *pose, const int32_t *pairs, int P, const uint32_t *records, int n_max,
@@ -411,7 +528,7 @@ void launch_graph(int N, const bt_pose *pose, const int32_t *pairs, int P, const
     L.end(K_GRAPH, s);
   }
   L.begin(K_GRAPH, s);
-  k_graph_assemble<<<dim3(N, N), 64, 0, s>>>(a);
+  k_graph_assemble<<<dim3(N, N), kAsmThreads, 0, s>>>(a);
   L.end(K_GRAPH, s);
   const size_t smem = graph_pcg_smem(N);
   static size_t attr = 0;

@@ -427,12 +427,12 @@ __global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) 
       f32x2 T2[12];                                                  // coalesced 8-B loads, L2-resident
       {
         const f32x2 *src = A.hyp + ((size_t)p * A.nb + b) * 12 * kScoreThreads + threadIdx.x;
-  #pragma unroll
+#pragma unroll
         for (int q = 0; q < 12; ++q) T2[q] = __ldcg(src + q * kScoreThreads);
       }
       const f32x2 nd2 = pk(A.ndelta2, A.ndelta2), nc2 = pk(A.ncosa, A.ncosa);
       unsigned cnt[kHypPerThread];
-  #pragma unroll
+#pragma unroll
       for (int k = 0; k < kHypPerThread; ++k) cnt[k] = 0u;
       for (int cs = m0; cs < m1; cs += A.chunk) {
         const int len = min(A.chunk, m1 - cs);
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) 
           sq[4 * k] = q0; sq[4 * k + 1] = q1; sq[4 * k + 2] = q2; sq[4 * k + 3] = q3;
         }
         __syncthreads();
-  #pragma unroll 2
+#pragma unroll 2
         for (int m = 0; m < len; ++m) {
           const float4 q0 = sq[4 * m], q1 = sq[4 * m + 1];
           const f32x2 d = dist_term2(T2, q0, q1, nd2);
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kScoreThreads, 3) k_ransac_score(ScoreArgs A) 
           }
         }
       }
-  #pragma unroll
+#pragma unroll
       for (int k = 0; k < kHypPerThread; ++k) {
         const int h = b * kHypPerBlock + k * kScoreThreads + threadIdx.x;
         if (h < H && cnt[k]) atomicAdd(A.counts + (size_t)p * H + h, (int)cnt[k]);

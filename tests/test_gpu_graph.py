@@ -219,3 +219,41 @@ def test_relinearize_equals_registration_and_gn_iterations_descend(bt, torch, ct
     assert E[1] < 0.5 * E[0] and E[3] <= E[1] * 1.001, E
     with pytest.raises(bt.BtError, match="EINVAL"):
         ctx.relinearize(fb, sc.K, P_, pr[:5], eprm, rec[:5])
+
+
+def test_relinearize_with_cached_matches_across_calls(bt, torch, ctx):
+    """The C_ij cache across calls: pairs registered in two bt_register_pairs calls,
+    their match lists kept by the caller (bt_copy_matches), re-linearized TOGETHER at new poses
+    (bt_relinearize_matches) == one bt_register_pairs of all pairs at those poses, bitwise."""
+    sc = synth.make_scene(8, seed=33)
+    pairs = synth.all_pairs(8)
+    P = len(pairs)
+    uids = np.arange(100, 100 + P, dtype=np.uint32)
+    fb = bt.FrameBatch.from_scene(sc)
+    rw = bt.record_words(512)
+    pr = torch.from_numpy(pairs).cuda()
+    ud = torch.from_numpy(uids.view(np.int32)).cuda()
+    rprm, eprm = bt.ransac_params(2048, synth.PHILOX_SEED), bt.edge_params()
+    P0 = torch.from_numpy(sc.perturbed_poses(13, rot_deg=2.0, trans_m=0.01)).cuda()
+    P1 = torch.from_numpy(sc.perturbed_poses(14, rot_deg=1.0, trans_m=0.005)).cuda()
+    rec = torch.zeros((P, rw), dtype=torch.int32, device="cuda")
+    mt = torch.full((P, 512, 2), -3, dtype=torch.int32, device="cuda")
+    nm = torch.zeros(P, dtype=torch.int32, device="cuda")
+    for lo, hi in ((0, 11), (11, P)):                              # two calls, like two frames
+        r = torch.zeros((hi - lo, rw), dtype=torch.int32, device="cuda")
+        ctx.register_pairs(fb, sc.K, P0, pr[lo:hi].contiguous(), ud[lo:hi].contiguous(), rprm, eprm, r)
+        m_ = torch.empty((hi - lo, 512, 2), dtype=torch.int32, device="cuda")
+        n_ = torch.empty(hi - lo, dtype=torch.int32, device="cuda")
+        ctx.copy_matches(m_, n_)
+        rec[lo:hi], mt[lo:hi], nm[lo:hi] = r, m_, n_
+    with pytest.raises(bt.BtError, match="EINVAL"):                # the last call had P - 11 pairs
+        ctx.copy_matches(mt[:11], nm[:11])
+    ctx.relinearize(fb, sc.K, P1, pr, eprm, rec, matches=mt, n_matches=nm)
+    fresh = torch.zeros_like(rec)
+    ctx.register_pairs(fb, sc.K, P1, pr, ud, rprm, eprm, fresh)
+    torch.cuda.synchronize()
+    assert torch.equal(rec, fresh)
+    d = bt.decode_records(fresh, 512)
+    assert (d["status"] == 0).sum() >= P // 2
+    with pytest.raises(bt.BtError, match="EINVAL"):
+        ctx.relinearize(fb, sc.K, P1, pr, eprm, rec, matches=mt, n_matches=None)
