@@ -32,6 +32,7 @@
 //                 Per (entry, edge): fp32 projection, gather of the target validity + map entry,
 //                 fp64 residual difference then fp32 gates / Huber, 29 running sums.
 //  k_dense_reduce fixed-order fp64 sum of the per-tile partials of an edge (deterministic).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -48,9 +49,16 @@ constexpr int kPer = kTile / kDenseThreads;   // 4 pixels / entries per thread
 constexpr int kAcc = 29;                      // H 21, g 6, E, count
 constexpr int kPartStride = 32;
 
-struct MapEntry {                             // 48 bytes, per valid pixel of every frame
-  double x, y, z;                             // x = R^T (p - t), fp64
-  float nx, ny, nz, pad[3];                   // object-frame normal
+// x_s = R^T (p - t) is computed in fp64 and stored as fp32 hi + fp16 lo: lo = (x - hi) * 2^24
+// in fp16 (|x - hi| <= ulp(hi) / 2, so |lo| <= 2^24 * 2^-24 * |x| / 2: in range up to |x| of
+// 65 km; below fp16's normal range the subnormals still resolve 2^-48 m).  hi + lo * 2^-24
+// reproduces x to ~1e-12 relative — the cancelling difference of Eq. (3) keeps its fp64-level
+// accuracy (reading R26) from one 32-byte sector.
+constexpr double kLoScale = 16777216.0;       // 2^24
+struct __align__(32) MapEntry {                // 32 bytes (one sector, one 256-bit load), per valid pixel
+  float x, y, z;                              // hi parts of x_s (object frame)
+  float nx, ny, nz;                           // object-frame normal
+  __half lx, ly, lz, pad;                     // lo parts * 2^24
 };
 
 struct DenseArgs {
@@ -198,14 +206,18 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
       const double p1 = ((double)v - A.cyd) * d * A.ifyd - P.t[1];
       const double p2 = d - P.t[2];
       MapEntry me;
-      me.x = P.R[0] * p0 + P.R[3] * p1 + P.R[6] * p2;
-      me.y = P.R[1] * p0 + P.R[4] * p1 + P.R[7] * p2;
-      me.z = P.R[2] * p0 + P.R[5] * p1 + P.R[8] * p2;
+      const double X0 = P.R[0] * p0 + P.R[3] * p1 + P.R[6] * p2;
+      const double X1 = P.R[1] * p0 + P.R[4] * p1 + P.R[7] * p2;
+      const double X2 = P.R[2] * p0 + P.R[5] * p1 + P.R[8] * p2;
+      me.x = (float)X0; me.y = (float)X1; me.z = (float)X2;
+      me.lx = __double2half((X0 - (double)me.x) * kLoScale);
+      me.ly = __double2half((X1 - (double)me.y) * kLoScale);
+      me.lz = __double2half((X2 - (double)me.z) * kLoScale);
+      me.pad = __float2half(0.f);
       const double m0 = nr[3 * k], m1 = nr[3 * k + 1], m2 = nr[3 * k + 2];
       me.nx = (float)(P.R[0] * m0 + P.R[3] * m1 + P.R[6] * m2);
       me.ny = (float)(P.R[1] * m0 + P.R[4] * m1 + P.R[7] * m2);
       me.nz = (float)(P.R[2] * m0 + P.R[5] * m1 + P.R[8] * m2);
-      me.pad[0] = me.pad[1] = me.pad[2] = 0.f;
       A.pmap[off + pix0 + k] = me;
     }
     src[k] = valid && (A.stride <= 1 || (u % A.stride == 0 && v % A.stride == 0));
@@ -280,16 +292,14 @@ constexpr int kEdgeThreads = 256;                // k_dense CTA (8 warps, each o
 
 // target-pixel gather of one (entry, edge) item, issued ahead of its use
 struct Gather {
-  float4 g0;                  // x_s.x, x_s.y (fp64 as 2 x 2 words)
-  float4 g1;                  // x_s.z (fp64), n_o,j.x, n_o,j.y
-  float nz;                   // n_o,j.z
+  float g[8];                 // one 32-B map entry: x_s hi, n_o,j, x_s lo (fp16 x 3)
   unsigned vb;                // target validity byte (tested only when consumed: the load stays in flight)
   bool in;                    // projected into the frame
 };
 
 // project entry k of the staged chunk with T = T_j T_i^-1 and issue its target gathers
 __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, const float (&T)[12], float fx, float fy,
-                                             float cx, float cy, int W, int H, const uint8_t *vm, const float4 *pm,
+                                             float cx, float cy, int W, int H, const uint8_t *vm, const float *pm,
                                              Gather &G) {
   int tj = -1;
   if (k < n) {
@@ -305,12 +315,12 @@ __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, con
     }
   }
   const int tt = tj < 0 ? 0 : tj;                                  // validity and map entry together
-  const float4 *q4 = pm + 3 * (size_t)tt;
   G.in = tj >= 0;
   G.vb = __ldg(vm + tt);
-  G.g0 = __ldg(q4);
-  G.g1 = __ldg(q4 + 1);
-  G.nz = __ldg(reinterpret_cast<const float *>(q4 + 2));
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(G.g[0]), "=f"(G.g[1]), "=f"(G.g[2]), "=f"(G.g[3]), "=f"(G.g[4]), "=f"(G.g[5]), "=f"(G.g[6]),
+        "=f"(G.g[7])
+      : "l"(pm + 8 * (size_t)tt));
 }
 
 // Each warp owns whole edges of the chunk: warp w walks edges w, w + 8, ... leaving the frame,
@@ -324,7 +334,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
   float4 *sP = reinterpret_cast<float4 *>(dsm);                    // p (camera, fp32), (u | v << 16)
   float4 *sN = sP + kTile;                                         // n_i (camera), n_o,i.x
   float2 *sNo = reinterpret_cast<float2 *>(sN + kTile);            // n_o,i.y, n_o,i.z
-  double *sX = reinterpret_cast<double *>(sNo + kTile);            // p - t_i (fp64)
+  double *sX = reinterpret_cast<double *>(sNo + kTile);            // p - t_i (fp64), SoA [3][kTile]
   int *sCb = reinterpret_cast<int *>(sX + 3 * kTile);              // [F + 1] chunk base per frame
   int *sOff = sCb + A.mp.n_frames + 1;                             // [tiles + 1] of the current frame
   const int F = A.mp.n_frames;
@@ -377,9 +387,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         const float4 a = e2[0], b = e2[1];
         const int uv = __float_as_int(a.w), u = uv & 0xffff, v = uv >> 16;
         const double d = a.z;                                      // p.z = depth exactly
-        sX[3 * k] = ((double)u - A.cxd) * d * A.ifxd - t0;
-        sX[3 * k + 1] = ((double)v - A.cyd) * d * A.ifyd - t1;
-        sX[3 * k + 2] = d - t2;
+        sX[k] = ((double)u - A.cxd) * d * A.ifxd - t0;
+        sX[kTile + k] = ((double)v - A.cyd) * d * A.ifyd - t1;
+        sX[2 * kTile + k] = d - t2;
         const double m0 = b.x, m1 = b.y, m2 = b.z;                 // n_o,i = R_i^T n_i
         const float o0 = (float)(Rd[0] * m0 + Rd[3] * m1 + Rd[6] * m2);
         const float o1 = (float)(Rd[1] * m0 + Rd[4] * m1 + Rd[7] * m2);
@@ -400,7 +410,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
       for (int q = 0; q < 12; ++q) T[q] = __ldg(A.tji + 12 * e + q);
       const size_t off_j = (size_t)fj * npx;
       const uint8_t *vm = A.vmap + off_j;
-      const float4 *pm = reinterpret_cast<const float4 *>(A.pmap + off_j);
+      const float *pm = reinterpret_cast<const float *>(A.pmap + off_j);
       float acc[32];
 #pragma unroll
       for (int q = 0; q < 32; ++q) acc[q] = 0.f;
@@ -409,16 +419,19 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
       auto consume = [&](const Gather &G, int k) {
         if (!G.in || G.vb == 0u) return;
         // target map entry: x_s = R_j^T (s - t_j) (fp64), n_o,j (fp32)
-        const double xs0 = __hiloint2double(__float_as_int(G.g0.y), __float_as_int(G.g0.x));
-        const double xs1 = __hiloint2double(__float_as_int(G.g0.w), __float_as_int(G.g0.z));
-        const double xs2 = __hiloint2double(__float_as_int(G.g1.y), __float_as_int(G.g1.x));
-        const float mj0 = G.g1.z, mj1 = G.g1.w, mj2 = G.nz;
+        const __half2 l01 = __halves2half2(__ushort_as_half((unsigned short)(__float_as_uint(G.g[6]) & 0xffffu)),
+                                           __ushort_as_half((unsigned short)(__float_as_uint(G.g[6]) >> 16)));
+        const __half l2 = __ushort_as_half((unsigned short)(__float_as_uint(G.g[7]) & 0xffffu));
+        const double xs0 = fma((double)__low2float(l01), 1.0 / kLoScale, (double)G.g[0]);
+        const double xs1 = fma((double)__high2float(l01), 1.0 / kLoScale, (double)G.g[1]);
+        const double xs2 = fma((double)__half2float(l2), 1.0 / kLoScale, (double)G.g[2]);
+        const float mj0 = G.g[3], mj1 = G.g[4], mj2 = G.g[5];
         // q - p = R_i x_s - (p - t_i): the cancelling difference in fp64, then fp32 (the
         // gates and r are ~1e-7 relative from the fp64 values: inside the band rule, R22)
         const double *Rs = Rd;
-        const float dq0 = (float)(fma(Rs[0], xs0, fma(Rs[1], xs1, Rs[2] * xs2)) - sX[3 * k]);
-        const float dq1 = (float)(fma(Rs[3], xs0, fma(Rs[4], xs1, Rs[5] * xs2)) - sX[3 * k + 1]);
-        const float dq2 = (float)(fma(Rs[6], xs0, fma(Rs[7], xs1, Rs[8] * xs2)) - sX[3 * k + 2]);
+        const float dq0 = (float)(fma(Rs[0], xs0, fma(Rs[1], xs1, Rs[2] * xs2)) - sX[k]);
+        const float dq1 = (float)(fma(Rs[3], xs0, fma(Rs[4], xs1, Rs[5] * xs2)) - sX[kTile + k]);
+        const float dq2 = (float)(fma(Rs[6], xs0, fma(Rs[7], xs1, Rs[8] * xs2)) - sX[2 * kTile + k]);
         const float dist2 = fmaf(dq0, dq0, fmaf(dq1, dq1, dq2 * dq2));
         const float4 nc = sN[k];
         const float2 no = sNo[k];
