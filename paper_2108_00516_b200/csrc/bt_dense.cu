@@ -55,6 +55,7 @@ constexpr int kPartStride = 32;
 // reproduces x to ~1e-12 relative — the cancelling difference of Eq. (3) keeps its fp64-level
 // accuracy (reading R26) from one 32-byte sector.
 constexpr double kLoScale = 16777216.0;       // 2^24
+constexpr float kLoInv = 5.9604644775390625e-08f;  // 2^-24
 struct __align__(32) MapEntry {                // 32 bytes (one sector, one 256-bit load), per valid pixel
   float x, y, z;                              // hi parts of x_s (object frame)
   float nx, ny, nz;                           // object-frame normal
@@ -301,19 +302,17 @@ struct Gather {
 __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, const float (&T)[12], float fx, float fy,
                                              float cx, float cy, int W, int H, const uint8_t *vm, const float *pm,
                                              Gather &G) {
-  int tj = -1;
-  if (k < n) {
-    const float4 a = sP[k];
-    const float yx = fmaf(T[0], a.x, fmaf(T[1], a.y, fmaf(T[2], a.z, T[9])));
-    const float yy = fmaf(T[3], a.x, fmaf(T[4], a.y, fmaf(T[5], a.z, T[10])));
-    const float yz = fmaf(T[6], a.x, fmaf(T[7], a.y, fmaf(T[8], a.z, T[11])));
-    if (yz > 0.f) {
-      const float iz = __fdividef(1.0f, yz);
-      const float up = fmaf(fx * yx, iz, cx), vp = fmaf(fy * yy, iz, cy);
-      const float xu = floorf(up + 0.5f), xv = floorf(vp + 0.5f);
-      if (xu >= 0.f && xu < (float)W && xv >= 0.f && xv < (float)H) tj = (int)xv * W + (int)xu;
-    }
-  }
+  // straight-line (no branches between the gathers of consecutive entries): out-of-range
+  // entries and failed projections are predicated off through tj = -1
+  const float4 a = sP[k < n ? k : 0];
+  const float yx = fmaf(T[0], a.x, fmaf(T[1], a.y, fmaf(T[2], a.z, T[9])));
+  const float yy = fmaf(T[3], a.x, fmaf(T[4], a.y, fmaf(T[5], a.z, T[10])));
+  const float yz = fmaf(T[6], a.x, fmaf(T[7], a.y, fmaf(T[8], a.z, T[11])));
+  const float iz = __fdividef(1.0f, yz);
+  const float up = fmaf(fx * yx, iz, cx), vp = fmaf(fy * yy, iz, cy);
+  const float xu = floorf(up + 0.5f), xv = floorf(vp + 0.5f);
+  const bool ok = k < n && yz > 0.f && xu >= 0.f && xu < (float)W && xv >= 0.f && xv < (float)H;
+  const int tj = ok ? (int)xv * W + (int)xu : -1;
   const int tt = tj < 0 ? 0 : tj;                                  // validity and map entry together
   G.in = tj >= 0;
   G.vb = __ldg(vm + tt);
@@ -334,8 +333,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
   float4 *sP = reinterpret_cast<float4 *>(dsm);                    // p (camera, fp32), (u | v << 16)
   float4 *sN = sP + kTile;                                         // n_i (camera), n_o,i.x
   float2 *sNo = reinterpret_cast<float2 *>(sN + kTile);            // n_o,i.y, n_o,i.z
-  double *sX = reinterpret_cast<double *>(sNo + kTile);            // p - t_i (fp64), SoA [3][kTile]
-  int *sCb = reinterpret_cast<int *>(sX + 3 * kTile);              // [F + 1] chunk base per frame
+  float *sYh = reinterpret_cast<float *>(sNo + kTile);             // y_p = R_i^-1 (p - t_i): hi [3][kTile]
+  float *sYl = sYh + 3 * kTile;                                    //   and lo [3][kTile] (fp32 + fp32)
+  int *sCb = reinterpret_cast<int *>(sYl + 3 * kTile);            // [F + 1] chunk base per frame
   int *sOff = sCb + A.mp.n_frames + 1;                             // [tiles + 1] of the current frame
   const int F = A.mp.n_frames;
   const int W = A.mp.W, H = A.mp.H, npx = W * H;
@@ -371,12 +371,20 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
     __syncthreads();
     const int n = min(kTile, sOff[A.tiles] - cl * kTile);
     const int ne = A.ecount[f];
-    double Rd[9];                                                  // R_i (fp64)
+    float Rf[9];                                                   // R_i as given (fp32)
     {
       const bt_pose P = A.node_pose[f];
+      double Rd[9], Ri[9];                                         // R_i and its exact inverse (fp64)
 #pragma unroll
-      for (int k = 0; k < 9; ++k) Rd[k] = P.R[k];
-
+      for (int k = 0; k < 9; ++k) { Rf[k] = P.R[k]; Rd[k] = P.R[k]; }
+      {
+        const double c0 = Rd[4] * Rd[8] - Rd[5] * Rd[7], c1 = Rd[5] * Rd[6] - Rd[3] * Rd[8],
+                     c2 = Rd[3] * Rd[7] - Rd[4] * Rd[6];
+        const double idet = 1.0 / (Rd[0] * c0 + Rd[1] * c1 + Rd[2] * c2);
+        Ri[0] = c0 * idet; Ri[1] = (Rd[2] * Rd[7] - Rd[1] * Rd[8]) * idet; Ri[2] = (Rd[1] * Rd[5] - Rd[2] * Rd[4]) * idet;
+        Ri[3] = c1 * idet; Ri[4] = (Rd[0] * Rd[8] - Rd[2] * Rd[6]) * idet; Ri[5] = (Rd[2] * Rd[3] - Rd[0] * Rd[5]) * idet;
+        Ri[6] = c2 * idet; Ri[7] = (Rd[1] * Rd[6] - Rd[0] * Rd[7]) * idet; Ri[8] = (Rd[0] * Rd[4] - Rd[1] * Rd[3]) * idet;
+      }
       const double t0 = P.t[0], t1 = P.t[1], t2 = P.t[2];
       const float4 *src = A.entries + (size_t)f * A.tiles * kTile * 2;
       for (int k = threadIdx.x; k < n; k += kEdgeThreads) {
@@ -387,9 +395,16 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         const float4 a = e2[0], b = e2[1];
         const int uv = __float_as_int(a.w), u = uv & 0xffff, v = uv >> 16;
         const double d = a.z;                                      // p.z = depth exactly
-        sX[k] = ((double)u - A.cxd) * d * A.ifxd - t0;
-        sX[kTile + k] = ((double)v - A.cyd) * d * A.ifyd - t1;
-        sX[2 * kTile + k] = d - t2;
+        const double x0 = ((double)u - A.cxd) * d * A.ifxd - t0, x1 = ((double)v - A.cyd) * d * A.ifyd - t1,
+                     x2 = d - t2;                                  // p - t_i
+        const double y[3] = {Ri[0] * x0 + Ri[1] * x1 + Ri[2] * x2, Ri[3] * x0 + Ri[4] * x1 + Ri[5] * x2,
+                             Ri[6] * x0 + Ri[7] * x1 + Ri[8] * x2};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float yh = (float)y[c];
+          sYh[c * kTile + k] = yh;
+          sYl[c * kTile + k] = (float)(y[c] - (double)yh);
+        }
         const double m0 = b.x, m1 = b.y, m2 = b.z;                 // n_o,i = R_i^T n_i
         const float o0 = (float)(Rd[0] * m0 + Rd[3] * m1 + Rd[6] * m2);
         const float o1 = (float)(Rd[1] * m0 + Rd[4] * m1 + Rd[7] * m2);
@@ -416,34 +431,44 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
       for (int q = 0; q < 32; ++q) acc[q] = 0.f;
       // three prefetch slots in a fixed rotation (unrolled by 3, so no loaded register is moved
       // and every gather has two entries of work to hide behind)
-      auto consume = [&](const Gather &G, int k) {
-        if (!G.in || G.vb == 0u) return;
-        // target map entry: x_s = R_j^T (s - t_j) (fp64), n_o,j (fp32)
-        const __half2 l01 = __halves2half2(__ushort_as_half((unsigned short)(__float_as_uint(G.g[6]) & 0xffffu)),
-                                           __ushort_as_half((unsigned short)(__float_as_uint(G.g[6]) >> 16)));
-        const __half l2 = __ushort_as_half((unsigned short)(__float_as_uint(G.g[7]) & 0xffffu));
-        const double xs0 = fma((double)__low2float(l01), 1.0 / kLoScale, (double)G.g[0]);
-        const double xs1 = fma((double)__high2float(l01), 1.0 / kLoScale, (double)G.g[1]);
-        const double xs2 = fma((double)__half2float(l2), 1.0 / kLoScale, (double)G.g[2]);
-        const float mj0 = G.g[3], mj1 = G.g[4], mj2 = G.g[5];
-        // q - p = R_i x_s - (p - t_i): the cancelling difference in fp64, then fp32 (the
-        // gates and r are ~1e-7 relative from the fp64 values: inside the band rule, R22)
-        const double *Rs = Rd;
-        const float dq0 = (float)(fma(Rs[0], xs0, fma(Rs[1], xs1, Rs[2] * xs2)) - sX[k]);
-        const float dq1 = (float)(fma(Rs[3], xs0, fma(Rs[4], xs1, Rs[5] * xs2)) - sX[kTile + k]);
-        const float dq2 = (float)(fma(Rs[6], xs0, fma(Rs[7], xs1, Rs[8] * xs2)) - sX[2 * kTile + k]);
+      // branch-free: rejected items (not in the frame, invalid target, gates failed) run the
+      // same straight-line code with w = rho = 0 and zeroed map values (stale map words of
+      // invalid pixels never reach the arithmetic), so the scheduler keeps the gathers of the
+      // next entries in flight across it; accepted items compute exactly as before
+      auto consume = [&](const Gather &G, int k0) {
+        const bool hit = G.in && G.vb != 0u;
+        const int k = k0 < n ? k0 : 0;                             // tail: any staged entry (masked)
+        float g[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) g[c] = hit ? G.g[c] : 0.f;
+        // q - p = R_i x_s - (p - t_i) = R_i (x_s - y_p), y_p = R_i^-1 (p - t_i) (exact algebra
+        // for the fp32 R_i as given, reading R26).  x_s - y_p cancels ~0.1 m coordinates: with
+        // both as hi + lo pairs, hi_s - hi_y is exact (Sterbenz) when they are close and the lo
+        // parts carry the rest, so the difference is fp64-accurate in fp32 arithmetic; the
+        // rotation of the small difference is fp32 (~1e-7 relative: inside the band rule, R22)
+        const unsigned w6 = __float_as_uint(g[6]), w7 = __float_as_uint(g[7]);
+        const float ls0 = __half2float(__ushort_as_half((unsigned short)(w6 & 0xffffu)));
+        const float ls1 = __half2float(__ushort_as_half((unsigned short)(w6 >> 16)));
+        const float ls2 = __half2float(__ushort_as_half((unsigned short)(w7 & 0xffffu)));
+        const float D0 = (g[0] - sYh[k]) + fmaf(ls0, kLoInv, -sYl[k]);
+        const float D1 = (g[1] - sYh[kTile + k]) + fmaf(ls1, kLoInv, -sYl[kTile + k]);
+        const float D2 = (g[2] - sYh[2 * kTile + k]) + fmaf(ls2, kLoInv, -sYl[2 * kTile + k]);
+        const float mj0 = g[3], mj1 = g[4], mj2 = g[5];
+        const float dq0 = fmaf(Rf[0], D0, fmaf(Rf[1], D1, Rf[2] * D2));
+        const float dq1 = fmaf(Rf[3], D0, fmaf(Rf[4], D1, Rf[5] * D2));
+        const float dq2 = fmaf(Rf[6], D0, fmaf(Rf[7], D1, Rf[8] * D2));
         const float dist2 = fmaf(dq0, dq0, fmaf(dq1, dq1, dq2 * dq2));
         const float4 nc = sN[k];
         const float2 no = sNo[k];
         const float c = fmaf(nc.w, mj0, fmaf(no.x, mj1, no.y * mj2));
-        if (!(dist2 < A.gate2f && c > A.cos_gate)) return;
+        const bool acc_ok = hit && dist2 < A.gate2f && c > A.cos_gate;
         const float n0 = nc.x, n1 = nc.y, n2 = nc.z;
         const float r = fmaf(n0, dq0, fmaf(n1, dq1, n2 * dq2));
         const float4 a = sP[k];
         const float qx = a.x + dq0, qy = a.y + dq1, qz = a.z + dq2;
         const float ar = fabsf(r);
-        const float w = ar <= A.huber ? 1.f : __fdividef(A.huber, ar);
-        const float rho = ar <= A.huber ? 0.5f * r * r : A.huber * (ar - 0.5f * A.huber);
+        const float w = !acc_ok ? 0.f : (ar <= A.huber ? 1.f : __fdividef(A.huber, ar));
+        const float rho = !acc_ok ? 0.f : (ar <= A.huber ? 0.5f * r * r : A.huber * (ar - 0.5f * A.huber));
         const float J[6] = {n0, n1, n2, qy * n2 - qz * n1, qz * n0 - qx * n2, qx * n1 - qy * n0};
         int q = 0;
 #pragma unroll
@@ -455,7 +480,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
 #pragma unroll
         for (int aa = 0; aa < 6; ++aa) acc[21 + aa] = fmaf(w * J[aa], r, acc[21 + aa]);
         acc[27] += rho;
-        acc[28] += 1.f;
+        acc[28] += acc_ok ? 1.f : 0.f;
       };
       Gather GA, GB, GC;
       issue_gather(sP, lane, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
