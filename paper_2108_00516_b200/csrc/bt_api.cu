@@ -6,6 +6,7 @@
 
 #include <cstdarg>
 #include <cstdlib>
+#include <utility>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -173,6 +174,10 @@ bt_status bt_create(bt_ctx **out, int cuda_device) {
   c->device = cuda_device;
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (const char *sp = getenv("BT_STREAM_PRIO")) {                 // dev A/B: 1 swapped, 2 equal
+    if (sp[0] == '1') std::swap(prio_lo, prio_hi);
+    else if (sp[0] == '2') prio_lo = prio_hi;
+  }
   if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
       cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join_hi, cudaEventDisableTiming) != cudaSuccess ||

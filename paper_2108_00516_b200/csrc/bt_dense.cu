@@ -39,6 +39,7 @@
 
 #include "bt_internal.cuh"
 
+
 namespace bt {
 namespace {
 
@@ -81,6 +82,8 @@ struct DenseArgs {
   int32_t *nch;               // [F] chunks of kTile compacted entries (0 if the frame has no outgoing edge)
   MapEntry *pmap;             // [F][H*W]
   uint8_t *vmap;              // [F][H*W]
+  int32_t *tlist;             // [F * tiles] masked tiles (f * tiles + t), k_dense_mask -> k_dense_prep
+  int32_t *tcount;            // [1] list length (zeroed by k_edge_setup)
   float *partials;            // [E][tiles][32] (per chunk of the edge's source frame; chunks <= tiles)
 };
 
@@ -97,6 +100,7 @@ __device__ __forceinline__ void edge_frames(const int32_t *edges, const int32_t 
 // of outgoing edges (deterministic ballot compaction); blocks F.. compute T_j T_i^-1 per edge
 __global__ void __launch_bounds__(256) k_edge_setup(DenseArgs A) {
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *A.tcount = 0;          // k_dense_mask's work list
   if ((int)blockIdx.x >= A.mp.n_frames) {
     const int e = (blockIdx.x - A.mp.n_frames) * blockDim.x + threadIdx.x;
     if (e >= A.E) return;
@@ -141,10 +145,32 @@ __global__ void __launch_bounds__(256) k_edge_setup(DenseArgs A) {
   if (threadIdx.x == 0) A.ecount[f] = base;
 }
 
-__global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
-  pdl_wait();
-  __shared__ int wsum[kDenseThreads / 32];
-  const int f = blockIdx.y, t = blockIdx.x;
+// map entry of one valid pixel: x = R^T (p - t) in fp64 from the exact inputs (stored hi + lo,
+// reading R26), n_o = R^T n
+__device__ __forceinline__ void write_map_entry(const DenseArgs &A, const bt_pose &P, MapEntry *dst, int u, int v,
+                                                float dep, float n0, float n1, float n2) {
+  const double d = dep;
+  const double p0 = ((double)u - A.cxd) * d * A.ifxd - P.t[0];
+  const double p1 = ((double)v - A.cyd) * d * A.ifyd - P.t[1];
+  const double p2 = d - P.t[2];
+  MapEntry me;
+  const double X0 = P.R[0] * p0 + P.R[3] * p1 + P.R[6] * p2;
+  const double X1 = P.R[1] * p0 + P.R[4] * p1 + P.R[7] * p2;
+  const double X2 = P.R[2] * p0 + P.R[5] * p1 + P.R[8] * p2;
+  me.x = (float)X0; me.y = (float)X1; me.z = (float)X2;
+  me.lx = __double2half((X0 - (double)me.x) * kLoScale);
+  me.ly = __double2half((X1 - (double)me.y) * kLoScale);
+  me.lz = __double2half((X2 - (double)me.z) * kLoScale);
+  me.pad = __float2half(0.f);
+  const double m0 = n0, m1 = n1, m2 = n2;
+  me.nx = (float)(P.R[0] * m0 + P.R[3] * m1 + P.R[6] * m2);
+  me.ny = (float)(P.R[1] * m0 + P.R[4] * m1 + P.R[7] * m2);
+  me.nz = (float)(P.R[2] * m0 + P.R[5] * m1 + P.R[8] * m2);
+  *dst = me;
+}
+
+// one masked 32x32 tile, 4 pixels per thread (CTA-uniform call)
+__device__ __forceinline__ void prep_tile(const DenseArgs &A, const int f, const int t, int *wsum) {
   const int W = A.mp.W, H = A.mp.H, npx = W * H;
   const int ty = t / A.tx, tx = t - ty * A.tx;
   const int row = threadIdx.x >> 3, col0 = (threadIdx.x & 7) * 4;
@@ -200,27 +226,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
   for (int k = 0; k < kPer; ++k) {
     const int u = u0 + k;
     const bool valid = vv[k];
-    if (valid) {
-      // x = R^T (p - t) in fp64 from the exact inputs; n_o = R^T n
-      const double d = dep[k];
-      const double p0 = ((double)u - A.cxd) * d * A.ifxd - P.t[0];
-      const double p1 = ((double)v - A.cyd) * d * A.ifyd - P.t[1];
-      const double p2 = d - P.t[2];
-      MapEntry me;
-      const double X0 = P.R[0] * p0 + P.R[3] * p1 + P.R[6] * p2;
-      const double X1 = P.R[1] * p0 + P.R[4] * p1 + P.R[7] * p2;
-      const double X2 = P.R[2] * p0 + P.R[5] * p1 + P.R[8] * p2;
-      me.x = (float)X0; me.y = (float)X1; me.z = (float)X2;
-      me.lx = __double2half((X0 - (double)me.x) * kLoScale);
-      me.ly = __double2half((X1 - (double)me.y) * kLoScale);
-      me.lz = __double2half((X2 - (double)me.z) * kLoScale);
-      me.pad = __float2half(0.f);
-      const double m0 = nr[3 * k], m1 = nr[3 * k + 1], m2 = nr[3 * k + 2];
-      me.nx = (float)(P.R[0] * m0 + P.R[3] * m1 + P.R[6] * m2);
-      me.ny = (float)(P.R[1] * m0 + P.R[4] * m1 + P.R[7] * m2);
-      me.nz = (float)(P.R[2] * m0 + P.R[5] * m1 + P.R[8] * m2);
-      A.pmap[off + pix0 + k] = me;
-    }
+    if (valid) write_map_entry(A, P, A.pmap + off + pix0 + k, u, v, dep[k], nr[3 * k], nr[3 * k + 1], nr[3 * k + 2]);
     src[k] = valid && (A.stride <= 1 || (u % A.stride == 0 && v % A.stride == 0));
     n_mine += src[k];
   }
@@ -253,6 +259,71 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
     ++pos;
   }
   if (threadIdx.x == 0) A.counts[(size_t)f * A.tiles + t] = total;
+}
+
+#ifndef BT_PREP_LIST
+#define BT_PREP_LIST 1
+#endif
+// one CTA per (tile, frame) (no mask pre-pass)
+__global__ void __launch_bounds__(kDenseThreads) k_dense_prep_grid(DenseArgs A) {
+  pdl_wait();
+  __shared__ int wsum[kDenseThreads / 32];
+  prep_tile(A, blockIdx.y, blockIdx.x, wsum);
+}
+
+// persistent: the CTAs drain the list of masked tiles written by k_dense_mask
+__global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
+  pdl_wait();
+  __shared__ int wsum[kDenseThreads / 32];
+  const int n_work = *A.tcount;
+  for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+    __syncthreads();                                                 // wsum of the previous tile read
+    const int f = A.tlist[w] / A.tiles, t = A.tlist[w] - f * A.tiles;
+    prep_tile(A, f, t, wsum);
+  }
+}
+
+
+// Masked-tile classification, warp per 32x32 tile (8 tiles per CTA): lane r reads row r of the
+// tile's mask as two 16-B vectors, so a whole tile is 2 loads per lane (the mask pass is ~85 %
+// of the frame and was latency-bound at one 4-B load per thread).  A tile without a masked
+// pixel is finished here (validity bytes 0, no source entries); the others are appended to a
+// work list (slot order is irrelevant: each tile writes only its own outputs) that the
+// persistent k_dense_prep drains with 256 threads per tile.
+__global__ void __launch_bounds__(kDenseThreads) k_dense_mask(DenseArgs A) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int f = blockIdx.y, t = blockIdx.x * (kDenseThreads / 32) + warp;
+  if (t >= A.tiles) return;                                        // warp-uniform
+  const int W = A.mp.W, H = A.mp.H;
+  const int ty = t / A.tx, tx = t - ty * A.tx;
+  const int v = ty * kTS + lane, u0 = tx * kTS;
+  const size_t row = (size_t)f * W * H + (size_t)v * W + u0;
+  const bool full = (W & 15) == 0 && u0 + kTS <= W;                // 16-B aligned full-width tile row
+  bool any = false;
+  if (v < H) {
+    if (full) {
+      const uint4 *m = reinterpret_cast<const uint4 *>(A.mp.mask + row);
+      const uint4 a = __ldg(m), b = __ldg(m + 1);
+      any = (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) != 0u;
+    } else {
+      for (int u = u0; u < min(W, u0 + kTS); ++u) any |= A.mp.mask[row + (u - u0)] != 0;
+    }
+  }
+  if (__ballot_sync(0xffffffffu, any) == 0u) {
+    if (v < H) {
+      if (full) {
+        uint4 *o = reinterpret_cast<uint4 *>(A.vmap + row);
+        o[0] = make_uint4(0u, 0u, 0u, 0u);
+        o[1] = make_uint4(0u, 0u, 0u, 0u);
+      } else {
+        for (int u = u0; u < min(W, u0 + kTS); ++u) A.vmap[row + (u - u0)] = 0;
+      }
+    }
+    if (lane == 0) A.counts[(size_t)f * A.tiles + t] = 0;
+  } else if (lane == 0) {
+    A.tlist[atomicAdd(A.tcount, 1)] = f * A.tiles + t;
+  }
 }
 
 // per frame: exclusive scan of the tile counts -> offs, and the number of kTile-entry chunks
@@ -564,7 +635,7 @@ size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H) {
   const size_t tiles = dense_tiles(W, H), F = max_frames, npx = (size_t)W * H;
   return align256(F * tiles * kTile * 32) + align256(F * tiles * 4) + align256(F * (tiles + 1) * 4) + align256(F * 4) + align256((size_t)max_edges * tiles * kPartStride * 4) +
          align256((size_t)max_edges * 48) + align256(F * max_edges * 4) + align256(F * 4) +
-         align256(F * npx * sizeof(MapEntry)) + align256(F * npx);
+         align256(F * npx * sizeof(MapEntry)) + align256(F * npx) + align256(F * tiles * 4) + align256(4);
 }
 
 void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
@@ -599,13 +670,32 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   a.elist = (int32_t *)p;    p += align256(F * E * 4);
   a.ecount = (int32_t *)p;   p += align256(F * 4);
   a.pmap = (MapEntry *)p;    p += align256(F * npx * sizeof(MapEntry));
-  a.vmap = (uint8_t *)p;
+  a.vmap = (uint8_t *)p;     p += align256(F * npx);
+  a.tlist = (int32_t *)p;    p += align256(F * tiles * 4);
+  a.tcount = (int32_t *)p;
   L.begin(K_DENSE_PREP, s);
   launch_pdl(k_edge_setup, mp.n_frames + (E + 255) / 256, 256, 0, s, a);
   L.end(K_DENSE_PREP, s);
   L.begin(K_DENSE_PREP, s);
-  launch_pdl(k_dense_prep, dim3(a.tiles, mp.n_frames), kDenseThreads, 0, s, a);
+#if !BT_PREP_LIST
+  launch_pdl(k_dense_prep_grid, dim3(a.tiles, mp.n_frames), kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);
+#else
+  launch_pdl(k_dense_mask, dim3((a.tiles + kDenseThreads / 32 - 1) / (kDenseThreads / 32), mp.n_frames),
+             kDenseThreads, 0, s, a);
+  L.end(K_DENSE_PREP, s);
+  L.begin(K_DENSE_PREP, s);
+  static int prep_grid = 0;
+  if (prep_grid == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_prep, kDenseThreads, 0);
+    prep_grid = sms * std::max(per_sm, 1);
+  }
+  launch_pdl(k_dense_prep, std::min(prep_grid, a.tiles * mp.n_frames), kDenseThreads, 0, s, a);
+  L.end(K_DENSE_PREP, s);
+#endif
   L.begin(K_DENSE_PREP, s);
   launch_pdl(k_dense_scan, mp.n_frames, kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);
