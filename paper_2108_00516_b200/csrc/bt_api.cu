@@ -36,6 +36,7 @@ struct bt_ctx {
   void *match = nullptr;                      // matching scratch (bt::MatchScratch)
   bt::MatchScratch ms{};
   CUtensorMap tmap_desc;                      // TMA view of ms.desc16: [frames * n_pad][128] fp16
+  CUtensorMap tmap_feat;                      // TMA view of rs.feat: [pairs * m_pad][64] fp16
   int force_fallback = 0;                     // BT_FORCE_FALLBACK: exact rescoring of every row
   int32_t *matches = nullptr, *n_matches = nullptr;
   void *rscratch = nullptr;                   // RANSAC hypotheses / counts (bt::RansacScratch)
@@ -230,10 +231,10 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
   const int mframes = max_frames > 0 ? max_frames : 1;
   bool ok = cudaMalloc(&c->match, bt::match_scratch_bytes(mframes, max_pairs, n_max)) == cudaSuccess &&
             cudaMalloc(&c->matches, PN * 8) == cudaSuccess && cudaMalloc(&c->n_matches, (size_t)max_pairs * 4) == cudaSuccess &&
-            cudaMalloc(&c->rscratch, bt::ransac_scratch_bytes(max_pairs, max_hyp)) == cudaSuccess;
+            cudaMalloc(&c->rscratch, bt::ransac_scratch_bytes(max_pairs, max_hyp, n_max)) == cudaSuccess;
   if (ok) {
     c->ms = bt::carve_match_scratch(c->match, mframes, max_pairs, n_max);
-    c->rs = bt::carve_ransac_scratch(c->rscratch, max_pairs, max_hyp);
+    c->rs = bt::carve_ransac_scratch(c->rscratch, max_pairs, max_hyp, n_max);
     // TMA tensor map over the fp16 unit descriptors: 2-D [rows][128], 64 x 128 boxes, 128B swizzle
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
@@ -250,6 +251,16 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
     ok = encode && encode(&c->tmap_desc, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, c->ms.desc16, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    // TMA view of the scoring features: 2-D [pairs * m_pad][64] fp16, 64 x 128 boxes, 128B swizzle
+    if (ok) {
+      cuuint64_t fd[2] = {64, (cuuint64_t)max_pairs * c->rs.m_pad};
+      cuuint64_t fs[1] = {128};
+      cuuint32_t fbox[2] = {64, 128};
+      ok = encode(&c->tmap_feat, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, c->rs.feat, fd, fs, fbox, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      c->rs.fmap = &c->tmap_feat;
+    }
   }
   if (ok && dense_bytes > 0) ok = cudaMalloc(&c->dense, dense_bytes) == cudaSuccess;
   if (ok) ok = cudaMalloc(&c->graph, bt::graph_scratch_bytes(mframes, max_pairs)) == cudaSuccess;

@@ -5,6 +5,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <utility>
 #include <stdint.h>
 
@@ -85,7 +87,11 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  static const bool dbg = getenv("BT_LAUNCH_DEBUG") != nullptr;   // dev aid: report the failing launch
+  if (dbg && e != cudaSuccess)
+    fprintf(stderr, "bt launch failed: grid %u x %u, block %u, smem %zu: %s\n", grid.x, grid.y, block.x, smem,
+            cudaGetErrorString(e));
 }
 
 // ---- launchers (stream-ordered, no sync) -------------------------------------------
@@ -102,9 +108,18 @@ struct RansacScratch {
   void *hyp;
   int32_t *counts;
   int32_t *work;               // the scoring kernel's slice counter
+  void *feat;                  // [P][m_pad][64] fp16 correspondence features (tensor-core scoring)
+  void *pfeat;                 // [P] per-pair centroids / scales / feature maxima
+  void *fix;                   // [P * H] (p, h) rows recounted whole (undecided-list overflow)
+  void *elist;                 // [P * H] (p, h, m) undecided tests, evaluated by k_score_fix
+  int ecap;
+  int32_t *fix_count;          // [2]: undecided tests, overflowed rows
+  int m_pad;
+  const CUtensorMap *fmap;     // TMA view of feat: [P * m_pad][64] fp16, 64 x 128 boxes, 128B swizzle
 };
-size_t ransac_scratch_bytes(int max_pairs, int max_hyp);
-RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp);
+size_t ransac_scratch_bytes(int max_pairs, int max_hyp, int n_max);
+RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp, int n_max);
+int score_m_pad(int n_max);
 void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, int P,
                    const int32_t *matches, const int32_t *n_matches, const bt_ransac_params &prm,
                    const RansacScratch &rs, uint32_t *records, int rec_stride,

@@ -20,9 +20,13 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <algorithm>
 #include <climits>
+#include <cmath>
+#include <cstdlib>
 
 #include "bt_internal.cuh"
+#include "bt_tc.cuh"
 
 namespace bt {
 namespace {
@@ -918,22 +922,562 @@ __global__ void __launch_bounds__(kFinThreads) k_feature_edges(FeatArgs A) {
                  A.huber, reinterpret_cast<float *>(inl + ((n_max + 3) & ~3)), fpart, rec + rec_feat(n_max));
 }
 
+__device__ __forceinline__ f32x2 add2v(f32x2 a, f32x2 b) {               // a + b
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 sub2s(float a, f32x2 b) {               // {a, a} - b
+  f32x2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk(a, a)), "l"(b));
+  return d;
+}
+
+// ---------------------------------------------------------------- scoring on the tensor cores
+// The inlier test of every (hypothesis h, correspondence m) as two small contractions
+// (reading R27 of DESIGN.md).  With the pair's centroids a_bar, b_bar (fp32), a' = a - a_bar,
+// b' = b - b_bar and t' = t + R a_bar - b_bar:
+//   |R a + t - b|^2 = |R a' + t' - b'|^2
+//                   = |t'|^2 + [ 2 R^T t' | -2 vec R | -2 t' | 1 ] . [ a' | vec(b' a'^T) | b' | |a'|^2 + |b'|^2 ]
+//                     (|R a'|^2 = |a'|^2 up to the fp32 rounding of R, bounded below)
+//   (R n_a) . n_b   = vec R . vec(n_b n_a^T)
+// i.e. D1 = X1(h) . Y1(m) (K = 16) and D2 = X2(h) . Y2(m) (K = 9, padded to 16).  Each fp32
+// feature x (scaled by a power of two into fp16 range) is split x = hi + lo (fp16 each,
+// |x - hi - lo| <= 2^-22 |x|) and the products run as kind::f16 tcgen05.mma with fp32
+// accumulation: D = X_hi.Y_hi + X_hi.Y_lo + X_lo.Y_hi (K = 48 per test type).
+// Exactness: per row h the kernel bounds |D - exact| (split + dropped lo.lo + accumulation,
+// from sum_k |X_hk| max_m |Y_mk|) plus the error of the fp32 FMA formula the finish kernel
+// uses (dist_term / normal_term), and counts twice: "certain" inliers (both gates pass with
+// margin) and "possible" ones (neither gate fails with margin).  Equal counts are the count
+// of the fp32 formula exactly; a row where they differ (a test within ~1e-6 of a gate, ~1e-4
+// of the tests) is listed and recounted with the fp32 formula itself (k_score_fix).  So the
+// counts are bit-identical to the FMA kernel's.
+constexpr int kTcRows = 128;                 // hypotheses per item (UMMA M)
+constexpr int kTcCols = 128;                 // correspondences per chunk (UMMA N)
+constexpr int kTcFeat = 64;                  // fp16 per feature row: X1/Y1 hi, lo | X2/Y2 hi, lo
+constexpr int kTcEpiWarps = 16;              // 4 warpgroups x 32 columns of a chunk
+constexpr int kTcThreads = (kTcEpiWarps + 1) * 32;
+constexpr int kTcBBuf = 3;
+constexpr size_t kTcSmem = 1024 + 2 * kTcRows * 128 + kTcBBuf * kTcCols * 128;
+constexpr float kTcSentinel = 65504.f;       // padded correspondence: D1 = 65504 * s_x > any threshold
+
+struct PairFeat {                            // per pair, written by k_corr_feat
+  float abar[3], bbar[3];
+  float sy1;                                 // power-of-two scale of Y1 (Y2: 2^14)
+  float ab;                                  // 2 max |a| + max |b| (reference-formula error)
+  float korth;                               // 2e-6 max |a'|^2 (|R a'|^2 vs |a'|^2, fp32 R)
+  float apmax2;
+  float ymax1[16], ymax2[16];                // max_m |Y_mk| (unscaled, rounded up)
+  int M, pad[3];
+};
+struct ScoreConst {                          // per launch (host-computed)
+  float delta2, cosa;                        // the fp32 gate values of dist_term / normal_term
+  float c_rel;                               // |D - exact| <= c_rel * sum |X||Y|
+  float e_a, e_b;                            // eref1 = E (e_a + 3 E) + e_b,  E = 2^-21 (ab + |t|_1)
+  float k2;                                  // constant part of eps2
+};
+
+struct ScoreTcArgs {
+  KpView kp;
+  const int32_t *pairs;
+  const int32_t *matches;
+  const int32_t *n_matches;
+  int P, n_hyp, nb, nht, m_pad;
+  float ndelta2, ncosa;
+  ScoreConst sc;
+  const f32x2 *hyp;
+  int32_t *counts;
+  PairFeat *pf;
+  __half *feat;                              // [P][m_pad][64]
+  int4 *elist;                               // undecided tests (p, h, m): evaluated by k_score_fix
+  int32_t *ecount;                           // [2]: undecided tests, overflowed rows
+  int ecap;
+  int2 *fix;                                 // rows whose tests overflowed elist: recounted whole
+};
+
+__device__ __forceinline__ void split_half(double x, __half &hi, __half &lo) {
+  hi = __float2half_rn((float)x);
+  lo = __float2half_rn((float)(x - (double)__half2float(hi)));
+}
+__device__ __forceinline__ float round_up_pos(double x) { return __double2float_ru(x); }
+
+// Y1 of a correspondence: [2 a', -2 vec(b' a'^T), -2 b', |a'|^2 + |b'|^2] (X1 = [R^T t', vec R, t', 1])
+__device__ __forceinline__ void corr_y1(const double *ap, const double *bp, double *y1) {
+  for (int k = 0; k < 3; ++k) { y1[k] = 2.0 * ap[k]; y1[12 + k] = -2.0 * bp[k]; }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) y1[3 + 3 * i + j] = -2.0 * bp[i] * ap[j];
+  y1[15] = ap[0] * ap[0] + ap[1] * ap[1] + ap[2] * ap[2] + bp[0] * bp[0] + bp[1] * bp[1] + bp[2] * bp[2];
+}
+
+// one CTA per pair: centroids, feature maxima, the fp16 hi/lo feature rows (padded rows:
+// Y1 = (0, ..., 0, 65504) so that D1 exceeds every threshold, Y2 = 0)
+__global__ void __launch_bounds__(256) k_corr_feat(ScoreTcArgs A) {
+  pdl_wait();
+  __shared__ double red[8][40];
+  __shared__ double bc[8];
+  __shared__ double mxs[26];
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (p == 0 && tid < 2) A.ecount[tid] = 0;
+  const int M = A.n_matches[p];
+  PairFeat *pf = A.pf + p;
+  if (tid == 0) pf->M = M;
+  if (M < 3) return;
+  const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+  const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
+  const float *pa = A.kp.pts + (size_t)fa * A.kp.n_max * 3, *pb = A.kp.pts + (size_t)fb * A.kp.n_max * 3;
+  const float *na = A.kp.nrm + (size_t)fa * A.kp.n_max * 3, *nb = A.kp.nrm + (size_t)fb * A.kp.n_max * 3;
+  // centroids (fp64 sums, fixed order: thread-strided then tree)
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int m = tid; m < M; m += 256) {
+    const float *x = pa + 3 * mt[2 * m], *y = pb + 3 * mt[2 * m + 1];
+    s[0] += x[0]; s[1] += x[1]; s[2] += x[2]; s[3] += y[0]; s[4] += y[1]; s[5] += y[2];
+    s[6] = fmax(s[6], sqrt((double)x[0] * x[0] + (double)x[1] * x[1] + (double)x[2] * x[2]));
+    s[7] = fmax(s[7], sqrt((double)y[0] * y[0] + (double)y[1] * y[1] + (double)y[2] * y[2]));
+  }
+  for (int k = 0; k < 8; ++k)
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double v = __shfl_xor_sync(0xffffffffu, s[k], o);
+      s[k] = k < 6 ? s[k] + v : fmax(s[k], v);
+    }
+  if (lane == 0) for (int k = 0; k < 8; ++k) red[warp][k] = s[k];
+  __syncthreads();
+  if (tid < 8) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v = tid < 6 ? v + red[w][tid] : fmax(v, red[w][tid]);
+    bc[tid] = v;
+  }
+  __syncthreads();
+  float cen[6];
+  for (int k = 0; k < 6; ++k) cen[k] = (float)(bc[k] / M);
+  // feature maxima
+  double mx[26];
+  for (int k = 0; k < 26; ++k) mx[k] = 0.0;
+  for (int m = tid; m < M; m += 256) {
+    const float *x = pa + 3 * mt[2 * m], *y = pb + 3 * mt[2 * m + 1];
+    const float *u = na + 3 * mt[2 * m], *v = nb + 3 * mt[2 * m + 1];
+    double ap[3], bp[3];
+    for (int k = 0; k < 3; ++k) { ap[k] = (double)x[k] - cen[k]; bp[k] = (double)y[k] - cen[3 + k]; }
+    double y1[16];
+    corr_y1(ap, bp, y1);
+    for (int k = 0; k < 16; ++k) mx[k] = fmax(mx[k], fabs(y1[k]));
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) mx[16 + 3 * i + j] = fmax(mx[16 + 3 * i + j], fabs((double)v[i] * u[j]));
+    mx[25] = fmax(mx[25], ap[0] * ap[0] + ap[1] * ap[1] + ap[2] * ap[2]);
+  }
+  __syncthreads();                                          // red / bc of the centroid pass consumed
+  for (int k = 0; k < 26; ++k) {
+    for (int o = 16; o >= 1; o >>= 1) mx[k] = fmax(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
+    if (lane == 0) red[warp][k] = mx[k];
+  }
+  __syncthreads();
+  if (tid < 26) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v = fmax(v, red[w][tid]);
+    mxs[tid] = v;
+    if (tid < 16) pf->ymax1[tid] = round_up_pos(v);
+    else if (tid < 25) pf->ymax2[tid - 16] = round_up_pos(v);
+    else pf->apmax2 = round_up_pos(v);
+  }
+  if (tid >= 9 && tid < 16) pf->ymax2[tid] = 0.f;
+  __syncthreads();
+  // Y1 scale: max |Y1| * sy1 < 2^14, and >= delta^2 so that the padded rows' 65504 * s_x
+  // exceeds every distance threshold (65504 / sy1 > 4 max(|Y1|max, delta^2))
+  double ymx = -(double)A.ndelta2;
+  for (int k = 0; k < 16; ++k) ymx = fmax(ymx, mxs[k]);
+  int e;
+  frexp(ymx, &e);                                           // ymx < 2^e
+  const double sy1 = ldexp(1.0, 14 - e), sy2 = 16384.0;
+  if (tid == 0) {
+    for (int k = 0; k < 6; ++k) (k < 3 ? pf->abar[k] : pf->bbar[k - 3]) = cen[k];
+    pf->sy1 = (float)sy1;
+    pf->ab = round_up_pos((2.0 * bc[6] + bc[7]) * (1.0 + 1e-6));
+    pf->korth = round_up_pos(2e-6 * mxs[25]);
+  }
+  const int mp = (M + kTcCols - 1) / kTcCols * kTcCols;
+  __half *F = A.feat + (size_t)p * A.m_pad * kTcFeat;
+  for (int m = tid; m < mp; m += 256) {
+    __half *row = F + (size_t)m * kTcFeat;
+    __half h1[16], l1[16], h2[16], l2[16];
+    if (m < M) {
+      const float *x = pa + 3 * mt[2 * m], *y = pb + 3 * mt[2 * m + 1];
+      const float *u = na + 3 * mt[2 * m], *v = nb + 3 * mt[2 * m + 1];
+      double ap[3], bp[3];
+      for (int k = 0; k < 3; ++k) { ap[k] = (double)x[k] - cen[k]; bp[k] = (double)y[k] - cen[3 + k]; }
+      double y1[16];
+      corr_y1(ap, bp, y1);
+      for (int k = 0; k < 16; ++k) split_half(y1[k] * sy1, h1[k], l1[k]);
+      for (int k = 0; k < 16; ++k) {
+        const double y2 = k < 9 ? (double)v[k / 3] * u[k % 3] * sy2 : 0.0;
+        split_half(y2, h2[k], l2[k]);
+      }
+    } else {
+      for (int k = 0; k < 16; ++k) {
+        h1[k] = __float2half_rn(k == 15 ? kTcSentinel : 0.f); l1[k] = h2[k] = l2[k] = __float2half_rn(0.f);
+      }
+    }
+    uint4 *dst = reinterpret_cast<uint4 *>(row);
+    const uint4 *s1 = reinterpret_cast<const uint4 *>(h1), *s2 = reinterpret_cast<const uint4 *>(l1);
+    const uint4 *s3 = reinterpret_cast<const uint4 *>(h2), *s4 = reinterpret_cast<const uint4 *>(l2);
+    dst[0] = s1[0]; dst[1] = s1[1]; dst[2] = s2[0]; dst[3] = s2[1];
+    dst[4] = s3[0]; dst[5] = s3[1]; dst[6] = s4[0]; dst[7] = s4[1];
+  }
+}
+
+// T of hypothesis h of pair p from the f32x2 hypothesis buffer (k_ransac_hyp's layout)
+__device__ __forceinline__ void load_T(const ScoreTcArgs &A, int p, int h, float *T) {
+  const int b = h / kHypPerBlock, r = h - b * kHypPerBlock;
+  const int t = r % kScoreThreads, k = r / kScoreThreads;
+  const float *src = reinterpret_cast<const float *>(A.hyp + ((size_t)p * A.nb + b) * 12 * kScoreThreads + t) + k;
+#pragma unroll
+  for (int q = 0; q < 12; ++q) T[q] = __ldcg(src + 2 * q * kScoreThreads);
+}
+
+struct RowConst {
+  float lo1B, lo2, hi2;                      // lo1B = lo1 * kSatB (certain-count thresholds pre-scaled)
+  float lo1, hi1, hi2B, lo2r;
+  bool valid;
+};
+constexpr float kSatB = 18446744073709551616.f;   // 2^64: sat((lo - x) 2^64) is 1 iff x < lo (scaled units)
+// Per-row thresholds (scaled units) and one quarter of the row's fp16 features, written into
+// the 128B-swizzled A tile (16-B chunk c of row r lands at c ^ (r & 7)): part 0 X1 hi, 1 X1 lo,
+// 2 X2 hi, 3 X2 lo.  fp32 throughout: the features' own rounding (2^-22 relative) is in c_rel,
+// the thresholds carry a 2^-21 (delta^2 + |t'|^2) slack for their fp32 evaluation.
+__device__ __forceinline__ RowConst row_setup(const ScoreTcArgs &A, const PairFeat &pf, const float *T, uint8_t *arow,
+                                              int r, int part, bool want_thr) {
+  RowConst rc;
+  rc.valid = T[11] < 1e30f;
+  float R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = rc.valid ? T[k] : 0.f;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = rc.valid ? T[9 + k] : 0.f;
+  float x1[16];                                            // [R^T t', vec R, t', 1]
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    x1[12 + i] = t[i] + fmaf(R[3 * i], pf.abar[0], fmaf(R[3 * i + 1], pf.abar[1], R[3 * i + 2] * pf.abar[2])) - pf.bbar[i];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) x1[j] = fmaf(R[j], x1[12], fmaf(R[3 + j], x1[13], R[6 + j] * x1[14]));
+#pragma unroll
+  for (int k = 0; k < 9; ++k) x1[3 + k] = R[k];
+  x1[15] = 1.f;
+  const float tn2 = fmaf(x1[12], x1[12], fmaf(x1[13], x1[13], x1[14] * x1[14]));
+  // max |X1| <= max(1.0001, 1.0001 |t'|) < 2^e  ->  sx = 2^(14 - e)
+  const float xm = fmaxf(1.0001f, 1.0001f * sqrtf(tn2) + 1e-6f);
+  const int e = ((__float_as_int(xm) >> 23) & 255) - 126;
+  const float sx = __int_as_float((127 + 14 - e) << 23);
+  if (want_thr) {
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s1 = fmaf(fabsf(x1[k]), pf.ymax1[k], s1);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) s2 = fmaf(fabsf(R[k]), pf.ymax2[k], s2);
+  const float E = 0x1p-21f * (pf.ab + fabsf(t[0]) + fabsf(t[1]) + fabsf(t[2]));
+  const float eref1 = fmaf(E, fmaf(3.f, E, A.sc.e_a), A.sc.e_b);
+  const float eps1 = fmaf(A.sc.c_rel, s1, pf.korth + eref1 + 0x1p-21f * (A.sc.delta2 + tn2)) * 1.0001f;
+  const float eps2 = fmaf(A.sc.c_rel, s2, A.sc.k2) * 1.0001f;
+  const float sc1 = sx * pf.sy1, sc2 = 268435456.f;         // D1, D2 scales (powers of two)
+  const float thr = A.sc.delta2 - tn2;
+  rc.lo1 = sc1 * (thr - eps1);
+  rc.hi1 = sc1 * (thr + eps1);
+  rc.lo2 = sc2 * (A.sc.cosa - eps2);
+  rc.hi2 = sc2 * (A.sc.cosa + eps2);
+  rc.lo1B = rc.lo1 * kSatB;
+  rc.hi2B = rc.hi2 * kSatB;
+  rc.lo2r = rc.lo2;
+  }
+  if (arow) {
+    __align__(16) __half h[16];
+    const bool lo = part & 1;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float x = part < 2 ? x1[k] * sx : (k < 9 ? R[k] * 16384.f : 0.f);
+      const __half hi = __float2half_rn(x);
+      h[k] = lo ? __float2half_rn(x - __half2float(hi)) : hi;
+    }
+    const uint4 *src = reinterpret_cast<const uint4 *>(h);
+    uint4 *dst = reinterpret_cast<uint4 *>(arow);
+    dst[(2 * part) ^ (r & 7)] = src[0];
+    dst[(2 * part + 1) ^ (r & 7)] = src[1];
+  }
+  return rc;
+}
+
+// Persistent, warp-specialized: items (pair p, tile of 128 hypotheses) walk blockIdx.x,
+// + gridDim.x, ...; chunks of 128 correspondences form one stream g per CTA.
+//   producer warp 16: TMA of feature chunk g into B buffer g % 3 (after the MMAs of g - 3
+//     released it), then 6 tcgen05.mma (D1: X1hi.Y1hi + X1hi.Y1lo + X1lo.Y1hi, D2 likewise)
+//     into TMEM buffer g & 1 (D1 columns 0-127, D2 128-255) once the epilogue released it.
+//   epilogue warps 0-15: warpgroup 0 builds the next item's A tile (features of its 128
+//     hypotheses) at the start of each item; every warp reads 32 columns of D1 and D2 for its
+//     32 TMEM lanes, releases the buffer, and counts certain / possible inliers per row.
+__global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constant__ CUtensorMap fmap, ScoreTcArgs A) {
+  pdl_wait();
+  extern __shared__ uint8_t tc_smem_raw[];
+  __shared__ __align__(8) uint64_t bar_a[2], bar_bfull[kTcBBuf], bar_bfree[kTcBBuf], bar_mma[2], bar_tfree[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float4 rowc[4][kTcRows];
+  __shared__ bool rowv[4][kTcRows];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = base;                                       // [2][128 rows][128 B]
+  uint8_t *sB = base + 2 * kTcRows * 128;                   // [3][128 rows][128 B]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_items = A.P * A.nht;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_a[b], kTcEpiWarps); mbar_init(&bar_mma[b], 1); mbar_init(&bar_tfree[b], kTcEpiWarps);
+    }
+    for (int b = 0; b < kTcBBuf; ++b) { mbar_init(&bar_bfull[b], 1); mbar_init(&bar_bfree[b], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcCols >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+
+  if (warp == kTcEpiWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint32_t g = 0, k = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int p = it / A.nht;
+        const int M = A.n_matches[p];
+        if (M < 3) continue;
+        const int nch = (M + kTcCols - 1) / kTcCols;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int bb = g % kTcBBuf, tb = g & 1;
+          const uint32_t use = g / kTcBBuf;
+          if (use > 0) mbar_wait(&bar_bfree[bb], (use - 1) & 1);
+          mbar_expect_tx(&bar_bfull[bb], kTcCols * 128);
+          tma_load_2d(sB + bb * kTcCols * 128, &fmap, 0, p * A.m_pad + c * kTcCols, &bar_bfull[bb]);
+          if (c == 0) mbar_wait(&bar_a[k & 1], (k >> 1) & 1);
+          if (g >= 2) mbar_wait(&bar_tfree[tb], ((g - 2) >> 1) & 1);
+          mbar_wait(&bar_bfull[bb], use & 1);
+          tc_fence_after();
+          const uint8_t *a = sA + (k & 1) * kTcRows * 128, *b = sB + bb * kTcCols * 128;
+          const uint32_t d1 = tmem + tb * 256, d2 = d1 + 128;
+          umma_f16(d1, umma_desc_sw128(a), umma_desc_sw128(b), idesc, 0u);             // X1hi . Y1hi
+          umma_f16(d1, umma_desc_sw128(a), umma_desc_sw128(b + 32), idesc, 1u);        // X1hi . Y1lo
+          umma_f16(d1, umma_desc_sw128(a + 32), umma_desc_sw128(b), idesc, 1u);        // X1lo . Y1hi
+          umma_f16(d2, umma_desc_sw128(a + 64), umma_desc_sw128(b + 64), idesc, 0u);   // X2hi . Y2hi
+          umma_f16(d2, umma_desc_sw128(a + 64), umma_desc_sw128(b + 96), idesc, 1u);   // X2hi . Y2lo
+          umma_f16(d2, umma_desc_sw128(a + 96), umma_desc_sw128(b + 64), idesc, 1u);   // X2lo . Y2hi
+          umma_commit(&bar_mma[tb]);
+          umma_commit(&bar_bfree[bb]);
+        }
+        ++k;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int wg = warp >> 2, q = warp & 3;
+    const int lrow = q * 32 + lane;                         // TMEM lane = hypothesis row
+    uint32_t g = 0, k = 0;
+    // Every warp builds its quarter of the A tile of the next item (warpgroup 0 also its row
+    // thresholds, into rowc[k & 3]) and arrives on bar_a; at an item's start every warp waits on
+    // bar_a and reads the thresholds (no warp can be a phase behind: all 16 arrive per item;
+    // rowc is 4 deep because a warp may lag the builders by up to two items).
+    int it = blockIdx.x;
+    while (it < n_items && A.n_matches[it / A.nht] < 3) it += gridDim.x;
+    float Tn[12];
+    auto build = [&](int itb, uint32_t kb) {
+      const int pb = itb / A.nht, hb = (itb - pb * A.nht) * kTcRows + lrow;
+      load_T(A, pb, hb, Tn);
+      const PairFeat pfb = A.pf[pb];
+      const RowConst r = row_setup(A, pfb, Tn, sA + (kb & 1) * kTcRows * 128 + lrow * 128, lrow, wg, wg == 0);
+      if (wg == 0) {
+        rowc[kb & 3][lrow] = make_float4(r.lo1B, r.hi1, r.lo2, r.hi2B);
+        rowv[kb & 3][lrow] = r.valid;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_a[kb & 1]);
+    };
+    if (it < n_items) build(it, 0);
+    while (it < n_items) {
+      const int p = it / A.nht, ht = it - p * A.nht;
+      const int M = A.n_matches[p];
+      const int nch = (M + kTcCols - 1) / kTcCols;
+      int itn = it + gridDim.x;
+      while (itn < n_items && A.n_matches[itn / A.nht] < 3) itn += gridDim.x;
+      if (itn < n_items) build(itn, k + 1);
+      mbar_wait(&bar_a[k & 1], (k >> 1) & 1);                     // this item's thresholds
+      RowConst rc;
+      {
+        const float4 v = rowc[k & 3][lrow];
+        rc.lo1B = v.x; rc.hi1 = v.y; rc.lo2 = v.z; rc.hi2B = v.w;
+        rc.lo1 = rc.lo1B * (1.f / kSatB); rc.hi2 = rc.hi2B * (1.f / kSatB); rc.lo2r = rc.lo2;
+        rc.valid = rowv[k & 3][lrow];
+      }
+      unsigned cert = 0;
+      bool overflow = false;
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int tb = g & 1;
+        mbar_wait(&bar_mma[tb], (g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * 256 + wg * 32);
+        if (c * kTcCols + wg * 32 >= M) {                           // all 32 columns padding: release only
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_tfree[tb]);
+          continue;
+        }
+        const f32x2 hi1 = pk(-rc.hi1, -rc.hi1);
+        // two halves of 16 columns (D1 and D2): 32 live registers instead of 64 (17 warps leave
+        // 96 registers per thread); the buffer is released after the second half's load
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t v1[16], v2[16];
+          BT_TMEM_LD16(ta + hf * 16, v1);
+          BT_TMEM_LD16(ta + 128 + hf * 16, v2);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (hf == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_tfree[tb]);
+          }
+          // certain (D1 < lo1 and D2 > hi2) on the FMA pipe: sat((lo1 - x) 2^64) * sat((y - hi2) 2^64);
+          // possible (D1 < hi1 and D2 > lo2) from sign bits
+          f32x2 cacc = pk(0.f, 0.f);
+          unsigned pc = 0;
+#pragma unroll
+          for (int col = 0; col < 16; col += 2) {
+            const float x0 = __uint_as_float(v1[col]), x1 = __uint_as_float(v1[col + 1]);
+            const float y0 = __uint_as_float(v2[col]), y1 = __uint_as_float(v2[col + 1]);
+            const f32x2 ia = pk(__saturatef(__fmaf_rn(x0, -kSatB, rc.lo1B)), __saturatef(__fmaf_rn(x1, -kSatB, rc.lo1B)));
+            const f32x2 ib = pk(__saturatef(__fmaf_rn(y0, kSatB, -rc.hi2B)), __saturatef(__fmaf_rn(y1, kSatB, -rc.hi2B)));
+            cacc = fma2v(ia, ib, cacc);
+            unsigned c0_, c1_, e0, e1;
+            split(add2v(pk(x0, x1), hi1), c0_, c1_);
+            split(sub2s(rc.lo2r, pk(y0, y1)), e0, e1);
+            pc += ((c0_ & e0) >> 31) + ((c1_ & e1) >> 31);
+          }
+          unsigned ca_, cb_;
+          split(cacc, ca_, cb_);
+          const unsigned cc = (unsigned)(__uint_as_float(ca_) + __uint_as_float(cb_));
+          cert += cc;
+          if (__any_sync(0xffffffffu, pc != cc)) {                // rare: list the undecided tests
+            if (pc != cc) {
+              const int h = ht * kTcRows + lrow;
+              for (int col = 0; col < 16; ++col) {
+                const float x = __uint_as_float(v1[col]), y = __uint_as_float(v2[col]);
+                const bool sure = x < rc.lo1 && y > rc.hi2, maybe = x < rc.hi1 && y > rc.lo2;
+                if (maybe && !sure && h < A.n_hyp && rc.valid) {
+                  const int slot = atomicAdd(A.ecount, 1);
+                  if (slot < A.ecap) A.elist[slot] = make_int4(p, h, c * kTcCols + wg * 32 + hf * 16 + col, 0);
+                  else overflow = true;
+                }
+              }
+            }
+          }
+        }
+      }
+      // this warpgroup's columns of the row (integer atomics: exact, order-free)
+      const int h = ht * kTcRows + lrow;
+      if (h < A.n_hyp && rc.valid) {
+        if (cert) atomicAdd(A.counts + (size_t)p * A.n_hyp + h, (int)cert);
+        if (overflow) A.fix[atomicAdd(A.ecount + 1, 1)] = make_int2(p, h);
+      }
+      it = itn;
+      ++k;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
+// the undecided tests, one thread each, with the fp32 formula of the finish kernel (the
+// tensor-core count holds the certain inliers; an undecided test that passes adds one)
+__global__ void __launch_bounds__(256) k_score_fix(ScoreTcArgs A) {
+  pdl_wait();
+  const int n = min(A.ecount[0], A.ecap);
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
+    const int4 e = A.elist[w];
+    const int p = e.x, h = e.y, m = e.z;
+    float T[12];
+    load_T(A, p, h, T);
+    const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+    const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
+    const int i = mt[2 * m], j = mt[2 * m + 1];
+    float4 q0, q1, q2, q3;
+    pack_corr(A.kp.pts + ((size_t)fa * A.kp.n_max + i) * 3, A.kp.nrm + ((size_t)fa * A.kp.n_max + i) * 3,
+              A.kp.pts + ((size_t)fb * A.kp.n_max + j) * 3, A.kp.nrm + ((size_t)fb * A.kp.n_max + j) * 3, q0, q1, q2, q3);
+    if (inlier(T, q0, q1, q2, q3, A.ndelta2, A.ncosa)) atomicAdd(A.counts + (size_t)p * A.n_hyp + h, 1);
+  }
+}
+
+// safety net (never taken at the configured capacity): rows whose undecided tests did not fit
+// the list are recounted whole, after k_score_fix (warp per row)
+__global__ void __launch_bounds__(256) k_score_fix_rows(ScoreTcArgs A) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int n = A.ecount[1];
+  for (int w = blockIdx.x * 8 + (threadIdx.x >> 5); w < n; w += gridDim.x * 8) {
+    const int2 ph = A.fix[w];
+    const int p = ph.x, h = ph.y;
+    float T[12];
+    load_T(A, p, h, T);
+    const int M = A.n_matches[p];
+    const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
+    const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
+    const float *pa = A.kp.pts + (size_t)fa * A.kp.n_max * 3, *pb = A.kp.pts + (size_t)fb * A.kp.n_max * 3;
+    const float *na = A.kp.nrm + (size_t)fa * A.kp.n_max * 3, *nb = A.kp.nrm + (size_t)fb * A.kp.n_max * 3;
+    int cnt = 0;
+    for (int m0 = 0; m0 < M; m0 += 32) {
+      const int m = m0 + lane;
+      bool in = false;
+      if (m < M) {
+        const int i = mt[2 * m], j = mt[2 * m + 1];
+        float4 q0, q1, q2, q3;
+        pack_corr(pa + 3 * i, na + 3 * i, pb + 3 * j, nb + 3 * j, q0, q1, q2, q3);
+        in = inlier(T, q0, q1, q2, q3, A.ndelta2, A.ncosa);
+      }
+      cnt += __popc(__ballot_sync(0xffffffffu, in));
+    }
+    if (lane == 0) A.counts[(size_t)p * A.n_hyp + h] = cnt;
+  }
+}
+
 }  // namespace
 
 static size_t hyp_slots(int max_pairs, int max_hyp) {
   return (size_t)max_pairs * ((max_hyp + kHypPerBlock - 1) / kHypPerBlock) * kHypPerBlock;
 }
 
-size_t ransac_scratch_bytes(int max_pairs, int max_hyp) {
-  return (hyp_slots(max_pairs, max_hyp) * 48 + 255) / 256 * 256 + ((size_t)max_pairs * max_hyp * 4 + 255) / 256 * 256 +
-         256;
+static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+int score_m_pad(int n_max) { return (n_max + kTcCols - 1) / kTcCols * kTcCols; }
+
+size_t ransac_scratch_bytes(int max_pairs, int max_hyp, int n_max) {
+  return al256(hyp_slots(max_pairs, max_hyp) * 48) + al256((size_t)max_pairs * max_hyp * 4) + 256 +
+         al256((size_t)max_pairs * score_m_pad(n_max) * kTcFeat * 2) + al256((size_t)max_pairs * sizeof(PairFeat)) +
+         al256((size_t)max_pairs * max_hyp * 8) + al256((size_t)max_pairs * max_hyp * 16) + 256;
 }
 
-RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp) {
+RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp, int n_max) {
   RansacScratch r;
-  r.hyp = scratch;
-  r.counts = (int32_t *)((char *)scratch + (hyp_slots(max_pairs, max_hyp) * 48 + 255) / 256 * 256);
-  r.work = (int32_t *)((char *)r.counts + ((size_t)max_pairs * max_hyp * 4 + 255) / 256 * 256);
+  char *c = (char *)scratch;
+  r.hyp = c;                      c += al256(hyp_slots(max_pairs, max_hyp) * 48);
+  r.counts = (int32_t *)c;        c += al256((size_t)max_pairs * max_hyp * 4);
+  r.work = (int32_t *)c;          c += 256;
+  r.feat = c;                     c += al256((size_t)max_pairs * score_m_pad(n_max) * kTcFeat * 2);
+  r.pfeat = c;                    c += al256((size_t)max_pairs * sizeof(PairFeat));
+  r.fix = c;                      c += al256((size_t)max_pairs * max_hyp * 8);
+  r.elist = c;                    c += al256((size_t)max_pairs * max_hyp * 16);
+  r.ecap = (int)std::min<size_t>((size_t)max_pairs * max_hyp, 0x7fffffff);
+  r.fix_count = (int32_t *)c;
+  r.m_pad = score_m_pad(n_max);
+  r.fmap = nullptr;
   return r;
 }
 
@@ -976,9 +1520,49 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   launch_pdl(k_ransac_hyp, dim3((a.nb * kHypPerBlock / kHypThreads + kHypIter - 1) / kHypIter, P), kHypThreads,
              hyp_smem, s, a);
   L.end(K_RANSAC_HYP, s);
-  L.begin(K_RANSAC_SCORE, s);
-  launch_pdl(k_ransac_score, score_slots, kScoreThreads, smem, s, a);
-  L.end(K_RANSAC_SCORE, s);
+  const char *fma_env = getenv("BT_SCORE_FMA");                  // 1: the FFMA2 kernel (A/B, equality test)
+  const bool use_fma = fma_env && fma_env[0] == '1';
+  if (use_fma || !rs.fmap) {
+    L.begin(K_RANSAC_SCORE, s);
+    launch_pdl(k_ransac_score, score_slots, kScoreThreads, smem, s, a);
+    L.end(K_RANSAC_SCORE, s);
+  } else {
+    ScoreTcArgs t;
+    t.kp = kp; t.pairs = pairs; t.matches = matches; t.n_matches = n_matches;
+    t.P = P; t.n_hyp = prm.n_hyp; t.nb = a.nb; t.nht = (prm.n_hyp + kTcRows - 1) / kTcRows; t.m_pad = rs.m_pad;
+    t.ndelta2 = a.ndelta2; t.ncosa = a.ncosa; t.hyp = a.hyp; t.counts = a.counts;
+    {
+      const double d2 = -(double)a.ndelta2, d = std::sqrt(d2);
+      t.sc.delta2 = -a.ndelta2;
+      t.sc.cosa = -a.ncosa;
+      t.sc.c_rel = (float)((4.0 * 0x1p-22 + 51.0 * 0x1p-23) * 1.01);
+      t.sc.e_a = (float)(4.0 * std::sqrt(3.0) * d * 1.0001);
+      t.sc.e_b = (float)(0x1p-21 * 5.0 * d2 * 1.0001);
+      t.sc.k2 = (float)(40.0 * 0x1p-24 + 0x1p-22 * (1.0 + std::fabs((double)a.ncosa)));
+    }
+    t.pf = (PairFeat *)rs.pfeat; t.feat = (__half *)rs.feat; t.fix = (int2 *)rs.fix; t.ecount = rs.fix_count;
+    t.elist = (int4 *)rs.elist; t.ecap = rs.ecap;
+    static int tc_grid = 0;
+    if (!tc_grid) {
+      cudaFuncSetAttribute(k_score_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+      int dev = 0, n_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+      tc_grid = n_sm;                                              // one CTA per SM (all 512 TMEM columns)
+    }
+    L.begin(K_RANSAC_SCORE, s);
+    launch_pdl(k_corr_feat, P, 256, 0, s, t);
+    L.end(K_RANSAC_SCORE, s);
+    L.begin(K_RANSAC_SCORE, s);
+    launch_pdl(k_score_tc, std::min(tc_grid, P * t.nht), kTcThreads, kTcSmem, s, *rs.fmap, t);
+    L.end(K_RANSAC_SCORE, s);
+    L.begin(K_RANSAC_SCORE, s);
+    launch_pdl(k_score_fix, 148, 256, 0, s, t);
+    L.end(K_RANSAC_SCORE, s);
+    L.begin(K_RANSAC_SCORE, s);
+    launch_pdl(k_score_fix_rows, 148, 256, 0, s, t);
+    L.end(K_RANSAC_SCORE, s);
+  }
   FinishArgs f;
   f.kp = kp; f.pairs = pairs; f.uid = uid; f.matches = matches; f.n_matches = n_matches;
   f.n_hyp = prm.n_hyp; f.min_inliers = prm.min_inliers;

@@ -1,0 +1,117 @@
+"""Tensor-core scoring (k_corr_feat / k_score_tc / k_score_fix, reading R27) against
+the FFMA2 scoring kernel (BT_SCORE_FMA=1): every per-hypothesis inlier count and every record
+word must be bit-identical — the certificate either decides a test with margin or the row is
+recounted with the fp32 formula itself.  Oracle parity of the default (tensor-core) path is in
+test_gpu_parity.py."""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+SEED = synth.PHILOX_SEED
+
+
+@pytest.fixture(scope="module")
+def bt():
+    import paper_2108_00516_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    return t
+
+
+def _run_both(bt, torch, ctx, sc, pairs, n_hyp, uids=None, match_lists=None):
+    fb = bt.FrameBatch.from_scene(sc)
+    P = len(pairs)
+    n_max = sc.desc.shape[1]
+    pr = torch.from_numpy(np.asarray(pairs, np.int32)).cuda()
+    uid = np.arange(P, dtype=np.uint32) if uids is None else np.asarray(uids, np.uint32)
+    tu = torch.from_numpy(uid.view(np.int32)).cuda()
+    if match_lists is None:
+        mt = torch.zeros((P, n_max, 2), dtype=torch.int32, device="cuda")
+        nm = torch.zeros(P, dtype=torch.int32, device="cuda")
+        ctx.match(fb, pr, mt, nm)
+    else:
+        m = np.zeros((P, n_max, 2), np.int32)
+        n = np.zeros(P, np.int32)
+        for p, l in enumerate(match_lists):
+            m[p, :len(l)] = l
+            n[p] = len(l)
+        mt, nm = torch.from_numpy(m).cuda(), torch.from_numpy(n).cuda()
+    out = {}
+    for mode in ("fma", "tc"):
+        if mode == "fma":
+            os.environ["BT_SCORE_FMA"] = "1"
+        else:
+            os.environ.pop("BT_SCORE_FMA", None)
+        rec = torch.zeros((P, bt.record_words(n_max)), dtype=torch.int32, device="cuda")
+        cnt = torch.full((P, n_hyp), -5, dtype=torch.int32, device="cuda")
+        ctx.ransac(fb, pr, tu, mt, nm, bt.ransac_params(n_hyp, SEED), rec, cnt)
+        torch.cuda.synchronize()
+        out[mode] = (rec.cpu().numpy(), cnt.cpu().numpy())
+    os.environ.pop("BT_SCORE_FMA", None)
+    return out, nm.cpu().numpy()
+
+
+def _assert_equal(out, what):
+    (rf, cf), (rt, ct) = out["fma"], out["tc"]
+    bad = np.argwhere(cf != ct)
+    assert bad.size == 0, f"{what}: {len(bad)} counts differ, first {bad[:5].tolist()} fma {cf[tuple(bad[0])]} tc {ct[tuple(bad[0])]}"
+    assert np.array_equal(rf, rt), f"{what}: records differ"
+
+
+def test_score_tc_equals_fma_c2(bt, torch):
+    """All 120 C2 pairs at 4096 hypotheses (the bench workload)."""
+    sc = synth.make_scene(16)
+    pairs = synth.all_pairs(16)
+    ctx = bt.Context(0)
+    ctx.reserve(len(pairs), sc.desc.shape[1], 4096, 16, 640, 480)
+    out, nm = _run_both(bt, torch, ctx, sc, pairs, 4096)
+    ctx.close()
+    assert (nm >= 3).all()
+    _assert_equal(out, "C2")
+    assert (out["tc"][1] > 0).any()
+
+
+def test_score_tc_equals_fma_c1_and_ragged(bt, torch):
+    """C1 (1024 hypotheses), a hypothesis count that is not a multiple of 128, noisy points."""
+    ctx = bt.Context(0)
+    ctx.reserve(4, 512, 2048, 2, 160, 120)
+    sc, *_ = synth.make_pair_c1()
+    out, _ = _run_both(bt, torch, ctx, sc, [(0, 1)], 1024)
+    _assert_equal(out, "C1")
+    sc, *_ = synth.make_pair_c1(seed=7, point_noise=0.001)
+    out, _ = _run_both(bt, torch, ctx, sc, [(0, 1)], 1000)
+    _assert_equal(out, "C1 noisy, H = 1000")
+    ctx.close()
+
+
+@pytest.mark.parametrize("M", [0, 1, 2, 3, 4, 127, 128, 129, 3000])
+def test_score_tc_equals_fma_match_counts(bt, torch, M):
+    """Degenerate and chunk-boundary correspondence counts (M = 3000: 24 chunks of 128)."""
+    rng = np.random.default_rng(100 + M)
+    n_max = 4096 if M > 512 else 512
+    sc = synth.make_scene(2, render_maps=False, seed=3)
+    Mm = max(M, 3)
+    pa, na, pb, nb, R, t, inl = synth.make_correspondences(rng, Mm, 0.45, noise=0.0005)
+    pts = np.zeros((2, n_max, 3), np.float32)
+    nrm = np.zeros((2, n_max, 3), np.float32)
+    nrm[:, :, 2] = -1.0
+    pts[:, :, 2] = 0.5
+    pts[0, :Mm], nrm[0, :Mm], pts[1, :Mm], nrm[1, :Mm] = pa, na, pb, nb
+    sc.pts, sc.nrm = pts, nrm
+    sc.desc = np.zeros((2, n_max, 128), np.float32)
+    sc.n_kp = np.array([Mm, Mm], np.int32)
+    sc.depth = sc.normal = sc.mask = None
+    m = np.stack([np.arange(M), np.arange(M)], 1).astype(np.int32)
+    ctx = bt.Context(0)
+    ctx.reserve(1, n_max, 2048, 2, 0, 0)
+    out, _ = _run_both(bt, torch, ctx, sc, [(0, 1)], 2048, match_lists=[m])
+    ctx.close()
+    _assert_equal(out, f"M = {M}")
