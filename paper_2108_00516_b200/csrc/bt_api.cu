@@ -255,7 +255,7 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
     if (ok) {
       cuuint64_t fd[2] = {64, (cuuint64_t)max_pairs * c->rs.m_pad};
       cuuint64_t fs[1] = {128};
-      cuuint32_t fbox[2] = {64, 128};
+      cuuint32_t fbox[2] = {64, (cuuint32_t)bt::score_chunk()};
       ok = encode(&c->tmap_feat, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, c->rs.feat, fd, fs, fbox, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;

@@ -120,6 +120,7 @@ struct RansacScratch {
 size_t ransac_scratch_bytes(int max_pairs, int max_hyp, int n_max);
 RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp, int n_max);
 int score_m_pad(int n_max);
+int score_chunk();                 // rows of a scoring feature chunk (TMA box)
 void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, int P,
                    const int32_t *matches, const int32_t *n_matches, const bt_ransac_params &prm,
                    const RansacScratch &rs, uint32_t *records, int rec_stride,

@@ -28,6 +28,10 @@
 #include "bt_internal.cuh"
 #include "bt_tc.cuh"
 
+#ifndef BT_TC_EPI_WARPS
+#define BT_TC_EPI_WARPS 16
+#endif
+
 namespace bt {
 namespace {
 
@@ -953,11 +957,15 @@ __device__ __forceinline__ f32x2 sub2s(float a, f32x2 b) {               // {a, 
 // of the tests) is listed and recounted with the fp32 formula itself (k_score_fix).  So the
 // counts are bit-identical to the FMA kernel's.
 constexpr int kTcRows = 128;                 // hypotheses per item (UMMA M)
-constexpr int kTcCols = 128;                 // correspondences per chunk (UMMA N)
+constexpr int kTcCols = 64;                  // correspondences per chunk (UMMA N)
+constexpr int kTcTBuf = 512 / (2 * kTcCols);  // TMEM buffers (D1 + D2 of a chunk each)
+constexpr int kTcWc = kTcCols / (BT_TC_EPI_WARPS / 4);  // columns per warpgroup and chunk
+constexpr int kTcPad = 128;                  // feature rows per pair: multiple of 128
 constexpr int kTcFeat = 64;                  // fp16 per feature row: X1/Y1 hi, lo | X2/Y2 hi, lo
-constexpr int kTcEpiWarps = 16;              // 4 warpgroups x 32 columns of a chunk
-constexpr int kTcThreads = (kTcEpiWarps + 1) * 32;
-constexpr int kTcBBuf = 3;
+constexpr int kTcEpiWarps = BT_TC_EPI_WARPS;  // warpgroups x (columns of a chunk / warpgroups)
+constexpr int kTcWgs = kTcEpiWarps / 4;
+constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;   // + MMA warp + TMA warp
+constexpr int kTcBBuf = 6;
 constexpr size_t kTcSmem = 1024 + 2 * kTcRows * 128 + kTcBBuf * kTcCols * 128;
 constexpr float kTcSentinel = 65504.f;       // padded correspondence: D1 = 65504 * s_x > any threshold
 
@@ -1009,14 +1017,48 @@ __device__ __forceinline__ void corr_y1(const double *ap, const double *bp, doub
   y1[15] = ap[0] * ap[0] + ap[1] * ap[1] + ap[2] * ap[2] + bp[0] * bp[0] + bp[1] * bp[1] + bp[2] * bp[2];
 }
 
-// one CTA per pair: centroids, feature maxima, the fp16 hi/lo feature rows (padded rows:
-// Y1 = (0, ..., 0, 65504) so that D1 exceeds every threshold, Y2 = 0)
-__global__ void __launch_bounds__(256) k_corr_feat(ScoreTcArgs A) {
+// One CTA per pair (512 threads, fp32): pass 1 gathers the pair's correspondences (kept in
+// registers for the first 512) and reduces the centroids and max |a|, |b|; pass 2 forms the
+// centred features, reduces their maxima (the error bound's max_m |Y_mk|, and the Y1 scale)
+// and writes the fp16 hi/lo rows (padded rows: Y1 = (0, ..., 0, 65504) so that D1 exceeds every
+// distance threshold, Y2 = 0).  The centroid need not be exact — any centring is algebraically
+// exact; fp32 feature rounding (2^-24) is inside the certificate's 2^-22 feature term.
+constexpr int kFeatThreads = 512;
+__device__ __forceinline__ void corr_y1f(const float *ap, const float *bp, float *y1) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { y1[k] = 2.f * ap[k]; y1[12 + k] = -2.f * bp[k]; }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) y1[3 + 3 * i + j] = -2.f * bp[i] * ap[j];
+  y1[15] = fmaf(ap[0], ap[0], fmaf(ap[1], ap[1], fmaf(ap[2], ap[2], fmaf(bp[0], bp[0], fmaf(bp[1], bp[1], bp[2] * bp[2])))));
+}
+template <int N, bool SUM>
+__device__ __forceinline__ void block_reduce_f(float (&v)[N], float (*red)[32]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const float y = __shfl_xor_sync(0xffffffffu, v[k], o);
+      v[k] = SUM ? v[k] + y : fmaxf(v[k], y);
+    }
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) red[k][warp] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    float t = SUM ? 0.f : 0.f;
+    for (int w = 0; w < kFeatThreads / 32; ++w) t = SUM ? t + red[k][w] : fmaxf(t, red[k][w]);
+    v[k] = t;
+  }
+}
+__global__ void __launch_bounds__(kFeatThreads) k_corr_feat(ScoreTcArgs A) {
   pdl_wait();
-  __shared__ double red[8][40];
-  __shared__ double bc[8];
-  __shared__ double mxs[26];
-  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ float red[26][32];
+  const int p = blockIdx.x, tid = threadIdx.x;
   if (p == 0 && tid < 2) A.ecount[tid] = 0;
   const int M = A.n_matches[p];
   PairFeat *pf = A.pf + p;
@@ -1026,96 +1068,92 @@ __global__ void __launch_bounds__(256) k_corr_feat(ScoreTcArgs A) {
   const int32_t *mt = A.matches + (size_t)p * A.kp.n_max * 2;
   const float *pa = A.kp.pts + (size_t)fa * A.kp.n_max * 3, *pb = A.kp.pts + (size_t)fb * A.kp.n_max * 3;
   const float *na = A.kp.nrm + (size_t)fa * A.kp.n_max * 3, *nb = A.kp.nrm + (size_t)fb * A.kp.n_max * 3;
-  // centroids (fp64 sums, fixed order: thread-strided then tree)
-  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int m = tid; m < M; m += 256) {
-    const float *x = pa + 3 * mt[2 * m], *y = pb + 3 * mt[2 * m + 1];
+  auto gather = [&](int m, float *x, float *y, float *u, float *w) {
+    const int i = mt[2 * m], j = mt[2 * m + 1];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { x[k] = pa[3 * i + k]; y[k] = pb[3 * j + k]; u[k] = na[3 * i + k]; w[k] = nb[3 * j + k]; }
+  };
+  float x0[3] = {0, 0, 0}, y0[3] = {0, 0, 0}, u0[3] = {0, 0, 0}, w0[3] = {0, 0, 0};
+  if (tid < M) gather(tid, x0, y0, u0, w0);
+  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int m = tid; m < M; m += kFeatThreads) {
+    float x[3], y[3], u[3], w[3];
+    if (m == tid) { for (int k = 0; k < 3; ++k) { x[k] = x0[k]; y[k] = y0[k]; } }
+    else gather(m, x, y, u, w);
     s[0] += x[0]; s[1] += x[1]; s[2] += x[2]; s[3] += y[0]; s[4] += y[1]; s[5] += y[2];
-    s[6] = fmax(s[6], sqrt((double)x[0] * x[0] + (double)x[1] * x[1] + (double)x[2] * x[2]));
-    s[7] = fmax(s[7], sqrt((double)y[0] * y[0] + (double)y[1] * y[1] + (double)y[2] * y[2]));
+    s[6] = fmaxf(s[6], sqrtf(fmaf(x[0], x[0], fmaf(x[1], x[1], x[2] * x[2]))));
+    s[7] = fmaxf(s[7], sqrtf(fmaf(y[0], y[0], fmaf(y[1], y[1], y[2] * y[2]))));
   }
-  for (int k = 0; k < 8; ++k)
-    for (int o = 16; o >= 1; o >>= 1) {
-      const double v = __shfl_xor_sync(0xffffffffu, s[k], o);
-      s[k] = k < 6 ? s[k] + v : fmax(s[k], v);
-    }
-  if (lane == 0) for (int k = 0; k < 8; ++k) red[warp][k] = s[k];
-  __syncthreads();
-  if (tid < 8) {
-    double v = 0.0;
-    for (int w = 0; w < 8; ++w) v = tid < 6 ? v + red[w][tid] : fmax(v, red[w][tid]);
-    bc[tid] = v;
+  {
+    float sm[6] = {s[0], s[1], s[2], s[3], s[4], s[5]}, mx[2] = {s[6], s[7]};
+    block_reduce_f<6, true>(sm, red);
+    block_reduce_f<2, false>(mx, red + 8);
+    for (int k = 0; k < 6; ++k) s[k] = sm[k] / (float)M;
+    s[6] = mx[0]; s[7] = mx[1];
   }
-  __syncthreads();
-  float cen[6];
-  for (int k = 0; k < 6; ++k) cen[k] = (float)(bc[k] / M);
-  // feature maxima
-  double mx[26];
-  for (int k = 0; k < 26; ++k) mx[k] = 0.0;
-  for (int m = tid; m < M; m += 256) {
-    const float *x = pa + 3 * mt[2 * m], *y = pb + 3 * mt[2 * m + 1];
-    const float *u = na + 3 * mt[2 * m], *v = nb + 3 * mt[2 * m + 1];
-    double ap[3], bp[3];
-    for (int k = 0; k < 3; ++k) { ap[k] = (double)x[k] - cen[k]; bp[k] = (double)y[k] - cen[3 + k]; }
-    double y1[16];
-    corr_y1(ap, bp, y1);
-    for (int k = 0; k < 16; ++k) mx[k] = fmax(mx[k], fabs(y1[k]));
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) mx[16 + 3 * i + j] = fmax(mx[16 + 3 * i + j], fabs((double)v[i] * u[j]));
-    mx[25] = fmax(mx[25], ap[0] * ap[0] + ap[1] * ap[1] + ap[2] * ap[2]);
+  const float cen[6] = {s[0], s[1], s[2], s[3], s[4], s[5]};
+  // pass 2: feature maxima
+  float mxv[26];
+#pragma unroll
+  for (int k = 0; k < 26; ++k) mxv[k] = 0.f;
+  for (int m = tid; m < M; m += kFeatThreads) {
+    float x[3], y[3], u[3], w[3];
+    if (m == tid) { for (int k = 0; k < 3; ++k) { x[k] = x0[k]; y[k] = y0[k]; u[k] = u0[k]; w[k] = w0[k]; } }
+    else gather(m, x, y, u, w);
+    float ap[3], bp[3], y1[16];
+    for (int k = 0; k < 3; ++k) { ap[k] = x[k] - cen[k]; bp[k] = y[k] - cen[3 + k]; }
+    corr_y1f(ap, bp, y1);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) mxv[k] = fmaxf(mxv[k], fabsf(y1[k]));
+#pragma unroll
+    for (int k = 0; k < 9; ++k) mxv[16 + k] = fmaxf(mxv[16 + k], fabsf(w[k / 3] * u[k % 3]));
+    mxv[25] = fmaxf(mxv[25], fmaf(ap[0], ap[0], fmaf(ap[1], ap[1], ap[2] * ap[2])));
   }
-  __syncthreads();                                          // red / bc of the centroid pass consumed
-  for (int k = 0; k < 26; ++k) {
-    for (int o = 16; o >= 1; o >>= 1) mx[k] = fmax(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
-    if (lane == 0) red[warp][k] = mx[k];
-  }
-  __syncthreads();
-  if (tid < 26) {
-    double v = 0.0;
-    for (int w = 0; w < 8; ++w) v = fmax(v, red[w][tid]);
-    mxs[tid] = v;
-    if (tid < 16) pf->ymax1[tid] = round_up_pos(v);
-    else if (tid < 25) pf->ymax2[tid - 16] = round_up_pos(v);
-    else pf->apmax2 = round_up_pos(v);
-  }
-  if (tid >= 9 && tid < 16) pf->ymax2[tid] = 0.f;
-  __syncthreads();
+  block_reduce_f<26, false>(mxv, red);
   // Y1 scale: max |Y1| * sy1 < 2^14, and >= delta^2 so that the padded rows' 65504 * s_x
   // exceeds every distance threshold (65504 / sy1 > 4 max(|Y1|max, delta^2))
-  double ymx = -(double)A.ndelta2;
-  for (int k = 0; k < 16; ++k) ymx = fmax(ymx, mxs[k]);
-  int e;
-  frexp(ymx, &e);                                           // ymx < 2^e
-  const double sy1 = ldexp(1.0, 14 - e), sy2 = 16384.0;
+  float ymx = A.sc.delta2;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) ymx = fmaxf(ymx, mxv[k]);
+  const int e = ((__float_as_int(ymx) >> 23) & 255) - 126;   // ymx < 2^e
+  const float sy1 = __int_as_float((127 + 14 - e) << 23), sy2 = 16384.f;
+  if (tid < 16) pf->ymax1[tid] = mxv[tid] * 1.0000002f;
+  else if (tid < 25) pf->ymax2[tid - 16] = mxv[tid] * 1.0000002f;
+  else if (tid < 32) pf->ymax2[tid - 16] = 0.f;
   if (tid == 0) {
     for (int k = 0; k < 6; ++k) (k < 3 ? pf->abar[k] : pf->bbar[k - 3]) = cen[k];
-    pf->sy1 = (float)sy1;
-    pf->ab = round_up_pos((2.0 * bc[6] + bc[7]) * (1.0 + 1e-6));
-    pf->korth = round_up_pos(2e-6 * mxs[25]);
+    pf->sy1 = sy1;
+    pf->ab = (2.f * s[6] + s[7]) * 1.00001f;
+    pf->korth = 2e-6f * mxv[25] * 1.0001f;
+    pf->apmax2 = mxv[25];
   }
   const int mp = (M + kTcCols - 1) / kTcCols * kTcCols;
   __half *F = A.feat + (size_t)p * A.m_pad * kTcFeat;
-  for (int m = tid; m < mp; m += 256) {
-    __half *row = F + (size_t)m * kTcFeat;
-    __half h1[16], l1[16], h2[16], l2[16];
+  for (int m = tid; m < mp; m += kFeatThreads) {
+    __align__(16) __half h1[16], l1[16], h2[16], l2[16];
     if (m < M) {
-      const float *x = pa + 3 * mt[2 * m], *y = pb + 3 * mt[2 * m + 1];
-      const float *u = na + 3 * mt[2 * m], *v = nb + 3 * mt[2 * m + 1];
-      double ap[3], bp[3];
-      for (int k = 0; k < 3; ++k) { ap[k] = (double)x[k] - cen[k]; bp[k] = (double)y[k] - cen[3 + k]; }
-      double y1[16];
-      corr_y1(ap, bp, y1);
-      for (int k = 0; k < 16; ++k) split_half(y1[k] * sy1, h1[k], l1[k]);
+      float x[3], y[3], u[3], w[3];
+      if (m == tid) { for (int k = 0; k < 3; ++k) { x[k] = x0[k]; y[k] = y0[k]; u[k] = u0[k]; w[k] = w0[k]; } }
+      else gather(m, x, y, u, w);
+      float ap[3], bp[3], y1[16];
+      for (int k = 0; k < 3; ++k) { ap[k] = x[k] - cen[k]; bp[k] = y[k] - cen[3 + k]; }
+      corr_y1f(ap, bp, y1);
+#pragma unroll
       for (int k = 0; k < 16; ++k) {
-        const double y2 = k < 9 ? (double)v[k / 3] * u[k % 3] * sy2 : 0.0;
-        split_half(y2, h2[k], l2[k]);
+        const float v1 = y1[k] * sy1;
+        h1[k] = __float2half_rn(v1);
+        l1[k] = __float2half_rn(v1 - __half2float(h1[k]));
+        const float v2 = k < 9 ? w[k / 3] * u[k % 3] * sy2 : 0.f;
+        h2[k] = __float2half_rn(v2);
+        l2[k] = __float2half_rn(v2 - __half2float(h2[k]));
       }
     } else {
+#pragma unroll
       for (int k = 0; k < 16; ++k) {
         h1[k] = __float2half_rn(k == 15 ? kTcSentinel : 0.f); l1[k] = h2[k] = l2[k] = __float2half_rn(0.f);
       }
     }
-    uint4 *dst = reinterpret_cast<uint4 *>(row);
+    uint4 *dst = reinterpret_cast<uint4 *>(F + (size_t)m * kTcFeat);
     const uint4 *s1 = reinterpret_cast<const uint4 *>(h1), *s2 = reinterpret_cast<const uint4 *>(l1);
     const uint4 *s3 = reinterpret_cast<const uint4 *>(h2), *s4 = reinterpret_cast<const uint4 *>(l2);
     dst[0] = s1[0]; dst[1] = s1[1]; dst[2] = s2[0]; dst[3] = s2[1];
@@ -1142,63 +1180,71 @@ constexpr float kSatB = 18446744073709551616.f;   // 2^64: sat((lo - x) 2^64) is
 // the 128B-swizzled A tile (16-B chunk c of row r lands at c ^ (r & 7)): part 0 X1 hi, 1 X1 lo,
 // 2 X2 hi, 3 X2 lo.  fp32 throughout: the features' own rounding (2^-22 relative) is in c_rel,
 // the thresholds carry a 2^-21 (delta^2 + |t'|^2) slack for their fp32 evaluation.
-__device__ __forceinline__ RowConst row_setup(const ScoreTcArgs &A, const PairFeat &pf, const float *T, uint8_t *arow,
-                                              int r, int part, bool want_thr) {
+__device__ __forceinline__ RowConst row_setup(const ScoreTcArgs &A, const PairFeat *pf, const float *T, uint8_t *arow,
+                                              int r, int part) {
   RowConst rc;
   rc.valid = T[11] < 1e30f;
-  float R[9], t[3];
+  float R[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) R[k] = rc.valid ? T[k] : 0.f;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) t[k] = rc.valid ? T[9 + k] : 0.f;
-  float x1[16];                                            // [R^T t', vec R, t', 1]
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-    x1[12 + i] = t[i] + fmaf(R[3 * i], pf.abar[0], fmaf(R[3 * i + 1], pf.abar[1], R[3 * i + 2] * pf.abar[2])) - pf.bbar[i];
-#pragma unroll
-  for (int j = 0; j < 3; ++j) x1[j] = fmaf(R[j], x1[12], fmaf(R[3 + j], x1[13], R[6 + j] * x1[14]));
-#pragma unroll
-  for (int k = 0; k < 9; ++k) x1[3 + k] = R[k];
-  x1[15] = 1.f;
-  const float tn2 = fmaf(x1[12], x1[12], fmaf(x1[13], x1[13], x1[14] * x1[14]));
-  // max |X1| <= max(1.0001, 1.0001 |t'|) < 2^e  ->  sx = 2^(14 - e)
-  const float xm = fmaxf(1.0001f, 1.0001f * sqrtf(tn2) + 1e-6f);
-  const int e = ((__float_as_int(xm) >> 23) & 255) - 126;
-  const float sx = __int_as_float((127 + 14 - e) << 23);
-  if (want_thr) {
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) s1 = fmaf(fabsf(x1[k]), pf.ymax1[k], s1);
-#pragma unroll
-  for (int k = 0; k < 9; ++k) s2 = fmaf(fabsf(R[k]), pf.ymax2[k], s2);
-  const float E = 0x1p-21f * (pf.ab + fabsf(t[0]) + fabsf(t[1]) + fabsf(t[2]));
-  const float eref1 = fmaf(E, fmaf(3.f, E, A.sc.e_a), A.sc.e_b);
-  const float eps1 = fmaf(A.sc.c_rel, s1, pf.korth + eref1 + 0x1p-21f * (A.sc.delta2 + tn2)) * 1.0001f;
-  const float eps2 = fmaf(A.sc.c_rel, s2, A.sc.k2) * 1.0001f;
-  const float sc1 = sx * pf.sy1, sc2 = 268435456.f;         // D1, D2 scales (powers of two)
-  const float thr = A.sc.delta2 - tn2;
-  rc.lo1 = sc1 * (thr - eps1);
-  rc.hi1 = sc1 * (thr + eps1);
-  rc.lo2 = sc2 * (A.sc.cosa - eps2);
-  rc.hi2 = sc2 * (A.sc.cosa + eps2);
-  rc.lo1B = rc.lo1 * kSatB;
-  rc.hi2B = rc.hi2 * kSatB;
-  rc.lo2r = rc.lo2;
-  }
-  if (arow) {
-    __align__(16) __half h[16];
-    const bool lo = part & 1;
+  __align__(16) __half h[16];
+  if (part >= 2) {                                         // X2 = vec R (scaled 2^14): hi or lo
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      const float x = part < 2 ? x1[k] * sx : (k < 9 ? R[k] * 16384.f : 0.f);
+      const float x = k < 9 ? R[k] * 16384.f : 0.f;
       const __half hi = __float2half_rn(x);
-      h[k] = lo ? __float2half_rn(x - __half2float(hi)) : hi;
+      h[k] = part == 3 ? __float2half_rn(x - __half2float(hi)) : hi;
     }
-    const uint4 *src = reinterpret_cast<const uint4 *>(h);
-    uint4 *dst = reinterpret_cast<uint4 *>(arow);
-    dst[(2 * part) ^ (r & 7)] = src[0];
-    dst[(2 * part + 1) ^ (r & 7)] = src[1];
+  } else {
+    float t[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[k] = rc.valid ? T[9 + k] : 0.f;
+    const float ab0 = pf->abar[0], ab1 = pf->abar[1], ab2 = pf->abar[2];
+    float x1[16];                                          // [R^T t', vec R, t', 1]
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      x1[12 + i] = t[i] + fmaf(R[3 * i], ab0, fmaf(R[3 * i + 1], ab1, R[3 * i + 2] * ab2)) - pf->bbar[i];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) x1[j] = fmaf(R[j], x1[12], fmaf(R[3 + j], x1[13], R[6 + j] * x1[14]));
+#pragma unroll
+    for (int k = 0; k < 9; ++k) x1[3 + k] = R[k];
+    x1[15] = 1.f;
+    const float tn2 = fmaf(x1[12], x1[12], fmaf(x1[13], x1[13], x1[14] * x1[14]));
+    // max |X1| <= max(1.0001, 1.0001 |t'|) < 2^e  ->  sx = 2^(14 - e)
+    const float xm = fmaxf(1.0001f, 1.0001f * sqrtf(tn2) + 1e-6f);
+    const int e = ((__float_as_int(xm) >> 23) & 255) - 126;
+    const float sx = __int_as_float((127 + 14 - e) << 23);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float x = x1[k] * sx;
+      const __half hi = __float2half_rn(x);
+      h[k] = part == 1 ? __float2half_rn(x - __half2float(hi)) : hi;
+    }
+    if (part == 0) {                                       // the row's thresholds
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) s1 = fmaf(fabsf(x1[k]), pf->ymax1[k], s1);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) s2 = fmaf(fabsf(R[k]), pf->ymax2[k], s2);
+      const float E = 0x1p-21f * (pf->ab + fabsf(t[0]) + fabsf(t[1]) + fabsf(t[2]));
+      const float eref1 = fmaf(E, fmaf(3.f, E, A.sc.e_a), A.sc.e_b);
+      const float eps1 = fmaf(A.sc.c_rel, s1, pf->korth + eref1 + 0x1p-21f * (A.sc.delta2 + tn2)) * 1.0001f;
+      const float eps2 = fmaf(A.sc.c_rel, s2, A.sc.k2) * 1.0001f;
+      const float sc1 = sx * pf->sy1, sc2 = 268435456.f;     // D1, D2 scales (powers of two)
+      const float thr = A.sc.delta2 - tn2;
+      rc.lo1 = sc1 * (thr - eps1);
+      rc.hi1 = sc1 * (thr + eps1);
+      rc.lo2 = sc2 * (A.sc.cosa - eps2);
+      rc.hi2 = sc2 * (A.sc.cosa + eps2);
+      rc.lo1B = rc.lo1 * kSatB;
+      rc.hi2B = rc.hi2 * kSatB;
+      rc.lo2r = rc.lo2;
+    }
   }
+  const uint4 *src = reinterpret_cast<const uint4 *>(h);
+  uint4 *dst = reinterpret_cast<uint4 *>(arow);
+  dst[(2 * part) ^ (r & 7)] = src[0];
+  dst[(2 * part + 1) ^ (r & 7)] = src[1];
   return rc;
 }
 
@@ -1213,7 +1259,7 @@ __device__ __forceinline__ RowConst row_setup(const ScoreTcArgs &A, const PairFe
 __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constant__ CUtensorMap fmap, ScoreTcArgs A) {
   pdl_wait();
   extern __shared__ uint8_t tc_smem_raw[];
-  __shared__ __align__(8) uint64_t bar_a[2], bar_bfull[kTcBBuf], bar_bfree[kTcBBuf], bar_mma[2], bar_tfree[2];
+  __shared__ __align__(8) uint64_t bar_a[2], bar_bfull[kTcBBuf], bar_bfree[kTcBBuf], bar_mma[kTcTBuf], bar_tfree[kTcTBuf];
   __shared__ uint32_t tmem_base_sh;
   __shared__ float4 rowc[4][kTcRows];
   __shared__ bool rowv[4][kTcRows];
@@ -1229,9 +1275,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bar_a[b], kTcEpiWarps); mbar_init(&bar_mma[b], 1); mbar_init(&bar_tfree[b], kTcEpiWarps);
-    }
+    for (int b = 0; b < 2; ++b) mbar_init(&bar_a[b], kTcEpiWarps);
+    for (int b = 0; b < kTcTBuf; ++b) { mbar_init(&bar_mma[b], 1); mbar_init(&bar_tfree[b], kTcEpiWarps); }
     for (int b = 0; b < kTcBBuf; ++b) { mbar_init(&bar_bfull[b], 1); mbar_init(&bar_bfree[b], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1242,8 +1287,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
   const uint32_t tmem = tmem_base_sh;
   const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcCols >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
 
-  if (warp == kTcEpiWarps) {
-    // ------------------------------------------------------------ producer
+  if (warp == kTcEpiWarps + 1) {
+    // ------------------------------------------------------------ TMA warp: runs up to
+    // kTcBBuf chunks ahead of the MMAs (a buffer is refilled once the MMAs of its last chunk ended)
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int p = it / A.nht;
+        const int M = A.n_matches[p];
+        if (M < 3) continue;
+        const int nch = (M + kTcCols - 1) / kTcCols;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int bb = g % kTcBBuf;
+          const uint32_t use = g / kTcBBuf;
+          if (use > 0) mbar_wait_sleep(&bar_bfree[bb], (use - 1) & 1);
+          mbar_expect_tx(&bar_bfull[bb], kTcCols * 128);
+          tma_load_2d(sB + bb * kTcCols * 128, &fmap, 0, p * A.m_pad + c * kTcCols, &bar_bfull[bb]);
+        }
+      }
+    }
+  } else if (warp == kTcEpiWarps) {
+    // ------------------------------------------------------------ MMA warp
     if (lane == 0) {
       uint32_t g = 0, k = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -1252,17 +1316,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
         if (M < 3) continue;
         const int nch = (M + kTcCols - 1) / kTcCols;
         for (int c = 0; c < nch; ++c, ++g) {
-          const int bb = g % kTcBBuf, tb = g & 1;
+          const int bb = g % kTcBBuf, tb = g % kTcTBuf;
           const uint32_t use = g / kTcBBuf;
-          if (use > 0) mbar_wait(&bar_bfree[bb], (use - 1) & 1);
-          mbar_expect_tx(&bar_bfull[bb], kTcCols * 128);
-          tma_load_2d(sB + bb * kTcCols * 128, &fmap, 0, p * A.m_pad + c * kTcCols, &bar_bfull[bb]);
-          if (c == 0) mbar_wait(&bar_a[k & 1], (k >> 1) & 1);
-          if (g >= 2) mbar_wait(&bar_tfree[tb], ((g - 2) >> 1) & 1);
-          mbar_wait(&bar_bfull[bb], use & 1);
+          if (c == 0) mbar_wait_sleep(&bar_a[k & 1], (k >> 1) & 1);
+          if (g >= kTcTBuf) mbar_wait_sleep(&bar_tfree[tb], ((g - kTcTBuf) / kTcTBuf) & 1);
+          mbar_wait_sleep(&bar_bfull[bb], use & 1);
           tc_fence_after();
           const uint8_t *a = sA + (k & 1) * kTcRows * 128, *b = sB + bb * kTcCols * 128;
-          const uint32_t d1 = tmem + tb * 256, d2 = d1 + 128;
+          const uint32_t d1 = tmem + tb * 2 * kTcCols, d2 = d1 + kTcCols;
           umma_f16(d1, umma_desc_sw128(a), umma_desc_sw128(b), idesc, 0u);             // X1hi . Y1hi
           umma_f16(d1, umma_desc_sw128(a), umma_desc_sw128(b + 32), idesc, 1u);        // X1hi . Y1lo
           umma_f16(d1, umma_desc_sw128(a + 32), umma_desc_sw128(b), idesc, 1u);        // X1lo . Y1hi
@@ -1290,8 +1351,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
     auto build = [&](int itb, uint32_t kb) {
       const int pb = itb / A.nht, hb = (itb - pb * A.nht) * kTcRows + lrow;
       load_T(A, pb, hb, Tn);
-      const PairFeat pfb = A.pf[pb];
-      const RowConst r = row_setup(A, pfb, Tn, sA + (kb & 1) * kTcRows * 128 + lrow * 128, lrow, wg, wg == 0);
+      RowConst r = row_setup(A, A.pf + pb, Tn, sA + (kb & 1) * kTcRows * 128 + lrow * 128, lrow, wg);
+      for (int part = wg + kTcWgs; part < 4; part += kTcWgs)
+        row_setup(A, A.pf + pb, Tn, sA + (kb & 1) * kTcRows * 128 + lrow * 128, lrow, part);
       if (wg == 0) {
         rowc[kb & 3][lrow] = make_float4(r.lo1B, r.hi1, r.lo2, r.hi2B);
         rowv[kb & 3][lrow] = r.valid;
@@ -1308,7 +1370,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
       int itn = it + gridDim.x;
       while (itn < n_items && A.n_matches[itn / A.nht] < 3) itn += gridDim.x;
       if (itn < n_items) build(itn, k + 1);
-      mbar_wait(&bar_a[k & 1], (k >> 1) & 1);                     // this item's thresholds
+      mbar_wait_sleep(&bar_a[k & 1], (k >> 1) & 1);               // this item's thresholds
       RowConst rc;
       {
         const float4 v = rowc[k & 3][lrow];
@@ -1319,48 +1381,52 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
       unsigned cert = 0;
       bool overflow = false;
       for (int c = 0; c < nch; ++c, ++g) {
-        const int tb = g & 1;
-        mbar_wait(&bar_mma[tb], (g >> 1) & 1);
+        const int tb = g % kTcTBuf;
+        mbar_wait_sleep(&bar_mma[tb], (g / kTcTBuf) & 1, 200);
         tc_fence_after();
-        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * 256 + wg * 32);
-        if (c * kTcCols + wg * 32 >= M) {                           // all 32 columns padding: release only
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * 2 * kTcCols + wg * kTcWc);
+        if (c * kTcCols + wg * kTcWc >= M) {                        // all columns padding: release only
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar_tfree[tb]);
           continue;
         }
         const f32x2 hi1 = pk(-rc.hi1, -rc.hi1);
-        // two halves of 16 columns (D1 and D2): 32 live registers instead of 64 (17 warps leave
-        // 96 registers per thread); the buffer is released after the second half's load
-#pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
-          uint32_t v1[16], v2[16];
-          BT_TMEM_LD16(ta + hf * 16, v1);
-          BT_TMEM_LD16(ta + 128 + hf * 16, v2);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (hf == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_tfree[tb]);
-          }
+        // the warp's columns of D1 and D2 in 16-column loads, all issued before one wait; the
+        // buffer is released as soon as they are in registers
+        constexpr int kH = kTcWc / 16;
+        uint32_t v1a[kH][16], v2a[kH][16];
+#pragma unroll
+        for (int hf = 0; hf < kH; ++hf) {
+          BT_TMEM_LD16(ta + hf * 16, v1a[hf]);
+          BT_TMEM_LD16(ta + kTcCols + hf * 16, v2a[hf]);
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_tfree[tb]);
+#pragma unroll
+        for (int hf = 0; hf < kH; ++hf) {
+          const uint32_t *v1 = v1a[hf], *v2 = v2a[hf];
           // certain (D1 < lo1 and D2 > hi2) on the FMA pipe: sat((lo1 - x) 2^64) * sat((y - hi2) 2^64);
           // possible (D1 < hi1 and D2 > lo2) from sign bits
-          f32x2 cacc = pk(0.f, 0.f);
-          unsigned pc = 0;
+          f32x2 cacc[4] = {pk(0.f, 0.f), pk(0.f, 0.f), pk(0.f, 0.f), pk(0.f, 0.f)};   // 4 short chains
+          unsigned pcs[2] = {0u, 0u};
 #pragma unroll
           for (int col = 0; col < 16; col += 2) {
             const float x0 = __uint_as_float(v1[col]), x1 = __uint_as_float(v1[col + 1]);
             const float y0 = __uint_as_float(v2[col]), y1 = __uint_as_float(v2[col + 1]);
             const f32x2 ia = pk(__saturatef(__fmaf_rn(x0, -kSatB, rc.lo1B)), __saturatef(__fmaf_rn(x1, -kSatB, rc.lo1B)));
             const f32x2 ib = pk(__saturatef(__fmaf_rn(y0, kSatB, -rc.hi2B)), __saturatef(__fmaf_rn(y1, kSatB, -rc.hi2B)));
-            cacc = fma2v(ia, ib, cacc);
+            cacc[(col >> 1) & 3] = fma2v(ia, ib, cacc[(col >> 1) & 3]);
             unsigned c0_, c1_, e0, e1;
             split(add2v(pk(x0, x1), hi1), c0_, c1_);
             split(sub2s(rc.lo2r, pk(y0, y1)), e0, e1);
-            pc += ((c0_ & e0) >> 31) + ((c1_ & e1) >> 31);
+            pcs[(col >> 1) & 1] += ((c0_ & e0) >> 31) + ((c1_ & e1) >> 31);
           }
+          const unsigned pc = pcs[0] + pcs[1];
           unsigned ca_, cb_;
-          split(cacc, ca_, cb_);
+          split(add2v(add2v(cacc[0], cacc[1]), add2v(cacc[2], cacc[3])), ca_, cb_);
           const unsigned cc = (unsigned)(__uint_as_float(ca_) + __uint_as_float(cb_));
           cert += cc;
           if (__any_sync(0xffffffffu, pc != cc)) {                // rare: list the undecided tests
@@ -1371,7 +1437,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
                 const bool sure = x < rc.lo1 && y > rc.hi2, maybe = x < rc.hi1 && y > rc.lo2;
                 if (maybe && !sure && h < A.n_hyp && rc.valid) {
                   const int slot = atomicAdd(A.ecount, 1);
-                  if (slot < A.ecap) A.elist[slot] = make_int4(p, h, c * kTcCols + wg * 32 + hf * 16 + col, 0);
+                  if (slot < A.ecap) A.elist[slot] = make_int4(p, h, c * kTcCols + wg * kTcWc + hf * 16 + col, 0);
                   else overflow = true;
                 }
               }
@@ -1456,7 +1522,8 @@ static size_t hyp_slots(int max_pairs, int max_hyp) {
 }
 
 static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
-int score_m_pad(int n_max) { return (n_max + kTcCols - 1) / kTcCols * kTcCols; }
+int score_m_pad(int n_max) { return (n_max + kTcPad - 1) / kTcPad * kTcPad; }
+int score_chunk() { return kTcCols; }
 
 size_t ransac_scratch_bytes(int max_pairs, int max_hyp, int n_max) {
   return al256(hyp_slots(max_pairs, max_hyp) * 48) + al256((size_t)max_pairs * max_hyp * 4) + 256 +
@@ -1551,7 +1618,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
       tc_grid = n_sm;                                              // one CTA per SM (all 512 TMEM columns)
     }
     L.begin(K_RANSAC_SCORE, s);
-    launch_pdl(k_corr_feat, P, 256, 0, s, t);
+    launch_pdl(k_corr_feat, P, kFeatThreads, 0, s, t);
     L.end(K_RANSAC_SCORE, s);
     L.begin(K_RANSAC_SCORE, s);
     launch_pdl(k_score_tc, std::min(tc_grid, P * t.nht), kTcThreads, kTcSmem, s, *rs.fmap, t);
