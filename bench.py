@@ -345,7 +345,18 @@ def main():
     add("k_match_tc", "tensor", 2 * pair_sizes * 128, "TFLOP/s", tc_peak,
         "2 n_a n_b 128 flop per pair (the Gram contraction, counted once)")
     add("k_ransac_score", "alu", tests * FLOPS_TEST, "TFLOP/s", fp32_peak_tflops,
-        f"{FLOPS_TEST} flop per (hypothesis, correspondence) test (SURVEY 8(d)); {tests} tests")
+        f"{FLOPS_TEST} flop per (hypothesis, correspondence) test (SURVEY 8(d)); {tests} tests; measured on "
+        "the scoring stage as launched: k_corr_feat + k_score_tc (tcgen05 fp16 hi/lo contractions + "
+        "FMA/ALU epilogue, DESIGN.md R27) + k_score_fix (+ k_score_fix_rows), or the FFMA2 kernel with "
+        "BT_SCORE_FMA=1; peak = the FP32 FMA pipe of the direct formulation")
+    if "k_ransac_score" in kern and not os.environ.get("BT_SCORE_FMA") == "1":
+        # the same stage seen as tensor work: 6 MMAs x 16 K x 2 flop per (hypothesis row,
+        # correspondence column) of every computed 128 x 64 tile, padding columns included
+        cols = float(sum(((int(c) + 63) // 64) * 64 for c in M if c >= 3))
+        tc_flop = cols * ((N_HYP + 127) // 128) * 128 * 6 * 16 * 2
+        t = kern["k_ransac_score"]
+        t["tensor_view"] = {"flop": tc_flop, "achieved_tflops": tc_flop / (t["avg_launch_ms"] * t["launches_per_step"] / 1e3) / 1e12,
+                            "peak_tflops": tc_peak}
     if "k_ransac_score" in kern:                       # the short-circuit lower bound, for reference
         lb = tests * FLOPS_DIST + sum_counts * FLOPS_NORMAL
         kern["k_ransac_score"]["frac_short_circuit_lower_bound"] = kern["k_ransac_score"]["frac"] * lb / (

@@ -11,5 +11,5 @@ timeout 600 python bench.py --impl reference --steps 10 --warmup 2 > gpurun_out/
 CMD="python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k "regex:k_ransac_score|k_ransac_hyp|k_match_tc|k_dense_prep|k_dense$|k_dense\(" -s 5 -c 10 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k "regex:k_corr_feat|k_score_tc|k_score_fix|k_ransac_hyp|k_match_ws|k_dense_mask|k_dense_prep|k_edge_setup|k_dense_scan|k_dense$|k_dense\(" -s 10 -c 22 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo done

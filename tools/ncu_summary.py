@@ -48,7 +48,7 @@ for r in rows[2:]:
 lines = [f"# ncu --set full summary ({os.path.basename(rep)})", "",
          "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
          "(cold cache, serialised, replayed: compare shares, not absolutes).  'FMA pipe inst %' counts an "
-         "FFMA2 (packed fp32x2, k_ransac_score) as one instruction; 'FMA pipe cycles %' / 'FMA-heavy "
+         "FFMA2 (packed fp32x2) as one instruction; 'FMA pipe cycles %' / 'FMA-heavy "
          "cycles %' measure the pipe's occupancy (FFMA2 issues on the FMA-heavy pipe).", "",
          "| kernel | launches | " + " | ".join(m[1] for m in METRICS) + " |",
          "|---|---|" + "---|" * len(METRICS)]
@@ -93,16 +93,17 @@ for k, v in tot.most_common():
 # the bt_register_pairs step alone (the bench command also runs standalone stage passes and the
 # NEXT-row sections, which reuse the dense kernels): split the list into maximal runs of step
 # kernels (the L2 flush between steps and every other kernel end a run) and keep the runs that
-# hold whole steps (as many k_dense as k_ransac_score launches, at least one)
-STEP = {"k_desc_prep", "k_match_tc", "k_fullscan", "k_rescore", "k_mutual", "k_ransac_hyp", "k_ransac_score",
-        "k_ransac_finish", "k_edge_setup", "k_dense_prep", "k_dense_scan", "k_dense", "k_dense_reduce"}
+# hold whole steps (as many k_dense as scoring launches, at least one)
+STEP = {"k_desc_prep", "k_match_tc", "k_match_ws", "k_fullscan", "k_rescore", "k_mutual", "k_ransac_hyp",
+        "k_ransac_score", "k_corr_feat", "k_score_tc", "k_score_fix", "k_score_fix_rows", "k_ransac_finish",
+        "k_edge_setup", "k_dense_mask", "k_dense_prep", "k_dense_scan", "k_dense", "k_dense_reduce"}
 stot, scnt, n_steps = collections.Counter(), collections.Counter(), 0
 run_t, run_c = collections.Counter(), collections.Counter()
 
 
 def close_run():
     global n_steps
-    ns = run_c["k_ransac_score"]
+    ns = run_c["k_ransac_score"] + run_c["k_score_tc"]
     if ns and run_c["k_dense"] == ns:
         stot.update(run_t)
         scnt.update(run_c)
@@ -129,6 +130,15 @@ if n_steps:
         lines.append(f"| {k} | {scnt[k] / n_steps:g} | {v / n_steps:.1f} | {100 * v / step_us:.1f}% |")
     lines.append(f"| (sum) | | {step_us / n_steps:.1f} | 100% |")
 open(out + ".md", "w").write("\n".join(lines) + "\n")
-json.dump({k: v for k, v in traffic.items()}, open(os.path.join(os.path.dirname(out), "ncu_traffic.json"), "w"),
-          indent=1)
+# per profiling bucket of libbt (bench.py's kernel names): the sum over the kernels the bucket
+# launches once per step (each kernel's traffic averaged over its captured launches)
+BUCKETS = {"k_ransac_score": ["k_corr_feat", "k_score_tc", "k_score_fix", "k_score_fix_rows", "k_ransac_score"],
+           "k_match_tc": ["k_match_ws", "k_match_tc"],
+           "k_dense_prep": ["k_edge_setup", "k_dense_mask", "k_dense_prep", "k_dense_scan"]}
+out_t = dict(traffic)
+for b, ks in BUCKETS.items():
+    got = [traffic[k] for k in ks if k in traffic]
+    if got:
+        out_t[b] = sum(got)
+json.dump(out_t, open(os.path.join(os.path.dirname(out), "ncu_traffic.json"), "w"), indent=1)
 print("\n".join(lines))
