@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 
@@ -1629,6 +1630,12 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
     L.begin(K_RANSAC_SCORE, s);
     launch_pdl(k_score_fix_rows, 148, 256, 0, s, t);
     L.end(K_RANSAC_SCORE, s);
+    if (getenv("BT_SCORE_STATS")) {                                // dev aid (synchronizes): undecided tests
+      int32_t c[2] = {0, 0};
+      cudaStreamSynchronize(s);
+      cudaMemcpy(c, rs.fix_count, 8, cudaMemcpyDeviceToHost);
+      fprintf(stderr, "bt scoring: %d undecided tests, %d overflowed rows\n", c[0], c[1]);
+    }
   }
   FinishArgs f;
   f.kp = kp; f.pairs = pairs; f.uid = uid; f.matches = matches; f.n_matches = n_matches;
