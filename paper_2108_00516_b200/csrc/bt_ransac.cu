@@ -1610,6 +1610,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
     }
     t.pf = (PairFeat *)rs.pfeat; t.feat = (__half *)rs.feat; t.fix = (int2 *)rs.fix; t.ecount = rs.fix_count;
     t.elist = (int4 *)rs.elist; t.ecap = rs.ecap;
+    if (const char *ec = getenv("BT_SCORE_ECAP")) t.ecap = std::max(0, std::min(t.ecap, atoi(ec)));   // tests: overflow path
     static int tc_grid = 0;
     if (!tc_grid) {
       cudaFuncSetAttribute(k_score_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);

@@ -115,3 +115,20 @@ def test_score_tc_equals_fma_match_counts(bt, torch, M):
     out, _ = _run_both(bt, torch, ctx, sc, [(0, 1)], 2048, match_lists=[m])
     ctx.close()
     _assert_equal(out, f"M = {M}")
+
+
+def test_score_tc_list_overflow_recounts_rows(bt, torch):
+    """The safety net: with the undecided-test list capped at 50 entries (BT_SCORE_ECAP), rows
+    whose tests do not fit are recounted whole by k_score_fix_rows — counts still equal the
+    FFMA2 kernel's (C2, 24 pairs)."""
+    sc = synth.make_scene(16)
+    pairs = synth.all_pairs(16)[:24]
+    ctx = bt.Context(0)
+    ctx.reserve(len(pairs), sc.desc.shape[1], 4096, 16, 640, 480)
+    os.environ["BT_SCORE_ECAP"] = "50"
+    try:
+        out, _ = _run_both(bt, torch, ctx, sc, pairs, 4096)
+    finally:
+        os.environ.pop("BT_SCORE_ECAP", None)
+    ctx.close()
+    _assert_equal(out, "C2 subset, list capped at 50")
