@@ -47,9 +47,6 @@
 
 #include <algorithm>
 
-#ifndef BT_MATCH_WS
-#define BT_MATCH_WS 1
-#endif
 
 namespace bt {
 namespace {
@@ -91,14 +88,8 @@ k_desc_prep(KpView kp, MatchScratch S, int n_pad) {
     for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const float nrm = sqrtf(s);
     const float inv = nrm > 0.f ? 1.0f / nrm : 0.f;
-    if (i < n_pad) {
-      __half2 h01 = __floats2half2_rn(a[q].x * inv, a[q].y * inv), h23 = __floats2half2_rn(a[q].z * inv, a[q].w * inv);
-      uint2 packed;
-      packed.x = *reinterpret_cast<uint32_t *>(&h01);
-      packed.y = *reinterpret_cast<uint32_t *>(&h23);
-      reinterpret_cast<uint2 *>(S.desc16 + ((size_t)f * n_pad + i) * kDim)[lane] = packed;
-      if (lane == 0) S.norm[(size_t)f * n_pad + i] = nrm;
-    }
+    (void)inv;
+    if (i < n_pad && lane == 0) S.norm[(size_t)f * n_pad + i] = nrm;
     if (i < n) mx = max(mx, __float_as_uint(nrm));                 // nrm >= 0: bits are monotone
   }
   if (lane == 0) wmax[warp] = mx;
@@ -108,6 +99,42 @@ k_desc_prep(KpView kp, MatchScratch S, int n_pad) {
 #pragma unroll
     for (int w = 0; w < kWarpsPerBlock; ++w) m = max(m, wmax[w]);
     if (m) atomicMax(S.maxnorm + f, m);
+  }
+}
+
+// the frame's scale P_f = max_i |a_i| (1 for an empty / all-zero frame)
+__device__ __forceinline__ float frame_scale(unsigned maxbits) {
+  const float m = __uint_as_float(maxbits);
+  return m > 0.f ? m : 1.f;
+}
+
+// fp16 descriptors scaled by the frame's max norm: a / P_f (|a / P_f| <= 1; the fp32 scaling
+// adds 2^-24 to fp16's 2^-11), zero rows past n (the TMA source of k_match_ws)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_desc_half(KpView kp, MatchScratch S, int n_pad) {
+  pdl_wait();
+  const int f = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = (blockIdx.x * kWarpsPerBlock + warp) * kPrepPerWarp;
+  const int n = min(kp.n_kp[f], kp.n_max);
+  const float inv = 1.f / frame_scale(S.maxnorm[f]);
+  float4 a[kPrepPerWarp];
+#pragma unroll
+  for (int q = 0; q < kPrepPerWarp; ++q) {
+    const int i = i0 + q;
+    a[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < n) a[q] = __ldg(reinterpret_cast<const float4 *>(kp.desc + ((size_t)f * kp.n_max + i) * kDim) + lane);
+  }
+#pragma unroll
+  for (int q = 0; q < kPrepPerWarp; ++q) {
+    const int i = i0 + q;
+    if (i < n_pad) {
+      __half2 h01 = __floats2half2_rn(a[q].x * inv, a[q].y * inv), h23 = __floats2half2_rn(a[q].z * inv, a[q].w * inv);
+      uint2 packed;
+      packed.x = *reinterpret_cast<uint32_t *>(&h01);
+      packed.y = *reinterpret_cast<uint32_t *>(&h23);
+      reinterpret_cast<uint2 *>(S.desc16 + ((size_t)f * n_pad + i) * kDim)[lane] = packed;
+    }
   }
 }
 
@@ -121,18 +148,19 @@ struct TcArgs {
   int fs_batched;                              // undecided rows -> per-tile lists (k_fullscan), else queue 1
 };
 
-constexpr int kTcWarps = 8;                   // 2 warpgroups: each reads all 128 TMEM lanes, half the columns
 constexpr int kN = 128;                       // B columns per MMA chunk (N); B and TMEM double-buffered
-constexpr size_t kTcSmem = 1024 /*align*/ + 32768 /*A*/ + 2 * 32768 /*B x2*/;
 
 // certificate of a row's packed top-3 keys: 1 = the best is the nearest neighbour, 2 = it is
 // one of the top two, 0 = undecided.  A reference ranked >= L cannot be the nearest
 // neighbour when d'_(L) - d'_(1) > 2 eps + (truncated key bits).
-__device__ __forceinline__ int certify(unsigned k1, unsigned k2, unsigned k3, float qn, float mr, int ibits) {
+__device__ __forceinline__ int certify(unsigned k1, unsigned k2, unsigned k3, float qn, float mr, float pp, int ibits) {
   const unsigned imask = (1u << ibits) - 1u;
   if (k1 == kNone) return 0;
   if (k2 == kNone) return 1;
-  const float eps2 = 2.f * (2.2e-3f * qn * mr + 1e-6f * (qn * qn + mr * mr));
+  // |d_hat - d| <= 2.2e-3 |a||b| (fp16 rounding of a / P_a and b / P_b, fp32 accumulation)
+  //   + 1e-6 (|a|^2 + |b|^2) + 3e-6 P_a P_b (fp16 subnormals, the fp32 key evaluation around the
+  //   offset 2.01 P_a P_b)
+  const float eps2 = 2.f * (2.2e-3f * qn * mr + 1e-6f * (qn * qn + mr * mr) + 3e-6f * pp);
   const float v1 = key_value(k1 & ~imask);
   const float v2 = key_value(k2 & ~imask);
   // truncated key bits + the rounding of the offset sum: a few ulps of the values compared
@@ -141,204 +169,6 @@ __device__ __forceinline__ int certify(unsigned k1, unsigned k2, unsigned k3, fl
   const float v3 = key_value(k3 & ~imask);
   if ((v3 - v1) > eps2 + ldexpf(fabsf(v1) + fabsf(v3), ibits - 21) + 1e-30f) return 2;
   return 0;
-}
-
-// One CTA per (128-row tile, pair, direction).  Direction 0 ranks frame b for each row of
-// frame a, direction 1 frame a for each row of frame b (the Gram tile is recomputed on the
-// tensor cores instead of reducing columns across lanes).  Thread 0 drives TMA and MMA; the
-// other threads wait at CTA barriers, not on the mbarriers.
-__global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_constant__ CUtensorMap tmap, TcArgs A) {
-  pdl_wait();
-  extern __shared__ uint8_t tc_smem_raw[];
-  __shared__ __align__(8) uint64_t bar_load[2], bar_mma[2];
-  __shared__ uint32_t tmem_base_sh;
-  __shared__ __align__(16) float4 cconst[2 * kN];                  // [2][128] (-2|b_j|, |b_j|^2, j bits, 0)
-  __shared__ __align__(16) uint4 rmerge[128];
-  __shared__ int fs_warp[4];
-  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sA = base;                        // [2 K-atoms][128 rows][128 B]
-  uint8_t *sB = base + 32768;                // [2 buffers][2 K-atoms][128 rows][128 B]
-
-  const int dir = blockIdx.z, p = blockIdx.y, rt = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wg = warp >> 2;
-  const int fa = A.pairs[2 * p + dir], fb = A.pairs[2 * p + 1 - dir];
-  const int na = min(A.kp.n_kp[fa], A.kp.n_max), nb = min(A.kp.n_kp[fb], A.kp.n_max);
-  const int fs_tile = (dir * A.P + p) * gridDim.x + rt;           // this tile's full-scan list
-  if (rt * 128 >= na || nb == 0) {                                 // block-uniform
-    if (A.fs_batched && threadIdx.x == 0) A.S.fs_count[fs_tile] = 0;
-    return;
-  }
-  const int n_pad = A.n_pad;
-  const unsigned imask = (1u << A.ibits) - 1u;
-  const int nchunks = (nb + kN - 1) / kN;
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(2 * kN)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  // column constants of chunk c into buffer c & 1
-  auto stage_consts = [&](int c) {
-    for (int jj = tid; jj < kN; jj += kTcWarps * 32) {
-      const int j = c * kN + jj;
-      // a column past n_b ranks at +inf: it sorts after every real column (certify then sees
-      // v - v1 = inf, as for a missing key), so the loop needs no per-element bound check
-      const float v = j < nb ? A.S.norm[(size_t)fb * n_pad + j] : 0.f;
-      cconst[(c & 1) * kN + jj] = make_float4(-2.f * v, j < nb ? v * v : CUDART_INF_F, __uint_as_float((unsigned)j), 0.f);
-    }
-  };
-  auto load_b = [&](int c) {                                      // thread 0 only
-    mbar_expect_tx(&bar_load[c & 1], (c == 0 ? 32768u : 0u) + 32768u);
-    if (c == 0) {
-      tma_load_2d(sA, &tmap, 0, fa * n_pad + rt * 128, &bar_load[0]);
-      tma_load_2d(sA + 16384, &tmap, 64, fa * n_pad + rt * 128, &bar_load[0]);
-    }
-    uint8_t *dst = sB + (c & 1) * 32768;
-    tma_load_2d(dst, &tmap, 0, fb * n_pad + c * kN, &bar_load[c & 1]);
-    tma_load_2d(dst + 16384, &tmap, 64, fb * n_pad + c * kN, &bar_load[c & 1]);
-  };
-  if (tid == 0) {
-    mbar_init(&bar_load[0], 1); mbar_init(&bar_load[1], 1);
-    mbar_init(&bar_mma[0], 1); mbar_init(&bar_mma[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    load_b(0);
-    if (nchunks > 1) load_b(1);
-  }
-  stage_consts(0);
-  if (nchunks > 1) stage_consts(1);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_base_sh;
-
-  const int lrow = (warp & 3) * 32 + lane;                         // TMEM lane = tile row
-  const int i = rt * 128 + lrow;
-  const float na_n = A.S.norm[(size_t)fa * n_pad + i];
-  // |S_hat| <= 1 + 1e-3, so d' >= -2.002 |a| max|b|: the offset keeps every ranked value >= 0
-  const float c_row = 2.01f * na_n * __uint_as_float(A.S.maxnorm[fb]) + 1e-30f;
-  // rank by d' = d_hat - |a|^2 = |b|^2 - 2 |a||b| S (the row constant does not change the order);
-  // two independent top-3 sets (even / odd columns) halve the min/max dependency chain
-  unsigned r1 = kNone, r2 = kNone, r3 = kNone, s1 = kNone, s2 = kNone, s3 = kNone;
-  // instruction descriptor: D f32, A/B f16, K-major both, N = 128, M = 128
-  const uint32_t idesc = (1u << 4) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-
-  // software pipeline: MMA(c + 1) is issued before the epilogue of chunk c (two TMEM
-  // accumulators), TMA(c + 2) as soon as MMA(c) has consumed its B buffer
-  auto issue_mma = [&](int c) {                                   // thread 0 only
-    const int b = c & 1;
-    mbar_wait(&bar_load[b], (c >> 1) & 1);
-    tc_fence_after();
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {                                 // K = 128 = 8 x 16
-      const int kb = k >> 2, ks = k & 3;
-      umma_f16(tmem + b * kN, umma_desc_sw128(sA + kb * 16384 + ks * 32),
-               umma_desc_sw128(sB + b * 32768 + kb * 16384 + ks * 32), idesc, k > 0 ? 1u : 0u);
-    }
-    umma_commit(&bar_mma[b]);
-  };
-  if (tid == 0) issue_mma(0);
-  for (int c = 0; c < nchunks; ++c) {
-    const int buf = c & 1;
-    if (tid == 0) {
-      if (c + 1 < nchunks) issue_mma(c + 1);                      // TMEM buffer (c+1)&1 was drained last round
-      mbar_wait(&bar_mma[buf], (c >> 1) & 1);                     // chunk c accumulated, its B buffer consumed
-      if (c + 2 < nchunks) load_b(c + 2);                         // prefetch into the freed buffer
-      tc_fence_before();
-    }
-    __syncthreads();
-    tc_fence_after();
-    // ---- epilogue: warpgroup wg reads columns [wg*64, wg*64+64) of the chunk
-#pragma unroll 1
-    for (int cc = wg * 2; cc < wg * 2 + 2; ++cc) {
-      const int j0 = c * kN + cc * 32;
-      if (j0 >= nb) break;                                        // warpgroup-uniform
-      uint32_t v[32];
-      BT_TMEM_LD32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(buf * kN + cc * 32), v);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const float4 *cb = cconst + buf * kN + cc * 32;
-      // two keys per step merged into a sorted top-3 with 3-input min (VIMNMX3):
-      //   m = min(x, y), M = max(x, y);  r1' = min(r1, m);  r2' = min(r2, max(r1, m), M);
-      //   r3' = min(r3, max(r2, m), max(r1, M))  — 8 ops per 2 keys; the column index comes with
-      //   the column constants (shared-memory broadcast), so a key is one LOP3
-#pragma unroll
-      for (int col = 0; col < 32; col += 2) {
-        const float4 ca = cb[col], cbb = cb[col + 1];
-        // d'' = d' + c_row >= 0, so the float bits order like the values
-        const float d0 = __fadd_rn(__fmaf_rn(na_n * ca.x, __uint_as_float(v[col]), ca.y), c_row);
-        const float d1 = __fadd_rn(__fmaf_rn(na_n * cbb.x, __uint_as_float(v[col + 1]), cbb.y), c_row);
-        const unsigned k0 = (__float_as_uint(d0) & ~imask) | __float_as_uint(ca.z);
-        const unsigned k1 = (__float_as_uint(d1) & ~imask) | __float_as_uint(cbb.z);
-        const unsigned m = min(k0, k1), M = max(k0, k1);
-        if ((col & 2) == 0) {
-          const unsigned n3 = min(min(r3, max(r2, m)), max(r1, M)), n2 = min(min(r2, max(r1, m)), M);
-          r1 = min(r1, m); r2 = n2; r3 = n3;
-        } else {
-          const unsigned n3 = min(min(s3, max(s2, m)), max(s1, M)), n2 = min(min(s2, max(s1, m)), M);
-          s1 = min(s1, m); s2 = n2; s3 = n3;
-        }
-      }
-    }
-    tc_fence_before();
-    __syncthreads();                                              // TMEM buffer free for chunk c + 2
-    if (c + 2 < nchunks) stage_consts(c + 2);                     // this buffer's constants are spent
-  }
-  // merge the even/odd sets, then the two warpgroups' top-3; certify; decide the row or queue it
-  {
-    const unsigned ks[3] = {s1, s2, s3};
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const unsigned k = ks[t];
-      const unsigned n3 = min(r3, max(r2, k)), n2 = min(r2, max(r1, k));
-      r1 = min(r1, k); r2 = n2; r3 = n3;
-    }
-  }
-  if (wg == 1) rmerge[lrow] = make_uint4(r1, r2, r3, 0u);
-  __syncthreads();
-  int level = 1;
-  if (wg == 0 && i < na) {
-    const uint4 o = rmerge[lrow];
-    const unsigned ks[3] = {o.x, o.y, o.z};
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const unsigned k = ks[t];
-      const unsigned n3 = min(r3, max(r2, k)), n2 = min(r2, max(r1, k));
-      r1 = min(r1, k);
-      r2 = n2;
-      r3 = n3;
-    }
-    level = 0;
-    if (!A.force_fallback && A.ratio2 >= 1.f)
-      level = certify(r1, r2, r3, na_n, __uint_as_float(A.S.maxnorm[fb]), A.ibits);
-    const size_t o_nn = (size_t)p * A.kp.n_max + i;
-    if (level == 1) {
-      (dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o_nn] = (int32_t)(r1 & imask);
-      if (dir == 0) A.S.ratio_ok[o_nn] = 1;
-    } else if (level == 2 || !A.fs_batched) {                     // queue: [0] top-2 rescoring, [1] full scan
-      const int qi = level == 2 ? 0 : 1;
-      const unsigned slot = atomicAdd(A.S.work_count + qi, 1u);
-      A.S.work[(size_t)qi * A.S.work_cap + slot] = make_uint4((unsigned)dir | ((unsigned)i << 1), (unsigned)p, r1, r2);
-    }
-  }
-  // large reference sets: rows left undecided (level 0) are compacted in row order into this
-  // tile's list for the batched full scan (k_fullscan)
-  if (A.fs_batched && wg == 0) {
-    const bool fs = i < na && level == 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, fs);
-    if (lane == 0) fs_warp[warp] = __popc(bal);
-    asm volatile("bar.sync 1, 128;" ::: "memory");                // warpgroup 0 only
-    int off = 0;
-    for (int w = 0; w < warp; ++w) off += fs_warp[w];
-    if (fs) A.S.fs_rows[(size_t)fs_tile * 128 + off + __popc(bal & ((1u << lane) - 1u))] = i;
-    if (threadIdx.x == 0) A.S.fs_count[fs_tile] = fs_warp[0] + fs_warp[1] + fs_warp[2] + fs_warp[3];
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kN) : "memory");
-  }
 }
 
 // ---------------------------------------------------------------- persistent, warp-specialized
@@ -357,7 +187,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) k_match_tc(const __grid_cons
 // phases ahead of its waiter (each is gated by the other side), so parity waits are exact.
 constexpr int kWsEpiWarps = 8;
 constexpr int kWsThreads = (kWsEpiWarps + 1) * 32;
-constexpr size_t kWsSmem = 1024 /*align*/ + 32768 /*A*/ + 2 * 32768 /*B x2*/ + 2 * kN * 16 /*consts x2*/;
+constexpr size_t kWsSmem = 1024 /*align*/ + 32768 /*A*/ + 2 * 32768 /*B x2*/ + 2 * kN * 8 /*consts x2*/;
 
 
 struct TcItem {
@@ -391,7 +221,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = base;                                           // [2 K-atoms][128 rows][128 B]
   uint8_t *sB = base + 32768;                                   // [2 buffers][2 K-atoms][128 rows][128 B]
-  float4 *cconst = reinterpret_cast<float4 *>(base + 3 * 32768);  // [2][kN] (-2|b_j|, |b_j|^2, j bits, 0)
+  float2 *cconst = reinterpret_cast<float2 *>(base + 3 * 32768);  // [2][kN] (|b_j|^2 + 2.01 P_a P_b, j bits)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_pad = A.n_pad;
   const int n_items = 2 * A.P * (n_pad / 128);
@@ -434,6 +264,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
       In.skip = true;
       if (itn < n_items) In = tc_item(A, itn);
       if (!I.skip) {
+        const float coff = 2.01f * frame_scale(A.S.maxnorm[I.fa]) * frame_scale(A.S.maxnorm[I.fb]);
         for (int c = 0; c < I.nchunks; ++c, ++g) {
           const int b = g & 1;
           if (!nv_ok) {
@@ -460,9 +291,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
 #pragma unroll
           for (int q = 0; q < kN / 32; ++q) {
             const int jj = q * 32 + lane, j = c * kN + jj;
-            // a column past n_b ranks at +inf (no per-element bound check in the epilogue)
-            cconst[b * kN + jj] = make_float4(-2.f * nv[q], j < I.nb ? nv[q] * nv[q] : CUDART_INF_F,
-                                              __uint_as_float((unsigned)j), 0.f);
+            // |b_j|^2 + the offset that keeps every ranked value >= 0; a column past n_b ranks at
+            // +inf (no per-element bound check in the epilogue)
+            cconst[b * kN + jj] = make_float2(j < I.nb ? __fmaf_rn(nv[q], nv[q], coff) : CUDART_INF_F,
+                                              __uint_as_float((unsigned)j));
           }
           __syncwarp();
           if (lane == 0) {
@@ -504,25 +336,29 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
     int it = blockIdx.x;
     TcItem In;
     float na_nx = 0.f, mr_nx = 0.f;                               // the next item's row norm / max |b|
+    unsigned ma_nx = 0u, mb_nx = 0u;                              // max-norm bits of its frames
     if (it < n_items) {
       In = tc_item(A, it);
       na_nx = A.S.norm[(size_t)In.fa * n_pad + In.rt * 128 + lrow];
-      mr_nx = __uint_as_float(A.S.maxnorm[In.fb]);
+      ma_nx = A.S.maxnorm[In.fa]; mb_nx = A.S.maxnorm[In.fb];
+      mr_nx = __uint_as_float(mb_nx);
     }
     for (; it < n_items; it += gridDim.x) {
       const TcItem I = In;
       const float na_n = na_nx, mr = mr_nx;
+      // S'' = (a / P_a).(b / P_b): d' = |b|^2 - 2 P_a P_b S''
+      const float pp = frame_scale(ma_nx) * frame_scale(mb_nx), kscale = -2.f * pp;
       if (it + (int)gridDim.x < n_items) {                        // prefetch the next item
         In = tc_item(A, it + gridDim.x);
         na_nx = A.S.norm[(size_t)In.fa * n_pad + In.rt * 128 + lrow];
-        mr_nx = __uint_as_float(A.S.maxnorm[In.fb]);
+        ma_nx = A.S.maxnorm[In.fa]; mb_nx = A.S.maxnorm[In.fb];
+        mr_nx = __uint_as_float(mb_nx);
       }
       if (I.skip) {
         if (A.fs_batched && tid == 0) A.S.fs_count[it] = 0;
         continue;
       }
       const int i = I.rt * 128 + lrow;
-      const float c_row = 2.01f * na_n * mr + 1e-30f;
       unsigned r1 = kNone, r2 = kNone, r3 = kNone, s1 = kNone, s2 = kNone, s3 = kNone;
       for (int c = 0; c < I.nchunks; ++c, ++g) {
         const int b = g & 1;
@@ -536,14 +372,15 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
           uint32_t v[32];
           BT_TMEM_LD32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(b * kN + cc * 32), v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          const float4 *cb = cconst + b * kN + cc * 32;
+          const float4 *cb = reinterpret_cast<const float4 *>(cconst + b * kN + cc * 32);   // 2 columns per load
 #pragma unroll
           for (int col = 0; col < 32; col += 2) {
-            const float4 ca = cb[col], cbb = cb[col + 1];
-            const float d0 = __fadd_rn(__fmaf_rn(na_n * ca.x, __uint_as_float(v[col]), ca.y), c_row);
-            const float d1 = __fadd_rn(__fmaf_rn(na_n * cbb.x, __uint_as_float(v[col + 1]), cbb.y), c_row);
-            const unsigned k0 = (__float_as_uint(d0) & ~imask) | __float_as_uint(ca.z);
-            const unsigned k1 = (__float_as_uint(d1) & ~imask) | __float_as_uint(cbb.z);
+            const float4 cc2 = cb[col >> 1];
+            // d'' = d' + 2.01 P_a P_b >= 0 (one FFMA), so the float bits order like the values
+            const float d0 = __fmaf_rn(kscale, __uint_as_float(v[col]), cc2.x);
+            const float d1 = __fmaf_rn(kscale, __uint_as_float(v[col + 1]), cc2.z);
+            const unsigned k0 = (__float_as_uint(d0) & ~imask) | __float_as_uint(cc2.y);
+            const unsigned k1 = (__float_as_uint(d1) & ~imask) | __float_as_uint(cc2.w);
             const unsigned m = min(k0, k1), M = max(k0, k1);
             if ((col & 2) == 0) {
               const unsigned n3 = min(min(r3, max(r2, m)), max(r1, M)), n2 = min(min(r2, max(r1, m)), M);
@@ -583,7 +420,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
         }
         level = 0;
         if (!A.force_fallback && A.ratio2 >= 1.f)
-          level = certify(r1, r2, r3, na_n, mr, A.ibits);
+          level = certify(r1, r2, r3, na_n, mr, pp, A.ibits);
         const size_t o_nn = (size_t)I.p * A.kp.n_max + i;
         if (level == 1) {
           (I.dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o_nn] = (int32_t)(r1 & imask);
@@ -1016,14 +853,13 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   const int n_pad = match_n_pad(kp.n_max);
   const int rt_count = n_pad / 128;
   const int ibits = ceil_log2(n_pad);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_match_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-    attr = true;
-  }
   L.begin(K_DESC_PREP, s);
   constexpr int per_cta = kWarpsPerBlock * kPrepPerWarp;
   launch_pdl(k_desc_prep, dim3((n_pad + per_cta - 1) / per_cta, kp.n_frames), kWarpsPerBlock * 32, 0, s, kp, S,
+             n_pad);
+  L.end(K_DESC_PREP, s);
+  L.begin(K_DESC_PREP, s);
+  launch_pdl(k_desc_half, dim3((n_pad + per_cta - 1) / per_cta, kp.n_frames), kWarpsPerBlock * 32, 0, s, kp, S,
              n_pad);
   L.end(K_DESC_PREP, s);
   const float ratio2 = ratio >= 1.f ? 1.f : ratio * ratio;
@@ -1032,24 +868,19 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   const int fs_batched = kp.n_max >= kFsBatchRefs ? 1 : 0;
   TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2, fs_batched};
   L.begin(K_MATCH_TC, s);
-#if BT_MATCH_WS
   static int ws_grid = 0;
   if (ws_grid == 0) {
     cudaFuncSetAttribute(k_match_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsSmem);
-    int dev = 0, sms = 0, per_sm = 0;
+    int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // two CTAs per SM by design (2 x 108 KB of shared memory, 2 x 256 TMEM columns, 96 registers;
     // ncu: block limits 2 / 2); the occupancy API reports 1 for this configuration, so the grid
     // is sized directly (a CTA that does not fit only waits: no CTA depends on another)
     cudaFuncSetAttribute(k_match_ws, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    (void)per_sm;
     ws_grid = sms * 2;
   }
   launch_pdl(k_match_ws, std::min(ws_grid, 2 * P * rt_count), kWsThreads, kWsSmem, s, *tmap, ta);
-#else
-  launch_pdl(k_match_tc, dim3(rt_count, P, 2), kTcWarps * 32, kTcSmem, s, *tmap, ta);
-#endif
   L.end(K_MATCH_TC, s);
   L.begin(K_RESOLVE, s);
   RescoreArgs ra{kp, pairs, S, ibits, ratio2};
