@@ -261,16 +261,6 @@ __device__ __forceinline__ void prep_tile(const DenseArgs &A, const int f, const
   if (threadIdx.x == 0) A.counts[(size_t)f * A.tiles + t] = total;
 }
 
-#ifndef BT_PREP_LIST
-#define BT_PREP_LIST 1
-#endif
-// one CTA per (tile, frame) (no mask pre-pass)
-__global__ void __launch_bounds__(kDenseThreads) k_dense_prep_grid(DenseArgs A) {
-  pdl_wait();
-  __shared__ int wsum[kDenseThreads / 32];
-  prep_tile(A, blockIdx.y, blockIdx.x, wsum);
-}
-
 // persistent: the CTAs drain the list of masked tiles written by k_dense_mask
 __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
   pdl_wait();
@@ -677,10 +667,6 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   launch_pdl(k_edge_setup, mp.n_frames + (E + 255) / 256, 256, 0, s, a);
   L.end(K_DENSE_PREP, s);
   L.begin(K_DENSE_PREP, s);
-#if !BT_PREP_LIST
-  launch_pdl(k_dense_prep_grid, dim3(a.tiles, mp.n_frames), kDenseThreads, 0, s, a);
-  L.end(K_DENSE_PREP, s);
-#else
   launch_pdl(k_dense_mask, dim3((a.tiles + kDenseThreads / 32 - 1) / (kDenseThreads / 32), mp.n_frames),
              kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);
@@ -695,7 +681,6 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   }
   launch_pdl(k_dense_prep, std::min(prep_grid, a.tiles * mp.n_frames), kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);
-#endif
   L.begin(K_DENSE_PREP, s);
   launch_pdl(k_dense_scan, mp.n_frames, kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);

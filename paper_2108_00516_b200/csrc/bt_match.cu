@@ -46,6 +46,8 @@
 #include "bt_tc.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 
 namespace bt {
@@ -897,6 +899,12 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   }
   launch_pdl(k_rescore, dim3(2 * 148, 2), kWarpsPerBlock * 32, 0, s, ra);
   L.end(K_RESOLVE, s);
+  if (getenv("BT_MATCH_STATS")) {                                 // dev aid (synchronizes): queue sizes
+    unsigned c[2] = {0, 0};
+    cudaStreamSynchronize(s);
+    cudaMemcpy(c, S.work_count, 8, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "bt matching: %u rows top-2 rescored, %u rows full-scanned\n", c[0], c[1]);
+  }
   L.begin(K_MUTUAL, s);
   launch_pdl(k_mutual, P, 512, 0, s, kp, pairs, (const int32_t *)S.nn_ab, (const int32_t *)S.nn_ba,
              (const uint8_t *)S.ratio_ok, matches, n_matches, S);
