@@ -94,7 +94,7 @@ for k, v in tot.most_common():
 # NEXT-row sections, which reuse the dense kernels): split the list into maximal runs of step
 # kernels (the L2 flush between steps and every other kernel end a run) and keep the runs that
 # hold whole steps (as many k_dense as scoring launches, at least one)
-STEP = {"k_desc_prep", "k_match_tc", "k_match_ws", "k_fullscan", "k_rescore", "k_mutual", "k_ransac_hyp",
+STEP = {"k_desc_prep", "k_desc_half", "k_match_tc", "k_match_ws", "k_fullscan", "k_rescore", "k_mutual", "k_ransac_hyp",
         "k_ransac_score", "k_corr_feat", "k_score_tc", "k_score_fix", "k_score_fix_rows", "k_ransac_finish",
         "k_edge_setup", "k_dense_mask", "k_dense_prep", "k_dense_scan", "k_dense", "k_dense_reduce"}
 stot, scnt, n_steps = collections.Counter(), collections.Counter(), 0
