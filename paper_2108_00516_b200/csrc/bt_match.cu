@@ -4,36 +4,37 @@
 // output ascending in i.  The result is the EXACT brute-force one; the tensor cores only
 // prune candidates under a proven error bound.
 //
-//  k_desc_prep   per frame and keypoint: |a| (fp32) and the unit descriptor a/|a| in fp16
-//                ([F][n_pad][128], zero padded), plus the frame's max |a| (certificate).
-//  k_match_tc    one CTA per (128-row tile, pair, direction a->b / b->a).  TMA (128B-swizzled
-//                boxes of 64 x 128 fp16) stages the A tile once and B in 128-column chunks,
-//                double buffered (the next chunk's TMA overlaps this chunk's epilogue); one
-//                thread issues tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = 128, K = 8 x 16)
-//                into one of two 128-column fp32 TMEM accumulators, S = A_hat . B_hat^T; two
-//                warpgroups read TMEM with tcgen05.ld (row = TMEM lane, each warpgroup half the
-//                columns), rank d' = |b|^2 - 2 |a||b| S (= d_hat - |a|^2) and keep the three
-//                smallest as packed (order-preserving value | index) keys, merging two keys per
-//                step with 3-input mins (8 ops per 2 keys; columns past n_b rank at +inf: no
-//                per-element bound check; the column index rides with the column constants).
-//                Both directions recompute the tile on the tensor cores rather than reducing
-//                columns across lanes.  The epilogue certifies each row (below) and decides it,
-//                queues it for top-2 rescoring, or lists it in the tile's full-scan list.
+//  k_desc_prep   per frame and keypoint: |a| (fp32) and the frame's max |a| = M_f.
+//  k_desc_half   a / M_f in fp16 ([F][n_pad][128], zero padded; |a / M_f| <= 1).
+//  k_match_ws    persistent, warp-specialized (2 CTAs per SM) over the items (128-row tile,
+//                pair, direction a->b / b->a): a producer warp issues the TMA (128B-swizzled
+//                boxes of 64 x 128 fp16) of the A tile once per item and of B in 128-column
+//                chunks (double buffered), stages each chunk's column constants and issues
+//                tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = 128, K = 8 x 16) into one of two
+//                128-column fp32 TMEM accumulators, S'' = (A / M_a) . (B / M_b)^T; 8 epilogue
+//                warps (two warpgroups, half the columns each) read TMEM with tcgen05.ld, rank
+//                d' = |b|^2 - 2 M_a M_b S'' (= d_hat - |a|^2; one FFMA with the per-column
+//                |b|^2 + 2.01 M_a M_b) and keep the three smallest as packed (order-preserving
+//                value | index) keys, merging two keys per step with 3-input mins (columns past
+//                n_b rank at +inf: no per-element bound check).  Both directions recompute the
+//                tile on the tensor cores rather than reducing columns across lanes.  The
+//                epilogue certifies each row (below) and decides it, queues it for top-2
+//                rescoring, or lists it in the item's full-scan list.
 //  certificate   With the bound
-//                eps = 2.2e-3 |a||b|max + 1e-6 (|a|^2 + |b|max^2) (+ key truncation) — fp16 unit
-//                vectors have relative error 2^-11 per element, so |S_hat - S| <= 2^-10 +
-//                128 * 2^-23 (fp32 accumulation, any rounding mode) ~ 1.0e-3 and
-//                |d_hat - d| <= 2.0e-3 |a||b| + fp32 evaluation error — a reference ranked at
-//                position >= L cannot be the nearest neighbour when d'_(L) - d'_(1) > 2 eps:
-//                L = 2 certifies the best candidate; L = 3 leaves the top two, rescored exactly
-//                in fp32; otherwise (ties, ratio test, BT_FORCE_FALLBACK) the row is rescanned
-//                exactly over all references, batched per row tile by k_fullscan (the same
-//                summation tree as the top-2 rescoring, bit for bit).
+//                eps = 2.2e-3 |a| M_b + 1e-6 (|a|^2 + M_b^2) + 3e-6 M_a M_b (+ key truncation) —
+//                fp16 elements of a / M_a have relative error 2^-11, so |S_hat - S''| <= (2^-10 +
+//                128 * 2^-23) |a||b| / (M_a M_b) (fp32 accumulation, any rounding mode) and
+//                |d_hat - d| <= 2.0e-3 |a||b| + subnormal and fp32 evaluation terms — a reference
+//                ranked at position >= L cannot be the nearest neighbour when d'_(L) - d'_(1) >
+//                2 eps: L = 2 certifies the best candidate; L = 3 leaves the top two, rescored
+//                exactly in fp32; otherwise (ties, ratio test, BT_FORCE_FALLBACK) the row is
+//                rescanned exactly over all references, batched per row tile by k_fullscan (the
+//                same summation tree as the top-2 rescoring, bit for bit).
 //  k_rescore     blockIdx.y 0: warps over the top-2 queue (two exact distances per row);
 //                1: CTAs over the full-scan queue (one row per CTA, references split over 8
 //                warps) — used when n_max < 1024.
 //  k_fullscan    n_max >= 1024: per (pair, direction) its undecided rows, compacted per row
-//                tile by k_match_tc, in groups of 32 against all references (chunks of 64)
+//                tile by k_match_ws, in groups of 32 against all references (chunks of 64)
 //                staged in shared memory, 8 exact distances per thread (a reference is read
 //                once per 32 rows instead of once per row); few rows: one row per CTA.
 //  k_mutual      keep (i, NN_ab(i)) iff NN_ba(NN_ab(i)) == i (+ ratio flag), compact ascending.
