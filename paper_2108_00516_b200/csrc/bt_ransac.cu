@@ -278,7 +278,10 @@ struct ScoreArgs {
 // initialised to 0, or to a very negative value when degenerate (it stays < 0 whatever the
 // scoring adds — degenerate hypotheses never pass the distance gate anyway).
 constexpr int kHypThreads = 256;
-constexpr int kHypIter = 8;                                       // hypotheses per thread (loop)
+#ifndef BT_HYP_ITER
+#define BT_HYP_ITER 8
+#endif
+constexpr int kHypIter = BT_HYP_ITER;                             // hypotheses per thread (loop)
 
 // One CTA = kHypThreads x kHypIter hypotheses of one pair.  The pair's matched points are first
 // staged in shared memory (match list, then a_m / b_m), then one thread per hypothesis per

@@ -121,6 +121,25 @@ def test_match_edge_cases(bt, torch, ctx):
     assert got[9].tolist() == [[i, i] for i in range(512)]
 
 
+def test_match_unnormalized_descriptor_norms(bt, torch, ctx):
+    """Raw descriptors whose norms span 1e-3 .. 1e2 inside a frame (the fp16 operands are
+    a / max|a| of the frame, so small-norm rows reach fp16's subnormal range): match lists
+    still equal brute force — the certificate sends what it cannot decide to the exact scan."""
+    rng = np.random.default_rng(77)
+    sc = _custom_scene([400, 380], seed=77)
+    for f in range(2):
+        n = sc.n_kp[f]
+        scale = 10.0 ** rng.uniform(-3, 2, size=(n, 1))
+        sc.desc[f, :n] *= scale.astype(np.float32)
+    sc.desc[1, :380] = sc.desc[0, :380] * np.float32(1.0) + rng.normal(scale=1e-3, size=(380, 128)).astype(np.float32) * np.abs(sc.desc[0, :380]).max(1, keepdims=True)
+    pairs = [(0, 1), (1, 0)]
+    got, _, _ = gpu_match(bt, torch, ctx, sc, pairs)
+    for p, (a, b) in enumerate(pairs):
+        o = oracle.match(sc.desc[a, :sc.n_kp[a]], sc.desc[b, :sc.n_kp[b]])
+        parity.compare_matches(got[p], o)
+    assert len(got[0]) > 300
+
+
 # -------------------------------------------------------------------------------- RANSAC
 def gpu_ransac(bt, torch, ctx, scene, pairs, match_lists, n_hyp, uids=None, seed=SEED):
     fb = bt.FrameBatch.from_scene(scene)

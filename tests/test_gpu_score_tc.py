@@ -132,3 +132,33 @@ def test_score_tc_list_overflow_recounts_rows(bt, torch):
         os.environ.pop("BT_SCORE_ECAP", None)
     ctx.close()
     _assert_equal(out, "C2 subset, list capped at 50")
+
+
+@pytest.mark.parametrize("scale,shift", [(10.0, 0.0), (0.05, 0.0), (1.0, 3.0)])
+def test_score_tc_equals_fma_scaled_scenes(bt, torch, scale, shift):
+    """Object size x10 (1.2 m) and x0.05 (6 mm, below the 5 mm gate's scale), and a scene 3 m
+    away: the per-pair feature scales and the per-row certificate adapt; counts equal the
+    FFMA2 kernel's."""
+    rng = np.random.default_rng(int(scale * 100 + shift))
+    M = 600
+    pa, na, pb, nb, R, t, inl = synth.make_correspondences(rng, M, 0.4, noise=0.0005)
+    ca = pa.mean(0)
+    pa = ((pa - ca) * scale + ca + [0, 0, shift]).astype(np.float32)
+    pb = ((pb - ca) * scale + ca + [0, 0, shift]).astype(np.float32)
+    n_max = 1024
+    sc = synth.make_scene(2, render_maps=False, seed=5)
+    pts = np.zeros((2, n_max, 3), np.float32)
+    nrm = np.zeros((2, n_max, 3), np.float32)
+    nrm[:, :, 2] = -1.0
+    pts[:, :, 2] = 0.5
+    pts[0, :M], nrm[0, :M], pts[1, :M], nrm[1, :M] = pa, na, pb, nb
+    sc.pts, sc.nrm = pts, nrm
+    sc.desc = np.zeros((2, n_max, 128), np.float32)
+    sc.n_kp = np.array([M, M], np.int32)
+    sc.depth = sc.normal = sc.mask = None
+    m = np.stack([np.arange(M), np.arange(M)], 1).astype(np.int32)
+    ctx = bt.Context(0)
+    ctx.reserve(1, n_max, 4096, 2, 0, 0)
+    out, _ = _run_both(bt, torch, ctx, sc, [(0, 1)], 4096, match_lists=[m])
+    ctx.close()
+    _assert_equal(out, f"scale {scale}, shift {shift}")
