@@ -347,7 +347,7 @@ def main():
     add("k_ransac_score", "alu", tests * FLOPS_TEST, "TFLOP/s", fp32_peak_tflops,
         f"{FLOPS_TEST} flop per (hypothesis, correspondence) test (SURVEY 8(d)); {tests} tests; measured on "
         "the scoring stage as launched: k_corr_feat + k_score_tc (tcgen05 fp16 hi/lo contractions + "
-        "FMA/ALU epilogue, DESIGN.md R27) + k_score_fix (+ k_score_fix_rows), or the FFMA2 kernel with "
+        "FMA/ALU epilogue, DESIGN.md R27) + k_score_fix, or the FFMA2 kernel with "
         "BT_SCORE_FMA=1; peak = the FP32 FMA pipe of the direct formulation")
     if "k_ransac_score" in kern and not os.environ.get("BT_SCORE_FMA") == "1":
         # the same stage seen as tensor work: 6 MMAs x 16 K x 2 flop per (hypothesis row,

@@ -113,6 +113,7 @@ struct RansacScratch {
   void *fix;                   // [P * H] (p, h) rows recounted whole (undecided-list overflow)
   void *elist;                 // [P * H] (p, h, m) undecided tests, evaluated by k_score_fix
   int ecap;
+  uint32_t *ofl;               // [P][ceil(H / 32)] rows recounted whole (bitmap)
   int32_t *fix_count;          // [2]: undecided tests, overflowed rows
   int m_pad;
   const CUtensorMap *fmap;     // TMA view of feat: [P * m_pad][64] fp16, 64 x 128 boxes, 128B swizzle

@@ -1005,6 +1005,7 @@ struct ScoreTcArgs {
   int32_t *ecount;                           // [2]: undecided tests, overflowed rows
   int ecap;
   int2 *fix;                                 // rows whose tests overflowed elist: recounted whole
+  uint32_t *ofl;                             // [P][ceil(H / 32)] bit = row in fix (cleared by k_corr_feat)
 };
 
 __device__ __forceinline__ void split_half(double x, __half &hi, __half &lo) {
@@ -1064,6 +1065,7 @@ __global__ void __launch_bounds__(kFeatThreads) k_corr_feat(ScoreTcArgs A) {
   __shared__ float red[26][32];
   const int p = blockIdx.x, tid = threadIdx.x;
   if (p == 0 && tid < 2) A.ecount[tid] = 0;
+  for (int w = tid, nw = (A.n_hyp + 31) / 32; w < nw; w += kFeatThreads) A.ofl[(size_t)p * nw + w] = 0u;
   const int M = A.n_matches[p];
   PairFeat *pf = A.pf + p;
   if (tid == 0) pf->M = M;
@@ -1453,7 +1455,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
       const int h = ht * kTcRows + lrow;
       if (h < A.n_hyp && rc.valid) {
         if (cert) atomicAdd(A.counts + (size_t)p * A.n_hyp + h, (int)cert);
-        if (overflow) A.fix[atomicAdd(A.ecount + 1, 1)] = make_int2(p, h);
+        if (overflow) {
+          atomicOr(A.ofl + (size_t)p * ((A.n_hyp + 31) / 32) + (h >> 5), 1u << (h & 31));
+          A.fix[atomicAdd(A.ecount + 1, 1)] = make_int2(p, h);
+        }
       }
       it = itn;
       ++k;
@@ -1467,14 +1472,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
   }
 }
 
-// the undecided tests, one thread each, with the fp32 formula of the finish kernel (the
-// tensor-core count holds the certain inliers; an undecided test that passes adds one)
+// The undecided tests, one thread each, with the fp32 formula of the finish kernel (the
+// tensor-core count holds the certain inliers; an undecided test that passes adds one) — and
+// the safety net, never taken at the configured list capacity: rows whose undecided tests did
+// not all fit the list are recounted whole (warp per row) and their listed tests skipped.
 __global__ void __launch_bounds__(256) k_score_fix(ScoreTcArgs A) {
   pdl_wait();
-  const int n = min(A.ecount[0], A.ecap);
+  const int n = min(A.ecount[0], A.ecap), nrow = A.ecount[1];
+  const int nw = (A.n_hyp + 31) / 32;
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < n; w += gridDim.x * blockDim.x) {
     const int4 e = A.elist[w];
     const int p = e.x, h = e.y, m = e.z;
+    if (nrow && (A.ofl[(size_t)p * nw + (h >> 5)] >> (h & 31)) & 1u) continue;   // recounted below
     float T[12];
     load_T(A, p, h, T);
     const int fa = A.pairs[2 * p], fb = A.pairs[2 * p + 1];
@@ -1485,15 +1494,8 @@ __global__ void __launch_bounds__(256) k_score_fix(ScoreTcArgs A) {
               A.kp.pts + ((size_t)fb * A.kp.n_max + j) * 3, A.kp.nrm + ((size_t)fb * A.kp.n_max + j) * 3, q0, q1, q2, q3);
     if (inlier(T, q0, q1, q2, q3, A.ndelta2, A.ncosa)) atomicAdd(A.counts + (size_t)p * A.n_hyp + h, 1);
   }
-}
-
-// safety net (never taken at the configured capacity): rows whose undecided tests did not fit
-// the list are recounted whole, after k_score_fix (warp per row)
-__global__ void __launch_bounds__(256) k_score_fix_rows(ScoreTcArgs A) {
-  pdl_wait();
   const int lane = threadIdx.x & 31;
-  const int n = A.ecount[1];
-  for (int w = blockIdx.x * 8 + (threadIdx.x >> 5); w < n; w += gridDim.x * 8) {
+  for (int w = blockIdx.x * 8 + (threadIdx.x >> 5); w < nrow; w += gridDim.x * 8) {
     const int2 ph = A.fix[w];
     const int p = ph.x, h = ph.y;
     float T[12];
@@ -1532,7 +1534,8 @@ int score_chunk() { return kTcCols; }
 size_t ransac_scratch_bytes(int max_pairs, int max_hyp, int n_max) {
   return al256(hyp_slots(max_pairs, max_hyp) * 48) + al256((size_t)max_pairs * max_hyp * 4) + 256 +
          al256((size_t)max_pairs * score_m_pad(n_max) * kTcFeat * 2) + al256((size_t)max_pairs * sizeof(PairFeat)) +
-         al256((size_t)max_pairs * max_hyp * 8) + al256((size_t)max_pairs * max_hyp * 16) + 256;
+         al256((size_t)max_pairs * max_hyp * 8) + al256((size_t)max_pairs * max_hyp * 16) +
+         al256((size_t)max_pairs * ((max_hyp + 31) / 32) * 4) + 256;
 }
 
 RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp, int n_max) {
@@ -1546,6 +1549,7 @@ RansacScratch carve_ransac_scratch(void *scratch, int max_pairs, int max_hyp, in
   r.fix = c;                      c += al256((size_t)max_pairs * max_hyp * 8);
   r.elist = c;                    c += al256((size_t)max_pairs * max_hyp * 16);
   r.ecap = (int)std::min<size_t>((size_t)max_pairs * max_hyp, 0x7fffffff);
+  r.ofl = (uint32_t *)c;          c += al256((size_t)max_pairs * ((max_hyp + 31) / 32) * 4);
   r.fix_count = (int32_t *)c;
   r.m_pad = score_m_pad(n_max);
   r.fmap = nullptr;
@@ -1612,7 +1616,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
       t.sc.k2 = (float)(40.0 * 0x1p-24 + 0x1p-22 * (1.0 + std::fabs((double)a.ncosa)));
     }
     t.pf = (PairFeat *)rs.pfeat; t.feat = (__half *)rs.feat; t.fix = (int2 *)rs.fix; t.ecount = rs.fix_count;
-    t.elist = (int4 *)rs.elist; t.ecap = rs.ecap;
+    t.elist = (int4 *)rs.elist; t.ecap = rs.ecap; t.ofl = rs.ofl;
     if (const char *ec = getenv("BT_SCORE_ECAP")) t.ecap = std::max(0, std::min(t.ecap, atoi(ec)));   // tests: overflow path
     static int tc_grid = 0;
     if (!tc_grid) {
@@ -1630,9 +1634,6 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
     L.end(K_RANSAC_SCORE, s);
     L.begin(K_RANSAC_SCORE, s);
     launch_pdl(k_score_fix, 148, 256, 0, s, t);
-    L.end(K_RANSAC_SCORE, s);
-    L.begin(K_RANSAC_SCORE, s);
-    launch_pdl(k_score_fix_rows, 148, 256, 0, s, t);
     L.end(K_RANSAC_SCORE, s);
     if (getenv("BT_SCORE_STATS")) {                                // dev aid (synchronizes): undecided tests
       int32_t c[2] = {0, 0};

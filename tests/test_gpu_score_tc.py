@@ -119,7 +119,7 @@ def test_score_tc_equals_fma_match_counts(bt, torch, M):
 
 def test_score_tc_list_overflow_recounts_rows(bt, torch):
     """The safety net: with the undecided-test list capped at 50 entries (BT_SCORE_ECAP), rows
-    whose tests do not fit are recounted whole by k_score_fix_rows — counts still equal the
+    whose tests do not fit are recounted whole by k_score_fix — counts still equal the
     FFMA2 kernel's (C2, 24 pairs)."""
     sc = synth.make_scene(16)
     pairs = synth.all_pairs(16)[:24]
