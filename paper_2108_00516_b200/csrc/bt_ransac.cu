@@ -1008,19 +1008,6 @@ struct ScoreTcArgs {
   uint32_t *ofl;                             // [P][ceil(H / 32)] bit = row in fix (cleared by k_corr_feat)
 };
 
-__device__ __forceinline__ void split_half(double x, __half &hi, __half &lo) {
-  hi = __float2half_rn((float)x);
-  lo = __float2half_rn((float)(x - (double)__half2float(hi)));
-}
-__device__ __forceinline__ float round_up_pos(double x) { return __double2float_ru(x); }
-
-// Y1 of a correspondence: [2 a', -2 vec(b' a'^T), -2 b', |a'|^2 + |b'|^2] (X1 = [R^T t', vec R, t', 1])
-__device__ __forceinline__ void corr_y1(const double *ap, const double *bp, double *y1) {
-  for (int k = 0; k < 3; ++k) { y1[k] = 2.0 * ap[k]; y1[12 + k] = -2.0 * bp[k]; }
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) y1[3 + 3 * i + j] = -2.0 * bp[i] * ap[j];
-  y1[15] = ap[0] * ap[0] + ap[1] * ap[1] + ap[2] * ap[2] + bp[0] * bp[0] + bp[1] * bp[1] + bp[2] * bp[2];
-}
 
 // One CTA per pair (512 threads, fp32): pass 1 gathers the pair's correspondences (kept in
 // registers for the first 512) and reduces the centroids and max |a|, |b|; pass 2 forms the
@@ -1029,6 +1016,7 @@ __device__ __forceinline__ void corr_y1(const double *ap, const double *bp, doub
 // distance threshold, Y2 = 0).  The centroid need not be exact — any centring is algebraically
 // exact; fp32 feature rounding (2^-24) is inside the certificate's 2^-22 feature term.
 constexpr int kFeatThreads = 512;
+// Y1 of a correspondence: [2 a', -2 vec(b' a'^T), -2 b', |a'|^2 + |b'|^2] (X1 = [R^T t', vec R, t', 1])
 __device__ __forceinline__ void corr_y1f(const float *ap, const float *bp, float *y1) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) { y1[k] = 2.f * ap[k]; y1[12 + k] = -2.f * bp[k]; }
