@@ -188,7 +188,7 @@ def make_scene(n_frames: int, n: int = 500, n_max: int = 512, width: int = 640, 
                seed: int = DATA_SEED, outlier_frac: float = 0.16, pool_size: int = 2000,
                desc_noise: float = 0.03, point_noise: float = 0.0, distance: float = 0.5,
                cone_deg: float = 60.0, min_geodesic_deg: float = 10.0, render_maps: bool = True,
-               focal: float = 600.0) -> Scene:
+               focal: float = 600.0, poses=None) -> Scene:
     """BundleTrack-shaped multi-view scene: node poses of one object seen from n_frames
     views inside a +-cone_deg cone whose pairwise rotation geodesics are >= 10 deg (the
     memory-pool novelty rule)."""
@@ -202,6 +202,9 @@ def make_scene(n_frames: int, n: int = 500, n_max: int = 512, width: int = 640, 
     R0 = rotvec_to_R(np.array([0.3, -0.5, 0.2]))
 
     Rs, ts = [], []
+    if poses is not None:                                    # given (R, t) per frame (trajectories)
+        Rs = [np.asarray(R, np.float64) for R, _ in poses]
+        ts = [np.asarray(t, np.float64) for _, t in poses]
     tries = 0
     while len(Rs) < n_frames:
         tries += 1
