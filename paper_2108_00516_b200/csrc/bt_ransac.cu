@@ -566,12 +566,17 @@ __device__ void block_sum_n(double (&v)[N], double *red) {
 #pragma unroll
     for (int k = 0; k < N; ++k) red[warp * N + k] = v[k];
   __syncthreads();
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
+  // lane k of warp 0 sums value k over the warps (the same order as before: w = 0, 1, ...)
+  // and every thread then reads the N totals — instead of every thread summing all of them
+  const int nw = (int)(blockDim.x >> 5);
+  if (warp == 0 && lane < N) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w * N + k];
-    v[k] = t;
+    for (int w = 0; w < nw; ++w) t += red[w * N + lane];
+    red[nw * N + lane] = t;
   }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = red[nw * N + k];
 }
 
 struct FinishArgs {
@@ -709,7 +714,7 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   pdl_wait();
   extern __shared__ int inl[];                     // [n_max] inlier match indices, in order
   __shared__ float Tb[12];
-  __shared__ double red[(kFinThreads / 32) * 9];
+  __shared__ double red[(kFinThreads / 32 + 1) * 9];
   __shared__ int wcnt[kFinThreads / 32];
   __shared__ double shT[12];
   __shared__ int sh_status;
