@@ -30,7 +30,7 @@
 #include "bt_tc.cuh"
 
 #ifndef BT_TC_EPI_WARPS
-#define BT_TC_EPI_WARPS 16
+#define BT_TC_EPI_WARPS 8
 #endif
 
 namespace bt {
@@ -967,14 +967,19 @@ __device__ __forceinline__ f32x2 sub2s(float a, f32x2 b) {               // {a, 
 // counts are bit-identical to the FMA kernel's.
 constexpr int kTcRows = 128;                 // hypotheses per item (UMMA M)
 constexpr int kTcCols = 64;                  // correspondences per chunk (UMMA N)
-constexpr int kTcTBuf = 512 / (2 * kTcCols);  // TMEM buffers (D1 + D2 of a chunk each)
+#ifndef BT_TC_CTAS
+#define BT_TC_CTAS 2
+#endif
+constexpr int kTcCtas = BT_TC_CTAS;            // CTAs per SM (each owns 512 / kTcCtas TMEM columns)
+constexpr int kTcTmem = 512 / kTcCtas;
+constexpr int kTcTBuf = kTcTmem / (2 * kTcCols);  // TMEM buffers (D1 + D2 of a chunk each)
 constexpr int kTcWc = kTcCols / (BT_TC_EPI_WARPS / 4);  // columns per warpgroup and chunk
 constexpr int kTcPad = 128;                  // feature rows per pair: multiple of 128
 constexpr int kTcFeat = 64;                  // fp16 per feature row: X1/Y1 hi, lo | X2/Y2 hi, lo
 constexpr int kTcEpiWarps = BT_TC_EPI_WARPS;  // warpgroups x (columns of a chunk / warpgroups)
 constexpr int kTcWgs = kTcEpiWarps / 4;
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;   // + MMA warp + TMA warp
-constexpr int kTcBBuf = 6;
+constexpr int kTcBBuf = kTcCtas == 1 ? 6 : 3;
 constexpr size_t kTcSmem = 1024 + 2 * kTcRows * 128 + kTcBBuf * kTcCols * 128;
 constexpr float kTcSentinel = 65504.f;       // padded correspondence: D1 = 65504 * s_x > any threshold
 
@@ -1255,7 +1260,7 @@ __device__ __forceinline__ RowConst row_setup(const ScoreTcArgs &A, const PairFe
 //   epilogue warps 0-15: warpgroup 0 builds the next item's A tile (features of its 128
 //     hypotheses) at the start of each item; every warp reads 32 columns of D1 and D2 for its
 //     32 TMEM lanes, releases the buffer, and counts certain / possible inliers per row.
-__global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constant__ CUtensorMap fmap, ScoreTcArgs A) {
+__global__ void __launch_bounds__(kTcThreads, kTcCtas) k_score_tc(const __grid_constant__ CUtensorMap fmap, ScoreTcArgs A) {
   pdl_wait();
   extern __shared__ uint8_t tc_smem_raw[];
   __shared__ __align__(8) uint64_t bar_a[2], bar_bfull[kTcBBuf], bar_bfree[kTcBBuf], bar_mma[kTcTBuf], bar_tfree[kTcTBuf];
@@ -1269,7 +1274,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
   const int n_items = A.P * A.nht;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(512)
+                 "r"(kTcTmem)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -1461,7 +1466,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_score_tc(const __grid_constan
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcTmem) : "memory");
   }
 }
 
@@ -1617,7 +1622,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
       int dev = 0, n_sm = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-      tc_grid = n_sm;                                              // one CTA per SM (all 512 TMEM columns)
+      tc_grid = n_sm * kTcCtas;                                    // kTcCtas CTAs per SM (TMEM split)
     }
     L.begin(K_RANSAC_SCORE, s);
     launch_pdl(k_corr_feat, P, kFeatThreads, 0, s, t);
