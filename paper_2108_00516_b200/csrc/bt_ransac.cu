@@ -966,7 +966,10 @@ __device__ __forceinline__ f32x2 sub2s(float a, f32x2 b) {               // {a, 
 // of the tests) is listed and recounted with the fp32 formula itself (k_score_fix).  So the
 // counts are bit-identical to the FMA kernel's.
 constexpr int kTcRows = 128;                 // hypotheses per item (UMMA M)
-constexpr int kTcCols = 64;                  // correspondences per chunk (UMMA N)
+#ifndef BT_TC_COLS
+#define BT_TC_COLS 64
+#endif
+constexpr int kTcCols = BT_TC_COLS;          // correspondences per chunk (UMMA N)
 #ifndef BT_TC_CTAS
 #define BT_TC_CTAS 2
 #endif
