@@ -982,7 +982,10 @@ constexpr int kTcFeat = 64;                  // fp16 per feature row: X1/Y1 hi, 
 constexpr int kTcEpiWarps = BT_TC_EPI_WARPS;  // warpgroups x (columns of a chunk / warpgroups)
 constexpr int kTcWgs = kTcEpiWarps / 4;
 constexpr int kTcThreads = (kTcEpiWarps + 2) * 32;   // + MMA warp + TMA warp
-constexpr int kTcBBuf = kTcCtas == 1 ? 6 : 3;
+#ifndef BT_TC_BBUF
+#define BT_TC_BBUF 0
+#endif
+constexpr int kTcBBuf = BT_TC_BBUF ? BT_TC_BBUF : (kTcCtas == 1 ? 6 : 3);
 constexpr size_t kTcSmem = 1024 + 2 * kTcRows * 128 + kTcBBuf * kTcCols * 128;
 constexpr float kTcSentinel = 65504.f;       // padded correspondence: D1 = 65504 * s_x > any threshold
 
@@ -1389,7 +1392,10 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtas) k_score_tc(const __grid_c
       bool overflow = false;
       for (int c = 0; c < nch; ++c, ++g) {
         const int tb = g % kTcTBuf;
-        mbar_wait_sleep(&bar_mma[tb], (g / kTcTBuf) & 1, 200);
+#ifndef BT_TC_SLEEP
+#define BT_TC_SLEEP 200
+#endif
+        mbar_wait_sleep(&bar_mma[tb], (g / kTcTBuf) & 1, BT_TC_SLEEP);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * 2 * kTcCols + wg * kTcWc);
         if (c * kTcCols + wg * kTcWc >= M) {                        // all columns padding: release only
