@@ -162,3 +162,17 @@ def test_score_tc_equals_fma_scaled_scenes(bt, torch, scale, shift):
     out, _ = _run_both(bt, torch, ctx, sc, [(0, 1)], 4096, match_lists=[m])
     ctx.close()
     _assert_equal(out, f"scale {scale}, shift {shift}")
+
+
+def test_score_tc_equals_fma_c5_shape(bt, torch):
+    """BASELINE configs[4] shape (n = 4096 keypoints, ~2600 matches per pair, 16384
+    hypotheses): 15 pairs of a 6-frame scene, every count bitwise equal to the FFMA2 kernel."""
+    sc = synth.make_scene(6, n=4096, n_max=4096, pool_size=12000, seed=4242, outlier_frac=0.16,
+                          render_maps=False)
+    pairs = synth.all_pairs(6)
+    ctx = bt.Context(0)
+    ctx.reserve(len(pairs), 4096, 16384, 6, 0, 0)
+    out, nm = _run_both(bt, torch, ctx, sc, pairs, 16384)
+    ctx.close()
+    assert (nm > 1500).all()
+    _assert_equal(out, "C5 shape")
