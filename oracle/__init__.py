@@ -77,7 +77,7 @@ def _setup(L):
     L.bto_feature_edge.argtypes = [_f32p, _f32p, _u32p, C.c_int32, _f32p, _f32p, C.c_double, _f64p]
     L.bto_dense_edge.argtypes = [_f32p, _f32p, _u8p, _f32p, _f32p, _u8p, C.c_int32, C.c_int32,
                                  C.c_double, C.c_double, C.c_double, C.c_double, _f32p, _f32p,
-                                 C.c_double, C.c_double, C.c_double, C.c_int32, _f64p, _vp, _vp]
+                                 C.c_double, C.c_double, C.c_double, C.c_int32, _f64p, _vp, _vp, _vp]
     L.bto_estimate_normals.argtypes = [_f32p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
                                        C.c_double, C.c_float, _f32p]
     L.bto_se3_exp.argtypes = [_f64p, _f64p, _f64p]
@@ -207,7 +207,7 @@ def feature_edge(pa, pb, mask, Ti, Tj, huber_delta=0.005) -> np.ndarray:
     pa = _c(pa, np.float32).reshape(-1)
     pb = _c(pb, np.float32).reshape(-1)
     M = len(pa) // 3
-    out = np.zeros(108)
+    out = np.zeros(186)
     mk = _c(mask, np.uint32) if M else np.zeros(1, np.uint32)
     z = np.zeros(3, np.float32)
     lib().bto_feature_edge(pa if M else z, pb if M else z, mk, M, _c(Ti, np.float32),
@@ -217,20 +217,27 @@ def feature_edge(pa, pb, mask, Ti, Tj, huber_delta=0.005) -> np.ndarray:
 
 def dense_edge(depth_i, normal_i, mask_i, depth_j, normal_j, mask_j, K, Ti, Tj, dist_gate=0.02,
                cos_gate=float(np.cos(np.deg2rad(45.0))), huber_delta=0.005, stride=1,
-               want_pixels=False):
+               want_pixels=False, want_allow=False):
+    """Eq. (3) edge i -> j (bto_dense_edge).  Returns out[72]; with want_pixels also the per-pixel
+    association [H][W] (target index or -1) and borderline flags; with want_allow also the
+    per-pixel allowance [H][W][8] of the borderline pixels."""
     H, W = np.asarray(depth_i).shape
-    out = np.zeros(48)
+    out = np.zeros(72)
     pix = np.zeros(H * W, np.int32) if want_pixels else None
     pbd = np.zeros(H * W, np.uint8) if want_pixels else None
+    pal = np.zeros(H * W * 8) if want_allow else None
     lib().bto_dense_edge(_c(depth_i, np.float32).reshape(-1), _c(normal_i, np.float32).reshape(-1),
                          _c(mask_i, np.uint8).reshape(-1), _c(depth_j, np.float32).reshape(-1),
                          _c(normal_j, np.float32).reshape(-1), _c(mask_j, np.uint8).reshape(-1),
                          W, H, float(K.fx), float(K.fy), float(K.cx), float(K.cy),
                          _c(Ti, np.float32), _c(Tj, np.float32), float(dist_gate), float(cos_gate),
-                         float(huber_delta), int(stride), out, _ptr(pix), _ptr(pbd))
+                         float(huber_delta), int(stride), out, _ptr(pix), _ptr(pbd), _ptr(pal))
+    res = (out,)
     if want_pixels:
-        return out, pix.reshape(H, W), pbd.reshape(H, W).astype(bool)
-    return out
+        res += (pix.reshape(H, W), pbd.reshape(H, W).astype(bool))
+    if want_allow:
+        res += (pal.reshape(H, W, 8),)
+    return res if len(res) > 1 else out
 
 
 # --------------------------------------------------------------- whole pair registration

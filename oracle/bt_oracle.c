@@ -391,12 +391,13 @@ static void skew(const double p[3], double S[9]) {
  *   J_i = -R_i^T [ I | -[p_m]x ],   J_j = R_j^T [ I | -[p_n]x ].
  * ------------------------------------------------------------------------------------- */
 void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, int32_t M,
-                      const float Ti[12], const float Tj[12], double huber_delta, double out[108]) {
+                      const float Ti[12], const float Tj[12], double huber_delta, double out[186]) {
   double Ri[9], ti[3], Rj[9], tj[3];
   pose_of(Ti, Ri, ti);
   pose_of(Tj, Rj, tj);
-  double Hf[12][12], g[12], gs[12], E = 0.0;
+  double Hf[12][12], Hs[12][12], g[12], gs[12], E = 0.0;
   memset(Hf, 0, sizeof Hf);
+  memset(Hs, 0, sizeof Hs);
   memset(g, 0, sizeof g);
   memset(gs, 0, sizeof gs);
   int32_t count = 0;
@@ -426,9 +427,10 @@ void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, in
       }
     for (int a = 0; a < 12; ++a) {
       for (int b = 0; b < 12; ++b) {
-        double s = 0.0;
-        for (int r = 0; r < 3; ++r) s += J[r][a] * J[r][b];
+        double s = 0.0, sa = 0.0;
+        for (int r = 0; r < 3; ++r) { s += J[r][a] * J[r][b]; sa += fabs(J[r][a] * J[r][b]); }
         Hf[a][b] += w * s;
+        Hs[a][b] += w * sa;
       }
       double s = 0.0, sa = 0.0;
       for (int r = 0; r < 3; ++r) { s += J[r][a] * e[r]; sa += fabs(J[r][a] * e[r]); }
@@ -438,7 +440,7 @@ void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, in
     E += rho;
     ++count;
   }
-  memset(out, 0, 108 * sizeof(double));
+  memset(out, 0, 186 * sizeof(double));
   int k = 0;
   for (int a = 0; a < 6; ++a)
     for (int b = a; b < 6; ++b) out[k++] = Hf[a][b];               /* H_ii upper */
@@ -450,6 +452,13 @@ void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, in
   out[k++] = E;
   out[k++] = count;
   for (int a = 0; a < 12; ++a) out[96 + a] = gs[a];             /* tolerance scale of g */
+  k = 108;                                                       /* tolerance scale of H, same packing */
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) out[k++] = Hs[a][b];
+  for (int a = 0; a < 6; ++a)
+    for (int b = 0; b < 6; ++b) out[k++] = Hs[a][6 + b];
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) out[k++] = Hs[6 + a][6 + b];
 }
 
 /* ---------------------------------------------------------------------------------------
@@ -492,8 +501,8 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
                     const float *depth_j, const float *normal_j, const uint8_t *mask_j,
                     int32_t W, int32_t H, double fx, double fy, double cx, double cy,
                     const float Ti[12], const float Tj[12], double dist_gate, double cos_gate,
-                    double huber_delta, int32_t stride, double out[48], int32_t *pix_out,
-                    uint8_t *pix_border) {
+                    double huber_delta, int32_t stride, double out[72], int32_t *pix_out,
+                    uint8_t *pix_border, double *pix_allow) {
   double Ri[9], ti[3], Rj[9], tj[3];
   pose_of(Ti, Ri, ti);
   pose_of(Tj, Rj, tj);
@@ -510,9 +519,10 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
     tji[r] = tj[r] - (Rji[r * 3 + 0] * ti[0] + Rji[r * 3 + 1] * ti[1] + Rji[r * 3 + 2] * ti[2]);
     tij[r] = ti[r] - (Rij[r * 3 + 0] * tj[0] + Rij[r * 3 + 1] * tj[1] + Rij[r * 3 + 2] * tj[2]);
   }
-  double Hs[6][6], g[6], gs[6], E = 0.0;
+  double Hs[6][6], Ha[6][6], g[6], gs[6], E = 0.0;
   double al_g[6] = {0, 0, 0, 0, 0, 0}, al_E = 0.0, al_H = 0.0;   /* borderline allowance */
   memset(Hs, 0, sizeof Hs);
+  memset(Ha, 0, sizeof Ha);
   memset(g, 0, sizeof g);
   memset(gs, 0, sizeof gs);
   int32_t count = 0, count_border = 0;
@@ -522,6 +532,7 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
       size_t pix = (size_t)v * W + u;
       if (pix_out) pix_out[pix] = -1;
       if (pix_border) pix_border[pix] = 0;
+      if (pix_allow) memset(pix_allow + 8 * pix, 0, 8 * sizeof(double));
       if (u % stride || v % stride) continue;
       double d = depth_i[pix];
       const float *ni_f = normal_i + 3 * pix;
@@ -592,6 +603,12 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
         al_H += mh;
         al_E += me;
         for (int k = 0; k < 6; ++k) al_g[k] += mg[k];
+        if (pix_allow) {
+          double *pa_ = pix_allow + 8 * pix;
+          pa_[0] = mh;
+          pa_[1] = me;
+          for (int k = 0; k < 6; ++k) pa_[2 + k] = mg[k];
+        }
       }
       if (!pass) continue;
       double r = ni[0] * dq[0] + ni[1] * dq[1] + ni[2] * dq[2];
@@ -600,7 +617,7 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
       double J[6] = {ni[0], ni[1], ni[2],
                      q[1] * ni[2] - q[2] * ni[1], q[2] * ni[0] - q[0] * ni[2], q[0] * ni[1] - q[1] * ni[0]};
       for (int a = 0; a < 6; ++a) {
-        for (int b = 0; b < 6; ++b) Hs[a][b] += w * J[a] * J[b];
+        for (int b = 0; b < 6; ++b) { Hs[a][b] += w * J[a] * J[b]; Ha[a][b] += w * fabs(J[a] * J[b]); }
         g[a] += w * J[a] * r;
         gs[a] += w * fabs(J[a] * r);
       }
@@ -608,8 +625,11 @@ void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *
       ++count;
       if (pix_out) pix_out[pix] = (int32_t)pj;
     }
-  memset(out, 0, 48 * sizeof(double));
-  int k = 0;
+  memset(out, 0, 72 * sizeof(double));
+  int k = 48;                                                    /* tolerance scale of H (upper) */
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) out[k++] = Ha[a][b];
+  k = 0;
   for (int a = 0; a < 6; ++a)
     for (int b = a; b < 6; ++b) out[k++] = Hs[a][b];
   for (int a = 0; a < 6; ++a) out[k++] = g[a];

@@ -90,25 +90,32 @@ void bto_huber(double r, double delta, double *rho, double *w);
 
 /* Eq. (2) feature-edge linearization at node poses Ti, Tj (12 floats each):
    e = Ti^-1 p_m - Tj^-1 p_n over the masked correspondences; left perturbation
-   T <- exp(d) T, twist order (v, w).  out[108]: H_ii(21, upper row-major) H_ij(36 row-major)
+   T <- exp(d) T, twist order (v, w).  out[186]: H_ii(21, upper row-major) H_ij(36 row-major)
    H_jj(21) g_i(6) g_j(6) E(1) count(1) pad(4), then (oracle only) [96..107] the tolerance
-   scale of g, sum w |J_k| . |e|.  H = sum w J^T J, g = sum w J^T e, E = sum rho(||e||). */
+   scale of g, sum w |J_k| . |e|, and [108..185] the tolerance scale of H in the same 78-entry
+   packing, sum w sum_r |J_ra J_rb| (the sum of absolute contributions: the magnitude that
+   floating-point summation error is relative to).  H = sum w J^T J, g = sum w J^T e,
+   E = sum rho(||e||). */
 void bto_feature_edge(const float *pa, const float *pb, const uint32_t *mask, int32_t M,
-                      const float Ti[12], const float Tj[12], double huber_delta, double out[108]);
+                      const float Ti[12], const float Tj[12], double huber_delta, double out[186]);
 
 /* Eq. (3) dense point-to-plane edge i -> j.  Maps: depth [H][W], normal [H][W][3],
-   mask [H][W].  out[48]: H(21 upper) g(6) E count count_border pad(2), then (oracle only)
-   [32..37] sum w |J_k r| (the scale the g tolerance is relative to), and the borderline
+   mask [H][W].  out[72]: H(21 upper) g(6) E count count_border pad(2), then (oracle only)
+   [32..37] sum w |J_k r| (the scale the g tolerance is relative to), the borderline
    allowance — summed over borderline pixels, the largest contribution over every target
-   pixel the pixel may round to: [38..43] w |J_k r|, [44] rho, [45] w |J|^2 (>= |w J^T J|_F).
-   pix_out (may be NULL): [H][W] int32 per source pixel: -1 skipped, else the associated
-   target pixel index y'*W+x'.  pix_border (may be NULL): [H][W] u8, 1 iff borderline. */
+   pixel the pixel may round to: [38..43] w |J_k r|, [44] rho, [45] w |J|^2 (>= |w J^T J|_F),
+   pad(2), and [48..68] sum w |J_a J_b| (upper, the scale of an element-wise H tolerance).
+   pix_out (may be NULL): [H][W] int32 per source pixel: -1 skipped or rejected by a gate,
+   else the associated target pixel index y'*W+x' (both gates passed).  pix_border (may be
+   NULL): [H][W] u8, 1 iff borderline.  pix_allow (may be NULL): [H][W][8] the allowance of
+   each borderline pixel (w |J|^2, rho, w |J_k r| x 6; zero elsewhere), so a comparison can
+   charge only the pixels whose decision actually differs. */
 void bto_dense_edge(const float *depth_i, const float *normal_i, const uint8_t *mask_i,
                     const float *depth_j, const float *normal_j, const uint8_t *mask_j,
                     int32_t W, int32_t H, double fx, double fy, double cx, double cy,
                     const float Ti[12], const float Tj[12], double dist_gate, double cos_gate,
-                    double huber_delta, int32_t stride, double out[48], int32_t *pix_out,
-                    uint8_t *pix_border);
+                    double huber_delta, int32_t stride, double out[72], int32_t *pix_out,
+                    uint8_t *pix_border, double *pix_allow);
 
 /* ---- NEXT-1: pose-graph Gauss-Newton step (§IV-D) -------------------
    Twists are (v, w) (translation first), perturbations are on the left: T <- exp(d) T

@@ -391,3 +391,24 @@ def make_correspondences(rng_or_seed, M: int, inlier_frac: float, noise: float =
         pb[inl] += noise * rng.normal(size=(int(inl.sum()), 3))
     f = np.float32
     return pa.astype(f), na.astype(f), pb.astype(f), nb.astype(f), R, t, inl
+
+
+def make_nearly_collinear(n_line: int = 200, length: float = 0.2, offset: float = 0.01, seed: int = 0,
+                          distance: float = 0.6):
+    """A correspondence set whose refit is degenerate while its best sample is not: n_line
+    points evenly spaced on a segment of `length` along x plus ONE point displaced by `offset`
+    along y, at `distance` in front of the camera, observed identically in both frames (p_b =
+    p_a, normals (0, 0, -1)), in a seeded random order.  Returns (pa, na, pb, nb, off_index).
+    The spread of the whole set across the line is ~offset^2 against ~n_line length^2 / 12
+    along it, while a sample holding the displaced point sees offset^2 against length^2."""
+    rng = np.random.default_rng(seed)
+    x = np.linspace(-length / 2, length / 2, n_line)
+    pts = np.zeros((n_line + 1, 3))
+    pts[:n_line, 0] = x
+    pts[n_line] = (rng.uniform(-length / 4, length / 4), offset, 0.0)
+    pts[:, 2] += distance
+    order = rng.permutation(n_line + 1)
+    pts = pts[order].astype(np.float32)
+    nrm = np.zeros_like(pts)
+    nrm[:, 2] = -1.0
+    return pts, nrm, pts.copy(), nrm.copy(), int(np.nonzero(order == n_line)[0][0])

@@ -241,3 +241,65 @@ def test_dense_gradient_by_finite_differences_on_a_tilted_plane():
         assert Ep[28] == Em[28] == out[28]
         fd = (Ep[27] - Em[27]) / (2 * eps)
         assert abs(fd - g[k]) <= 2e-2 * np.abs(g).max(), (k, fd, g[k])
+
+
+def test_dense_tolerance_scales_and_per_pixel_allowance():
+    """The oracle's comparison aids of Eq. (3): the element-wise H scale sum w |J_a J_b| has
+    the diagonal of H itself (w J_a^2 >= 0) and bounds |H| element-wise; the per-pixel
+    allowances are non-zero only on borderline pixels and sum to the edge's allowance totals;
+    the association map holds exactly `count` accepted pixels (P:72 gates)."""
+    sc = synth.make_scene(4, seed=5)
+    poses = sc.perturbed_poses(3)
+    for i, j in ((0, 1), (2, 3), (3, 0)):
+        out, pix, bd, pal = oracle.dense_edge(sc.depth[i], sc.normal[i], sc.mask[i], sc.depth[j], sc.normal[j],
+                                              sc.mask[j], sc.K, poses[i], poses[j], want_pixels=True,
+                                              want_allow=True)
+        H, S = _unpack_sym(out[:21]), _unpack_sym(out[48:69])
+        assert np.allclose(np.diag(S), np.diag(H), rtol=1e-12, atol=0)
+        assert (np.abs(H) <= S * (1 + 1e-12)).all()
+        assert (pix >= 0).sum() == out[28] > 1000
+        assert not pal[~bd].any()
+        tot = pal.reshape(-1, 8).sum(0)
+        assert np.isclose(tot[0], out[45], rtol=1e-12) and np.isclose(tot[1], out[44], rtol=1e-12)
+        assert np.allclose(tot[2:], out[38:44], rtol=1e-12)
+        assert bd.sum() == out[29]
+
+
+def test_dense_identical_frames_h_scale_closed_form():
+    """Identical frames (all weights 1): the H scale is |J|^T |J| in closed form."""
+    sc, *_ = synth.make_pair_c1()
+    T = sc.node_poses()[0]
+    out = oracle.dense_edge(sc.depth[0], sc.normal[0], sc.mask[0], sc.depth[0], sc.normal[0], sc.mask[0], sc.K, T, T)
+    valid = np.nonzero(sc.mask[0].reshape(-1))[0]
+    v, u = np.divmod(valid, sc.K.width)
+    d = sc.depth[0].reshape(-1)[valid].astype(float)
+    p = np.stack([(u - sc.K.cx) * d / sc.K.fx, (v - sc.K.cy) * d / sc.K.fy, d], 1)
+    n = sc.normal[0].reshape(-1, 3)[valid].astype(float)
+    J = np.abs(np.concatenate([n, np.cross(p, n)], 1))
+    Sc = J.T @ J
+    assert np.abs(_unpack_sym(out[48:69]) - Sc).max() <= 1e-7 * Sc.max()
+
+
+def test_feature_edge_h_scale_invariants():
+    """Eq. (2): the H scale sum w sum_r |J_ra J_rb| (out[108:186], same packing as H) equals H
+    on the diagonal, bounds |H| element-wise, and for one correspondence at identity poses with
+    p = 0 (J_i = -[I | 0], J_j = [I | 0]) is the 0/1 pattern of |J|^T |J|."""
+    rng = np.random.default_rng(3)
+    pa = rng.normal(scale=0.05, size=(40, 3)).astype(np.float32) + np.float32([0, 0, 0.6])
+    pb = pa + rng.normal(scale=0.003, size=pa.shape).astype(np.float32)
+    Ti = synth.pose12(synth.random_rotation(rng, 0.2), rng.normal(scale=0.05, size=3))
+    Tj = synth.pose12(synth.random_rotation(rng, 0.2), rng.normal(scale=0.05, size=3))
+    mask = np.array([0xffffffff, 0xff], np.uint32)
+    out = oracle.feature_edge(pa, pb, mask, Ti, Tj)
+    H, _, _, _ = _feat_blocks(out)
+    S, _, _, _ = _feat_blocks(np.concatenate([out[108:186], out[78:108]]))
+    assert np.allclose(np.diag(S), np.diag(H), rtol=1e-12, atol=0)
+    assert (np.abs(H) <= S * (1 + 1e-12)).all()
+    I = synth.pose12(np.eye(3), np.zeros(3))
+    z = np.zeros((1, 3), np.float32)
+    one = oracle.feature_edge(z, z, np.array([1], np.uint32), I, I)
+    S1, _, _, _ = _feat_blocks(np.concatenate([one[108:186], one[78:108]]))
+    Jabs = np.zeros((3, 12))
+    Jabs[:, 0:3] = np.eye(3)
+    Jabs[:, 6:9] = np.eye(3)
+    assert np.array_equal(S1, Jabs.T @ Jabs)

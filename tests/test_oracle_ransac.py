@@ -166,3 +166,39 @@ def test_determinism_and_uid_keying():
     c = oracle.ransac_counts(pa, na, pb, nb, 64, 6, SEED)
     assert np.array_equal(a["cnt"], b["cnt"]) and np.array_equal(a["tri"], b["tri"])
     assert not np.array_equal(a["tri"], c["tri"])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_refit_degenerate_status(seed):
+    """REFIT_DEGENERATE (status 3, reading R8 applied to the refit): 200 evenly spaced collinear
+    points plus one point 1 cm off the line, seen identically in both frames.  Samples of three
+    line points are degenerate (count -1); every sample holding the off-line point fits the
+    identity exactly, so h* = the first h whose Philox triple contains it and count* = M.  The
+    whole inlier set spreads ~12 h^2 / (N L^2) ~ 1.5e-4 across the line (< tau = 1e-3, the
+    ratio of the covariance's two largest eigenvalues, here from LAPACK), so the refit is
+    rejected and T_refit = T_best."""
+    pa, na, pb, nb, off = synth.make_nearly_collinear(seed=seed)
+    M = len(pa)
+    c = pa.astype(np.float64) - pa.astype(np.float64).mean(0)
+    ev = np.linalg.eigvalsh(c.T @ c)[::-1]
+    assert ev[1] / ev[0] < 3e-4                                # far below tau = 1e-3
+    H = 512
+    res = oracle.ransac_counts(pa, na, pb, nb, H, 7, SEED)
+    key = [SEED & 0xffffffff, SEED >> 32]
+    first = None
+    for h in range(H):
+        tri = oracle.triple(oracle.philox([h, 7, 0, 0], key), M)
+        if off in tri:
+            first = h if first is None else first
+            assert res["cnt"][h] == M
+        else:
+            assert res["cnt"][h] == -1
+    fin = oracle.ransac_finish(pa, na, pb, nb, res)
+    assert fin["best_hyp"] == first and fin["best_count"] == M
+    assert fin["status"] == oracle.STATUS_REFIT_DEGENERATE
+    assert np.isclose(fin["refit_sig_ratio"], ev[1] / ev[0], rtol=1e-6)
+    assert np.array_equal(fin["T_refit"], fin["T_best"])
+    # the same set without the degeneracy (off-line point 5 cm away: ratio ~ 4e-3) refits
+    pa2, na2, pb2, nb2, _ = synth.make_nearly_collinear(seed=seed, offset=0.05)
+    fin2 = oracle.ransac_finish(pa2, na2, pb2, nb2, oracle.ransac_counts(pa2, na2, pb2, nb2, H, 7, SEED))
+    assert fin2["status"] == oracle.STATUS_OK and fin2["refit_sig_ratio"] > 1e-3
