@@ -151,6 +151,19 @@ bt_status bt_dense_corr(bt_ctx *ctx, const bt_maps *maps, const bt_intrinsics *K
                         const bt_pose *node_pose, const int32_t *edges, int32_t E,
                         const bt_edge_params *prm, float *out, void *stream);
 
+/* Debug / verification entry of Eq. (3) ("dense pixel-wise correspondences are
+   associated by point re-projection, while outliers are filtered based on the distance ...
+   and the angle"): bt_dense_corr plus the per-pixel DECISION it took.  Same arguments and the
+   same `out` (bitwise equal to bt_dense_corr's); in addition assoc [E][H][W] int32 (device,
+   caller-owned, written in full): for each source pixel x of I_i, the target pixel index
+   y'*W + x' it was associated with (projection in the frame, valid target, both gates passed),
+   else -1 (not a source pixel: outside the mask / invalid / off-stride; or rejected).  A
+   separate kernel instantiation: bt_dense_corr and bt_register_pairs never write it.  Errors
+   as bt_dense_corr; BT_EINVAL if assoc is NULL. */
+bt_status bt_dense_assoc(bt_ctx *ctx, const bt_maps *maps, const bt_intrinsics *K,
+                         const bt_pose *node_pose, const int32_t *edges, int32_t E,
+                         const bt_edge_params *prm, float *out, int32_t *assoc, void *stream);
+
 /* The whole per-pair hot path for P pairs: bt_match -> bt_ransac -> Eq. (2) blocks at the
    node poses -> both directed Eq. (3) edges.  eprm may be NULL: dense + feature words are
    then left untouched (the first stage of a frame step). */

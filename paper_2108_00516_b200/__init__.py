@@ -26,7 +26,8 @@ SYMBOLS = ("bt_create", "bt_destroy", "bt_last_error", "bt_status_string", "bt_r
            "bt_record_words", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
            "bt_register_pairs_host", "bt_compose_poses", "bt_last_launch_count", "bt_profile_enable",
            "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step",
-           "bt_estimate_normals", "bt_relinearize", "bt_relinearize_matches", "bt_copy_matches")
+           "bt_estimate_normals", "bt_relinearize", "bt_relinearize_matches", "bt_copy_matches",
+           "bt_dense_assoc")
 
 
 class BtError(RuntimeError):
@@ -98,6 +99,8 @@ def lib():
         L.bt_ransac.argtypes = [vp, C.POINTER(Keypoints), vp, vp, i32, vp, vp, C.POINTER(RansacParams), vp, vp, vp]
         L.bt_dense_corr.argtypes = [vp, C.POINTER(Maps), C.POINTER(Intrinsics), vp, vp, i32, C.POINTER(EdgeParams),
                                     vp, vp]
+        L.bt_dense_assoc.argtypes = [vp, C.POINTER(Maps), C.POINTER(Intrinsics), vp, vp, i32, C.POINTER(EdgeParams),
+                                     vp, vp, vp]
         rp = [vp, C.POINTER(Keypoints), C.POINTER(Maps), C.POINTER(Intrinsics), vp, vp, vp, i32,
               C.POINTER(MatchParams), C.POINTER(RansacParams), C.POINTER(EdgeParams), vp, vp]
         L.bt_register_pairs.argtypes = rp
@@ -120,7 +123,7 @@ def lib():
         L.bt_profile_name.restype = C.c_char_p
         L.bt_profile_read.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.bt_profile_read.restype = C.c_int
-        for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_register_pairs",
+        for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_dense_assoc", "bt_register_pairs",
                   "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals", "bt_relinearize",
                   "bt_relinearize_matches", "bt_copy_matches"):
             getattr(L, f).restype = C.c_int
@@ -262,6 +265,15 @@ class Context:
         self._check(lib().bt_dense_corr(self._h, C.byref(mp), C.byref(Ki), _ptr(node_pose), _ptr(edges),
                                         int(edges.shape[0]), C.byref(prm), _ptr(out), self._stream(stream)),
                     "bt_dense_corr")
+
+    def dense_assoc(self, fb: FrameBatch, K, node_pose, edges, prm: EdgeParams, out, assoc, stream=None):
+        """bt_dense_corr plus the per-source-pixel association assoc [E][H][W] int32 (target
+        pixel index or -1) — the verification entry bt_dense_assoc."""
+        mp = fb.maps()
+        Ki = intrinsics(K) if not isinstance(K, Intrinsics) else K
+        self._check(lib().bt_dense_assoc(self._h, C.byref(mp), C.byref(Ki), _ptr(node_pose), _ptr(edges),
+                                         int(edges.shape[0]), C.byref(prm), _ptr(out), _ptr(assoc),
+                                         self._stream(stream)), "bt_dense_assoc")
 
     def register_pairs(self, fb: FrameBatch, K, node_pose, pairs, uid, rprm: RansacParams,
                        eprm: EdgeParams | None, records, ratio: float = 1.0, stream=None, host=False):

@@ -9,7 +9,10 @@
 #include <utility>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <tuple>
 #include <vector>
 
 #include "bt_internal.cuh"
@@ -52,6 +55,54 @@ struct bt_ctx {
   uint8_t *st_mask = nullptr;
   bt_pose *st_pose = nullptr;
 };
+
+namespace bt {
+namespace {
+std::mutex g_setup_mu;
+std::map<std::pair<int, const void *>, size_t> g_smem;           // (device, kernel) -> opted-in bytes
+std::map<int, int> g_sms;                                        // device -> SM count
+std::map<std::tuple<int, const void *, int, size_t>, int> g_grid;
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+}  // namespace
+
+void smem_optin(const void *kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_setup_mu);
+  size_t &have = g_smem[{dev, kernel}];
+  if (bytes > have) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    have = bytes;
+  }
+}
+
+int sm_count() {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_setup_mu);
+  auto it = g_sms.find(dev);
+  if (it != g_sms.end()) return it->second;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return g_sms[dev] = sms > 0 ? sms : 1;
+}
+
+int resident_grid(const void *kernel, int threads, size_t smem) {
+  smem_optin(kernel, smem);
+  const int sms = sm_count();
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_setup_mu);
+  const auto key = std::make_tuple(dev, kernel, threads, smem);
+  auto it = g_grid.find(key);
+  if (it != g_grid.end()) return it->second;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  return g_grid[key] = sms * (per_sm > 0 ? per_sm : 1);
+}
+}  // namespace bt
 
 namespace {
 
@@ -116,13 +167,25 @@ bt_status check_maps(bt_ctx *c, const bt_maps *mp, const bt_intrinsics *K) {
   if (mp->width != K->width || mp->height != K->height)
     return fail(c, BT_EINVAL, "maps %dx%d != intrinsics %dx%d", mp->width, mp->height, K->width, K->height);
   if (mp->width < 1 || mp->height < 1 || mp->n_frames < 1) return fail(c, BT_EINVAL, "maps: empty");
-  if (mp->n_frames > c->cap_frames || (size_t)mp->width * mp->height > (size_t)c->cap_w * c->cap_h || !c->dense)
+  // the dense scratch is carved per call from the frame count, the pixel count AND the 32x32
+  // tile count (a 600x512 map has fewer pixels than 640x480 but more tiles): all three bounded
+  if (mp->n_frames > c->cap_frames || (size_t)mp->width * mp->height > (size_t)c->cap_w * c->cap_h ||
+      bt::dense_tiles(mp->width, mp->height) > bt::dense_tiles(c->cap_w, c->cap_h) || !c->dense)
     return fail(c, BT_ECAPACITY, "maps %d x %dx%d beyond reserved %d x %dx%d", mp->n_frames, mp->width, mp->height,
                 c->cap_frames, c->cap_w, c->cap_h);
   if (!mp->depth || !mp->normal || !mp->mask) return fail(c, BT_EINVAL, "maps: NULL buffer");
   if (!aligned16(mp->depth) || !aligned16(mp->normal) || !aligned16(mp->mask))
     return fail(c, BT_EINVAL, "maps: buffers must be 16-byte aligned");
   if (!(K->fx > 0.f) || !(K->fy > 0.f)) return fail(c, BT_EINVAL, "intrinsics: fx, fy must be > 0");
+  return BT_OK;
+}
+
+// the scratch one launch_dense carves (frames, edges, pixels, tiles) against the reservation
+bt_status check_dense_bytes(bt_ctx *c, const bt_maps *mp, int E) {
+  const size_t need = bt::dense_scratch_bytes(mp->n_frames, E, mp->width, mp->height);
+  if (need > c->cap_dense)
+    return fail(c, BT_ECAPACITY, "dense scratch %zu B for %d frames x %d edges at %dx%d > reserved %zu B", need,
+                mp->n_frames, E, mp->width, mp->height, c->cap_dense);
   return BT_OK;
 }
 
@@ -225,6 +288,7 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
   free_scratch(c);
   c->cap_pairs = c->cap_nmax = c->cap_hyp = c->cap_frames = c->cap_w = c->cap_h = 0;
   c->cap_dense = 0;
+  c->cached_P = c->cached_nmax = -1;                             // the match lists are gone with the scratch
   const size_t PN = (size_t)max_pairs * n_max;
   const size_t dense_bytes = (width > 0 && height > 0 && max_frames > 0)
                                  ? bt::dense_scratch_bytes(max_frames, 2 * max_pairs, width, height) : 0;
@@ -236,13 +300,15 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
     c->ms = bt::carve_match_scratch(c->match, mframes, max_pairs, n_max);
     c->rs = bt::carve_ransac_scratch(c->rscratch, max_pairs, max_hyp, n_max);
     // TMA tensor map over the fp16 unit descriptors: 2-D [rows][128], 64 x 128 boxes, 128B swizzle
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
+    // process-wide driver entry point (not per device); a magic static is initialized once, thread-safely
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
       cudaDriverEntryPointQueryResult q;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&fn, cudaEnableDefault, &q) != cudaSuccess ||
           q != cudaDriverEntryPointSuccess)
-        encode = nullptr;
-    }
+        fn = nullptr;
+      return fn;
+    }();
     const cuuint64_t rows = (cuuint64_t)mframes * bt::match_n_pad(n_max);
     cuuint64_t dims[2] = {(cuuint64_t)bt::kDim, rows};
     cuuint64_t strides[1] = {(cuuint64_t)bt::kDim * 2};
@@ -325,10 +391,28 @@ bt_status bt_dense_corr(bt_ctx *c, const bt_maps *maps, const bt_intrinsics *K, 
   if (E < 0) return fail(c, BT_EINVAL, "E < 0");
   if (E > 2 * c->cap_pairs) return fail(c, BT_ECAPACITY, "E %d > 2 * reserved pairs %d", E, c->cap_pairs);
   if (E == 0) return BT_OK;
+  if ((s = check_dense_bytes(c, maps, E)) != BT_OK) return s;
   if (!node_pose || !edges || !out) return fail(c, BT_EINVAL, "bt_dense_corr: NULL buffer");
   bt::launch_dense(mview(maps), *K, node_pose, edges, nullptr, E, *prm, c->dense, out, 32, nullptr, 0, 0, 0,
                    (cudaStream_t)stream, c->launch);
   return after_launch(c, "bt_dense_corr");
+}
+
+bt_status bt_dense_assoc(bt_ctx *c, const bt_maps *maps, const bt_intrinsics *K, const bt_pose *node_pose,
+                         const int32_t *edges, int32_t E, const bt_edge_params *prm, float *out, int32_t *assoc,
+                         void *stream) {
+  BT_CHECK_CTX(c);
+  bt_status s;
+  if ((s = check_maps(c, maps, K)) != BT_OK) return s;
+  if ((s = check_edge(c, prm)) != BT_OK) return s;
+  if (E < 0) return fail(c, BT_EINVAL, "E < 0");
+  if (E > 2 * c->cap_pairs) return fail(c, BT_ECAPACITY, "E %d > 2 * reserved pairs %d", E, c->cap_pairs);
+  if (E == 0) return BT_OK;
+  if ((s = check_dense_bytes(c, maps, E)) != BT_OK) return s;
+  if (!node_pose || !edges || !out || !assoc) return fail(c, BT_EINVAL, "bt_dense_assoc: NULL buffer");
+  bt::launch_dense(mview(maps), *K, node_pose, edges, nullptr, E, *prm, c->dense, out, 32, nullptr, 0, 0, 0,
+                   (cudaStream_t)stream, c->launch, assoc);
+  return after_launch(c, "bt_dense_assoc");
 }
 
 static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_maps *maps,
@@ -384,6 +468,7 @@ bt_status bt_register_pairs(bt_ctx *c, const bt_keypoints *kp, const bt_maps *ma
   if (P < 0) return fail(c, BT_EINVAL, "P < 0");
   if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
   if (P == 0) return BT_OK;
+  if (eprm && (s = check_dense_bytes(c, maps, 2 * P)) != BT_OK) return s;
   if (!pairs || !pair_uid || !records) return fail(c, BT_EINVAL, "bt_register_pairs: NULL buffer");
   return register_pairs_dev(c, kp, maps, K, node_pose, pairs, pair_uid, P, mprm, rprm, eprm, records,
                             (cudaStream_t)stream);
@@ -404,10 +489,23 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
   if (P == 0) return BT_OK;
   if (!pairs || !pair_uid || !records || !kp->n_kp || !kp->desc || !kp->pts || !kp->nrm)
     return fail(c, BT_EINVAL, "bt_register_pairs_host: NULL buffer");
+  // every check before the first copy is enqueued (on failure nothing is enqueued): the staged
+  // views carry the staging pointers, so the device-path checks apply to them unchanged
+  bt_keypoints dk = *kp;
+  dk.n_kp = c->st_nkp; dk.desc = c->st_desc; dk.pts = c->st_pts; dk.nrm = c->st_nrm;
+  if ((s = check_kp(c, &dk)) != BT_OK) return s;                // dim == 128, n_max in [1, reserved]
+  bt_maps dm{};
   if (eprm) {
     if (!maps || !K || !node_pose) return fail(c, BT_EINVAL, "bt_register_pairs_host: NULL maps/K/poses");
-    if (maps->n_frames > c->cap_stage || maps->width * maps->height > c->cap_w * c->cap_h)
+    if (!maps->depth || !maps->normal || !maps->mask) return fail(c, BT_EINVAL, "bt_register_pairs_host: NULL map buffer");
+    if (maps->n_frames > c->cap_stage || (size_t)maps->width * maps->height > (size_t)c->cap_w * c->cap_h)
       return fail(c, BT_ECAPACITY, "maps beyond reserved staging");
+    dm = *maps;
+    dm.depth = c->st_depth; dm.normal = c->st_normal; dm.mask = c->st_mask;
+    if ((s = check_maps(c, &dm, K)) != BT_OK) return s;
+    if ((s = check_edge(c, eprm)) != BT_OK) return s;
+    if ((s = check_dense_bytes(c, &dm, 2 * P)) != BT_OK) return s;
+    if (maps->n_frames < kp->n_frames) return fail(c, BT_EINVAL, "maps cover fewer frames than keypoints");
   }
   const cudaStream_t st = (cudaStream_t)stream;
   const int F = kp->n_frames;
@@ -425,9 +523,6 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
   cudaMemcpyAsync(c->st_nrm, kp->nrm, FN * 12, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(c->st_pairs, pairs, (size_t)P * 8, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(c->st_uid, pair_uid, (size_t)P * 4, cudaMemcpyHostToDevice, st);
-  bt_keypoints dk = *kp;
-  dk.n_kp = c->st_nkp; dk.desc = c->st_desc; dk.pts = c->st_pts; dk.nrm = c->st_nrm;
-  if ((s = check_kp(c, &dk)) != BT_OK) return s;
   if (eprm) {
     const size_t FP = (size_t)maps->n_frames * maps->width * maps->height;
     // poses on the caller's stream: the finish kernel (Eq. (2) blocks) reads them there
@@ -435,10 +530,6 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
     cudaMemcpyAsync(c->st_mask, maps->mask, FP, cudaMemcpyHostToDevice, c->side);
     cudaMemcpyAsync(c->st_depth, maps->depth, FP * 4, cudaMemcpyHostToDevice, c->side);
     cudaMemcpyAsync(c->st_normal, maps->normal, FP * 12, cudaMemcpyHostToDevice, c->side);
-    bt_maps dm = *maps;
-    dm.depth = c->st_depth; dm.normal = c->st_normal; dm.mask = c->st_mask;
-    if ((s = check_maps(c, &dm, K)) != BT_OK) return s;
-    if ((s = check_edge(c, eprm)) != BT_OK) return s;
     // the dense kernels need the pair list and poses too: wait for the caller-stream copies
     cudaEventRecord(c->ev_join, st);
     cudaStreamWaitEvent(c->side, c->ev_join, 0);
@@ -521,6 +612,7 @@ static bt_status relinearize(bt_ctx *c, const char *what, const bt_keypoints *kp
   if (P < 0) return fail(c, BT_EINVAL, "P < 0");
   if (P == 0) return BT_OK;
   if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "%s: P %d > reserved %d", what, P, c->cap_pairs);
+  if ((s = check_dense_bytes(c, maps, 2 * P)) != BT_OK) return s;
   if (!node_pose || !pairs || !records || !matches || !n_matches) return fail(c, BT_EINVAL, "%s: NULL buffer", what);
   const cudaStream_t st = (cudaStream_t)stream;
   const int rw = bt::rec_words(kp->n_max);

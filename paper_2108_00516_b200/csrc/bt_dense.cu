@@ -85,6 +85,7 @@ struct DenseArgs {
   int32_t *tlist;             // [F * tiles] masked tiles (f * tiles + t), k_dense_mask -> k_dense_prep
   int32_t *tcount;            // [1] list length (zeroed by k_edge_setup)
   float *partials;            // [E][tiles][32] (per chunk of the edge's source frame; chunks <= tiles)
+  int32_t *assoc;             // debug (bt_dense_assoc): [E][H][W] associated target pixel or -1
 };
 
 __device__ __forceinline__ void edge_frames(const int32_t *edges, const int32_t *pairs, int e, int &fi, int &fj) {
@@ -357,6 +358,7 @@ struct Gather {
   float g[8];                 // one 32-B map entry: x_s hi, n_o,j, x_s lo (fp16 x 3)
   unsigned vb;                // target validity byte (tested only when consumed: the load stays in flight)
   bool in;                    // projected into the frame
+  int tj;                     // target pixel index (read only by the association output)
 };
 
 // project entry k of the staged chunk with T = T_j T_i^-1 and issue its target gathers
@@ -376,6 +378,7 @@ __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, con
   const int tj = ok ? (int)xv * W + (int)xu : -1;
   const int tt = tj < 0 ? 0 : tj;                                  // validity and map entry together
   G.in = tj >= 0;
+  G.tj = tj;
   G.vb = __ldg(vm + tt);
   asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
       : "=f"(G.g[0]), "=f"(G.g[1]), "=f"(G.g[2]), "=f"(G.g[3]), "=f"(G.g[4]), "=f"(G.g[5]), "=f"(G.g[6]),
@@ -388,6 +391,10 @@ __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, con
 // gathers software-pipelined two entries ahead so loads stay in flight.  One 31-shuffle
 // transpose reduction per (warp, edge) puts the 29 sums straight into the edge's chunk partial:
 // no shared reduction buffer, no barrier between edges.
+// kAssoc (bt_dense_assoc, a debug entry): the same arithmetic, plus one store per (entry, edge)
+// of the associated target pixel (-1 when rejected) — the per-pixel decision the parity tests
+// compare with the oracle's; a separate instantiation, so the product kernel carries no trace
+template <bool kAssoc>
 __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -542,6 +549,12 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         for (int aa = 0; aa < 6; ++aa) acc[21 + aa] = fmaf(w * J[aa], r, acc[21 + aa]);
         acc[27] += rho;
         acc[28] += acc_ok ? 1.f : 0.f;
+        if constexpr (kAssoc) {
+          if (k0 < n) {
+            const int uv = __float_as_int(a.w);
+            A.assoc[(size_t)e * npx + (size_t)(uv >> 16) * W + (uv & 0xffff)] = acc_ok ? G.tj : -1;
+          }
+        }
       };
       Gather GA, GB, GC;
       issue_gather(sP, lane, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
@@ -631,9 +644,10 @@ size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H) {
 void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
                   const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, float *out,
                   int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
-                  cudaStream_t s, Launch &L) {
+                  cudaStream_t s, Launch &L, int32_t *assoc) {
   if (E <= 0) return;
   DenseArgs a;
+  a.assoc = assoc;
   a.mp = mp;
   a.fx = K.fx; a.fy = K.fy; a.cx = K.cx; a.cy = K.cy;
   a.ifx = 1.0f / K.fx; a.ify = 1.0f / K.fy;
@@ -671,30 +685,21 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
              kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);
   L.begin(K_DENSE_PREP, s);
-  static int prep_grid = 0;
-  if (prep_grid == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_prep, kDenseThreads, 0);
-    prep_grid = sms * std::max(per_sm, 1);
-  }
+  const int prep_grid = resident_grid((const void *)k_dense_prep, kDenseThreads, 0);
   launch_pdl(k_dense_prep, std::min(prep_grid, a.tiles * mp.n_frames), kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);
   L.begin(K_DENSE_PREP, s);
   launch_pdl(k_dense_scan, mp.n_frames, kDenseThreads, 0, s, a);
   L.end(K_DENSE_PREP, s);
   const size_t smem = kDenseSmem + (size_t)(mp.n_frames + 1 + a.tiles + 1) * 4;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  auto kd = assoc ? k_dense<true> : k_dense<false>;
+  smem_optin((const void *)kd, smem);
+  if (assoc) cudaMemsetAsync(assoc, 0xff, (size_t)E * mp.W * mp.H * sizeof(int32_t), s);   // -1: no source entry
   // one CTA per possible chunk (idle ones exit at once), not persistent: CTA boundaries let the
   // higher-priority match / RANSAC kernels interleave (bt_api.cu register_pairs_dev)
   const int grid = a.tiles * mp.n_frames;
   L.begin(K_DENSE, s);
-  launch_pdl(k_dense, grid, kEdgeThreads, smem, s, a);
+  launch_pdl(kd, grid, kEdgeThreads, smem, s, a);
   L.end(K_DENSE, s);
   L.begin(K_DENSE_REDUCE, s);
   launch_pdl(k_dense_reduce, E, 256, 0, s, a.partials, a.nch, a.tiles, edges, pairs, out, out_stride, records,

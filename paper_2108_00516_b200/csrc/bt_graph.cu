@@ -531,11 +531,7 @@ void launch_graph(int N, const bt_pose *pose, const int32_t *pairs, int P, const
   k_graph_assemble<<<dim3(N, N), kAsmThreads, 0, s>>>(a);
   L.end(K_GRAPH, s);
   const size_t smem = graph_pcg_smem(N);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(k_graph_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  smem_optin((const void *)k_graph_pcg, smem);
   L.begin(K_GRAPH, s);
   k_graph_pcg<<<1, kPcgThreads, smem, s>>>(a);
   L.end(K_GRAPH, s);

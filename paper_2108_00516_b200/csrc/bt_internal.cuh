@@ -94,6 +94,14 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
             cudaGetErrorString(e));
 }
 
+// ---- per-device launch setup (thread-safe, bt_api.cu) ---------------------------------
+// cudaFuncSetAttribute applies to the CURRENT device only, so the dynamic shared-memory opt-in
+// and the occupancy-derived grid sizes are cached per (device, kernel) behind a mutex: a second
+// context on another GPU of the same process (or another host thread) sets its own.
+void smem_optin(const void *kernel, size_t bytes);               // raise the kernel's opt-in if needed
+int sm_count();                                                  // SMs of the current device
+int resident_grid(const void *kernel, int threads, size_t smem); // SMs x max resident CTAs per SM (>= 1 per SM)
+
 // ---- launchers (stream-ordered, no sync) -------------------------------------------
 // matching
 int match_n_pad(int n_max);
@@ -131,7 +139,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
 void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
                   const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, float *out,
                   int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
-                  cudaStream_t s, Launch &L);
+                  cudaStream_t s, Launch &L, int32_t *assoc = nullptr);
 int dense_tiles(int W, int H);
 size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H);
 // Eq. (2) blocks re-linearized at new node poses from the records' inlier masks (C_ij reuse)

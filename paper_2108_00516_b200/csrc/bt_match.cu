@@ -871,29 +871,19 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   const int fs_batched = kp.n_max >= kFsBatchRefs ? 1 : 0;
   TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2, fs_batched};
   L.begin(K_MATCH_TC, s);
-  static int ws_grid = 0;
-  if (ws_grid == 0) {
-    cudaFuncSetAttribute(k_match_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsSmem);
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // two CTAs per SM by design (2 x 108 KB of shared memory, 2 x 256 TMEM columns, 96 registers;
-    // ncu: block limits 2 / 2); the occupancy API reports 1 for this configuration, so the grid
-    // is sized directly (a CTA that does not fit only waits: no CTA depends on another)
-    cudaFuncSetAttribute(k_match_ws, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    ws_grid = sms * 2;
-  }
+  // two CTAs per SM by design (2 x 108 KB of shared memory, 2 x 256 TMEM columns, 96 registers;
+  // ncu: block limits 2 / 2); the occupancy API reports 1 for this configuration, so the grid
+  // is sized directly (a CTA that does not fit only waits: no CTA depends on another)
+  smem_optin((const void *)k_match_ws, kWsSmem);
+  cudaFuncSetAttribute(k_match_ws, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  const int ws_grid = sm_count() * 2;
   launch_pdl(k_match_ws, std::min(ws_grid, 2 * P * rt_count), kWsThreads, kWsSmem, s, *tmap, ta);
   L.end(K_MATCH_TC, s);
   L.begin(K_RESOLVE, s);
   RescoreArgs ra{kp, pairs, S, ibits, ratio2};
   if (fs_batched) {
     FullScanArgs fa{kp, pairs, S, P, n_pad, ibits, ratio2};
-    static bool fs_attr = false;
-    if (!fs_attr) {
-      cudaFuncSetAttribute(k_fullscan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFsSmem);
-      fs_attr = true;
-    }
+    smem_optin((const void *)k_fullscan, kFsSmem);
     launch_pdl(k_fullscan, dim3(n_pad / kFsRows, P, 2), 256, kFsSmem, s, fa);
     L.end(K_RESOLVE, s);
     L.begin(K_RESOLVE, s);

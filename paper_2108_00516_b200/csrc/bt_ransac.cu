@@ -1462,9 +1462,10 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtas) k_score_tc(const __grid_c
       const int h = ht * kTcRows + lrow;
       if (h < A.n_hyp && rc.valid) {
         if (cert) atomicAdd(A.counts + (size_t)p * A.n_hyp + h, (int)cert);
-        if (overflow) {
-          atomicOr(A.ofl + (size_t)p * ((A.n_hyp + 31) / 32) + (h >> 5), 1u << (h & 31));
-          A.fix[atomicAdd(A.ecount + 1, 1)] = make_int2(p, h);
+        if (overflow) {                                            // both warpgroups may overflow one row:
+          const unsigned bit = 1u << (h & 31);                     // only the first to set its bit lists it,
+          if (!(atomicOr(A.ofl + (size_t)p * ((A.n_hyp + 31) / 32) + (h >> 5), bit) & bit))   // so fix holds
+            A.fix[atomicAdd(A.ecount + 1, 1)] = make_int2(p, h);   // <= P * H rows (its capacity)
         }
       }
       it = itn;
@@ -1571,16 +1572,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   if (P <= 0) return;
   const int chunk = kp.n_max < kMaxChunk ? ((kp.n_max + 31) / 32) * 32 : kMaxChunk;   // multiple of 32
   const size_t smem = (size_t)4 * chunk * sizeof(float4);
-  static int score_slots = 0;
-  if (!score_slots) {
-    const int max_smem = (int)(4 * kMaxChunk * sizeof(float4));
-    cudaFuncSetAttribute(k_ransac_score, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    int dev = 0, n_sm = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ransac_score, kScoreThreads, max_smem);
-    score_slots = n_sm * (per_sm > 0 ? per_sm : 1);
-  }
+  const int score_slots = resident_grid((const void *)k_ransac_score, kScoreThreads, 4 * kMaxChunk * sizeof(float4));
   ScoreArgs a;
   a.hyp = (f32x2 *)rs.hyp;
   a.counts = rs.counts;
@@ -1593,11 +1585,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   a.ncosa = -prm.cos_alpha;
   a.tau = prm.min_sigma_ratio;
   const size_t hyp_smem = (size_t)kp.n_max * 6 * sizeof(float);
-  static size_t hyp_attr = 0;
-  if (hyp_smem > hyp_attr) {
-    cudaFuncSetAttribute(k_ransac_hyp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hyp_smem);
-    hyp_attr = hyp_smem;
-  }
+  smem_optin((const void *)k_ransac_hyp, hyp_smem);
   L.begin(K_RANSAC_HYP, s);
   launch_pdl(k_ransac_hyp, dim3((a.nb * kHypPerBlock / kHypThreads + kHypIter - 1) / kHypIter, P), kHypThreads,
              hyp_smem, s, a);
@@ -1625,14 +1613,8 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
     t.pf = (PairFeat *)rs.pfeat; t.feat = (__half *)rs.feat; t.fix = (int2 *)rs.fix; t.ecount = rs.fix_count;
     t.elist = (int4 *)rs.elist; t.ecap = rs.ecap; t.ofl = rs.ofl;
     if (const char *ec = getenv("BT_SCORE_ECAP")) t.ecap = std::max(0, std::min(t.ecap, atoi(ec)));   // tests: overflow path
-    static int tc_grid = 0;
-    if (!tc_grid) {
-      cudaFuncSetAttribute(k_score_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-      int dev = 0, n_sm = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-      tc_grid = n_sm * kTcCtas;                                    // kTcCtas CTAs per SM (TMEM split)
-    }
+    smem_optin((const void *)k_score_tc, kTcSmem);
+    const int tc_grid = sm_count() * kTcCtas;                      // kTcCtas CTAs per SM (TMEM split)
     L.begin(K_RANSAC_SCORE, s);
     launch_pdl(k_corr_feat, P, kFeatThreads, 0, s, t);
     L.end(K_RANSAC_SCORE, s);
@@ -1658,11 +1640,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   L.begin(K_RANSAC_FINISH, s);
   const size_t fin_smem = (size_t)((mask_words(kp.n_max) * 32 + 3) & ~3) * sizeof(int) +
                           (node_pose ? (size_t)kFeatChunk * kFeatRow * sizeof(float) : 0);
-  static size_t fin_attr = 0;
-  if (fin_smem > fin_attr) {
-    cudaFuncSetAttribute(k_ransac_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fin_smem);
-    fin_attr = fin_smem;
-  }
+  smem_optin((const void *)k_ransac_finish, fin_smem);
   launch_pdl(k_ransac_finish, dim3(P, node_pose ? 2 : 1), kFinThreads, fin_smem, s, f);
   L.end(K_RANSAC_FINISH, s);
 }
@@ -1679,11 +1657,7 @@ void launch_feature_edges(const KpView &kp, const int32_t *pairs, int P, const i
   f.rec_stride = rec_stride; f.node_pose = node_pose; f.huber = huber;
   const size_t smem = (size_t)((mask_words(kp.n_max) * 32 + 3) & ~3) * sizeof(int) +
                       (size_t)kFeatChunk * kFeatRow * sizeof(float);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(k_feature_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
+  smem_optin((const void *)k_feature_edges, smem);
   L.begin(K_RANSAC_FINISH, s);
   k_feature_edges<<<P, kFinThreads, smem, s>>>(f);
   L.end(K_RANSAC_FINISH, s);

@@ -139,3 +139,62 @@ def compare_ransac(gpu_counts, rec, orc_counts, pa, na, pb, nb, what=""):
     else:
         assert rec["status"] == fin["status"], f"{what}: status {rec['status']} vs {fin['status']}"
     return fin
+
+
+# ------------------------------------------------- decision-level dense / feature parity
+def dense_decisions(g32, assoc, o72, pix, border, allow, what=""):
+    """Eq. (3) edge compared DECISION by decision, then element by element.
+
+    assoc [H][W]: the GPU's association (bt_dense_assoc: target pixel index or -1); pix /
+    border / allow: the oracle's (bto_dense_edge pix_out / pix_border / pix_allow).
+    * every source pixel outside the band (reading R22) takes the oracle's decision, bit-exact:
+      same target pixel, or rejected on both sides;
+    * count = the number of associated pixels, exactly;
+    * H element-wise within 1e-4 of the oracle's sum of absolute contributions
+      sum w |J_a J_b| (out[48..68]: the magnitude fp summation error is relative to; on the
+      diagonal it IS |H_aa|), g within 1e-4 of sum w |J_k r|, E within 1e-4 relative — plus,
+      only for the borderline pixels whose decision actually differs, twice the largest
+      contribution they can make (pix_allow; both sides may associate them, to different
+      neighbours).
+    Returns (pixels differing, max relative H error)."""
+    g = np.asarray(g32, float)
+    o = np.asarray(o72, float)
+    assoc = np.asarray(assoc)
+    pix = np.asarray(pix)
+    diff = assoc != pix
+    out_band = diff & ~border
+    assert not out_band.any(), (f"{what}: {int(out_band.sum())} pixel decisions differ outside the band, e.g. "
+                                f"{[(int(v), int(u), int(assoc[v, u]), int(pix[v, u])) for v, u in np.argwhere(out_band)[:5]]}")
+    assert g[28] == float((assoc >= 0).sum()), f"{what}: count {g[28]} vs {(assoc >= 0).sum()} associated pixels"
+    assert o[28] == float((pix >= 0).sum())
+    fl = 2.0 * allow[diff].sum(axis=0) if diff.any() else np.zeros(8)
+    dH = np.abs(g[:21] - o[:21])
+    tolH = H_REL_TOL * o[48:69] + fl[0] + 1e-12
+    bad = dH > tolH
+    assert not bad.any(), f"{what}: H[{np.nonzero(bad)[0]}] |dH| {dH[bad]} > tol {tolH[bad]}"
+    dg = np.abs(g[21:27] - o[21:27])
+    tolg = H_REL_TOL * o[32:38] + fl[2:8] + 1e-12
+    bad = dg > tolg
+    assert not bad.any(), f"{what}: g[{np.nonzero(bad)[0]}] |dg| {dg[bad]} > tol {tolg[bad]}"
+    assert abs(g[27] - o[27]) <= H_REL_TOL * abs(o[27]) + fl[1] + 1e-12, f"{what}: E {g[27]} vs {o[27]}"
+    rel = float((dH / np.maximum(o[48:69], 1e-300)).max()) if o[28] > 0 else 0.0
+    return int(diff.sum()), rel
+
+
+def feat_elementwise(g96, o186, what=""):
+    """Eq. (2) blocks element by element against the oracle evaluated on the SAME inlier
+    set: H_ii / H_ij / H_jj within 1e-4 of the oracle's sum w |J_ra J_rb| (out[108..185]), g within
+    1e-4 of sum w |J_k| |e| (out[96..107]), E within 1e-4 relative, count exact.  Returns the max
+    relative H error."""
+    g = np.asarray(g96, float)
+    o = np.asarray(o186, float)
+    assert g[91] == o[91], f"{what}: count {g[91]} vs {o[91]}"
+    dH = np.abs(g[:78] - o[:78])
+    tol = H_REL_TOL * o[108:186] + 1e-12
+    bad = dH > tol
+    assert not bad.any(), f"{what}: H[{np.nonzero(bad)[0][:8]}] |dH| {dH[bad][:8]} > tol {tol[bad][:8]}"
+    dg = np.abs(g[78:90] - o[78:90])
+    bad = dg > H_REL_TOL * o[96:108] + 1e-12
+    assert not bad.any(), f"{what}: g {g[78:90][bad]} vs {o[78:90][bad]}"
+    assert abs(g[90] - o[90]) <= H_REL_TOL * abs(o[90]) + 1e-12, f"{what}: E {g[90]} vs {o[90]}"
+    return float((dH / np.maximum(o[108:186], 1e-300)).max())

@@ -292,21 +292,28 @@ def test_register_pairs_c2_full_size_sampled(bt, torch, ctx, c2):
     uids = np.arange(len(pairs), dtype=np.uint32)
     poses = c2.perturbed_poses(11)
     raw = gpu_register(bt, torch, ctx, c2, pairs, uids, poses, 4096)
-    rec = bt.decode_records(raw, c2.desc.shape[1])
+    n_max = c2.desc.shape[1]
+    mt = torch.zeros((len(pairs), n_max, 2), dtype=torch.int32, device="cuda")
+    nm = torch.zeros(len(pairs), dtype=torch.int32, device="cuda")
+    ctx.copy_matches(mt, nm)                        # the C_ij lists this very call matched
+    torch.cuda.synchronize()
+    mt, nm = mt.cpu().numpy(), nm.cpu().numpy()
+    rec = bt.decode_records(raw, n_max)
     assert (rec["status"] == 0).all()
     for p in (0, 17, 64, 119):
         a, b = pairs[p]
         o = oracle.register_pair(c2, a, b, int(uids[p]), 4096, SEED, node_poses=poses, dense=DENSE,
                                  counts_out=True)
-        assert rec["n_matches"][p] == o["n_matches"]
-        parity.compare_matches(o["match"]["pairs"], o["match"])
+        assert rec["n_matches"][p] == o["n_matches"] == nm[p]
+        parity.compare_matches(mt[p, :nm[p]], o["match"])
         r = {k: v[p] for k, v in rec.items()}
         P_ = o["match"]["pairs"]
         pa, na, pb, nb = _pair_arrays(c2, a, b, P_)
-        fin = parity.compare_ransac(None, r, o["counts"], pa, na, pb, nb, what=f"pair {p}")
-        if fin is not None and np.array_equal(parity.mask_bits(r["mask"], len(P_)),
-                                              parity.mask_bits(o["mask"], len(P_))):
-            parity.assert_feat_close(r["feat"], o["feat"], f"pair {p} feat")
+        parity.compare_ransac(None, r, o["counts"], pa, na, pb, nb, what=f"pair {p}")
+        # Eq. (2) on the GPU's own match list and inlier set: unconditional, element-wise
+        ml = mt[p, :nm[p]]
+        of = oracle.feature_edge(c2.pts[a][ml[:, 0]], c2.pts[b][ml[:, 1]], r["mask"], poses[a], poses[b])
+        parity.feat_elementwise(r["feat"], of, f"pair {p} feat")
         parity.assert_dense_close(r["dense_ij"], o["dense_ij"], f"pair {p} ij")
         parity.assert_dense_close(r["dense_ji"], o["dense_ji"], f"pair {p} ji")
     # determinism: bitwise identical on a second run and under a different batching
@@ -510,3 +517,33 @@ def test_ransac_many_pairs_dynamic_slices(bt, torch):
         pa, na, pb, nb = _pair_arrays(sc, a, b, mls[p])
         oc = oracle.ransac_counts(pa, na, pb, nb, H, int(uids[p]), SEED)
         parity.compare_ransac(cnt[p], {k: v[p] for k, v in rec.items()}, oc, pa, na, pb, nb, what=f"pair {p}")
+
+
+def test_capacity_counts_tiles_and_reserve_drops_match_cache(bt, torch):
+    """a 600x512 map has fewer pixels than a 640x480 reservation but more 32x32 tiles
+    (304 > 300), so the scratch it would carve does not fit -> BT_ECAPACITY, nothing enqueued;
+    and a re-reserve forgets the cached match lists (bt_copy_matches / bt_relinearize refuse)."""
+    c = bt.Context(0)
+    c.reserve(4, 512, 256, 2, 640, 480)
+    sc = synth.make_scene(2, width=600, height=512, seed=3)
+    fb = bt.FrameBatch.from_scene(sc)
+    out = torch.zeros((2, 32), dtype=torch.float32, device="cuda")
+    with pytest.raises(bt.BtError) as e:
+        c.dense_corr(fb, sc.K, _dev(torch, sc.node_poses()), _dev(torch, np.array([[0, 1], [1, 0]], np.int32)),
+                     bt.edge_params(), out)
+    assert e.value.status == bt.BT_ECAPACITY
+    ok = synth.make_scene(2, seed=3)
+    fb = bt.FrameBatch.from_scene(ok)
+    pr = _dev(torch, np.array([[0, 1]], np.int32))
+    rec = torch.zeros((1, bt.record_words(512)), dtype=torch.int32, device="cuda")
+    c.register_pairs(fb, ok.K, _dev(torch, ok.node_poses()), pr, _dev(torch, np.zeros(1, np.int32)),
+                     bt.ransac_params(256, SEED), bt.edge_params(), rec)
+    mt = torch.zeros((1, 512, 2), dtype=torch.int32, device="cuda")
+    nm = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c.copy_matches(mt, nm)
+    c.reserve(4, 512, 256, 2, 640, 480)
+    with pytest.raises(bt.BtError) as e:
+        c.copy_matches(mt, nm)
+    assert e.value.status == bt.BT_EINVAL
+    torch.cuda.synchronize()
+    c.close()
