@@ -9,6 +9,11 @@ blocks -> both directed Eq. (3) dense edges (240).  Under torchrun each rank run
 track (weak scaling) and the per-pair records are all-gathered over NCCL (the exchange the
 pose-graph solve needs).
 
+Beside the headline, the line carries SURVEY §8(e)'s sharded configurations, strong scaling
+(fixed total work split over the N ranks, records all-gathered over NCCL, max over ranks):
+`c4` = BASELINE configs[3], 64 tracks x 120 pairs track-major (default; --no-c4 skips it) and,
+with --c5, `c5` = configs[4], 2016 pairs of n = 4096 keypoints in contiguous pair blocks.
+
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (oracle/, plain C,
 fp64) on a bounded sample of the same workload instead.
 """
@@ -54,6 +59,12 @@ def parse():
                     help="launch the step's kernels one by one instead of replaying it as a CUDA graph")
     ap.add_argument("--no-kernel-events", action="store_true",
                     help="time the step without the per-kernel CUDA-event brackets (overhead check)")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 multi-track block")
+    ap.add_argument("--c4-steps", type=int, default=10)
+    ap.add_argument("--c4-scenes", type=int, default=8,
+                    help="distinct synthetic scenes the 64 tracks cycle through (bounds CPU scene generation)")
+    ap.add_argument("--c5", action="store_true", help="add the C5 stress block (n=4096, 2016 pairs; slow to generate)")
+    ap.add_argument("--c5-steps", type=int, default=3)
     return ap.parse_args()
 
 
@@ -65,6 +76,119 @@ def workload(rank: int):
     uids = (rank * len(pairs) + np.arange(len(pairs))).astype(np.uint32)
     poses = sc.perturbed_poses(seed=1000 + rank)
     return sc, pairs, uids, poses
+
+
+C4_TRACKS = 64
+
+
+def multi_block(kind, args, bt, parallel, torch, dist, world, rank, local, dev, flush):
+    """SURVEY §8(e)'s sharded configurations, timed like the headline (L2 flushed before each
+    step outside the events, CUDA events on the launching stream, barrier + synchronize on both
+    sides, max over ranks), each step = this rank's bt_register_pairs + the NCCL
+    all_gather_into_tensor of the records (the exchange the pose-graph solve needs).  Strong
+    scaling: the total work is fixed, each rank takes its share.
+      c4: BASELINE configs[3] — 64 tracks x 120 pairs (the C2 step of every track), track-major:
+          rank r holds only its 64/N tracks' frames (no input replication);
+      c5: BASELINE configs[4] — 64 frames, n = 4096, 2016 pairs, 16384 hypotheses, pair blocks:
+          frames replicated, rank r registers the contiguous block shard_range(2016, N, r)."""
+    t0 = time.perf_counter()
+    if kind == "c4":
+        S = max(1, args.c4_scenes)
+        tp = synth.all_pairs(N_FRAMES)
+        plan = parallel.track_plan(C4_TRACKS, N_FRAMES, tp, world, rank)
+        t_lo, t_hi = plan.frame_lo // N_FRAMES, plan.frame_hi // N_FRAMES
+        need = sorted({t % S for t in range(t_lo, t_hi)})
+        scenes = {s_: synth.make_scene(N_FRAMES, n=N_KP, n_max=N_MAX, width=W, height=H, seed=synth.DATA_SEED + 100 + s_)
+                  for s_ in need}
+        tsc = [scenes[t % S] for t in range(t_lo, t_hi)]
+        poses = np.concatenate([tsc[t - t_lo].perturbed_poses(seed=2000 + t) for t in range(t_lo, t_hi)])
+        n_max, n_hyp, steps, K = N_MAX, N_HYP, args.c4_steps, tsc[0].K
+        workload_ = (f"C4: {C4_TRACKS} tracks x {len(tp)} pairs = {C4_TRACKS * len(tp)} pairs per step "
+                     f"({C4_TRACKS * N_FRAMES} frames, {2 * C4_TRACKS * len(tp)} dense edges, 640x480, n=500, "
+                     f"{N_HYP} hypotheses/pair), track-major: {t_hi - t_lo} tracks on this rank; tracks cycle "
+                     f"through {S} distinct synthetic scenes, each with its own node poses and global pair uids")
+
+        def field(f):
+            return torch.cat([torch.from_numpy(np.ascontiguousarray(getattr(x, f))).to(dev) for x in tsc], 0)
+    else:
+        sc = synth.make_scene(64, n=4096, n_max=4096, pool_size=14000, seed=5005, outlier_frac=0.16)
+        pairs_all = synth.all_pairs(64)
+        plan = parallel.pair_block_plan(pairs_all, 64, world, rank)
+        poses = sc.perturbed_poses(7)
+        n_max, n_hyp, steps, K = 4096, 16384, args.c5_steps, sc.K
+        workload_ = (f"C5: 64 frames, n=4096, {len(pairs_all)} pairs ({2 * len(pairs_all)} dense edges at 640x480), "
+                     f"16384 hypotheses/pair; pair blocks: pairs [{plan.row_lo}, {plan.row_lo + len(plan.pairs)}) on "
+                     "this rank, frames replicated")
+
+        def field(f):
+            return torch.from_numpy(np.ascontiguousarray(getattr(sc, f))).to(dev)
+    gen_s = time.perf_counter() - t0
+    fb = bt.FrameBatch(*(field(f) for f in ("n_kp", "desc", "pts", "nrm", "depth", "normal", "mask")))
+    P_r = len(plan.pairs)
+    n_total = int(sum(plan.rows))
+    t_pairs = torch.from_numpy(plan.pairs).to(dev)
+    t_uid = torch.from_numpy(plan.uids.view(np.int32)).to(dev)
+    t_pose = torch.from_numpy(np.ascontiguousarray(poses)).to(dev)
+    rec = torch.zeros((P_r, bt.record_words(n_max)), dtype=torch.int32, device=dev)
+    ctx = bt.Context(local)
+    ctx.reserve(max(P_r, 1), n_max, n_hyp, int(fb.desc.shape[0]), W, H)
+    rprm, eprm = bt.ransac_params(n_hyp, synth.PHILOX_SEED), bt.edge_params()
+    stream = torch.cuda.current_stream(dev)
+    gathered = [None]
+
+    def one():
+        if P_r:
+            ctx.register_pairs(fb, K, t_pose, t_pairs, t_uid, rprm, eprm, rec, stream=stream)
+        if world > 1:
+            gathered[0] = parallel.all_gather_rows(rec, plan.rows)
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    launches = ctx.last_launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    gx = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            if P_r:
+                ctx.register_pairs(fb, K, t_pose, t_pairs, t_uid, rprm, eprm, rec, stream=stream)
+            gx[k][0].record(stream)
+            if world > 1:
+                gathered[0] = parallel.all_gather_rows(rec, plan.rows)
+            gx[k][1].record(stream)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    gms = float(sum(a.elapsed_time(b) for a, b in gx))
+    t_ = torch.tensor([ms, gms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+    ms_max, gms_max = float(t_[0].item()), float(t_[1].item())
+    d = bt.decode_records(rec, n_max)
+    ok = torch.tensor([int((d["status"] == 0).sum()), int(d["n_matches"].astype(np.int64).sum())],
+                      dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(ok)
+        assert gathered[0].shape[0] == n_total
+    ctx.close()
+    del fb, rec
+    torch.cuda.empty_cache()
+    sec = ms_max / 1e3
+    return {"workload": workload_, "pairs_per_step": n_total, "value": n_total * steps / sec, "unit": UNIT,
+            "hypotheses_per_s": n_total * n_hyp * steps / sec, "tests_per_s": float(ok[1].item()) * n_hyp * steps / sec,
+            "ms_per_step": ms_max / steps, "exchange_ms_per_step": gms_max / steps, "steps": steps, "warmup": 2,
+            "scaling": "strong", "n_gpus": world, "pairs_this_rank": P_r, "status_ok": int(ok[0].item()),
+            "gpu_launches": launches * steps, "clocks": clk.summary(), "scene_generation_s": gen_s,
+            "exchange": f"one all_gather_into_tensor of the fixed-stride records ({4 * bt.record_words(n_max)} B "
+                        f"per pair, {n_total} pairs) over NCCL" if world > 1 else "none (one rank)",
+            "l2": "flushed (512 MiB memset) before each step, outside the events",
+            "launch": "eager (the step is ms-long; launch overhead is negligible)"}
 
 
 def dense_params():
@@ -137,6 +261,40 @@ def oracle_pairs_per_s(sc, pairs, uids, poses, sample_pairs):
                              dense=dense_params())
     dt = time.perf_counter() - t0
     return len(sample_pairs) / dt, dt
+
+
+_ORC = None
+
+
+def _oracle_one(p):
+    sc, pairs, uids, poses = _ORC
+    import oracle
+    a, b = pairs[p]
+    oracle.register_pair(sc, int(a), int(b), int(uids[p]), N_HYP, synth.PHILOX_SEED, node_poses=poses,
+                         dense=dense_params())
+    return p
+
+
+def oracle_all_cores(sc, pairs, uids, poses, sample_pairs, reps=3):
+    """The same oracle, unchanged (each pair's registration stays plain and serial), over all
+    host cores: a process per core, pairs handed out one at a time ("all cores
+    with OpenMP parallel for over pairs/edges" — processes instead of threads, same partition).
+    Returns (pairs/s, cores, seconds of the timed reps)."""
+    import multiprocessing as mp
+    global _ORC
+    import oracle
+    oracle.build()
+    oracle.lib()
+    _ORC = (sc, pairs, uids, poses)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_oracle_one, list(sample_pairs)[:cores], chunksize=1)        # warm the workers
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            pool.map(_oracle_one, list(sample_pairs), chunksize=1)
+        dt = time.perf_counter() - t0
+    _ORC = None
+    return reps * len(sample_pairs) / dt, cores, dt
 
 
 def cpu_model():
@@ -470,6 +628,10 @@ def main():
                 "frac": nbytes / (t_ms * 1e-3) / 1e9 / hbm_peak, "l2": "flushed + cleaned before each call"}
         del clean
 
+    # ---- the sharded multi-track / stress configurations ---------------------
+    c4 = None if args.no_c4 else multi_block("c4", args, bt, parallel, torch, dist, world, rank, local, dev, flush)
+    c5 = multi_block("c5", args, bt, parallel, torch, dist, world, rank, local, dev, flush) if args.c5 else None
+
     # ---- end to end through the C ABI with pinned HOST buffers -------------------------
     e2e = None
     if not args.no_e2e:
@@ -516,6 +678,13 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu": cpu_model(),
                "sample": f"the full C2 step ({len(sample)} pairs: matching, {N_HYP}-hypothesis RANSAC, refit, "
                          f"Eq.(2) blocks, 240 dense edges), single-threaded C fp64, {dt:.1f} s"}
+        try:
+            va, cores, dta = oracle_all_cores(sc, pairs, uids, poses, sample)
+            cpu["all_cores"] = {"value": va, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                "sample": f"the full C2 step x 3, one process per core, pairs handed out one at a "
+                                          f"time (the per-pair oracle unchanged), {dta:.1f} s"}
+        except Exception as e:                         # pragma: no cover (host without fork)
+            cpu["all_cores"] = {"unavailable": str(e)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -532,7 +701,7 @@ def main():
                 "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
                 "roofline": roof, "kernels": kern, "kernel_ms_per_step": step_ms_by_kernel,
                 "e2e": e2e, "cpu_baseline": cpu, "next_pose_graph": graph,
-                "next_input_prep": prep}
+                "next_input_prep": prep, "c4": c4, "c5": c5}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -80,6 +80,9 @@ def _setup(L):
                                  C.c_double, C.c_double, C.c_double, C.c_int32, _f64p, _vp, _vp, _vp]
     L.bto_estimate_normals.argtypes = [_f32p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
                                        C.c_double, C.c_float, _f32p]
+    L.bto_lift_keypoints.argtypes = [C.c_int32, C.c_int32, C.c_int32, _f32p, _f32p, _vp, _f32p, _f32p, _u8p,
+                                     C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double, _vp,
+                                     _f32p, _f32p, _f32p, _vp]
     L.bto_se3_exp.argtypes = [_f64p, _f64p, _f64p]
     L.bto_se3_adjoint.argtypes = [_f64p, _f64p, _f64p]
     L.bto_graph_system.restype = C.c_int32
@@ -339,3 +342,26 @@ def estimate_normals(depth, K, jump: float = 0.05) -> np.ndarray:
     lib().bto_estimate_normals(d.reshape(-1), F, W, H, float(K.fx), float(K.fy), float(K.cx), float(K.cy),
                                float(jump), out.reshape(-1))
     return out[0] if squeeze else out
+
+
+# ------------------------------------------------------------ NEXT-4: keypoint lifting
+def lift_keypoints(uv, desc, n_in, depth, normal, mask, K):
+    """The keypoints' 3-D points and normals from their pixels (bto_lift_keypoints, reading R29;
+    P:25, P:72 pi_D^-1): uv [F][n_max][2], desc [F][n_max][dim], n_in [F]; maps
+    [F][H][W](.., 3).  Returns dict(n [F], desc, pts, nrm [F][n_max][..] (rows >= n zero),
+    border [F][n_max] bool)."""
+    uv = _c(uv, np.float32)
+    desc = _c(desc, np.float32)
+    F, n_max, dim = desc.shape
+    depth = _c(depth, np.float32)
+    Fd, H, W = depth.shape
+    n_out = np.zeros(F, np.int32)
+    od = np.zeros_like(desc)
+    pts = np.zeros((F, n_max, 3), np.float32)
+    nrm = np.zeros((F, n_max, 3), np.float32)
+    bd = np.zeros((F, n_max), np.uint8)
+    lib().bto_lift_keypoints(F, n_max, dim, uv.reshape(-1), desc.reshape(-1), _ptr(_c(n_in, np.int32)),
+                             depth.reshape(-1), _c(normal, np.float32).reshape(-1), _c(mask, np.uint8).reshape(-1),
+                             W, H, float(K.fx), float(K.fy), float(K.cx), float(K.cy), _ptr(n_out), od.reshape(-1),
+                             pts.reshape(-1), nrm.reshape(-1), _ptr(bd))
+    return dict(n=n_out, desc=od, pts=pts, nrm=nrm, border=bd.astype(bool))

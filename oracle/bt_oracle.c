@@ -844,6 +844,40 @@ int32_t bto_graph_step(int32_t n_nodes, const float *poses, const int32_t *pairs
   return st;
 }
 
+/* ============================================================ NEXT-4: keypoint lifting (R29) */
+void bto_lift_keypoints(int32_t F, int32_t n_max, int32_t dim, const float *uv, const float *desc_in,
+                        const int32_t *n_in, const float *depth, const float *normal, const uint8_t *mask,
+                        int32_t W, int32_t H, double fx, double fy, double cx, double cy, int32_t *n_out,
+                        float *desc, float *pts, float *nrm, uint8_t *border) {
+  for (int32_t f = 0; f < F; ++f) {
+    int32_t m = 0;
+    const int32_t n = n_in[f] < n_max ? n_in[f] : n_max;
+    for (int32_t k = 0; k < n; ++k) {
+      const size_t in = (size_t)f * n_max + k;
+      const double u = uv[2 * in], v = uv[2 * in + 1];
+      const double xu = floor(u + 0.5), xv = floor(v + 0.5);   /* nearest pixel (R14) */
+      if (border) {
+        const double fu = u + 0.5 - xu, fv = v + 0.5 - xv;
+        border[in] = fu <= band(u + 0.5) || 1.0 - fu <= band(u + 0.5) || fv <= band(v + 0.5) ||
+                     1.0 - fv <= band(v + 0.5);
+      }
+      if (!(xu >= 0.0 && xu < W && xv >= 0.0 && xv < H)) continue;
+      const size_t px = (size_t)f * W * H + (size_t)xv * W + (size_t)xu;
+      const double d = depth[px];
+      const float *nm = normal + 3 * px;
+      if (!mask[px] || !(d > 0.0) || (nm[0] == 0.f && nm[1] == 0.f && nm[2] == 0.f)) continue;
+      const size_t o = (size_t)f * n_max + m;
+      pts[3 * o + 0] = (float)((u - cx) * d / fx);         /* pi_D^-1 at the keypoint */
+      pts[3 * o + 1] = (float)((v - cy) * d / fy);
+      pts[3 * o + 2] = (float)d;
+      for (int c = 0; c < 3; ++c) nrm[3 * o + c] = nm[c];
+      for (int32_t c = 0; c < dim; ++c) desc[o * dim + c] = desc_in[in * dim + c];
+      ++m;
+    }
+    n_out[f] = m;
+  }
+}
+
 /* ======================================================================= NEXT-4: normals */
 void bto_estimate_normals(const float *depth, int32_t F, int32_t W, int32_t H, double fx, double fy,
                           double cx, double cy, float jump, float *normal) {

@@ -163,6 +163,25 @@ int32_t bto_graph_step(int32_t n_nodes, const float *poses, const int32_t *pairs
 void bto_estimate_normals(const float *depth, int32_t F, int32_t W, int32_t H, double fx, double fy,
                           double cx, double cy, float jump, float *normal);
 
+/* ---- NEXT-4: keypoint lifting — the keypoints' 3-D points and normals from their pixels
+   ("n keypoints x_i ... along with the feature descriptor D_i"; "pi_D^-1 ... recovers
+   a 3D point in the camera's frame by looking up the depth value on the pixel location";
+   n_i(x) "returns the normal of the pixel"; SPEC Keypoint invariant S:247 point =
+   unproject(pixel, depth), detect_keypoints S:262 "inside the mask with valid depth").
+   Reading R29: keypoint k of frame f at (u, v) (float pixel coordinates, centres at integers)
+   looks up the pixel x' = (floor(u + 0.5), floor(v + 0.5)) (R14's rounding); it is KEPT iff x'
+   lies in the frame, mask(x') != 0, depth(x') = d > 0 and normal(x') != 0; then
+   point = ((u - cx) d / fx, (v - cy) d / fy, d) (fp64, rounded to float) and normal =
+   normal(x').  Kept keypoints are compacted in their input order with their descriptors.
+   uv [F][n_max][2], desc_in [F][n_max][dim], n_in [F]; maps [F][H][W] (normal [..][3]).
+   Out: n_out [F], desc [F][n_max][dim], pts / nrm [F][n_max][3] (rows >= n_out untouched),
+   border [F][n_max] (may be NULL): 1 iff input keypoint k's rounding is borderline (band rule
+   R22: u + 0.5 or v + 0.5 within 1e-6 max(1, |.|) of an integer). */
+void bto_lift_keypoints(int32_t F, int32_t n_max, int32_t dim, const float *uv, const float *desc_in,
+                        const int32_t *n_in, const float *depth, const float *normal, const uint8_t *mask,
+                        int32_t W, int32_t H, double fx, double fy, double cx, double cy, int32_t *n_out,
+                        float *desc, float *pts, float *nrm, uint8_t *border);
+
 #ifdef __cplusplus
 }
 #endif

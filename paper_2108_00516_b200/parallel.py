@@ -5,9 +5,21 @@ data-path collective: every rank registers its own block of pairs — Philox is 
 GLOBAL pair uid, so each record is bitwise identical whichever rank computes it — and the
 fixed-stride per-pair records are exchanged once with all_gather_into_tensor (NCCL over
 NVLink / NVSwitch on B200; gloo in the CPU tests).  This is the exchange the pose-graph solve
- needs: every rank then holds every edge's blocks.
+ needs: every rank then holds every edge's blocks.  The paper builds the
+pairs' correspondences "in parallel on GPU" on one GPU (§IV-D); the sharding
+over GPUs is this build's.
+
+Two partitions:
+  * track-major (C4, `track_plan`): rank r owns whole tracks (their frames' maps and keypoints
+    stay resident on that rank only; no input replication), 64 / G tracks each;
+  * pair blocks (C5, `pair_block_plan`): the frames are replicated, rank r registers the
+    contiguous global pair-id block shard_range(P, G, r).
 """
 from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
 
 
 def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -25,29 +37,76 @@ def shard_capacity(n: int, world: int) -> int:
     return -(-n // world) if world > 0 else 0
 
 
-def all_gather_records(local, n_total: int, group=None):
-    """All-gather per-pair records sharded by shard_range.  `local` is this rank's
-    [hi - lo][words] tensor; returns the [n_total][words] tensor in global pair order on every
-    rank.  Shards are padded to a common size for the single all_gather_into_tensor call."""
+@dataclass
+class ShardPlan:
+    """One rank's share of a multi-pair batch.
+
+    frame_lo / frame_hi: the global frames this rank needs resident ([lo, hi));
+    pairs: [P_r][2] int32 frame ids RELATIVE to frame_lo (what bt_register_pairs receives);
+    uids: [P_r] uint32 global pair ids (the Philox counter word: shard-invariant records);
+    rows: per-rank record counts (identical on every rank; the gather's layout);
+    row_lo: this rank's first global record row."""
+    frame_lo: int
+    frame_hi: int
+    pairs: np.ndarray
+    uids: np.ndarray
+    rows: list
+    row_lo: int
+
+
+def track_plan(n_tracks: int, frames_per_track: int, track_pairs: np.ndarray, world: int, rank: int,
+               uid_base: int = 0) -> ShardPlan:
+    """Track-major partition (C4): tracks shard_range(n_tracks, world, rank); track t's frames are
+    [t F, (t + 1) F) globally, its pairs track_pairs + t F, its global pair uids
+    uid_base + t |track_pairs| + k — so the rank's records are rows [t_lo |tp|, t_hi |tp|) of the
+    unsharded batch, in order."""
+    tp = np.asarray(track_pairs, np.int32).reshape(-1, 2)
+    t_lo, t_hi = shard_range(n_tracks, world, rank)
+    F, k = frames_per_track, len(tp)
+    pairs = np.concatenate([tp + F * (t - t_lo) for t in range(t_lo, t_hi)]) if t_hi > t_lo else np.zeros((0, 2), np.int32)
+    uids = (uid_base + k * t_lo + np.arange(k * (t_hi - t_lo))).astype(np.uint32)
+    rows = [k * (b - a) for a, b in (shard_range(n_tracks, world, r) for r in range(world))]
+    return ShardPlan(F * t_lo, F * t_hi, pairs.astype(np.int32), uids, rows, k * t_lo)
+
+
+def pair_block_plan(pairs: np.ndarray, n_frames: int, world: int, rank: int, uid_base: int = 0) -> ShardPlan:
+    """Pair-block partition (C5): the global pair list cut into contiguous blocks
+    shard_range(P, world, rank); every rank holds all n_frames frames (replicated inputs)."""
+    pr = np.asarray(pairs, np.int32).reshape(-1, 2)
+    lo, hi = shard_range(len(pr), world, rank)
+    rows = [b - a for a, b in (shard_range(len(pr), world, r) for r in range(world))]
+    return ShardPlan(0, n_frames, pr[lo:hi].copy(), (uid_base + np.arange(lo, hi)).astype(np.uint32), rows, lo)
+
+
+def all_gather_rows(local, rows, group=None):
+    """All-gather a row-sharded tensor: rank r holds rows[r] rows (`rows` identical on every rank,
+    in rank order).  One all_gather_into_tensor of shards padded to max(rows); returns the
+    [sum(rows)][...] tensor in global row order on every rank."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    cap = shard_capacity(n_total, world)
-    lo, hi = shard_range(n_total, world, rank)
-    if local.shape[0] != hi - lo:
-        raise ValueError(f"rank {rank}: {local.shape[0]} local records, shard has {hi - lo}")
+    if len(rows) != world:
+        raise ValueError(f"{len(rows)} shard sizes for world size {world}")
+    if local.shape[0] != rows[rank]:
+        raise ValueError(f"rank {rank}: {local.shape[0]} local records, shard has {rows[rank]}")
+    cap = max(rows) if rows else 0
     send = local
     if local.shape[0] != cap:
         send = torch.zeros((cap,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
         send[: local.shape[0]] = local
     out = torch.empty((world * cap,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, send.contiguous(), group=group)
-    if cap * world == n_total:
+    if all(r == cap for r in rows):
         return out
-    parts = []
-    for r in range(world):
-        a, b = shard_range(n_total, world, r)
-        parts.append(out[r * cap: r * cap + (b - a)])
-    return torch.cat(parts, 0)
+    return torch.cat([out[r * cap: r * cap + rows[r]] for r in range(world)], 0)
+
+
+def all_gather_records(local, n_total: int, group=None):
+    """All-gather per-pair records sharded by shard_range(n_total, world, rank)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rows = [b - a for a, b in (shard_range(n_total, world, r) for r in range(world))]
+    return all_gather_rows(local, rows, group)
