@@ -626,6 +626,30 @@ def main():
                 "ms_per_call": t_ms, "bound": "hbm", "bytes_per_call": nbytes,
                 "achieved_gbs": nbytes / (t_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
                 "frac": nbytes / (t_ms * 1e-3) / 1e9 / hbm_peak, "l2": "flushed + cleaned before each call"}
+        # keypoint lifting (bt_lift_keypoints): the detector's 2-D keypoints (each keypoint's
+        # projection, sub-pixel) + descriptors + the maps -> the registration inputs
+        p_ = sc.pts.astype(np.float64)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            uv_ = np.stack([sc.K.fx * p_[..., 0] / p_[..., 2] + sc.K.cx, sc.K.fy * p_[..., 1] / p_[..., 2] + sc.K.cy], -1)
+        uv_t = torch.from_numpy(np.nan_to_num(uv_, nan=-10.0).astype(np.float32)).to(dev)
+        lo_ = bt.FrameBatch(torch.zeros_like(fb.n_kp), torch.empty_like(fb.desc), torch.empty_like(fb.pts),
+                            torch.empty_like(fb.nrm))
+        for _ in range(3):
+            ctx.lift_keypoints(uv_t, fb.desc, fb.n_kp, fb, sc.K, lo_, stream=stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+        for a_, b_ in ev:
+            flush.zero_()
+            clean.sum()
+            a_.record(stream)
+            ctx.lift_keypoints(uv_t, fb.desc, fb.n_kp, fb, sc.K, lo_, stream=stream)
+            b_.record(stream)
+        torch.cuda.synchronize()
+        l_ms = float(np.median([a_.elapsed_time(b_) for a_, b_ in ev]))
+        nk = int(sc.n_kp.sum())
+        lbytes = nk * (8 + 512 + 512 + 24 + 17)
+        prep["lift"] = {"api": "bt_lift_keypoints", "keypoints": nk, "kept": int(lo_.n_kp.sum().item()),
+                        "ms_per_call": l_ms, "bound": "latency (one CTA per frame; ~9 MB)",
+                        "bytes_per_call": lbytes, "achieved_gbs": lbytes / (l_ms * 1e-3) / 1e9}
         del clean
 
     # ---- the sharded multi-track / stress configurations ---------------------

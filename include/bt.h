@@ -266,6 +266,25 @@ bt_status bt_relinearize_matches(bt_ctx *ctx, const bt_keypoints *kp, const bt_m
 bt_status bt_estimate_normals(bt_ctx *ctx, const float *depth, int32_t n_frames, int32_t width, int32_t height,
                               const bt_intrinsics *K, float jump_m, float *normal, void *stream);
 
+/* ---- NEXT-4: input prep — keypoint lifting ("n keypoints x_i ... along with the feature
+   descriptor D_i"; "pi_D^-1 ... recovers a 3D point in the camera's frame by looking up
+   the depth value on the pixel location", n_i(x) "returns the normal of the pixel"
+   point = unproject(pixel, depth), S:262 keypoints "inside the mask with valid depth") --------
+   uv [F][n_max][2] f32 (pixel coordinates, centres at integers), desc_in [F][n_max][dim] f32,
+   n_in [F]: the detector's raw output; maps: depth / normal (e.g. bt_estimate_normals) / mask
+   of the same frames.  Keypoint k of frame f looks up x' = (floor(u + 0.5), floor(v + 0.5))
+   (reading R29); it is kept iff x' is in the frame, mask(x') != 0, depth(x') = d > 0 and
+   normal(x') != 0, with point ((u - cx) d / fx, (v - cy) d / fy, d) (fp64, rounded) and
+   normal(x').  Out (device, caller-owned, NOT aliasing the inputs): n_kp [F], desc
+   [F][n_max][dim], pts / nrm [F][n_max][3] — the kept keypoints compacted in input order (rows
+   >= n_kp[f] are not written): exactly the bt_keypoints of the registration calls.
+   Errors: BT_EUNSUPPORTED if dim != 128; BT_EINVAL for NULL / misaligned (16 B: uv, desc)
+   buffers, maps that do not cover n_frames or mismatch K, n_max < 1. */
+bt_status bt_lift_keypoints(bt_ctx *ctx, int32_t n_frames, int32_t n_max, int32_t dim, const float *uv,
+                            const float *desc_in, const int32_t *n_in, const bt_maps *maps,
+                            const bt_intrinsics *K, int32_t *n_kp, float *desc, float *pts, float *nrm,
+                            void *stream);
+
 /* number of kernels the last bt_* call enqueued (for the bench's gpu_launches claim) */
 int32_t bt_last_launch_count(const bt_ctx *ctx);
 

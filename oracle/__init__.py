@@ -365,3 +365,46 @@ def lift_keypoints(uv, desc, n_in, depth, normal, mask, K):
                              W, H, float(K.fx), float(K.fy), float(K.cx), float(K.cy), _ptr(n_out), od.reshape(-1),
                              pts.reshape(-1), nrm.reshape(-1), _ptr(bd))
     return dict(n=n_out, desc=od, pts=pts, nrm=nrm, border=bd.astype(bool))
+
+
+# ------------------------------------------------------------ NEXT-2: tracker decisions
+def _setup_track(L):
+    L.bto_rot_geodesic.argtypes = [_f32p, _f32p]
+    L.bto_rot_geodesic.restype = C.c_double
+    L.bto_coarse_pose.argtypes = [C.c_int32, _f32p, _f32p, _f32p]
+    L.bto_select_keyframes.argtypes = [_f32p, C.c_int32, _f32p, C.c_int32, _vp]
+    L.bto_select_keyframes.restype = C.c_int32
+    L.bto_is_novel.argtypes = [_f32p, C.c_int32, _f32p, C.c_double]
+    L.bto_is_novel.restype = C.c_int32
+    return L
+
+
+def rot_geodesic(Ta, Tb) -> float:
+    """arccos((tr(R_a^T R_b) - 1) / 2)."""
+    return float(_setup_track(lib()).bto_rot_geodesic(_c(Ta, np.float32).reshape(-1), _c(Tb, np.float32).reshape(-1)))
+
+
+def coarse_pose(status: int, T_best, T_prev) -> np.ndarray:
+    """T~_t = T_rel . T_prev with T_rel the best sampled hypothesis (reading R13); T_prev
+    when the pair has none (status FEW_MATCHES / FEW_INLIERS)."""
+    out = np.zeros(12, np.float32)
+    _setup_track(lib()).bto_coarse_pose(int(status), _c(T_best, np.float32).reshape(-1),
+                                        _c(T_prev, np.float32).reshape(-1), out)
+    return out
+
+
+def select_keyframes(pool, cur, K: int) -> np.ndarray:
+    """Greedy keyframe selection of P:39 over pool poses [N][12] for the current pose: pool
+    indices in selection order (I_0 first)."""
+    pool = _c(pool, np.float32).reshape(-1, 12)
+    sel = np.zeros(max(K, 1), np.int32)
+    n = _setup_track(lib()).bto_select_keyframes(pool.reshape(-1) if len(pool) else np.zeros(12, np.float32),
+                                                 len(pool), _c(cur, np.float32).reshape(-1), int(K), _ptr(sel))
+    return sel[:n]
+
+
+def is_novel(pool, cur, thresh_rad=float(np.deg2rad(10.0))) -> bool:
+    """the current pose is farther than thresh from every pool keyframe (rotation geodesic)."""
+    pool = _c(pool, np.float32).reshape(-1, 12)
+    return bool(_setup_track(lib()).bto_is_novel(pool.reshape(-1) if len(pool) else np.zeros(12, np.float32),
+                                                 len(pool), _c(cur, np.float32).reshape(-1), float(thresh_rad)))

@@ -844,6 +844,59 @@ int32_t bto_graph_step(int32_t n_nodes, const float *poses, const int32_t *pairs
   return st;
 }
 
+/* ============================================================ NEXT-2: tracker decisions */
+double bto_rot_geodesic(const float Ta[12], const float Tb[12]) {
+  double tr = 0.0;                                        /* tr(Ra^T Rb) = sum_ij Ra_ij Rb_ij */
+  for (int k = 0; k < 9; ++k) tr += (double)Ta[k] * (double)Tb[k];
+  double c = (tr - 1.0) / 2.0;
+  if (c > 1.0) c = 1.0;
+  if (c < -1.0) c = -1.0;
+  return acos(c);
+}
+
+void bto_coarse_pose(int32_t status, const float T_best[12], const float T_prev[12], float out[12]) {
+  if (status != 0 && status != 3) {                       /* no sampled hypothesis */
+    for (int k = 0; k < 12; ++k) out[k] = T_prev[k];
+    return;
+  }
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) {
+      double x = 0.0;
+      for (int k = 0; k < 3; ++k) x += (double)T_best[3 * r + k] * (double)T_prev[3 * k + c];
+      out[3 * r + c] = (float)x;
+    }
+    double y = T_best[9 + r];
+    for (int k = 0; k < 3; ++k) y += (double)T_best[3 * r + k] * (double)T_prev[9 + k];
+    out[9 + r] = (float)y;
+  }
+}
+
+int32_t bto_select_keyframes(const float *pool, int32_t n_pool, const float cur[12], int32_t K, int32_t *sel) {
+  if (n_pool <= 0 || K <= 0) return 0;
+  int32_t n_sel = 0;
+  sel[n_sel++] = 0;                                       /* I_0 */
+  while (n_sel < K && n_sel < n_pool) {
+    int32_t best = -1;
+    double best_s = 0.0;
+    for (int32_t k = 0; k < n_pool; ++k) {
+      int taken = 0;
+      for (int32_t q = 0; q < n_sel; ++q) taken |= sel[q] == k;
+      if (taken) continue;
+      double s = bto_rot_geodesic(pool + 12 * k, cur);
+      for (int32_t q = 0; q < n_sel; ++q) s += bto_rot_geodesic(pool + 12 * k, pool + 12 * sel[q]);
+      if (best < 0 || s < best_s) { best = k; best_s = s; }
+    }
+    sel[n_sel++] = best;
+  }
+  return n_sel;
+}
+
+int32_t bto_is_novel(const float *pool, int32_t n_pool, const float cur[12], double thresh_rad) {
+  for (int32_t k = 0; k < n_pool; ++k)
+    if (!(bto_rot_geodesic(pool + 12 * k, cur) > thresh_rad)) return 0;
+  return 1;
+}
+
 /* ============================================================ NEXT-4: keypoint lifting (R29) */
 void bto_lift_keypoints(int32_t F, int32_t n_max, int32_t dim, const float *uv, const float *desc_in,
                         const int32_t *n_in, const float *depth, const float *normal, const uint8_t *mask,

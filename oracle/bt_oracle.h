@@ -182,6 +182,23 @@ void bto_lift_keypoints(int32_t F, int32_t n_max, int32_t dim, const float *uv, 
                         int32_t W, int32_t H, double fx, double fy, double cx, double cy, int32_t *n_out,
                         float *desc, float *pts, float *nrm, uint8_t *border);
 
+/* ---- NEXT-2: the causal tracker's per-frame decisions (§IV-B/C/E) -----------------
+   Poses are the 12-float (R row-major, t) layout above. */
+/* rotation geodesic arccos((tr(R_a^T R_b) - 1) / 2) in fp64, argument clamped to [-1, 1] */
+double bto_rot_geodesic(const float Ta[12], const float Tb[12]);
+/* coarse pose: T~_t = T_{t-1} T_t^{t-1} read as T_rel . T_prev (reading R13), T_rel = the
+   record's best sampled hypothesis T_best (maps frame t-1 points to frame t points); a pair
+   without one (status FEW_MATCHES / FEW_INLIERS) leaves T~_t = T_prev.  fp64, rounded. */
+void bto_coarse_pose(int32_t status, const float T_best[12], const float T_prev[12], float out[12]);
+/* keyframe selection: start from {I_0} (pool index 0), then repeatedly add the pool
+   keyframe with the smallest sum of geodesic distances against I_t (cur) and every keyframe
+   selected so far (ties -> lowest pool index), until min(K, n_pool) are selected.  sel[] in
+   selection order; returns the count. */
+int32_t bto_select_keyframes(const float *pool, int32_t n_pool, const float cur[12], int32_t K, int32_t *sel);
+/* pool augmentation: 1 iff the geodesic from cur to EVERY pool keyframe is larger than
+   thresh_rad (reading R21: 10 degrees); an empty pool admits. */
+int32_t bto_is_novel(const float *pool, int32_t n_pool, const float cur[12], double thresh_rad);
+
 #ifdef __cplusplus
 }
 #endif

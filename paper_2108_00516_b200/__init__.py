@@ -27,7 +27,7 @@ SYMBOLS = ("bt_create", "bt_destroy", "bt_last_error", "bt_status_string", "bt_r
            "bt_register_pairs_host", "bt_compose_poses", "bt_last_launch_count", "bt_profile_enable",
            "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step",
            "bt_estimate_normals", "bt_relinearize", "bt_relinearize_matches", "bt_copy_matches",
-           "bt_dense_assoc")
+           "bt_dense_assoc", "bt_lift_keypoints")
 
 
 class BtError(RuntimeError):
@@ -113,6 +113,8 @@ def lib():
         L.bt_relinearize_matches.argtypes = [vp, C.POINTER(Keypoints), C.POINTER(Maps), C.POINTER(Intrinsics), vp, vp,
                                              i32, vp, vp, C.POINTER(EdgeParams), vp, vp]
         L.bt_copy_matches.argtypes = [vp, i32, i32, vp, vp, vp]
+        L.bt_lift_keypoints.argtypes = [vp, i32, i32, i32, vp, vp, vp, C.POINTER(Maps), C.POINTER(Intrinsics), vp, vp,
+                                        vp, vp, vp]
         L.bt_last_launch_count.argtypes = [vp]
         L.bt_last_launch_count.restype = i32
         L.bt_profile_enable.argtypes = [vp, i32]
@@ -125,7 +127,7 @@ def lib():
         L.bt_profile_read.restype = C.c_int
         for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_dense_assoc", "bt_register_pairs",
                   "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals", "bt_relinearize",
-                  "bt_relinearize_matches", "bt_copy_matches"):
+                  "bt_relinearize_matches", "bt_copy_matches", "bt_lift_keypoints"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -343,6 +345,17 @@ class Context:
         Ki = intrinsics(K) if not isinstance(K, Intrinsics) else K
         self._check(lib().bt_estimate_normals(self._h, _ptr(depth), int(F), int(W), int(H), C.byref(Ki),
                                               float(jump), _ptr(normal), self._stream(stream)), "bt_estimate_normals")
+
+    def lift_keypoints(self, uv, desc_in, n_in, maps_fb: FrameBatch, K, out: FrameBatch, stream=None):
+        """Raw detector output (uv [F][n_max][2], desc_in [F][n_max][128], n_in [F]) + the frames'
+        depth / normal / mask maps (maps_fb) -> the registration inputs out.n_kp / desc / pts /
+        nrm (bt_lift_keypoints; NEXT-4, reading R29)."""
+        F, n_max, dim = (int(x) for x in desc_in.shape)
+        mp = maps_fb.maps()
+        Ki = intrinsics(K) if not isinstance(K, Intrinsics) else K
+        self._check(lib().bt_lift_keypoints(self._h, F, n_max, dim, _ptr(uv), _ptr(desc_in), _ptr(n_in), C.byref(mp),
+                                            C.byref(Ki), _ptr(out.n_kp), _ptr(out.desc), _ptr(out.pts),
+                                            _ptr(out.nrm), self._stream(stream)), "bt_lift_keypoints")
 
     def compose_poses(self, a, b, out, stream=None):
         self._check(lib().bt_compose_poses(self._h, _ptr(a), _ptr(b), _ptr(out), int(a.shape[0]),

@@ -600,6 +600,30 @@ bt_status bt_estimate_normals(bt_ctx *c, const float *depth, int32_t n_frames, i
   return after_launch(c, "bt_estimate_normals");
 }
 
+bt_status bt_lift_keypoints(bt_ctx *c, int32_t n_frames, int32_t n_max, int32_t dim, const float *uv,
+                            const float *desc_in, const int32_t *n_in, const bt_maps *maps, const bt_intrinsics *K,
+                            int32_t *n_kp, float *desc, float *pts, float *nrm, void *stream) {
+  BT_CHECK_CTX(c);
+  if (dim != bt::kDim) return fail(c, BT_EUNSUPPORTED, "bt_lift_keypoints: descriptor dim %d != 128", dim);
+  if (n_frames < 0 || n_max < 1) return fail(c, BT_EINVAL, "bt_lift_keypoints: bad sizes");
+  if (n_frames == 0) return BT_OK;
+  if (!maps || !K) return fail(c, BT_EINVAL, "bt_lift_keypoints: NULL maps / intrinsics");
+  if (maps->n_frames < n_frames) return fail(c, BT_EINVAL, "bt_lift_keypoints: maps cover %d < %d frames",
+                                             maps->n_frames, n_frames);
+  if (maps->width != K->width || maps->height != K->height || maps->width < 1 || maps->height < 1)
+    return fail(c, BT_EINVAL, "bt_lift_keypoints: maps %dx%d vs intrinsics %dx%d", maps->width, maps->height,
+                K->width, K->height);
+  if (!(K->fx > 0.f) || !(K->fy > 0.f)) return fail(c, BT_EINVAL, "bt_lift_keypoints: fx, fy must be > 0");
+  if (!uv || !desc_in || !n_in || !maps->depth || !maps->normal || !maps->mask || !n_kp || !desc || !pts || !nrm)
+    return fail(c, BT_EINVAL, "bt_lift_keypoints: NULL buffer");
+  if (!aligned16(uv) || !aligned16(desc_in) || !aligned16(desc))
+    return fail(c, BT_EINVAL, "bt_lift_keypoints: uv / desc buffers must be 16-byte aligned");
+  c->launch.count = 0;
+  bt::launch_lift(n_frames, n_max, uv, desc_in, n_in, mview(maps), *K, n_kp, desc, pts, nrm, (cudaStream_t)stream,
+                  c->launch);
+  return after_launch(c, "bt_lift_keypoints");
+}
+
 static bt_status relinearize(bt_ctx *c, const char *what, const bt_keypoints *kp, const bt_maps *maps,
                              const bt_intrinsics *K, const bt_pose *node_pose, const int32_t *pairs, int32_t P,
                              const int32_t *matches, const int32_t *n_matches, const bt_edge_params *eprm,

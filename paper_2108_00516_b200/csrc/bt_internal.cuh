@@ -149,6 +149,10 @@ void launch_feature_edges(const KpView &kp, const int32_t *pairs, int P, const i
 // NEXT-4 input prep: normal map from depth (bt_prep.cu)
 void launch_normals(const float *depth, int F, int W, int H, const bt_intrinsics &K, float jump, float *normal,
                     cudaStream_t s, Launch &L);
+// NEXT-4 keypoint lifting (bt_prep.cu)
+void launch_lift(int F, int n_max, const float *uv, const float *desc_in, const int32_t *n_in, const MapView &mp,
+                 const bt_intrinsics &K, int32_t *n_out, float *desc, float *pts, float *nrm, cudaStream_t s,
+                 Launch &L);
 // NEXT-1 pose-graph Gauss-Newton step (bt_graph.cu)
 size_t graph_scratch_bytes(int max_nodes, int max_pairs);
 void launch_graph(int N, const bt_pose *pose, const int32_t *pairs, int P, const uint32_t *records, int n_max,

@@ -11,12 +11,101 @@
 //             normalized, flipped to face the camera (n . P < 0).  Invalid (0, 0, 0) at the
 //             border, for depth <= 0 at the pixel or a 4-neighbour, and for a neighbour
 //             farther than `jump` in depth.  HBM roofline: 4 B read + 12 B written per pixel.
+//
+//  k_lift     NEXT-4 keypoint lifting (reading R29; P:25 keypoints x_i + D_i, P:72 pi_D^-1 "looking
+//             up the depth value on the pixel location", SPEC S:247 / S:262): one CTA per frame,
+//             a thread per keypoint in blocks of kLiftThreads: nearest pixel (floor(u + 0.5)),
+//             validity (in frame, mask, depth > 0, normal != 0), block-scan compaction in input
+//             order, the point in fp64 ((u - cx) d / fx, (v - cy) d / fy, d) rounded to fp32 and
+//             the pixel's normal; then each warp copies its lanes' kept descriptors (128 floats
+//             as one float4 per lane, coalesced).  HBM: 8 B (uv) + 512 B (desc) read and 512 +
+//             24 B written per keypoint + 17 B of map lookups.
 #include <cuda_runtime.h>
 
 #include "bt_internal.cuh"
 
 namespace bt {
 namespace {
+
+constexpr int kLiftThreads = 512;
+constexpr int kLiftSplit = 8;                      // CTAs per frame, each writing 1/8 of the output slots
+
+struct LiftArgs {
+  int F, n_max, W, H, span;                        // span = output slots per CTA
+  const float *uv, *desc_in;
+  const int32_t *n_in;
+  MapView mp;
+  double fx, fy, cx, cy;
+  int32_t *n_out;
+  float *desc, *pts, *nrm;
+};
+
+// grid (F, kLiftSplit): every CTA of a frame evaluates all of the frame's keypoints (8 B of uv +
+// 17 B of map lookups each: cheap) and their output slots (block scan in input order), but writes
+// only the slots [lo, lo + span) — so the 512-B descriptor copies spread over F x 8 CTAs with
+// several rows in flight per warp instead of one frame's rows serialised in one CTA
+__global__ void __launch_bounds__(kLiftThreads) k_lift(LiftArgs A) {
+  extern __shared__ int src_of[];                  // [span] input index of each of this CTA's slots
+  __shared__ int wsum[kLiftThreads / 32];
+  const int f = blockIdx.x, lo = blockIdx.y * A.span, hi = lo + A.span;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = min(A.n_in[f], A.n_max);
+  const size_t fpx = (size_t)f * A.W * A.H;
+  int base = 0;
+  for (int k0 = 0; k0 < n; k0 += kLiftThreads) {
+    const int k = k0 + threadIdx.x;
+    bool keep = false;
+    float p0 = 0.f, p1 = 0.f, p2 = 0.f, m0 = 0.f, m1 = 0.f, m2 = 0.f;
+    if (k < n) {
+      const float2 uv = __ldg(reinterpret_cast<const float2 *>(A.uv) + (size_t)f * A.n_max + k);
+      const double u = uv.x, v = uv.y;
+      const double xu = floor(u + 0.5), xv = floor(v + 0.5);      // nearest pixel (R14)
+      if (xu >= 0.0 && xu < (double)A.W && xv >= 0.0 && xv < (double)A.H) {
+        const size_t px = fpx + (size_t)xv * A.W + (size_t)xu;
+        const float d = __ldg(A.mp.depth + px);
+        m0 = __ldg(A.mp.normal + 3 * px); m1 = __ldg(A.mp.normal + 3 * px + 1); m2 = __ldg(A.mp.normal + 3 * px + 2);
+        keep = A.mp.mask[px] != 0 && d > 0.f && !(m0 == 0.f && m1 == 0.f && m2 == 0.f);
+        const double dd = d;
+        p0 = (float)__ddiv_rn(__dmul_rn(__dsub_rn(u, A.cx), dd), A.fx);   // pi_D^-1 at the keypoint
+        p1 = (float)__ddiv_rn(__dmul_rn(__dsub_rn(v, A.cy), dd), A.fy);
+        p2 = d;
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);        // block scan in input order
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kLiftThreads / 32; ++w) { off += w < warp ? wsum[w] : 0; tot += wsum[w]; }
+    const int slot = base + off + __popc(bal & ((1u << lane) - 1u));
+    if (keep && slot >= lo && slot < hi) {
+      const size_t o = (size_t)f * A.n_max + slot;
+      A.pts[3 * o] = p0; A.pts[3 * o + 1] = p1; A.pts[3 * o + 2] = p2;
+      A.nrm[3 * o] = m0; A.nrm[3 * o + 1] = m1; A.nrm[3 * o + 2] = m2;
+      src_of[slot - lo] = k;
+    }
+    base += tot;
+    __syncthreads();                                               // wsum reused
+  }
+  if (blockIdx.y == 0 && threadIdx.x == 0) A.n_out[f] = base;
+  // this CTA's descriptor rows: warp w copies rows w, w + 16, ... four at a time (loads in flight)
+  const int rows = max(0, min(hi, base) - lo);
+  constexpr int kW = kLiftThreads / 32;
+  for (int r0 = warp; r0 < rows; r0 += 4 * kW) {
+    float4 x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + q * kW;
+      if (r < rows)
+        x[q] = __ldg(reinterpret_cast<const float4 *>(A.desc_in + ((size_t)f * A.n_max + src_of[r]) * kDim) + lane);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + q * kW;
+      if (r < rows) reinterpret_cast<float4 *>(A.desc + ((size_t)f * A.n_max + lo + r) * kDim)[lane] = x[q];
+    }
+  }
+}
 
 constexpr int kNormThreads = 256;                 // one thread per 4 horizontally adjacent pixels
 
@@ -139,6 +228,21 @@ __global__ void __launch_bounds__(kNormThreads) k_normals(NormArgs A) {
 }
 
 }  // namespace
+
+void launch_lift(int F, int n_max, const float *uv, const float *desc_in, const int32_t *n_in, const MapView &mp,
+                 const bt_intrinsics &K, int32_t *n_out, float *desc, float *pts, float *nrm, cudaStream_t s,
+                 Launch &L) {
+  if (F <= 0) return;
+  LiftArgs a;
+  a.F = F; a.n_max = n_max; a.W = mp.W; a.H = mp.H;
+  a.uv = uv; a.desc_in = desc_in; a.n_in = n_in; a.mp = mp;
+  a.fx = K.fx; a.fy = K.fy; a.cx = K.cx; a.cy = K.cy;
+  a.n_out = n_out; a.desc = desc; a.pts = pts; a.nrm = nrm;
+  a.span = (n_max + kLiftSplit - 1) / kLiftSplit;
+  L.begin(K_NORMALS, s);
+  k_lift<<<dim3(F, kLiftSplit), kLiftThreads, (size_t)a.span * sizeof(int), s>>>(a);
+  L.end(K_NORMALS, s);
+}
 
 void launch_normals(const float *depth, int F, int W, int H, const bt_intrinsics &K, float jump, float *normal,
                     cudaStream_t s, Launch &L) {

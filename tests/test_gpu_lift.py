@@ -1,0 +1,152 @@
+"""NEXT-4 on the GPU: raw detector output (2-D keypoints + descriptors) and the depth / mask maps
+are the only inputs.  bt_lift_keypoints (reading R29: pi_D^-1 at the keypoint with the nearest
+pixel's depth; SPEC S:247 / S:262) against the oracle's bto_lift_keypoints — counts,
+order, descriptors, points and normals bit for bit — and the whole raw-input chain
+depth -> bt_estimate_normals -> bt_lift_keypoints -> bt_register_pairs against the oracle run
+stage-isolated on the GPU's intermediate maps (the normal map's own parity: test_gpu_normals)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import parity
+import synth
+
+pytestmark = pytest.mark.gpu
+
+SEED = synth.PHILOX_SEED
+DENSE = dict(dist_gate=0.02, cos_gate=float(np.cos(np.deg2rad(45.0))), huber_delta=0.005, stride=1)
+
+
+@pytest.fixture(scope="module")
+def bt():
+    import paper_2108_00516_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    return t
+
+
+def detector_output(sc, seed=0, n_extra=24):
+    """The scene's keypoints as a detector would report them: sub-pixel (u, v) of each keypoint
+    (its projection) plus n_extra spurious ones per frame (background, off-frame, borders), at
+    random positions in the list; descriptors alongside."""
+    rng = np.random.default_rng(seed)
+    F, n_max = sc.desc.shape[:2]
+    K = sc.K
+    uv = np.zeros((F, n_max, 2), np.float32)
+    desc = np.zeros_like(sc.desc)
+    n_in = np.zeros(F, np.int32)
+    for f in range(F):
+        n = int(sc.n_kp[f])
+        p = sc.pts[f, :n].astype(np.float64)
+        real = np.stack([K.fx * p[:, 0] / p[:, 2] + K.cx, K.fy * p[:, 1] / p[:, 2] + K.cy], 1)
+        m = min(n_extra, n_max - n)
+        extra = np.stack([rng.uniform(-3, K.width + 3, m), rng.uniform(-3, K.height + 3, m)], 1)
+        allp = np.concatenate([real, extra])
+        alld = np.concatenate([sc.desc[f, :n], rng.normal(size=(m, 128)).astype(np.float32)])
+        order = rng.permutation(n + m)
+        uv[f, :n + m] = allp[order]
+        desc[f, :n + m] = alld[order]
+        n_in[f] = n + m
+    return uv, desc, n_in
+
+
+def gpu_lift(bt, torch, ctx, uv, desc, n_in, maps_fb, K):
+    F, n_max = desc.shape[:2]
+    out = bt.FrameBatch(torch.zeros(F, dtype=torch.int32, device="cuda"),
+                        torch.zeros((F, n_max, 128), dtype=torch.float32, device="cuda"),
+                        torch.zeros((F, n_max, 3), dtype=torch.float32, device="cuda"),
+                        torch.zeros((F, n_max, 3), dtype=torch.float32, device="cuda"),
+                        maps_fb.depth, maps_fb.normal, maps_fb.mask)
+    ctx.lift_keypoints(torch.from_numpy(uv).cuda(), torch.from_numpy(desc).cuda(), torch.from_numpy(n_in).cuda(),
+                       maps_fb, K, out)
+    torch.cuda.synchronize()
+    return out
+
+
+def _compare(out, ref):
+    n = out.n_kp.cpu().numpy()
+    assert np.array_equal(n, ref["n"])
+    d, p, q = out.desc.cpu().numpy(), out.pts.cpu().numpy(), out.nrm.cpu().numpy()
+    for f in range(len(n)):
+        k = n[f]
+        assert np.array_equal(d[f, :k], ref["desc"][f, :k])
+        assert np.array_equal(p[f, :k], ref["pts"][f, :k]), f"frame {f}: points differ"
+        assert np.array_equal(q[f, :k], ref["nrm"][f, :k])
+
+
+def test_lift_parity_c2(bt, torch):
+    sc = synth.make_scene(16)
+    uv, desc, n_in = detector_output(sc)
+    ctx = bt.Context(0)
+    fb = bt.FrameBatch.from_scene(sc)
+    out = gpu_lift(bt, torch, ctx, uv, desc, n_in, fb, sc.K)
+    ref = oracle.lift_keypoints(uv, desc, n_in, sc.depth, sc.normal, sc.mask, sc.K)
+    # borderline roundings (band rule) need no exclusion: both sides round the same float in the
+    # same fp64 arithmetic, so every keypoint must agree exactly
+    _compare(out, ref)
+    assert (ref["n"] > 400).all() and (ref["n"] < n_in).all()          # spurious ones dropped
+    ctx.close()
+
+
+def test_lift_edge_cases(bt, torch):
+    """Empty frames, n_in > n_max (clamped), keypoints exactly on the frame edge, all dropped."""
+    sc = synth.make_scene(3, n=100, n_max=128, width=160, height=120, distance=0.9, seed=3)
+    uv, desc, n_in = detector_output(sc, seed=5, n_extra=28)
+    n_in[0] = 0
+    n_in[2] = 1000                                                      # clamped to n_max
+    uv[1, :4] = [[-0.5, 10.0], [159.49, 10.0], [-0.51, 10.0], [159.5, 10.0]]   # first two in frame
+    ctx = bt.Context(0)
+    fb = bt.FrameBatch.from_scene(sc)
+    out = gpu_lift(bt, torch, ctx, uv, desc, n_in, fb, sc.K)
+    ref = oracle.lift_keypoints(uv, desc, n_in, sc.depth, sc.normal, sc.mask, sc.K)
+    _compare(out, ref)
+    assert ref["n"][0] == 0
+    ctx.close()
+
+
+def test_raw_input_chain_depth_mask_keypoints_only(bt, torch):
+    """C2 from raw inputs only: depth + mask -> bt_estimate_normals -> bt_lift_keypoints ->
+    bt_register_pairs (120 pairs, 4096 hypotheses, 640x480).  The oracle, run on the GPU's
+    normal map (stage isolation), lifts the same keypoints bit for bit, and registers sampled
+    pairs equal to the GPU's records (band rule, tolerances of the north star)."""
+    sc = synth.make_scene(16)
+    uv, desc, n_in = detector_output(sc, seed=9)
+    ctx = bt.Context(0)
+    ctx.reserve(120, 512, 4096, 16, 640, 480)
+    depth = torch.from_numpy(sc.depth).cuda()
+    mask = torch.from_numpy(sc.mask).cuda()
+    normal = torch.empty((16, 480, 640, 3), dtype=torch.float32, device="cuda")
+    ctx.estimate_normals(depth, sc.K, normal)
+    maps = bt.FrameBatch(None, None, None, None, depth, normal, mask)
+    kp = gpu_lift(bt, torch, ctx, uv, desc, n_in, maps, sc.K)
+    nrm_map = normal.cpu().numpy()
+    ref = oracle.lift_keypoints(uv, desc, n_in, sc.depth, nrm_map, sc.mask, sc.K)
+    _compare(kp, ref)
+    pairs = synth.all_pairs(16)
+    poses = sc.perturbed_poses(11)
+    rec = torch.zeros((len(pairs), bt.record_words(512)), dtype=torch.int32, device="cuda")
+    ctx.register_pairs(kp, sc.K, torch.from_numpy(poses).cuda(), torch.from_numpy(pairs).cuda(),
+                       torch.arange(len(pairs), dtype=torch.int32, device="cuda"), bt.ransac_params(4096, SEED),
+                       bt.edge_params(), rec)
+    torch.cuda.synchronize()
+    r_all = bt.decode_records(rec, 512)
+    assert (r_all["status"] == 0).all()
+    lifted = dataclasses.replace(sc, n_kp=ref["n"], desc=ref["desc"], pts=ref["pts"], nrm=ref["nrm"], normal=nrm_map)
+    for p in (0, 33, 77, 119):
+        a, b = pairs[p]
+        o = oracle.register_pair(lifted, a, b, p, 4096, SEED, node_poses=poses, dense=DENSE, counts_out=True)
+        r = {k: v[p] for k, v in r_all.items()}
+        assert r["n_matches"] == o["n_matches"]
+        P_ = o["match"]["pairs"]
+        ia, ib = P_[:, 0], P_[:, 1]
+        parity.compare_ransac(None, r, o["counts"], lifted.pts[a][ia], lifted.nrm[a][ia], lifted.pts[b][ib],
+                              lifted.nrm[b][ib], what=f"raw pair {p}")
+        parity.assert_dense_close(r["dense_ij"], o["dense_ij"], f"raw pair {p} ij")
+        parity.assert_dense_close(r["dense_ji"], o["dense_ji"], f"raw pair {p} ji")
+    ctx.close()
