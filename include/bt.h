@@ -285,6 +285,29 @@ bt_status bt_lift_keypoints(bt_ctx *ctx, int32_t n_frames, int32_t n_max, int32_
                             const bt_intrinsics *K, int32_t *n_kp, float *desc, float *pts, float *nrm,
                             void *stream);
 
+/* ---- NEXT-2: the causal tracker's per-frame decisions, on the device (§IV-B/C/E) -----
+   geo(a, b) = arccos((tr(R_a^T R_b) - 1) / 2), the rotation geodesic of P:33, in fp64.
+   Pose arrays are device bt_pose; every call only enqueues (graph-capturable). */
+/* Coarse pose of the current frame ("T~_t = T_{t-1} T_t^{t-1} where T_t^{t-1} is the best
+   sampled correspondence hypothesis"; reading R13: out = T_rel . prev with T_rel = record's
+   T_best, the (t-1 -> t) pair's record from bt_ransac / bt_register_pairs).  A record whose
+   status is FEW_MATCHES / FEW_INLIERS (no hypothesis) gives out = prev.  `record`: one record
+   (words 0..15 read); out may alias prev. */
+bt_status bt_coarse_pose(bt_ctx *ctx, const uint32_t *record, const bt_pose *prev, bt_pose *out, void *stream);
+/* Keyframe selection: from the pool poses pool[0 .. *n_pool) (pool[0] = I_0), the
+   greedy minimum-H-subgraph heuristic — start with {I_0}; each round add the keyframe with the
+   smallest sum of geodesics to cur (I_t) and to every keyframe selected so far (ties -> lowest
+   index) — until min(K, *n_pool) are selected.  Out: sel [K] pool indices in selection order,
+   *n_sel.  n_pool is a DEVICE int (bt_pool_admit grows it).  BT_EINVAL: pool_cap outside
+   [1, 4096], K < 1, NULL buffers. */
+bt_status bt_select_keyframes(bt_ctx *ctx, const bt_pose *pool, const int32_t *n_pool, int32_t pool_cap,
+                              const bt_pose *cur, int32_t K, int32_t *sel, int32_t *n_sel, void *stream);
+/* Memory-pool augmentation: if geo(cur, pool[k]) > thresh_rad for every k < *n_pool
+   (reading R21: 10 degrees) and *n_pool < pool_cap, pool[*n_pool] = cur and ++*n_pool.
+   *admitted (may be NULL) = the new pool index, or -1.  Device n_pool / admitted. */
+bt_status bt_pool_admit(bt_ctx *ctx, bt_pose *pool, int32_t *n_pool, int32_t pool_cap, const bt_pose *cur,
+                        float thresh_rad, int32_t *admitted, void *stream);
+
 /* number of kernels the last bt_* call enqueued (for the bench's gpu_launches claim) */
 int32_t bt_last_launch_count(const bt_ctx *ctx);
 

@@ -27,7 +27,7 @@ SYMBOLS = ("bt_create", "bt_destroy", "bt_last_error", "bt_status_string", "bt_r
            "bt_register_pairs_host", "bt_compose_poses", "bt_last_launch_count", "bt_profile_enable",
            "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step",
            "bt_estimate_normals", "bt_relinearize", "bt_relinearize_matches", "bt_copy_matches",
-           "bt_dense_assoc", "bt_lift_keypoints")
+           "bt_dense_assoc", "bt_lift_keypoints", "bt_coarse_pose", "bt_select_keyframes", "bt_pool_admit")
 
 
 class BtError(RuntimeError):
@@ -115,6 +115,9 @@ def lib():
         L.bt_copy_matches.argtypes = [vp, i32, i32, vp, vp, vp]
         L.bt_lift_keypoints.argtypes = [vp, i32, i32, i32, vp, vp, vp, C.POINTER(Maps), C.POINTER(Intrinsics), vp, vp,
                                         vp, vp, vp]
+        L.bt_coarse_pose.argtypes = [vp, vp, vp, vp, vp]
+        L.bt_select_keyframes.argtypes = [vp, vp, vp, i32, vp, i32, vp, vp, vp]
+        L.bt_pool_admit.argtypes = [vp, vp, vp, i32, vp, C.c_float, vp, vp]
         L.bt_last_launch_count.argtypes = [vp]
         L.bt_last_launch_count.restype = i32
         L.bt_profile_enable.argtypes = [vp, i32]
@@ -127,7 +130,8 @@ def lib():
         L.bt_profile_read.restype = C.c_int
         for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_dense_assoc", "bt_register_pairs",
                   "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals", "bt_relinearize",
-                  "bt_relinearize_matches", "bt_copy_matches", "bt_lift_keypoints"):
+                  "bt_relinearize_matches", "bt_copy_matches", "bt_lift_keypoints", "bt_coarse_pose",
+                  "bt_select_keyframes", "bt_pool_admit"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -356,6 +360,22 @@ class Context:
         self._check(lib().bt_lift_keypoints(self._h, F, n_max, dim, _ptr(uv), _ptr(desc_in), _ptr(n_in), C.byref(mp),
                                             C.byref(Ki), _ptr(out.n_kp), _ptr(out.desc), _ptr(out.pts),
                                             _ptr(out.nrm), self._stream(stream)), "bt_lift_keypoints")
+
+    # ---- NEXT-2: the tracker's per-frame decisions (device-resident pool, P:25 / P:39 / P:88)
+    def coarse_pose(self, record, prev, out, stream=None):
+        """out = T_best(record) . prev, or prev when the pair has no hypothesis (bt_coarse_pose)."""
+        self._check(lib().bt_coarse_pose(self._h, _ptr(record), _ptr(prev), _ptr(out), self._stream(stream)),
+                    "bt_coarse_pose")
+
+    def select_keyframes(self, pool, n_pool, cur, K, sel, n_sel, stream=None):
+        """Greedy selection of P:39 over pool[0 .. n_pool) (device int) -> sel [K], n_sel [1]."""
+        self._check(lib().bt_select_keyframes(self._h, _ptr(pool), _ptr(n_pool), int(pool.shape[0]), _ptr(cur), int(K),
+                                              _ptr(sel), _ptr(n_sel), self._stream(stream)), "bt_select_keyframes")
+
+    def pool_admit(self, pool, n_pool, cur, thresh_rad, admitted=None, stream=None):
+        """cur joins the pool iff its rotation is > thresh from every keyframe (bt_pool_admit)."""
+        self._check(lib().bt_pool_admit(self._h, _ptr(pool), _ptr(n_pool), int(pool.shape[0]), _ptr(cur),
+                                        float(thresh_rad), _ptr(admitted), self._stream(stream)), "bt_pool_admit")
 
     def compose_poses(self, a, b, out, stream=None):
         self._check(lib().bt_compose_poses(self._h, _ptr(a), _ptr(b), _ptr(out), int(a.shape[0]),

@@ -624,6 +624,32 @@ bt_status bt_lift_keypoints(bt_ctx *c, int32_t n_frames, int32_t n_max, int32_t 
   return after_launch(c, "bt_lift_keypoints");
 }
 
+bt_status bt_coarse_pose(bt_ctx *c, const uint32_t *record, const bt_pose *prev, bt_pose *out, void *stream) {
+  BT_CHECK_CTX(c);
+  if (!record || !prev || !out) return fail(c, BT_EINVAL, "bt_coarse_pose: NULL buffer");
+  bt::launch_coarse_pose(record, prev, out, (cudaStream_t)stream, c->launch);
+  return after_launch(c, "bt_coarse_pose");
+}
+
+bt_status bt_select_keyframes(bt_ctx *c, const bt_pose *pool, const int32_t *n_pool, int32_t pool_cap,
+                              const bt_pose *cur, int32_t K, int32_t *sel, int32_t *n_sel, void *stream) {
+  BT_CHECK_CTX(c);
+  if (pool_cap < 1 || pool_cap > 4096 || K < 1) return fail(c, BT_EINVAL, "bt_select_keyframes: pool_cap %d / K %d",
+                                                            pool_cap, K);
+  if (!pool || !n_pool || !cur || !sel || !n_sel) return fail(c, BT_EINVAL, "bt_select_keyframes: NULL buffer");
+  bt::launch_select(pool, n_pool, pool_cap, cur, K, sel, n_sel, (cudaStream_t)stream, c->launch);
+  return after_launch(c, "bt_select_keyframes");
+}
+
+bt_status bt_pool_admit(bt_ctx *c, bt_pose *pool, int32_t *n_pool, int32_t pool_cap, const bt_pose *cur,
+                        float thresh_rad, int32_t *admitted, void *stream) {
+  BT_CHECK_CTX(c);
+  if (pool_cap < 1 || !(thresh_rad >= 0.f)) return fail(c, BT_EINVAL, "bt_pool_admit: pool_cap %d / thresh", pool_cap);
+  if (!pool || !n_pool || !cur) return fail(c, BT_EINVAL, "bt_pool_admit: NULL buffer");
+  bt::launch_admit(pool, n_pool, pool_cap, cur, (double)thresh_rad, admitted, (cudaStream_t)stream, c->launch);
+  return after_launch(c, "bt_pool_admit");
+}
+
 static bt_status relinearize(bt_ctx *c, const char *what, const bt_keypoints *kp, const bt_maps *maps,
                              const bt_intrinsics *K, const bt_pose *node_pose, const int32_t *pairs, int32_t P,
                              const int32_t *matches, const int32_t *n_matches, const bt_edge_params *eprm,
@@ -689,7 +715,8 @@ bt_status bt_copy_matches(bt_ctx *c, int32_t P, int32_t n_max, int32_t *matches,
 
 static const char *kKernelNames[bt::K_COUNT] = {"k_desc_prep", "k_match_tc", "k_rescore", "k_mutual",
                                                  "k_ransac_hyp", "k_ransac_score", "k_ransac_finish", "k_dense_prep",
-                                                 "k_dense", "k_dense_reduce", "k_compose", "k_graph", "k_normals"};
+                                                 "k_dense", "k_dense_reduce", "k_compose", "k_graph", "k_normals",
+                                                 "k_track"};
 
 static cudaEvent_t take_event(bt_ctx *c) {
   if (c->ev_pool.empty()) {

@@ -40,7 +40,7 @@ struct MapView {
 // ---- launch bookkeeping: counts kernels and (optionally) brackets each with events ----
 enum KernelId {
   K_DESC_PREP = 0, K_MATCH_TC, K_RESOLVE, K_MUTUAL, K_RANSAC_HYP, K_RANSAC_SCORE, K_RANSAC_FINISH, K_DENSE_PREP,
-  K_DENSE, K_DENSE_REDUCE, K_COMPOSE, K_GRAPH, K_NORMALS,
+  K_DENSE, K_DENSE_REDUCE, K_COMPOSE, K_GRAPH, K_NORMALS, K_TRACK,
   K_COUNT
 };
 
@@ -153,6 +153,12 @@ void launch_normals(const float *depth, int F, int W, int H, const bt_intrinsics
 void launch_lift(int F, int n_max, const float *uv, const float *desc_in, const int32_t *n_in, const MapView &mp,
                  const bt_intrinsics &K, int32_t *n_out, float *desc, float *pts, float *nrm, cudaStream_t s,
                  Launch &L);
+// NEXT-2 tracker decisions (bt_track.cu)
+void launch_coarse_pose(const uint32_t *record, const bt_pose *prev, bt_pose *out, cudaStream_t s, Launch &L);
+void launch_select(const bt_pose *pool, const int32_t *n_pool, int cap, const bt_pose *cur, int K, int32_t *sel,
+                   int32_t *n_sel, cudaStream_t s, Launch &L);
+void launch_admit(bt_pose *pool, int32_t *n_pool, int cap, const bt_pose *cur, double thresh, int32_t *admitted,
+                  cudaStream_t s, Launch &L);
 // NEXT-1 pose-graph Gauss-Newton step (bt_graph.cu)
 size_t graph_scratch_bytes(int max_nodes, int max_pairs);
 void launch_graph(int N, const bt_pose *pose, const int32_t *pairs, int P, const uint32_t *records, int n_max,
