@@ -86,10 +86,10 @@ def _setup(L):
     L.bto_se3_exp.argtypes = [_f64p, _f64p, _f64p]
     L.bto_se3_adjoint.argtypes = [_f64p, _f64p, _f64p]
     L.bto_graph_system.restype = C.c_int32
-    L.bto_graph_system.argtypes = [C.c_int32, _f32p, _i32p, C.c_int32, _f64p, _vp, _vp, C.c_double, C.c_double,
+    L.bto_graph_system.argtypes = [C.c_int32, _f32p, _i32p, C.c_int32, _f64p, _vp, _vp, _vp, C.c_double, C.c_double,
                                    _f64p, _f64p, _f64p]
     L.bto_graph_step.restype = C.c_int32
-    L.bto_graph_step.argtypes = [C.c_int32, _f32p, _i32p, C.c_int32, _f64p, _vp, _vp, C.c_double, C.c_double,
+    L.bto_graph_step.argtypes = [C.c_int32, _f32p, _i32p, C.c_int32, _f64p, _vp, _vp, _vp, C.c_double, C.c_double,
                                  C.c_int32, _f64p, _f32p, _f64p]
 
 
@@ -298,32 +298,36 @@ def _graph_inputs(poses, pairs, feat, dense_ij, dense_ji):
     return poses, pairs, feat, dij, dji
 
 
-def graph_system(poses, pairs, feat, dense_ij=None, dense_ji=None, lambda_f=1.0, lambda_g=1.0):
+def graph_system(poses, pairs, feat, dense_ij=None, dense_ji=None, lambda_f=1.0, lambda_g=1.0, status=None):
     """Gauss-Newton system of Eq. (1) from per-pair Eq. (2) blocks feat[P][96] and
-    the Eq. (3) blocks of both directed edges [P][32] at node poses [N][12]: (A, b, (E_f, E_g))."""
+    the Eq. (3) blocks of both directed edges [P][32] at node poses [N][12]: (A, b, (E_f, E_g)).
+    status [P] (optional): pairs with status 1 / 2 (failed registration) bring no Eq. (2) term."""
+    st_ = None if status is None else _c(status, np.int32)
     poses, pairs, feat, dij, dji = _graph_inputs(poses, pairs, feat, dense_ij, dense_ji)
     n = 6 * len(poses)
     A = np.zeros(n * n)
     b = np.zeros(n)
     e = np.zeros(2)
     st = lib().bto_graph_system(len(poses), poses, pairs.reshape(-1), len(pairs), feat.reshape(-1), _ptr(dij),
-                                _ptr(dji), float(lambda_f), float(lambda_g), A, b, e)
+                                _ptr(dji), _ptr(st_), float(lambda_f), float(lambda_g), A, b, e)
     if st != 0:
         raise ValueError("bad pair list")
     return A.reshape(n, n), b, tuple(e)
 
 
-def graph_step(poses, pairs, feat, dense_ij=None, dense_ji=None, lambda_f=1.0, lambda_g=1.0, fixed_node=0):
+def graph_step(poses, pairs, feat, dense_ij=None, dense_ji=None, lambda_f=1.0, lambda_g=1.0, fixed_node=0,
+               status=None):
     """One Gauss-Newton step: solve A d = -b (Cholesky; the fixed node's and
     unconstrained DOFs pinned), T_i <- exp(d_i) T_i.  Returns (delta [N][6], poses [N][12],
-    (E_f, E_g) at the input poses)."""
+    (E_f, E_g) at the input poses).  status: as graph_system."""
+    st_ = None if status is None else _c(status, np.int32)
     poses, pairs, feat, dij, dji = _graph_inputs(poses, pairs, feat, dense_ij, dense_ji)
     N = len(poses)
     d = np.zeros(6 * N)
     out = np.zeros(12 * N, np.float32)
     e = np.zeros(2)
     st = lib().bto_graph_step(N, poses, pairs.reshape(-1), len(pairs), feat.reshape(-1), _ptr(dij), _ptr(dji),
-                              float(lambda_f), float(lambda_g), int(fixed_node), d, out, e)
+                              _ptr(st_), float(lambda_f), float(lambda_g), int(fixed_node), d, out, e)
     if st != 0:
         raise np.linalg.LinAlgError("pose-graph system not positive definite")
     return d.reshape(N, 6), out.reshape(N, 12), tuple(e)

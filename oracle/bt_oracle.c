@@ -750,7 +750,8 @@ static void add_dense(double *A, double *b, int n, int i, int j, const double *b
 
 int32_t bto_graph_system(int32_t n_nodes, const float *poses, const int32_t *pairs, int32_t P,
                          const double *feat, const double *dense_ij, const double *dense_ji,
-                         double lambda_f, double lambda_g, double *A, double *b, double energy[2]) {
+                         const int32_t *status, double lambda_f, double lambda_g, double *A, double *b,
+                         double energy[2]) {
   const int n = 6 * n_nodes;
   memset(A, 0, sizeof(double) * (size_t)n * n);
   memset(b, 0, sizeof(double) * (size_t)n);
@@ -758,19 +759,20 @@ int32_t bto_graph_system(int32_t n_nodes, const float *poses, const int32_t *pai
   for (int p = 0; p < P; ++p) {
     const int i = pairs[2 * p], j = pairs[2 * p + 1];
     if (i < 0 || j < 0 || i >= n_nodes || j >= n_nodes || i == j) return -1;
-    /* Eq. (2) blocks, as given (12 x 12 over [i, j]) */
+    /* Eq. (2) blocks, as given (12 x 12 over [i, j]); none for a failed registration (R30) */
     const double *f = feat + (size_t)96 * p;
+    const double lf = (status && (status[p] == 1 || status[p] == 2)) ? 0.0 : lambda_f;
     double Hii[36], Hjj[36], Hij[36], Hji[36];
     sym6(f, Hii);
     sym6(f + 57, Hjj);
     for (int r = 0; r < 6; ++r)
       for (int c = 0; c < 6; ++c) { Hij[6 * r + c] = f[21 + 6 * r + c]; Hji[6 * c + r] = f[21 + 6 * r + c]; }
-    add_block(A, n, i, i, Hii, lambda_f);
-    add_block(A, n, i, j, Hij, lambda_f);
-    add_block(A, n, j, i, Hji, lambda_f);
-    add_block(A, n, j, j, Hjj, lambda_f);
-    for (int r = 0; r < 6; ++r) { b[6 * i + r] += lambda_f * f[78 + r]; b[6 * j + r] += lambda_f * f[84 + r]; }
-    energy[0] += lambda_f * f[90];
+    add_block(A, n, i, i, Hii, lf);
+    add_block(A, n, i, j, Hij, lf);
+    add_block(A, n, j, i, Hji, lf);
+    add_block(A, n, j, j, Hjj, lf);
+    for (int r = 0; r < 6; ++r) { b[6 * i + r] += lf * f[78 + r]; b[6 * j + r] += lf * f[84 + r]; }
+    energy[0] += lf * f[90];
     /* Eq. (3) blocks of both directed edges */
     double Ri[9], ti[3], Rj[9], tj[3];
     pose_of(poses + 12 * i, Ri, ti);
@@ -789,13 +791,14 @@ int32_t bto_graph_system(int32_t n_nodes, const float *poses, const int32_t *pai
 
 int32_t bto_graph_step(int32_t n_nodes, const float *poses, const int32_t *pairs, int32_t P,
                        const double *feat, const double *dense_ij, const double *dense_ji,
-                       double lambda_f, double lambda_g, int32_t fixed_node, double *delta,
-                       float *new_poses, double energy[2]) {
+                       const int32_t *status, double lambda_f, double lambda_g, int32_t fixed_node,
+                       double *delta, float *new_poses, double energy[2]) {
   const int n = 6 * n_nodes;
   double *A = (double *)malloc(sizeof(double) * (size_t)n * n);
   double *b = (double *)malloc(sizeof(double) * (size_t)n);
   int *free_idx = (int *)malloc(sizeof(int) * (size_t)n);
-  int32_t st = bto_graph_system(n_nodes, poses, pairs, P, feat, dense_ij, dense_ji, lambda_f, lambda_g, A, b, energy);
+  int32_t st = bto_graph_system(n_nodes, poses, pairs, P, feat, dense_ij, dense_ji, status, lambda_f, lambda_g, A, b,
+                                energy);
   int m = 0;
   for (int k = 0; k < n; ++k) {
     delta[k] = 0.0;

@@ -141,7 +141,11 @@ void bto_se3_adjoint(const double R[9], const double t[3], double Adj[36]);
    E_f, sum lambda_g E_g).  Nodes outside [0, N) are an error (returns -1). */
 int32_t bto_graph_system(int32_t n_nodes, const float *poses, const int32_t *pairs, int32_t P,
                          const double *feat, const double *dense_ij, const double *dense_ji,
-                         double lambda_f, double lambda_g, double *A, double *b, double energy[2]);
+                         const int32_t *status, double lambda_f, double lambda_g, double *A, double *b,
+                         double energy[2]);
+/* status [P] (may be NULL = all registered): a pair whose registration failed (1 FEW_MATCHES,
+   2 FEW_INLIERS — S:290's signal) contributes no Eq. (2) term (reading R30); its Eq. (3)
+   edges are kept. */
 
 /* One Gauss-Newton step: solve A d = -b exactly (dense Cholesky, fp64) with the DOFs of
    fixed_node (I_0, kept constant) and every DOF whose diagonal is 0 (unconstrained)
@@ -150,8 +154,8 @@ int32_t bto_graph_system(int32_t n_nodes, const float *poses, const int32_t *pai
    definite. */
 int32_t bto_graph_step(int32_t n_nodes, const float *poses, const int32_t *pairs, int32_t P,
                        const double *feat, const double *dense_ij, const double *dense_ji,
-                       double lambda_f, double lambda_g, int32_t fixed_node, double *delta,
-                       float *new_poses, double energy[2]);
+                       const int32_t *status, double lambda_f, double lambda_g, int32_t fixed_node,
+                       double *delta, float *new_poses, double energy[2]);
 
 /* ---- NEXT-4: input prep — normal map from depth (SPEC estimate_normals; the
    paper's n_i(x), method unspecified) ------------------------------------------------

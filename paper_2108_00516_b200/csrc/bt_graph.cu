@@ -89,6 +89,10 @@ __global__ void __launch_bounds__(64) k_graph_contrib(GraphArgs A) {
   const float *dij = reinterpret_cast<const float *>(rec + rec_dense_ij(A.n_max));
   const float *dji = reinterpret_cast<const float *>(rec + rec_dense_ji(A.n_max));
   const float *feat = reinterpret_cast<const float *>(rec + rec_feat(A.n_max));
+  // a failed registration (S:290's signal: FEW_MATCHES / FEW_INLIERS) contributes no Eq. (2)
+  // term — its few "inliers" are not correspondences (reading R30); its dense edges stay
+  const int st = (int)rec[kRecStatus];
+  const double lf = (st == BT_PAIR_FEW_MATCHES || st == BT_PAIR_FEW_INLIERS) ? 0.0 : A.lf;
   if (tid < 36) {
     const int r = tid / 6, c = tid % 6;
     H1[tid] = dij[up21(r, c)];
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(64) k_graph_contrib(GraphArgs A) {
       d1 = -HA1[6 * c + r];
       d2 = -HA2[6 * r + c];
     }
-    C[e] = A.lf * f + A.lg * d1 + A.lg * d2;
+    C[e] = lf * f + A.lg * d1 + A.lg * d2;
   }
   if (tid < 12) {
     const int bi = tid / 6, r = tid % 6;
@@ -147,9 +151,9 @@ __global__ void __launch_bounds__(64) k_graph_contrib(GraphArgs A) {
       for (int k = 0; k < 6; ++k) d1 -= Adj1[6 * k + r] * g1[k];
       d2 = g2[r];
     }
-    C[144 + tid] = A.lf * (double)F[78 + tid] + A.lg * d1 + A.lg * d2;
+    C[144 + tid] = lf * (double)F[78 + tid] + A.lg * d1 + A.lg * d2;
   } else if (tid == 12) {
-    C[156] = A.lf * (double)F[90];
+    C[156] = lf * (double)F[90];
     C[157] = A.lg * ((double)dij[27] + (double)dji[27]);
   }
 }

@@ -30,7 +30,7 @@ PHILOX_SEED = 0x0123456789ABCDEF
 class Tracker:
     def __init__(self, K, n_max: int = 512, n_hyp: int = 4096, kf: int = 15, gn_iters: int = 2,
                  pool_cap: int = 96, cache_cap: int = 2048, novelty_deg: float = 10.0, device: int = 0,
-                 log: bool = False, seed: int = PHILOX_SEED):
+                 log: bool = False, seed: int = PHILOX_SEED, min_inliers: int = 20):
         import torch
         self.torch = torch
         self.K, self.n_max, self.kf, self.G = K, n_max, kf, gn_iters
@@ -44,7 +44,9 @@ class Tracker:
         W, H = int(K.width), int(K.height)
         maxp = max(self.NS * (self.NS - 1) // 2, 1)
         self.ctx.reserve(maxp, n_max, n_hyp, self.NS + 1, W, H)
-        self.rprm, self.eprm = ransac_params(n_hyp, seed), edge_params()
+        # a pair with fewer inliers is a failed registration (status FEW_INLIERS): the graph then
+        # drops its Eq. (2) term (reading R30) and the coarse pose keeps T_{t-1}
+        self.rprm, self.eprm = ransac_params(n_hyp, seed, min_inliers=min_inliers), edge_params()
         self.rw = record_words(n_max)
         dev = self.dev
 

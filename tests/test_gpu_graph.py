@@ -257,3 +257,27 @@ def test_relinearize_with_cached_matches_across_calls(bt, torch, ctx):
     assert (d["status"] == 0).sum() >= P // 2
     with pytest.raises(bt.BtError, match="EINVAL"):
         ctx.relinearize(fb, sc.K, P1, pr, eprm, rec, matches=mt, n_matches=None)
+
+
+def test_graph_step_failed_registrations_bring_no_feature_term(bt, torch, ctx):
+    """Reading R30: a pair whose record says FEW_MATCHES / FEW_INLIERS contributes its dense edges
+    but no Eq. (2) block — GPU and oracle (status array) agree; the same records with status OK
+    give a different step."""
+    sc = synth.make_scene(5, n=300, seed=23)
+    pairs = synth.all_pairs(5)
+    poses = sc.perturbed_poses(5, rot_deg=2.0, trans_m=0.01)
+    feat, dij, dji = oracle_blocks(sc, poses, pairs)
+    rec = records_from_blocks(bt, 512, feat, dij, dji)
+    status = np.zeros(len(pairs), np.int32)
+    status[[1, 4, 7]] = [2, 1, 2]
+    rec[:, 0] = status
+    f32 = rec.view(np.float32)
+    o = 28 + 16
+    args = (f32[:, o + 64:o + 160].astype(np.float64), f32[:, o:o + 32].astype(np.float64),
+            f32[:, o + 32:o + 64].astype(np.float64))
+    d_o, p_o, _ = oracle.graph_step(poses, pairs, *args, status=status)
+    d_ok, _, _ = oracle.graph_step(poses, pairs, *args)
+    d_g, p_g, _ = gpu_step(bt, torch, ctx, poses, pairs, rec, 512, max_iter=2000, rel_tol=1e-13)
+    assert np.abs(d_g - d_o).max() <= 1e-7 * np.abs(d_o).max() + 1e-12
+    assert np.abs(p_g - p_o).max() <= 2e-6
+    assert np.abs(d_ok - d_o).max() > 1e-3 * np.abs(d_o).max()

@@ -260,3 +260,22 @@ def test_graph_step_with_dense_edges_descends(scene3):
     assert E1 < 0.5 * E0 and E2 < E1
     assert np.array_equal(new[0], poses[0]) and np.array_equal(new2[0], poses[0])    # I_0 fixed
     del gtp
+
+
+def test_failed_registration_status_drops_only_the_feature_term():
+    """Reading R30: status 1 / 2 (S:290's registration-failure signal) zeroes the pair's Eq. (2)
+    contribution and keeps its Eq. (3) edges — the same system as zeroing those feat rows."""
+    rng = np.random.default_rng(4)
+    N, pairs = 4, np.array([(0, 1), (1, 2), (0, 3), (2, 3)], np.int32)
+    poses = np.stack([synth.pose12(synth.random_rotation(rng, 0.5), rng.normal(size=3) * 0.1 + [0, 0, 0.5])
+                      for _ in range(N)])
+    feat = rng.normal(size=(4, 96))
+    dij, dji = rng.normal(size=(4, 32)), rng.normal(size=(4, 32))
+    status = np.array([0, 2, 3, 1], np.int32)
+    A, b, e = oracle.graph_system(poses, pairs, feat, dij, dji, status=status)
+    fz = feat.copy()
+    fz[[1, 3]] = 0.0
+    A0, b0, e0 = oracle.graph_system(poses, pairs, fz, dij, dji)
+    assert np.array_equal(A, A0) and np.array_equal(b, b0) and e == e0
+    A1, _, _ = oracle.graph_system(poses, pairs, feat, dij, dji)
+    assert not np.array_equal(A, A1)

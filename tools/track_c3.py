@@ -39,6 +39,9 @@ def stats(r, t):
             "max_deg": float(r.max()), "mean_mm": 1e3 * float(t.mean()), "max_mm": 1e3 * float(t.max())}
 
 
+if os.environ.get("TRACK_DUMP"):                                  # per-frame errors for analysis
+    np.savez(os.environ["TRACK_DUMP"], rot=rot, trans=trans, orot=orot, otrans=otrans, ms=out["ms"],
+             order=np.array(order))
 print(json.dumps({
     "workload": f"C3: {FRAMES}-frame ORBIT replay (2 deg / frame, {V} views cycled, 0.5 mm keypoint noise), causal "
                 f"tracker: coarse pose from the consecutive pair (P:25), greedy K=15 keyframes on estimated "
