@@ -494,10 +494,14 @@ def main():
         step_ms = tot / args.steps                      # this kernel's device time per step
         ach = work_per_step / (step_ms / 1e3) / (1e12 if unit == "TFLOP/s" else 1e9)
         st, sn = solo.get(name, (0.0, 0))
+        solo_ms = st / 5 if sn else None
         kern[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
                       "avg_launch_ms": tot / n, "launches_per_step": n / args.steps,
                       "share_of_step": tot / ms_i if ms_i else None,
-                      "standalone_ms_per_step": st / 5 if sn else None, "work": note}
+                      "standalone_ms_per_step": solo_ms,
+                      # the same work over the stage's time when it runs alone (no dense stream beside it)
+                      "frac_standalone": (work_per_step / (solo_ms / 1e3) / (1e12 if unit == "TFLOP/s" else 1e9) / peak)
+                      if solo_ms else None, "work": note}
     pair_sizes = float(sum(int(sc.n_kp[a]) * int(sc.n_kp[b]) for a, b in pairs))
     tc_peak = float(peaks.get("bf16_tflops", 1614.4))     # fp16 kind::f16 = bf16 rate (guide ratio 1:1)
     add("k_match_tc", "tensor", 2 * pair_sizes * 128, "TFLOP/s", tc_peak,

@@ -149,6 +149,7 @@ struct TcArgs {
   int n_pad, ibits, P, force_fallback;
   float ratio2;
   int fs_batched;                              // undecided rows -> per-tile lists (k_fullscan), else queue 1
+  unsigned kmul;                               // 512 (IMAD-key variant): a runtime operand keeps it an IMAD
 };
 
 constexpr int kN = 128;                       // B columns per MMA chunk (N); B and TMEM double-buffered
@@ -171,6 +172,30 @@ __device__ __forceinline__ int certify(unsigned k1, unsigned k2, unsigned k3, fl
   if (k3 == kNone) return 2;
   const float v3 = key_value(k3 & ~imask);
   if ((v3 - v1) > eps2 + ldexpf(fabsf(v1) + fabsf(v3), ibits - 21) + 1e-30f) return 2;
+  return 0;
+}
+
+// IMAD keys (n_pad <= 512): the ranked value is mapped into [1, 2) — v = 1 + c d'' with
+// c = 1 / (M_b^2 + 4.02 M_a M_b), still ONE FFMA per element (column constant 1 + c(|b|^2 +
+// 2.01 M_a M_b), scale -2 M_a M_b c) — so its float bits are 0x3F8xxxxx with a fixed exponent,
+// and bits * 512 + j (mod 2^32; the exponent bits shift out) is the 23-bit mantissa followed by
+// the 9-bit column index: the key is ONE IMAD on the FMA pipe instead of a LOP3 on the ALU
+// pipe (the epilogue is ALU-bound: min / max of the top-3), and no value bit is truncated.
+// d'' in [0.008 M_a M_b, M_b^2 + 4.012 M_a M_b] (S'' <= 1 + 1e-3) keeps v strictly inside
+// [1, 2 - 1.6e-3); a padded column's constant is the largest float below 2 (key 0xFFFFFE00 | j).
+// Certificate in key units u = 2^-23 / c: each key's value is within 2.5 u of 1 + c d'' (the
+// FFMA, the constant's and the scale's fp32 rounding), so 8 u covers a difference of two.
+__device__ __forceinline__ int certify_imad(unsigned k1, unsigned k2, unsigned k3, float qn, float mr, float pp,
+                                            float ma, float mb) {
+  if (k1 == kNone) return 0;
+  if (k2 == kNone) return 1;
+  const float u = ldexpf(mb * mb + 4.02f * ma * mb, -23);
+  const float eps2 = 2.f * (2.2e-3f * qn * mr + 1e-6f * (qn * qn + mr * mr) + 3e-6f * pp) + 8.f * u;
+  const float d21 = (float)((k2 >> 9) - (k1 >> 9)) * u;
+  if (d21 > eps2) return 1;
+  if (k3 == kNone) return 2;
+  const float d31 = (float)((k3 >> 9) - (k1 >> 9)) * u;
+  if (d31 > eps2) return 2;
   return 0;
 }
 
@@ -214,6 +239,7 @@ __device__ __forceinline__ TcItem tc_item(const TcArgs &A, int it) {
   return I;
 }
 
+template <bool kImad>
 __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constant__ CUtensorMap tmap, TcArgs A) {
   pdl_wait();
   extern __shared__ uint8_t tc_smem_raw[];
@@ -221,7 +247,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
   __shared__ uint32_t tmem_base_sh;
   __shared__ __align__(16) uint4 rmerge[2][128];
   __shared__ int fs_warp[4];
-  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned by an offset from the shared array itself (not an integer round trip), so the
+  // compiler keeps the shared address space: LDS for the column constants, not generic LD
+  uint8_t *base = tc_smem_raw + ((1024u - (smem_u32(tc_smem_raw) & 1023u)) & 1023u);
   uint8_t *sA = base;                                           // [2 K-atoms][128 rows][128 B]
   uint8_t *sB = base + 32768;                                   // [2 buffers][2 K-atoms][128 rows][128 B]
   float2 *cconst = reinterpret_cast<float2 *>(base + 3 * 32768);  // [2][kN] (|b_j|^2 + 2.01 P_a P_b, j bits)
@@ -267,7 +295,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
       In.skip = true;
       if (itn < n_items) In = tc_item(A, itn);
       if (!I.skip) {
-        const float coff = 2.01f * frame_scale(A.S.maxnorm[I.fa]) * frame_scale(A.S.maxnorm[I.fb]);
+        const float ma_ = frame_scale(A.S.maxnorm[I.fa]), mb_ = frame_scale(A.S.maxnorm[I.fb]);
+        const float coff = 2.01f * ma_ * mb_;
+        const float cinv = kImad ? 1.0f / (mb_ * mb_ + 4.02f * ma_ * mb_) : 0.f;
         for (int c = 0; c < I.nchunks; ++c, ++g) {
           const int b = g & 1;
           if (!nv_ok) {
@@ -296,8 +326,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
             const int jj = q * 32 + lane, j = c * kN + jj;
             // |b_j|^2 + the offset that keeps every ranked value >= 0; a column past n_b ranks at
             // +inf (no per-element bound check in the epilogue)
-            cconst[b * kN + jj] = make_float2(j < I.nb ? __fmaf_rn(nv[q], nv[q], coff) : CUDART_INF_F,
-                                              __uint_as_float((unsigned)j));
+            if (kImad)
+              cconst[b * kN + jj] = make_float2(j < I.nb ? __fmaf_rn(cinv, __fmaf_rn(nv[q], nv[q], coff), 1.0f)
+                                                         : __uint_as_float(0x3FFFFFFFu),
+                                                __uint_as_float((unsigned)j));
+            else
+              cconst[b * kN + jj] = make_float2(j < I.nb ? __fmaf_rn(nv[q], nv[q], coff) : CUDART_INF_F,
+                                                __uint_as_float((unsigned)j));
           }
           __syncwarp();
           if (lane == 0) {
@@ -350,7 +385,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
       const TcItem I = In;
       const float na_n = na_nx, mr = mr_nx;
       // S'' = (a / P_a).(b / P_b): d' = |b|^2 - 2 P_a P_b S''
-      const float pp = frame_scale(ma_nx) * frame_scale(mb_nx), kscale = -2.f * pp;
+      const float fsa = frame_scale(ma_nx), fsb = frame_scale(mb_nx);
+      const float pp = fsa * fsb;
+      const float kscale = kImad ? -2.f * pp * (1.0f / (fsb * fsb + 4.02f * pp)) : -2.f * pp;
       if (it + (int)gridDim.x < n_items) {                        // prefetch the next item
         In = tc_item(A, it + gridDim.x);
         na_nx = A.S.norm[(size_t)In.fa * n_pad + In.rt * 128 + lrow];
@@ -382,8 +419,14 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
             // d'' = d' + 2.01 P_a P_b >= 0 (one FFMA), so the float bits order like the values
             const float d0 = __fmaf_rn(kscale, __uint_as_float(v[col]), cc2.x);
             const float d1 = __fmaf_rn(kscale, __uint_as_float(v[col + 1]), cc2.z);
-            const unsigned k0 = (__float_as_uint(d0) & ~imask) | __float_as_uint(cc2.y);
-            const unsigned k1 = (__float_as_uint(d1) & ~imask) | __float_as_uint(cc2.w);
+            unsigned k0, k1;
+            if (kImad) {                                          // one IMAD each (FMA pipe)
+              asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k0) : "r"(__float_as_uint(d0)), "r"(A.kmul), "r"(__float_as_uint(cc2.y)));
+              asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k1) : "r"(__float_as_uint(d1)), "r"(A.kmul), "r"(__float_as_uint(cc2.w)));
+            } else {
+              k0 = (__float_as_uint(d0) & ~imask) | __float_as_uint(cc2.y);
+              k1 = (__float_as_uint(d1) & ~imask) | __float_as_uint(cc2.w);
+            }
             const unsigned m = min(k0, k1), M = max(k0, k1);
             if ((col & 2) == 0) {
               const unsigned n3 = min(min(r3, max(r2, m)), max(r1, M)), n2 = min(min(r2, max(r1, m)), M);
@@ -423,7 +466,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
         }
         level = 0;
         if (!A.force_fallback && A.ratio2 >= 1.f)
-          level = certify(r1, r2, r3, na_n, mr, pp, A.ibits);
+          level = kImad ? certify_imad(r1, r2, r3, na_n, mr, pp, fsa, fsb) : certify(r1, r2, r3, na_n, mr, pp, A.ibits);
         const size_t o_nn = (size_t)I.p * A.kp.n_max + i;
         if (level == 1) {
           (I.dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o_nn] = (int32_t)(r1 & imask);
@@ -869,15 +912,17 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   // batched full scans pay off when a row's scan reads >= 512 KB of references (n >= 1024);
   // below that the per-row queue (one CTA per row, 8 warps split the references) is faster
   const int fs_batched = kp.n_max >= kFsBatchRefs ? 1 : 0;
-  TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2, fs_batched};
+  TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2, fs_batched, 512u};
+  const bool imad_keys = ibits <= 9 && !getenv("BT_MATCH_LOP3");   // BT_MATCH_LOP3: dev A/B of the key packing
+  auto kws = imad_keys ? k_match_ws<true> : k_match_ws<false>;
   L.begin(K_MATCH_TC, s);
   // two CTAs per SM by design (2 x 108 KB of shared memory, 2 x 256 TMEM columns, 96 registers;
   // ncu: block limits 2 / 2); the occupancy API reports 1 for this configuration, so the grid
   // is sized directly (a CTA that does not fit only waits: no CTA depends on another)
-  smem_optin((const void *)k_match_ws, kWsSmem);
-  cudaFuncSetAttribute(k_match_ws, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  smem_optin((const void *)kws, kWsSmem);
+  cudaFuncSetAttribute(kws, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   const int ws_grid = sm_count() * 2;
-  launch_pdl(k_match_ws, std::min(ws_grid, 2 * P * rt_count), kWsThreads, kWsSmem, s, *tmap, ta);
+  launch_pdl(kws, std::min(ws_grid, 2 * P * rt_count), kWsThreads, kWsSmem, s, *tmap, ta);
   L.end(K_MATCH_TC, s);
   L.begin(K_RESOLVE, s);
   RescoreArgs ra{kp, pairs, S, ibits, ratio2};

@@ -176,3 +176,53 @@ def test_score_tc_equals_fma_c5_shape(bt, torch):
     ctx.close()
     assert (nm > 1500).all()
     _assert_equal(out, "C5 shape")
+
+
+def test_score_tc_equals_fma_adversarial_exponent_spread(bt, torch):
+    """an adversarial check of R27's accumulator model.  Correspondence sets whose
+    centred features span many binades in ONE pair (points from 0.1 mm to 5 m from the centroid,
+    so Y1's k-columns mix magnitudes ~1e-8 .. 25 m^2), hypotheses from triples that mix the
+    scales (huge |t'|, heavy cancellation in |R a' + t' - b'|^2 - |t'|^2), near-gate
+    inliers at exactly delta +- 1e-3 delta, and flipped / grazing normals.  The tensor-core counts
+    must still equal the FFMA2 kernel's bit for bit: every test the certificate cannot decide is
+    recounted by the fp32 formula."""
+    rng = np.random.default_rng(1234)
+    n_max = 1024
+    F = 6
+    sc = synth.make_scene(2, render_maps=False, seed=3)
+    sc.n_kp = np.zeros(F, np.int32)
+    sc.desc = np.zeros((F, n_max, 128), np.float32)
+    sc.pts = np.zeros((F, n_max, 3), np.float32)
+    sc.nrm = np.zeros((F, n_max, 3), np.float32)
+    mls, pairs = [], []
+    for q in range(F // 2):
+        M = 900
+        scale = 10.0 ** rng.uniform(-4, np.log10(5.0), size=(M, 1))      # 0.1 mm .. 5 m
+        d = rng.normal(size=(M, 3))
+        pa = d / np.linalg.norm(d, axis=1, keepdims=True) * scale + [0, 0, 0.6]
+        R = synth.random_rotation(rng, np.pi)
+        t = rng.normal(size=3) * 10.0 ** rng.uniform(-3, 1)
+        pb = pa @ R.T + t
+        # a third of the partners sit on the distance gate (delta = 5 mm) +- 1e-3 delta
+        k = rng.permutation(M)[:M // 3]
+        u = rng.normal(size=(len(k), 3))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        pb[k] += u * 0.005 * (1.0 + rng.choice([-1e-3, 1e-3], size=(len(k), 1)))
+        na = rng.normal(size=(M, 3))
+        na /= np.linalg.norm(na, axis=1, keepdims=True)
+        nb = na @ R.T
+        flip = rng.random(M) < 0.2
+        nb[flip] *= -1.0                                                 # flipped normals
+        a, b = 2 * q, 2 * q + 1
+        sc.n_kp[a] = sc.n_kp[b] = M
+        sc.pts[a, :M], sc.pts[b, :M] = pa, pb
+        sc.nrm[a, :M], sc.nrm[b, :M] = na, nb
+        mls.append(np.stack([np.arange(M), rng.permutation(M)], 1).astype(np.int32) if q == 2 else
+                   np.stack([np.arange(M), np.arange(M)], 1).astype(np.int32))
+        pairs.append((a, b))
+    ctx = bt.Context(0)
+    ctx.reserve(len(pairs), n_max, 4096, F)
+    out, nm = _run_both(bt, torch, ctx, sc, pairs, 4096, match_lists=mls)
+    ctx.close()
+    _assert_equal(out, "adversarial")
+    assert (out["tc"][1][:2] > 100).any()                                # real inliers exist
