@@ -65,6 +65,8 @@ def parse():
                     help="distinct synthetic scenes the 64 tracks cycle through (bounds CPU scene generation)")
     ap.add_argument("--c5", action="store_true", help="add the C5 stress block (n=4096, 2016 pairs; slow to generate)")
     ap.add_argument("--c5-steps", type=int, default=3)
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N > 1 record exchange: fused producer stores into symmetric memory (NEXT-3) or NCCL")
     return ap.parse_args()
 
 
@@ -135,12 +137,28 @@ def multi_block(kind, args, bt, parallel, torch, dist, world, rank, local, dev, 
     rprm, eprm = bt.ransac_params(n_hyp, synth.PHILOX_SEED), bt.edge_params()
     stream = torch.cuda.current_stream(dev)
     gathered = [None]
+    # the exchange: NEXT-3's fused record stores into every rank's symmetric-memory gather buffer
+    # (one barrier), else one NCCL all_gather_into_tensor of the records
+    fused = None
+    if world > 1 and args.exchange != "nccl" and parallel.FusedRecordExchange.available():
+        try:
+            fused = parallel.FusedRecordExchange(ctx, plan.rows, bt.record_words(n_max), device=dev)
+        except Exception as e:                                   # no peer access: NCCL all-gather
+            print(f"[bench] fused record exchange unavailable ({type(e).__name__}: {e}); NCCL all-gather",
+                  file=sys.stderr)
+            fused = None
+    exchange_kind = ("fused: producer kernels store each record word into every rank's symmetric-memory "
+                     "gather buffer (bt_set_record_peers), one barrier" if fused is not None else
+                     f"one all_gather_into_tensor of the fixed-stride records over NCCL")
+
+    def exchange():
+        if world > 1:
+            gathered[0] = fused.finish() if fused is not None else parallel.all_gather_rows(rec, plan.rows)
 
     def one():
         if P_r:
             ctx.register_pairs(fb, K, t_pose, t_pairs, t_uid, rprm, eprm, rec, stream=stream)
-        if world > 1:
-            gathered[0] = parallel.all_gather_rows(rec, plan.rows)
+        exchange()
     for _ in range(2):
         one()
     torch.cuda.synchronize()
@@ -157,8 +175,7 @@ def multi_block(kind, args, bt, parallel, torch, dist, world, rank, local, dev, 
             if P_r:
                 ctx.register_pairs(fb, K, t_pose, t_pairs, t_uid, rprm, eprm, rec, stream=stream)
             gx[k][0].record(stream)
-            if world > 1:
-                gathered[0] = parallel.all_gather_rows(rec, plan.rows)
+            exchange()
             gx[k][1].record(stream)
             ev[k][1].record(stream)
         torch.cuda.synchronize()
@@ -173,9 +190,14 @@ def multi_block(kind, args, bt, parallel, torch, dist, world, rank, local, dev, 
     d = bt.decode_records(rec, n_max)
     ok = torch.tensor([int((d["status"] == 0).sum()), int(d["n_matches"].astype(np.int64).sum())],
                       dtype=torch.int64, device=dev)
+    same = None
     if world > 1:
         dist.all_reduce(ok)
         assert gathered[0].shape[0] == n_total
+        # the exchange is exact: this rank's rows of the gathered table are its own records
+        same = bool(torch.equal(gathered[0][plan.row_lo: plan.row_lo + P_r], rec))
+    if fused is not None:
+        fused.close()
     ctx.close()
     del fb, rec
     torch.cuda.empty_cache()
@@ -185,8 +207,9 @@ def multi_block(kind, args, bt, parallel, torch, dist, world, rank, local, dev, 
             "ms_per_step": ms_max / steps, "exchange_ms_per_step": gms_max / steps, "steps": steps, "warmup": 2,
             "scaling": "strong", "n_gpus": world, "pairs_this_rank": P_r, "status_ok": int(ok[0].item()),
             "gpu_launches": launches * steps, "clocks": clk.summary(), "scene_generation_s": gen_s,
-            "exchange": f"one all_gather_into_tensor of the fixed-stride records ({4 * bt.record_words(n_max)} B "
-                        f"per pair, {n_total} pairs) over NCCL" if world > 1 else "none (one rank)",
+            "exchange": (f"{exchange_kind} ({4 * bt.record_words(n_max)} B per pair, {n_total} pairs)"
+                         if world > 1 else "none (one rank)"),
+            "exchange_rows_match_local": same,
             "l2": "flushed (512 MiB memset) before each step, outside the events",
             "launch": "eager (the step is ms-long; launch overhead is negligible)"}
 

@@ -183,6 +183,23 @@ bt_status bt_register_pairs_host(bt_ctx *ctx, const bt_keypoints *kp, const bt_m
                                  const bt_match_params *mprm, const bt_ransac_params *rprm,
                                  const bt_edge_params *eprm, uint32_t *records, void *stream);
 
+/* NEXT-3: fused record exchange.  The per-pair records are what every rank's
+   pose-graph solve needs (the pair correspondences built "in parallel on GPU", §IV-D);
+   instead of a separate all-gather, after this call every bt_register_pairs (device entry) on
+   this context ALSO stores each word of local pair p's record into row (row_offset + p) of
+   every peer buffer peers[k], k < n_peers: device addresses valid in this process (another
+   rank's gather buffer mapped through CUDA IPC / symmetric memory, or a local buffer), each
+   holding `rows` records of bt_record_words(n_max) words (the call's n_max).  The stores are
+   issued by the kernels that produce the words (RANSAC finish: header, mask, Eq. (2) blocks;
+   dense reduce: Eq. (3) blocks), so the exchange rides on them; the caller orders them before
+   any reader on another device with a barrier after the call (e.g. the symmetric-memory
+   barrier).  The local `records` output is written as before.  n_peers = 0 turns it off.
+   Ownership: the peer buffers stay the caller's; the context keeps the addresses only.
+   Errors: BT_EINVAL (n_peers outside [0, 8], peers NULL or holding a 0 address, row_offset < 0,
+   rows < 1); bt_register_pairs then fails with BT_ECAPACITY when row_offset + P > rows. */
+bt_status bt_set_record_peers(bt_ctx *ctx, int32_t n_peers, const uint64_t *peers, int32_t row_offset,
+                              int32_t rows);
+
 /* out[n] = a[n] * b[n] (device bt_pose arrays): the coarse pose T~_t = T_rel T_{t-1} of
    P:25 under object->camera poses (reading R13), without a host round trip. */
 bt_status bt_compose_poses(bt_ctx *ctx, const bt_pose *a, const bt_pose *b, bt_pose *out,

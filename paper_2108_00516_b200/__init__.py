@@ -27,7 +27,8 @@ SYMBOLS = ("bt_create", "bt_destroy", "bt_last_error", "bt_status_string", "bt_r
            "bt_register_pairs_host", "bt_compose_poses", "bt_last_launch_count", "bt_profile_enable",
            "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step",
            "bt_estimate_normals", "bt_relinearize", "bt_relinearize_matches", "bt_copy_matches",
-           "bt_dense_assoc", "bt_lift_keypoints", "bt_coarse_pose", "bt_select_keyframes", "bt_pool_admit")
+           "bt_dense_assoc", "bt_lift_keypoints", "bt_coarse_pose", "bt_select_keyframes", "bt_pool_admit",
+           "bt_set_record_peers")
 
 
 class BtError(RuntimeError):
@@ -118,6 +119,7 @@ def lib():
         L.bt_coarse_pose.argtypes = [vp, vp, vp, vp, vp]
         L.bt_select_keyframes.argtypes = [vp, vp, vp, i32, vp, i32, vp, vp, vp]
         L.bt_pool_admit.argtypes = [vp, vp, vp, i32, vp, C.c_float, vp, vp]
+        L.bt_set_record_peers.argtypes = [vp, i32, C.POINTER(C.c_uint64), i32, i32]
         L.bt_last_launch_count.argtypes = [vp]
         L.bt_last_launch_count.restype = i32
         L.bt_profile_enable.argtypes = [vp, i32]
@@ -131,7 +133,7 @@ def lib():
         for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_dense_assoc", "bt_register_pairs",
                   "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals", "bt_relinearize",
                   "bt_relinearize_matches", "bt_copy_matches", "bt_lift_keypoints", "bt_coarse_pose",
-                  "bt_select_keyframes", "bt_pool_admit"):
+                  "bt_select_keyframes", "bt_pool_admit", "bt_set_record_peers"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -292,6 +294,15 @@ class Context:
                 C.byref(rprm), C.byref(eprm) if eprm is not None else None, _ptr(records),
                 self._stream(stream))
         self._check(st, "bt_register_pairs_host" if host else "bt_register_pairs")
+
+    def set_record_peers(self, peer_ptrs, row_offset: int = 0, rows: int = 0):
+        """NEXT-3 (bt_set_record_peers): register_pairs also stores local pair p's record into row
+        row_offset + p of every peer buffer (device addresses, e.g. symmetric-memory buffer_ptrs
+        of the other ranks' gather buffers); an empty list turns it off."""
+        ptrs = [int(x) for x in peer_ptrs]
+        arr = (C.c_uint64 * max(1, len(ptrs)))(*ptrs)
+        self._check(lib().bt_set_record_peers(self._h, len(ptrs), arr, int(row_offset), int(rows)),
+                    "bt_set_record_peers")
 
     def profile(self, on: bool = True):
         """Bracket every kernel launch with CUDA events on its stream (bt_profile_enable)."""

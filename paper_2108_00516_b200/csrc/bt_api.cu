@@ -48,6 +48,8 @@ struct bt_ctx {
   void *graph = nullptr;                      // pose-graph step scratch (bt_graph.cu)
   int cached_P = -1;                          // pairs whose match lists c->matches holds (C_ij cache)
   int cached_nmax = -1;                       // ... and their row stride
+  bt::PeerRec peers;                          // NEXT-3: fused record exchange (bt_set_record_peers)
+  int peer_rows = 0;                          // rows each peer buffer holds
   // staging for bt_register_pairs_host
   int32_t *st_nkp = nullptr, *st_pairs = nullptr;
   uint32_t *st_uid = nullptr, *st_records = nullptr;
@@ -277,6 +279,22 @@ int32_t bt_last_launch_count(const bt_ctx *c) { return c ? c->launch.count : 0; 
 
 size_t bt_record_words(int32_t n_max) { return n_max < 1 ? 0 : (size_t)bt::rec_words(n_max); }
 
+bt_status bt_set_record_peers(bt_ctx *c, int32_t n_peers, const uint64_t *peers, int32_t row_offset, int32_t rows) {
+  BT_CHECK_CTX(c);
+  if (n_peers < 0 || n_peers > bt::kMaxPeers) return fail(c, BT_EINVAL, "bt_set_record_peers: n_peers %d", n_peers);
+  if (n_peers > 0 && (!peers || row_offset < 0 || rows < 1))
+    return fail(c, BT_EINVAL, "bt_set_record_peers: bad peers / row_offset / rows");
+  for (int k = 0; k < n_peers; ++k)
+    if (!peers[k]) return fail(c, BT_EINVAL, "bt_set_record_peers: peer %d NULL", k);
+  bt::PeerRec pr;
+  for (int k = 0; k < bt::kMaxPeers; ++k) pr.ptr[k] = k < n_peers ? (uint32_t *)(uintptr_t)peers[k] : nullptr;
+  pr.n = n_peers;
+  pr.row_off = n_peers ? row_offset : 0;
+  c->peers = pr;
+  c->peer_rows = n_peers ? rows : 0;
+  return BT_OK;
+}
+
 bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hyp, int32_t max_frames,
                      int32_t width, int32_t height) {
   BT_CHECK_CTX(c);
@@ -422,6 +440,9 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
                                     uint32_t *records, cudaStream_t st) {
   const int rw = bt::rec_words(kp->n_max);
   const float ratio = mprm ? mprm->ratio : 1.f;
+  bt::PeerRec pr = c->peers;                                    // NEXT-3: stores into the peers' rows too
+  pr.stride = rw;
+  const bt::PeerRec *peers = pr.n ? &pr : nullptr;
   // fork: the dense edges only need the maps and node poses, so they run on the side stream
   // while matching and RANSAC run on the caller's stream (event fork / join: capturable)
   // with the dense edges forked off, match -> RANSAC (the longer chain) runs on a high-priority
@@ -432,12 +453,12 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
     cudaStreamWaitEvent(c->side, c->ev_fork, 0);
     if (ms != st) cudaStreamWaitEvent(ms, c->ev_fork, 0);
     bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, nullptr, 0, records, rw,
-                     bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch);
+                     bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch, nullptr, peers);
   }
   bt::launch_match(kview(kp), pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches, c->n_matches,
                    ms, c->launch);
   bt::launch_ransac(kview(kp), pairs, uid, P, c->matches, c->n_matches, *rprm, c->rs, records, rw, nullptr,
-                    eprm ? node_pose : nullptr, eprm ? eprm->huber_m : 0.f, ms, c->launch);
+                    eprm ? node_pose : nullptr, eprm ? eprm->huber_m : 0.f, ms, c->launch, peers);
   if (eprm) {
     cudaEventRecord(c->ev_join, c->side);
     cudaStreamWaitEvent(st, c->ev_join, 0);
@@ -470,6 +491,8 @@ bt_status bt_register_pairs(bt_ctx *c, const bt_keypoints *kp, const bt_maps *ma
   if (P == 0) return BT_OK;
   if (eprm && (s = check_dense_bytes(c, maps, 2 * P)) != BT_OK) return s;
   if (!pairs || !pair_uid || !records) return fail(c, BT_EINVAL, "bt_register_pairs: NULL buffer");
+  if (c->peers.n && c->peers.row_off + P > c->peer_rows)
+    return fail(c, BT_ECAPACITY, "bt_register_pairs: peer rows %d + P %d > %d", c->peers.row_off, P, c->peer_rows);
   return register_pairs_dev(c, kp, maps, K, node_pose, pairs, pair_uid, P, mprm, rprm, eprm, records,
                             (cudaStream_t)stream);
 }

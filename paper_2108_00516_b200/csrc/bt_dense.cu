@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
 __global__ void __launch_bounds__(256) k_dense_reduce(const float *__restrict__ partials, const int32_t *__restrict__ nch,
                                                        int tiles, const int32_t *edges, const int32_t *pairs, float *out,
                                                        int out_stride, uint32_t *records, int rec_stride, int off_ij,
-                                                       int off_ji) {
+                                                       int off_ji, PeerRec peers) {
   pdl_wait();
   __shared__ double wsum[8][32];
   const int e = blockIdx.x;
@@ -606,6 +606,7 @@ __global__ void __launch_bounds__(256) k_dense_reduce(const float *__restrict__ 
   if (records) {
     const int p = e >> 1;
     records[(size_t)p * rec_stride + ((e & 1) ? off_ji : off_ij) + lane] = __float_as_uint(v);
+    peer_put(peers, p, ((e & 1) ? off_ji : off_ij) + lane, __float_as_uint(v));
   } else {
     out[(size_t)e * out_stride + lane] = v;
   }
@@ -644,7 +645,7 @@ size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H) {
 void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
                   const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, float *out,
                   int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
-                  cudaStream_t s, Launch &L, int32_t *assoc) {
+                  cudaStream_t s, Launch &L, int32_t *assoc, const PeerRec *peers) {
   if (E <= 0) return;
   DenseArgs a;
   a.assoc = assoc;
@@ -703,7 +704,7 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   L.end(K_DENSE, s);
   L.begin(K_DENSE_REDUCE, s);
   launch_pdl(k_dense_reduce, E, 256, 0, s, a.partials, a.nch, a.tiles, edges, pairs, out, out_stride, records,
-                                  rec_stride, rec_off_ij, rec_off_ji);
+             rec_stride, rec_off_ij, rec_off_ji, peers ? *peers : PeerRec{});
   L.end(K_DENSE_REDUCE, s);
 }
 

@@ -25,6 +25,20 @@ __host__ __device__ inline int rec_dense_ji(int n_max) { return rec_dense_ij(n_m
 __host__ __device__ inline int rec_feat(int n_max) { return rec_dense_ij(n_max) + 64; }
 __host__ __device__ inline int rec_words(int n_max) { return rec_dense_ij(n_max) + 64 + 96; }
 
+// ---- NEXT-3: fused record exchange (bt_set_record_peers) ----------------------------------
+// The kernels that produce a record's words also store each word into row (row_off + p) of
+// every peer's gather buffer (another rank's buffer mapped into this process through CUDA IPC /
+// symmetric memory, or a local one): the all-gather of the records rides on the producers'
+// own stores, no separate collective kernel.
+constexpr int kMaxPeers = 8;
+struct PeerRec {
+  uint32_t *ptr[kMaxPeers];
+  int n = 0, row_off = 0, stride = 0;
+};
+__device__ __forceinline__ void peer_put(const PeerRec &pr, int p, int w, uint32_t v) {
+  for (int k = 0; k < pr.n; ++k) pr.ptr[k][(size_t)(pr.row_off + p) * pr.stride + w] = v;
+}
+
 // ---- device views of the ABI structs ---------------------------------------------------
 struct KpView {
   int n_frames, n_max;
@@ -134,12 +148,12 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
                    const int32_t *matches, const int32_t *n_matches, const bt_ransac_params &prm,
                    const RansacScratch &rs, uint32_t *records, int rec_stride,
                    int32_t *hyp_counts, const bt_pose *node_pose, float huber, cudaStream_t s,
-                   Launch &L);
+                   Launch &L, const PeerRec *peers = nullptr);
 // dense Eq. (3): edges either explicit (edges != null) or derived from pairs (2 per pair)
 void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
                   const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, float *out,
                   int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
-                  cudaStream_t s, Launch &L, int32_t *assoc = nullptr);
+                  cudaStream_t s, Launch &L, int32_t *assoc = nullptr, const PeerRec *peers = nullptr);
 int dense_tiles(int W, int H);
 size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H);
 // Eq. (2) blocks re-linearized at new node poses from the records' inlier masks (C_ij reuse)

@@ -597,6 +597,7 @@ struct FinishArgs {
   int rec_stride;
   const bt_pose *node_pose;      // null: no feature blocks
   double huber;
+  PeerRec peers;                 // NEXT-3: the record words also go to the peers' gather buffers
 };
 
 constexpr int kFinThreads = 256;
@@ -608,7 +609,8 @@ constexpr int kFeatRow = 3 * 13 + 2;             // per residual component q: J_
 // inl[0 .. n_feat) = the inlier match indices in ascending order (C_ij), frow: smem rows.
 __device__ void feature_blocks(const int *inl, int n_feat, const int32_t *mt, const float *pa_f, const float *pb_f,
                                const bt_pose &Pi, const bt_pose &Pj, double huber, float *frow,
-                               float (*fpart)[96], uint32_t *feat_out) {
+                               float (*fpart)[96], uint32_t *feat_out, const PeerRec *pr = nullptr, int pp = 0,
+                               int pw = 0) {
   // e = R_i^T (p_m - t_i) - R_j^T (p_n - t_j) (fp64: it cancels ~0.5 m coordinates);
   // J_i = -R_i^T [I | -[p_m]x], J_j = R_j^T [I | -[p_n]x];  H += w J^T J, g += w J^T e,
   // E += rho(|e|).  Every thread builds rows (fp32 after the fp64 residual) into smem; warp w
@@ -707,6 +709,7 @@ __device__ void feature_blocks(const int *inl, int n_feat, const int32_t *mt, co
     float t = 0.f;
     for (int w = 0; w < kFinThreads / 32; ++w) t += fpart[w][tid];
     feat_out[tid] = __float_as_uint(tid < 92 ? t : 0.f);
+    if (pr) peer_put(*pr, pp, pw + tid, __float_as_uint(tid < 92 ? t : 0.f));
   }
 }
 
@@ -807,7 +810,10 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     }
     const unsigned bal = __ballot_sync(0xffffffffu, in);
     if (lane == 0) {
-      if (!feat_cta && (m0 >> 5) + warp < W) rec[kRecMask + (m0 >> 5) + warp] = bal;
+      if (!feat_cta && (m0 >> 5) + warp < W) {
+        rec[kRecMask + (m0 >> 5) + warp] = bal;
+        peer_put(A.peers, p, kRecMask + (m0 >> 5) + warp, bal);
+      }
       wcnt[warp] = __popc(bal);
     }
     __syncthreads();
@@ -825,7 +831,8 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
   if (feat_cta) {
     // ---- Eq. (2) feature edge at the node poses ----------------------------------
     feature_blocks(inl, best_h >= 0 ? best_count : 0, mt, pa_f, pb_f, A.node_pose[fa], A.node_pose[fb], A.huber,
-                   reinterpret_cast<float *>(inl + ((n_max + 3) & ~3)), fpart, rec + rec_feat(n_max));
+                   reinterpret_cast<float *>(inl + ((n_max + 3) & ~3)), fpart, rec + rec_feat(n_max),
+                   A.peers.n ? &A.peers : nullptr, p, rec_feat(n_max));
     return;
   }
   if (best_h >= 0 && best_count < A.min_inliers) status = BT_PAIR_FEW_INLIERS;
@@ -890,6 +897,8 @@ __global__ void __launch_bounds__(kFinThreads) k_ransac_finish(FinishArgs A) {
     for (int k = 0; k < 12; ++k) rec[kRecTBest + k] = __float_as_uint(Tb[k]);
     for (int k = 0; k < 12; ++k)
       rec[kRecTRefit + k] = __float_as_uint(refit_ok ? (float)(k < 9 ? Rr[k] : tr[k - 9]) : Tb[k]);
+    if (A.peers.n)
+      for (int w = 0; w < kRecMask; ++w) peer_put(A.peers, p, w, rec[w]);
   }
 }
 
@@ -1568,7 +1577,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
                    const int32_t *matches, const int32_t *n_matches, const bt_ransac_params &prm,
                    const RansacScratch &rs, uint32_t *records, int rec_stride,
                    int32_t *hyp_counts, const bt_pose *node_pose, float huber, cudaStream_t s,
-                   Launch &L) {
+                   Launch &L, const PeerRec *peers) {
   if (P <= 0) return;
   const int chunk = kp.n_max < kMaxChunk ? ((kp.n_max + 31) / 32) * 32 : kMaxChunk;   // multiple of 32
   const size_t smem = (size_t)4 * chunk * sizeof(float4);
@@ -1637,6 +1646,7 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
   f.k0 = a.k0; f.k1 = a.k1; f.ndelta2 = a.ndelta2; f.ncosa = a.ncosa; f.tau = a.tau;
   f.counts = a.counts; f.hyp = a.hyp; f.nb = a.nb; f.hyp_counts = hyp_counts; f.records = records; f.rec_stride = rec_stride;
   f.node_pose = node_pose; f.huber = huber;
+  if (peers) f.peers = *peers;
   L.begin(K_RANSAC_FINISH, s);
   const size_t fin_smem = (size_t)((mask_words(kp.n_max) * 32 + 3) & ~3) * sizeof(int) +
                           (node_pose ? (size_t)kFeatChunk * kFeatRow * sizeof(float) : 0);

@@ -110,3 +110,51 @@ def all_gather_records(local, n_total: int, group=None):
     world = dist.get_world_size(group)
     rows = [b - a for a, b in (shard_range(n_total, world, r) for r in range(world))]
     return all_gather_rows(local, rows, group)
+
+
+class FusedRecordExchange:
+    """NEXT-3: the record exchange fused into the producers.  Every rank allocates
+    the full [sum(rows)][rw] gather buffer in symmetric memory (torch.distributed
+    _symmetric_memory: each rank's buffer mapped into every other rank over NVLink / NVSwitch);
+    the rank's context gets every rank's buffer address (bt_set_record_peers), so the kernels
+    that produce a record word (RANSAC finish, Eq. (2) blocks, dense reduce) store it straight
+    into row (row_lo + p) of all ranks' buffers — no all-gather kernel.  `finish()` is the one
+    synchronisation: a symmetric-memory barrier on the stream, after which this rank's buffer
+    holds every rank's records.  Needs the NCCL backend and peer access between the GPUs."""
+
+    def __init__(self, ctx, rows, rw: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if len(rows) != self.world:
+            raise ValueError(f"{len(rows)} shard sizes for world size {self.world}")
+        self.rows = list(rows)
+        self.row_lo = int(sum(self.rows[: self.rank]))
+        total = int(sum(self.rows))
+        self.buf = symm.empty((max(total, 1), rw), dtype=torch.int32, device=device)
+        pg = group if group is not None else dist.group.WORLD
+        self.handle = symm.rendezvous(self.buf, pg.group_name)
+        self.ptrs = [int(self.handle.buffer_ptrs[r]) for r in range(self.world)]
+        self.ctx = ctx
+        ctx.set_record_peers(self.ptrs, self.row_lo, max(total, 1))
+
+    def finish(self):
+        """Barrier over all ranks (stream-ordered after this rank's register_pairs): afterwards the
+        local gather buffer holds every rank's records in global row order."""
+        self.handle.barrier(channel=0)
+        return self.buf[: sum(self.rows)]
+
+    def close(self):
+        self.ctx.set_record_peers([])
+
+    @staticmethod
+    def available(group=None) -> bool:
+        try:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory  # noqa: F401
+            return dist.is_initialized() and dist.get_backend(group) == "nccl"
+        except Exception:
+            return False
