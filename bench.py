@@ -684,42 +684,76 @@ def main():
     c5 = multi_block("c5", args, bt, parallel, torch, dist, world, rank, local, dev, flush) if args.c5 else None
 
     # ---- end to end through the C ABI with pinned HOST buffers -------------------------
+    # Primary: bt_register_raw_host from the RAW per-frame inputs — depth, mask and the keypoint
+    # detector's output (2-D pixels + descriptors); normals and the keypoints' 3-D points are
+    # derived on the device (NEXT-4), so only those bytes cross PCIe.  Also the older entry
+    # bt_register_pairs_host with precomputed normal maps and 3-D keypoints (e2e_precomputed_maps).
     e2e = None
+    e2e_pre = None
     if not args.no_e2e:
-        hb = bt.FrameBatch.from_scene(sc, device="cpu", pin=True)
+        def timed(step, n):
+            for _ in range(2):
+                step()
+            e_s = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+            e_e = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            for k in range(n):
+                e_s[k].record(stream)
+                step()
+                e_e[k].record(stream)
+            torch.cuda.synchronize()
+            e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(e_s, e_e))], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+            return world * P * n / (float(e_ms.item()) / 1e3)
+
         h_pairs = torch.from_numpy(pairs).pin_memory()
         h_uid = torch.from_numpy(uids.view(np.int32)).pin_memory()
         h_pose = torch.from_numpy(poses).pin_memory()
         h_rec = torch.zeros((P, rw), dtype=torch.int32).pin_memory()
-        h2d = sum(x.numel() * x.element_size() for x in (hb.n_kp, hb.desc, hb.pts, hb.nrm, hb.depth, hb.normal,
-                                                         hb.mask, h_pairs, h_uid, h_pose))
+        small = sum(x.numel() * x.element_size() for x in (h_pairs, h_uid, h_pose))
         d2h = h_rec.numel() * 4
-        if world > 1:                                    # the exchanged records travel H2D and back
-            h2d += h_rec.numel() * 4
-            d2h += world * h_rec.numel() * 4
-        def e2e_step():
-            ctx.register_pairs(hb, sc.K, h_pose, h_pairs, h_uid, rprm, eprm, h_rec, stream=stream, host=True)
+        xh2d, xd2h = (h_rec.numel() * 4, world * h_rec.numel() * 4) if world > 1 else (0, 0)
+
+        def exchange_host():
             if world > 1:                                # records back to HBM for the exchange
                 g = parallel.all_gather_records(h_rec.to(dev, non_blocking=True), world * P)
                 g.cpu()
-        for _ in range(2):
-            e2e_step()
-        e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.e2e_steps)]
-        e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.e2e_steps)]
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        for k in range(args.e2e_steps):
-            e_s[k].record(stream)
-            e2e_step()
-            e_e[k].record(stream)
-        torch.cuda.synchronize()
-        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(e_s, e_e))], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * P * args.e2e_steps / (float(e_ms.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "api": "bt_register_pairs_host (pinned host buffers, copies + sync inside the call)"}
+        # raw inputs: the detector's output = each keypoint's projection (sub-pixel) + descriptor
+        Kc = sc.K
+        uv = np.zeros(sc.desc.shape[:2] + (2,), np.float32)
+        for f in range(sc.desc.shape[0]):
+            n_ = int(sc.n_kp[f])
+            p_ = sc.pts[f, :n_].astype(np.float64)
+            uv[f, :n_, 0] = Kc.fx * p_[:, 0] / p_[:, 2] + Kc.cx
+            uv[f, :n_, 1] = Kc.fy * p_[:, 1] / p_[:, 2] + Kc.cy
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        h_depth, h_mask, h_uv, h_desc, h_nin = pin(sc.depth), pin(sc.mask), pin(uv), pin(sc.desc), pin(sc.n_kp)
+        h2d_raw = small + sum(x.numel() * x.element_size() for x in (h_depth, h_mask, h_uv, h_desc, h_nin))
+
+        def raw_step():
+            ctx.register_raw(h_depth, h_mask, h_uv, h_desc, h_nin, sc.K, h_pose, h_pairs, h_uid, rprm, eprm, h_rec,
+                             stream=stream)
+            exchange_host()
+        v_raw = timed(raw_step, args.e2e_steps)
+        d_raw = bt.decode_records(h_rec, N_MAX)
+        e2e = {"value": v_raw, "unit": UNIT, "h2d_bytes_per_step": int(h2d_raw + xh2d), "d2h_bytes_per_step": int(d2h + xd2h),
+               "api": "bt_register_raw_host: pinned host depth, mask, 2-D keypoints + descriptors in, records out "
+                      "(normal map and keypoint lifting on the device; copies + sync inside the call)",
+               "pairs_ok": int((d_raw["status"] == 0).sum())}
+        hb = bt.FrameBatch.from_scene(sc, device="cpu", pin=True)
+        h2d_pre = small + sum(x.numel() * x.element_size() for x in (hb.n_kp, hb.desc, hb.pts, hb.nrm, hb.depth,
+                                                                   hb.normal, hb.mask))
+
+        def pre_step():
+            ctx.register_pairs(hb, sc.K, h_pose, h_pairs, h_uid, rprm, eprm, h_rec, stream=stream, host=True)
+            exchange_host()
+        v_pre = timed(pre_step, args.e2e_steps)
+        e2e_pre = {"value": v_pre, "unit": UNIT, "h2d_bytes_per_step": int(h2d_pre + xh2d),
+                   "d2h_bytes_per_step": int(d2h + xd2h),
+                   "api": "bt_register_pairs_host (precomputed normal maps and 3-D keypoints; pinned host buffers)"}
         assert np.array_equal(h_rec.numpy(), rec.cpu().numpy()), "host-buffer path disagrees with device path"
 
     cpu = None
@@ -751,7 +785,7 @@ def main():
                 else "single GPU",
                 "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
                 "roofline": roof, "kernels": kern, "kernel_ms_per_step": step_ms_by_kernel,
-                "e2e": e2e, "cpu_baseline": cpu, "next_pose_graph": graph,
+                "e2e": e2e, "e2e_precomputed_maps": e2e_pre, "cpu_baseline": cpu, "next_pose_graph": graph,
                 "next_input_prep": prep, "c4": c4, "c5": c5}
         print(json.dumps(line), flush=True)
     ctx.close()

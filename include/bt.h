@@ -16,7 +16,7 @@
  *
  * Conventions
  *  - Every buffer pointer is a CUDA DEVICE pointer owned by the caller (except in
- *    bt_register_pairs_host), 16-byte aligned.  Inputs are read-only.  The library owns only
+ *    bt_register_pairs_host / bt_register_raw_host), 16-byte aligned.  Inputs are read-only.  The library owns only
  *    the scratch reserved by bt_reserve; calls never allocate, never synchronise the host and
  *    only enqueue work on `stream` (a cudaStream_t passed as void*, NULL = legacy default
  *    stream), so they can be captured in a CUDA graph.  Outputs are valid once the stream
@@ -182,6 +182,35 @@ bt_status bt_register_pairs_host(bt_ctx *ctx, const bt_keypoints *kp, const bt_m
                                  const int32_t *pairs, const uint32_t *pair_uid, int32_t P,
                                  const bt_match_params *mprm, const bt_ransac_params *rprm,
                                  const bt_edge_params *eprm, uint32_t *records, void *stream);
+
+/* NEXT-4 end to end: the whole path from the RAW per-frame inputs in HOST memory
+   — depth, mask and the keypoint detector's output (2-D pixels + descriptors) — "only the RGB-D
+   frames and the segmentation masks" plus the keypoints of P:25; the normal map n_i(x) of Eq. (3)
+    and the keypoints' 3-D points / normals (pi_D^-1) are derived on the device.
+   Equivalent to: bt_estimate_normals(depth, jump_m) -> bt_lift_keypoints(uv, desc, n_in, maps)
+   -> bt_register_pairs on those outputs (bitwise the same records), with the host -> device
+   copies of the inputs, and the device -> host copy of the records, inside the call; it
+   synchronises `stream` before returning.  Needs bt_reserve(max_frames, width, height) (staging;
+   the raw-input staging, uv and descriptors, is allocated on the first call: BT_ENOMEM).
+   Layouts: depth [F][H][W] f32, mask [F][H][W] u8, uv [F][n_max][2] f32, desc [F][n_max][dim]
+   f32, n_in [F] (detector counts); node_pose [F], pairs [P][2], pair_uid [P], records
+   [P][bt_record_words(n_max)].  eprm may be NULL (no dense edges).  Errors: as bt_register_pairs
+   plus BT_EUNSUPPORTED (dim != 128), BT_ECAPACITY (beyond the reserved staging), BT_EINVAL
+   (NULL buffers, jump_m < 0, non-positive sizes). */
+typedef struct {
+  int32_t n_frames, width, height;
+  int32_t n_max, dim;            /* keypoint rows per frame; descriptor length (128)              */
+  float jump_m;                  /* normal estimation: neighbour depth-jump limit (SPEC: 0.05)    */
+  const float *depth;            /* [F][H][W]  metres, <= 0 invalid                               */
+  const uint8_t *mask;           /* [F][H][W]  nonzero = object                                    */
+  const float *uv;               /* [F][n_max][2] keypoint pixel coordinates                      */
+  const float *desc;             /* [F][n_max][dim] descriptors                                    */
+  const int32_t *n_in;           /* [F] detected keypoints per frame                               */
+} bt_raw_frames;
+bt_status bt_register_raw_host(bt_ctx *ctx, const bt_raw_frames *raw, const bt_intrinsics *K,
+                               const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid,
+                               int32_t P, const bt_match_params *mprm, const bt_ransac_params *rprm,
+                               const bt_edge_params *eprm, uint32_t *records, void *stream);
 
 /* NEXT-3: fused record exchange.  The per-pair records are what every rank's
    pose-graph solve needs (the pair correspondences built "in parallel on GPU", §IV-D);

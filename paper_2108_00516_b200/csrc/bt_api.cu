@@ -56,6 +56,9 @@ struct bt_ctx {
   float *st_desc = nullptr, *st_pts = nullptr, *st_nrm = nullptr, *st_depth = nullptr, *st_normal = nullptr;
   uint8_t *st_mask = nullptr;
   bt_pose *st_pose = nullptr;
+  float *st_uv = nullptr, *st_desc_in = nullptr;             // bt_register_raw_host (allocated on first use)
+  int32_t *st_nin = nullptr;
+  cudaEvent_t ev_maps = nullptr;                              // raw entry: maps + normals staged
 };
 
 namespace bt {
@@ -133,6 +136,7 @@ void free_scratch(bt_ctx *c) {
   free_dev(c->st_nkp); free_dev(c->st_pairs); free_dev(c->st_uid); free_dev(c->st_records);
   free_dev(c->st_desc); free_dev(c->st_pts); free_dev(c->st_nrm); free_dev(c->st_depth);
   free_dev(c->st_normal); free_dev(c->st_mask); free_dev(c->st_pose);
+  free_dev(c->st_uv); free_dev(c->st_desc_in); free_dev(c->st_nin);
 }
 
 #define BT_CHECK_CTX(c)                                                                  \
@@ -248,7 +252,8 @@ bt_status bt_create(bt_ctx **out, int cuda_device) {
       cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join_hi, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_maps, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return BT_ECUDA;
   }
@@ -268,6 +273,7 @@ void bt_destroy(bt_ctx *c) {
   if (c->hi) cudaStreamDestroy(c->hi);
   if (c->ev_join_hi) cudaEventDestroy(c->ev_join_hi);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_maps) cudaEventDestroy(c->ev_maps);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   free_scratch(c);
   delete c;
@@ -575,6 +581,95 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
   if (cudaStreamSynchronize(st) != cudaSuccess) return fail(c, BT_ECUDA, "bt_register_pairs_host: sync failed");
   c->launch.count = launches;
   return after_launch(c, "bt_register_pairs_host");
+}
+
+// NEXT-4 end to end: the raw per-frame inputs (depth, mask, the detector's 2-D keypoints and
+// descriptors) from host memory; normals (bt_estimate_normals) and the keypoints' 3-D points /
+// normals (bt_lift_keypoints) are derived on the device, then the whole per-pair path.
+bt_status bt_register_raw_host(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *K,
+                               const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid, int32_t P,
+                               const bt_match_params *mprm, const bt_ransac_params *rprm,
+                               const bt_edge_params *eprm, uint32_t *records, void *stream) {
+  BT_CHECK_CTX(c);
+  bt_status s;
+  if (!raw || !K || !node_pose) return fail(c, BT_EINVAL, "bt_register_raw_host: NULL raw / K / poses");
+  if (raw->dim != bt::kDim) return fail(c, BT_EUNSUPPORTED, "bt_register_raw_host: descriptor dim %d != 128", raw->dim);
+  const int F = raw->n_frames, W = raw->width, H = raw->height, n_max = raw->n_max;
+  if (F < 1 || W < 1 || H < 1 || n_max < 1 || P < 0) return fail(c, BT_EINVAL, "bt_register_raw_host: bad sizes");
+  if (!(raw->jump_m >= 0.f)) return fail(c, BT_EINVAL, "bt_register_raw_host: jump < 0");
+  if (F > c->cap_stage) return fail(c, BT_ECAPACITY, "frames %d > reserved staging %d", F, c->cap_stage);
+  if ((size_t)W * H > (size_t)c->cap_w * c->cap_h) return fail(c, BT_ECAPACITY, "maps beyond reserved staging");
+  if (n_max > c->cap_nmax) return fail(c, BT_ECAPACITY, "n_max %d > reserved %d", n_max, c->cap_nmax);
+  if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
+  if ((s = check_ransac(c, rprm)) != BT_OK) return s;
+  if (P == 0) return BT_OK;
+  if (!raw->depth || !raw->mask || !raw->uv || !raw->desc || !raw->n_in || !pairs || !pair_uid || !records)
+    return fail(c, BT_EINVAL, "bt_register_raw_host: NULL buffer");
+  bt_maps dm{};
+  dm.n_frames = F; dm.width = W; dm.height = H;
+  dm.depth = c->st_depth; dm.normal = c->st_normal; dm.mask = c->st_mask;
+  if ((s = check_maps(c, &dm, K)) != BT_OK) return s;
+  if (eprm) {
+    if ((s = check_edge(c, eprm)) != BT_OK) return s;
+    if ((s = check_dense_bytes(c, &dm, 2 * P)) != BT_OK) return s;
+  }
+  bt_keypoints dk{};
+  dk.n_frames = F; dk.n_max = n_max; dk.dim = bt::kDim;
+  dk.n_kp = c->st_nkp; dk.desc = c->st_desc; dk.pts = c->st_pts; dk.nrm = c->st_nrm;
+  if ((s = check_kp(c, &dk)) != BT_OK) return s;
+  if (!c->st_uv) {                                               // raw staging, on first use
+    const size_t FN = (size_t)c->cap_stage * c->cap_nmax;
+    if (cudaMalloc(&c->st_uv, FN * 8) != cudaSuccess || cudaMalloc(&c->st_desc_in, FN * bt::kDim * 4) != cudaSuccess ||
+        cudaMalloc(&c->st_nin, (size_t)c->cap_stage * 4) != cudaSuccess) {
+      cudaGetLastError();
+      free_dev(c->st_uv); free_dev(c->st_desc_in); free_dev(c->st_nin);
+      return fail(c, BT_ENOMEM, "bt_register_raw_host: staging cudaMalloc failed");
+    }
+  }
+  const cudaStream_t st = (cudaStream_t)stream;
+  const size_t FN = (size_t)F * n_max, FP = (size_t)F * W * H;
+  c->cached_P = -1;                                              // match lists from staged keypoints
+  const int rw = bt::rec_words(n_max);
+  c->launch.count = 0;
+  // side stream: the maps (the bulk of the bytes) and the normal map from depth; caller's stream:
+  // keypoints, pairs, poses, then (once the maps are in) the lifting, matching and RANSAC
+  cudaEventRecord(c->ev_fork, st);                               // staging buffers free
+  cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+  cudaMemcpyAsync(c->st_mask, raw->mask, FP, cudaMemcpyHostToDevice, c->side);
+  cudaMemcpyAsync(c->st_depth, raw->depth, FP * 4, cudaMemcpyHostToDevice, c->side);
+  bt::launch_normals(c->st_depth, F, W, H, *K, raw->jump_m, c->st_normal, c->side, c->launch);
+  cudaEventRecord(c->ev_maps, c->side);
+  cudaMemcpyAsync(c->st_nin, raw->n_in, (size_t)F * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_uv, raw->uv, FN * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_desc_in, raw->desc, FN * bt::kDim * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_pairs, pairs, (size_t)P * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_uid, pair_uid, (size_t)P * 4, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(c->st_pose, node_pose, (size_t)F * sizeof(bt_pose), cudaMemcpyHostToDevice, st);
+  if (eprm) {                                                    // dense edges: maps (side) + pairs / poses
+    cudaEventRecord(c->ev_join, st);
+    cudaStreamWaitEvent(c->side, c->ev_join, 0);
+    bt::launch_dense(mview(&dm), *K, c->st_pose, nullptr, c->st_pairs, 2 * P, *eprm, c->dense, nullptr, 0,
+                     c->st_records, rw, bt::rec_dense_ij(n_max), bt::rec_dense_ji(n_max), c->side, c->launch);
+  }
+  cudaStreamWaitEvent(st, c->ev_maps, 0);
+  bt::launch_lift(F, n_max, c->st_uv, c->st_desc_in, c->st_nin, mview(&dm), *K, c->st_nkp, c->st_desc, c->st_pts,
+                  c->st_nrm, st, c->launch);
+  const float ratio = mprm ? mprm->ratio : 1.f;
+  bt::launch_match(kview(&dk), c->st_pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches,
+                   c->n_matches, st, c->launch);
+  bt::launch_ransac(kview(&dk), c->st_pairs, c->st_uid, P, c->matches, c->n_matches, *rprm, c->rs,
+                    c->st_records, rw, nullptr, eprm ? c->st_pose : nullptr, eprm ? eprm->huber_m : 0.f, st,
+                    c->launch);
+  if (eprm) {
+    cudaEventRecord(c->ev_join, c->side);
+    cudaStreamWaitEvent(st, c->ev_join, 0);
+  }
+  if ((s = after_launch(c, "bt_register_raw_host")) != BT_OK) return s;
+  const int launches = c->launch.count;
+  cudaMemcpyAsync(records, c->st_records, (size_t)P * rw * 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return fail(c, BT_ECUDA, "bt_register_raw_host: sync failed");
+  c->launch.count = launches;
+  return after_launch(c, "bt_register_raw_host");
 }
 
 bt_status bt_compose_poses(bt_ctx *c, const bt_pose *a, const bt_pose *b, bt_pose *out, int32_t n, void *stream) {

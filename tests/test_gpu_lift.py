@@ -150,3 +150,50 @@ def test_raw_input_chain_depth_mask_keypoints_only(bt, torch):
         parity.assert_dense_close(r["dense_ij"], o["dense_ij"], f"raw pair {p} ij")
         parity.assert_dense_close(r["dense_ji"], o["dense_ji"], f"raw pair {p} ji")
     ctx.close()
+
+
+def test_raw_host_entry_equals_device_chain(bt, torch):
+    """bt_register_raw_host (host depth / mask / 2-D keypoints / descriptors in, records out; the
+    end-to-end entry bench.py times) equals the device chain bt_estimate_normals ->
+    bt_lift_keypoints -> bt_register_pairs on the same inputs bit for bit — with and without the
+    dense edges — and its capacity / argument errors."""
+    sc = synth.make_scene(16)
+    uv, desc, n_in = detector_output(sc, seed=13)
+    pairs = synth.all_pairs(16)
+    poses = sc.perturbed_poses(12)
+    uid = np.arange(len(pairs), dtype=np.int32) + 7
+    ctx = bt.Context(0)
+    ctx.reserve(120, 512, 4096, 16, 640, 480)
+    rprm = bt.ransac_params(4096, SEED)
+    depth = torch.from_numpy(sc.depth).cuda()
+    mask = torch.from_numpy(sc.mask).cuda()
+    normal = torch.empty((16, 480, 640, 3), dtype=torch.float32, device="cuda")
+    ctx.estimate_normals(depth, sc.K, normal, jump=0.05)           # the raw entry's jump_m default
+    maps = bt.FrameBatch(None, None, None, None, depth, normal, mask)
+    kp = gpu_lift(bt, torch, ctx, uv, desc, n_in, maps, sc.K)
+    for eprm in (bt.edge_params(), None):
+        dev_rec = torch.zeros((len(pairs), bt.record_words(512)), dtype=torch.int32, device="cuda")
+        ctx.register_pairs(kp, sc.K, torch.from_numpy(poses).cuda(), torch.from_numpy(pairs).cuda(),
+                           torch.from_numpy(uid).cuda(), rprm, eprm, dev_rec)
+        torch.cuda.synchronize()
+        host_rec = torch.zeros((len(pairs), bt.record_words(512)), dtype=torch.int32).pin_memory()
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        ctx.register_raw(pin(sc.depth), pin(sc.mask), pin(uv), pin(desc), pin(n_in), sc.K, pin(poses),
+                         pin(pairs.astype(np.int32)), pin(uid), rprm, eprm, host_rec)
+        got = host_rec.numpy()
+        want = dev_rec.cpu().numpy()
+        if eprm is None:                                          # dense / feature words are not written
+            n_ransac = 28 + 512 // 32
+            got, want = got[:, :n_ransac], want[:, :n_ransac]
+        assert np.array_equal(got, want), "raw host entry differs from the device chain"
+    # errors: dim != 128, frames beyond the staging, NULL buffers
+    host_rec = np.zeros((len(pairs), bt.record_words(512)), np.int32)
+    with pytest.raises(bt.BtError, match="EUNSUPPORTED"):
+        ctx.register_raw(sc.depth, sc.mask, uv, desc[:, :, :64].copy(), n_in, sc.K, poses, pairs.astype(np.int32),
+                         uid, rprm, None, host_rec)
+    big = np.zeros((17, 480, 640), np.float32)
+    with pytest.raises(bt.BtError, match="ECAPACITY"):
+        ctx.register_raw(big, np.zeros((17, 480, 640), np.uint8), np.zeros((17, 512, 2), np.float32),
+                         np.zeros((17, 512, 128), np.float32), np.zeros(17, np.int32), sc.K,
+                         np.zeros((17, 12), np.float32), pairs.astype(np.int32), uid, rprm, None, host_rec)
+    ctx.close()
