@@ -352,7 +352,11 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
       c->rs.fmap = &c->tmap_feat;
     }
   }
-  if (ok && dense_bytes > 0) ok = cudaMalloc(&c->dense, dense_bytes) == cudaSuccess;
+  // the dense map region (offset 0) starts zeroed and is only ever written with finite map
+  // entries: k_dense reads stale words of rejected items without a select
+  if (ok && dense_bytes > 0)
+    ok = cudaMalloc(&c->dense, dense_bytes) == cudaSuccess &&
+         cudaMemset(c->dense, 0, (size_t)mframes * width * height * 32) == cudaSuccess;
   if (ok) ok = cudaMalloc(&c->graph, bt::graph_scratch_bytes(mframes, max_pairs)) == cudaSuccess;
   if (ok && max_frames > 0) {
     const size_t FN = (size_t)max_frames * n_max, FP = (size_t)max_frames * width * height;

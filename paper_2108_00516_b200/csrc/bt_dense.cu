@@ -373,9 +373,11 @@ __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, con
   const float yz = fmaf(T[6], a.x, fmaf(T[7], a.y, fmaf(T[8], a.z, T[11])));
   const float iz = __fdividef(1.0f, yz);
   const float up = fmaf(fx * yx, iz, cx), vp = fmaf(fy * yy, iz, cy);
-  const float xu = floorf(up + 0.5f), xv = floorf(vp + 0.5f);
-  const bool ok = k < n && yz > 0.f && xu >= 0.f && xu < (float)W && xv >= 0.f && xv < (float)H;
-  const int tj = ok ? (int)xv * W + (int)xu : -1;
+  // nearest pixel (R14): floor(x + 0.5) as one F2I.FLOOR (saturating: far-off projections fail
+  // the unsigned range test like the float one)
+  const int xu = __float2int_rd(up + 0.5f), xv = __float2int_rd(vp + 0.5f);
+  const bool ok = k < n && yz > 0.f && (unsigned)xu < (unsigned)W && (unsigned)xv < (unsigned)H;
+  const int tj = ok ? xv * W + xu : -1;
   const int tt = tj < 0 ? 0 : tj;                                  // validity and map entry together
   G.in = tj >= 0;
   G.tj = tj;
@@ -400,10 +402,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];
   float4 *sP = reinterpret_cast<float4 *>(dsm);                    // p (camera, fp32), (u | v << 16)
   float4 *sN = sP + kTile;                                         // n_i (camera), n_o,i.x
-  float2 *sNo = reinterpret_cast<float2 *>(sN + kTile);            // n_o,i.y, n_o,i.z
-  float *sYh = reinterpret_cast<float *>(sNo + kTile);             // y_p = R_i^-1 (p - t_i): hi [3][kTile]
-  float *sYl = sYh + 3 * kTile;                                    //   and lo [3][kTile] (fp32 + fp32)
-  int *sCb = reinterpret_cast<int *>(sYl + 3 * kTile);            // [F + 1] chunk base per frame
+  float4 *sYh = sN + kTile;                                        // y_p = R_i^-1 (p - t_i) hi, n_o,i.y
+  float4 *sYl = sYh + kTile;                                       //   and lo (fp32 + fp32), n_o,i.z
+  int *sCb = reinterpret_cast<int *>(sYl + kTile);                // [F + 1] chunk base per frame
   int *sOff = sCb + A.mp.n_frames + 1;                             // [tiles + 1] of the current frame
   const int F = A.mp.n_frames;
   const int W = A.mp.W, H = A.mp.H, npx = W * H;
@@ -467,11 +468,11 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
                      x2 = d - t2;                                  // p - t_i
         const double y[3] = {Ri[0] * x0 + Ri[1] * x1 + Ri[2] * x2, Ri[3] * x0 + Ri[4] * x1 + Ri[5] * x2,
                              Ri[6] * x0 + Ri[7] * x1 + Ri[8] * x2};
+        float yh[3], yl[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const float yh = (float)y[c];
-          sYh[c * kTile + k] = yh;
-          sYl[c * kTile + k] = (float)(y[c] - (double)yh);
+          yh[c] = (float)y[c];
+          yl[c] = (float)(y[c] - (double)yh[c]);
         }
         const double m0 = b.x, m1 = b.y, m2 = b.z;                 // n_o,i = R_i^T n_i
         const float o0 = (float)(Rd[0] * m0 + Rd[3] * m1 + Rd[6] * m2);
@@ -479,7 +480,8 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         const float o2 = (float)(Rd[2] * m0 + Rd[5] * m1 + Rd[8] * m2);
         sP[k] = a;
         sN[k] = make_float4(b.x, b.y, b.z, o0);
-        sNo[k] = make_float2(o1, o2);
+        sYh[k] = make_float4(yh[0], yh[1], yh[2], o1);               // one 16-B entry each: two
+        sYl[k] = make_float4(yl[0], yl[1], yl[2], o2);               // LDS.128 per (entry, edge)
       }
     }
     __syncthreads();
@@ -506,9 +508,10 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
       auto consume = [&](const Gather &G, int k0) {
         const bool hit = G.in && G.vb != 0u;
         const int k = k0 < n ? k0 : 0;                             // tail: any staged entry (masked)
-        float g[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) g[c] = hit ? G.g[c] : 0.f;
+        // no select on the gathered words: a rejected item reads either pixel 0's entry or an
+        // invalid pixel's — the map region sits at a fixed offset, zeroed by bt_reserve and only
+        // ever written with finite map entries, so its words are finite and w = rho = 0 cancel them
+        const float *g = G.g;
         // q - p = R_i x_s - (p - t_i) = R_i (x_s - y_p), y_p = R_i^-1 (p - t_i) (exact algebra
         // for the fp32 R_i as given, reading R26).  x_s - y_p cancels ~0.1 m coordinates: with
         // both as hi + lo pairs, hi_s - hi_y is exact (Sterbenz) when they are close and the lo
@@ -518,17 +521,17 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         const float ls0 = __half2float(__ushort_as_half((unsigned short)(w6 & 0xffffu)));
         const float ls1 = __half2float(__ushort_as_half((unsigned short)(w6 >> 16)));
         const float ls2 = __half2float(__ushort_as_half((unsigned short)(w7 & 0xffffu)));
-        const float D0 = (g[0] - sYh[k]) + fmaf(ls0, kLoInv, -sYl[k]);
-        const float D1 = (g[1] - sYh[kTile + k]) + fmaf(ls1, kLoInv, -sYl[kTile + k]);
-        const float D2 = (g[2] - sYh[2 * kTile + k]) + fmaf(ls2, kLoInv, -sYl[2 * kTile + k]);
+        const float4 yh = sYh[k], yl = sYl[k];
+        const float D0 = (g[0] - yh.x) + fmaf(ls0, kLoInv, -yl.x);
+        const float D1 = (g[1] - yh.y) + fmaf(ls1, kLoInv, -yl.y);
+        const float D2 = (g[2] - yh.z) + fmaf(ls2, kLoInv, -yl.z);
         const float mj0 = g[3], mj1 = g[4], mj2 = g[5];
         const float dq0 = fmaf(Rf[0], D0, fmaf(Rf[1], D1, Rf[2] * D2));
         const float dq1 = fmaf(Rf[3], D0, fmaf(Rf[4], D1, Rf[5] * D2));
         const float dq2 = fmaf(Rf[6], D0, fmaf(Rf[7], D1, Rf[8] * D2));
         const float dist2 = fmaf(dq0, dq0, fmaf(dq1, dq1, dq2 * dq2));
         const float4 nc = sN[k];
-        const float2 no = sNo[k];
-        const float c = fmaf(nc.w, mj0, fmaf(no.x, mj1, no.y * mj2));
+        const float c = fmaf(nc.w, mj0, fmaf(yh.w, mj1, yl.w * mj2));
         const bool acc_ok = hit && dist2 < A.gate2f && c > A.cos_gate;
         const float n0 = nc.x, n1 = nc.y, n2 = nc.z;
         const float r = fmaf(n0, dq0, fmaf(n1, dq1, n2 * dq2));
@@ -666,6 +669,7 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   // carve the scratch
   char *p = (char *)scratch;
   const size_t tiles = a.tiles, F = mp.n_frames, npx = (size_t)mp.W * mp.H;
+  a.pmap = (MapEntry *)p;    p += align256(F * npx * sizeof(MapEntry));   // offset 0: zeroed by bt_reserve
   a.entries = (float4 *)p;   p += align256(F * tiles * kTile * 32);
   a.counts = (int32_t *)p;   p += align256(F * tiles * 4);
   a.offs = (int32_t *)p;     p += align256(F * (tiles + 1) * 4);
@@ -674,7 +678,6 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   a.tji = (float *)p;        p += align256((size_t)E * 48);
   a.elist = (int32_t *)p;    p += align256(F * E * 4);
   a.ecount = (int32_t *)p;   p += align256(F * 4);
-  a.pmap = (MapEntry *)p;    p += align256(F * npx * sizeof(MapEntry));
   a.vmap = (uint8_t *)p;     p += align256(F * npx);
   a.tlist = (int32_t *)p;    p += align256(F * tiles * 4);
   a.tcount = (int32_t *)p;
