@@ -1,5 +1,5 @@
 # Round evidence: GPU tests, full bench (with cpu_baseline + e2e), the reference arm,
-# the ncu launch list of the bench command, and one ncu --set full capture per hot kernel.
+# the ncu launch list of the bench command, and an ncu --set full capture of one step's kernels.
 # usage: bash tools/gpu_full.sh <tag>
 set -x
 cd $GRAFT_REPO_ROOT
@@ -11,5 +11,5 @@ timeout 600 python bench.py --impl reference --steps 10 --warmup 2 > gpurun_out/
 CMD="python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k "regex:k_corr_feat|k_score_tc|k_score_fix|k_ransac_hyp|k_match_ws|k_dense_mask|k_dense_prep|k_edge_setup|k_dense_scan|k_dense$|k_dense\(" -s 10 -c 22 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k "regex:^k_" -s 40 -c 22 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo done
