@@ -38,6 +38,7 @@
 #include <algorithm>
 
 #include "bt_internal.cuh"
+#include "bt_tc.cuh"
 
 
 namespace bt {
@@ -76,7 +77,7 @@ struct DenseArgs {
   float *tji;                 // [E][12] T_j T_i^-1
   int32_t *elist;             // [F][E] outgoing edges per source frame, ascending
   int32_t *ecount;            // [F]
-  float4 *entries;            // [F][tiles][kTile][2]
+  float4 *entries;            // [F][tiles][2][kTile]: per tile its points (p, u | v << 16), then its normals
   int32_t *counts;            // [F][tiles]
   int32_t *offs;              // [F][tiles + 1] exclusive scan of counts (entries of frame f before tile t)
   int32_t *nch;               // [F] chunks of kTile compacted entries (0 if the frame has no outgoing edge)
@@ -254,9 +255,9 @@ __device__ __forceinline__ void prep_tile(const DenseArgs &A, const int f, const
     if (!src[k]) continue;
     const int u = u0 + k;
     const float d = dep[k];
-    out[2 * pos] = make_float4(((float)u - A.cx) * d * A.ifx, ((float)v - A.cy) * d * A.ify, d,
-                               __int_as_float(u | (v << 16)));
-    out[2 * pos + 1] = make_float4(nr[3 * k], nr[3 * k + 1], nr[3 * k + 2], 0.f);
+    out[pos] = make_float4(((float)u - A.cx) * d * A.ifx, ((float)v - A.cy) * d * A.ify, d,
+                           __int_as_float(u | (v << 16)));
+    out[kTile + pos] = make_float4(nr[3 * k], nr[3 * k + 1], nr[3 * k + 2], 0.f);
     ++pos;
   }
   if (threadIdx.x == 0) A.counts[(size_t)f * A.tiles + t] = total;
@@ -400,15 +401,23 @@ template <bool kAssoc>
 __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char dsm[];
+  // the chunk's entries as the prep stored them per tile (points, normals: two arrays), copied
+  // in by the TMA engine; the normal's pad word is replaced by n_o,i.x once staged
   float4 *sP = reinterpret_cast<float4 *>(dsm);                    // p (camera, fp32), (u | v << 16)
   float4 *sN = sP + kTile;                                         // n_i (camera), n_o,i.x
   float4 *sYh = sN + kTile;                                        // y_p = R_i^-1 (p - t_i) hi, n_o,i.y
   float4 *sYl = sYh + kTile;                                       //   and lo (fp32 + fp32), n_o,i.z
-  int *sCb = reinterpret_cast<int *>(sYl + kTile);                // [F + 1] chunk base per frame
+  int *sCb = reinterpret_cast<int *>(sYl + kTile);             // [F + 1] chunk base per frame
   int *sOff = sCb + A.mp.n_frames + 1;                             // [tiles + 1] of the current frame
   const int F = A.mp.n_frames;
   const int W = A.mp.W, H = A.mp.H, npx = W * H;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ __align__(8) uint64_t bar_e;                           // the chunk's bulk copies landed
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_e, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t e_phase = 0;
   if (warp == 0) {                                                 // chunk bases: prefix over frames
     int carry = 0;
     for (int f0 = 0; f0 < F; f0 += 32) {
@@ -440,6 +449,25 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
     __syncthreads();
     const int n = min(kTile, sOff[A.tiles] - cl * kTile);
     const int ne = A.ecount[f];
+    // the chunk's compacted entries [g0, g0 + n) are contiguous runs of 32-B entries, one per
+    // tile they overlap: staged by the TMA engine (one bulk copy per run) while the pose's
+    // inverse is computed
+    const float4 *src = A.entries + (size_t)f * A.tiles * kTile * 2;
+    if (threadIdx.x == 0 && n > 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // previous chunk's accesses of sP / sN
+      mbar_expect_tx(&bar_e, (uint32_t)n * 32u);                 // two 16-B words per entry
+      const int g0 = cl * kTile;
+      int t = 0, hi = A.tiles;                                     // tile holding g0: sOff[t] <= g0 < sOff[t + 1]
+      while (hi - t > 1) { const int mid = (t + hi) >> 1; if (sOff[mid] <= g0) t = mid; else hi = mid; }
+      for (; t < A.tiles && sOff[t] < g0 + n; ++t) {
+        const int lo_ = max(g0, sOff[t]), hi_ = min(g0 + n, sOff[t + 1]);
+        if (hi_ > lo_) {
+          const float4 *tp = src + (size_t)t * kTile * 2 + (lo_ - sOff[t]);
+          bulk_load(sP + (lo_ - g0), tp, (uint32_t)(hi_ - lo_) * 16u, &bar_e);
+          bulk_load(sN + (lo_ - g0), tp + kTile, (uint32_t)(hi_ - lo_) * 16u, &bar_e);
+        }
+      }
+    }
     float Rf[9];                                                   // R_i as given (fp32)
     {
       const bt_pose P = A.node_pose[f];
@@ -455,13 +483,12 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         Ri[6] = c2 * idet; Ri[7] = (Rd[1] * Rd[6] - Rd[0] * Rd[7]) * idet; Ri[8] = (Rd[0] * Rd[4] - Rd[1] * Rd[3]) * idet;
       }
       const double t0 = P.t[0], t1 = P.t[1], t2 = P.t[2];
-      const float4 *src = A.entries + (size_t)f * A.tiles * kTile * 2;
+      if (n > 0) {
+        mbar_wait(&bar_e, e_phase);
+        e_phase ^= 1u;
+      }
       for (int k = threadIdx.x; k < n; k += kEdgeThreads) {
-        const int gi = cl * kTile + k;                             // compacted entry index within frame f
-        int lo = 0, hi = A.tiles;                                  // sOff[lo] <= gi < sOff[hi]
-        while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (sOff[mid] <= gi) lo = mid; else hi = mid; }
-        const float4 *e2 = src + ((size_t)lo * kTile + (gi - sOff[lo])) * 2;
-        const float4 a = e2[0], b = e2[1];
+        const float4 a = sP[k], b = sN[k];
         const int uv = __float_as_int(a.w), u = uv & 0xffff, v = uv >> 16;
         const double d = a.z;                                      // p.z = depth exactly
         const double x0 = ((double)u - A.cxd) * d * A.ifxd - t0, x1 = ((double)v - A.cyd) * d * A.ifyd - t1,
@@ -478,8 +505,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         const float o0 = (float)(Rd[0] * m0 + Rd[3] * m1 + Rd[6] * m2);
         const float o1 = (float)(Rd[1] * m0 + Rd[4] * m1 + Rd[7] * m2);
         const float o2 = (float)(Rd[2] * m0 + Rd[5] * m1 + Rd[8] * m2);
-        sP[k] = a;
-        sN[k] = make_float4(b.x, b.y, b.z, o0);
+        sN[k].w = o0;
         sYh[k] = make_float4(yh[0], yh[1], yh[2], o1);               // one 16-B entry each: two
         sYl[k] = make_float4(yl[0], yl[1], yl[2], o2);               // LDS.128 per (entry, edge)
       }
