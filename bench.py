@@ -65,8 +65,9 @@ def parse():
                     help="distinct synthetic scenes the 64 tracks cycle through (bounds CPU scene generation)")
     ap.add_argument("--c5", action="store_true", help="add the C5 stress block (n=4096, 2016 pairs; slow to generate)")
     ap.add_argument("--c5-steps", type=int, default=3)
-    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
-                    help="N > 1 record exchange: fused producer stores into symmetric memory (NEXT-3) or NCCL")
+    ap.add_argument("--exchange", default="nccl", choices=["fused", "nccl"],
+                    help="N > 1 record exchange: NCCL all_gather_into_tensor (default, measured path) or the fused "
+                         "producer stores into symmetric-memory gather buffers (NEXT-3; tested on one GPU only)")
     return ap.parse_args()
 
 
@@ -140,7 +141,7 @@ def multi_block(kind, args, bt, parallel, torch, dist, world, rank, local, dev, 
     # the exchange: NEXT-3's fused record stores into every rank's symmetric-memory gather buffer
     # (one barrier), else one NCCL all_gather_into_tensor of the records
     fused = None
-    if world > 1 and args.exchange != "nccl" and parallel.FusedRecordExchange.available():
+    if world > 1 and args.exchange == "fused" and parallel.FusedRecordExchange.available():
         try:
             fused = parallel.FusedRecordExchange(ctx, plan.rows, bt.record_words(n_max), device=dev)
         except Exception as e:                                   # no peer access: NCCL all-gather
@@ -546,6 +547,21 @@ def main():
         t = kern["k_ransac_score"]
         t["tensor_view"] = {"flop": tc_flop, "achieved_tflops": tc_flop / (t["avg_launch_ms"] * t["launches_per_step"] / 1e3) / 1e12,
                             "peak_tflops": tc_peak}
+    if "k_match_tc" in kern:
+        # the matching kernel is bound by its epilogue, not the tensor pipe (ncu: ALU pipe ~56 %,
+        # tensor ~22 %): the same launches seen as the top-3 selection's work — 4
+        # integer min/max per (row, column) element and direction (two keys per step: min, max,
+        # 3 max + 3 min-of-3 into the running top-3), on the ALU pipe's 64 lanes/clk/SM
+        t = kern["k_match_tc"]
+        sel_ops = 2 * pair_sizes * 4
+        alu_peak = SM_COUNT * 64 * mhz_max * 1e6 / 1e12          # T lane-ops/s
+        sec = t["avg_launch_ms"] * t["launches_per_step"] / 1e3
+        t["alu_view"] = {"ops": sel_ops, "achieved_tops": sel_ops / sec / 1e12, "peak_tops": alu_peak,
+                         "frac": sel_ops / sec / 1e12 / alu_peak,
+                         "frac_standalone": (sel_ops / (t["standalone_ms_per_step"] / 1e3) / 1e12 / alu_peak
+                                             if t.get("standalone_ms_per_step") else None),
+                         "work": "4 integer min/max per element per direction (2 n_a n_b per pair), "
+                                 "ALU pipe 64 lanes/clk/SM"}
     if "k_ransac_score" in kern:                       # the short-circuit lower bound, for reference
         lb = tests * FLOPS_DIST + sum_counts * FLOPS_NORMAL
         kern["k_ransac_score"]["frac_short_circuit_lower_bound"] = kern["k_ransac_score"]["frac"] * lb / (
