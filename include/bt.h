@@ -190,8 +190,8 @@ bt_status bt_register_pairs_host(bt_ctx *ctx, const bt_keypoints *kp, const bt_m
    Equivalent to: bt_estimate_normals(depth, jump_m) -> bt_lift_keypoints(uv, desc, n_in, maps)
    -> bt_register_pairs on those outputs (bitwise the same records), with the host -> device
    copies of the inputs, and the device -> host copy of the records, inside the call; it
-   synchronises `stream` before returning.  Needs bt_reserve(max_frames, width, height) (staging;
-   the raw-input staging, uv and descriptors, is allocated on the first call: BT_ENOMEM).
+   synchronises `stream` before returning.  Needs bt_reserve(max_frames, width, height) (its
+   staging holds the raw inputs).
    Layouts: depth [F][H][W] f32, mask [F][H][W] u8, uv [F][n_max][2] f32, desc [F][n_max][dim]
    f32, n_in [F] (detector counts); node_pose [F], pairs [P][2], pair_uid [P], records
    [P][bt_record_words(n_max)].  eprm may be NULL (no dense edges).  Errors: as bt_register_pairs

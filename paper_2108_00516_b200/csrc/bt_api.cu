@@ -56,7 +56,7 @@ struct bt_ctx {
   float *st_desc = nullptr, *st_pts = nullptr, *st_nrm = nullptr, *st_depth = nullptr, *st_normal = nullptr;
   uint8_t *st_mask = nullptr;
   bt_pose *st_pose = nullptr;
-  float *st_uv = nullptr, *st_desc_in = nullptr;             // bt_register_raw_host (allocated on first use)
+  float *st_uv = nullptr, *st_desc_in = nullptr;             // bt_register_raw_host staging
   int32_t *st_nin = nullptr;
   cudaEvent_t ev_maps = nullptr;                              // raw entry: maps + normals staged
 };
@@ -364,7 +364,9 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
          cudaMalloc(&c->st_desc, FN * 128 * 4) == cudaSuccess && cudaMalloc(&c->st_pts, FN * 12) == cudaSuccess &&
          cudaMalloc(&c->st_nrm, FN * 12) == cudaSuccess && cudaMalloc(&c->st_pose, (size_t)max_frames * sizeof(bt_pose)) == cudaSuccess &&
          cudaMalloc(&c->st_pairs, (size_t)max_pairs * 8) == cudaSuccess && cudaMalloc(&c->st_uid, (size_t)max_pairs * 4) == cudaSuccess &&
-         cudaMalloc(&c->st_records, (size_t)max_pairs * bt::rec_words(n_max) * 4) == cudaSuccess;
+         cudaMalloc(&c->st_records, (size_t)max_pairs * bt::rec_words(n_max) * 4) == cudaSuccess &&
+         cudaMalloc(&c->st_uv, FN * 8) == cudaSuccess && cudaMalloc(&c->st_desc_in, FN * bt::kDim * 4) == cudaSuccess &&
+         cudaMalloc(&c->st_nin, (size_t)max_frames * 4) == cudaSuccess;
     if (ok && FP > 0)
       ok = cudaMalloc(&c->st_depth, FP * 4) == cudaSuccess && cudaMalloc(&c->st_normal, FP * 12) == cudaSuccess &&
            cudaMalloc(&c->st_mask, FP) == cudaSuccess;
@@ -621,15 +623,7 @@ bt_status bt_register_raw_host(bt_ctx *c, const bt_raw_frames *raw, const bt_int
   dk.n_frames = F; dk.n_max = n_max; dk.dim = bt::kDim;
   dk.n_kp = c->st_nkp; dk.desc = c->st_desc; dk.pts = c->st_pts; dk.nrm = c->st_nrm;
   if ((s = check_kp(c, &dk)) != BT_OK) return s;
-  if (!c->st_uv) {                                               // raw staging, on first use
-    const size_t FN = (size_t)c->cap_stage * c->cap_nmax;
-    if (cudaMalloc(&c->st_uv, FN * 8) != cudaSuccess || cudaMalloc(&c->st_desc_in, FN * bt::kDim * 4) != cudaSuccess ||
-        cudaMalloc(&c->st_nin, (size_t)c->cap_stage * 4) != cudaSuccess) {
-      cudaGetLastError();
-      free_dev(c->st_uv); free_dev(c->st_desc_in); free_dev(c->st_nin);
-      return fail(c, BT_ENOMEM, "bt_register_raw_host: staging cudaMalloc failed");
-    }
-  }
+  if (!c->st_uv || !c->st_depth) return fail(c, BT_ECAPACITY, "bt_register_raw_host: no staging reserved");
   const cudaStream_t st = (cudaStream_t)stream;
   const size_t FN = (size_t)F * n_max, FP = (size_t)F * W * H;
   c->cached_P = -1;                                              // match lists from staged keypoints
