@@ -61,6 +61,7 @@ enum KernelId {
 // matching scratch (carved from one allocation; see match_scratch_bytes)
 struct MatchScratch {
   __half *desc16;          // [F][n_pad][128] unit descriptors (TMA source)
+  __half *desc16lo;        // [F][n_pad][128] their fp16 remainders (a / M_f - hi): level-2 certification
   float *norm;             // [F][n_pad]
   unsigned *maxnorm;       // [F] float bits of max |a|
   uint4 *work;             // [2 queues][work_cap] undecided rows: (dir | i << 1, p, k1, k2);
@@ -71,6 +72,8 @@ struct MatchScratch {
   uint8_t *ratio_ok;       // [P][n_max]
   int32_t *fs_rows;        // [2 dirs][P][n_pad / 128 tiles][128] undecided rows for the batched full scan
   int32_t *fs_count;       // [2][P][tiles]
+  int32_t *l3_rows;        // [2][P][n_pad] rows left uncertified by the level-2 pass (k_fullscan's input)
+  int32_t *l3_count;       // [2][P] (0 between calls: k_mutual resets it)
 };
 struct Launch {
   int count = 0;

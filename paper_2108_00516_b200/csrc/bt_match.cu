@@ -49,6 +49,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 
 namespace bt {
@@ -132,11 +133,19 @@ k_desc_half(KpView kp, MatchScratch S, int n_pad) {
   for (int q = 0; q < kPrepPerWarp; ++q) {
     const int i = i0 + q;
     if (i < n_pad) {
-      __half2 h01 = __floats2half2_rn(a[q].x * inv, a[q].y * inv), h23 = __floats2half2_rn(a[q].z * inv, a[q].w * inv);
+      const float x0 = a[q].x * inv, x1 = a[q].y * inv, x2 = a[q].z * inv, x3 = a[q].w * inv;
+      __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
       uint2 packed;
       packed.x = *reinterpret_cast<uint32_t *>(&h01);
       packed.y = *reinterpret_cast<uint32_t *>(&h23);
       reinterpret_cast<uint2 *>(S.desc16 + ((size_t)f * n_pad + i) * kDim)[lane] = packed;
+      if (S.desc16lo) {                                            // the remainders (exact in fp32)
+        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+        __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+        packed.x = *reinterpret_cast<uint32_t *>(&l01);
+        packed.y = *reinterpret_cast<uint32_t *>(&l23);
+        reinterpret_cast<uint2 *>(S.desc16lo + ((size_t)f * n_pad + i) * kDim)[lane] = packed;
+      }
     }
   }
 }
@@ -631,6 +640,213 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_rescore(RescoreArgs A) 
   }
 }
 
+// ---------------------------------------------------------------- level-2 certification
+// The rows k_match_ws could not certify (fp16 operands: |d_hat - d| <= 2.2e-3 |a| M_b) are
+// re-ranked by warp-level tensor-core MMAs (mma.sync m16n8k16, fp32 accumulation) on hi + lo
+// fp16 operands — S'' = A_hi B_hi + A_hi B_lo + A_lo B_hi of the frame-max-scaled descriptors,
+// which leaves out only A_lo B_lo (<= 2^-22 |a||b| / M_a M_b) — over ALL references, with a
+// certificate 9x tighter: |S''_hat - S''| <= 2^-13 |a||b| / (M_a M_b) (the dropped term, the hi /
+// lo representation, and the fp32 accumulation of 24 MMA steps, with margin), so
+// |d_hat - d| <= 2.5e-4 |a| M_b + 1e-6 (|a|^2 + M_b^2) + 3e-6 M_a M_b.  A row is then decided (its
+// best certified), queued for the exact top-2 rescoring (k_rescore), or left for the exact full
+// scan (k_fullscan, the l3 list).  Keys: the ranked value mapped into [1, 2) (one FFMA with a
+// per-column constant, as k_match_ws) and packed as its top 20 mantissa bits above the 12-bit
+// column index (n_pad <= 4096): the 3 truncated bits are in the certificate.
+// CTA = 4 warps x 16 rows of one (pair, direction); references in chunks of 128 (hi + lo staged
+// with cp.async, rows padded to 136 halves: conflict-free ldmatrix).
+constexpr int kL2Rows = 64, kL2Refs = 128, kL2Pitch = 136;      // halves per staged row
+constexpr size_t kL2Smem = (size_t)(2 * kL2Rows + 2 * kL2Refs) * kL2Pitch * 2 + kL2Refs * 8;
+
+struct L2Args {
+  KpView kp;
+  const int32_t *pairs;
+  MatchScratch S;
+  int P, n_pad;
+  int certify;                                 // 0: ratio test / forced fallback — forward every row
+};
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void *p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], const void *p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+__global__ void __launch_bounds__(128) k_match_l2(L2Args A) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint8_t l2sm[];
+  __half *sAh = reinterpret_cast<__half *>(l2sm);                 // [64][136]
+  __half *sAl = sAh + kL2Rows * kL2Pitch;
+  __half *sBh = sAl + kL2Rows * kL2Pitch;                          // [128][136]
+  __half *sBl = sBh + kL2Refs * kL2Pitch;
+  float2 *sC = reinterpret_cast<float2 *>(sBl + kL2Refs * kL2Pitch);   // [128] (column constant, j)
+  __shared__ int toff[65];
+  __shared__ int grow[kL2Rows];
+  const int g = blockIdx.x, p = blockIdx.y, dir = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_tiles = A.n_pad / 128;
+  const int tile0 = (dir * A.P + p) * n_tiles;
+  if (tid == 0) {                                                  // the (pair, direction)'s rows, in tile order
+    int acc = 0;
+    for (int t = 0; t < n_tiles; ++t) { toff[t] = acc; acc += A.S.fs_count[tile0 + t]; }
+    toff[n_tiles] = acc;
+  }
+  __syncthreads();
+  const int u = toff[n_tiles];
+  const int g0 = g * kL2Rows;
+  if (g0 >= u) return;                                             // block-uniform
+  const int gn = min(kL2Rows, u - g0);
+  if (tid < kL2Rows) {
+    int r = -1;
+    if (tid < gn) {
+      const int gi = g0 + tid;
+      int t = 0;
+      while (toff[t + 1] <= gi) ++t;
+      r = A.S.fs_rows[(size_t)(tile0 + t) * 128 + (gi - toff[t])];
+    }
+    grow[tid] = r;
+  }
+  __syncthreads();
+  const int lq = (dir * A.P + p);
+  int32_t *l3 = A.S.l3_rows + (size_t)lq * A.n_pad;
+  if (!A.certify) {                                                // forward the rows to the exact scan
+    if (tid < gn) l3[atomicAdd(A.S.l3_count + lq, 1)] = grow[tid];
+    return;
+  }
+  const int fq = A.pairs[2 * p + dir], fr = A.pairs[2 * p + 1 - dir];
+  const int nr = min(A.kp.n_kp[fr], A.kp.n_max);
+  const int n_pad = A.n_pad;
+  const __half *Qh = A.S.desc16 + (size_t)fq * n_pad * kDim, *Ql = A.S.desc16lo + (size_t)fq * n_pad * kDim;
+  const __half *Rh = A.S.desc16 + (size_t)fr * n_pad * kDim, *Rl = A.S.desc16lo + (size_t)fr * n_pad * kDim;
+  // A rows: 64 x (256 B hi + 256 B lo) in 16-B pieces
+  for (int x = tid; x < kL2Rows * 16; x += 128) {
+    const int r = x >> 4, c = x & 15;
+    const int row = grow[r] < 0 ? 0 : grow[r];                    // padded rows: any row (ignored)
+    cp_async16(sAh + r * kL2Pitch + c * 8, Qh + (size_t)row * kDim + c * 8);
+    cp_async16(sAl + r * kL2Pitch + c * 8, Ql + (size_t)row * kDim + c * 8);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  const float ma = frame_scale(A.S.maxnorm[fq]), mb = frame_scale(A.S.maxnorm[fr]);
+  const float pp = ma * mb;
+  const float cinv = 1.0f / (mb * mb + 4.02f * pp);
+  const float kscale = -2.f * pp * cinv;
+  // per thread: rows r0 = 16 warp + lane / 4 and r0 + 8, columns 2 (lane % 4) + {0, 1} of each n-tile
+  unsigned t0[3] = {kNone, kNone, kNone}, t1[3] = {kNone, kNone, kNone};
+  auto ins = [](unsigned (&t)[3], unsigned k) {
+    const unsigned n3 = min(t[2], max(t[1], k)), n2 = min(t[1], max(t[0], k));
+    t[0] = min(t[0], k); t[1] = n2; t[2] = n3;
+  };
+  for (int jc = 0; jc < nr; jc += kL2Refs) {
+    __syncthreads();                                               // the previous chunk consumed
+    for (int x = tid; x < kL2Refs * 16; x += 128) {
+      const int j = x >> 4, c = x & 15;
+      const int jj = min(jc + j, n_pad - 1);                       // rows past n_r: zero-padded rows
+      cp_async16(sBh + j * kL2Pitch + c * 8, Rh + (size_t)jj * kDim + c * 8);
+      cp_async16(sBl + j * kL2Pitch + c * 8, Rl + (size_t)jj * kDim + c * 8);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    {                                                              // column constants (IMAD-free: value in [1, 2))
+      const int j = jc + tid;
+      const float nb = j < nr ? A.S.norm[(size_t)fr * n_pad + j] : 0.f;
+      sC[tid] = make_float2(j < nr ? __fmaf_rn(cinv, __fmaf_rn(nb, nb, 2.01f * pp), 1.0f)
+                                   : __uint_as_float(0x3FFFFFFFu), __uint_as_float((unsigned)j));
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    float acc[16][4];
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[nt][k] = 0.f;
+#pragma unroll 2
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t ah[4], al[4];
+      // A fragment (16 x 16 at rows 16 warp, k 16 kk): ldmatrix x4, lane -> row (lane & 15), k-half (lane >> 4)
+      const int ar = 16 * warp + (lane & 15), ak = 16 * kk + 8 * (lane >> 4);
+      ldsm_x4(ah, sAh + ar * kL2Pitch + ak);
+      ldsm_x4(al, sAl + ar * kL2Pitch + ak);
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+        uint32_t bh[2], bl[2];
+        // B fragment (16 k x 8 n, "col"): the 8 reference rows 8 nt.., k halves by lanes 0-7 / 8-15
+        const int br = 8 * nt + (lane & 7), bk = 16 * kk + 8 * ((lane >> 3) & 1);
+        ldsm_x2(bh, sBh + br * kL2Pitch + bk);
+        ldsm_x2(bl, sBl + br * kL2Pitch + bk);
+        mma16816(acc[nt], ah, bh);
+        mma16816(acc[nt], ah, bl);
+        mma16816(acc[nt], al, bh);
+      }
+    }
+    // ranking: d'' mapped into [1, 2), key = top 20 mantissa bits | 12-bit column
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float2 cc = sC[8 * nt + 2 * (lane & 3) + e];
+        const float v0 = __fmaf_rn(kscale, acc[nt][e], cc.x), v1 = __fmaf_rn(kscale, acc[nt][2 + e], cc.x);
+        const unsigned k0 = ((__float_as_uint(v0) << 9) & 0xFFFFF000u) | __float_as_uint(cc.y);
+        const unsigned k1 = ((__float_as_uint(v1) << 9) & 0xFFFFF000u) | __float_as_uint(cc.y);
+        ins(t0, k0);
+        ins(t1, k1);
+      }
+    }
+  }
+  // merge the 4 lanes of each row (xor 1, 2), then certify
+#pragma unroll
+  for (int o = 1; o <= 2; o <<= 1) {
+    unsigned x0[3], x1[3];                                         // the partner's lists, read first
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      x0[q] = __shfl_xor_sync(0xffffffffu, t0[q], o);
+      x1[q] = __shfl_xor_sync(0xffffffffu, t1[q], o);
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {                                  // columns are disjoint across lanes
+      ins(t0, x0[q]);
+      ins(t1, x1[q]);
+    }
+  }
+  if ((lane & 3) == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = 16 * warp + (lane >> 2) + 8 * h;
+      if (r >= gn) continue;
+      const int i = grow[r];
+      const unsigned *t = h ? t1 : t0;
+      const float qn = A.S.norm[(size_t)fq * n_pad + i];
+      // key units: 2^-20 of the [1, 2) value = 2^-20 / c in d; each key within 3 units of 1 + c d''
+      const float uk = ldexpf(mb * mb + 4.02f * pp, -20);
+      const float eps2 = 2.f * (2.5e-4f * qn * mb + 1e-6f * (qn * qn + mb * mb) + 3e-6f * pp) + 8.f * uk;
+      int level = 0;
+      if (t[0] != kNone) {
+        if (t[1] == kNone) level = 1;
+        else if ((float)((t[1] >> 12) - (t[0] >> 12)) * uk > eps2) level = 1;
+        else if (t[2] == kNone || (float)((t[2] >> 12) - (t[0] >> 12)) * uk > eps2) level = 2;
+      }
+      const size_t o_nn = (size_t)p * A.kp.n_max + i;
+      if (level == 1) {
+        (dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o_nn] = (int32_t)(t[0] & 0xFFFu);
+        if (dir == 0) A.S.ratio_ok[o_nn] = 1;
+      } else if (level == 2) {                                     // the exact top-2 (k_rescore, queue 0)
+        const unsigned slot = atomicAdd(A.S.work_count, 1u);
+        A.S.work[slot] = make_uint4((unsigned)dir | ((unsigned)i << 1), (unsigned)p, t[0] & 0xFFFu, t[1] & 0xFFFu);
+      } else {
+        l3[atomicAdd(A.S.l3_count + lq, 1)] = i;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- exact full scans, batched
 // One CTA per (group of 32, pair, direction): the undecided rows of a (pair, direction) — the
 // row tiles' lists of k_match_tc concatenated in order — in groups of 32 against all
@@ -664,28 +880,17 @@ __global__ void __launch_bounds__(256) k_fullscan(FullScanArgs A) {
   extern __shared__ __align__(16) float fsm[];
   float *sA = fsm;                                   // [32][128] rows (broadcast reads)
   float *sB = fsm + kFsRows * kDim;                  // [128][kFsPitch] k-major reference chunk
-  __shared__ int toff[65];                           // prefix of the tiles' list lengths (n_max <= 8192)
   __shared__ int grow[kFsRows];                      // this group's rows
   const int g = blockIdx.x, p = blockIdx.y, dir = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n_tiles = A.n_pad / 128;
-  const int tile0 = (dir * A.P + p) * n_tiles;
-  if (threadIdx.x == 0) {                            // the (pair, direction)'s rows, all tiles, in order
-    int acc = 0;
-    for (int t = 0; t < n_tiles; ++t) { toff[t] = acc; acc += A.S.fs_count[tile0 + t]; }
-    toff[n_tiles] = acc;
-  }
-  __syncthreads();
-  const int u = toff[n_tiles];
+  // the (pair, direction)'s rows the level-2 pass left uncertified (k_match_l2)
+  const int u = A.S.l3_count[dir * A.P + p];
+  const int32_t *l3 = A.S.l3_rows + (size_t)(dir * A.P + p) * A.n_pad;
   const int fq = A.pairs[2 * p + dir], fr = A.pairs[2 * p + 1 - dir];
   const int nr = min(A.kp.n_kp[fr], A.kp.n_max);
   const float *Q = A.kp.desc + (size_t)fq * A.kp.n_max * kDim;
   const float *R = A.kp.desc + (size_t)fr * A.kp.n_max * kDim;
-  auto row_of = [&](int gi) {                        // gi-th undecided row of (p, dir)
-    int t = 0;
-    while (toff[t + 1] <= gi) ++t;
-    return A.S.fs_rows[(size_t)(tile0 + t) * 128 + (gi - toff[t])];
-  };
+  auto row_of = [&](int gi) { return l3[gi]; };     // gi-th undecided row of (p, dir)
   if (u <= kFsSmall || nr < kFsBatchRefs) {
     // few rows (or few references in this pair): one row per CTA, the 8 warps split the
     // references and read them straight from L2 (exact_scan — the same distances, bit for bit)
@@ -818,6 +1023,7 @@ k_mutual(KpView kp, const int32_t *__restrict__ pairs, const int32_t *__restrict
     for (int f = threadIdx.x; f < kp.n_frames; f += blockDim.x) S.maxnorm[f] = 0u;
     if (threadIdx.x < 2) S.work_count[threadIdx.x] = 0u;
   }
+  if (S.l3_count && threadIdx.x < 2) S.l3_count[threadIdx.x * gridDim.x + p] = 0;   // k_fullscan is done
   const int fa = pairs[2 * p], fb = pairs[2 * p + 1];
   const int na = min(kp.n_kp[fa], kp.n_max), nb = min(kp.n_kp[fb], kp.n_max);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -866,7 +1072,8 @@ size_t match_scratch_bytes(int max_frames, int max_pairs, int n_max) {
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   (void)rt;
   return al(F * np * kDim * 2) + al(F * np * 4) + al(F * 4) + al(2 * 2 * P * n_max * 16) + al(16) +
-         al(P * n_max * 4) * 2 + al(P * n_max) + al(2 * P * np * 4) + al(2 * P * (np / 128) * 4);
+         al(P * n_max * 4) * 2 + al(P * n_max) + al(2 * P * np * 4) + al(2 * P * (np / 128) * 4) +
+         (n_max >= kFsBatchRefs ? al(F * np * kDim * 2) + al(2 * P * np * 4) + al(2 * P * 4) : 0);
 }
 
 MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_max) {
@@ -885,7 +1092,14 @@ MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_m
   S.nn_ba = (int32_t *)c;        c += al(P * n_max * 4);
   S.ratio_ok = (uint8_t *)c;     c += al(P * n_max);
   S.fs_rows = (int32_t *)c;      c += al(2 * P * np * 4);
-  S.fs_count = (int32_t *)c;
+  S.fs_count = (int32_t *)c;     c += al(2 * P * (np / 128) * 4);
+  S.desc16lo = nullptr; S.l3_rows = nullptr; S.l3_count = nullptr;
+  if (n_max >= kFsBatchRefs) {                                   // the level-2 pass (batched full scans only)
+    S.desc16lo = (__half *)c;    c += al(F * np * kDim * 2);
+    S.l3_rows = (int32_t *)c;    c += al(2 * P * np * 4);
+    S.l3_count = (int32_t *)c;
+    cudaMemset(S.l3_count, 0, 2 * P * 4);
+  }
   // maxnorm and the queue counters are zero between calls: zeroed here, re-zeroed by k_mutual
   cudaMemset(S.maxnorm, 0, F * 4);
   cudaMemset(S.work_count, 0, 16);
@@ -927,6 +1141,13 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   L.begin(K_RESOLVE, s);
   RescoreArgs ra{kp, pairs, S, ibits, ratio2};
   if (fs_batched) {
+    // level 2: tensor-core hi + lo re-ranking of the rows k_match_ws left undecided; what it
+    // cannot certify goes to the exact batched scan
+    L2Args la{kp, pairs, S, P, n_pad, (!force_fallback && ratio2 >= 1.f && n_pad <= 4096) ? 1 : 0};
+    smem_optin((const void *)k_match_l2, kL2Smem);
+    launch_pdl(k_match_l2, dim3(n_pad / kL2Rows, P, 2), 128, kL2Smem, s, la);
+    L.end(K_RESOLVE, s);
+    L.begin(K_RESOLVE, s);
     FullScanArgs fa{kp, pairs, S, P, n_pad, ibits, ratio2};
     smem_optin((const void *)k_fullscan, kFsSmem);
     launch_pdl(k_fullscan, dim3(n_pad / kFsRows, P, 2), 256, kFsSmem, s, fa);
@@ -940,6 +1161,13 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
     cudaStreamSynchronize(s);
     cudaMemcpy(c, S.work_count, 8, cudaMemcpyDeviceToHost);
     fprintf(stderr, "bt matching: %u rows top-2 rescored, %u rows full-scanned\n", c[0], c[1]);
+    if (fs_batched && S.l3_count) {
+      std::vector<int32_t> l3(2 * P);
+      cudaMemcpy(l3.data(), S.l3_count, 2 * P * 4, cudaMemcpyDeviceToHost);
+      long long t = 0;
+      for (int v : l3) t += v;
+      fprintf(stderr, "bt matching: %lld rows left to the exact batched scan after the level-2 pass\n", t);
+    }
   }
   L.begin(K_MUTUAL, s);
   launch_pdl(k_mutual, P, 512, 0, s, kp, pairs, (const int32_t *)S.nn_ab, (const int32_t *)S.nn_ba,
