@@ -703,9 +703,10 @@ __global__ void __launch_bounds__(128) k_match_l2(L2Args A) {
   }
   __syncthreads();
   const int u = toff[n_tiles];
-  const int g0 = g * kL2Rows;
-  if (g0 >= u) return;                                             // block-uniform
+  for (int gg = g; gg * kL2Rows < u; gg += gridDim.x) {             // groups of 64 rows, block-uniform
+  const int g0 = gg * kL2Rows;
   const int gn = min(kL2Rows, u - g0);
+  __syncthreads();                                                 // the previous group's smem reads done
   if (tid < kL2Rows) {
     int r = -1;
     if (tid < gn) {
@@ -721,7 +722,7 @@ __global__ void __launch_bounds__(128) k_match_l2(L2Args A) {
   int32_t *l3 = A.S.l3_rows + (size_t)lq * A.n_pad;
   if (!A.certify) {                                                // forward the rows to the exact scan
     if (tid < gn) l3[atomicAdd(A.S.l3_count + lq, 1)] = grow[tid];
-    return;
+    continue;
   }
   const int fq = A.pairs[2 * p + dir], fr = A.pairs[2 * p + 1 - dir];
   const int nr = min(A.kp.n_kp[fr], A.kp.n_max);
@@ -820,7 +821,7 @@ __global__ void __launch_bounds__(128) k_match_l2(L2Args A) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int r = 16 * warp + (lane >> 2) + 8 * h;
-      if (r >= gn) continue;
+      if (r >= gn) continue;                                       // (the row loop)
       const int i = grow[r];
       const unsigned *t = h ? t1 : t0;
       const float qn = A.S.norm[(size_t)fq * n_pad + i];
@@ -844,6 +845,7 @@ __global__ void __launch_bounds__(128) k_match_l2(L2Args A) {
         l3[atomicAdd(A.S.l3_count + lq, 1)] = i;
       }
     }
+  }
   }
 }
 
@@ -922,9 +924,10 @@ __global__ void __launch_bounds__(256) k_fullscan(FullScanArgs A) {
     }
     return;
   }
-  const int g0 = g * kFsRows;
-  if (g0 >= u) return;                               // block-uniform
+  for (int gg = g; gg * kFsRows < u; gg += gridDim.x) {             // groups of 32 rows, block-uniform
+  const int g0 = gg * kFsRows;
   const int gn = min(kFsRows, u - g0);
+  __syncthreads();                                   // the previous group's grow / sA reads done
   if (threadIdx.x < kFsRows) grow[threadIdx.x] = threadIdx.x < gn ? row_of(g0 + threadIdx.x) : -1;
   __syncthreads();                                   // grow visible to every thread
   const bool active = 4 * warp < gn;                 // warp-uniform: this warp has rows
@@ -1008,6 +1011,7 @@ __global__ void __launch_bounds__(256) k_fullscan(FullScanArgs A) {
         if (dir == 0) A.S.ratio_ok[o] = (A.ratio2 >= 1.f) || (nr < 2) || (b1[q] < A.ratio2 * b2[q]);
       }
     }
+  }
   }
 }
 
@@ -1145,12 +1149,12 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
     // cannot certify goes to the exact batched scan
     L2Args la{kp, pairs, S, P, n_pad, (!force_fallback && ratio2 >= 1.f && n_pad <= 4096) ? 1 : 0};
     smem_optin((const void *)k_match_l2, kL2Smem);
-    launch_pdl(k_match_l2, dim3(n_pad / kL2Rows, P, 2), 128, kL2Smem, s, la);
+    launch_pdl(k_match_l2, dim3(std::min(n_pad / kL2Rows, 4), P, 2), 128, kL2Smem, s, la);
     L.end(K_RESOLVE, s);
     L.begin(K_RESOLVE, s);
     FullScanArgs fa{kp, pairs, S, P, n_pad, ibits, ratio2};
     smem_optin((const void *)k_fullscan, kFsSmem);
-    launch_pdl(k_fullscan, dim3(n_pad / kFsRows, P, 2), 256, kFsSmem, s, fa);
+    launch_pdl(k_fullscan, dim3(std::min(n_pad / kFsRows, 4), P, 2), 256, kFsSmem, s, fa);
     L.end(K_RESOLVE, s);
     L.begin(K_RESOLVE, s);
   }
