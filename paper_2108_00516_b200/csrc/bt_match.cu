@@ -158,7 +158,10 @@ struct TcArgs {
   int n_pad, ibits, P, force_fallback;
   float ratio2;
   int fs_batched;                              // undecided rows -> per-tile lists (k_fullscan), else queue 1
-  unsigned kmul;                               // 512 (IMAD-key variant): a runtime operand keeps it an IMAD
+  unsigned kmul;                               // 2^kshift (IMAD keys): a runtime operand keeps it an IMAD
+  int kshift;                                  // IMAD keys: index bits, max(ibits, 9)
+  float kwin;                                  // IMAD keys: value window width 2^-(kshift - 9)
+  unsigned kpad;                               // IMAD keys: largest float below 1 + kwin (padded columns)
 };
 
 constexpr int kN = 128;                       // B columns per MMA chunk (N); B and TMEM double-buffered
@@ -184,26 +187,29 @@ __device__ __forceinline__ int certify(unsigned k1, unsigned k2, unsigned k3, fl
   return 0;
 }
 
-// IMAD keys (n_pad <= 512): the ranked value is mapped into [1, 2) — v = 1 + c d'' with
-// c = 1 / (M_b^2 + 4.02 M_a M_b), still ONE FFMA per element (column constant 1 + c(|b|^2 +
-// 2.01 M_a M_b), scale -2 M_a M_b c) — so its float bits are 0x3F8xxxxx with a fixed exponent,
-// and bits * 512 + j (mod 2^32; the exponent bits shift out) is the 23-bit mantissa followed by
-// the 9-bit column index: the key is ONE IMAD on the FMA pipe instead of a LOP3 on the ALU
-// pipe (the epilogue is ALU-bound: min / max of the top-3), and no value bit is truncated.
+// IMAD keys (s = max(index bits, 9) <= 16): the ranked value is mapped into the window
+// [1, 1 + w), w = 2^-(s - 9) — v = 1 + c d'' with c = w / (M_b^2 + 4.02 M_a M_b), still ONE FFMA
+// per element (column constant 1 + c(|b|^2 + 2.01 M_a M_b), scale -2 M_a M_b c) — so its float
+// bits are 0x3F8xxxxx with a fixed exponent and the top s - 9 mantissa bits zero, and
+// bits * 2^s + j (mod 2^32; exponent and zero bits shift out) is the remaining 32 - s mantissa
+// bits followed by the s-bit column index: the key is ONE IMAD on the FMA pipe instead of a
+// LOP3 on the ALU pipe (the epilogue is ALU-bound: min / max of the top-3), and no value bit
+// is truncated (the value's resolution is 2^-23 / c = (M_b^2 + 4.02 M_a M_b) 2^(s - 32)).
 // d'' in [0.008 M_a M_b, M_b^2 + 4.012 M_a M_b] (S'' <= 1 + 1e-3) keeps v strictly inside
-// [1, 2 - 1.6e-3); a padded column's constant is the largest float below 2 (key 0xFFFFFE00 | j).
-// Certificate in key units u = 2^-23 / c: each key's value is within 2.5 u of 1 + c d'' (the
-// FFMA, the constant's and the scale's fp32 rounding), so 8 u covers a difference of two.
+// [1, 1 + w (1 - 1.6e-3)); a padded column's constant is the largest float below 1 + w (key
+// 0xFFFFFFFF << s | j).  Certificate in key units u = 2^-23 / c: each key's value is within
+// 2.5 u of 1 + c d'' (the FFMA, the constant's and the scale's fp32 rounding; all values lie in
+// [1, 2) where the ulp is 2^-23), so 8 u covers a difference of two.
 __device__ __forceinline__ int certify_imad(unsigned k1, unsigned k2, unsigned k3, float qn, float mr, float pp,
-                                            float ma, float mb) {
+                                            float ma, float mb, int s) {
   if (k1 == kNone) return 0;
   if (k2 == kNone) return 1;
-  const float u = ldexpf(mb * mb + 4.02f * ma * mb, -23);
+  const float u = ldexpf(mb * mb + 4.02f * ma * mb, s - 32);
   const float eps2 = 2.f * (2.2e-3f * qn * mr + 1e-6f * (qn * qn + mr * mr) + 3e-6f * pp) + 8.f * u;
-  const float d21 = (float)((k2 >> 9) - (k1 >> 9)) * u;
+  const float d21 = (float)((k2 >> s) - (k1 >> s)) * u;
   if (d21 > eps2) return 1;
   if (k3 == kNone) return 2;
-  const float d31 = (float)((k3 >> 9) - (k1 >> 9)) * u;
+  const float d31 = (float)((k3 >> s) - (k1 >> s)) * u;
   if (d31 > eps2) return 2;
   return 0;
 }
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
       if (!I.skip) {
         const float ma_ = frame_scale(A.S.maxnorm[I.fa]), mb_ = frame_scale(A.S.maxnorm[I.fb]);
         const float coff = 2.01f * ma_ * mb_;
-        const float cinv = kImad ? 1.0f / (mb_ * mb_ + 4.02f * ma_ * mb_) : 0.f;
+        const float cinv = kImad ? A.kwin / (mb_ * mb_ + 4.02f * ma_ * mb_) : 0.f;
         for (int c = 0; c < I.nchunks; ++c, ++g) {
           const int b = g & 1;
           if (!nv_ok) {
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
             // +inf (no per-element bound check in the epilogue)
             if (kImad)
               cconst[b * kN + jj] = make_float2(j < I.nb ? __fmaf_rn(cinv, __fmaf_rn(nv[q], nv[q], coff), 1.0f)
-                                                         : __uint_as_float(0x3FFFFFFFu),
+                                                         : __uint_as_float(A.kpad),
                                                 __uint_as_float((unsigned)j));
             else
               cconst[b * kN + jj] = make_float2(j < I.nb ? __fmaf_rn(nv[q], nv[q], coff) : CUDART_INF_F,
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
       // S'' = (a / P_a).(b / P_b): d' = |b|^2 - 2 P_a P_b S''
       const float fsa = frame_scale(ma_nx), fsb = frame_scale(mb_nx);
       const float pp = fsa * fsb;
-      const float kscale = kImad ? -2.f * pp * (1.0f / (fsb * fsb + 4.02f * pp)) : -2.f * pp;
+      const float kscale = kImad ? -2.f * pp * (A.kwin / (fsb * fsb + 4.02f * pp)) : -2.f * pp;
       if (it + (int)gridDim.x < n_items) {                        // prefetch the next item
         In = tc_item(A, it + gridDim.x);
         na_nx = A.S.norm[(size_t)In.fa * n_pad + In.rt * 128 + lrow];
@@ -475,7 +481,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
         }
         level = 0;
         if (!A.force_fallback && A.ratio2 >= 1.f)
-          level = kImad ? certify_imad(r1, r2, r3, na_n, mr, pp, fsa, fsb) : certify(r1, r2, r3, na_n, mr, pp, A.ibits);
+          level = kImad ? certify_imad(r1, r2, r3, na_n, mr, pp, fsa, fsb, A.kshift) : certify(r1, r2, r3, na_n, mr, pp, A.ibits);
         const size_t o_nn = (size_t)I.p * A.kp.n_max + i;
         if (level == 1) {
           (I.dir == 0 ? A.S.nn_ab : A.S.nn_ba)[o_nn] = (int32_t)(r1 & imask);
@@ -1130,8 +1136,10 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   // batched full scans pay off when a row's scan reads >= 512 KB of references (n >= 1024);
   // below that the per-row queue (one CTA per row, 8 warps split the references) is faster
   const int fs_batched = kp.n_max >= kFsBatchRefs ? 1 : 0;
-  TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2, fs_batched, 512u};
-  const bool imad_keys = ibits <= 9 && !getenv("BT_MATCH_LOP3");   // BT_MATCH_LOP3: dev A/B of the key packing
+  const int kshift = std::max(ibits, 9);
+  TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2, fs_batched, 1u << kshift, kshift,
+            ldexpf(1.f, 9 - kshift), 0x3F800000u + (1u << (32 - kshift)) - 1u};
+  const bool imad_keys = kshift <= 16 && !getenv("BT_MATCH_LOP3");   // BT_MATCH_LOP3: dev A/B of the key packing
   auto kws = imad_keys ? k_match_ws<true> : k_match_ws<false>;
   L.begin(K_MATCH_TC, s);
   // two CTAs per SM by design (2 x 108 KB of shared memory, 2 x 256 TMEM columns, 96 registers;
