@@ -254,7 +254,15 @@ __device__ __forceinline__ TcItem tc_item(const TcArgs &A, int it) {
   return I;
 }
 
-template <bool kImad>
+// kTop2 (the batched path, n_max >= 1024, where undecided rows go to the level-2 pass): four
+// interleaved top-2 sets per thread instead of two top-3 sets — 2.5 instead of 4 ALU min / max
+// per element.  The global top-2 is exact (each of its keys is in its set's top-2); for the
+// third-best value only a lower bound is known: LB = min(3rd of the union of the sets' top-2s,
+// min over sets of their 2nd) — if all of the global top-3 are in the union, LB <= the union's
+// 3rd = the true 3rd; else a global top-3 key lies beyond its set's 2nd, so the true 3rd >= that
+// set's 2nd >= LB.  The certificate takes LB for the third-best value (level 2 only), so a row
+// may be left undecided where the exact top-3 would have certified it, never the converse.
+template <bool kImad, bool kTop2>
 __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constant__ CUtensorMap tmap, TcArgs A) {
   pdl_wait();
   extern __shared__ uint8_t tc_smem_raw[];
@@ -415,6 +423,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
       }
       const int i = I.rt * 128 + lrow;
       unsigned r1 = kNone, r2 = kNone, r3 = kNone, s1 = kNone, s2 = kNone, s3 = kNone;
+      unsigned x1[4] = {kNone, kNone, kNone, kNone}, x2[4] = {kNone, kNone, kNone, kNone};   // kTop2 sets
       for (int c = 0; c < I.nchunks; ++c, ++g) {
         const int b = g & 1;
         mbar_wait(&bar_mma[b], (g >> 1) & 1);
@@ -443,7 +452,11 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
               k1 = (__float_as_uint(d1) & ~imask) | __float_as_uint(cc2.w);
             }
             const unsigned m = min(k0, k1), M = max(k0, k1);
-            if ((col & 2) == 0) {
+            if (kTop2) {
+              const int st = (col >> 1) & 3;
+              x2[st] = min(min(x2[st], max(x1[st], m)), M);
+              x1[st] = min(x1[st], m);
+            } else if ((col & 2) == 0) {
               const unsigned n3 = min(min(r3, max(r2, m)), max(r1, M)), n2 = min(min(r2, max(r1, m)), M);
               r1 = min(r1, m); r2 = n2; r3 = n3;
             } else {
@@ -457,7 +470,16 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
         if (lane == 0) mbar_arrive(&bar_free[b]);                 // TMEM + constants of buffer b released
       }
       // merge the even/odd sets, then the two warpgroups' top-3; certify; decide the row or queue it
-      {
+      unsigned mr2 = kNone;                                        // kTop2: min of the sets' 2nd
+      if (kTop2) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const unsigned k = t < 4 ? x1[t] : x2[t - 4];
+          const unsigned n3 = min(r3, max(r2, k)), n2 = min(r2, max(r1, k));
+          r1 = min(r1, k); r2 = n2; r3 = n3;
+        }
+        mr2 = min(min(x2[0], x2[1]), min(x2[2], x2[3]));
+      } else {
         const unsigned ks[3] = {s1, s2, s3};
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
@@ -467,7 +489,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
         }
       }
       uint4 *rm = rmerge[nitem & 1];
-      if (wg == 1) rm[lrow] = make_uint4(r1, r2, r3, 0u);
+      if (wg == 1) rm[lrow] = make_uint4(r1, r2, r3, mr2);
       named_bar(1, kWsEpiWarps * 32);
       int level = 1;
       if (wg == 0 && i < I.na) {
@@ -479,6 +501,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
           const unsigned n3 = min(r3, max(r2, k)), n2 = min(r2, max(r1, k));
           r1 = min(r1, k); r2 = n2; r3 = n3;
         }
+        if (kTop2) r3 = min(r3, min(mr2, o.w));                   // the third-best lower bound
         level = 0;
         if (!A.force_fallback && A.ratio2 >= 1.f)
           level = kImad ? certify_imad(r1, r2, r3, na_n, mr, pp, fsa, fsb, A.kshift) : certify(r1, r2, r3, na_n, mr, pp, A.ibits);
@@ -1140,7 +1163,11 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2, fs_batched, 1u << kshift, kshift,
             ldexpf(1.f, 9 - kshift), 0x3F800000u + (1u << (32 - kshift)) - 1u};
   const bool imad_keys = kshift <= 16 && !getenv("BT_MATCH_LOP3");   // BT_MATCH_LOP3: dev A/B of the key packing
-  auto kws = imad_keys ? k_match_ws<true> : k_match_ws<false>;
+  // four top-2 sets where the level-2 pass takes the rows they leave undecided (BT_MATCH_TOP3:
+  // dev A/B against the exact top-3)
+  const bool top2 = fs_batched && !getenv("BT_MATCH_TOP3");
+  auto kws = imad_keys ? (top2 ? k_match_ws<true, true> : k_match_ws<true, false>)
+                       : (top2 ? k_match_ws<false, true> : k_match_ws<false, false>);
   L.begin(K_MATCH_TC, s);
   // two CTAs per SM by design (2 x 108 KB of shared memory, 2 x 256 TMEM columns, 96 registers;
   // ncu: block limits 2 / 2); the occupancy API reports 1 for this configuration, so the grid
@@ -1150,6 +1177,16 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   const int ws_grid = sm_count() * 2;
   launch_pdl(kws, std::min(ws_grid, 2 * P * rt_count), kWsThreads, kWsSmem, s, *tmap, ta);
   L.end(K_MATCH_TC, s);
+  if (getenv("BT_MATCH_STATS") && fs_batched) {                   // dev aid (synchronizes): first-level outcome
+    unsigned c0 = 0;
+    cudaStreamSynchronize(s);
+    cudaMemcpy(&c0, S.work_count, 4, cudaMemcpyDeviceToHost);
+    std::vector<int32_t> fc(2 * P * rt_count);
+    cudaMemcpy(fc.data(), S.fs_count, fc.size() * 4, cudaMemcpyDeviceToHost);
+    long long t = 0;
+    for (int v : fc) t += v;
+    fprintf(stderr, "bt matching: first level left %u rows top-2, %lld rows undecided\n", c0, t);
+  }
   L.begin(K_RESOLVE, s);
   RescoreArgs ra{kp, pairs, S, ibits, ratio2};
   if (fs_batched) {

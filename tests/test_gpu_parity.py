@@ -409,6 +409,57 @@ def test_match_large_n_multi_chunk(bt, torch, ctx):
     assert len(got[0]) >= 3900
 
 
+def test_match_top2_sets_three_near_ties_in_one_set(bt, torch):
+    """n_max >= 1024: the candidate kernel keeps four top-2 sets per row (columns j with equal
+    (j mod 128) < 64 and ((j mod 32) >> 1) & 3 share one) and certifies "the nearest neighbour is
+    one of the top two" against a LOWER bound of the third-best value.  Adversarial rows: three
+    near-copies of row i (distance gaps far below the fp16 certificate) in three columns of ONE
+    set, every other reference far away — the union of the sets' top-2 then holds only two of
+    the three close keys, and a third-best taken from the union alone would certify a top-2
+    rescoring that misses the true nearest neighbour whenever fp16 ranks it third.  Both
+    directions, against the oracle and against the forced exact path."""
+    import os
+    rng = np.random.default_rng(2027)
+    n_max, na = 1024, 256
+    a = rng.normal(size=(na, 128))
+    a /= np.linalg.norm(a, axis=1, keepdims=True)
+    b = rng.normal(size=(n_max, 128))
+    b /= np.linalg.norm(b, axis=1, keepdims=True)
+    # per 32-column block: set s (0..3) owns columns {2s, 2s + 1} + 8 k; two triples per set
+    i = 0
+    for blk in range(n_max // 32):
+        for s_ in range(4):
+            cols = [blk * 32 + 2 * s_ + o + 8 * k for k in range(4) for o in (0, 1)]
+            for tri in (cols[0::2][:3], cols[1::2][:3]):
+                # squared distances 1.00 / 1.21 / 1.44 e-4 in a random column order: gaps far
+                # outside the oracle's band (1e-6), far inside both certificates (~4e-3, ~5e-4)
+                for c, r in zip(tri, rng.permutation([0.010, 0.011, 0.012])):
+                    d = rng.normal(size=128)
+                    b[c] = a[i] + r * d / np.linalg.norm(d)
+                i += 1
+    assert i == na
+    sc = _custom_scene([na, n_max], n_max=n_max, seed=3)
+    sc.desc[0] = 0.0
+    sc.desc[0, :na] = a
+    sc.desc[1] = b
+    pairs = [(0, 1), (1, 0)]
+    outs = []
+    for force in ("0", "1"):
+        os.environ["BT_FORCE_FALLBACK"] = force
+        c = bt.Context(0)
+        c.reserve(len(pairs), n_max, 256, 2)
+        got, _, _ = gpu_match(bt, torch, c, sc, pairs)
+        outs.append(got)
+        c.close()
+    os.environ.pop("BT_FORCE_FALLBACK", None)
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
+    for p, (fa, fb_) in enumerate(pairs):
+        o = oracle.match(sc.desc[fa, :sc.n_kp[fa]], sc.desc[fb_, :sc.n_kp[fb_]])
+        assert parity.compare_matches(outs[0][p], o) == 0          # no row excused by the band
+    assert len(outs[0][0]) == na
+
+
 def test_register_pairs_c5_stress_sampled(bt, torch):
     """BASELINE configs[4] shape on one GPU, reduced in frames: n = 4096 keypoints
     (n_max 4096), 16384 hypotheses, 6 frames (15 pairs, 30 dense edges at 640x480); two
