@@ -709,6 +709,7 @@ def main():
     # derived on the device (NEXT-4), so only those bytes cross PCIe.  Also the older entry
     # bt_register_pairs_host with precomputed normal maps and 3-D keypoints (e2e_precomputed_maps).
     e2e = None
+    e2e_blocking = None
     e2e_pre = None
     if not args.no_e2e:
         def timed(step, n):
@@ -759,10 +760,40 @@ def main():
             exchange_host()
         v_raw = timed(raw_step, args.e2e_steps)
         d_raw = bt.decode_records(h_rec, N_MAX)
-        e2e = {"value": v_raw, "unit": UNIT, "h2d_bytes_per_step": int(h2d_raw + xh2d), "d2h_bytes_per_step": int(d2h + xd2h),
-               "api": "bt_register_raw_host: pinned host depth, mask, 2-D keypoints + descriptors in, records out "
-                      "(normal map and keypoint lifting on the device; copies + sync inside the call)",
-               "pairs_ok": int((d_raw["status"] == 0).sum())}
+        e2e_blocking = {"value": v_raw, "unit": UNIT, "h2d_bytes_per_step": int(h2d_raw + xh2d),
+                        "d2h_bytes_per_step": int(d2h + xd2h),
+                        "api": "bt_register_raw_host: pinned host depth, mask, 2-D keypoints + descriptors in, "
+                               "records out (normal map and keypoint lifting on the device; copies + sync inside "
+                               "the call)", "pairs_ok": int((d_raw["status"] == 0).sum())}
+        e2e = e2e_blocking
+        if world == 1:
+            # the streaming form: bt_register_raw_host_async per step (each step still copies its
+            # inputs in and its records out), one synchronisation at the end — the copies of step
+            # t + 1 run on the copy engine while the kernels of step t run.  One event pair on the
+            # caller's stream around the K calls (the device is idle when the first is recorded,
+            # so no copy of the first call can precede it).
+            h_recs = [torch.zeros_like(h_rec).pin_memory() for _ in range(2)]
+
+            def raw_async(k):
+                ctx.register_raw(h_depth, h_mask, h_uv, h_desc, h_nin, sc.K, h_pose, h_pairs, h_uid, rprm, eprm,
+                                 h_recs[k & 1], stream=stream, blocking=False)
+            for k in range(3):
+                raw_async(k)
+            torch.cuda.synchronize()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record(stream)
+            for k in range(args.e2e_steps):
+                raw_async(k)
+            eb.record(stream)
+            torch.cuda.synchronize()
+            v_pipe = P * args.e2e_steps / (ea.elapsed_time(eb) / 1e3)
+            assert all(np.array_equal(r.numpy(), h_rec.numpy()) for r in h_recs), "async records differ"
+            e2e = {"value": v_pipe, "unit": UNIT, "h2d_bytes_per_step": int(h2d_raw), "d2h_bytes_per_step": int(d2h),
+                   "api": "bt_register_raw_host_async per step: pinned host depth, mask, 2-D keypoints + "
+                          "descriptors in, records out to pinned host memory (normal map and keypoint lifting on "
+                          "the device); two staging slots, so the host->device copies of step t + 1 overlap the "
+                          "kernels of step t; one synchronisation after the K steps",
+                   "pairs_ok": int((d_raw["status"] == 0).sum()), "blocking_value": v_raw}
         hb = bt.FrameBatch.from_scene(sc, device="cpu", pin=True)
         h2d_pre = small + sum(x.numel() * x.element_size() for x in (hb.n_kp, hb.desc, hb.pts, hb.nrm, hb.depth,
                                                                    hb.normal, hb.mask))
@@ -805,7 +836,7 @@ def main():
                 else "single GPU",
                 "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
                 "roofline": roof, "kernels": kern, "kernel_ms_per_step": step_ms_by_kernel,
-                "e2e": e2e, "e2e_precomputed_maps": e2e_pre, "cpu_baseline": cpu, "next_pose_graph": graph,
+                "e2e": e2e, "e2e_blocking": e2e_blocking, "e2e_precomputed_maps": e2e_pre, "cpu_baseline": cpu, "next_pose_graph": graph,
                 "next_input_prep": prep, "c4": c4, "c5": c5}
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -190,8 +190,10 @@ bt_status bt_register_pairs_host(bt_ctx *ctx, const bt_keypoints *kp, const bt_m
    Equivalent to: bt_estimate_normals(depth, jump_m) -> bt_lift_keypoints(uv, desc, n_in, maps)
    -> bt_register_pairs on those outputs (bitwise the same records), with the host -> device
    copies of the inputs, and the device -> host copy of the records, inside the call; it
-   synchronises `stream` before returning.  Needs bt_reserve(max_frames, width, height) (its
-   staging holds the raw inputs).
+   synchronises `stream` before returning.  Needs bt_reserve(max_frames, width, height); the
+   first raw call allocates two staging slots at that capacity (the raw inputs of two calls),
+   which consecutive calls use in turn.  The copies run on the context's copy stream once the
+   call that used the slot before is done with it.
    Layouts: depth [F][H][W] f32, mask [F][H][W] u8, uv [F][n_max][2] f32, desc [F][n_max][dim]
    f32, n_in [F] (detector counts); node_pose [F], pairs [P][2], pair_uid [P], records
    [P][bt_record_words(n_max)].  eprm may be NULL (no dense edges).  Errors: as bt_register_pairs
@@ -211,6 +213,17 @@ bt_status bt_register_raw_host(bt_ctx *ctx, const bt_raw_frames *raw, const bt_i
                                const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid,
                                int32_t P, const bt_match_params *mprm, const bt_ransac_params *rprm,
                                const bt_edge_params *eprm, uint32_t *records, void *stream);
+/* The same call without the final synchronisation — the streaming form for consecutive frame
+   batches: the host -> device copies of call t + 1 (other slot) overlap the kernels of call t.
+   On return the work is enqueued; `records` (pinned host memory) holds the result once `stream`
+   has reached the call's end (cudaStreamSynchronize / an event recorded after the call).  The
+   host input buffers must stay unchanged until then, and two calls in flight must not share a
+   `records` buffer the caller still reads.  Errors found at enqueue time as above; a failure
+   inside the kernels surfaces as BT_ECUDA on a later call. */
+bt_status bt_register_raw_host_async(bt_ctx *ctx, const bt_raw_frames *raw, const bt_intrinsics *K,
+                                     const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid,
+                                     int32_t P, const bt_match_params *mprm, const bt_ransac_params *rprm,
+                                     const bt_edge_params *eprm, uint32_t *records, void *stream);
 
 /* NEXT-3: fused record exchange.  The per-pair records are what every rank's
    pose-graph solve needs (the pair correspondences built "in parallel on GPU", §IV-D);

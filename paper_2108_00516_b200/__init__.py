@@ -28,7 +28,7 @@ SYMBOLS = ("bt_create", "bt_destroy", "bt_last_error", "bt_status_string", "bt_r
            "bt_profile_kernels", "bt_profile_name", "bt_profile_read", "bt_pose_graph_step",
            "bt_estimate_normals", "bt_relinearize", "bt_relinearize_matches", "bt_copy_matches",
            "bt_dense_assoc", "bt_lift_keypoints", "bt_coarse_pose", "bt_select_keyframes", "bt_pool_admit",
-           "bt_set_record_peers", "bt_register_raw_host")
+           "bt_set_record_peers", "bt_register_raw_host", "bt_register_raw_host_async")
 
 
 class BtError(RuntimeError):
@@ -127,9 +127,9 @@ def lib():
         L.bt_select_keyframes.argtypes = [vp, vp, vp, i32, vp, i32, vp, vp, vp]
         L.bt_pool_admit.argtypes = [vp, vp, vp, i32, vp, C.c_float, vp, vp]
         L.bt_set_record_peers.argtypes = [vp, i32, C.POINTER(C.c_uint64), i32, i32]
-        L.bt_register_raw_host.argtypes = [vp, C.POINTER(RawFrames), C.POINTER(Intrinsics), vp, vp, vp, i32,
-                                           C.POINTER(MatchParams), C.POINTER(RansacParams), C.POINTER(EdgeParams),
-                                           vp, vp]
+        for f in ("bt_register_raw_host", "bt_register_raw_host_async"):
+            getattr(L, f).argtypes = [vp, C.POINTER(RawFrames), C.POINTER(Intrinsics), vp, vp, vp, i32,
+                                      C.POINTER(MatchParams), C.POINTER(RansacParams), C.POINTER(EdgeParams), vp, vp]
         L.bt_last_launch_count.argtypes = [vp]
         L.bt_last_launch_count.restype = i32
         L.bt_profile_enable.argtypes = [vp, i32]
@@ -143,7 +143,8 @@ def lib():
         for f in ("bt_create", "bt_reserve", "bt_match", "bt_ransac", "bt_dense_corr", "bt_dense_assoc", "bt_register_pairs",
                   "bt_register_pairs_host", "bt_compose_poses", "bt_pose_graph_step", "bt_estimate_normals", "bt_relinearize",
                   "bt_relinearize_matches", "bt_copy_matches", "bt_lift_keypoints", "bt_coarse_pose",
-                  "bt_select_keyframes", "bt_pool_admit", "bt_set_record_peers", "bt_register_raw_host"):
+                  "bt_select_keyframes", "bt_pool_admit", "bt_set_record_peers", "bt_register_raw_host",
+                  "bt_register_raw_host_async"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -306,19 +307,23 @@ class Context:
         self._check(st, "bt_register_pairs_host" if host else "bt_register_pairs")
 
     def register_raw(self, depth, mask, uv, desc, n_in, K, node_pose, pairs, uid, rprm: RansacParams,
-                     eprm: EdgeParams | None, records, jump_m: float = 0.05, ratio: float = 1.0, stream=None):
+                     eprm: EdgeParams | None, records, jump_m: float = 0.05, ratio: float = 1.0, stream=None,
+                     blocking: bool = True):
         """bt_register_raw_host: depth [F][H][W] f32, mask [F][H][W] u8, uv [F][n_max][2] f32, desc
         [F][n_max][128] f32, n_in [F] i32, node_pose [F] (12 f32), pairs [P][2], uid [P], records
         [P][record_words] — all HOST tensors / arrays (pinned for full speed); normals and the
-        keypoints' points / normals are derived on the device.  Synchronises the stream."""
+        keypoints' points / normals are derived on the device.  Synchronises the stream; with
+        blocking=False (bt_register_raw_host_async) only enqueues: the copies of the next call
+        overlap this call's kernels, and `records` is valid once the stream has passed the call."""
         F, H, W = (int(x) for x in depth.shape)
         raw = RawFrames(F, W, H, int(uv.shape[1]), int(desc.shape[2]), float(jump_m), _ptr(depth), _ptr(mask),
                         _ptr(uv), _ptr(desc), _ptr(n_in))
         Ki = intrinsics(K) if not isinstance(K, Intrinsics) else K
-        self._check(lib().bt_register_raw_host(self._h, C.byref(raw), C.byref(Ki), _ptr(node_pose), _ptr(pairs),
-                                               _ptr(uid), int(pairs.shape[0]), C.byref(MatchParams(ratio)),
-                                               C.byref(rprm), C.byref(eprm) if eprm is not None else None,
-                                               _ptr(records), self._stream(stream)), "bt_register_raw_host")
+        name = "bt_register_raw_host" if blocking else "bt_register_raw_host_async"
+        self._check(getattr(lib(), name)(self._h, C.byref(raw), C.byref(Ki), _ptr(node_pose), _ptr(pairs),
+                                         _ptr(uid), int(pairs.shape[0]), C.byref(MatchParams(ratio)),
+                                         C.byref(rprm), C.byref(eprm) if eprm is not None else None,
+                                         _ptr(records), self._stream(stream)), name)
 
     def set_record_peers(self, peer_ptrs, row_offset: int = 0, rows: int = 0):
         """NEXT-3 (bt_set_record_peers): register_pairs also stores local pair p's record into row

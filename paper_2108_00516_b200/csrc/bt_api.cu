@@ -56,9 +56,21 @@ struct bt_ctx {
   float *st_desc = nullptr, *st_pts = nullptr, *st_nrm = nullptr, *st_depth = nullptr, *st_normal = nullptr;
   uint8_t *st_mask = nullptr;
   bt_pose *st_pose = nullptr;
-  float *st_uv = nullptr, *st_desc_in = nullptr;             // bt_register_raw_host staging
-  int32_t *st_nin = nullptr;
   cudaEvent_t ev_maps = nullptr;                              // raw entry: maps + normals staged
+  // bt_register_raw_host(_async) staging: two slots (allocated on the first raw call), used in
+  // turn, so the copies of call t + 1 (on the copy stream) overlap the kernels of call t; a
+  // slot's copies wait for ev_free, recorded once the call that used it last is done with it
+  struct RawSlot {
+    float *depth = nullptr, *normal = nullptr, *uv = nullptr, *desc_in = nullptr;
+    uint8_t *mask = nullptr;
+    int32_t *nin = nullptr, *pairs = nullptr;
+    uint32_t *uid = nullptr;
+    bt_pose *pose = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_free = nullptr;
+  };
+  RawSlot raw[2];
+  int raw_next = 0;
+  cudaStream_t h2d = nullptr;                                 // host -> device copies of the raw entry
 };
 
 namespace bt {
@@ -136,7 +148,10 @@ void free_scratch(bt_ctx *c) {
   free_dev(c->st_nkp); free_dev(c->st_pairs); free_dev(c->st_uid); free_dev(c->st_records);
   free_dev(c->st_desc); free_dev(c->st_pts); free_dev(c->st_nrm); free_dev(c->st_depth);
   free_dev(c->st_normal); free_dev(c->st_mask); free_dev(c->st_pose);
-  free_dev(c->st_uv); free_dev(c->st_desc_in); free_dev(c->st_nin);
+  for (auto &r : c->raw) {
+    free_dev(r.depth); free_dev(r.normal); free_dev(r.uv); free_dev(r.desc_in); free_dev(r.mask);
+    free_dev(r.nin); free_dev(r.pairs); free_dev(r.uid); free_dev(r.pose);
+  }
 }
 
 #define BT_CHECK_CTX(c)                                                                  \
@@ -253,10 +268,17 @@ bt_status bt_create(bt_ctx **out, int cuda_device) {
       cudaEventCreateWithFlags(&c->ev_join_hi, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_maps, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_maps, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return BT_ECUDA;
   }
+  for (auto &r : c->raw)
+    if (cudaEventCreateWithFlags(&r.ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&r.ev_free, cudaEventDisableTiming) != cudaSuccess) {
+      delete c;
+      return BT_ECUDA;
+    }
   const char *ff = getenv("BT_FORCE_FALLBACK");
   c->force_fallback = ff && ff[0] && ff[0] != '0';
   *out = c;
@@ -275,6 +297,11 @@ void bt_destroy(bt_ctx *c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_maps) cudaEventDestroy(c->ev_maps);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  for (auto &r : c->raw) {
+    if (r.ev_in) cudaEventDestroy(r.ev_in);
+    if (r.ev_free) cudaEventDestroy(r.ev_free);
+  }
   free_scratch(c);
   delete c;
 }
@@ -364,9 +391,7 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
          cudaMalloc(&c->st_desc, FN * 128 * 4) == cudaSuccess && cudaMalloc(&c->st_pts, FN * 12) == cudaSuccess &&
          cudaMalloc(&c->st_nrm, FN * 12) == cudaSuccess && cudaMalloc(&c->st_pose, (size_t)max_frames * sizeof(bt_pose)) == cudaSuccess &&
          cudaMalloc(&c->st_pairs, (size_t)max_pairs * 8) == cudaSuccess && cudaMalloc(&c->st_uid, (size_t)max_pairs * 4) == cudaSuccess &&
-         cudaMalloc(&c->st_records, (size_t)max_pairs * bt::rec_words(n_max) * 4) == cudaSuccess &&
-         cudaMalloc(&c->st_uv, FN * 8) == cudaSuccess && cudaMalloc(&c->st_desc_in, FN * bt::kDim * 4) == cudaSuccess &&
-         cudaMalloc(&c->st_nin, (size_t)max_frames * 4) == cudaSuccess;
+         cudaMalloc(&c->st_records, (size_t)max_pairs * bt::rec_words(n_max) * 4) == cudaSuccess;
     if (ok && FP > 0)
       ok = cudaMalloc(&c->st_depth, FP * 4) == cudaSuccess && cudaMalloc(&c->st_normal, FP * 12) == cudaSuccess &&
            cudaMalloc(&c->st_mask, FP) == cudaSuccess;
@@ -592,17 +617,39 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
 // NEXT-4 end to end: the raw per-frame inputs (depth, mask, the detector's 2-D keypoints and
 // descriptors) from host memory; normals (bt_estimate_normals) and the keypoints' 3-D points /
 // normals (bt_lift_keypoints) are derived on the device, then the whole per-pair path.
-bt_status bt_register_raw_host(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *K,
-                               const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid, int32_t P,
-                               const bt_match_params *mprm, const bt_ransac_params *rprm,
-                               const bt_edge_params *eprm, uint32_t *records, void *stream) {
-  BT_CHECK_CTX(c);
+namespace {
+// the raw entry's two staging slots, at the reserved capacity (first raw call only)
+bool ensure_raw_slots(bt_ctx *c) {
+  if (c->raw[0].depth) return true;
+  const size_t F = (size_t)c->cap_stage, FN = F * c->cap_nmax, FP = F * c->cap_w * c->cap_h;
+  bool ok = F > 0 && FP > 0;
+  for (auto &r : c->raw)
+    ok = ok && cudaMalloc(&r.depth, FP * 4) == cudaSuccess && cudaMalloc(&r.normal, FP * 12) == cudaSuccess &&
+         cudaMalloc(&r.mask, FP) == cudaSuccess && cudaMalloc(&r.uv, FN * 8) == cudaSuccess &&
+         cudaMalloc(&r.desc_in, FN * bt::kDim * 4) == cudaSuccess && cudaMalloc(&r.nin, F * 4) == cudaSuccess &&
+         cudaMalloc(&r.pairs, (size_t)c->cap_pairs * 8) == cudaSuccess &&
+         cudaMalloc(&r.uid, (size_t)c->cap_pairs * 4) == cudaSuccess && cudaMalloc(&r.pose, F * sizeof(bt_pose)) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    for (auto &r : c->raw) {
+      free_dev(r.depth); free_dev(r.normal); free_dev(r.uv); free_dev(r.desc_in); free_dev(r.mask);
+      free_dev(r.nin); free_dev(r.pairs); free_dev(r.uid); free_dev(r.pose);
+    }
+  }
+  return ok;
+}
+
+// validate, then enqueue one raw call on staging slot c->raw_next (see include/bt.h)
+bt_status raw_enqueue(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *K, const bt_pose *node_pose,
+                      const int32_t *pairs, const uint32_t *pair_uid, int32_t P, const bt_match_params *mprm,
+                      const bt_ransac_params *rprm, const bt_edge_params *eprm, uint32_t *records, cudaStream_t st,
+                      const char *what) {
   bt_status s;
-  if (!raw || !K || !node_pose) return fail(c, BT_EINVAL, "bt_register_raw_host: NULL raw / K / poses");
-  if (raw->dim != bt::kDim) return fail(c, BT_EUNSUPPORTED, "bt_register_raw_host: descriptor dim %d != 128", raw->dim);
+  if (!raw || !K || !node_pose) return fail(c, BT_EINVAL, "%s: NULL raw / K / poses", what);
+  if (raw->dim != bt::kDim) return fail(c, BT_EUNSUPPORTED, "%s: descriptor dim %d != 128", what, raw->dim);
   const int F = raw->n_frames, W = raw->width, H = raw->height, n_max = raw->n_max;
-  if (F < 1 || W < 1 || H < 1 || n_max < 1 || P < 0) return fail(c, BT_EINVAL, "bt_register_raw_host: bad sizes");
-  if (!(raw->jump_m >= 0.f)) return fail(c, BT_EINVAL, "bt_register_raw_host: jump < 0");
+  if (F < 1 || W < 1 || H < 1 || n_max < 1 || P < 0) return fail(c, BT_EINVAL, "%s: bad sizes", what);
+  if (!(raw->jump_m >= 0.f)) return fail(c, BT_EINVAL, "%s: jump < 0", what);
   if (F > c->cap_stage) return fail(c, BT_ECAPACITY, "frames %d > reserved staging %d", F, c->cap_stage);
   if ((size_t)W * H > (size_t)c->cap_w * c->cap_h) return fail(c, BT_ECAPACITY, "maps beyond reserved staging");
   if (n_max > c->cap_nmax) return fail(c, BT_ECAPACITY, "n_max %d > reserved %d", n_max, c->cap_nmax);
@@ -610,10 +657,14 @@ bt_status bt_register_raw_host(bt_ctx *c, const bt_raw_frames *raw, const bt_int
   if ((s = check_ransac(c, rprm)) != BT_OK) return s;
   if (P == 0) return BT_OK;
   if (!raw->depth || !raw->mask || !raw->uv || !raw->desc || !raw->n_in || !pairs || !pair_uid || !records)
-    return fail(c, BT_EINVAL, "bt_register_raw_host: NULL buffer");
+    return fail(c, BT_EINVAL, "%s: NULL buffer", what);
+  if (!c->st_depth) return fail(c, BT_ECAPACITY, "%s: no staging reserved", what);
+  if (!ensure_raw_slots(c)) return fail(c, BT_ENOMEM, "%s: staging allocation failed", what);
+  const int slot = c->raw_next;
+  bt_ctx::RawSlot &r = c->raw[slot];
   bt_maps dm{};
   dm.n_frames = F; dm.width = W; dm.height = H;
-  dm.depth = c->st_depth; dm.normal = c->st_normal; dm.mask = c->st_mask;
+  dm.depth = r.depth; dm.normal = r.normal; dm.mask = r.mask;
   if ((s = check_maps(c, &dm, K)) != BT_OK) return s;
   if (eprm) {
     if ((s = check_edge(c, eprm)) != BT_OK) return s;
@@ -623,51 +674,75 @@ bt_status bt_register_raw_host(bt_ctx *c, const bt_raw_frames *raw, const bt_int
   dk.n_frames = F; dk.n_max = n_max; dk.dim = bt::kDim;
   dk.n_kp = c->st_nkp; dk.desc = c->st_desc; dk.pts = c->st_pts; dk.nrm = c->st_nrm;
   if ((s = check_kp(c, &dk)) != BT_OK) return s;
-  if (!c->st_uv || !c->st_depth) return fail(c, BT_ECAPACITY, "bt_register_raw_host: no staging reserved");
-  const cudaStream_t st = (cudaStream_t)stream;
+  c->raw_next ^= 1;
   const size_t FN = (size_t)F * n_max, FP = (size_t)F * W * H;
   c->cached_P = -1;                                              // match lists from staged keypoints
   const int rw = bt::rec_words(n_max);
   c->launch.count = 0;
-  // side stream: the maps (the bulk of the bytes) and the normal map from depth; caller's stream:
-  // keypoints, pairs, poses, then (once the maps are in) the lifting, matching and RANSAC
-  cudaEventRecord(c->ev_fork, st);                               // staging buffers free
-  cudaStreamWaitEvent(c->side, c->ev_fork, 0);
-  cudaMemcpyAsync(c->st_mask, raw->mask, FP, cudaMemcpyHostToDevice, c->side);
-  cudaMemcpyAsync(c->st_depth, raw->depth, FP * 4, cudaMemcpyHostToDevice, c->side);
-  bt::launch_normals(c->st_depth, F, W, H, *K, raw->jump_m, c->st_normal, c->side, c->launch);
+  // copy stream: every input into the slot, once the call that used the slot before is done
+  // with it (so they overlap the kernels of the previous call)
+  cudaStreamWaitEvent(c->h2d, r.ev_free, 0);
+  cudaMemcpyAsync(r.mask, raw->mask, FP, cudaMemcpyHostToDevice, c->h2d);
+  cudaMemcpyAsync(r.depth, raw->depth, FP * 4, cudaMemcpyHostToDevice, c->h2d);
+  cudaMemcpyAsync(r.pairs, pairs, (size_t)P * 8, cudaMemcpyHostToDevice, c->h2d);
+  cudaMemcpyAsync(r.uid, pair_uid, (size_t)P * 4, cudaMemcpyHostToDevice, c->h2d);
+  cudaMemcpyAsync(r.pose, node_pose, (size_t)F * sizeof(bt_pose), cudaMemcpyHostToDevice, c->h2d);
+  cudaMemcpyAsync(r.nin, raw->n_in, (size_t)F * 4, cudaMemcpyHostToDevice, c->h2d);
+  cudaMemcpyAsync(r.uv, raw->uv, FN * 8, cudaMemcpyHostToDevice, c->h2d);
+  cudaMemcpyAsync(r.desc_in, raw->desc, FN * bt::kDim * 4, cudaMemcpyHostToDevice, c->h2d);
+  cudaEventRecord(r.ev_in, c->h2d);
+  // side stream: the normal map from depth, then (after the caller's stream reached this call:
+  // the previous call's records are read) the dense edges
+  cudaStreamWaitEvent(c->side, r.ev_in, 0);
+  bt::launch_normals(r.depth, F, W, H, *K, raw->jump_m, r.normal, c->side, c->launch);
   cudaEventRecord(c->ev_maps, c->side);
-  cudaMemcpyAsync(c->st_nin, raw->n_in, (size_t)F * 4, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(c->st_uv, raw->uv, FN * 8, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(c->st_desc_in, raw->desc, FN * bt::kDim * 4, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(c->st_pairs, pairs, (size_t)P * 8, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(c->st_uid, pair_uid, (size_t)P * 4, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(c->st_pose, node_pose, (size_t)F * sizeof(bt_pose), cudaMemcpyHostToDevice, st);
-  if (eprm) {                                                    // dense edges: maps (side) + pairs / poses
-    cudaEventRecord(c->ev_join, st);
-    cudaStreamWaitEvent(c->side, c->ev_join, 0);
-    bt::launch_dense(mview(&dm), *K, c->st_pose, nullptr, c->st_pairs, 2 * P, *eprm, c->dense, nullptr, 0,
-                     c->st_records, rw, bt::rec_dense_ij(n_max), bt::rec_dense_ji(n_max), c->side, c->launch);
+  if (eprm) {
+    cudaEventRecord(c->ev_fork, st);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    bt::launch_dense(mview(&dm), *K, r.pose, nullptr, r.pairs, 2 * P, *eprm, c->dense, nullptr, 0, c->st_records, rw,
+                     bt::rec_dense_ij(n_max), bt::rec_dense_ji(n_max), c->side, c->launch);
   }
+  // caller's stream: lifting (needs the normal map), matching, RANSAC
   cudaStreamWaitEvent(st, c->ev_maps, 0);
-  bt::launch_lift(F, n_max, c->st_uv, c->st_desc_in, c->st_nin, mview(&dm), *K, c->st_nkp, c->st_desc, c->st_pts,
-                  c->st_nrm, st, c->launch);
+  bt::launch_lift(F, n_max, r.uv, r.desc_in, r.nin, mview(&dm), *K, c->st_nkp, c->st_desc, c->st_pts, c->st_nrm, st,
+                  c->launch);
   const float ratio = mprm ? mprm->ratio : 1.f;
-  bt::launch_match(kview(&dk), c->st_pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches,
-                   c->n_matches, st, c->launch);
-  bt::launch_ransac(kview(&dk), c->st_pairs, c->st_uid, P, c->matches, c->n_matches, *rprm, c->rs,
-                    c->st_records, rw, nullptr, eprm ? c->st_pose : nullptr, eprm ? eprm->huber_m : 0.f, st,
-                    c->launch);
+  bt::launch_match(kview(&dk), r.pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches, c->n_matches,
+                   st, c->launch);
+  bt::launch_ransac(kview(&dk), r.pairs, r.uid, P, c->matches, c->n_matches, *rprm, c->rs, c->st_records, rw, nullptr,
+                    eprm ? r.pose : nullptr, eprm ? eprm->huber_m : 0.f, st, c->launch);
   if (eprm) {
     cudaEventRecord(c->ev_join, c->side);
     cudaStreamWaitEvent(st, c->ev_join, 0);
   }
-  if ((s = after_launch(c, "bt_register_raw_host")) != BT_OK) return s;
-  const int launches = c->launch.count;
   cudaMemcpyAsync(records, c->st_records, (size_t)P * rw * 4, cudaMemcpyDeviceToHost, st);
+  cudaEventRecord(r.ev_free, st);
+  return after_launch(c, what);
+}
+}  // namespace
+
+bt_status bt_register_raw_host(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *K,
+                               const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid, int32_t P,
+                               const bt_match_params *mprm, const bt_ransac_params *rprm,
+                               const bt_edge_params *eprm, uint32_t *records, void *stream) {
+  BT_CHECK_CTX(c);
+  const cudaStream_t st = (cudaStream_t)stream;
+  bt_status s = raw_enqueue(c, raw, K, node_pose, pairs, pair_uid, P, mprm, rprm, eprm, records, st,
+                            "bt_register_raw_host");
+  if (s != BT_OK || P == 0) return s;
+  const int launches = c->launch.count;
   if (cudaStreamSynchronize(st) != cudaSuccess) return fail(c, BT_ECUDA, "bt_register_raw_host: sync failed");
   c->launch.count = launches;
   return after_launch(c, "bt_register_raw_host");
+}
+
+bt_status bt_register_raw_host_async(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *K,
+                                     const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid,
+                                     int32_t P, const bt_match_params *mprm, const bt_ransac_params *rprm,
+                                     const bt_edge_params *eprm, uint32_t *records, void *stream) {
+  BT_CHECK_CTX(c);
+  return raw_enqueue(c, raw, K, node_pose, pairs, pair_uid, P, mprm, rprm, eprm, records, (cudaStream_t)stream,
+                     "bt_register_raw_host_async");
 }
 
 bt_status bt_compose_poses(bt_ctx *c, const bt_pose *a, const bt_pose *b, bt_pose *out, int32_t n, void *stream) {

@@ -197,3 +197,40 @@ def test_raw_host_entry_equals_device_chain(bt, torch):
                          np.zeros((17, 512, 128), np.float32), np.zeros(17, np.int32), sc.K,
                          np.zeros((17, 12), np.float32), pairs.astype(np.int32), uid, rprm, None, host_rec)
     ctx.close()
+
+
+def test_raw_host_async_pipelined_equals_blocking(bt, torch):
+    """bt_register_raw_host_async: four calls in flight on one stream (two different frame
+    batches A, B alternating, so the two staging slots hold different inputs while the copies
+    of call t + 1 overlap the kernels of call t) give, after one synchronisation, the records
+    of the blocking calls bit for bit."""
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    batches = []
+    for seed in (21, 22):
+        sc = synth.make_scene(16, seed=seed)
+        uv, desc, n_in = detector_output(sc, seed=seed + 1)
+        pairs = synth.all_pairs(16)
+        batches.append((sc, [pin(sc.depth), pin(sc.mask), pin(uv), pin(desc), pin(n_in)],
+                        pin(sc.perturbed_poses(seed)), pin(pairs.astype(np.int32)),
+                        pin(np.arange(len(pairs), dtype=np.int32) + seed)))
+    ctx = bt.Context(0)
+    ctx.reserve(120, 512, 4096, 16, 640, 480)
+    rprm, eprm = bt.ransac_params(4096, SEED), bt.edge_params()
+    rw = bt.record_words(512)
+    want = []
+    for sc, inp, poses, pairs, uid in batches:
+        r = torch.zeros((len(pairs), rw), dtype=torch.int32).pin_memory()
+        ctx.register_raw(*inp, sc.K, poses, pairs, uid, rprm, eprm, r)
+        want.append(r.numpy().copy())
+    s = torch.cuda.Stream()
+    outs = []
+    for k in range(4):
+        sc, inp, poses, pairs, uid = batches[k % 2]
+        r = torch.zeros((len(pairs), rw), dtype=torch.int32).pin_memory()
+        ctx.register_raw(*inp, sc.K, poses, pairs, uid, rprm, eprm, r, stream=s, blocking=False)
+        outs.append(r)
+    s.synchronize()
+    for k, r in enumerate(outs):
+        assert np.array_equal(r.numpy(), want[k % 2]), f"async call {k} differs from the blocking call"
+    assert not np.array_equal(want[0], want[1])
+    ctx.close()
