@@ -208,6 +208,12 @@ typedef struct {
   const float *uv;               /* [F][n_max][2] keypoint pixel coordinates                      */
   const float *desc;             /* [F][n_max][dim] descriptors                                    */
   const int32_t *n_in;           /* [F] detected keypoints per frame                               */
+  /* optional: depth as the sensor / the paper's datasets store it, [F][H][W] uint16 (0 invalid),
+     metres = (float)value * depth_scale rounded to fp32 on the device (e.g. 0.001 for mm) — half
+     the bytes of `depth` over PCIe.  Exactly one of depth / depth_u16 is non-NULL; the records
+     equal those of `depth` holding the same fp32 values.                                         */
+  const uint16_t *depth_u16;
+  float depth_scale;             /* > 0 with depth_u16                                             */
 } bt_raw_frames;
 bt_status bt_register_raw_host(bt_ctx *ctx, const bt_raw_frames *raw, const bt_intrinsics *K,
                                const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid,

@@ -62,6 +62,7 @@ struct bt_ctx {
   // slot's copies wait for ev_free, recorded once the call that used it last is done with it
   struct RawSlot {
     float *depth = nullptr, *normal = nullptr, *uv = nullptr, *desc_in = nullptr;
+    uint16_t *depth_u16 = nullptr;
     uint8_t *mask = nullptr;
     int32_t *nin = nullptr, *pairs = nullptr;
     uint32_t *uid = nullptr;
@@ -150,7 +151,7 @@ void free_scratch(bt_ctx *c) {
   free_dev(c->st_normal); free_dev(c->st_mask); free_dev(c->st_pose);
   for (auto &r : c->raw) {
     free_dev(r.depth); free_dev(r.normal); free_dev(r.uv); free_dev(r.desc_in); free_dev(r.mask);
-    free_dev(r.nin); free_dev(r.pairs); free_dev(r.uid); free_dev(r.pose);
+    free_dev(r.nin); free_dev(r.pairs); free_dev(r.uid); free_dev(r.pose); free_dev(r.depth_u16);
   }
 }
 
@@ -628,12 +629,13 @@ bool ensure_raw_slots(bt_ctx *c) {
          cudaMalloc(&r.mask, FP) == cudaSuccess && cudaMalloc(&r.uv, FN * 8) == cudaSuccess &&
          cudaMalloc(&r.desc_in, FN * bt::kDim * 4) == cudaSuccess && cudaMalloc(&r.nin, F * 4) == cudaSuccess &&
          cudaMalloc(&r.pairs, (size_t)c->cap_pairs * 8) == cudaSuccess &&
-         cudaMalloc(&r.uid, (size_t)c->cap_pairs * 4) == cudaSuccess && cudaMalloc(&r.pose, F * sizeof(bt_pose)) == cudaSuccess;
+         cudaMalloc(&r.uid, (size_t)c->cap_pairs * 4) == cudaSuccess && cudaMalloc(&r.pose, F * sizeof(bt_pose)) == cudaSuccess &&
+         cudaMalloc(&r.depth_u16, FP * 2) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     for (auto &r : c->raw) {
       free_dev(r.depth); free_dev(r.normal); free_dev(r.uv); free_dev(r.desc_in); free_dev(r.mask);
-      free_dev(r.nin); free_dev(r.pairs); free_dev(r.uid); free_dev(r.pose);
+      free_dev(r.nin); free_dev(r.pairs); free_dev(r.uid); free_dev(r.pose); free_dev(r.depth_u16);
     }
   }
   return ok;
@@ -656,8 +658,12 @@ bt_status raw_enqueue(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *
   if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
   if ((s = check_ransac(c, rprm)) != BT_OK) return s;
   if (P == 0) return BT_OK;
-  if (!raw->depth || !raw->mask || !raw->uv || !raw->desc || !raw->n_in || !pairs || !pair_uid || !records)
+  if (!raw->mask || !raw->uv || !raw->desc || !raw->n_in || !pairs || !pair_uid || !records)
     return fail(c, BT_EINVAL, "%s: NULL buffer", what);
+  if (!raw->depth == !raw->depth_u16)
+    return fail(c, BT_EINVAL, "%s: exactly one of depth / depth_u16 must be given", what);
+  if (raw->depth_u16 && !(raw->depth_scale > 0.f))
+    return fail(c, BT_EINVAL, "%s: depth_scale %g <= 0 with depth_u16", what, (double)raw->depth_scale);
   if (!c->st_depth) return fail(c, BT_ECAPACITY, "%s: no staging reserved", what);
   if (!ensure_raw_slots(c)) return fail(c, BT_ENOMEM, "%s: staging allocation failed", what);
   const int slot = c->raw_next;
@@ -683,7 +689,8 @@ bt_status raw_enqueue(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *
   // with it (so they overlap the kernels of the previous call)
   cudaStreamWaitEvent(c->h2d, r.ev_free, 0);
   cudaMemcpyAsync(r.mask, raw->mask, FP, cudaMemcpyHostToDevice, c->h2d);
-  cudaMemcpyAsync(r.depth, raw->depth, FP * 4, cudaMemcpyHostToDevice, c->h2d);
+  if (raw->depth) cudaMemcpyAsync(r.depth, raw->depth, FP * 4, cudaMemcpyHostToDevice, c->h2d);
+  else cudaMemcpyAsync(r.depth_u16, raw->depth_u16, FP * 2, cudaMemcpyHostToDevice, c->h2d);
   cudaMemcpyAsync(r.pairs, pairs, (size_t)P * 8, cudaMemcpyHostToDevice, c->h2d);
   cudaMemcpyAsync(r.uid, pair_uid, (size_t)P * 4, cudaMemcpyHostToDevice, c->h2d);
   cudaMemcpyAsync(r.pose, node_pose, (size_t)F * sizeof(bt_pose), cudaMemcpyHostToDevice, c->h2d);
@@ -694,6 +701,7 @@ bt_status raw_enqueue(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *
   // side stream: the normal map from depth, then (after the caller's stream reached this call:
   // the previous call's records are read) the dense edges
   cudaStreamWaitEvent(c->side, r.ev_in, 0);
+  if (!raw->depth) bt::launch_depth_u16(r.depth_u16, raw->depth_scale, FP, r.depth, c->side, c->launch);
   bt::launch_normals(r.depth, F, W, H, *K, raw->jump_m, r.normal, c->side, c->launch);
   cudaEventRecord(c->ev_maps, c->side);
   if (eprm) {

@@ -234,3 +234,37 @@ def test_raw_host_async_pipelined_equals_blocking(bt, torch):
         assert np.array_equal(r.numpy(), want[k % 2]), f"async call {k} differs from the blocking call"
     assert not np.array_equal(want[0], want[1])
     ctx.close()
+
+
+def test_raw_host_depth_u16_equals_f32(bt, torch):
+    """A uint16 depth map (the sensor / dataset format, 0 = invalid) with depth_scale gives the
+    records of the f32 depth map holding float32(value) * float32(scale) — blocking and async —
+    and depth_scale <= 0 is rejected."""
+    sc = synth.make_scene(16, seed=31)
+    uv, desc, n_in = detector_output(sc, seed=32)
+    pairs = synth.all_pairs(16).astype(np.int32)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    d_mm = np.where(sc.depth > 0, np.rint(sc.depth * 1000.0), 0).clip(0, 65535).astype(np.uint16)
+    d_f = d_mm.astype(np.float32) * np.float32(1e-3)
+    ctx = bt.Context(0)
+    ctx.reserve(120, 512, 4096, 16, 640, 480)
+    rprm, eprm = bt.ransac_params(4096, SEED), bt.edge_params()
+    rw = bt.record_words(512)
+    args = (pin(sc.mask), pin(uv), pin(desc), pin(n_in), sc.K, pin(sc.perturbed_poses(3)), pin(pairs),
+            pin(np.arange(len(pairs), dtype=np.int32)), rprm, eprm)
+    want = torch.zeros((len(pairs), rw), dtype=torch.int32).pin_memory()
+    ctx.register_raw(pin(d_f), *args, want)
+    got = torch.zeros_like(want).pin_memory()
+    ctx.register_raw(pin(d_mm), *args, got, depth_scale=1e-3)
+    assert np.array_equal(got.numpy(), want.numpy())
+    s = torch.cuda.Stream()
+    got2 = [torch.zeros_like(want).pin_memory() for _ in range(2)]
+    for r in got2:
+        ctx.register_raw(pin(d_mm), *args, r, stream=s, blocking=False, depth_scale=1e-3)
+    s.synchronize()
+    for r in got2:
+        assert np.array_equal(r.numpy(), want.numpy())
+    assert (bt.decode_records(want, 512)["status"] == 0).all()
+    with pytest.raises(bt.BtError, match="EINVAL"):
+        ctx.register_raw(pin(d_mm), *args, got, depth_scale=0.0)
+    ctx.close()
