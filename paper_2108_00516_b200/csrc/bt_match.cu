@@ -892,6 +892,12 @@ __global__ void __launch_bounds__(128) k_match_l2(L2Args A) {
 constexpr int kFsRows = 32, kFsRefs = 64, kFsPitch = kFsRefs + 2;   // sB row pitch (8-B aligned pairs)
 constexpr int kFsSmall = 4;                      // (pair, dir)s with at most this many rows: per-row path
 constexpr int kFsBatchRefs = 1024;               // batch only when a row scan reads >= 512 KB
+#ifndef BT_L2_MIN_NMAX
+#define BT_L2_MIN_NMAX 1024
+#endif
+// n_max from which the rows the first level leaves undecided go to the level-2 pass (per-tile
+// lists) instead of the per-row exact queue
+constexpr int kL2MinNmax = BT_L2_MIN_NMAX;
 constexpr size_t kFsSmem = (size_t)(kFsRows * kDim + kDim * kFsPitch) * sizeof(float);
 
 struct FullScanArgs {
@@ -1106,7 +1112,7 @@ size_t match_scratch_bytes(int max_frames, int max_pairs, int n_max) {
   (void)rt;
   return al(F * np * kDim * 2) + al(F * np * 4) + al(F * 4) + al(2 * 2 * P * n_max * 16) + al(16) +
          al(P * n_max * 4) * 2 + al(P * n_max) + al(2 * P * np * 4) + al(2 * P * (np / 128) * 4) +
-         (n_max >= kFsBatchRefs ? al(F * np * kDim * 2) + al(2 * P * np * 4) + al(2 * P * 4) : 0);
+         (n_max >= kL2MinNmax ? al(F * np * kDim * 2) + al(2 * P * np * 4) + al(2 * P * 4) : 0);
 }
 
 MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_max) {
@@ -1127,7 +1133,7 @@ MatchScratch carve_match_scratch(void *p, int max_frames, int max_pairs, int n_m
   S.fs_rows = (int32_t *)c;      c += al(2 * P * np * 4);
   S.fs_count = (int32_t *)c;     c += al(2 * P * (np / 128) * 4);
   S.desc16lo = nullptr; S.l3_rows = nullptr; S.l3_count = nullptr;
-  if (n_max >= kFsBatchRefs) {                                   // the level-2 pass (batched full scans only)
+  if (n_max >= kL2MinNmax) {                                     // the level-2 pass (batched full scans only)
     S.desc16lo = (__half *)c;    c += al(F * np * kDim * 2);
     S.l3_rows = (int32_t *)c;    c += al(2 * P * np * 4);
     S.l3_count = (int32_t *)c;
@@ -1158,7 +1164,7 @@ void launch_match(const KpView &kp, const int32_t *pairs, int P, float ratio, co
   const float ratio2 = ratio >= 1.f ? 1.f : ratio * ratio;
   // batched full scans pay off when a row's scan reads >= 512 KB of references (n >= 1024);
   // below that the per-row queue (one CTA per row, 8 warps split the references) is faster
-  const int fs_batched = kp.n_max >= kFsBatchRefs ? 1 : 0;
+  const int fs_batched = kp.n_max >= kL2MinNmax ? 1 : 0;
   const int kshift = std::max(ibits, 9);
   TcArgs ta{kp, pairs, S, n_pad, ibits, P, force_fallback, ratio2, fs_batched, 1u << kshift, kshift,
             ldexpf(1.f, 9 - kshift), 0x3F800000u + (1u << (32 - kshift)) - 1u};
