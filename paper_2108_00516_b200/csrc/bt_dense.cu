@@ -564,8 +564,14 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         const float4 a = sP[k];
         const float qx = a.x + dq0, qy = a.y + dq1, qz = a.z + dq2;
         const float ar = fabsf(r);
-        const float w = !acc_ok ? 0.f : (ar <= A.huber ? 1.f : __fdividef(A.huber, ar));
-        const float rho = !acc_ok ? 0.f : (ar <= A.huber ? 0.5f * r * r : A.huber * (ar - 0.5f * A.huber));
+        // Huber (R17) without branches: with m = min(|r|, h), rho = m (|r| - m / 2) is 0.5 r^2
+        // inside and h (|r| - h / 2) beyond (the same roundings as the two formulas); the weight
+        // h / |r| beyond is h * rcp(|r|) (|r| > h > 0: no range fix-up needed)
+        const float m = fminf(ar, A.huber);
+        float rcp;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(ar));
+        const float w = acc_ok ? (ar <= A.huber ? 1.f : A.huber * rcp) : 0.f;
+        const float rho = acc_ok ? m * fmaf(-0.5f, m, ar) : 0.f;
         const float J[6] = {n0, n1, n2, qy * n2 - qz * n1, qz * n0 - qx * n2, qx * n1 - qy * n0};
         int q = 0;
 #pragma unroll
