@@ -379,7 +379,9 @@ int32_t bt_last_launch_count(const bt_ctx *ctx);
 /* Per-kernel timing for roofline accounting.  When enabled, every kernel launch is bracketed
    by a pair of CUDA events recorded on the launching stream.  bt_profile_read waits for the
    recorded events, and returns (and resets) the accumulated time in ms and the launch count
-   of kernel `kernel_id` (0 .. bt_profile_kernels()-1) since the previous read. */
+   of kernel `kernel_id` (0 .. bt_profile_kernels()-1) since the previous read.  on: 0 off,
+   1 every kernel, 2 + kernel_id only that kernel's launches (the others run unbracketed, so the
+   overlap of the streams is perturbed less); BT_EINVAL outside [0, 2 + bt_profile_kernels()). */
 bt_status bt_profile_enable(bt_ctx *ctx, int32_t on);
 int32_t bt_profile_kernels(void);
 const char *bt_profile_name(int32_t kernel_id);

@@ -339,9 +339,15 @@ class Context:
         self._check(lib().bt_set_record_peers(self._h, len(ptrs), arr, int(row_offset), int(rows)),
                     "bt_set_record_peers")
 
-    def profile(self, on: bool = True):
-        """Bracket every kernel launch with CUDA events on its stream (bt_profile_enable)."""
-        self._check(lib().bt_profile_enable(self._h, 1 if on else 0), "bt_profile_enable")
+    def profile(self, on: bool = True, only: str | None = None):
+        """Bracket every kernel launch with CUDA events on its stream (bt_profile_enable); with
+        `only` (a kernel name of profile_read) just that kernel's launches."""
+        code = 1 if on else 0
+        if on and only is not None:
+            L = lib()
+            names = [L.bt_profile_name(k).decode() for k in range(L.bt_profile_kernels())]
+            code = 2 + names.index(only)
+        self._check(lib().bt_profile_enable(self._h, code), "bt_profile_enable")
 
     def profile_read(self) -> dict:
         """{kernel name: (total ms, launches)} since the previous read (waits for the events)."""

@@ -28,6 +28,7 @@ struct bt_ctx {
   // per-kernel event timing (bt_profile_*)
   struct Pending { int kid; cudaEvent_t start, stop; };
   bool prof_on = false;
+  int prof_only = -1;                         // >= 0: bracket only this kernel bucket's launches
   std::vector<cudaEvent_t> ev_pool;
   std::vector<Pending> pending;
   double prof_ms[bt::K_COUNT] = {0};
@@ -930,6 +931,7 @@ static cudaEvent_t take_event(bt_ctx *c) {
 
 static void prof_hook(void *user, int kid, int phase, cudaStream_t s) {
   bt_ctx *c = (bt_ctx *)user;
+  if (c->prof_only >= 0 && kid != c->prof_only) return;
   cudaEvent_t e = take_event(c);
   cudaEventRecord(e, s);
   if (phase == 0) c->pending.push_back({kid, e, nullptr});
@@ -938,7 +940,9 @@ static void prof_hook(void *user, int kid, int phase, cudaStream_t s) {
 
 bt_status bt_profile_enable(bt_ctx *c, int32_t on) {
   BT_CHECK_CTX(c);
+  if (on < 0 || on >= 2 + bt::K_COUNT) return fail(c, BT_EINVAL, "bt_profile_enable: on = %d", on);
   c->prof_on = on != 0;
+  c->prof_only = on >= 2 ? on - 2 : -1;
   c->launch.hook = c->prof_on ? prof_hook : nullptr;
   c->launch.user = c;
   return BT_OK;
