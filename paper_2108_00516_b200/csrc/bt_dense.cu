@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "bt_internal.cuh"
 #include "bt_tc.cuh"
@@ -363,12 +364,14 @@ struct Gather {
 };
 
 // project entry k of the staged chunk with T = T_j T_i^-1 and issue its target gathers
+// (kCheck false: the caller guarantees k < n)
+template <bool kCheck = true>
 __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, const float (&T)[12], float fx, float fy,
                                              float cx, float cy, int W, int H, const uint8_t *vm, const float *pm,
                                              Gather &G) {
   // straight-line (no branches between the gathers of consecutive entries): out-of-range
   // entries and failed projections are predicated off through tj = -1
-  const float4 a = sP[k < n ? k : 0];
+  const float4 a = sP[!kCheck || k < n ? k : 0];
   const float yx = fmaf(T[0], a.x, fmaf(T[1], a.y, fmaf(T[2], a.z, T[9])));
   const float yy = fmaf(T[3], a.x, fmaf(T[4], a.y, fmaf(T[5], a.z, T[10])));
   const float yz = fmaf(T[6], a.x, fmaf(T[7], a.y, fmaf(T[8], a.z, T[11])));
@@ -377,7 +380,7 @@ __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, con
   // nearest pixel (R14): floor(x + 0.5) as one F2I.FLOOR (saturating: far-off projections fail
   // the unsigned range test like the float one)
   const int xu = __float2int_rd(up + 0.5f), xv = __float2int_rd(vp + 0.5f);
-  const bool ok = k < n && yz > 0.f && (unsigned)xu < (unsigned)W && (unsigned)xv < (unsigned)H;
+  const bool ok = (!kCheck || k < n) && yz > 0.f && (unsigned)xu < (unsigned)W && (unsigned)xv < (unsigned)H;
   const int tj = ok ? xv * W + xu : -1;
   const int tt = tj < 0 ? 0 : tj;                                  // validity and map entry together
   G.in = tj >= 0;
@@ -531,9 +534,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
       // same straight-line code with w = rho = 0 and zeroed map values (stale map words of
       // invalid pixels never reach the arithmetic), so the scheduler keeps the gathers of the
       // next entries in flight across it; accepted items compute exactly as before
-      auto consume = [&](const Gather &G, int k0) {
+      auto consume = [&](const Gather &G, int k0, auto checked) {
         const bool hit = G.in && G.vb != 0u;
-        const int k = k0 < n ? k0 : 0;                             // tail: any staged entry (masked)
+        const int k = !decltype(checked)::value || k0 < n ? k0 : 0;   // tail: any staged entry (masked)
         // no select on the gathered words: a rejected item reads either pixel 0's entry or an
         // invalid pixel's — the map region sits at a fixed offset, zeroed by bt_reserve and only
         // ever written with finite map entries, so its words are finite and w = rho = 0 cancel them
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         acc[27] += rho;
         acc[28] += acc_ok ? 1.f : 0.f;
         if constexpr (kAssoc) {
-          if (k0 < n) {
+          if (!decltype(checked)::value || k0 < n) {
             const int uv = __float_as_int(a.w);
             A.assoc[(size_t)e * npx + (size_t)(uv >> 16) * W + (uv & 0xffff)] = acc_ok ? G.tj : -1;
           }
@@ -594,13 +597,26 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
       Gather GA, GB, GC;
       issue_gather(sP, lane, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
       issue_gather(sP, lane + 32, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GB);
-      for (int k = lane; k < n; k += 96) {
+      // while every lane's six items of an iteration are inside the chunk (warp-uniform bound),
+      // the range checks are compiled out; the tail iterations keep them
+      const std::true_type chk;
+      const std::false_type nochk;
+      int k = lane;
+      for (; k - lane + 31 + 128 < n; k += 96) {
+        issue_gather<false>(sP, k + 64, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GC);
+        consume(GA, k, nochk);
+        issue_gather<false>(sP, k + 96, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
+        consume(GB, k + 32, nochk);
+        issue_gather<false>(sP, k + 128, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GB);
+        consume(GC, k + 64, nochk);
+      }
+      for (; k < n; k += 96) {
         issue_gather(sP, k + 64, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GC);
-        consume(GA, k);
+        consume(GA, k, chk);
         issue_gather(sP, k + 96, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
-        consume(GB, k + 32);
+        consume(GB, k + 32, chk);
         issue_gather(sP, k + 128, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GB);
-        consume(GC, k + 64);
+        consume(GC, k + 64, chk);
       }
       // warp transpose reduction: lane l ends with the warp total of acc[l]
 #pragma unroll
