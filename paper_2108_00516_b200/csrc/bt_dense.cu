@@ -375,7 +375,10 @@ __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, con
   const float yx = fmaf(T[0], a.x, fmaf(T[1], a.y, fmaf(T[2], a.z, T[9])));
   const float yy = fmaf(T[3], a.x, fmaf(T[4], a.y, fmaf(T[5], a.z, T[10])));
   const float yz = fmaf(T[6], a.x, fmaf(T[7], a.y, fmaf(T[8], a.z, T[11])));
-  const float iz = __fdividef(1.0f, yz);
+  // 1 / z as one MUFU.RCP (what __fdividef(1, z) computes for a normal z, without its
+  // denormal-range fix-up: a projection with z <= 0 or a far-off pixel fails the tests below)
+  float iz;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(iz) : "f"(yz));
   const float up = fmaf(fx * yx, iz, cx), vp = fmaf(fy * yy, iz, cy);
   // nearest pixel (R14): floor(x + 0.5) as one F2I.FLOOR (saturating: far-off projections fail
   // the unsigned range test like the float one)
