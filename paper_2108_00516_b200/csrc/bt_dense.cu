@@ -31,7 +31,8 @@
 //                 edge)).
 //                 Per (entry, edge): fp32 projection, gather of the target validity + map entry,
 //                 fp64 residual difference then fp32 gates / Huber, 29 running sums.
-//  k_dense_reduce fixed-order fp64 sum of the per-tile partials of an edge (deterministic).
+//  k_dense_reduce fixed-order fp64 sum of the per-tile partials of an edge (deterministic), then
+//                 the object-frame blocks to camera i: H = M H_o M^T, g = M g_o (reading R32).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -474,12 +475,11 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         }
       }
     }
-    float Rf[9];                                                   // R_i as given (fp32)
     {
       const bt_pose P = A.node_pose[f];
       double Rd[9], Ri[9];                                         // R_i and its exact inverse (fp64)
 #pragma unroll
-      for (int k = 0; k < 9; ++k) { Rf[k] = P.R[k]; Rd[k] = P.R[k]; }
+      for (int k = 0; k < 9; ++k) Rd[k] = P.R[k];
       {
         const double c0 = Rd[4] * Rd[8] - Rd[5] * Rd[7], c1 = Rd[5] * Rd[6] - Rd[3] * Rd[8],
                      c2 = Rd[3] * Rd[7] - Rd[4] * Rd[6];
@@ -558,17 +558,18 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         const float D1 = (g[1] - yh.y) + fmaf(ls1, kLoInv, -yl.y);
         const float D2 = (g[2] - yh.z) + fmaf(ls2, kLoInv, -yl.z);
         const float mj0 = g[3], mj1 = g[4], mj2 = g[5];
-        const float dq0 = fmaf(Rf[0], D0, fmaf(Rf[1], D1, Rf[2] * D2));
-        const float dq1 = fmaf(Rf[3], D0, fmaf(Rf[4], D1, Rf[5] * D2));
-        const float dq2 = fmaf(Rf[6], D0, fmaf(Rf[7], D1, Rf[8] * D2));
-        const float dist2 = fmaf(dq0, dq0, fmaf(dq1, dq1, dq2 * dq2));
-        const float4 nc = sN[k];
-        const float c = fmaf(nc.w, mj0, fmaf(yh.w, mj1, yl.w * mj2));
+        // everything in the object frame (reading R32): q - p = R_i D, so r = n_i . (R_i D) =
+        // (R_i^T n_i) . D = n_o,i . D exactly, |q - p|^2 = |D|^2 for the (orthonormal to fp32
+        // rounding) R_i — a ~1e-7 relative difference, far inside the gate's band (R22) — and
+        // J = [n_i, q x n_i] = M_i [n_o,i, x_s x n_o,i] with the per-frame 6 x 6
+        // M_i = [[R_i, 0], [[t_i]x R_i, R_i]]: the blocks are accumulated with J_o and rotated
+        // once per edge, in fp64, by k_dense_reduce (no per-item rotation of D, no q)
+        const float dist2 = fmaf(D0, D0, fmaf(D1, D1, D2 * D2));
+        const float o0 = sN[k].w, o1 = yh.w, o2 = yl.w;            // n_o,i
+        const float c = fmaf(o0, mj0, fmaf(o1, mj1, o2 * mj2));
         const bool acc_ok = hit && dist2 < A.gate2f && c > A.cos_gate;
-        const float n0 = nc.x, n1 = nc.y, n2 = nc.z;
-        const float r = fmaf(n0, dq0, fmaf(n1, dq1, n2 * dq2));
-        const float4 a = sP[k];
-        const float qx = a.x + dq0, qy = a.y + dq1, qz = a.z + dq2;
+        const float r = fmaf(o0, D0, fmaf(o1, D1, o2 * D2));
+        const float xs0 = g[0], xs1 = g[1], xs2 = g[2];             // x_s (hi): the target point, object frame
         const float ar = fabsf(r);
         // Huber (R17) without branches: with m = min(|r|, h), rho = m (|r| - m / 2) is 0.5 r^2
         // inside and h (|r| - h / 2) beyond (the same roundings as the two formulas); the weight
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(ar));
         const float w = acc_ok ? (ar <= A.huber ? 1.f : A.huber * rcp) : 0.f;
         const float rho = acc_ok ? m * fmaf(-0.5f, m, ar) : 0.f;
-        const float J[6] = {n0, n1, n2, qy * n2 - qz * n1, qz * n0 - qx * n2, qx * n1 - qy * n0};
+        const float J[6] = {o0, o1, o2, xs1 * o2 - xs2 * o1, xs2 * o0 - xs0 * o2, xs0 * o1 - xs1 * o0};
         int q = 0;
 #pragma unroll
         for (int aa = 0; aa < 6; ++aa) {
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         acc[28] += acc_ok ? 1.f : 0.f;
         if constexpr (kAssoc) {
           if (!decltype(checked)::value || k0 < n) {
-            const int uv = __float_as_int(a.w);
+            const int uv = __float_as_int(sP[k].w);
             A.assoc[(size_t)e * npx + (size_t)(uv >> 16) * W + (uv & 0xffff)] = acc_ok ? G.tj : -1;
           }
         }
@@ -638,11 +639,13 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
 }
 
 __global__ void __launch_bounds__(256) k_dense_reduce(const float *__restrict__ partials, const int32_t *__restrict__ nch,
-                                                       int tiles, const int32_t *edges, const int32_t *pairs, float *out,
+                                                       int tiles, const int32_t *edges, const int32_t *pairs,
+                                                       const bt_pose *node_pose, float *out,
                                                        int out_stride, uint32_t *records, int rec_stride, int off_ij,
                                                        int off_ji, PeerRec peers) {
   pdl_wait();
   __shared__ double wsum[8][32];
+  __shared__ double Ho[6][6], go[6], Mi[6][6];
   const int e = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int fi, fj;
@@ -656,7 +659,43 @@ __global__ void __launch_bounds__(256) k_dense_reduce(const float *__restrict__ 
   double tsum = 0.0;
 #pragma unroll
   for (int w = 0; w < 8; ++w) tsum += wsum[w][lane];
-  const float v = lane < kAcc ? (float)tsum : 0.f;
+  // the object-frame blocks (J_o = [n_o, x_s x n_o]) to the camera frame of frame i (reading
+  // R32): H = M Ho M^T, g = M go, with M = [[R, 0], [[t]x R, R]] of T_i — fp64, once per edge
+  {
+    int a = 0, b = 0, q = lane;
+    if (q < 21) { while (q >= 6 - a) { q -= 6 - a; ++a; } b = a + q; Ho[a][b] = tsum; Ho[b][a] = tsum; }
+    else if (lane < 27) go[lane - 21] = tsum;
+    if (lane < 9) {
+      const bt_pose P = node_pose[fi];
+      const int r = lane / 3, c = lane % 3;
+      const double R_rc = P.R[3 * r + c];
+      const double t0 = P.t[0], t1 = P.t[1], t2 = P.t[2];
+      // ([t]x R)[r][c] = sum_k [t]x[r][k] R[k][c]
+      const double tx[3][3] = {{0.0, -t2, t1}, {t2, 0.0, -t0}, {-t1, t0, 0.0}};
+      double v = 0.0;
+      for (int k = 0; k < 3; ++k) v += tx[r][k] * (double)P.R[3 * k + c];
+      Mi[r][c] = R_rc; Mi[r][3 + c] = 0.0; Mi[3 + r][c] = v; Mi[3 + r][3 + c] = R_rc;
+    }
+  }
+  __syncwarp();
+  double outv = tsum;
+  if (lane < 21) {
+    int a = 0, q = lane;
+    while (q >= 6 - a) { q -= 6 - a; ++a; }
+    const int b = a + q;
+    double h = 0.0;
+    for (int c = 0; c < 6; ++c) {
+      double mh = 0.0;
+      for (int d = 0; d < 6; ++d) mh += Ho[c][d] * Mi[b][d];
+      h += Mi[a][c] * mh;
+    }
+    outv = h;
+  } else if (lane < 27) {
+    double gg = 0.0;
+    for (int c = 0; c < 6; ++c) gg += Mi[lane - 21][c] * go[c];
+    outv = gg;
+  }
+  const float v = lane < kAcc ? (float)outv : 0.f;
   if (records) {
     const int p = e >> 1;
     records[(size_t)p * rec_stride + ((e & 1) ? off_ji : off_ij) + lane] = __float_as_uint(v);
@@ -757,7 +796,7 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   launch_pdl(kd, grid, kEdgeThreads, smem, s, a);
   L.end(K_DENSE, s);
   L.begin(K_DENSE_REDUCE, s);
-  launch_pdl(k_dense_reduce, E, 256, 0, s, a.partials, a.nch, a.tiles, edges, pairs, out, out_stride, records,
+  launch_pdl(k_dense_reduce, E, 256, 0, s, a.partials, a.nch, a.tiles, edges, pairs, a.node_pose, out, out_stride, records,
              rec_stride, rec_off_ij, rec_off_ji, peers ? *peers : PeerRec{});
   L.end(K_DENSE_REDUCE, s);
 }
