@@ -381,11 +381,23 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
       c->rs.fmap = &c->tmap_feat;
     }
   }
-  // the dense map region (offset 0) starts zeroed and is only ever written with finite map
-  // entries: k_dense reads stale words of rejected items without a select
-  if (ok && dense_bytes > 0)
-    ok = cudaMalloc(&c->dense, dense_bytes) == cudaSuccess &&
-         cudaMemset(c->dense, 0, (size_t)mframes * width * height * 32) == cudaSuccess;
+  // the dense scratch's header (call counter / map-entry epoch, offset 0) and map region (offset
+  // 256) start zeroed — epoch 0 is never a call's, so no entry is valid — and the maps are only
+  // ever written with finite entries: k_dense reads stale words of rejected items without a
+  // select.  Header word 2: the reserved map entries (cleared when the epochs wrap).
+  if (ok && dense_bytes > 0) {
+    const size_t map_entries = (size_t)mframes * width * height;
+    const uint32_t hdr2 = (uint32_t)map_entries;
+    ok = map_entries < 0xFFFFFFFFull && cudaMalloc(&c->dense, dense_bytes) == cudaSuccess &&
+         cudaMemset(c->dense, 0, 256 + map_entries * 32) == cudaSuccess &&
+         cudaMemcpy((char *)c->dense + 8, &hdr2, 4, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok) {
+      if (const char *e0 = getenv("BT_DENSE_EPOCH0")) {           // tests: start near the epoch wrap
+        const uint32_t v = (uint32_t)strtoul(e0, nullptr, 10);
+        ok = cudaMemcpy(c->dense, &v, 4, cudaMemcpyHostToDevice) == cudaSuccess;
+      }
+    }
+  }
   if (ok) ok = cudaMalloc(&c->graph, bt::graph_scratch_bytes(mframes, max_pairs)) == cudaSuccess;
   if (ok && max_frames > 0) {
     const size_t FN = (size_t)max_frames * n_max, FP = (size_t)max_frames * width * height;

@@ -18,8 +18,8 @@
 //  k_dense_prep   one CTA per (frame, 32x32 tile): coalesced vector reads (uchar4 mask,
 //                 float4 depth, 3 x float4 normals) of 4 pixels per thread; per valid pixel the
 //                 fp64 object-frame point and fp32 object-frame normal go to a per-frame map
-//                 (gathered as a TARGET), a validity byte is written for every pixel, and a
-//                 block scan compacts the tile's valid source pixels (pixel order, stride
+//                 (gathered as a TARGET) tagged with the call's epoch (the tag is the pixel's
+//                 validity: no per-pixel validity map), and a block scan compacts the tile's valid source pixels (pixel order, stride
 //                 applied) into 32-byte entries.
 //  k_dense_scan   one CTA per frame: exclusive scan of the tile counts, so the frame's valid
 //                 source pixels form one compacted sequence cut into chunks of kTile entries.
@@ -29,7 +29,8 @@
 //                 every edge leaving the frame; each warp owns whole edges (gathers pipelined
 //                 two entries ahead in three fixed slots, one transpose reduction per (warp,
 //                 edge)).
-//                 Per (entry, edge): fp32 projection, gather of the target validity + map entry,
+//                 Per (entry, edge): fp32 projection, gather of the target's map entry (valid iff
+//                 it carries this call's epoch),
 //                 fp64 residual difference then fp32 gates / Huber, 29 running sums.
 //  k_dense_reduce fixed-order fp64 sum of the per-tile partials of an edge (deterministic), then
 //                 the object-frame blocks to camera i: H = M H_o M^T, g = M g_o (reading R32).
@@ -63,7 +64,8 @@ constexpr float kLoInv = 5.9604644775390625e-08f;  // 2^-24
 struct __align__(32) MapEntry {                // 32 bytes (one sector, one 256-bit load), per valid pixel
   float x, y, z;                              // hi parts of x_s (object frame)
   float nx, ny, nz;                           // object-frame normal
-  __half lx, ly, lz, pad;                     // lo parts * 2^24
+  __half lx, ly, lz;                          // lo parts * 2^24
+  unsigned short epoch;                       // the call that wrote it (valid iff == this call's)
 };
 
 struct DenseArgs {
@@ -83,8 +85,9 @@ struct DenseArgs {
   int32_t *counts;            // [F][tiles]
   int32_t *offs;              // [F][tiles + 1] exclusive scan of counts (entries of frame f before tile t)
   int32_t *nch;               // [F] chunks of kTile compacted entries (0 if the frame has no outgoing edge)
-  MapEntry *pmap;             // [F][H*W]
-  uint8_t *vmap;              // [F][H*W]
+  MapEntry *pmap;             // [F][H*W]: valid pixels' entries, tagged with the call's epoch
+  uint32_t *hdr;              // [0] call counter (epoch = low 16 bits, never 0), [1] wrap flag,
+                              // [2] map entries reserved (bt_reserve); zeroed with the maps
   int32_t *tlist;             // [F * tiles] masked tiles (f * tiles + t), k_dense_mask -> k_dense_prep
   int32_t *tcount;            // [1] list length (zeroed by k_edge_setup)
   float *partials;            // [E][tiles][32] (per chunk of the edge's source frame; chunks <= tiles)
@@ -104,7 +107,16 @@ __device__ __forceinline__ void edge_frames(const int32_t *edges, const int32_t 
 // of outgoing edges (deterministic ballot compaction); blocks F.. compute T_j T_i^-1 per edge
 __global__ void __launch_bounds__(256) k_edge_setup(DenseArgs A) {
   pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x == 0) *A.tcount = 0;          // k_dense_mask's work list
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *A.tcount = 0;                                                 // k_dense_mask's work list
+    // this call's epoch: a map entry is a valid target iff it carries it, so no per-pixel
+    // validity map is written or gathered; every 65535 calls the tags wrap and the maps are
+    // cleared (k_dense_mask) before any entry is written
+    uint32_t e = A.hdr[0] + 1;
+    if ((e & 0xFFFFu) == 0u) ++e;
+    A.hdr[0] = e;
+    A.hdr[1] = (e & 0xFFFFu) == 1u && e > 1u;
+  }
   if ((int)blockIdx.x >= A.mp.n_frames) {
     const int e = (blockIdx.x - A.mp.n_frames) * blockDim.x + threadIdx.x;
     if (e >= A.E) return;
@@ -152,7 +164,7 @@ __global__ void __launch_bounds__(256) k_edge_setup(DenseArgs A) {
 // map entry of one valid pixel: x = R^T (p - t) in fp64 from the exact inputs (stored hi + lo,
 // reading R26), n_o = R^T n
 __device__ __forceinline__ void write_map_entry(const DenseArgs &A, const bt_pose &P, MapEntry *dst, int u, int v,
-                                                float dep, float n0, float n1, float n2) {
+                                                float dep, float n0, float n1, float n2, unsigned epoch) {
   const double d = dep;
   const double p0 = ((double)u - A.cxd) * d * A.ifxd - P.t[0];
   const double p1 = ((double)v - A.cyd) * d * A.ifyd - P.t[1];
@@ -165,7 +177,7 @@ __device__ __forceinline__ void write_map_entry(const DenseArgs &A, const bt_pos
   me.lx = __double2half((X0 - (double)me.x) * kLoScale);
   me.ly = __double2half((X1 - (double)me.y) * kLoScale);
   me.lz = __double2half((X2 - (double)me.z) * kLoScale);
-  me.pad = __float2half(0.f);
+  me.epoch = (unsigned short)epoch;
   const double m0 = n0, m1 = n1, m2 = n2;
   me.nx = (float)(P.R[0] * m0 + P.R[3] * m1 + P.R[6] * m2);
   me.ny = (float)(P.R[1] * m0 + P.R[4] * m1 + P.R[7] * m2);
@@ -174,7 +186,7 @@ __device__ __forceinline__ void write_map_entry(const DenseArgs &A, const bt_pos
 }
 
 // one masked 32x32 tile, 4 pixels per thread (CTA-uniform call)
-__device__ __forceinline__ void prep_tile(const DenseArgs &A, const int f, const int t, int *wsum) {
+__device__ __forceinline__ void prep_tile(const DenseArgs &A, const int f, const int t, int *wsum, unsigned epoch) {
   const int W = A.mp.W, H = A.mp.H, npx = W * H;
   const int ty = t / A.tx, tx = t - ty * A.tx;
   const int row = threadIdx.x >> 3, col0 = (threadIdx.x & 7) * 4;
@@ -218,19 +230,11 @@ __device__ __forceinline__ void prep_tile(const DenseArgs &A, const int f, const
 #pragma unroll
   for (int k = 0; k < kPer; ++k)
     vv[k] = in[k] && dep[k] > 0.f && !(nr[3 * k] == 0.f && nr[3 * k + 1] == 0.f && nr[3 * k + 2] == 0.f);
-  if (v < H) {
-    if ((W & 3) == 0 && u0 + kPer <= W)
-      *reinterpret_cast<uchar4 *>(A.vmap + off + pix0) = make_uchar4(vv[0], vv[1], vv[2], vv[3]);
-    else
-#pragma unroll
-      for (int k = 0; k < kPer; ++k)
-        if (u0 + k < W) A.vmap[off + pix0 + k] = vv[k] ? 1 : 0;
-  }
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     const int u = u0 + k;
     const bool valid = vv[k];
-    if (valid) write_map_entry(A, P, A.pmap + off + pix0 + k, u, v, dep[k], nr[3 * k], nr[3 * k + 1], nr[3 * k + 2]);
+    if (valid) write_map_entry(A, P, A.pmap + off + pix0 + k, u, v, dep[k], nr[3 * k], nr[3 * k + 1], nr[3 * k + 2], epoch);
     src[k] = valid && (A.stride <= 1 || (u % A.stride == 0 && v % A.stride == 0));
     n_mine += src[k];
   }
@@ -270,10 +274,11 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
   pdl_wait();
   __shared__ int wsum[kDenseThreads / 32];
   const int n_work = *A.tcount;
+  const unsigned epoch = A.hdr[0] & 0xFFFFu;
   for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
     __syncthreads();                                                 // wsum of the previous tile read
     const int f = A.tlist[w] / A.tiles, t = A.tlist[w] - f * A.tiles;
-    prep_tile(A, f, t, wsum);
+    prep_tile(A, f, t, wsum, epoch);
   }
 }
 
@@ -281,11 +286,17 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_prep(DenseArgs A) {
 // Masked-tile classification, warp per 32x32 tile (8 tiles per CTA): lane r reads row r of the
 // tile's mask as two 16-B vectors, so a whole tile is 2 loads per lane (the mask pass is ~85 %
 // of the frame and was latency-bound at one 4-B load per thread).  A tile without a masked
-// pixel is finished here (validity bytes 0, no source entries); the others are appended to a
+// pixel is finished here (no source entries, no map entries); the others are appended to a
 // work list (slot order is irrelevant: each tile writes only its own outputs) that the
 // persistent k_dense_prep drains with 256 threads per tile.
 __global__ void __launch_bounds__(kDenseThreads) k_dense_mask(DenseArgs A) {
   pdl_wait();
+  if (A.hdr[1]) {                                                  // epoch wrap: clear every reserved entry
+    const size_t n = (size_t)A.hdr[2] * 2, st = (size_t)gridDim.x * gridDim.y * blockDim.x;
+    uint4 *m = reinterpret_cast<uint4 *>(A.pmap);
+    for (size_t i = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += st)
+      m[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int f = blockIdx.y, t = blockIdx.x * (kDenseThreads / 32) + warp;
   if (t >= A.tiles) return;                                        // warp-uniform
@@ -305,15 +316,6 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_mask(DenseArgs A) {
     }
   }
   if (__ballot_sync(0xffffffffu, any) == 0u) {
-    if (v < H) {
-      if (full) {
-        uint4 *o = reinterpret_cast<uint4 *>(A.vmap + row);
-        o[0] = make_uint4(0u, 0u, 0u, 0u);
-        o[1] = make_uint4(0u, 0u, 0u, 0u);
-      } else {
-        for (int u = u0; u < min(W, u0 + kTS); ++u) A.vmap[row + (u - u0)] = 0;
-      }
-    }
     if (lane == 0) A.counts[(size_t)f * A.tiles + t] = 0;
   } else if (lane == 0) {
     A.tlist[atomicAdd(A.tcount, 1)] = f * A.tiles + t;
@@ -358,8 +360,7 @@ constexpr int kEdgeThreads = 256;                // k_dense CTA (8 warps, each o
 
 // target-pixel gather of one (entry, edge) item, issued ahead of its use
 struct Gather {
-  float g[8];                 // one 32-B map entry: x_s hi, n_o,j, x_s lo (fp16 x 3)
-  unsigned vb;                // target validity byte (tested only when consumed: the load stays in flight)
+  float g[8];                 // one 32-B map entry: x_s hi, n_o,j, x_s lo (fp16 x 3), epoch tag
   bool in;                    // projected into the frame
   int tj;                     // target pixel index (read only by the association output)
 };
@@ -368,8 +369,7 @@ struct Gather {
 // (kCheck false: the caller guarantees k < n)
 template <bool kCheck = true>
 __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, const float (&T)[12], float fx, float fy,
-                                             float cx, float cy, int W, int H, const uint8_t *vm, const float *pm,
-                                             Gather &G) {
+                                             float cx, float cy, int W, int H, const float *pm, Gather &G) {
   // straight-line (no branches between the gathers of consecutive entries): out-of-range
   // entries and failed projections are predicated off through tj = -1
   const float4 a = sP[!kCheck || k < n ? k : 0];
@@ -386,10 +386,9 @@ __device__ __forceinline__ void issue_gather(const float4 *sP, int k, int n, con
   const int xu = __float2int_rd(up + 0.5f), xv = __float2int_rd(vp + 0.5f);
   const bool ok = (!kCheck || k < n) && yz > 0.f && (unsigned)xu < (unsigned)W && (unsigned)xv < (unsigned)H;
   const int tj = ok ? xv * W + xu : -1;
-  const int tt = tj < 0 ? 0 : tj;                                  // validity and map entry together
+  const int tt = tj < 0 ? 0 : tj;                                  // the map entry (its tag = validity)
   G.in = tj >= 0;
   G.tj = tj;
-  G.vb = __ldg(vm + tt);
   asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
       : "=f"(G.g[0]), "=f"(G.g[1]), "=f"(G.g[2]), "=f"(G.g[3]), "=f"(G.g[4]), "=f"(G.g[5]), "=f"(G.g[6]),
         "=f"(G.g[7])
@@ -419,6 +418,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
   const int F = A.mp.n_frames;
   const int W = A.mp.W, H = A.mp.H, npx = W * H;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned epoch = A.hdr[0] & 0xFFFFu;                      // this call's map-entry tag
   __shared__ __align__(8) uint64_t bar_e;                           // the chunk's bulk copies landed
   if (threadIdx.x == 0) {
     mbar_init(&bar_e, 1);
@@ -526,7 +526,6 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
 #pragma unroll
       for (int q = 0; q < 12; ++q) T[q] = __ldg(A.tji + 12 * e + q);
       const size_t off_j = (size_t)fj * npx;
-      const uint8_t *vm = A.vmap + off_j;
       const float *pm = reinterpret_cast<const float *>(A.pmap + off_j);
       float acc[32];
 #pragma unroll
@@ -538,11 +537,12 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
       // invalid pixels never reach the arithmetic), so the scheduler keeps the gathers of the
       // next entries in flight across it; accepted items compute exactly as before
       auto consume = [&](const Gather &G, int k0, auto checked) {
-        const bool hit = G.in && G.vb != 0u;
+        const bool hit = G.in && (__float_as_uint(G.g[7]) >> 16) == epoch;   // a valid target of this call
         const int k = !decltype(checked)::value || k0 < n ? k0 : 0;   // tail: any staged entry (masked)
         // no select on the gathered words: a rejected item reads either pixel 0's entry or an
-        // invalid pixel's — the map region sits at a fixed offset, zeroed by bt_reserve and only
-        // ever written with finite map entries, so its words are finite and w = rho = 0 cancel them
+        // invalid pixel's (a stale entry of an earlier call, or zeros) — the map region sits at a
+        // fixed offset, zeroed by bt_reserve and only ever written with finite map entries, so
+        // its words are finite and w = rho = 0 cancel them
         const float *g = G.g;
         // q - p = R_i x_s - (p - t_i) = R_i (x_s - y_p), y_p = R_i^-1 (p - t_i) (exact algebra
         // for the fp32 R_i as given, reading R26).  x_s - y_p cancels ~0.1 m coordinates: with
@@ -599,27 +599,27 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_dense(DenseArgs A) {
         }
       };
       Gather GA, GB, GC;
-      issue_gather(sP, lane, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
-      issue_gather(sP, lane + 32, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GB);
+      issue_gather(sP, lane, n, T, A.fx, A.fy, A.cx, A.cy, W, H, pm, GA);
+      issue_gather(sP, lane + 32, n, T, A.fx, A.fy, A.cx, A.cy, W, H, pm, GB);
       // while every lane's six items of an iteration are inside the chunk (warp-uniform bound),
       // the range checks are compiled out; the tail iterations keep them
       const std::true_type chk;
       const std::false_type nochk;
       int k = lane;
       for (; k - lane + 31 + 128 < n; k += 96) {
-        issue_gather<false>(sP, k + 64, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GC);
+        issue_gather<false>(sP, k + 64, n, T, A.fx, A.fy, A.cx, A.cy, W, H, pm, GC);
         consume(GA, k, nochk);
-        issue_gather<false>(sP, k + 96, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
+        issue_gather<false>(sP, k + 96, n, T, A.fx, A.fy, A.cx, A.cy, W, H, pm, GA);
         consume(GB, k + 32, nochk);
-        issue_gather<false>(sP, k + 128, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GB);
+        issue_gather<false>(sP, k + 128, n, T, A.fx, A.fy, A.cx, A.cy, W, H, pm, GB);
         consume(GC, k + 64, nochk);
       }
       for (; k < n; k += 96) {
-        issue_gather(sP, k + 64, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GC);
+        issue_gather(sP, k + 64, n, T, A.fx, A.fy, A.cx, A.cy, W, H, pm, GC);
         consume(GA, k, chk);
-        issue_gather(sP, k + 96, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GA);
+        issue_gather(sP, k + 96, n, T, A.fx, A.fy, A.cx, A.cy, W, H, pm, GA);
         consume(GB, k + 32, chk);
-        issue_gather(sP, k + 128, n, T, A.fx, A.fy, A.cx, A.cy, W, H, vm, pm, GB);
+        issue_gather(sP, k + 128, n, T, A.fx, A.fy, A.cx, A.cy, W, H, pm, GB);
         consume(GC, k + 64, chk);
       }
       // warp transpose reduction: lane l ends with the warp total of acc[l]
@@ -732,7 +732,7 @@ size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H) {
   const size_t tiles = dense_tiles(W, H), F = max_frames, npx = (size_t)W * H;
   return align256(F * tiles * kTile * 32) + align256(F * tiles * 4) + align256(F * (tiles + 1) * 4) + align256(F * 4) + align256((size_t)max_edges * tiles * kPartStride * 4) +
          align256((size_t)max_edges * 48) + align256(F * max_edges * 4) + align256(F * 4) +
-         align256(F * npx * sizeof(MapEntry)) + align256(F * npx) + align256(F * tiles * 4) + align256(4);
+         256 + align256(F * npx * sizeof(MapEntry)) + align256(F * tiles * 4) + align256(4);
 }
 
 void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
@@ -759,7 +759,8 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   // carve the scratch
   char *p = (char *)scratch;
   const size_t tiles = a.tiles, F = mp.n_frames, npx = (size_t)mp.W * mp.H;
-  a.pmap = (MapEntry *)p;    p += align256(F * npx * sizeof(MapEntry));   // offset 0: zeroed by bt_reserve
+  a.hdr = (uint32_t *)p;     p += 256;                                     // header + maps: zeroed by bt_reserve
+  a.pmap = (MapEntry *)p;    p += align256(F * npx * sizeof(MapEntry));
   a.entries = (float4 *)p;   p += align256(F * tiles * kTile * 32);
   a.counts = (int32_t *)p;   p += align256(F * tiles * 4);
   a.offs = (int32_t *)p;     p += align256(F * (tiles + 1) * 4);
@@ -768,7 +769,6 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   a.tji = (float *)p;        p += align256((size_t)E * 48);
   a.elist = (int32_t *)p;    p += align256(F * E * 4);
   a.ecount = (int32_t *)p;   p += align256(F * 4);
-  a.vmap = (uint8_t *)p;     p += align256(F * npx);
   a.tlist = (int32_t *)p;    p += align256(F * tiles * 4);
   a.tcount = (int32_t *)p;
   L.begin(K_DENSE_PREP, s);

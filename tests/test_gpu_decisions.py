@@ -218,3 +218,83 @@ def test_refit_degenerate_status(bt, torch, ctx):
         assert np.array_equal(r["T_refit"].view(np.uint32), r["T_best"].view(np.uint32))
         recs.append(r)
     assert len(recs) == 3
+
+
+def test_dense_map_epochs_stale_entries_and_wrap(bt, torch):
+    """k_dense decides a target pixel's validity by the epoch tag of its map entry (no validity
+    map): entries left by earlier calls on other frames must never count.  Two different scenes
+    alternate on one context, through the epoch wrap (BT_DENSE_EPOCH0 starts the call counter
+    three calls before it; the wrapping call clears every reserved entry): every call's dense
+    blocks equal those of a fresh context."""
+    import os
+    scenes = [synth.make_scene(4, seed=s) for s in (61, 62)]
+    pairs = synth.all_pairs(4)
+    eprm = bt.edge_params()
+
+    def dense(ctx, sc):
+        fb = bt.FrameBatch.from_scene(sc)
+        out = torch.zeros((2 * len(pairs), 32), dtype=torch.float32, device="cuda")
+        edges = np.concatenate([pairs, pairs[:, ::-1]], 0).astype(np.int32)
+        ctx.dense_corr(fb, sc.K, torch.from_numpy(sc.perturbed_poses(3)).cuda(),
+                       torch.from_numpy(np.ascontiguousarray(edges)).cuda(), eprm, out)
+        torch.cuda.synchronize()
+        return out.cpu().numpy()
+
+    want = []
+    for sc in scenes:
+        c = bt.Context(0)
+        c.reserve(len(pairs), 512, 256, 4, 640, 480)
+        want.append(dense(c, sc))
+        c.close()
+    assert not np.array_equal(want[0], want[1])
+    os.environ["BT_DENSE_EPOCH0"] = str(65536 - 3)
+    try:
+        c = bt.Context(0)
+        c.reserve(len(pairs), 512, 256, 4, 640, 480)
+    finally:
+        os.environ.pop("BT_DENSE_EPOCH0", None)
+    for k in range(8):                                  # epochs 65534, 65535, 1 (wrap), 2, ...
+        got = dense(c, scenes[k % 2])
+        assert np.array_equal(got, want[k % 2]), f"call {k}"
+    c.close()
+
+
+def test_dense_graph_replay_with_new_frames(bt, torch):
+    """A CUDA graph of bt_dense_corr captured once and replayed on new frame content (the same
+    device buffers, refilled): the epoch comes from device memory, bumped by every execution, so
+    map entries the previous replay wrote for pixels no longer valid are never targets — each
+    replay equals a fresh context's result for its frames."""
+    scenes = [synth.make_scene(4, seed=s) for s in (71, 72)]
+    pairs = synth.all_pairs(4)
+    edges = torch.from_numpy(np.ascontiguousarray(np.concatenate([pairs, pairs[:, ::-1]], 0).astype(np.int32))).cuda()
+    poses = torch.from_numpy(scenes[0].perturbed_poses(3)).cuda()
+    eprm = bt.edge_params()
+    want = []
+    for sc in scenes:
+        c = bt.Context(0)
+        c.reserve(len(pairs), 512, 256, 4, 640, 480)
+        fb = bt.FrameBatch.from_scene(sc)
+        o = torch.zeros((edges.shape[0], 32), dtype=torch.float32, device="cuda")
+        c.dense_corr(fb, sc.K, poses, edges, eprm, o)
+        torch.cuda.synchronize()
+        want.append(o.cpu().numpy())
+        c.close()
+    assert not np.array_equal(want[0], want[1])
+    c = bt.Context(0)
+    c.reserve(len(pairs), 512, 256, 4, 640, 480)
+    fb = bt.FrameBatch.from_scene(scenes[0])
+    out = torch.zeros((edges.shape[0], 32), dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    c.dense_corr(fb, scenes[0].K, poses, edges, eprm, out, stream=s)       # warm-up (attributes)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        c.dense_corr(fb, scenes[0].K, poses, edges, eprm, out, stream=s)
+    for k in range(4):
+        src = bt.FrameBatch.from_scene(scenes[k % 2])
+        for name in ("depth", "normal", "mask"):
+            getattr(fb, name).copy_(getattr(src, name))
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), want[k % 2]), f"replay {k}"
+    c.close()
