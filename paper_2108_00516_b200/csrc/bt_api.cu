@@ -36,6 +36,7 @@ struct bt_ctx {
   // capacity
   int cap_pairs = 0, cap_nmax = 0, cap_hyp = 0, cap_frames = 0, cap_w = 0, cap_h = 0, cap_stage = 0;
   size_t cap_dense = 0;                       // bytes of dense scratch
+  size_t dense_map_cap = 0;                   // dense map entries reserved (frames x pixels)
   // scratch
   void *match = nullptr;                      // matching scratch (bt::MatchScratch)
   bt::MatchScratch ms{};
@@ -387,6 +388,7 @@ bt_status bt_reserve(bt_ctx *c, int32_t max_pairs, int32_t n_max, int32_t max_hy
   // select.  Header word 2: the reserved map entries (cleared when the epochs wrap).
   if (ok && dense_bytes > 0) {
     const size_t map_entries = (size_t)mframes * width * height;
+    c->dense_map_cap = map_entries;
     const uint32_t hdr2 = (uint32_t)map_entries;
     ok = map_entries < 0xFFFFFFFFull && cudaMalloc(&c->dense, dense_bytes) == cudaSuccess &&
          cudaMemset(c->dense, 0, 256 + map_entries * 32) == cudaSuccess &&
@@ -462,7 +464,7 @@ bt_status bt_dense_corr(bt_ctx *c, const bt_maps *maps, const bt_intrinsics *K, 
   if (E == 0) return BT_OK;
   if ((s = check_dense_bytes(c, maps, E)) != BT_OK) return s;
   if (!node_pose || !edges || !out) return fail(c, BT_EINVAL, "bt_dense_corr: NULL buffer");
-  bt::launch_dense(mview(maps), *K, node_pose, edges, nullptr, E, *prm, c->dense, out, 32, nullptr, 0, 0, 0,
+  bt::launch_dense(mview(maps), *K, node_pose, edges, nullptr, E, *prm, c->dense, c->dense_map_cap, out, 32, nullptr, 0, 0, 0,
                    (cudaStream_t)stream, c->launch);
   return after_launch(c, "bt_dense_corr");
 }
@@ -479,7 +481,7 @@ bt_status bt_dense_assoc(bt_ctx *c, const bt_maps *maps, const bt_intrinsics *K,
   if (E == 0) return BT_OK;
   if ((s = check_dense_bytes(c, maps, E)) != BT_OK) return s;
   if (!node_pose || !edges || !out || !assoc) return fail(c, BT_EINVAL, "bt_dense_assoc: NULL buffer");
-  bt::launch_dense(mview(maps), *K, node_pose, edges, nullptr, E, *prm, c->dense, out, 32, nullptr, 0, 0, 0,
+  bt::launch_dense(mview(maps), *K, node_pose, edges, nullptr, E, *prm, c->dense, c->dense_map_cap, out, 32, nullptr, 0, 0, 0,
                    (cudaStream_t)stream, c->launch, assoc);
   return after_launch(c, "bt_dense_assoc");
 }
@@ -503,7 +505,7 @@ static bt_status register_pairs_dev(bt_ctx *c, const bt_keypoints *kp, const bt_
     cudaEventRecord(c->ev_fork, st);
     cudaStreamWaitEvent(c->side, c->ev_fork, 0);
     if (ms != st) cudaStreamWaitEvent(ms, c->ev_fork, 0);
-    bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, nullptr, 0, records, rw,
+    bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, c->dense_map_cap, nullptr, 0, records, rw,
                      bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch, nullptr, peers);
   }
   bt::launch_match(kview(kp), pairs, P, ratio, c->ms, &c->tmap_desc, c->force_fallback, c->matches, c->n_matches,
@@ -607,7 +609,7 @@ bt_status bt_register_pairs_host(bt_ctx *c, const bt_keypoints *kp, const bt_map
     // the dense kernels need the pair list and poses too: wait for the caller-stream copies
     cudaEventRecord(c->ev_join, st);
     cudaStreamWaitEvent(c->side, c->ev_join, 0);
-    bt::launch_dense(mview(&dm), *K, c->st_pose, nullptr, c->st_pairs, 2 * P, *eprm, c->dense, nullptr, 0,
+    bt::launch_dense(mview(&dm), *K, c->st_pose, nullptr, c->st_pairs, 2 * P, *eprm, c->dense, c->dense_map_cap, nullptr, 0,
                      c->st_records, rw, bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch);
   }
   const float ratio = mprm ? mprm->ratio : 1.f;
@@ -720,7 +722,7 @@ bt_status raw_enqueue(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *
   if (eprm) {
     cudaEventRecord(c->ev_fork, st);
     cudaStreamWaitEvent(c->side, c->ev_fork, 0);
-    bt::launch_dense(mview(&dm), *K, r.pose, nullptr, r.pairs, 2 * P, *eprm, c->dense, nullptr, 0, c->st_records, rw,
+    bt::launch_dense(mview(&dm), *K, r.pose, nullptr, r.pairs, 2 * P, *eprm, c->dense, c->dense_map_cap, nullptr, 0, c->st_records, rw,
                      bt::rec_dense_ij(n_max), bt::rec_dense_ji(n_max), c->side, c->launch);
   }
   // caller's stream: lifting (needs the normal map), matching, RANSAC
@@ -881,7 +883,7 @@ static bt_status relinearize(bt_ctx *c, const char *what, const bt_keypoints *kp
   c->launch.count = 0;
   cudaEventRecord(c->ev_fork, st);                                 // dense edges beside the feature blocks
   cudaStreamWaitEvent(c->side, c->ev_fork, 0);
-  bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, nullptr, 0, records, rw,
+  bt::launch_dense(mview(maps), *K, node_pose, nullptr, pairs, 2 * P, *eprm, c->dense, c->dense_map_cap, nullptr, 0, records, rw,
                    bt::rec_dense_ij(kp->n_max), bt::rec_dense_ji(kp->n_max), c->side, c->launch);
   bt::launch_feature_edges(kview(kp), pairs, P, matches, n_matches, records, rw, node_pose, eprm->huber_m, st,
                            c->launch);

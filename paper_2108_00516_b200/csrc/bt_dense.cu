@@ -736,8 +736,8 @@ size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H) {
 }
 
 void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
-                  const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, float *out,
-                  int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
+                  const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, size_t map_cap,
+                  float *out, int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
                   cudaStream_t s, Launch &L, int32_t *assoc, const PeerRec *peers) {
   if (E <= 0) return;
   DenseArgs a;
@@ -760,7 +760,9 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   char *p = (char *)scratch;
   const size_t tiles = a.tiles, F = mp.n_frames, npx = (size_t)mp.W * mp.H;
   a.hdr = (uint32_t *)p;     p += 256;                                     // header + maps: zeroed by bt_reserve
-  a.pmap = (MapEntry *)p;    p += align256(F * npx * sizeof(MapEntry));
+  // the maps at their reserved size (map_cap entries: what bt_reserve zeroed and the epoch wrap
+  // clears), so no other region of a call with fewer frames / pixels ever overlaps them
+  a.pmap = (MapEntry *)p;    p += align256(std::max(map_cap, F * npx) * sizeof(MapEntry));
   a.entries = (float4 *)p;   p += align256(F * tiles * kTile * 32);
   a.counts = (int32_t *)p;   p += align256(F * tiles * 4);
   a.offs = (int32_t *)p;     p += align256(F * (tiles + 1) * 4);

@@ -154,8 +154,8 @@ void launch_ransac(const KpView &kp, const int32_t *pairs, const uint32_t *uid, 
                    Launch &L, const PeerRec *peers = nullptr);
 // dense Eq. (3): edges either explicit (edges != null) or derived from pairs (2 per pair)
 void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node_pose, const int32_t *edges,
-                  const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, float *out,
-                  int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
+                  const int32_t *pairs, int E, const bt_edge_params &prm, void *scratch, size_t map_cap,
+                  float *out, int out_stride, uint32_t *records, int rec_stride, int rec_off_ij, int rec_off_ji,
                   cudaStream_t s, Launch &L, int32_t *assoc = nullptr, const PeerRec *peers = nullptr);
 int dense_tiles(int W, int H);
 size_t dense_scratch_bytes(int max_frames, int max_edges, int W, int H);

@@ -224,8 +224,9 @@ def test_dense_map_epochs_stale_entries_and_wrap(bt, torch):
     """k_dense decides a target pixel's validity by the epoch tag of its map entry (no validity
     map): entries left by earlier calls on other frames must never count.  Two different scenes
     alternate on one context, through the epoch wrap (BT_DENSE_EPOCH0 starts the call counter
-    three calls before it; the wrapping call clears every reserved entry): every call's dense
-    blocks equal those of a fresh context."""
+    three calls before it; the wrapping call clears every reserved entry — the maps are carved at
+    their reserved size, so with more frames reserved than used the clear touches no other
+    scratch): every call's dense blocks equal those of a fresh context."""
     import os
     scenes = [synth.make_scene(4, seed=s) for s in (61, 62)]
     pairs = synth.all_pairs(4)
@@ -250,7 +251,8 @@ def test_dense_map_epochs_stale_entries_and_wrap(bt, torch):
     os.environ["BT_DENSE_EPOCH0"] = str(65536 - 3)
     try:
         c = bt.Context(0)
-        c.reserve(len(pairs), 512, 256, 4, 640, 480)
+        c.reserve(len(pairs), 512, 256, 9, 640, 480)     # more frames reserved than used: the
+                                                          # wrap's clear must stay in the maps
     finally:
         os.environ.pop("BT_DENSE_EPOCH0", None)
     for k in range(8):                                  # epochs 65534, 65535, 1 (wrap), 2, ...
