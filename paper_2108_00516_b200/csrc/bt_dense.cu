@@ -791,9 +791,11 @@ void launch_dense(const MapView &mp, const bt_intrinsics &K, const bt_pose *node
   auto kd = assoc ? k_dense<true> : k_dense<false>;
   smem_optin((const void *)kd, smem);
   if (assoc) cudaMemsetAsync(assoc, 0xff, (size_t)E * mp.W * mp.H * sizeof(int32_t), s);   // -1: no source entry
-  // one CTA per possible chunk (idle ones exit at once), not persistent: CTA boundaries let the
-  // higher-priority match / RANSAC kernels interleave (bt_api.cu register_pairs_dev)
-  const int grid = a.tiles * mp.n_frames;
+  // CTAs walk the chunks ch = blockIdx.x, + gridDim.x, ...: at most 8 per SM (a C2 step has
+  // ~600 chunks, so most CTAs take one and their boundaries still let the higher-priority match /
+  // RANSAC kernels interleave, bt_api.cu register_pairs_dev) — one CTA per possible chunk (4800
+  // at C2, most exiting at once) measured 1.5 us slower per step
+  const int grid = std::min(a.tiles * mp.n_frames, 8 * sm_count());
   L.begin(K_DENSE, s);
   launch_pdl(kd, grid, kEdgeThreads, smem, s, a);
   L.end(K_DENSE, s);
