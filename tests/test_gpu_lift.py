@@ -268,3 +268,26 @@ def test_raw_host_depth_u16_equals_f32(bt, torch):
     with pytest.raises(bt.BtError, match="EINVAL"):
         ctx.register_raw(pin(d_mm), *args, got, depth_scale=0.0)
     ctx.close()
+
+
+def test_raw_host_depth_u16_odd_size(bt, torch):
+    """The uint16 depth conversion's tail (a pixel count that is not a multiple of 8, odd row
+    length): records equal the f32 call on the same values."""
+    sc = synth.make_scene(3, n=100, n_max=128, width=161, height=121, distance=0.35, seed=41)
+    uv, desc, n_in = detector_output(sc, seed=42)
+    pairs = synth.all_pairs(3).astype(np.int32)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    d_mm = np.where(sc.depth > 0, np.rint(sc.depth * 1000.0), 0).clip(0, 65535).astype(np.uint16)
+    d_f = d_mm.astype(np.float32) * np.float32(1e-3)
+    assert d_mm.size % 8 != 0
+    ctx = bt.Context(0)
+    ctx.reserve(len(pairs), 128, 1024, 3, 161, 121)
+    rprm, eprm = bt.ransac_params(1024, SEED), bt.edge_params()
+    args = (pin(sc.mask), pin(uv), pin(desc), pin(n_in), sc.K, pin(sc.perturbed_poses(2)), pin(pairs),
+            pin(np.arange(len(pairs), dtype=np.int32)), rprm, eprm)
+    want = torch.zeros((len(pairs), bt.record_words(128)), dtype=torch.int32).pin_memory()
+    got = torch.zeros_like(want).pin_memory()
+    ctx.register_raw(pin(d_f), *args, want)
+    ctx.register_raw(pin(d_mm), *args, got, depth_scale=1e-3)
+    assert np.array_equal(got.numpy(), want.numpy())
+    ctx.close()
