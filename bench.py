@@ -844,6 +844,27 @@ def main():
                        "api": "bt_register_raw_host_async with uint16 depth (mm, depth_scale 1e-3) instead of "
                               "f32 metres; otherwise as e2e",
                        "pairs_ok": int((bt.decode_records(h_rq, N_MAX)["status"] == 0).sum())}
+            # ... and the mask as packed bits (LSB first, unpacked on the device): the sensor /
+            # segmentation formats, 1 + 2 bytes per pixel become 1/8 + 2
+            h_bits = pin(np.packbits(sc.mask != 0, axis=-1, bitorder="little"))
+
+            def raw_compact(k):
+                ctx.register_raw(h_dmm, h_bits, h_uv, h_desc, h_nin, sc.K, h_pose, h_pairs, h_uid, rprm, eprm,
+                                 h_recs[k & 1], stream=stream, blocking=False, depth_scale=1e-3, mask_bits=True)
+            for k in range(3):
+                raw_compact(k)
+            torch.cuda.synchronize()
+            ea.record(stream)
+            for k in range(args.e2e_steps):
+                raw_compact(k)
+            eb.record(stream)
+            torch.cuda.synchronize()
+            assert all(np.array_equal(r.numpy(), h_rq.numpy()) for r in h_recs), "packed-mask records differ"
+            h2d_c = h2d_u16 - h_mask.numel() + h_bits.numel()
+            e2e_u16["compact_mask_bits"] = {
+                "value": P * args.e2e_steps / (ea.elapsed_time(eb) / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d_c), "d2h_bytes_per_step": int(d2h),
+                "api": "as e2e_depth_u16 with the mask as packed bits (mask_bits)"}
         hb = bt.FrameBatch.from_scene(sc, device="cpu", pin=True)
         h2d_pre = small + sum(x.numel() * x.element_size() for x in (hb.n_kp, hb.desc, hb.pts, hb.nrm, hb.depth,
                                                                    hb.normal, hb.mask))

@@ -214,6 +214,10 @@ typedef struct {
      equal those of `depth` holding the same fp32 values.                                         */
   const uint16_t *depth_u16;
   float depth_scale;             /* > 0 with depth_u16                                             */
+  /* optional: the mask as packed bits, [F][H][ceil(W / 8)] bytes, pixel (u, v) = bit (u & 7)
+     (LSB first) of byte (u >> 3) of row v — an eighth of the bytes of `mask` over PCIe, unpacked
+     on the device.  Exactly one of mask / mask_bits is non-NULL.                                 */
+  const uint8_t *mask_bits;
 } bt_raw_frames;
 bt_status bt_register_raw_host(bt_ctx *ctx, const bt_raw_frames *raw, const bt_intrinsics *K,
                                const bt_pose *node_pose, const int32_t *pairs, const uint32_t *pair_uid,

@@ -60,7 +60,7 @@ class RawFrames(C.Structure):
     _fields_ = [("n_frames", C.c_int32), ("width", C.c_int32), ("height", C.c_int32), ("n_max", C.c_int32),
                 ("dim", C.c_int32), ("jump_m", C.c_float), ("depth", C.c_void_p), ("mask", C.c_void_p),
                 ("uv", C.c_void_p), ("desc", C.c_void_p), ("n_in", C.c_void_p), ("depth_u16", C.c_void_p),
-                ("depth_scale", C.c_float)]
+                ("depth_scale", C.c_float), ("mask_bits", C.c_void_p)]
 
 
 class MatchParams(C.Structure):
@@ -309,7 +309,7 @@ class Context:
 
     def register_raw(self, depth, mask, uv, desc, n_in, K, node_pose, pairs, uid, rprm: RansacParams,
                      eprm: EdgeParams | None, records, jump_m: float = 0.05, ratio: float = 1.0, stream=None,
-                     blocking: bool = True, depth_scale: float = 0.0):
+                     blocking: bool = True, depth_scale: float = 0.0, mask_bits: bool = False):
         """bt_register_raw_host: depth [F][H][W] f32, mask [F][H][W] u8, uv [F][n_max][2] f32, desc
         [F][n_max][128] f32, n_in [F] i32, node_pose [F] (12 f32), pairs [P][2], uid [P], records
         [P][record_words] — all HOST tensors / arrays (pinned for full speed); normals and the
@@ -317,12 +317,13 @@ class Context:
         blocking=False (bt_register_raw_host_async) only enqueues: the copies of the next call
         overlap this call's kernels, and `records` is valid once the stream has passed the call.
         A uint16 `depth` (the sensor format; 0 invalid) is sent as is and scaled on the device:
-        metres = value * depth_scale (fp32)."""
+        metres = value * depth_scale (fp32).  mask_bits=True: `mask` is packed bits [F][H][ceil(W/8)]
+        (LSB first), unpacked on the device."""
         F, H, W = (int(x) for x in depth.shape)
         u16 = str(depth.dtype) in ("torch.uint16", "uint16")
         raw = RawFrames(F, W, H, int(uv.shape[1]), int(desc.shape[2]), float(jump_m), None if u16 else _ptr(depth),
-                        _ptr(mask), _ptr(uv), _ptr(desc), _ptr(n_in), _ptr(depth) if u16 else None,
-                        float(depth_scale))
+                        None if mask_bits else _ptr(mask), _ptr(uv), _ptr(desc), _ptr(n_in),
+                        _ptr(depth) if u16 else None, float(depth_scale), _ptr(mask) if mask_bits else None)
         Ki = intrinsics(K) if not isinstance(K, Intrinsics) else K
         name = "bt_register_raw_host" if blocking else "bt_register_raw_host_async"
         self._check(getattr(lib(), name)(self._h, C.byref(raw), C.byref(Ki), _ptr(node_pose), _ptr(pairs),

@@ -65,7 +65,7 @@ struct bt_ctx {
   struct RawSlot {
     float *depth = nullptr, *normal = nullptr, *uv = nullptr, *desc_in = nullptr;
     uint16_t *depth_u16 = nullptr;
-    uint8_t *mask = nullptr;
+    uint8_t *mask = nullptr, *mask_bits = nullptr;
     int32_t *nin = nullptr, *pairs = nullptr;
     uint32_t *uid = nullptr;
     bt_pose *pose = nullptr;
@@ -154,6 +154,7 @@ void free_scratch(bt_ctx *c) {
   for (auto &r : c->raw) {
     free_dev(r.depth); free_dev(r.normal); free_dev(r.uv); free_dev(r.desc_in); free_dev(r.mask);
     free_dev(r.nin); free_dev(r.pairs); free_dev(r.uid); free_dev(r.pose); free_dev(r.depth_u16);
+    free_dev(r.mask_bits);
   }
 }
 
@@ -645,12 +646,14 @@ bool ensure_raw_slots(bt_ctx *c) {
          cudaMalloc(&r.desc_in, FN * bt::kDim * 4) == cudaSuccess && cudaMalloc(&r.nin, F * 4) == cudaSuccess &&
          cudaMalloc(&r.pairs, (size_t)c->cap_pairs * 8) == cudaSuccess &&
          cudaMalloc(&r.uid, (size_t)c->cap_pairs * 4) == cudaSuccess && cudaMalloc(&r.pose, F * sizeof(bt_pose)) == cudaSuccess &&
-         cudaMalloc(&r.depth_u16, FP * 2) == cudaSuccess;
+         cudaMalloc(&r.depth_u16, FP * 2) == cudaSuccess &&
+         cudaMalloc(&r.mask_bits, F * (size_t)c->cap_h * ((c->cap_w + 7) / 8) + 16) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     for (auto &r : c->raw) {
       free_dev(r.depth); free_dev(r.normal); free_dev(r.uv); free_dev(r.desc_in); free_dev(r.mask);
       free_dev(r.nin); free_dev(r.pairs); free_dev(r.uid); free_dev(r.pose); free_dev(r.depth_u16);
+      free_dev(r.mask_bits);
     }
   }
   return ok;
@@ -673,8 +676,10 @@ bt_status raw_enqueue(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *
   if (P > c->cap_pairs) return fail(c, BT_ECAPACITY, "P %d > reserved %d", P, c->cap_pairs);
   if ((s = check_ransac(c, rprm)) != BT_OK) return s;
   if (P == 0) return BT_OK;
-  if (!raw->mask || !raw->uv || !raw->desc || !raw->n_in || !pairs || !pair_uid || !records)
+  if (!raw->uv || !raw->desc || !raw->n_in || !pairs || !pair_uid || !records)
     return fail(c, BT_EINVAL, "%s: NULL buffer", what);
+  if (!raw->mask == !raw->mask_bits)
+    return fail(c, BT_EINVAL, "%s: exactly one of mask / mask_bits must be given", what);
   if (!raw->depth == !raw->depth_u16)
     return fail(c, BT_EINVAL, "%s: exactly one of depth / depth_u16 must be given", what);
   if (raw->depth_u16 && !(raw->depth_scale > 0.f))
@@ -703,7 +708,9 @@ bt_status raw_enqueue(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *
   // copy stream: every input into the slot, once the call that used the slot before is done
   // with it (so they overlap the kernels of the previous call)
   cudaStreamWaitEvent(c->h2d, r.ev_free, 0);
-  cudaMemcpyAsync(r.mask, raw->mask, FP, cudaMemcpyHostToDevice, c->h2d);
+  const size_t FB = (size_t)F * H * ((W + 7) / 8);                // packed mask bytes
+  if (raw->mask) cudaMemcpyAsync(r.mask, raw->mask, FP, cudaMemcpyHostToDevice, c->h2d);
+  else cudaMemcpyAsync(r.mask_bits, raw->mask_bits, FB, cudaMemcpyHostToDevice, c->h2d);
   if (raw->depth) cudaMemcpyAsync(r.depth, raw->depth, FP * 4, cudaMemcpyHostToDevice, c->h2d);
   else cudaMemcpyAsync(r.depth_u16, raw->depth_u16, FP * 2, cudaMemcpyHostToDevice, c->h2d);
   cudaMemcpyAsync(r.pairs, pairs, (size_t)P * 8, cudaMemcpyHostToDevice, c->h2d);
@@ -717,6 +724,7 @@ bt_status raw_enqueue(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *
   // the previous call's records are read) the dense edges
   cudaStreamWaitEvent(c->side, r.ev_in, 0);
   if (!raw->depth) bt::launch_depth_u16(r.depth_u16, raw->depth_scale, FP, r.depth, c->side, c->launch);
+  if (!raw->mask) bt::launch_mask_bits(r.mask_bits, F, W, H, r.mask, c->side, c->launch);
   bt::launch_normals(r.depth, F, W, H, *K, raw->jump_m, r.normal, c->side, c->launch);
   cudaEventRecord(c->ev_maps, c->side);
   if (eprm) {

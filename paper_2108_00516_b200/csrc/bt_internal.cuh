@@ -165,6 +165,7 @@ void launch_feature_edges(const KpView &kp, const int32_t *pairs, int P, const i
                           float huber, cudaStream_t s, Launch &L);
 // NEXT-4 input prep: normal map from depth (bt_prep.cu)
 void launch_depth_u16(const uint16_t *in, float scale, size_t n, float *out, cudaStream_t s, Launch &L);
+void launch_mask_bits(const uint8_t *bits, int F, int W, int H, uint8_t *mask, cudaStream_t s, Launch &L);
 void launch_normals(const float *depth, int F, int W, int H, const bt_intrinsics &K, float jump, float *normal,
                     cudaStream_t s, Launch &L);
 // NEXT-4 keypoint lifting (bt_prep.cu)

@@ -271,6 +271,34 @@ __global__ void __launch_bounds__(256) k_depth_u16(const uint16_t *__restrict__ 
   }
 }
 
+// packed-bit mask rows (ceil(W / 8) bytes, LSB first) -> one byte per pixel: a thread per
+// output byte group of 8 pixels (one input byte), 8-B stores where the row allows
+__global__ void __launch_bounds__(256) k_mask_bits(const uint8_t *__restrict__ bits, int W, size_t rows, int rb,
+                                                   uint8_t *__restrict__ mask) {
+  const size_t n = rows * (size_t)rb, st = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+    const size_t row = i / rb;
+    const int u0 = (int)(i - row * rb) * 8;
+    const unsigned b = bits[i];
+    uint8_t *o = mask + row * (size_t)W + u0;
+    if (u0 + 8 <= W && ((uintptr_t)o & 7) == 0) {
+      unsigned lo = 0, hi = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { lo |= ((b >> k) & 1u) << (8 * k); hi |= ((b >> (4 + k)) & 1u) << (8 * k); }
+      *reinterpret_cast<uint2 *>(o) = make_uint2(lo, hi);
+    } else {
+      for (int k = 0; k < 8 && u0 + k < W; ++k) o[k] = (uint8_t)((b >> k) & 1u);
+    }
+  }
+}
+
+void launch_mask_bits(const uint8_t *bits, int F, int W, int H, uint8_t *mask, cudaStream_t s, Launch &L) {
+  if (F <= 0 || W <= 0 || H <= 0) return;
+  L.begin(K_NORMALS, s);
+  k_mask_bits<<<sm_count() * 8, 256, 0, s>>>(bits, W, (size_t)F * H, (W + 7) / 8, mask);
+  L.end(K_NORMALS, s);
+}
+
 void launch_depth_u16(const uint16_t *in, float scale, size_t n, float *out, cudaStream_t s, Launch &L) {
   if (n == 0) return;
   const int vec = ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0);

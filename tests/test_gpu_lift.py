@@ -291,3 +291,37 @@ def test_raw_host_depth_u16_odd_size(bt, torch):
     ctx.register_raw(pin(d_mm), *args, got, depth_scale=1e-3)
     assert np.array_equal(got.numpy(), want.numpy())
     ctx.close()
+
+
+@pytest.mark.parametrize("width", [640, 161])
+def test_raw_host_mask_bits_equal_bytes(bt, torch, width):
+    """A packed-bit mask ([F][H][ceil(W/8)], LSB first; unpacked on the device) gives the records
+    of the byte mask — blocking and async, a row length that is and one that is not a multiple of
+    8 — and mask + mask_bits together are rejected."""
+    H = 480 if width == 640 else 121
+    sc = synth.make_scene(3, n=300 if width == 640 else 100, n_max=512 if width == 640 else 128, width=width,
+                          height=H, distance=0.6 if width == 640 else 0.35, seed=51)
+    n_max = sc.desc.shape[1]
+    uv, desc, n_in = detector_output(sc, seed=52)
+    pairs = synth.all_pairs(3).astype(np.int32)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    bits = np.packbits(sc.mask != 0, axis=-1, bitorder="little")
+    assert bits.shape == (3, H, (width + 7) // 8)
+    ctx = bt.Context(0)
+    ctx.reserve(len(pairs), n_max, 1024, 3, width, H)
+    rprm, eprm = bt.ransac_params(1024, SEED), bt.edge_params()
+    tail = (pin(uv), pin(desc), pin(n_in), sc.K, pin(sc.perturbed_poses(4)), pin(pairs),
+            pin(np.arange(len(pairs), dtype=np.int32)), rprm, eprm)
+    want = torch.zeros((len(pairs), bt.record_words(n_max)), dtype=torch.int32).pin_memory()
+    ctx.register_raw(pin(sc.depth), pin((sc.mask != 0).astype(np.uint8)), *tail, want)
+    got = torch.zeros_like(want).pin_memory()
+    ctx.register_raw(pin(sc.depth), pin(bits), *tail, got, mask_bits=True)
+    assert np.array_equal(got.numpy(), want.numpy())
+    s = torch.cuda.Stream()
+    got2 = [torch.zeros_like(want).pin_memory() for _ in range(2)]
+    for r in got2:
+        ctx.register_raw(pin(sc.depth), pin(bits), *tail, r, stream=s, blocking=False, mask_bits=True)
+    s.synchronize()
+    for r in got2:
+        assert np.array_equal(r.numpy(), want.numpy())
+    ctx.close()
