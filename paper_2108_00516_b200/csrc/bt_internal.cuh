@@ -87,8 +87,11 @@ struct Launch {
 // Chain kernels are launched with programmatic stream serialization and call pdl_wait() before
 // any memory access (griddepcontrol.wait returns once the predecessor grid has completed and
 // its memory is visible): the dependent's launch overlaps the predecessor's completion
-// (measured 0.385 -> 0.381 ms per step).  No early griddepcontrol.launch_dependents: CTAs
-// launched early park on SM resources the low-priority dense stream needs (measured 0.459 ms).
+// (measured 0.385 -> 0.381 ms per step).  No early griddepcontrol.launch_dependents in general:
+// CTAs launched early park on SM resources the low-priority dense stream needs (measured 0.459 ms
+// with every kernel triggering).  One exception: k_desc_half triggers k_match_ws, which sets up
+// TMEM and its barriers before its own wait (0.2868 -> 0.2834 ms); the same for k_corr_feat ->
+// k_score_tc measured slower (0.2834 -> 0.287 ms).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <typename... KArgs, typename... Args>

@@ -117,6 +117,9 @@ __device__ __forceinline__ float frame_scale(unsigned maxbits) {
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_desc_half(KpView kp, MatchScratch S, int n_pad) {
   pdl_wait();
+  // the matching kernel may launch now: it allocates TMEM and sets up its barriers before its
+  // own griddepcontrol.wait (which still waits for this grid to complete)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int f = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i0 = (blockIdx.x * kWarpsPerBlock + warp) * kPrepPerWarp;
@@ -264,7 +267,6 @@ __device__ __forceinline__ TcItem tc_item(const TcArgs &A, int it) {
 // may be left undecided where the exact top-3 would have certified it, never the converse.
 template <bool kImad, bool kTop2>
 __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constant__ CUtensorMap tmap, TcArgs A) {
-  pdl_wait();
   extern __shared__ uint8_t tc_smem_raw[];
   __shared__ __align__(8) uint64_t bar_a, bar_b[2], bar_mma[2], bar_free[2], bar_c[2];
   __shared__ uint32_t tmem_base_sh;
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_match_ws(const __grid_constan
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();                       // the setup above (no global memory) overlapped k_desc_half's end
   const uint32_t tmem = tmem_base_sh;
   // instruction descriptor: D f32, A/B f16, K-major both, N = 128, M = 128
   const uint32_t idesc = (1u << 4) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
