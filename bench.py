@@ -54,7 +54,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--e2e-warmup-s", type=float, default=1.0,
+                    help="seconds of untimed calls before each e2e measurement (the host link's "
+                         "throughput ramps up over the first ~second of transfers)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the step's kernels one by one instead of replaying it as a CUDA graph")
     ap.add_argument("--no-kernel-events", action="store_true",
@@ -734,9 +737,21 @@ def main():
     e2e_u16 = None
     e2e_pre = None
     if not args.no_e2e:
+        def warm(fn):
+            # untimed calls for >= e2e_warmup_s (and >= 3): pinned-host -> device copies run at
+            # a fraction of the link's rate for the first ~second of traffic
+            # (a fixed count under torchrun: the blocking step holds a collective, so every rank
+            # must make the same number of calls)
+            t0, k = time.time(), 0
+            while k < 3 or (time.time() - t0 < args.e2e_warmup_s if world == 1 else k < 200):
+                fn(k)
+                k += 1
+                if k % 8 == 0:
+                    torch.cuda.synchronize()
+            torch.cuda.synchronize()
+
         def timed(step, n):
-            for _ in range(2):
-                step()
+            warm(lambda k: step())
             e_s = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
             e_e = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
             if world > 1:
@@ -799,9 +814,7 @@ def main():
             def raw_async(k):
                 ctx.register_raw(h_depth, h_mask, h_uv, h_desc, h_nin, sc.K, h_pose, h_pairs, h_uid, rprm, eprm,
                                  h_recs[k & 1], stream=stream, blocking=False)
-            for k in range(3):
-                raw_async(k)
-            torch.cuda.synchronize()
+            warm(raw_async)
             ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ea.record(stream)
             for k in range(args.e2e_steps):
@@ -829,9 +842,7 @@ def main():
             def raw_u16(k):
                 ctx.register_raw(h_dmm, h_mask, h_uv, h_desc, h_nin, sc.K, h_pose, h_pairs, h_uid, rprm, eprm,
                                  h_recs[k & 1], stream=stream, blocking=False, depth_scale=1e-3)
-            for k in range(3):
-                raw_u16(k)
-            torch.cuda.synchronize()
+            warm(raw_u16)
             ea.record(stream)
             for k in range(args.e2e_steps):
                 raw_u16(k)
@@ -851,9 +862,7 @@ def main():
             def raw_compact(k):
                 ctx.register_raw(h_dmm, h_bits, h_uv, h_desc, h_nin, sc.K, h_pose, h_pairs, h_uid, rprm, eprm,
                                  h_recs[k & 1], stream=stream, blocking=False, depth_scale=1e-3, mask_bits=True)
-            for k in range(3):
-                raw_compact(k)
-            torch.cuda.synchronize()
+            warm(raw_compact)
             ea.record(stream)
             for k in range(args.e2e_steps):
                 raw_compact(k)
