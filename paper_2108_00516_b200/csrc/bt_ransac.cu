@@ -1343,12 +1343,15 @@ __global__ void __launch_bounds__(kTcThreads, kTcCtas) k_score_tc(const __grid_c
           tc_fence_after();
           const uint8_t *a = sA + (k & 1) * kTcRows * 128, *b = sB + bb * kTcCols * 128;
           const uint32_t d1 = tmem + tb * 2 * kTcCols, d2 = d1 + kTcCols;
-          umma_f16(d1, umma_desc_sw128(a), umma_desc_sw128(b), idesc, 0u);             // X1hi . Y1hi
-          umma_f16(d1, umma_desc_sw128(a), umma_desc_sw128(b + 32), idesc, 1u);        // X1hi . Y1lo
-          umma_f16(d1, umma_desc_sw128(a + 32), umma_desc_sw128(b), idesc, 1u);        // X1lo . Y1hi
-          umma_f16(d2, umma_desc_sw128(a + 64), umma_desc_sw128(b + 64), idesc, 0u);   // X2hi . Y2hi
-          umma_f16(d2, umma_desc_sw128(a + 64), umma_desc_sw128(b + 96), idesc, 1u);   // X2hi . Y2lo
-          umma_f16(d2, umma_desc_sw128(a + 96), umma_desc_sw128(b + 64), idesc, 1u);   // X2lo . Y2hi
+          // the operands' 32-B K slices: the descriptors' start-address field (16-B units, 14 bits;
+          // shared memory < 228 KB, so + 6 never carries) advanced by 2 per slice
+          const uint64_t da = umma_desc_sw128(a), db = umma_desc_sw128(b);
+          umma_f16(d1, da, db, idesc, 0u);                          // X1hi . Y1hi
+          umma_f16(d1, da, db + 2, idesc, 1u);                      // X1hi . Y1lo
+          umma_f16(d1, da + 2, db, idesc, 1u);                      // X1lo . Y1hi
+          umma_f16(d2, da + 4, db + 4, idesc, 0u);                  // X2hi . Y2hi
+          umma_f16(d2, da + 4, db + 6, idesc, 1u);                  // X2hi . Y2lo
+          umma_f16(d2, da + 6, db + 4, idesc, 1u);                  // X2lo . Y2hi
           umma_commit(&bar_mma[tb]);
           umma_commit(&bar_bfree[bb]);
         }
