@@ -90,7 +90,14 @@ int current_device() {
 }  // namespace
 
 void smem_optin(const void *kernel, size_t bytes) {
-  if (bytes <= 48 * 1024) return;
+  // opt in when static + dynamic shared memory exceed the 48 KB default (not only the dynamic part)
+  if (bytes <= 48 * 1024) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess || fa.sharedSizeBytes + bytes <= 48 * 1024) {
+      cudaGetLastError();
+      return;
+    }
+  }
   const int dev = current_device();
   std::lock_guard<std::mutex> g(g_setup_mu);
   size_t &have = g_smem[{dev, kernel}];
