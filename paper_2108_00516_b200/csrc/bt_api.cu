@@ -691,6 +691,8 @@ bt_status raw_enqueue(bt_ctx *c, const bt_raw_frames *raw, const bt_intrinsics *
     return fail(c, BT_EINVAL, "%s: exactly one of depth / depth_u16 must be given", what);
   if (raw->depth_u16 && !(raw->depth_scale > 0.f))
     return fail(c, BT_EINVAL, "%s: depth_scale %g <= 0 with depth_u16", what, (double)raw->depth_scale);
+  if (raw->mask_bits && (size_t)H * ((W + 7) / 8) > (size_t)c->cap_h * ((c->cap_w + 7) / 8))
+    return fail(c, BT_ECAPACITY, "%s: packed mask rows beyond the reserved staging", what);
   if (!c->st_depth) return fail(c, BT_ECAPACITY, "%s: no staging reserved", what);
   if (!ensure_raw_slots(c)) return fail(c, BT_ENOMEM, "%s: staging allocation failed", what);
   const int slot = c->raw_next;
