@@ -90,16 +90,20 @@ int current_device() {
 }  // namespace
 
 void smem_optin(const void *kernel, size_t bytes) {
-  // opt in when static + dynamic shared memory exceed the 48 KB default (not only the dynamic part)
-  if (bytes <= 48 * 1024) {
-    cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess || fa.sharedSizeBytes + bytes <= 48 * 1024) {
-      cudaGetLastError();
-      return;
-    }
-  }
+  // opt in when static + dynamic shared memory exceed the 48 KB default (not only the dynamic
+  // part); the kernel's static size is looked up once
   const int dev = current_device();
   std::lock_guard<std::mutex> g(g_setup_mu);
+  static std::map<std::pair<int, const void *>, size_t> statics;
+  auto st = statics.find({dev, kernel});
+  if (st == statics.end()) {
+    cudaFuncAttributes fa;
+    size_t v = 0;
+    if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess) v = fa.sharedSizeBytes;
+    else cudaGetLastError();
+    st = statics.emplace(std::make_pair(dev, kernel), v).first;
+  }
+  if (st->second + bytes <= 48 * 1024) return;
   size_t &have = g_smem[{dev, kernel}];
   if (bytes > have) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
