@@ -315,7 +315,9 @@ class Context:
         [P][record_words] — all HOST tensors / arrays (pinned for full speed); normals and the
         keypoints' points / normals are derived on the device.  Synchronises the stream; with
         blocking=False (bt_register_raw_host_async) only enqueues: the copies of the next call
-        overlap this call's kernels, and `records` is valid once the stream has passed the call.
+        overlap this call's kernels, and `records` is valid once the stream has passed the call;
+        the host tensors passed in must stay alive and unchanged until then (the copies read them
+        asynchronously — a temporary such as `t.pin_memory()` in the argument list is not safe).
         A uint16 `depth` (the sensor format; 0 invalid) is sent as is and scaled on the device:
         metres = value * depth_scale (fp32).  mask_bits=True: `mask` is packed bits [F][H][ceil(W/8)]
         (LSB first), unpacked on the device."""

@@ -259,8 +259,9 @@ def test_raw_host_depth_u16_equals_f32(bt, torch):
     assert np.array_equal(got.numpy(), want.numpy())
     s = torch.cuda.Stream()
     got2 = [torch.zeros_like(want).pin_memory() for _ in range(2)]
+    h_dmm = pin(d_mm)                                   # alive until the stream has passed the calls
     for r in got2:
-        ctx.register_raw(pin(d_mm), *args, r, stream=s, blocking=False, depth_scale=1e-3)
+        ctx.register_raw(h_dmm, *args, r, stream=s, blocking=False, depth_scale=1e-3)
     s.synchronize()
     for r in got2:
         assert np.array_equal(r.numpy(), want.numpy())
@@ -319,9 +320,52 @@ def test_raw_host_mask_bits_equal_bytes(bt, torch, width):
     assert np.array_equal(got.numpy(), want.numpy())
     s = torch.cuda.Stream()
     got2 = [torch.zeros_like(want).pin_memory() for _ in range(2)]
+    h_depth, h_bits = pin(sc.depth), pin(bits)          # alive until the stream has passed the calls
     for r in got2:
-        ctx.register_raw(pin(sc.depth), pin(bits), *tail, r, stream=s, blocking=False, mask_bits=True)
+        ctx.register_raw(h_depth, h_bits, *tail, r, stream=s, blocking=False, mask_bits=True)
     s.synchronize()
     for r in got2:
         assert np.array_equal(r.numpy(), want.numpy())
+    ctx.close()
+
+
+def test_raw_host_large_n_compact_inputs_equal_device_chain(bt, torch):
+    """The streaming raw entry at a stress-config keypoint count (n = 2048: the batched
+    matching path with its level-2 pass and the top-2 candidate sets) from the compact inputs —
+    uint16 depth and a packed-bit mask — equals the device chain bt_estimate_normals ->
+    bt_lift_keypoints -> bt_register_pairs on the same (dequantised) maps, bit for bit."""
+    sc = synth.make_scene(4, n=2048, n_max=2048, pool_size=7000, seed=81, outlier_frac=0.16)
+    uv, desc, n_in = detector_output(sc, seed=82)
+    pairs = synth.all_pairs(4).astype(np.int32)
+    uid = np.arange(len(pairs), dtype=np.int32) + 3
+    poses = sc.perturbed_poses(6)
+    d_mm = np.where(sc.depth > 0, np.rint(sc.depth * 1000.0), 0).clip(0, 65535).astype(np.uint16)
+    d_f = d_mm.astype(np.float32) * np.float32(1e-3)
+    bits = np.packbits(sc.mask != 0, axis=-1, bitorder="little")
+    ctx = bt.Context(0)
+    ctx.reserve(len(pairs), 2048, 4096, 4, 640, 480)
+    rprm, eprm = bt.ransac_params(4096, SEED), bt.edge_params()
+    depth = torch.from_numpy(d_f).cuda()
+    mask = torch.from_numpy((sc.mask != 0).astype(np.uint8)).cuda()
+    normal = torch.empty((4, 480, 640, 3), dtype=torch.float32, device="cuda")
+    ctx.estimate_normals(depth, sc.K, normal, jump=0.05)
+    maps = bt.FrameBatch(None, None, None, None, depth, normal, mask)
+    kp = gpu_lift(bt, torch, ctx, uv, desc, n_in, maps, sc.K)
+    dev_rec = torch.zeros((len(pairs), bt.record_words(2048)), dtype=torch.int32, device="cuda")
+    ctx.register_pairs(kp, sc.K, torch.from_numpy(poses).cuda(), torch.from_numpy(pairs).cuda(),
+                       torch.from_numpy(uid).cuda(), rprm, eprm, dev_rec)
+    torch.cuda.synchronize()
+    want = dev_rec.cpu().numpy()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    # the host inputs stay alive (and unchanged) until the stream has passed the calls
+    h = [pin(x) for x in (d_mm, bits, uv, desc, n_in)]
+    hp = [pin(x) for x in (poses, pairs, uid)]
+    s = torch.cuda.Stream()
+    outs = [torch.zeros((len(pairs), bt.record_words(2048)), dtype=torch.int32).pin_memory() for _ in range(3)]
+    for r in outs:
+        ctx.register_raw(*h, sc.K, *hp, rprm, eprm, r, stream=s, blocking=False, depth_scale=1e-3, mask_bits=True)
+    s.synchronize()
+    for r in outs:
+        assert np.array_equal(r.numpy(), want)
+    assert (bt.decode_records(want, 2048)["status"] == 0).all()
     ctx.close()
