@@ -582,6 +582,23 @@ def main():
     # prep: must-read bytes = every mask byte + depth & normal of valid pixels; writes 32 B per entry
     add("k_dense_prep", "hbm", N_FRAMES * npx * 1 + valid_per_frame.sum() * (16 + 32), "GB/s", hbm_peak,
         "mask of every pixel + depth/normal of valid pixels + 32-B entry per valid pixel")
+    # DRAM bytes per step of each stage's launches (ncu --set full, profiles/ncu_traffic.json:
+    # dram__bytes_read.sum + dram__bytes_write.sum per launch), beside the algorithmic bytes of
+    # the HBM-bound stage — traffic well above them would be re-reads
+    tf_all = {}
+    tf_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf_path):
+        tf_all = _j.load(open(tf_path))
+    members = {"k_match_tc": ["k_match_ws"], "k_ransac_score": ["k_corr_feat", "k_score_tc", "k_score_fix"],
+               "k_dense": ["k_dense"], "k_dense_prep": ["k_edge_setup", "k_dense_mask", "k_dense_prep", "k_dense_scan"]}
+    for name, ks in members.items():
+        if name in kern and all(k in tf_all for k in ks):
+            kern[name]["traffic_per_step"] = float(sum(tf_all[k] for k in ks))
+    if "k_dense_prep" in kern:
+        alg = N_FRAMES * npx * 1 + valid_per_frame.sum() * (16 + 32)
+        kern["k_dense_prep"]["algorithmic_bytes_per_step"] = float(alg)
+        if "traffic_per_step" in kern["k_dense_prep"]:
+            kern["k_dense_prep"]["traffic_over_algorithmic"] = kern["k_dense_prep"]["traffic_per_step"] / alg
     # dominant = the largest standalone device time per step (agrees with the serialised ncu
     # launch list); `achieved` stays the in-step CUDA-event duration, overlap included
     dom = max(kern, key=lambda k: kern[k]["standalone_ms_per_step"] or 0) if kern else None
